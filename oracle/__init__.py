@@ -1,0 +1,327 @@
+"""CPU oracle for the MU-NMF nTT hot path of arXiv 2008.01340.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` leg / ``--impl reference`` arm may import this
+package.  The product (``paper_2008_01340_b200``) never imports it, and the two
+share no code: the arithmetic lives in ``oracle/ntt_oracle.c`` (plain C, fp64),
+this module only marshals numpy arrays through ctypes.
+
+Every function cites the passage it follows (P:n = PAPER.md line n, S:n =
+SPEC.md line n); readings R1..R20 are listed in DESIGN.md section 3.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "ntt_oracle.c")
+_LIB = os.path.join(_HERE, "libntt_oracle.so")
+
+# plain C, fp64, no fast-math, no FMA contraction: the sums are the definitions.
+CFLAGS = ["-O2", "-fPIC", "-shared", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-std=c11"]
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle/ntt_oracle.c -> oracle/libntt_oracle.so (gcc)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+_lib = None
+
+_d = ctypes.c_double
+_p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+_u64 = ctypes.c_uint64
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        sig = {
+            "ora_mix64": (_u64, [_u64]),
+            "ora_rng_u24": (ctypes.c_uint32, [_u64, _u64, _u64]),
+            "ora_rng_uniform": (_d, [_u64, _u64, _u64]),
+            "ora_fill_uniform": (None, [_p, _i64, _u64, _u64, _i64]),
+            "ora_stream_w": (_u64, [ctypes.c_int]),
+            "ora_stream_h": (_u64, [ctypes.c_int]),
+            "ora_core_offset": (_i64, [ctypes.c_int, _p, _p, ctypes.c_int]),
+            "ora_tt_element": (_d, [ctypes.c_int, _p, _p, _p, _p]),
+            "ora_tt_full": (ctypes.c_int, [ctypes.c_int, _p, _p, _p, _p]),
+            "ora_tt_full_f32": (ctypes.c_int, [ctypes.c_int, _p, _p, _p, _d, _u64, _u64, _p]),
+            "ora_xht": (None, [_p, _p, _i64, _i64, ctypes.c_int, _p, _p]),
+            "ora_gram_rows": (None, [_p, ctypes.c_int, _i64, _p]),
+            "ora_gram_cols": (None, [_p, _i64, ctypes.c_int, _p]),
+            "ora_w_update": (None, [_p, _i64, ctypes.c_int, _p, _p, _d]),
+            "ora_wtx_cols": (None, [_p, _p, _p, _i64, _i64, ctypes.c_int, _p, _i64, _p]),
+            "ora_h_update_cols": (None, [_p, _i64, ctypes.c_int, _p, _p, _d]),
+            "ora_objective": (_d, [_p, _p, _i64, _i64, ctypes.c_int, _p, _p]),
+            "ora_nmf_mu": (ctypes.c_int, [_p, _p, _i64, _i64, ctypes.c_int, ctypes.c_int, _d, _p, _p, _p]),
+            "ora_check_ranks": (ctypes.c_int, [ctypes.c_int, _p, _p]),
+            "ora_ntt_decompose": (ctypes.c_int, [_p, ctypes.c_int, _p, _p, ctypes.c_int, _u64, _d, _p]),
+            "ora_rel_error_f32": (_d, [_p, _p, _i64]),
+            "ora_rel_error": (_d, [_p, _p, _i64]),
+            "ora_compression_ratio": (_d, [ctypes.c_int, _p, _p]),
+            "ora_tt_rel_error_f32": (_d, [ctypes.c_int, _p, _p, _p, _p]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+_ERR = {1: "invalid argument", 2: "rank error", 3: "degenerate input", 4: "out of memory"}
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise OracleError(f"oracle error {rc}: {_ERR.get(rc, '?')}")
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _dims(dims: Sequence[int]) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(dims, dtype=np.int64))
+
+
+def _ranks(ranks: Sequence[int]) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(ranks, dtype=np.int32))
+
+
+def _xargs(X: np.ndarray):
+    X = np.ascontiguousarray(X)
+    if X.dtype == np.float32:
+        return X, _ptr(X), None
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    return X, None, _ptr(X)
+
+
+# ---------------------------------------------------------------- RNG ------
+STREAM_NOISE = 0x300
+STREAM_W0 = 0x400
+STREAM_H0 = 0x401
+
+
+def stream_w(l: int) -> int:
+    """RNG stream of the W init at TT step l (reading R20)."""
+    return int(lib().ora_stream_w(l))
+
+
+def stream_h(l: int) -> int:
+    """RNG stream of the H init at TT step l (reading R20)."""
+    return int(lib().ora_stream_h(l))
+
+
+def mix64(z: int) -> int:
+    """SplitMix64 finaliser (the RNG spec's mixing function)."""
+    return int(lib().ora_mix64(z))
+
+
+def rng_u24(seed: int, stream: int, i: int) -> int:
+    return int(lib().ora_rng_u24(seed, stream, i))
+
+
+def fill_uniform(count: int, seed: int, stream: int, index_offset: int = 0) -> np.ndarray:
+    """u(seed, stream, offset+i), i < count, as fp64 (values k*2^-24, exact in fp32)."""
+    out = np.empty(count, dtype=np.float64)
+    lib().ora_fill_uniform(_ptr(out), count, seed, stream, index_offset)
+    return out
+
+
+# ------------------------------------------------------------ TT algebra --
+def core_offset(dims, ranks, l: int) -> int:
+    D, R = _dims(dims), _ranks(ranks)
+    return int(lib().ora_core_offset(len(D), _ptr(D), _ptr(R), l))
+
+
+def cores_size(dims, ranks) -> int:
+    full = [1, *ranks, 1]
+    return int(sum(full[l] * dims[l] * full[l + 1] for l in range(len(dims))))
+
+
+def tt_element(dims, ranks, cores: np.ndarray, idx) -> float:
+    """Eq. 2: literal sum over every k-tuple."""
+    D, R = _dims(dims), _ranks(ranks)
+    C = np.ascontiguousarray(cores, dtype=np.float64)
+    I = _dims(idx)
+    return float(lib().ora_tt_element(len(D), _ptr(D), _ptr(R), _ptr(C), _ptr(I)))
+
+
+def tt_full(dims, ranks, cores: np.ndarray) -> np.ndarray:
+    """Eq. 1, left to right; returns the fp64 tensor, shape dims."""
+    D, R = _dims(dims), _ranks(ranks)
+    C = np.ascontiguousarray(cores, dtype=np.float64)
+    out = np.empty(int(np.prod(D)), dtype=np.float64)
+    _check(lib().ora_tt_full(len(D), _ptr(D), _ptr(R), _ptr(C), _ptr(out)))
+    return out.reshape(tuple(int(x) for x in D))
+
+
+def tt_full_f32(dims, ranks, cores: np.ndarray, noise_amp: float = 0.0, seed: int = 0,
+                noise_stream: int = STREAM_NOISE) -> np.ndarray:
+    """Synthetic fp32 tensor: the TT contraction (Eq. 1) split at the
+    middle bond, plus noise_amp * u(seed, noise_stream, flat) (reading R12),
+    accumulated in fp64 and rounded once to fp32."""
+    D, R = _dims(dims), _ranks(ranks)
+    C = np.ascontiguousarray(cores, dtype=np.float64)
+    out = np.empty(int(np.prod(D)), dtype=np.float32)
+    _check(lib().ora_tt_full_f32(len(D), _ptr(D), _ptr(R), _ptr(C), float(noise_amp), seed,
+                                 noise_stream, _ptr(out)))
+    return out.reshape(tuple(int(x) for x in D))
+
+
+# --------------------------------------------------------- MU building blocks
+def xht(X: np.ndarray, H: np.ndarray) -> np.ndarray:
+    """P = X H^T (Alg. 5 l.2)."""
+    X, xf, xd = _xargs(X)
+    m, n = X.shape
+    H = np.ascontiguousarray(H, dtype=np.float64)
+    r = H.shape[0]
+    P = np.empty((m, r))
+    lib().ora_xht(xf, xd, m, n, r, _ptr(H), _ptr(P))
+    return P
+
+
+def gram_rows(H: np.ndarray) -> np.ndarray:
+    """Q = H H^T (Alg. 4)."""
+    H = np.ascontiguousarray(H, dtype=np.float64)
+    r, n = H.shape
+    Q = np.empty((r, r))
+    lib().ora_gram_rows(_ptr(H), r, n, _ptr(Q))
+    return Q
+
+
+def gram_cols(W: np.ndarray) -> np.ndarray:
+    """G = W^T W (Alg. 4)."""
+    W = np.ascontiguousarray(W, dtype=np.float64)
+    m, r = W.shape
+    G = np.empty((r, r))
+    lib().ora_gram_cols(_ptr(W), m, r, _ptr(G))
+    return G
+
+
+def w_update(W: np.ndarray, P: np.ndarray, Q: np.ndarray, eps: float = 1e-16) -> np.ndarray:
+    """W <- W*P / (W Q + eps) (MU, reading R1-R4).  Returns a new array."""
+    W = np.array(W, dtype=np.float64, order="C", copy=True)
+    m, r = W.shape
+    P = np.ascontiguousarray(P, dtype=np.float64)
+    Q = np.ascontiguousarray(Q, dtype=np.float64)
+    lib().ora_w_update(_ptr(W), m, r, _ptr(P), _ptr(Q), eps)
+    return W
+
+
+def wtx_cols(W: np.ndarray, X: np.ndarray, cols: Optional[Sequence[int]] = None) -> np.ndarray:
+    """S = W^T X at the listed columns (Alg. 6 l.2)."""
+    X, xf, xd = _xargs(X)
+    m, n = X.shape
+    W = np.ascontiguousarray(W, dtype=np.float64)
+    r = W.shape[1]
+    if cols is None:
+        C, nc = None, n
+    else:
+        C = _dims(cols)
+        nc = len(C)
+    S = np.empty((r, nc))
+    lib().ora_wtx_cols(_ptr(W), xf, xd, m, n, r, _ptr(C), nc, _ptr(S))
+    return S
+
+
+def h_update_cols(Hcols: np.ndarray, S: np.ndarray, G: np.ndarray, eps: float = 1e-16) -> np.ndarray:
+    """H <- H*S / (G H + eps) on a column slice (MU, reading R1-R4)."""
+    Hc = np.array(Hcols, dtype=np.float64, order="C", copy=True)
+    r, nc = Hc.shape
+    S = np.ascontiguousarray(S, dtype=np.float64)
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    lib().ora_h_update_cols(_ptr(Hc), nc, r, _ptr(S), _ptr(G), eps)
+    return Hc
+
+
+def objective(X: np.ndarray, W: np.ndarray, H: np.ndarray) -> float:
+    """1/2 ||X - WH||_F^2 by direct differences (Alg. 3 l.16)."""
+    X, xf, xd = _xargs(X)
+    m, n = X.shape
+    W = np.ascontiguousarray(W, dtype=np.float64)
+    H = np.ascontiguousarray(H, dtype=np.float64)
+    return float(lib().ora_objective(xf, xd, m, n, W.shape[1], _ptr(W), _ptr(H)))
+
+
+def nmf_mu(X: np.ndarray, W0: np.ndarray, H0: np.ndarray, iters: int, eps: float = 1e-16,
+           trace: bool = False):
+    """MU NMF from (W0, H0) for `iters` iterations (W half then H half).
+    Returns (W, H) or (W, H, objective_trace)."""
+    X, xf, xd = _xargs(X)
+    m, n = X.shape
+    W = np.array(W0, dtype=np.float64, order="C", copy=True)
+    H = np.array(H0, dtype=np.float64, order="C", copy=True)
+    r = W.shape[1]
+    assert W.shape == (m, r) and H.shape == (r, n)
+    tr = np.empty(iters) if trace else None
+    _check(lib().ora_nmf_mu(xf, xd, m, n, r, iters, eps, _ptr(W), _ptr(H), _ptr(tr)))
+    return (W, H, tr) if trace else (W, H)
+
+
+# -------------------------------------------------------------- nTT sweep --
+def check_ranks(dims, ranks) -> int:
+    D, R = _dims(dims), _ranks(ranks)
+    return int(lib().ora_check_ranks(len(D), _ptr(D), _ptr(R)))
+
+
+def ntt_decompose(A: np.ndarray, ranks, iters: int, seed: int = 0, eps: float = 1e-16) -> np.ndarray:
+    """Alg. 2 with fixed ranks and MU NMF; returns packed fp64 cores."""
+    A = np.ascontiguousarray(A, dtype=np.float32)
+    D, R = _dims(A.shape), _ranks(ranks)
+    cores = np.empty(cores_size(list(A.shape), list(ranks)))
+    _check(lib().ora_ntt_decompose(_ptr(A), len(D), _ptr(D), _ptr(R), iters, seed, eps, _ptr(cores)))
+    return cores
+
+
+def unpack_cores(dims, ranks, cores: np.ndarray):
+    """Split the packed buffer into the d cores, core l of shape (r_{l-1}, n_l, r_l)."""
+    full = [1, *ranks, 1]
+    out, off = [], 0
+    for l in range(len(dims)):
+        sz = full[l] * dims[l] * full[l + 1]
+        out.append(np.asarray(cores[off:off + sz]).reshape(full[l], dims[l], full[l + 1]))
+        off += sz
+    return out
+
+
+def rel_error(A: np.ndarray, B: np.ndarray) -> float:
+    """Eq. 3 by direct differences."""
+    Bd = np.ascontiguousarray(B, dtype=np.float64).ravel()
+    if A.dtype == np.float32:
+        Af = np.ascontiguousarray(A).ravel()
+        return float(lib().ora_rel_error_f32(_ptr(Af), _ptr(Bd), Af.size))
+    Ad = np.ascontiguousarray(A, dtype=np.float64).ravel()
+    return float(lib().ora_rel_error(_ptr(Ad), _ptr(Bd), Ad.size))
+
+
+def tt_rel_error(A: np.ndarray, ranks, cores: np.ndarray) -> float:
+    """Eq. 3 of the TT reconstruction against fp32 A, element by element via Eq. 2's
+    sequential vector-matrix products (no materialised reconstruction)."""
+    A = np.ascontiguousarray(A, dtype=np.float32)
+    D, R = _dims(A.shape), _ranks(ranks)
+    C = np.ascontiguousarray(cores, dtype=np.float64)
+    return float(lib().ora_tt_rel_error_f32(len(D), _ptr(D), _ptr(R), _ptr(C), _ptr(A)))
+
+
+def compression_ratio(dims, ranks) -> float:
+    """Eq. 4."""
+    D, R = _dims(dims), _ranks(ranks)
+    return float(lib().ora_compression_ratio(len(D), _ptr(D), _ptr(R)))
