@@ -1,0 +1,175 @@
+/*
+ * ntt.h -- C ABI of the B200-native MU-NMF non-negative tensor-train library
+ * (libntt.so), after arXiv 2008.01340 "Distributed Non-Negative Tensor Train
+ * Decomposition".
+ *
+ * Citation keys: P:n = line n of the paper's LaTeX (/root/reference/PAPER.md at
+ * build time; the library never reads it), Alg./Eq. numbers are the paper's.
+ * Readings of silent or garbled passages (R1..R20) are listed in DESIGN.md s.3.
+ *
+ * General conventions (all entry points)
+ *   - Element type is IEEE fp32, every matrix / tensor is ROW-MAJOR (C order,
+ *     reading R8).  Index types are int64_t; ranks int32_t.
+ *   - Pointers: unless stated otherwise a data pointer may be DEVICE memory
+ *     (cudaMalloc / torch CUDA tensors, on the handle's device) or HOST memory
+ *     (pageable or, for speed, pinned).  Host buffers are staged through device
+ *     memory by the library inside the call (host<->device copies are part of
+ *     the call).  The caller owns every buffer; the library never frees caller
+ *     memory and never keeps a caller pointer after the call returns.
+ *   - Work is enqueued on the handle's CUDA stream and is stream-ordered.  A call
+ *     that returns a host scalar (rel_err, objective_trace, host outputs)
+ *     synchronises that stream before returning.  Other calls return as soon as
+ *     the work is enqueued.
+ *   - Errors: every entry point validates its arguments BEFORE launching any
+ *     kernel and returns a non-zero ntt_status without side effects on invalid
+ *     input.  A CUDA failure after launch returns NTT_ERR_CUDA; outputs are then
+ *     unspecified.  ntt_last_error(h) gives a one-line description.
+ *   - A handle is bound to one device and one stream; it is not thread-safe
+ *     (use one handle per host thread / per rank).
+ *   - No silent CPU fallback exists: every arithmetic step runs in this
+ *     library's sm_100a kernels.  Without a usable CUDA device ntt_create fails.
+ */
+#ifndef NTT_H_
+#define NTT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NTT_ABI_VERSION 1
+
+typedef enum {
+    NTT_OK = 0,
+    NTT_ERR_INVALID_ARG = 1,  /* null pointer, negative size, bad leading dim   */
+    NTT_ERR_DIMENSION = 2,    /* d < 2, a dim < 1, size overflow        */
+    NTT_ERR_RANK = 3,         /* rank outside 1..min(rows, cols), > 64  */
+    NTT_ERR_DEGENERATE = 4,   /* ||A||_F = 0 in an error evaluation     */
+    NTT_ERR_NONNEG = 5,       /* reserved: negative input detected             */
+    NTT_ERR_WORKSPACE = 6,    /* caller workspace too small                    */
+    NTT_ERR_CUDA = 7,         /* CUDA runtime / launch failure                 */
+    NTT_ERR_NCCL = 8,         /* NCCL failure (distributed handles)            */
+    NTT_ERR_UNSUPPORTED = 9   /* valid request this build does not implement   */
+} ntt_status;
+
+typedef struct ntt_handle_s* ntt_handle;
+
+/* ---------------------------------------------------------------- handles --
+ * ntt_create: bind a handle to CUDA `device` and `cuda_stream` (a cudaStream_t;
+ * NULL = the legacy default stream).  Fails with NTT_ERR_CUDA if the device is
+ * absent or is not sm_100 (B200).                                            */
+ntt_status ntt_create(ntt_handle* out, int device, void* cuda_stream);
+ntt_status ntt_destroy(ntt_handle h);
+/* Change the stream subsequent calls enqueue on. */
+ntt_status ntt_set_stream(ntt_handle h, void* cuda_stream);
+const char* ntt_status_string(ntt_status s);
+const char* ntt_last_error(ntt_handle h);
+int ntt_abi_version(void);
+/* Number of kernel launches this handle has issued since creation (for the
+ * bench's gpu_launches count; graph-replayed kernels are counted per replay). */
+int64_t ntt_launch_count(ntt_handle h);
+
+/* ------------------------------------------------------------- RNG / init --
+ * Counter-based uniform draws (DESIGN.md s.4; Alg. 3 l.1 "rand"):
+ *   p[i] = u(seed, stream, index_offset + i),  i < count,
+ *   u(s, t, k) = (mix64(mix64(s ^ mix64(t + G)) + (k + 1) G) >> 40) * 2^-24,
+ *   mix64 = SplitMix64 finaliser, G = 0x9E3779B97F4A7C15 (all mod 2^64).
+ * Values are k * 2^-24 in [0, 1), exact in fp32.  p: device or host, count
+ * floats.  Stream ids used by ntt_decompose: W init at step l = 0x200 + 2l,
+ * H init = 0x201 + 2l (l = 1..d-1), indices = global row-major element index. */
+ntt_status ntt_fill_uniform(ntt_handle h, float* p, int64_t count, uint64_t seed,
+                            uint64_t stream, int64_t index_offset);
+
+/* ------------------------------------------------------------------ MU NMF --
+ * Multiplicative-update NMF, X ~= W H with W >= 0 (m x r), H >= 0 (r x n)
+ * minimising ||X - W H||_F^2 (Alg. 3 Ensure; MU named at P:312/P:461;
+ * rule per reading R1-R4):   for it = 1..iters
+ *     W <- W o (X H^T) / (W (H H^T) + eps)            (Alg. 5 / Alg. 4 products)
+ *     H <- H o (W^T X) / ((W^T W) H + eps)            (Alg. 6 / Alg. 4 products)
+ * W is updated first and the H update uses the new W (R2).  The quotient is
+ * evaluated as (w * num) / (den + eps) (R4).  eps >= 0 (the reference value is
+ * 1e-16, R3).
+ *   X   : m x n, row stride ldx >= n (floats), read-only.  For the fast 1-pass
+ *         path X and ldx should be 16-byte aligned (ldx % 4 == 0); other inputs
+ *         take a slower path, results are the same up to rounding.
+ *   W,H : in/out.  On entry the initial factors (caller-drawn, e.g. with
+ *         ntt_fill_uniform), on exit the factors after `iters` iterations.
+ *   objective_trace : nullable HOST array of `iters` doubles; if given,
+ *         receives 1/2 ||X - W H||_F^2 after each iteration (direct differences,
+ *         fp64 sums; diagnostic, costs one extra pass over X per iteration).
+ * Returns NTT_ERR_INVALID_ARG (null / m,n < 1 / ldx < n / iters < 0 / eps < 0)
+ * or NTT_ERR_RANK (r < 1, r > min(m, n), r > 64).                            */
+ntt_status ntt_nmf_mu(ntt_handle h, const float* X, int64_t m, int64_t n, int64_t ldx,
+                      int32_t r, int32_t iters, float eps, float* W, float* H,
+                      double* objective_trace);
+
+/* ------------------------------------------------------------ nTT sweep ----
+ * Non-negative tensor train with FIXED ranks (Alg. 2, section III-A
+ * P:194, with the SVD rank rule l.5-6 replaced by the caller's ranks, R11):
+ *   T_0 = A;  for l = 1..d-1:
+ *     X_l = reshape(T_{l-1}, [r_{l-1} n_l, prod_{i>l} n_i])   (zero-copy, R9)
+ *     W_l, H_l initialised by ntt_fill_uniform(seed, 0x200+2l / 0x201+2l)
+ *     (W_l, H_l) = ntt_nmf_mu(X_l, r_l, iters, eps)
+ *     core_l = reshape(W_l, [r_{l-1}, n_l, r_l])               (Alg. 2 l.8)
+ *     T_l = H_l                                                (Alg. 2 l.9)
+ *   core_d = reshape(T_{d-1}, [r_{d-1}, n_d, 1])               (Alg. 2 l.11)
+ *   A     : prod(dims) floats, row-major n_1 x ... x n_d, entries >= 0.
+ *   dims  : d extents (host).  ranks: the d-1 inner ranks r_1..r_{d-1} (host);
+ *           r_0 = r_d = 1.  Valid iff 1 <= r_l <= min(r_{l-1} n_l, prod_{i>l} n_i)
+ *           and r_l <= 64 (else NTT_ERR_RANK); d in [2, 64] and every dim >= 1
+ *           (else NTT_ERR_DIMENSION).
+ *   cores : packed output, sum_l r_{l-1} n_l r_l floats; core l (row-major
+ *           r_{l-1} x n_l x r_l) starts at o_l = sum_{j<l} r_{j-1} n_j r_j.
+ *   workspace : device scratch of >= ntt_decompose_workspace_bytes(...) bytes,
+ *           or NULL to let the handle allocate (and keep) its own.          */
+size_t ntt_decompose_workspace_bytes(int32_t d, const int64_t* dims, const int32_t* ranks);
+ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t* dims,
+                         const int32_t* ranks, int32_t iters, uint64_t seed, float eps,
+                         float* cores, void* workspace, size_t workspace_bytes);
+
+/* --------------------------------------------------- reconstruction / error
+ * Contract a TT (Eq. 1):  A~ = G_1 o G_2 o ... o G_d, and/or the
+ * relative error of Eq. 3: ||ref - A~||_F / ||ref||_F by direct
+ * differences with fp64 sums (never the Gram identity, R18).
+ *   cores : packed as in ntt_decompose.  out: nullable, prod(dims) floats.
+ *   ref   : nullable, prod(dims) floats.  rel_err: nullable HOST double; needs
+ *           ref.  NTT_ERR_DEGENERATE if ||ref||_F = 0.                       */
+ntt_status ntt_reconstruct(ntt_handle h, int32_t d, const int64_t* dims, const int32_t* ranks,
+                           const float* cores, float* out, const float* ref, double* rel_err);
+
+/* Synthetic data (section IV-A): out = fp32(A~ + noise_amp *
+ * u(seed, noise_stream, flat index)) with A~ the contraction of `cores`,
+ * accumulated in fp32 along the middle bond (reading R12).  out: prod(dims). */
+ntt_status ntt_generate(ntt_handle h, int32_t d, const int64_t* dims, const int32_t* ranks,
+                        const float* cores, float noise_amp, uint64_t seed,
+                        uint64_t noise_stream, float* out);
+
+/* Eq. 4: C = prod n_i / sum n_i r_{i-1} r_i.  Host-only; returns a
+ * negative value for invalid input.                                          */
+double ntt_compression_ratio(int32_t d, const int64_t* dims, const int32_t* ranks);
+
+/* ----------------------------------------------------- multi-GPU (NCCL) ----
+ * One process per GPU.  Rank 0 calls ntt_get_unique_id and broadcasts the 128
+ * bytes (e.g. over a torch process group); every rank then calls
+ * ntt_create_dist with the same id.  Distributed layout for ntt_decompose
+ * (DESIGN.md s.7): the LAST tensor mode is block-partitioned, rank g holds
+ * A[..., i_d in [b_g, b_{g+1})] as a row-major n_1 x ... x n_{d-1} x (b_{g+1}-b_g)
+ * tensor with b_g = floor(g n_d / p); every unfolding is then a column
+ * partition, reshapes stay local, and each MU pass needs one all-reduce of the
+ * fp64 (X H^T, H H^T) partials (Alg. 4/5 reduced to AR).  Cores are returned
+ * replicated on every rank.  Returns NTT_ERR_UNSUPPORTED if NCCL cannot be
+ * loaded.                                                                    */
+ntt_status ntt_get_unique_id(void* id128);
+ntt_status ntt_create_dist(ntt_handle* out, int device, void* cuda_stream, const void* id128,
+                           int nranks, int rank);
+int ntt_dist_rank(ntt_handle h);
+int ntt_dist_size(ntt_handle h);
+/* Local extent of the last mode on `rank` for a global extent n_d over p ranks. */
+int64_t ntt_dist_block(int64_t n_last, int nranks, int rank, int64_t* offset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NTT_H_ */

@@ -1,0 +1,168 @@
+"""paper_2008_01340_b200 -- B200-native MU-NMF non-negative tensor train.
+
+Thin Python binding of libntt.so (include/ntt.h), arXiv 2008.01340.  Functions
+keep the C names (``ntt_nmf_mu``, ``ntt_decompose``, ``ntt_reconstruct`` ...)
+and accept torch tensors (CUDA or CPU) or raw integer pointers; they only
+marshal arguments -- every step of the hot path runs in the library's sm_100a
+kernels.  PyTorch is used for device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence
+
+import numpy as np
+
+from ._lib import LIB_PATH, lib  # noqa: F401
+
+__all__ = [
+    "NttError", "Handle", "ntt_compression_ratio", "ntt_decompose_workspace_bytes", "ntt_dist_block",
+    "ntt_get_unique_id", "STREAM_NOISE", "stream_w", "stream_h", "cores_size", "LIB_PATH",
+]
+
+STREAM_NOISE = 0x300
+
+
+def stream_w(l: int) -> int:
+    return 0x200 + 2 * l
+
+
+def stream_h(l: int) -> int:
+    return 0x201 + 2 * l
+
+
+class NttError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"ntt status {status}: {msg}")
+        self.status = status
+
+
+def _ptr(x) -> Optional[int]:
+    """Pointer of a torch tensor / numpy array / int / None (no copies made)."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return x.data_ptr()
+    if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return x.ctypes.data
+    raise TypeError(f"cannot take a pointer of {type(x)}")
+
+
+def _i64arr(v: Sequence[int]):
+    return (ctypes.c_int64 * len(v))(*[int(x) for x in v])
+
+
+def _i32arr(v: Sequence[int]):
+    return (ctypes.c_int32 * max(1, len(v)))(*[int(x) for x in v])
+
+
+def cores_size(dims, ranks) -> int:
+    fr = [1, *ranks, 1]
+    return int(sum(fr[l] * dims[l] * fr[l + 1] for l in range(len(dims))))
+
+
+def ntt_compression_ratio(dims, ranks) -> float:
+    return float(lib().ntt_compression_ratio(len(dims), _i64arr(dims), _i32arr(ranks)))
+
+
+def ntt_decompose_workspace_bytes(dims, ranks) -> int:
+    return int(lib().ntt_decompose_workspace_bytes(len(dims), _i64arr(dims), _i32arr(ranks)))
+
+
+def ntt_dist_block(n_last: int, nranks: int, rank: int):
+    off = ctypes.c_int64(0)
+    b = lib().ntt_dist_block(n_last, nranks, rank, ctypes.byref(off))
+    return int(b), int(off.value)
+
+
+def ntt_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    st = lib().ntt_get_unique_id(buf)
+    if st != 0:
+        raise NttError(st, "ntt_get_unique_id failed")
+    return buf.raw
+
+
+class Handle:
+    """Owns an ntt_handle bound to (device, stream)."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None, unique_id: Optional[bytes] = None,
+                 nranks: int = 1, rank: int = 0):
+        self._h = ctypes.c_void_p()
+        if stream is None:
+            try:
+                import torch
+                stream = torch.cuda.current_stream(device).cuda_stream
+            except Exception:
+                stream = 0
+        if unique_id is None:
+            st = lib().ntt_create(ctypes.byref(self._h), device, ctypes.c_void_p(stream))
+        else:
+            idb = ctypes.create_string_buffer(unique_id, 128)
+            st = lib().ntt_create_dist(ctypes.byref(self._h), device, ctypes.c_void_p(stream), idb, nranks, rank)
+        if st != 0:
+            raise NttError(st, f"ntt_create failed ({lib().ntt_status_string(st).decode()})")
+
+    # -------------------------------------------------------------- plumbing
+    def _check(self, st: int):
+        if st != 0:
+            raise NttError(st, f"{lib().ntt_status_string(st).decode()}: {lib().ntt_last_error(self._h).decode()}")
+
+    def close(self):
+        if self._h:
+            lib().ntt_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream: int):
+        self._check(lib().ntt_set_stream(self._h, ctypes.c_void_p(stream)))
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib().ntt_launch_count(self._h))
+
+    @property
+    def rank(self) -> int:
+        return int(lib().ntt_dist_rank(self._h))
+
+    @property
+    def size(self) -> int:
+        return int(lib().ntt_dist_size(self._h))
+
+    def last_error(self) -> str:
+        return lib().ntt_last_error(self._h).decode()
+
+    # ------------------------------------------------------------------ ABI
+    def ntt_fill_uniform(self, p, count: int, seed: int, stream: int, index_offset: int = 0):
+        self._check(lib().ntt_fill_uniform(self._h, _ptr(p), count, seed, stream, index_offset))
+
+    def ntt_nmf_mu(self, X, m: int, n: int, ldx: int, r: int, iters: int, eps: float, W, H, trace: bool = False):
+        tr = (ctypes.c_double * max(1, iters))() if trace else None
+        self._check(lib().ntt_nmf_mu(self._h, _ptr(X), m, n, ldx, r, iters, eps, _ptr(W), _ptr(H), tr))
+        return list(tr)[:iters] if trace else None
+
+    def ntt_decompose(self, A, dims, ranks, iters: int, seed: int, eps: float, cores, workspace=None,
+                      workspace_bytes: int = 0):
+        self._check(lib().ntt_decompose(self._h, _ptr(A), len(dims), _i64arr(dims), _i32arr(ranks), iters, seed, eps,
+                                        _ptr(cores), _ptr(workspace), workspace_bytes))
+
+    def ntt_reconstruct(self, dims, ranks, cores, out=None, ref=None, want_error: bool = False) -> Optional[float]:
+        err = ctypes.c_double(-1.0) if want_error else None
+        self._check(lib().ntt_reconstruct(self._h, len(dims), _i64arr(dims), _i32arr(ranks), _ptr(cores), _ptr(out),
+                                          _ptr(ref), ctypes.byref(err) if err is not None else None))
+        return float(err.value) if want_error else None
+
+    def ntt_generate(self, dims, ranks, cores, noise_amp: float, seed: int, noise_stream: int, out):
+        self._check(lib().ntt_generate(self._h, len(dims), _i64arr(dims), _i32arr(ranks), _ptr(cores), noise_amp,
+                                       seed, noise_stream, _ptr(out)))

@@ -1,0 +1,56 @@
+// common.cuh -- shared device helpers of libntt (product path only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ntt {
+
+constexpr int kMaxRank = 64;
+
+// ---------------------------------------------------------------------------
+// Counter-based RNG, implemented from the text spec in include/ntt.h
+// (ntt_fill_uniform).  u = top 24 bits of mix64(key + (i+1) G) times 2^-24.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t rng_mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
+
+__host__ __device__ __forceinline__ uint64_t rng_key(uint64_t seed, uint64_t stream) {
+  return rng_mix64(seed ^ rng_mix64(stream + kGolden));
+}
+__host__ __device__ __forceinline__ float rng_uniform(uint64_t key, uint64_t i) {
+  uint32_t v = (uint32_t)(rng_mix64(key + (i + 1ULL) * kGolden) >> 40);
+  return (float)v * (1.0f / 16777216.0f);  // exact: v < 2^24
+}
+
+__host__ __device__ __forceinline__ uint64_t stream_w(int l) { return 0x200ULL + 2ULL * (uint64_t)l; }
+__host__ __device__ __forceinline__ uint64_t stream_h(int l) { return 0x201ULL + 2ULL * (uint64_t)l; }
+
+// MU quotient, reading R4: (w * num) / (den + eps), IEEE division.
+__device__ __forceinline__ float mu_quot(float w, float num, float den, float eps) {
+  return __fdiv_rn(__fmul_rn(w, num), __fadd_rn(den, eps));
+}
+__device__ __forceinline__ double mu_quot(double w, double num, double den, double eps) {
+  return __ddiv_rn(__dmul_rn(w, num), __dadd_rn(den, eps));
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// packed fp32x2 FMA (FFMA2 on sm_100a): d = a * b + c lane-wise
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  return __ffma2_rn(a, b, c);
+}
+
+}  // namespace ntt

@@ -1,0 +1,67 @@
+// kernels.h -- internal launcher declarations of libntt (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ntt {
+
+// ---- RNG -------------------------------------------------------------------
+cudaError_t launch_fill_uniform(float* p, int64_t count, uint64_t seed, uint64_t stream,
+                                int64_t index_offset, cudaStream_t st);
+
+// ---- generic (2-pass) MU building blocks ------------------------------------
+// Partials are fp64, laid out [split][rows*r].
+struct XhtPlan {
+  int ncs;          // column splits (number of partial copies)
+  int nrb;          // row blocks
+  int64_t chunk;    // columns per split (multiple of the tile width)
+};
+XhtPlan plan_xht(int64_t m, int64_t n, int num_sms);
+// Ppart[b][i*r+k] = sum_{j in split b} X[i][j] * H[k][j]
+cudaError_t launch_xht_partial(const float* X, int64_t ldx, int64_t m, int64_t n, const float* H,
+                               int64_t ldh, int r, const XhtPlan& pl, double* Ppart, cudaStream_t st);
+
+// W <- W o P / (W Q + eps) with P = sum_b Ppart[b], Q = sum_b Qpart[b] (fixed order);
+// Gpart[c][k*r+l] = sum over CTA c's rows of Wn[i][k] Wn[i][l]  (c < wupdate_ctas(m))
+int wupdate_ctas(int64_t m, int r);
+cudaError_t launch_wupdate(float* W, int64_t m, int r, const double* Ppart, int nP, const double* Qpart,
+                           int nQ, float eps, double* Gpart, cudaStream_t st);
+
+// H pass: G = sum_c Gpart[c]; S = W^T X; H <- H o S / (G H + eps) in place.
+// If Ppart != nullptr, also accumulates per-CTA partials of P' = X Hn^T, Q' = Hn Hn^T
+// (the 1-pass fusion; requires m*r <= kMaxAccMR) into Ppart[cta], Qpart[cta].
+constexpr int64_t kMaxAccMR = 4096;
+int hpass_ctas(int64_t m, int64_t n, int r, bool acc, int num_sms);
+cudaError_t launch_hpass(const float* X, int64_t ldx, int64_t m, int64_t n, const float* W, int r,
+                         const double* Gpart, int nG, float eps, float* H, int grid, double* Ppart,
+                         double* Qpart, cudaStream_t st);
+
+// 1/2 ||X - W H||^2 partial sums (fp64), one per CTA; returns number of partials.
+int objective_ctas(int64_t n);
+cudaError_t launch_objective(const float* X, int64_t ldx, int64_t m, int64_t n, const float* W,
+                             const float* H, int r, double* part, cudaStream_t st);
+
+// ---- tensor-train contraction ------------------------------------------------
+// out[(a*nl+i)*rl+c] = sum_k L[a*rp+k] * G[(k*nl+i)*rl+c]      (left step)
+cudaError_t launch_contract_left(const float* L, int64_t N, int rp, const float* G, int64_t nl, int rl,
+                                 float* out, cudaStream_t st);
+// out[k*(nl*NR) + i*NR + b] = sum_c G[(k*nl+i)*rl+c] * R[c*NR+b] (right step)
+cudaError_t launch_contract_right(const float* G, int rp, int64_t nl, int rl, const float* R, int64_t NR,
+                                  float* out, cudaStream_t st);
+// A~[a,b] = sum_q L[a*rk+q] R[q*NR+b]; optional out (+ noise), optional error partials vs ref
+int stream_ctas(int64_t NL, int64_t NR, int num_sms);
+cudaError_t launch_tt_stream(const float* L, const float* R, int64_t NL, int64_t NR, int rk, float* out,
+                             float noise_amp, uint64_t noise_key, const float* ref, double* err_part,
+                             int grid, cudaStream_t st);
+
+}  // namespace ntt
+
+namespace ntt {
+// out[t] = sum_b part[b*len + t]   (fixed order b = 0..n-1)
+cudaError_t launch_sum_partials(const double* part, int nparts, int64_t len, double* out, cudaStream_t st);
+// H init for a last-mode column block (DESIGN.md s.7): H[k][c] = u(key, k*nglob + (c/b)*nd + off + c%b)
+cudaError_t launch_fill_uniform_cols(float* H, int r, int64_t nloc, int64_t b, int64_t nd, int64_t off, int64_t nglob,
+                                     uint64_t seed, uint64_t stream, cudaStream_t st);
+// gathered rank-major blocks [g][r][b_g] -> core [r][nd]
+cudaError_t launch_gather_last_core(const float* gath, int64_t r, int64_t nd, int nranks, float* core, cudaStream_t st);
+}  // namespace ntt

@@ -1,0 +1,792 @@
+// ntt_api.cu -- the C ABI of libntt (include/ntt.h): validation, planning,
+// workspace management, the MU iteration driver, the nTT sweep, contraction /
+// error, and the NCCL layer for the last-mode-partitioned multi-GPU sweep.
+#include <dlfcn.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <nccl.h>
+
+#include "../../include/ntt.h"
+#include "common.cuh"
+#include "kernels.h"
+#include "mu_fused.h"
+
+using namespace ntt;
+
+// ----------------------------------------------------------------- NCCL (dlopen)
+namespace {
+struct NcclApi {
+  bool loaded = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+bool load_nccl() {
+  if (g_nccl.loaded) return true;
+  const char* env = getenv("NTT_NCCL_LIB");
+  const char* names[] = {env, "libnccl.so.2", "libnccl.so"};
+  void* lib = nullptr;
+  for (const char* nm : names) {
+    if (!nm) continue;
+    lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+    if (lib) break;
+  }
+  if (!lib) return false;
+#define SYM(f, n) g_nccl.f = reinterpret_cast<decltype(g_nccl.f)>(dlsym(lib, n)); if (!g_nccl.f) return false;
+  SYM(GetUniqueId, "ncclGetUniqueId")
+  SYM(CommInitRank, "ncclCommInitRank")
+  SYM(CommDestroy, "ncclCommDestroy")
+  SYM(AllReduce, "ncclAllReduce")
+  SYM(Broadcast, "ncclBroadcast")
+  SYM(GroupStart, "ncclGroupStart")
+  SYM(GroupEnd, "ncclGroupEnd")
+  SYM(GetErrorString, "ncclGetErrorString")
+#undef SYM
+  g_nccl.loaded = true;
+  return true;
+}
+}  // namespace
+
+// --------------------------------------------------------------------- handle
+struct ntt_handle_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  std::string err;
+  int64_t launches = 0;
+  // internal scratch (grown, never shrunk)
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  // staging for host buffers
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+  double* host_part = nullptr;  // pinned host landing zone for small reductions
+  size_t host_part_count = 0;
+  // distributed
+  int nranks = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  FusedCtx fused;
+};
+
+namespace {
+
+ntt_status fail(ntt_handle h, ntt_status s, const char* fmt, ...) {
+  if (h) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    h->err = buf;
+  }
+  return s;
+}
+
+#define CU(h, call)                                                                          \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail((h), NTT_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define LAUNCH(h, call)      \
+  do {                       \
+    CU(h, (call));           \
+    (h)->launches++;         \
+  } while (0)
+
+#define NC(h, call)                                                                             \
+  do {                                                                                          \
+    ncclResult_t r_ = (call);                                                                   \
+    if (r_ != ncclSuccess)                                                                      \
+      return fail((h), NTT_ERR_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call, g_nccl.GetErrorString(r_)); \
+  } while (0)
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+ntt_status ensure_ws(ntt_handle h, size_t bytes) {
+  if (bytes <= h->ws_bytes) return NTT_OK;
+  CU(h, cudaStreamSynchronize(h->stream));
+  if (h->ws) CU(h, cudaFree(h->ws));
+  h->ws = nullptr;
+  h->ws_bytes = 0;
+  CU(h, cudaMalloc(&h->ws, bytes));
+  h->ws_bytes = bytes;
+  return NTT_OK;
+}
+
+ntt_status ensure_stage(ntt_handle h, size_t bytes) {
+  if (bytes <= h->stage_bytes) return NTT_OK;
+  CU(h, cudaStreamSynchronize(h->stream));
+  if (h->stage) CU(h, cudaFree(h->stage));
+  h->stage = nullptr;
+  h->stage_bytes = 0;
+  CU(h, cudaMalloc(&h->stage, bytes));
+  h->stage_bytes = bytes;
+  return NTT_OK;
+}
+
+ntt_status ensure_host_part(ntt_handle h, size_t count) {
+  if (count <= h->host_part_count) return NTT_OK;
+  if (h->host_part) CU(h, cudaFreeHost(h->host_part));
+  h->host_part = nullptr;
+  h->host_part_count = 0;
+  CU(h, cudaMallocHost(&h->host_part, count * sizeof(double)));
+  h->host_part_count = count;
+  return NTT_OK;
+}
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+bool mul_ok(int64_t a, int64_t b, int64_t* out) {
+  if (a < 0 || b < 0) return false;
+  if (a != 0 && b > INT64_MAX / a) return false;
+  *out = a * b;
+  return true;
+}
+
+// ---------------------------------------------------------- MU iteration driver
+// Scratch requirement (bytes) of one MU run on an m x n problem with rank r.
+struct MuPlan {
+  int64_t m, n;
+  int r;
+  bool fused;     // 1-pass short-wide kernel (mu_fused.cu)
+  bool acc;       // generic 1-pass (hpass accumulates P, Q)
+  XhtPlan xp;     // X H^T pass
+  XhtPlan qp;     // H H^T pass
+  int hgrid;      // H-pass CTAs
+  int nwup;       // W-update CTAs
+  int fgrid;      // fused kernel CTAs
+  size_t off_P, off_Q, off_G, off_S, bytes;
+};
+
+MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, int nranks) {
+  MuPlan p;
+  p.m = m;
+  p.n = n;
+  p.r = r;
+  p.fused = fused_supported(m, n, r);
+  p.acc = !p.fused && (m * r <= kMaxAccMR);
+  p.xp = plan_xht(m, n, num_sms);
+  p.qp = plan_xht(r, n, num_sms);
+  p.hgrid = hpass_ctas(m, n, r, p.acc, num_sms);
+  p.nwup = wupdate_ctas(m, r);
+  p.fgrid = p.fused ? fused_grid(m, n, r, num_sms) : 0;
+  int64_t nP = std::max<int64_t>({(int64_t)p.xp.ncs, p.acc ? p.hgrid : 0, (int64_t)p.fgrid, 1});
+  int64_t nQ = std::max<int64_t>({(int64_t)p.qp.ncs, p.acc ? p.hgrid : 0, (int64_t)p.fgrid, 1});
+  size_t o = 0;
+  p.off_P = o;
+  o = align_up(o + sizeof(double) * (size_t)(nP * m * r));
+  p.off_Q = o;
+  o = align_up(o + sizeof(double) * (size_t)(nQ * r * r));
+  p.off_G = o;
+  o = align_up(o + sizeof(double) * (size_t)(std::max(p.nwup, 1) * r * r));
+  p.off_S = o;  // reduced (m r + r r) vector for distributed all-reduce / fused reductions
+  o = align_up(o + sizeof(double) * (size_t)(m * r + r * r) + fused_scratch_bytes(m, n, r, p.fgrid));
+  p.bytes = o;
+  (void)nranks;
+  return p;
+}
+
+// Sum nP partials of (P, Q) into one vector and all-reduce it over the ranks.
+ntt_status dist_reduce(ntt_handle h, const MuPlan& p, double* Ppart, int nP, double* Qpart, int nQ, double* red) {
+  LAUNCH(h, launch_sum_partials(Ppart, nP, p.m * p.r, red, h->stream));
+  LAUNCH(h, launch_sum_partials(Qpart, nQ, (int64_t)p.r * p.r, red + p.m * p.r, h->stream));
+  NC(h, g_nccl.AllReduce(red, red, (size_t)(p.m * p.r + p.r * p.r), ncclFloat64, ncclSum, h->comm, h->stream));
+  return NTT_OK;
+}
+
+ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, int32_t iters, float eps, float* W,
+                  float* H, char* scratch, double* dev_trace /*nullable: iters*nobj*/) {
+  const int64_t m = p.m, n = p.n;
+  const int r = p.r;
+  double* Ppart = reinterpret_cast<double*>(scratch + p.off_P);
+  double* Qpart = reinterpret_cast<double*>(scratch + p.off_Q);
+  double* Gpart = reinterpret_cast<double*>(scratch + p.off_G);
+  double* red = reinterpret_cast<double*>(scratch + p.off_S);
+  const bool dist = h->nranks > 1;
+  cudaStream_t st = h->stream;
+  int nobj = objective_ctas(n);
+  if (iters <= 0) return NTT_OK;
+
+  if (p.fused) return fail(h, NTT_ERR_UNSUPPORTED, "fused path not built");
+
+  // prologue (1-pass) or first W pass: P = X H^T, Q = H H^T
+  int nP = 0, nQ = 0;
+  for (int it = 0; it < iters; ++it) {
+    if (!p.acc || it == 0) {
+      LAUNCH(h, launch_xht_partial(X, ldx, m, n, H, n, r, p.xp, Ppart, st));
+      LAUNCH(h, launch_xht_partial(H, n, r, n, H, n, r, p.qp, Qpart, st));
+      nP = p.xp.ncs;
+      nQ = p.qp.ncs;
+    }
+    if (dist) {
+      ntt_status s = dist_reduce(h, p, Ppart, nP, Qpart, nQ, red);
+      if (s) return s;
+      LAUNCH(h, launch_wupdate(W, m, r, red, 1, red + m * r, 1, eps, Gpart, st));
+    } else {
+      LAUNCH(h, launch_wupdate(W, m, r, Ppart, nP, Qpart, nQ, eps, Gpart, st));
+    }
+    const bool acc_now = p.acc && (it + 1 < iters);
+    LAUNCH(h, launch_hpass(X, ldx, m, n, W, r, Gpart, p.nwup, eps, H, p.hgrid, acc_now ? Ppart : nullptr,
+                           acc_now ? Qpart : nullptr, st));
+    if (acc_now) {
+      nP = p.hgrid;
+      nQ = p.hgrid;
+    }
+    if (dev_trace) LAUNCH(h, launch_objective(X, ldx, m, n, W, H, r, dev_trace + (int64_t)it * nobj, st));
+  }
+  return NTT_OK;
+}
+
+ntt_status check_mu_args(ntt_handle h, const float* X, int64_t m, int64_t n, int64_t ldx, int32_t r, int32_t iters,
+                         float eps, const float* W, const float* H) {
+  if (!h) return NTT_ERR_INVALID_ARG;
+  if (!X || !W || !H) return fail(h, NTT_ERR_INVALID_ARG, "null X, W or H");
+  if (m < 1 || n < 1) return fail(h, NTT_ERR_INVALID_ARG, "m, n must be >= 1 (got %lld, %lld)", (long long)m, (long long)n);
+  if (ldx < n) return fail(h, NTT_ERR_INVALID_ARG, "ldx (%lld) < n (%lld)", (long long)ldx, (long long)n);
+  if (iters < 0) return fail(h, NTT_ERR_INVALID_ARG, "iters < 0");
+  if (!(eps >= 0.0f)) return fail(h, NTT_ERR_INVALID_ARG, "eps must be >= 0");
+  if (r < 1 || r > kMaxRank || r > m || r > n)
+    return fail(h, NTT_ERR_RANK, "rank %d outside [1, min(m, n, %d)]", r, kMaxRank);
+  int64_t t;
+  if (!mul_ok(m, ldx, &t)) return fail(h, NTT_ERR_DIMENSION, "m * ldx overflows");
+  return NTT_OK;
+}
+
+struct TTShape {
+  int d;
+  int64_t dims[64];
+  int64_t r[65];   // r_0..r_d
+  int64_t N;       // prod dims
+  int64_t cores;   // packed size
+  int64_t off[65]; // core offsets o_1..o_d (1-based)
+};
+
+ntt_status check_tt(ntt_handle h, int32_t d, const int64_t* dims, const int32_t* ranks, TTShape* s, bool check_ranks) {
+  if (d < 2 || d > 64 || !dims || (d > 1 && !ranks)) return fail(h, NTT_ERR_DIMENSION, "need 2 <= d <= 64 and dims/ranks");
+  s->d = d;
+  s->N = 1;
+  for (int l = 0; l < d; ++l) {
+    if (dims[l] < 1) return fail(h, NTT_ERR_DIMENSION, "dims[%d] = %lld < 1", l, (long long)dims[l]);
+    s->dims[l] = dims[l];
+    if (!mul_ok(s->N, dims[l], &s->N)) return fail(h, NTT_ERR_DIMENSION, "prod(dims) overflows");
+  }
+  s->r[0] = 1;
+  s->r[d] = 1;
+  for (int l = 1; l < d; ++l) s->r[l] = ranks[l - 1];
+  int64_t rest = s->N;
+  for (int l = 1; l < d; ++l) {
+    rest /= dims[l - 1];  // prod_{i>l} n_i
+    int64_t rows = s->r[l - 1] * dims[l - 1];
+    if (s->r[l] < 1 || s->r[l] > kMaxRank || (check_ranks && (s->r[l] > rows || s->r[l] > rest)))
+      return fail(h, NTT_ERR_RANK, "rank r_%d = %lld outside [1, min(%lld, %lld, %d)]", l, (long long)s->r[l],
+                  (long long)rows, (long long)rest, kMaxRank);
+  }
+  s->cores = 0;
+  for (int l = 1; l <= d; ++l) {
+    s->off[l] = s->cores;
+    s->cores += s->r[l - 1] * dims[l - 1] * s->r[l];
+  }
+  return NTT_OK;
+}
+
+}  // namespace
+
+// ============================================================================ ABI
+extern "C" {
+
+int ntt_abi_version(void) { return NTT_ABI_VERSION; }
+
+const char* ntt_status_string(ntt_status s) {
+  switch (s) {
+    case NTT_OK: return "ok";
+    case NTT_ERR_INVALID_ARG: return "invalid argument";
+    case NTT_ERR_DIMENSION: return "dimension error";
+    case NTT_ERR_RANK: return "rank error";
+    case NTT_ERR_DEGENERATE: return "degenerate input";
+    case NTT_ERR_NONNEG: return "negative input";
+    case NTT_ERR_WORKSPACE: return "workspace too small";
+    case NTT_ERR_CUDA: return "CUDA error";
+    case NTT_ERR_NCCL: return "NCCL error";
+    case NTT_ERR_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+const char* ntt_last_error(ntt_handle h) { return h ? h->err.c_str() : "null handle"; }
+int64_t ntt_launch_count(ntt_handle h) { return h ? h->launches : -1; }
+
+static ntt_status create_common(ntt_handle* out, int device, void* stream) {
+  if (!out) return NTT_ERR_INVALID_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device || device < 0) {
+    cudaGetLastError();
+    return NTT_ERR_CUDA;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) return NTT_ERR_CUDA;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return NTT_ERR_CUDA;
+  if (prop.major != 10) return NTT_ERR_CUDA;  // sm_100a image only
+  ntt_handle h = new ntt_handle_s();
+  h->device = device;
+  h->stream = reinterpret_cast<cudaStream_t>(stream);
+  h->num_sms = prop.multiProcessorCount;
+  *out = h;
+  return NTT_OK;
+}
+
+ntt_status ntt_create(ntt_handle* out, int device, void* cuda_stream) {
+  return create_common(out, device, cuda_stream);
+}
+
+ntt_status ntt_set_stream(ntt_handle h, void* cuda_stream) {
+  if (!h) return NTT_ERR_INVALID_ARG;
+  h->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  return NTT_OK;
+}
+
+ntt_status ntt_destroy(ntt_handle h) {
+  if (!h) return NTT_ERR_INVALID_ARG;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  fused_destroy(h->fused);
+  if (h->ws) cudaFree(h->ws);
+  if (h->stage) cudaFree(h->stage);
+  if (h->host_part) cudaFreeHost(h->host_part);
+  if (h->comm && g_nccl.loaded) g_nccl.CommDestroy(h->comm);
+  delete h;
+  return NTT_OK;
+}
+
+ntt_status ntt_fill_uniform(ntt_handle h, float* p, int64_t count, uint64_t seed, uint64_t stream,
+                            int64_t index_offset) {
+  if (!h) return NTT_ERR_INVALID_ARG;
+  if (!p || count < 0 || index_offset < 0) return fail(h, NTT_ERR_INVALID_ARG, "bad fill_uniform arguments");
+  CU(h, cudaSetDevice(h->device));
+  if (count == 0) return NTT_OK;
+  if (is_device_ptr(p)) {
+    LAUNCH(h, launch_fill_uniform(p, count, seed, stream, index_offset, h->stream));
+    return NTT_OK;
+  }
+  ntt_status s = ensure_stage(h, sizeof(float) * (size_t)count);
+  if (s) return s;
+  float* d = reinterpret_cast<float*>(h->stage);
+  LAUNCH(h, launch_fill_uniform(d, count, seed, stream, index_offset, h->stream));
+  CU(h, cudaMemcpyAsync(p, d, sizeof(float) * (size_t)count, cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  return NTT_OK;
+}
+
+ntt_status ntt_nmf_mu(ntt_handle h, const float* X, int64_t m, int64_t n, int64_t ldx, int32_t r, int32_t iters,
+                      float eps, float* W, float* H, double* objective_trace) {
+  ntt_status s = check_mu_args(h, X, m, n, ldx, r, iters, eps, W, H);
+  if (s) return s;
+  CU(h, cudaSetDevice(h->device));
+  MuPlan p = plan_mu(m, n, r, h->num_sms, h->nranks);
+  const bool xd = is_device_ptr(X), wd = is_device_ptr(W), hd = is_device_ptr(H);
+  // staging layout for host buffers: [X | W | H]
+  size_t sx = xd ? 0 : align_up(sizeof(float) * (size_t)(m * ldx));
+  size_t sw = wd ? 0 : align_up(sizeof(float) * (size_t)(m * r));
+  size_t sh = hd ? 0 : align_up(sizeof(float) * (size_t)(r * n));
+  int nobj = objective_ctas(n);
+  size_t strace = objective_trace ? align_up(sizeof(double) * (size_t)iters * nobj) : 0;
+  if ((s = ensure_ws(h, p.bytes + strace))) return s;
+  if (sx + sw + sh) {
+    if ((s = ensure_stage(h, sx + sw + sh))) return s;
+  }
+  char* stg = reinterpret_cast<char*>(h->stage);
+  const float* dX = X;
+  float* dW = W;
+  float* dH = H;
+  if (!xd) {
+    dX = reinterpret_cast<float*>(stg);
+    CU(h, cudaMemcpyAsync((void*)dX, X, sizeof(float) * (size_t)(m * ldx), cudaMemcpyHostToDevice, h->stream));
+  }
+  if (!wd) {
+    dW = reinterpret_cast<float*>(stg + sx);
+    CU(h, cudaMemcpyAsync(dW, W, sizeof(float) * (size_t)(m * r), cudaMemcpyHostToDevice, h->stream));
+  }
+  if (!hd) {
+    dH = reinterpret_cast<float*>(stg + sx + sw);
+    CU(h, cudaMemcpyAsync(dH, H, sizeof(float) * (size_t)(r * n), cudaMemcpyHostToDevice, h->stream));
+  }
+  char* scratch = reinterpret_cast<char*>(h->ws);
+  double* dtrace = objective_trace ? reinterpret_cast<double*>(scratch + p.bytes) : nullptr;
+  if ((s = run_mu(h, p, dX, ldx, iters, eps, dW, dH, scratch, dtrace))) return s;
+  if (!wd) CU(h, cudaMemcpyAsync(W, dW, sizeof(float) * (size_t)(m * r), cudaMemcpyDeviceToHost, h->stream));
+  if (!hd) CU(h, cudaMemcpyAsync(H, dH, sizeof(float) * (size_t)(r * n), cudaMemcpyDeviceToHost, h->stream));
+  if (objective_trace) {
+    std::vector<double> tmp((size_t)iters * nobj);
+    CU(h, cudaMemcpyAsync(tmp.data(), dtrace, sizeof(double) * tmp.size(), cudaMemcpyDeviceToHost, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    for (int it = 0; it < iters; ++it) {
+      double acc = 0.0;
+      for (int b = 0; b < nobj; ++b) acc += tmp[(size_t)it * nobj + b];
+      objective_trace[it] = 0.5 * acc;
+    }
+  }
+  if (!wd || !hd) CU(h, cudaStreamSynchronize(h->stream));
+  return NTT_OK;
+}
+
+// ------------------------------------------------------------------ decompose
+namespace {
+struct DecompPlan {
+  TTShape s;
+  int64_t nloc_last;         // local extent of the last mode (distributed)
+  int64_t last_off;          // global offset of this rank's block
+  int64_t m[65], ncol[65];   // per step l: rows m_l and LOCAL columns n_l
+  int64_t hbuf[2];           // ping-pong H buffer sizes (floats)
+  int64_t wmax;              // max m_l r_l
+  size_t mu_bytes;
+  size_t off_h0, off_h1, off_w, off_mu, off_cores, bytes;
+  MuPlan mu[65];
+};
+
+void plan_decompose(const TTShape& s, int num_sms, int nranks, int rank, DecompPlan* P) {
+  P->s = s;
+  int64_t off = 0;
+  P->nloc_last = ntt_dist_block(s.dims[s.d - 1], nranks, rank, &off);
+  P->last_off = off;
+  int64_t Nloc = s.N / s.dims[s.d - 1] * P->nloc_last;
+  int64_t rest = Nloc;
+  P->hbuf[0] = P->hbuf[1] = 1;
+  P->wmax = 1;
+  P->mu_bytes = 0;
+  for (int l = 1; l < s.d; ++l) {
+    P->m[l] = s.r[l - 1] * s.dims[l - 1];
+    rest /= s.dims[l - 1];
+    P->ncol[l] = rest;
+    int64_t hsz = s.r[l] * rest;
+    P->hbuf[(l - 1) & 1] = std::max(P->hbuf[(l - 1) & 1], hsz);
+    P->wmax = std::max(P->wmax, P->m[l] * s.r[l]);
+    P->mu[l] = plan_mu(P->m[l], P->ncol[l], (int)s.r[l], num_sms, nranks);
+    P->mu_bytes = std::max(P->mu_bytes, P->mu[l].bytes);
+  }
+  size_t o = 0;
+  P->off_h0 = o;
+  o = align_up(o + sizeof(float) * (size_t)P->hbuf[0]);
+  P->off_h1 = o;
+  o = align_up(o + sizeof(float) * (size_t)P->hbuf[1]);
+  P->off_w = o;
+  o = align_up(o + sizeof(float) * (size_t)P->wmax);
+  P->off_cores = o;
+  o = align_up(o + sizeof(float) * (size_t)s.cores);
+  P->off_mu = o;
+  o = align_up(o + P->mu_bytes);
+  P->bytes = o;
+}
+}  // namespace
+
+size_t ntt_decompose_workspace_bytes(int32_t d, const int64_t* dims, const int32_t* ranks) {
+  TTShape s;
+  if (check_tt(nullptr, d, dims, ranks, &s, true) != NTT_OK) return 0;
+  DecompPlan* P = new DecompPlan();
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaGetLastError();
+  plan_decompose(s, sms, 1, 0, P);
+  size_t b = P->bytes;
+  delete P;
+  return b;
+}
+
+ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t* dims, const int32_t* ranks,
+                         int32_t iters, uint64_t seed, float eps, float* cores, void* workspace,
+                         size_t workspace_bytes) {
+  if (!h) return NTT_ERR_INVALID_ARG;
+  if (!A || !cores) return fail(h, NTT_ERR_INVALID_ARG, "null A or cores");
+  if (iters < 0) return fail(h, NTT_ERR_INVALID_ARG, "iters < 0");
+  if (!(eps >= 0.0f)) return fail(h, NTT_ERR_INVALID_ARG, "eps must be >= 0");
+  TTShape s;
+  ntt_status st = check_tt(h, d, dims, ranks, &s, true);
+  if (st) return st;
+  if (h->nranks > 1 && s.dims[d - 1] < h->nranks)
+    return fail(h, NTT_ERR_DIMENSION, "last mode (%lld) smaller than the number of ranks (%d)",
+                (long long)s.dims[d - 1], h->nranks);
+  CU(h, cudaSetDevice(h->device));
+  DecompPlan* Pp = new DecompPlan();
+  std::unique_ptr<DecompPlan> guard(Pp);
+  DecompPlan& P = *Pp;
+  plan_decompose(s, h->num_sms, h->nranks, h->rank, &P);
+  char* ws;
+  if (workspace) {
+    if (workspace_bytes < P.bytes)
+      return fail(h, NTT_ERR_WORKSPACE, "workspace %zu < required %zu bytes", workspace_bytes, P.bytes);
+    if (!is_device_ptr(workspace)) return fail(h, NTT_ERR_INVALID_ARG, "workspace must be device memory");
+    ws = reinterpret_cast<char*>(workspace);
+  } else {
+    if ((st = ensure_ws(h, P.bytes))) return st;
+    ws = reinterpret_cast<char*>(h->ws);
+  }
+  cudaStream_t cs = h->stream;
+  const int64_t Nloc = s.N / s.dims[d - 1] * P.nloc_last;
+  const float* dA = A;
+  if (!is_device_ptr(A)) {
+    if ((st = ensure_stage(h, sizeof(float) * (size_t)Nloc))) return st;
+    dA = reinterpret_cast<const float*>(h->stage);
+    CU(h, cudaMemcpyAsync((void*)dA, A, sizeof(float) * (size_t)Nloc, cudaMemcpyHostToDevice, cs));
+  }
+  const bool cores_dev = is_device_ptr(cores);
+  float* dcores = cores_dev ? cores : reinterpret_cast<float*>(ws + P.off_cores);
+  float* hb[2] = {reinterpret_cast<float*>(ws + P.off_h0), reinterpret_cast<float*>(ws + P.off_h1)};
+  float* Wd = reinterpret_cast<float*>(ws + P.off_w);
+  char* mus = ws + P.off_mu;
+  const float* X = dA;
+  float* Hl = nullptr;
+  for (int l = 1; l < d; ++l) {
+    const int64_t m = P.m[l], n = P.ncol[l];
+    const int r = (int)s.r[l];
+    Hl = hb[(l - 1) & 1];
+    LAUNCH(h, launch_fill_uniform(Wd, m * r, seed, stream_w(l), 0, cs));
+    if (h->nranks == 1) {
+      LAUNCH(h, launch_fill_uniform(Hl, (int64_t)r * n, seed, stream_h(l), 0, cs));
+    } else {
+      // global column index of local column c: (c / b) * n_d + off + c % b  (DESIGN.md s.7)
+      const int64_t nglob = n / P.nloc_last * s.dims[d - 1];
+      LAUNCH(h, launch_fill_uniform_cols(Hl, r, n, P.nloc_last, s.dims[d - 1], P.last_off, nglob, seed,
+                                         stream_h(l), cs));
+    }
+    if ((st = run_mu(h, P.mu[l], X, n, iters, eps, Wd, Hl, mus, nullptr))) return st;
+    CU(h, cudaMemcpyAsync(dcores + s.off[l], Wd, sizeof(float) * (size_t)(m * r), cudaMemcpyDeviceToDevice, cs));
+    X = Hl;
+  }
+  // last core G_d[k][i][0] = T_{d-1}[k][i]  (Alg. 2 l.11)
+  const int64_t rl = s.r[d - 1], nd = s.dims[d - 1];
+  if (h->nranks == 1) {
+    CU(h, cudaMemcpyAsync(dcores + s.off[d], Hl, sizeof(float) * (size_t)(rl * nd), cudaMemcpyDeviceToDevice, cs));
+  } else {
+    // all_gather of the ragged column blocks: one broadcast per rank into a
+    // staging area (rank-major), then a permute into the core layout.
+    float* gath = Wd;  // reuse: needs rl * nd floats <= wmax? not guaranteed -> use mu scratch
+    gath = reinterpret_cast<float*>(mus);
+    NC(h, g_nccl.GroupStart());
+    for (int g = 0; g < h->nranks; ++g) {
+      int64_t og = 0;
+      int64_t bg = ntt_dist_block(nd, h->nranks, g, &og);
+      const float* src = (g == h->rank) ? Hl : nullptr;
+      NC(h, g_nccl.Broadcast(src ? src : gath + rl * og, gath + rl * og, (size_t)(rl * bg), ncclFloat32, g, h->comm,
+                             cs));
+    }
+    NC(h, g_nccl.GroupEnd());
+    LAUNCH(h, launch_gather_last_core(gath, rl, nd, h->nranks, dcores + s.off[d], cs));
+  }
+  if (!cores_dev) {
+    CU(h, cudaMemcpyAsync(cores, dcores, sizeof(float) * (size_t)s.cores, cudaMemcpyDeviceToHost, cs));
+    CU(h, cudaStreamSynchronize(cs));
+  }
+  return NTT_OK;
+}
+
+// -------------------------------------------------------- reconstruct / error
+namespace {
+ntt_status contract_stream(ntt_handle h, const TTShape& s, const float* cores, float* out, float noise_amp,
+                           uint64_t noise_key, const float* ref, double* rel_err) {
+  cudaStream_t cs = h->stream;
+  const int d = s.d;
+  // split bond k minimising |L| + |R| = N_L r_k + r_k N_R
+  int best = 1;
+  double bestc = 1e300;
+  for (int k = 1; k < d; ++k) {
+    double NL = 1, NR = 1;
+    for (int l = 0; l < k; ++l) NL *= (double)s.dims[l];
+    for (int l = k; l < d; ++l) NR *= (double)s.dims[l];
+    double c = (NL + NR) * (double)s.r[k];
+    if (c < bestc) {
+      bestc = c;
+      best = k;
+    }
+  }
+  const int k = best;
+  int64_t NL = 1, NR = 1;
+  for (int l = 0; l < k; ++l) NL *= s.dims[l];
+  for (int l = k; l < d; ++l) NR *= s.dims[l];
+  // scratch sizes: left chain max N_l r_l (l <= k), right chain max r_{l-1} prod_{i>=l} n_i
+  int64_t lmax = 1, rmax = 1, acc = 1;
+  for (int l = 1; l <= k; ++l) {
+    acc *= s.dims[l - 1];
+    lmax = std::max(lmax, acc * s.r[l]);
+  }
+  acc = 1;
+  for (int l = d; l > k; --l) {
+    acc *= s.dims[l - 1];
+    rmax = std::max(rmax, s.r[l - 1] * acc);
+  }
+  const bool cores_dev = is_device_ptr(cores);
+  const bool out_dev = !out || is_device_ptr(out);
+  const bool ref_dev = !ref || is_device_ptr(ref);
+  int grid = stream_ctas(NL, NR, h->num_sms);
+  size_t need = align_up(sizeof(float) * (size_t)(2 * lmax)) + align_up(sizeof(float) * (size_t)(2 * rmax)) +
+                align_up(sizeof(double) * 2 * (size_t)grid) + align_up(sizeof(float) * (size_t)s.cores);
+  ntt_status st = ensure_ws(h, need);
+  if (st) return st;
+  char* ws = reinterpret_cast<char*>(h->ws);
+  float* Lb[2] = {reinterpret_cast<float*>(ws), reinterpret_cast<float*>(ws) + lmax};
+  ws += align_up(sizeof(float) * (size_t)(2 * lmax));
+  float* Rb[2] = {reinterpret_cast<float*>(ws), reinterpret_cast<float*>(ws) + rmax};
+  ws += align_up(sizeof(float) * (size_t)(2 * rmax));
+  double* part = reinterpret_cast<double*>(ws);
+  ws += align_up(sizeof(double) * 2 * (size_t)grid);
+  const float* dc = cores;
+  if (!cores_dev) {
+    float* t = reinterpret_cast<float*>(ws);
+    CU(h, cudaMemcpyAsync(t, cores, sizeof(float) * (size_t)s.cores, cudaMemcpyHostToDevice, cs));
+    dc = t;
+  }
+  // host staging for out / ref
+  size_t sbytes = (out_dev ? 0 : align_up(sizeof(float) * (size_t)s.N)) + (ref_dev ? 0 : align_up(sizeof(float) * (size_t)s.N));
+  if (sbytes && (st = ensure_stage(h, sbytes))) return st;
+  float* dout = out;
+  const float* dref = ref;
+  char* sg = reinterpret_cast<char*>(h->stage);
+  if (!out_dev) {
+    dout = reinterpret_cast<float*>(sg);
+    sg += align_up(sizeof(float) * (size_t)s.N);
+  }
+  if (!ref_dev) {
+    float* t = reinterpret_cast<float*>(sg);
+    CU(h, cudaMemcpyAsync(t, ref, sizeof(float) * (size_t)s.N, cudaMemcpyHostToDevice, cs));
+    dref = t;
+  }
+  // left chain: L_1 = G_1 (n_1 x r_1)
+  const float* L = dc + s.off[1];
+  int64_t Ncur = s.dims[0];
+  for (int l = 2; l <= k; ++l) {
+    float* o = Lb[l & 1];
+    LAUNCH(h, launch_contract_left(L, Ncur, (int)s.r[l - 1], dc + s.off[l], s.dims[l - 1], (int)s.r[l], o, cs));
+    L = o;
+    Ncur *= s.dims[l - 1];
+  }
+  // right chain: R_d = G_d (r_{d-1} x n_d)
+  const float* R = dc + s.off[d];
+  int64_t NRcur = s.dims[d - 1];
+  for (int l = d - 1; l > k; --l) {
+    float* o = Rb[l & 1];
+    LAUNCH(h, launch_contract_right(dc + s.off[l], (int)s.r[l - 1], s.dims[l - 1], (int)s.r[l], R, NRcur, o, cs));
+    R = o;
+    NRcur *= s.dims[l - 1];
+  }
+  LAUNCH(h, launch_tt_stream(L, R, NL, NR, (int)s.r[k], dout, noise_amp, noise_key, dref, dref ? part : nullptr, grid, cs));
+  if (!out_dev) CU(h, cudaMemcpyAsync(out, dout, sizeof(float) * (size_t)s.N, cudaMemcpyDeviceToHost, cs));
+  if (rel_err) {
+    if ((st = ensure_host_part(h, 2 * (size_t)grid))) return st;
+    CU(h, cudaMemcpyAsync(h->host_part, part, sizeof(double) * 2 * (size_t)grid, cudaMemcpyDeviceToHost, cs));
+    CU(h, cudaStreamSynchronize(cs));
+    double num = 0.0, den = 0.0;
+    for (int b = 0; b < grid; ++b) {
+      num += h->host_part[2 * b];
+      den += h->host_part[2 * b + 1];
+    }
+    if (den == 0.0) return fail(h, NTT_ERR_DEGENERATE, "||ref||_F = 0");
+    *rel_err = sqrt(num) / sqrt(den);
+  }
+  if (!out_dev) CU(h, cudaStreamSynchronize(cs));
+  return NTT_OK;
+}
+}  // namespace
+
+ntt_status ntt_reconstruct(ntt_handle h, int32_t d, const int64_t* dims, const int32_t* ranks, const float* cores,
+                           float* out, const float* ref, double* rel_err) {
+  if (!h) return NTT_ERR_INVALID_ARG;
+  if (!cores) return fail(h, NTT_ERR_INVALID_ARG, "null cores");
+  if (rel_err && !ref) return fail(h, NTT_ERR_INVALID_ARG, "rel_err needs ref");
+  TTShape s;
+  ntt_status st = check_tt(h, d, dims, ranks, &s, false);
+  if (st) return st;
+  CU(h, cudaSetDevice(h->device));
+  return contract_stream(h, s, cores, out, 0.0f, 0, ref, rel_err);
+}
+
+ntt_status ntt_generate(ntt_handle h, int32_t d, const int64_t* dims, const int32_t* ranks, const float* cores,
+                        float noise_amp, uint64_t seed, uint64_t noise_stream, float* out) {
+  if (!h) return NTT_ERR_INVALID_ARG;
+  if (!cores || !out) return fail(h, NTT_ERR_INVALID_ARG, "null cores or out");
+  TTShape s;
+  ntt_status st = check_tt(h, d, dims, ranks, &s, false);
+  if (st) return st;
+  CU(h, cudaSetDevice(h->device));
+  return contract_stream(h, s, cores, out, noise_amp, rng_key(seed, noise_stream), nullptr, nullptr);
+}
+
+double ntt_compression_ratio(int32_t d, const int64_t* dims, const int32_t* ranks) {
+  if (d < 1 || d > 64 || !dims || (d > 1 && !ranks)) return -1.0;
+  double num = 1.0, den = 0.0;
+  for (int i = 1; i <= d; ++i) {
+    double rp = (i == 1) ? 1.0 : (double)ranks[i - 2];
+    double rn = (i == d) ? 1.0 : (double)ranks[i - 1];
+    if (dims[i - 1] < 1 || rp < 1 || rn < 1) return -1.0;
+    num *= (double)dims[i - 1];
+    den += (double)dims[i - 1] * rp * rn;
+  }
+  return num / den;
+}
+
+// ------------------------------------------------------------------ distributed
+int64_t ntt_dist_block(int64_t n_last, int nranks, int rank, int64_t* offset) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || n_last < 0) {
+    if (offset) *offset = 0;
+    return -1;
+  }
+  int64_t b0 = n_last * rank / nranks, b1 = n_last * (rank + 1) / nranks;
+  if (offset) *offset = b0;
+  return b1 - b0;
+}
+
+ntt_status ntt_get_unique_id(void* id128) {
+  if (!id128) return NTT_ERR_INVALID_ARG;
+  if (!load_nccl()) return NTT_ERR_UNSUPPORTED;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return NTT_ERR_NCCL;
+  memcpy(id128, &id, sizeof id);
+  return NTT_OK;
+}
+
+ntt_status ntt_create_dist(ntt_handle* out, int device, void* cuda_stream, const void* id128, int nranks, int rank) {
+  if (!out || !id128 || nranks < 1 || rank < 0 || rank >= nranks) return NTT_ERR_INVALID_ARG;
+  if (!load_nccl()) return NTT_ERR_UNSUPPORTED;
+  ntt_status s = create_common(out, device, cuda_stream);
+  if (s) return s;
+  ntt_handle h = *out;
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof id);
+  ncclResult_t r = g_nccl.CommInitRank(&h->comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    delete h;
+    *out = nullptr;
+    return NTT_ERR_NCCL;
+  }
+  h->nranks = nranks;
+  h->rank = rank;
+  return NTT_OK;
+}
+
+int ntt_dist_rank(ntt_handle h) { return h ? h->rank : -1; }
+int ntt_dist_size(ntt_handle h) { return h ? h->nranks : -1; }
+
+}  // extern "C"

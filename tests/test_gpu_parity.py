@@ -1,0 +1,270 @@
+"""GPU parity: libntt's sm_100a kernels (through the C ABI) vs the CPU oracle.
+
+Tolerances (BASELINE north_star, readings R14/R15, DESIGN.md s.6):
+  factors / cores after <= 10 iterations (and after the full config-1 run):
+      ||G_gpu - G_ora||_F <= 1e-4 ||G_ora||_F  and  max|G_gpu - G_ora| <= 1e-4 max|G_ora|
+  final relative reconstruction error:  |e_gpu - e_ora| <= 1e-3 e_ora + 1e-6
+  RNG / init: bit exact.
+"""
+import numpy as np
+import pytest
+
+import ntt_inputs as ni
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def h():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2008_01340_b200 as P
+    return P.Handle(0)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def assert_close_factor(got, ref, tol=TOL, what=""):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    assert got.shape == ref.shape
+    assert np.all(np.isfinite(got)), what
+    fro = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    mx = np.abs(got - ref).max() / np.abs(ref).max()
+    assert fro <= tol and mx <= tol, f"{what}: rel fro {fro:.3e}, rel max {mx:.3e}"
+
+
+# ------------------------------------------------------------------- RNG ------
+@pytest.mark.parametrize("seed,stream,off", [(0, 0x203, 0), (12345, 0x201, 7), (2**63 + 1, 0x300, 2**33)])
+def test_fill_uniform_bit_exact(h, ora, seed, stream, off):
+    n = 300_001
+    t = torch.empty(n, dtype=torch.float32, device="cuda")
+    h.ntt_fill_uniform(t, n, seed, stream, off)
+    got = host(t).astype(np.float64)
+    assert np.array_equal(got, ni.uniform(n, seed, stream, off))
+    idx = [0, 1, 17, n - 1]
+    assert [got[i] for i in idx] == [ora.fill_uniform(1, seed, stream, off + i)[0] for i in idx]
+
+
+def test_fill_uniform_host_pointer(h):
+    a = np.empty(1000, np.float32)
+    h.ntt_fill_uniform(a, 1000, 3, 0x205, 0)
+    assert np.array_equal(a.astype(np.float64), ni.uniform(1000, 3, 0x205))
+
+
+# ---------------------------------------------------------------- MU NMF -----
+MU_CASES = [
+    # m, n, r, iters  -- short-wide (1-pass), ragged tails, tall / square (2-pass), r up to 32
+    (5, 120, 4, 10),
+    (16, 30, 3, 10),
+    (32, 5003, 8, 10),
+    (6, 10001, 5, 10),
+    (30, 4097, 5, 10),
+    (256, 2051, 8, 10),
+    (128, 700, 16, 10),
+    (700, 90, 3, 10),
+    (300, 257, 32, 6),
+    (1, 50, 1, 10),
+    (40, 1, 1, 10),
+]
+
+
+def _mu_inputs(m, n, r, seed):
+    rng = np.random.default_rng(seed)
+    X = (rng.random((m, n)) * 4).astype(np.float32)
+    W0 = ni.uniform(m * r, seed, 0x202).reshape(m, r).astype(np.float32)
+    H0 = ni.uniform(r * n, seed, 0x203).reshape(r, n).astype(np.float32)
+    return X, W0, H0
+
+
+@pytest.mark.parametrize("m,n,r,iters", MU_CASES)
+def test_nmf_mu_parity(h, ora, m, n, r, iters):
+    X, W0, H0 = _mu_inputs(m, n, r, m * 7 + n)
+    Xd, Wd, Hd = dev(X), dev(W0), dev(H0)
+    h.ntt_nmf_mu(Xd, m, n, n, r, iters, 1e-16, Wd, Hd)
+    Wo, Ho = ora.nmf_mu(X, W0.astype(np.float64), H0.astype(np.float64), iters, eps=1e-16)
+    assert_close_factor(host(Wd), Wo, what=f"W {m}x{n} r{r}")
+    assert_close_factor(host(Hd), Ho, what=f"H {m}x{n} r{r}")
+    assert np.all(host(Wd) >= 0) and np.all(host(Hd) >= 0)
+
+
+def test_nmf_mu_leading_dimension(h, ora):
+    m, n, r, ldx = 20, 333, 4, 400
+    X, W0, H0 = _mu_inputs(m, ldx, r, 5)
+    H0 = np.ascontiguousarray(H0[:, :n])
+    Xd, Wd, Hd = dev(X), dev(W0), dev(H0)
+    h.ntt_nmf_mu(Xd, m, n, ldx, r, 8, 1e-16, Wd, Hd)
+    Wo, Ho = ora.nmf_mu(np.ascontiguousarray(X[:, :n]), W0.astype(np.float64), H0.astype(np.float64), 8)
+    assert_close_factor(host(Wd), Wo, what="W ldx")
+    assert_close_factor(host(Hd), Ho, what="H ldx")
+
+
+def test_nmf_mu_objective_trace_and_monotone(h, ora):
+    m, n, r, iters = 24, 999, 4, 25
+    X, W0, H0 = _mu_inputs(m, n, r, 1)
+    Xd, Wd, Hd = dev(X), dev(W0), dev(H0)
+    tr = np.array(h.ntt_nmf_mu(Xd, m, n, n, r, iters, 1e-16, Wd, Hd, trace=True))
+    _, _, tro = ora.nmf_mu(X, W0.astype(np.float64), H0.astype(np.float64), iters, trace=True)
+    assert np.allclose(tr, tro, rtol=1e-4)
+    assert np.all(np.diff(tr) <= 1e-5 * tr[:-1])
+
+
+def test_nmf_mu_host_pointers(h, ora):
+    m, n, r = 12, 500, 3
+    X, W0, H0 = _mu_inputs(m, n, r, 2)
+    W, H = W0.copy(), H0.copy()
+    h.ntt_nmf_mu(X, m, n, n, r, 5, 1e-16, W, H)
+    Wo, Ho = ora.nmf_mu(X, W0.astype(np.float64), H0.astype(np.float64), 5)
+    assert_close_factor(W, Wo, what="W host")
+    assert_close_factor(H, Ho, what="H host")
+
+
+def test_nmf_mu_zero_iterations_is_identity(h):
+    X, W0, H0 = _mu_inputs(8, 64, 2, 3)
+    Wd, Hd = dev(W0), dev(H0)
+    h.ntt_nmf_mu(dev(X), 8, 64, 64, 2, 0, 1e-16, Wd, Hd)
+    assert np.array_equal(host(Wd), W0) and np.array_equal(host(Hd), H0)
+
+
+def test_nmf_mu_scale_invariance_and_determinism(h):
+    """Metamorphic (no oracle): X -> 8X gives W -> 8W, H unchanged; repeat runs bit-identical."""
+    m, n, r = 32, 4096, 8
+    X, W0, H0 = _mu_inputs(m, n, r, 4)
+    outs = []
+    for scale in (1.0, 8.0, 1.0):
+        Wd, Hd = dev(W0), dev(H0)
+        h.ntt_nmf_mu(dev(X * np.float32(scale)), m, n, n, r, 5, 0.0, Wd, Hd)
+        outs.append((host(Wd), host(Hd)))
+    assert np.array_equal(outs[0][0], outs[2][0]) and np.array_equal(outs[0][1], outs[2][1])
+    assert np.array_equal(outs[1][0], 8 * outs[0][0])
+    assert np.array_equal(outs[1][1], outs[0][1])
+
+
+@pytest.mark.parametrize("bad", ["rank0", "rank_big", "ldx", "iters"])
+def test_nmf_mu_rejects_bad_args(h, bad):
+    import paper_2008_01340_b200 as P
+    X, W0, H0 = _mu_inputs(8, 64, 2, 3)
+    args = dict(m=8, n=64, ldx=64, r=2, iters=3)
+    if bad == "rank0":
+        args["r"] = 0
+    elif bad == "rank_big":
+        args["r"] = 9
+    elif bad == "ldx":
+        args["ldx"] = 10
+    else:
+        args["iters"] = -1
+    with pytest.raises(P.NttError) as e:
+        h.ntt_nmf_mu(dev(X), args["m"], args["n"], args["ldx"], args["r"], args["iters"], 1e-16, dev(W0), dev(H0))
+    assert e.value.status == (3 if bad.startswith("rank") else 1)
+
+
+# ----------------------------------------------------------------- nTT -------
+def _tt_case(dims, ranks, seed=0, noise=0.0):
+    import oracle
+    cores = ni.make_cores(dims, ranks, seed)
+    A = oracle.tt_full_f32(dims, ranks, cores, noise_amp=noise, seed=seed)
+    return A
+
+
+def _cores_check(dims, ranks, got, ref, tol=TOL):
+    import oracle
+    for l, (g, o) in enumerate(zip(oracle.unpack_cores(dims, ranks, got), oracle.unpack_cores(dims, ranks, ref))):
+        assert_close_factor(g, o, tol, what=f"core {l + 1}")
+
+
+NTT_CASES = [
+    # dims, ranks, iters, noise
+    ([5, 4, 5, 6], [4, 3, 2], 10, 0.0),      # config 1 shape at the 10-iteration parity point
+    ([5, 4, 5, 6], [4, 3, 2], 200, 0.0),     # config 1 in full
+    ([8, 8, 8, 8, 8], [4, 4, 4, 4], 10, 0.5),
+    ([6] * 7, [5] * 6, 10, 0.0),             # config-4-like, 6^7
+    ([16, 16, 16, 16], [8, 8, 8], 10, 1.0),
+    ([7, 3, 11], [3, 5], 10, 0.0),
+]
+
+
+@pytest.mark.parametrize("dims,ranks,iters,noise", NTT_CASES)
+def test_decompose_parity(h, ora, dims, ranks, iters, noise):
+    A = _tt_case(dims, ranks, 0, noise)
+    ncore = ora.cores_size(dims, ranks)
+    cores = torch.empty(ncore, dtype=torch.float32, device="cuda")
+    h.ntt_decompose(dev(A), dims, ranks, iters, 0, 1e-16, cores)
+    got = host(cores)
+    ref = ora.ntt_decompose(A, ranks, iters, seed=0)
+    _cores_check(dims, ranks, got, ref)
+    assert np.all(got >= 0)
+    e_gpu = h.ntt_reconstruct(dims, ranks, cores, ref=dev(A), want_error=True)
+    e_ora = ora.tt_rel_error(A, ranks, ref)
+    assert abs(e_gpu - e_ora) <= 1e-3 * e_ora + 1e-6, (e_gpu, e_ora)
+
+
+def test_decompose_rank1_exact(h, ora):
+    dims = [5, 4, 6, 3, 2]
+    cores = (np.floor(ni.make_cores(dims, [1] * 4, seed=3) * 8) + 1) / 8
+    A = ora.tt_full_f32(dims, [1] * 4, cores)
+    out = torch.empty(ora.cores_size(dims, [1] * 4), dtype=torch.float32, device="cuda")
+    h.ntt_decompose(dev(A), dims, [1] * 4, 1, 0, 1e-16, out)
+    e = h.ntt_reconstruct(dims, [1] * 4, out, ref=dev(A), want_error=True)
+    assert e < 1e-6
+
+
+def test_decompose_host_pointers_and_workspace(h, ora):
+    import paper_2008_01340_b200 as P
+    dims, ranks = [6, 5, 4, 7], [3, 4, 2]
+    A = _tt_case(dims, ranks, 1, 0.2)
+    c_host = np.empty(ora.cores_size(dims, ranks), np.float32)
+    h.ntt_decompose(A, dims, ranks, 10, 1, 1e-16, c_host)
+    wsb = P.ntt_decompose_workspace_bytes(dims, ranks)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    c_dev = torch.empty_like(torch.from_numpy(c_host)).cuda()
+    h.ntt_decompose(dev(A), dims, ranks, 10, 1, 1e-16, c_dev, ws, wsb)
+    assert np.array_equal(host(c_dev), c_host)
+    with pytest.raises(P.NttError) as e:
+        h.ntt_decompose(dev(A), dims, ranks, 10, 1, 1e-16, c_dev, ws, wsb - 1)
+    assert e.value.status == 6
+    with pytest.raises(P.NttError) as e:
+        h.ntt_decompose(dev(A), dims, [3, 40, 2], 10, 1, 1e-16, c_dev)
+    assert e.value.status == 3
+
+
+# ---------------------------------------------------- reconstruct / generate --
+@pytest.mark.parametrize("dims,ranks", [([5, 4, 5, 6], [4, 3, 2]), ([3, 7], [2]), ([4] * 6, [3, 5, 2, 4, 3]),
+                                        ([9, 1, 5, 2], [2, 2, 2])])
+def test_reconstruct_parity(h, ora, dims, ranks):
+    cores = ni.make_cores(dims, ranks, seed=2).astype(np.float32)
+    out = torch.empty(int(np.prod(dims)), dtype=torch.float32, device="cuda")
+    h.ntt_reconstruct(dims, ranks, dev(cores), out=out)
+    ref = ora.tt_full(dims, ranks, cores.astype(np.float64)).ravel()
+    got = host(out).astype(np.float64)
+    assert np.all(np.abs(got - ref) <= 1e-5 * np.abs(ref).max())
+    A = ora.tt_full_f32(dims, ranks, ni.make_cores(dims, ranks, seed=3), noise_amp=0.1, seed=3)
+    e = h.ntt_reconstruct(dims, ranks, dev(cores), ref=dev(A), want_error=True)
+    eo = ora.tt_rel_error(A, ranks, cores.astype(np.float64))
+    assert abs(e - eo) <= 1e-5 * eo
+
+
+def test_reconstruct_degenerate(h):
+    import paper_2008_01340_b200 as P
+    dims, ranks = [3, 4], [2]
+    with pytest.raises(P.NttError) as e:
+        h.ntt_reconstruct(dims, ranks, dev(np.ones(14, np.float32)), ref=dev(np.zeros(12, np.float32)), want_error=True)
+    assert e.value.status == 4
+
+
+def test_generate_matches_oracle_generator(h, ora):
+    dims, ranks = [8, 6, 7, 5], [3, 4, 2]
+    cores = ni.make_cores(dims, ranks, seed=5)
+    out = torch.empty(int(np.prod(dims)), dtype=torch.float32, device="cuda")
+    h.ntt_generate(dims, ranks, dev(cores.astype(np.float32)), 0.25, 5, 0x300, out)
+    ref = ora.tt_full_f32(dims, ranks, cores, noise_amp=0.25, seed=5).ravel()
+    assert np.allclose(host(out), ref, rtol=2e-6, atol=0)
