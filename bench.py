@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""bench.py -- MU-NMF nTT hot path on B200 (arXiv 2008.01340), BASELINE.json metric.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload config3]
+
+A step is one pass of the whole hot path (SURVEY s.8(a) rows a1-a7) over one
+synthetic input: ntt_decompose (unfold, init, MU W/H half-steps, core emission,
+sweep) plus the Eq. 3 relative error of the result.  Default workload: config 3
+(32^6 fp32 = 4.29 GB > L2, TT ranks 8, 100 MU iterations per step -> 500 MU
+iterations per decomposition), the largest BASELINE config the nTT sweep runs on
+at 1 GPU.  Under torchrun (N > 1) the last tensor mode is block-partitioned over
+the ranks (strong scaling, one NCCL all-reduce of the fp64 (XH^T, HH^T)
+partials per MU pass).
+
+Prints ONE JSON line (rank 0).  See DESIGN.md s.8 for the roofline bytes.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "NMF-MU iterations/sec (nTT sweep, all d-1 steps; ntt wall time and HBM GB/s in roofline)"
+UNIT = "MU-iter/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="config3")
+    ap.add_argument("--iters", type=int, default=None, help="override MU iterations per TT step")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rk = int(os.environ.get("RANK", "0"))
+    lr = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rk, lr
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            return None
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------ workload
+def workload(name: str, iters_override=None):
+    import ntt_inputs as ni
+    w = ni.workloads()[name]
+    if w.kind != "ntt":
+        raise SystemExit(f"bench runs the nTT sweep; {name} is a single-NMF parity case")
+    if iters_override:
+        w.iters = iters_override
+    return w
+
+
+def step_shapes(dims, ranks):
+    fr = [1, *ranks, 1]
+    N = 1
+    for x in dims:
+        N *= x
+    out, rest = [], N
+    for l in range(1, len(dims)):
+        rest //= dims[l - 1]
+        out.append((fr[l - 1] * dims[l - 1], rest, fr[l]))
+    return out
+
+
+# ------------------------------------------------------------- oracle timing
+def oracle_sample_time(dims, ranks, iters, budget_elems=1 << 25):
+    """Oracle (as it stands) timed on the host: for every TT step l, one MU iteration
+    on a column sample of X_l (<= budget_elems entries, real shape otherwise),
+    scaled linearly in the column count, times `iters`.  Returns (seconds per full
+    decomposition, threads, description)."""
+    import numpy as np
+
+    import ntt_inputs as ni
+    import oracle
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    total = 0.0
+    parts = []
+    for l, (m, n, r) in enumerate(step_shapes(dims, ranks), start=1):
+        ns = max(1, min(n, budget_elems // m))
+        X = ni.uniform(m * ns, 7, 0x500 + l).reshape(m, ns)
+        X = X.astype(np.float32) if l == 1 else X
+        W0 = ni.uniform(m * r, 0, ni.stream_w(l)).reshape(m, r)
+        H0 = ni.uniform(r * ns, 0, ni.stream_h(l)).reshape(r, ns)
+        t0 = time.perf_counter()
+        oracle.nmf_mu(X, W0, H0, 1)
+        dt = time.perf_counter() - t0
+        total += dt * (n / ns) * iters
+        parts.append(f"step{l}:{m}x{ns}/{n}")
+    desc = ("oracle (C, fp64, OpenMP over independent outputs) 1 MU iteration per TT step on a column sample "
+            f"({', '.join(parts)}), scaled by n/sample and x{iters} iterations")
+    return total, threads, desc
+
+
+def run_reference(args):
+    ws, rk, _ = dist_env()
+    if ws > 1 and rk != 0:
+        return 0
+    w = workload(args.workload, args.iters)
+    its = (len(w.dims) - 1) * w.iters
+    times = []
+    threads, desc = 1, ""
+    for s in range(args.warmup + args.steps):
+        t, threads, desc = oracle_sample_time(w.dims, w.ranks, w.iters)
+        if s >= args.warmup:
+            times.append(t)
+    t = statistics.median(times)
+    v = its / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "dims": w.dims, "ranks": w.ranks, "iters_per_step": w.iters,
+                   "mu_iters_per_step": its},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------- ours ---
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import ntt_inputs as ni
+    import paper_2008_01340_b200 as P
+
+    ws, rk, lr = dist_env()
+    torch.cuda.set_device(lr)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+    w = workload(args.workload, args.iters)
+    dims, ranks, iters = list(w.dims), list(w.ranks), w.iters
+    d = len(dims)
+    its = (d - 1) * iters
+    stream = torch.cuda.current_stream()
+    if ws > 1:
+        uid = [P.ntt_get_unique_id() if rk == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        h = P.Handle(lr, stream.cuda_stream, unique_id=uid[0], nranks=ws, rank=rk)
+    else:
+        h = P.Handle(lr, stream.cuda_stream)
+
+    # synthetic input: random TT cores, contracted + noise on device
+    cores0 = ni.make_cores(dims, ranks, w.seed)
+    b, off = P.ntt_dist_block(dims[-1], ws, rk)
+    ldims = dims[:-1] + [b]
+    fr = [1, *ranks, 1]
+    last = cores0[-fr[d - 1] * dims[-1]:].reshape(fr[d - 1], dims[-1])[:, off:off + b]
+    lcores = np.concatenate([cores0[:-fr[d - 1] * dims[-1]], last.ravel()]).astype(np.float32)
+    Nloc = int(np.prod(ldims))
+    A = torch.empty(Nloc, dtype=torch.float32, device="cuda")
+    h.ntt_generate(ldims, ranks, torch.from_numpy(lcores).cuda(), w.noise_amp, w.seed, ni.STREAM_NOISE, A)
+    cores = torch.empty(P.cores_size(dims, ranks), dtype=torch.float32, device="cuda")
+
+    def step():
+        return h.ntt_decompose(A, dims, ranks, iters, w.seed, 1e-16, cores, want_error=True)
+
+    for _ in range(args.warmup):
+        err = step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = ClockSampler(lr)
+    clk.start()
+    h.ntt_profile_enable(True)
+    l0 = h.launch_count
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        err = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = clk.stop()
+    launches = h.launch_count - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    prof = {c: h.ntt_profile_get(c) for c in range(5)}
+    h.ntt_profile_enable(False)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- e2e: same call with HOST buffers (pinned), H2D/D2H inside the call
+    e2e = None
+    if not args.no_e2e:
+        Ah = torch.empty(Nloc, dtype=torch.float32, pin_memory=True)
+        Ah.copy_(A)
+        ch = torch.empty(cores.numel(), dtype=torch.float32, pin_memory=True)
+        h.ntt_decompose(Ah, dims, ranks, iters, w.seed, 1e-16, ch, want_error=True)  # warm staging buffers
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record(stream)
+        for _ in range(args.steps):
+            h.ntt_decompose(Ah, dims, ranks, iters, w.seed, 1e-16, ch, want_error=True)
+        q1.record(stream)
+        torch.cuda.synchronize()
+        ems = q0.elapsed_time(q1) / args.steps
+        if dist:
+            t = torch.tensor([ems], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": its / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(Nloc * 4) * ws,
+               "d2h_bytes_per_step": int(cores.numel() * 4 + 8) * ws, "ms_per_step": ems}
+        del Ah
+
+    # ---- roofline: dominant kernel = MU X-stream pass (class 0)
+    pk, pk_kind = peaks()
+    n0, ms0, by0 = prof[0]
+    achieved = (by0 / (ms0 / 1e3)) / 1e9 if ms0 > 0 else 0.0
+    total_prof_ms = sum(v[1] for v in prof.values())
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        traffic = tj.get(args.workload, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": pk, "unit": "GB/s", "frac": achieved / pk,
+                "traffic": traffic, "peak_kind": pk_kind, "kernel": "MU X-stream pass (class 0)",
+                "launches": n0, "kernel_ms_per_step": ms0 / args.steps,
+                "kernel_share_of_step": (ms0 / args.steps) / ms if ms > 0 else None,
+                "algorithmic_bytes_per_launch": by0 / n0 if n0 else None,
+                "classes_ms_per_step": {str(c): v[1] / args.steps for c, v in prof.items()},
+                "pct_of_8TBs": achieved / 8000.0}
+
+    line = {
+        "metric": METRIC, "value": its / (ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if ws > 1 else "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": args.workload, "dims": dims, "ranks": ranks, "iters_per_step": iters,
+                   "mu_iters_per_step": its, "noise": f"{w.noise} amp {w.noise_amp}",
+                   "l2": "input (4.29 GB) larger than L2; no flush", "parallelism": f"last-mode x{ws}",
+                   "ntt_wall_ms": ms, "rel_error": err},
+        "roofline": roofline,
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "e2e": e2e,
+    }
+    if rk == 0 and ws == 1 and not args.no_cpu:
+        t, threads, desc = oracle_sample_time(dims, ranks, iters)
+        line["cpu_baseline"] = {"value": its / t, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc}
+    if rk == 0:
+        print(json.dumps(line))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

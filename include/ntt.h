@@ -122,12 +122,15 @@ ntt_status ntt_nmf_mu(ntt_handle h, const float* X, int64_t m, int64_t n, int64_
  *           (else NTT_ERR_DIMENSION).
  *   cores : packed output, sum_l r_{l-1} n_l r_l floats; core l (row-major
  *           r_{l-1} x n_l x r_l) starts at o_l = sum_{j<l} r_{j-1} n_j r_j.
+ *   rel_err : nullable HOST double; if given, receives Eq. 3 of the
+ *           resulting train against A, ||A - A~||_F / ||A||_F (as ntt_reconstruct
+ *           computes it, fp64 sums), reusing the device copy of A.
  *   workspace : device scratch of >= ntt_decompose_workspace_bytes(...) bytes,
  *           or NULL to let the handle allocate (and keep) its own.          */
 size_t ntt_decompose_workspace_bytes(int32_t d, const int64_t* dims, const int32_t* ranks);
 ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t* dims,
                          const int32_t* ranks, int32_t iters, uint64_t seed, float eps,
-                         float* cores, void* workspace, size_t workspace_bytes);
+                         float* cores, double* rel_err, void* workspace, size_t workspace_bytes);
 
 /* --------------------------------------------------- reconstruction / error
  * Contract a TT (Eq. 1):  A~ = G_1 o G_2 o ... o G_d, and/or the
@@ -149,6 +152,20 @@ ntt_status ntt_generate(ntt_handle h, int32_t d, const int64_t* dims, const int3
 /* Eq. 4: C = prod n_i / sum n_i r_{i-1} r_i.  Host-only; returns a
  * negative value for invalid input.                                          */
 double ntt_compression_ratio(int32_t d, const int64_t* dims, const int32_t* ranks);
+
+/* ------------------------------------------------------------ profiling ----
+ * Per-kernel-class timing for the roofline report.  When enabled, the library
+ * brackets every launch of its kernels with CUDA events on the handle's stream
+ * and records the launch's ALGORITHMIC bytes (DESIGN.md s.8).  ntt_profile_get
+ * synchronises the stream and returns, for kernel class `cls`, the number of
+ * launches, their summed device time in ms and summed algorithmic bytes.
+ * Classes: 0 = MU X-stream pass (fused H pass / 1-pass), 1 = X H^T pass,
+ * 2 = W update, 3 = TT contraction stream (error / generate), 4 = other.
+ * Enabling resets the counters.                                              */
+#define NTT_PROF_CLASSES 5
+ntt_status ntt_profile_enable(ntt_handle h, int enable);
+ntt_status ntt_profile_get(ntt_handle h, int cls, int64_t* launches, double* total_ms,
+                           double* total_bytes);
 
 /* ----------------------------------------------------- multi-GPU (NCCL) ----
  * One process per GPU.  Rank 0 calls ntt_get_unique_id and broadcasts the 128

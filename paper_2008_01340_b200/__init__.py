@@ -153,9 +153,21 @@ class Handle:
         return list(tr)[:iters] if trace else None
 
     def ntt_decompose(self, A, dims, ranks, iters: int, seed: int, eps: float, cores, workspace=None,
-                      workspace_bytes: int = 0):
+                      workspace_bytes: int = 0, want_error: bool = False) -> Optional[float]:
+        err = ctypes.c_double(-1.0) if want_error else None
         self._check(lib().ntt_decompose(self._h, _ptr(A), len(dims), _i64arr(dims), _i32arr(ranks), iters, seed, eps,
-                                        _ptr(cores), _ptr(workspace), workspace_bytes))
+                                        _ptr(cores), ctypes.byref(err) if err is not None else None,
+                                        _ptr(workspace), workspace_bytes))
+        return float(err.value) if want_error else None
+
+    def ntt_profile_enable(self, enable: bool = True):
+        self._check(lib().ntt_profile_enable(self._h, 1 if enable else 0))
+
+    def ntt_profile_get(self, cls: int):
+        """(launches, total_ms, total_algorithmic_bytes) for kernel class `cls`."""
+        n, ms, by = ctypes.c_int64(0), ctypes.c_double(0), ctypes.c_double(0)
+        self._check(lib().ntt_profile_get(self._h, cls, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(by)))
+        return int(n.value), float(ms.value), float(by.value)
 
     def ntt_reconstruct(self, dims, ranks, cores, out=None, ref=None, want_error: bool = False) -> Optional[float]:
         err = ctypes.c_double(-1.0) if want_error else None

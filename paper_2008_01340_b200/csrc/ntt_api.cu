@@ -81,6 +81,16 @@ struct ntt_handle_s {
   int nranks = 1, rank = 0;
   ncclComm_t comm = nullptr;
   FusedCtx fused;
+  // profiling (ntt_profile_enable)
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  struct Rec {
+    int cls;
+    int ev0;
+    double bytes;
+  };
+  std::vector<Rec> recs;
 };
 
 namespace {
@@ -104,10 +114,15 @@ ntt_status fail(ntt_handle h, ntt_status s, const char* fmt, ...) {
       return fail((h), NTT_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
   } while (0)
 
-#define LAUNCH(h, call)      \
-  do {                       \
-    CU(h, (call));           \
-    (h)->launches++;         \
+#define LAUNCH(h, call) PLAUNCH(h, 4, 0.0, call)
+
+// Launch with optional event bracketing for the roofline profile (class, algorithmic bytes).
+#define PLAUNCH(h, cls, bytes, call)          \
+  do {                                        \
+    int ev0_ = prof_begin(h);                 \
+    CU(h, (call));                            \
+    (h)->launches++;                          \
+    prof_end(h, ev0_, (cls), (bytes));        \
   } while (0)
 
 #define NC(h, call)                                                                             \
@@ -157,6 +172,27 @@ ntt_status ensure_host_part(ntt_handle h, size_t count) {
   CU(h, cudaMallocHost(&h->host_part, count * sizeof(double)));
   h->host_part_count = count;
   return NTT_OK;
+}
+
+int prof_begin(ntt_handle h) {
+  if (!h->prof) return -1;
+  if (h->ev_used + 2 > h->ev_pool.size()) {
+    for (int i = 0; i < 256; ++i) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return -1;
+      h->ev_pool.push_back(e);
+    }
+  }
+  int i = (int)h->ev_used;
+  h->ev_used += 2;
+  cudaEventRecord(h->ev_pool[i], h->stream);
+  return i;
+}
+
+void prof_end(ntt_handle h, int ev0, int cls, double bytes) {
+  if (ev0 < 0) return;
+  cudaEventRecord(h->ev_pool[ev0 + 1], h->stream);
+  h->recs.push_back({cls, ev0, bytes});
 }
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
@@ -238,20 +274,22 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
   int nP = 0, nQ = 0;
   for (int it = 0; it < iters; ++it) {
     if (!p.acc || it == 0) {
-      LAUNCH(h, launch_xht_partial(X, ldx, m, n, H, n, r, p.xp, Ppart, st));
-      LAUNCH(h, launch_xht_partial(H, n, r, n, H, n, r, p.qp, Qpart, st));
+      PLAUNCH(h, 1, 4.0 * (double)(m + r) * (double)n, launch_xht_partial(X, ldx, m, n, H, n, r, p.xp, Ppart, st));
+      PLAUNCH(h, 4, 4.0 * (double)r * (double)n, launch_xht_partial(H, n, r, n, H, n, r, p.qp, Qpart, st));
       nP = p.xp.ncs;
       nQ = p.qp.ncs;
     }
     if (dist) {
       ntt_status s = dist_reduce(h, p, Ppart, nP, Qpart, nQ, red);
       if (s) return s;
-      LAUNCH(h, launch_wupdate(W, m, r, red, 1, red + m * r, 1, eps, Gpart, st));
+      PLAUNCH(h, 2, 8.0 * (double)(m * r + r * r) + 8.0 * (double)(m * r), launch_wupdate(W, m, r, red, 1, red + m * r, 1, eps, Gpart, st));
     } else {
-      LAUNCH(h, launch_wupdate(W, m, r, Ppart, nP, Qpart, nQ, eps, Gpart, st));
+      PLAUNCH(h, 2, 8.0 * ((double)nP * m * r + (double)nQ * r * r) + 8.0 * (double)(m * r),
+              launch_wupdate(W, m, r, Ppart, nP, Qpart, nQ, eps, Gpart, st));
     }
     const bool acc_now = p.acc && (it + 1 < iters);
-    LAUNCH(h, launch_hpass(X, ldx, m, n, W, r, Gpart, p.nwup, eps, H, p.hgrid, acc_now ? Ppart : nullptr,
+    PLAUNCH(h, 0, 4.0 * (double)(m + 2 * r) * (double)n,
+            launch_hpass(X, ldx, m, n, W, r, Gpart, p.nwup, eps, H, p.hgrid, acc_now ? Ppart : nullptr,
                            acc_now ? Qpart : nullptr, st));
     if (acc_now) {
       nP = p.hgrid;
@@ -314,6 +352,152 @@ ntt_status check_tt(ntt_handle h, int32_t d, const int64_t* dims, const int32_t*
   return NTT_OK;
 }
 
+}  // namespace
+
+// -------------------------------------------------------- reconstruct / error
+namespace {
+struct ContractPlan {
+  int k;                 // split bond
+  int64_t NL, NR, lmax, rmax;
+  int grid;
+  size_t off_L, off_R, off_part, off_cores, bytes;
+};
+
+ContractPlan plan_contract(const TTShape& s, int num_sms) {
+  ContractPlan c;
+  const int d = s.d;
+  // split bond k minimising |L| + |R| = (N_L + N_R) r_k
+  int best = 1;
+  double bestc = 1e300;
+  for (int k = 1; k < d; ++k) {
+    double NL = 1, NR = 1;
+    for (int l = 0; l < k; ++l) NL *= (double)s.dims[l];
+    for (int l = k; l < d; ++l) NR *= (double)s.dims[l];
+    double cst = (NL + NR) * (double)s.r[k];
+    if (cst < bestc) {
+      bestc = cst;
+      best = k;
+    }
+  }
+  c.k = best;
+  c.NL = 1;
+  c.NR = 1;
+  for (int l = 0; l < c.k; ++l) c.NL *= s.dims[l];
+  for (int l = c.k; l < d; ++l) c.NR *= s.dims[l];
+  c.lmax = 1;
+  c.rmax = 1;
+  int64_t acc = 1;
+  for (int l = 1; l <= c.k; ++l) {
+    acc *= s.dims[l - 1];
+    c.lmax = std::max(c.lmax, acc * s.r[l]);
+  }
+  acc = 1;
+  for (int l = d; l > c.k; --l) {
+    acc *= s.dims[l - 1];
+    c.rmax = std::max(c.rmax, s.r[l - 1] * acc);
+  }
+  c.grid = stream_ctas(c.NL, c.NR, num_sms);
+  size_t o = 0;
+  c.off_L = o;
+  o = align_up(o + sizeof(float) * (size_t)(2 * c.lmax));
+  c.off_R = o;
+  o = align_up(o + sizeof(float) * (size_t)(2 * c.rmax));
+  c.off_part = o;
+  o = align_up(o + sizeof(double) * 2 * (size_t)(c.grid + 1));
+  c.off_cores = o;
+  o = align_up(o + sizeof(float) * (size_t)s.cores);
+  c.bytes = o;
+  return c;
+}
+
+// Contract the train (device cores `dc`) and stream it against ref / into out.
+// Leaves the per-CTA (num, den) error partials at scratch + off_part when ref.
+ntt_status contract_run(ntt_handle h, const TTShape& s, const ContractPlan& c, const float* dc, float* dout,
+                        float noise_amp, uint64_t noise_key, const float* dref, char* scratch) {
+  cudaStream_t cs = h->stream;
+  const int d = s.d, k = c.k;
+  float* Lb[2] = {reinterpret_cast<float*>(scratch + c.off_L), reinterpret_cast<float*>(scratch + c.off_L) + c.lmax};
+  float* Rb[2] = {reinterpret_cast<float*>(scratch + c.off_R), reinterpret_cast<float*>(scratch + c.off_R) + c.rmax};
+  double* part = reinterpret_cast<double*>(scratch + c.off_part);
+  // left chain: L_1 = G_1 (n_1 x r_1); L_l = L_{l-1} G_l
+  const float* L = dc + s.off[1];
+  int64_t Ncur = s.dims[0];
+  for (int l = 2; l <= k; ++l) {
+    float* o = Lb[l & 1];
+    PLAUNCH(h, 4, 0.0, launch_contract_left(L, Ncur, (int)s.r[l - 1], dc + s.off[l], s.dims[l - 1], (int)s.r[l], o, cs));
+    L = o;
+    Ncur *= s.dims[l - 1];
+  }
+  // right chain: R_d = G_d (r_{d-1} x n_d); R_l = G_l R_{l+1}
+  const float* R = dc + s.off[d];
+  int64_t NRcur = s.dims[d - 1];
+  for (int l = d - 1; l > k; --l) {
+    float* o = Rb[l & 1];
+    PLAUNCH(h, 4, 0.0, launch_contract_right(dc + s.off[l], (int)s.r[l - 1], s.dims[l - 1], (int)s.r[l], R, NRcur, o, cs));
+    R = o;
+    NRcur *= s.dims[l - 1];
+  }
+  // algorithmic bytes: ref read + out write (+ L, R once)
+  double bytes = 4.0 * (double)s.N * ((dref ? 1 : 0) + (dout ? 1 : 0)) + 4.0 * (double)(c.NL + c.NR) * (double)s.r[k];
+  PLAUNCH(h, 3, bytes, launch_tt_stream(L, R, c.NL, c.NR, (int)s.r[k], dout, noise_amp, noise_key, dref,
+                                         dref ? part : nullptr, c.grid, cs));
+  return NTT_OK;
+}
+
+// Sum the error partials (fixed order), optionally all-reduce over ranks, return Eq. 3.
+ntt_status finish_error(ntt_handle h, const ContractPlan& c, char* scratch, bool allreduce, double* rel_err) {
+  cudaStream_t cs = h->stream;
+  double* part = reinterpret_cast<double*>(scratch + c.off_part);
+  double* tot = part + 2 * c.grid;
+  PLAUNCH(h, 4, 0.0, launch_sum_partials(part, c.grid, 2, tot, cs));
+  if (allreduce) NC(h, g_nccl.AllReduce(tot, tot, 2, ncclFloat64, ncclSum, h->comm, cs));
+  ntt_status st = ensure_host_part(h, 2);
+  if (st) return st;
+  CU(h, cudaMemcpyAsync(h->host_part, tot, 2 * sizeof(double), cudaMemcpyDeviceToHost, cs));
+  CU(h, cudaStreamSynchronize(cs));
+  if (h->host_part[1] == 0.0) return fail(h, NTT_ERR_DEGENERATE, "||ref||_F = 0");
+  *rel_err = sqrt(h->host_part[0]) / sqrt(h->host_part[1]);
+  return NTT_OK;
+}
+
+ntt_status contract_stream(ntt_handle h, const TTShape& s, const float* cores, float* out, float noise_amp,
+                           uint64_t noise_key, const float* ref, double* rel_err) {
+  cudaStream_t cs = h->stream;
+  ContractPlan c = plan_contract(s, h->num_sms);
+  const bool cores_dev = is_device_ptr(cores);
+  const bool out_dev = !out || is_device_ptr(out);
+  const bool ref_dev = !ref || is_device_ptr(ref);
+  ntt_status st = ensure_ws(h, c.bytes);
+  if (st) return st;
+  char* ws = reinterpret_cast<char*>(h->ws);
+  const float* dc = cores;
+  if (!cores_dev) {
+    float* t = reinterpret_cast<float*>(ws + c.off_cores);
+    CU(h, cudaMemcpyAsync(t, cores, sizeof(float) * (size_t)s.cores, cudaMemcpyHostToDevice, cs));
+    dc = t;
+  }
+  size_t sbytes = (out_dev ? 0 : align_up(sizeof(float) * (size_t)s.N)) + (ref_dev ? 0 : align_up(sizeof(float) * (size_t)s.N));
+  if (sbytes && (st = ensure_stage(h, sbytes))) return st;
+  float* dout = out;
+  const float* dref = ref;
+  char* sg = reinterpret_cast<char*>(h->stage);
+  if (!out_dev) {
+    dout = reinterpret_cast<float*>(sg);
+    sg += align_up(sizeof(float) * (size_t)s.N);
+  }
+  if (!ref_dev) {
+    float* t = reinterpret_cast<float*>(sg);
+    CU(h, cudaMemcpyAsync(t, ref, sizeof(float) * (size_t)s.N, cudaMemcpyHostToDevice, cs));
+    dref = t;
+  }
+  if ((st = contract_run(h, s, c, dc, dout, noise_amp, noise_key, dref, ws))) return st;
+  if (!out_dev) CU(h, cudaMemcpyAsync(out, dout, sizeof(float) * (size_t)s.N, cudaMemcpyDeviceToHost, cs));
+  if (rel_err) {
+    if ((st = finish_error(h, c, ws, false, rel_err))) return st;
+  }
+  if (!out_dev) CU(h, cudaStreamSynchronize(cs));
+  return NTT_OK;
+}
 }  // namespace
 
 // ============================================================================ ABI
@@ -379,6 +563,7 @@ ntt_status ntt_destroy(ntt_handle h) {
   if (h->stage) cudaFree(h->stage);
   if (h->host_part) cudaFreeHost(h->host_part);
   if (h->comm && g_nccl.loaded) g_nccl.CommDestroy(h->comm);
+  for (auto e : h->ev_pool) cudaEventDestroy(e);
   delete h;
   return NTT_OK;
 }
@@ -454,6 +639,7 @@ ntt_status ntt_nmf_mu(ntt_handle h, const float* X, int64_t m, int64_t n, int64_
   return NTT_OK;
 }
 
+
 // ------------------------------------------------------------------ decompose
 namespace {
 struct DecompPlan {
@@ -464,8 +650,10 @@ struct DecompPlan {
   int64_t hbuf[2];           // ping-pong H buffer sizes (floats)
   int64_t wmax;              // max m_l r_l
   size_t mu_bytes;
-  size_t off_h0, off_h1, off_w, off_mu, off_cores, bytes;
+  size_t off_h0, off_h1, off_w, off_mu, off_cores, off_err, bytes;
   MuPlan mu[65];
+  TTShape sl;        // local shape (last mode = local block) for the error pass
+  ContractPlan cp;
 };
 
 void plan_decompose(const TTShape& s, int num_sms, int nranks, int rank, DecompPlan* P) {
@@ -499,6 +687,13 @@ void plan_decompose(const TTShape& s, int num_sms, int nranks, int rank, DecompP
   o = align_up(o + sizeof(float) * (size_t)s.cores);
   P->off_mu = o;
   o = align_up(o + P->mu_bytes);
+  P->sl = s;
+  P->sl.dims[s.d - 1] = P->nloc_last;
+  P->sl.N = s.N / s.dims[s.d - 1] * P->nloc_last;
+  P->sl.cores = s.cores - s.r[s.d - 1] * (s.dims[s.d - 1] - P->nloc_last);
+  P->cp = plan_contract(P->sl, num_sms);
+  P->off_err = o;
+  o = align_up(o + P->cp.bytes);
   P->bytes = o;
 }
 }  // namespace
@@ -518,8 +713,8 @@ size_t ntt_decompose_workspace_bytes(int32_t d, const int64_t* dims, const int32
 }
 
 ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t* dims, const int32_t* ranks,
-                         int32_t iters, uint64_t seed, float eps, float* cores, void* workspace,
-                         size_t workspace_bytes) {
+                         int32_t iters, uint64_t seed, float eps, float* cores, double* rel_err,
+                         void* workspace, size_t workspace_bytes) {
   if (!h) return NTT_ERR_INVALID_ARG;
   if (!A || !cores) return fail(h, NTT_ERR_INVALID_ARG, "null A or cores");
   if (iters < 0) return fail(h, NTT_ERR_INVALID_ARG, "iters < 0");
@@ -597,119 +792,22 @@ ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t*
     NC(h, g_nccl.GroupEnd());
     LAUNCH(h, launch_gather_last_core(gath, rl, nd, h->nranks, dcores + s.off[d], cs));
   }
+  if (rel_err) {
+    // Eq. 3 of the result against (this rank's block of) A; the local train is
+    // cores 1..d-1 plus this rank's column block of the last core (= H_{d-1}).
+    char* es = ws + P.off_err;
+    float* lc = reinterpret_cast<float*>(es + P.cp.off_cores);
+    CU(h, cudaMemcpyAsync(lc, dcores, sizeof(float) * (size_t)s.off[d], cudaMemcpyDeviceToDevice, cs));
+    CU(h, cudaMemcpyAsync(lc + s.off[d], Hl, sizeof(float) * (size_t)(rl * P.nloc_last), cudaMemcpyDeviceToDevice, cs));
+    if ((st = contract_run(h, P.sl, P.cp, lc, nullptr, 0.0f, 0, dA, es))) return st;
+    if ((st = finish_error(h, P.cp, es, h->nranks > 1, rel_err))) return st;
+  }
   if (!cores_dev) {
     CU(h, cudaMemcpyAsync(cores, dcores, sizeof(float) * (size_t)s.cores, cudaMemcpyDeviceToHost, cs));
     CU(h, cudaStreamSynchronize(cs));
   }
   return NTT_OK;
 }
-
-// -------------------------------------------------------- reconstruct / error
-namespace {
-ntt_status contract_stream(ntt_handle h, const TTShape& s, const float* cores, float* out, float noise_amp,
-                           uint64_t noise_key, const float* ref, double* rel_err) {
-  cudaStream_t cs = h->stream;
-  const int d = s.d;
-  // split bond k minimising |L| + |R| = N_L r_k + r_k N_R
-  int best = 1;
-  double bestc = 1e300;
-  for (int k = 1; k < d; ++k) {
-    double NL = 1, NR = 1;
-    for (int l = 0; l < k; ++l) NL *= (double)s.dims[l];
-    for (int l = k; l < d; ++l) NR *= (double)s.dims[l];
-    double c = (NL + NR) * (double)s.r[k];
-    if (c < bestc) {
-      bestc = c;
-      best = k;
-    }
-  }
-  const int k = best;
-  int64_t NL = 1, NR = 1;
-  for (int l = 0; l < k; ++l) NL *= s.dims[l];
-  for (int l = k; l < d; ++l) NR *= s.dims[l];
-  // scratch sizes: left chain max N_l r_l (l <= k), right chain max r_{l-1} prod_{i>=l} n_i
-  int64_t lmax = 1, rmax = 1, acc = 1;
-  for (int l = 1; l <= k; ++l) {
-    acc *= s.dims[l - 1];
-    lmax = std::max(lmax, acc * s.r[l]);
-  }
-  acc = 1;
-  for (int l = d; l > k; --l) {
-    acc *= s.dims[l - 1];
-    rmax = std::max(rmax, s.r[l - 1] * acc);
-  }
-  const bool cores_dev = is_device_ptr(cores);
-  const bool out_dev = !out || is_device_ptr(out);
-  const bool ref_dev = !ref || is_device_ptr(ref);
-  int grid = stream_ctas(NL, NR, h->num_sms);
-  size_t need = align_up(sizeof(float) * (size_t)(2 * lmax)) + align_up(sizeof(float) * (size_t)(2 * rmax)) +
-                align_up(sizeof(double) * 2 * (size_t)grid) + align_up(sizeof(float) * (size_t)s.cores);
-  ntt_status st = ensure_ws(h, need);
-  if (st) return st;
-  char* ws = reinterpret_cast<char*>(h->ws);
-  float* Lb[2] = {reinterpret_cast<float*>(ws), reinterpret_cast<float*>(ws) + lmax};
-  ws += align_up(sizeof(float) * (size_t)(2 * lmax));
-  float* Rb[2] = {reinterpret_cast<float*>(ws), reinterpret_cast<float*>(ws) + rmax};
-  ws += align_up(sizeof(float) * (size_t)(2 * rmax));
-  double* part = reinterpret_cast<double*>(ws);
-  ws += align_up(sizeof(double) * 2 * (size_t)grid);
-  const float* dc = cores;
-  if (!cores_dev) {
-    float* t = reinterpret_cast<float*>(ws);
-    CU(h, cudaMemcpyAsync(t, cores, sizeof(float) * (size_t)s.cores, cudaMemcpyHostToDevice, cs));
-    dc = t;
-  }
-  // host staging for out / ref
-  size_t sbytes = (out_dev ? 0 : align_up(sizeof(float) * (size_t)s.N)) + (ref_dev ? 0 : align_up(sizeof(float) * (size_t)s.N));
-  if (sbytes && (st = ensure_stage(h, sbytes))) return st;
-  float* dout = out;
-  const float* dref = ref;
-  char* sg = reinterpret_cast<char*>(h->stage);
-  if (!out_dev) {
-    dout = reinterpret_cast<float*>(sg);
-    sg += align_up(sizeof(float) * (size_t)s.N);
-  }
-  if (!ref_dev) {
-    float* t = reinterpret_cast<float*>(sg);
-    CU(h, cudaMemcpyAsync(t, ref, sizeof(float) * (size_t)s.N, cudaMemcpyHostToDevice, cs));
-    dref = t;
-  }
-  // left chain: L_1 = G_1 (n_1 x r_1)
-  const float* L = dc + s.off[1];
-  int64_t Ncur = s.dims[0];
-  for (int l = 2; l <= k; ++l) {
-    float* o = Lb[l & 1];
-    LAUNCH(h, launch_contract_left(L, Ncur, (int)s.r[l - 1], dc + s.off[l], s.dims[l - 1], (int)s.r[l], o, cs));
-    L = o;
-    Ncur *= s.dims[l - 1];
-  }
-  // right chain: R_d = G_d (r_{d-1} x n_d)
-  const float* R = dc + s.off[d];
-  int64_t NRcur = s.dims[d - 1];
-  for (int l = d - 1; l > k; --l) {
-    float* o = Rb[l & 1];
-    LAUNCH(h, launch_contract_right(dc + s.off[l], (int)s.r[l - 1], s.dims[l - 1], (int)s.r[l], R, NRcur, o, cs));
-    R = o;
-    NRcur *= s.dims[l - 1];
-  }
-  LAUNCH(h, launch_tt_stream(L, R, NL, NR, (int)s.r[k], dout, noise_amp, noise_key, dref, dref ? part : nullptr, grid, cs));
-  if (!out_dev) CU(h, cudaMemcpyAsync(out, dout, sizeof(float) * (size_t)s.N, cudaMemcpyDeviceToHost, cs));
-  if (rel_err) {
-    if ((st = ensure_host_part(h, 2 * (size_t)grid))) return st;
-    CU(h, cudaMemcpyAsync(h->host_part, part, sizeof(double) * 2 * (size_t)grid, cudaMemcpyDeviceToHost, cs));
-    CU(h, cudaStreamSynchronize(cs));
-    double num = 0.0, den = 0.0;
-    for (int b = 0; b < grid; ++b) {
-      num += h->host_part[2 * b];
-      den += h->host_part[2 * b + 1];
-    }
-    if (den == 0.0) return fail(h, NTT_ERR_DEGENERATE, "||ref||_F = 0");
-    *rel_err = sqrt(num) / sqrt(den);
-  }
-  if (!out_dev) CU(h, cudaStreamSynchronize(cs));
-  return NTT_OK;
-}
-}  // namespace
 
 ntt_status ntt_reconstruct(ntt_handle h, int32_t d, const int64_t* dims, const int32_t* ranks, const float* cores,
                            float* out, const float* ref, double* rel_err) {
@@ -745,6 +843,35 @@ double ntt_compression_ratio(int32_t d, const int64_t* dims, const int32_t* rank
     den += (double)dims[i - 1] * rp * rn;
   }
   return num / den;
+}
+
+// ------------------------------------------------------------------- profiling
+ntt_status ntt_profile_enable(ntt_handle h, int enable) {
+  if (!h) return NTT_ERR_INVALID_ARG;
+  CU(h, cudaStreamSynchronize(h->stream));
+  h->prof = enable != 0;
+  h->ev_used = 0;
+  h->recs.clear();
+  return NTT_OK;
+}
+
+ntt_status ntt_profile_get(ntt_handle h, int cls, int64_t* launches, double* total_ms, double* total_bytes) {
+  if (!h || cls < 0 || cls >= NTT_PROF_CLASSES) return NTT_ERR_INVALID_ARG;
+  CU(h, cudaStreamSynchronize(h->stream));
+  int64_t n = 0;
+  double ms = 0.0, by = 0.0;
+  for (const auto& r : h->recs) {
+    if (r.cls != cls) continue;
+    float t = 0.0f;
+    CU(h, cudaEventElapsedTime(&t, h->ev_pool[r.ev0], h->ev_pool[r.ev0 + 1]));
+    ++n;
+    ms += t;
+    by += r.bytes;
+  }
+  if (launches) *launches = n;
+  if (total_ms) *total_ms = ms;
+  if (total_bytes) *total_bytes = by;
+  return NTT_OK;
 }
 
 // ------------------------------------------------------------------ distributed

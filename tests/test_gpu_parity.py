@@ -198,7 +198,7 @@ def test_decompose_parity(h, ora, dims, ranks, iters, noise):
     A = _tt_case(dims, ranks, 0, noise)
     ncore = ora.cores_size(dims, ranks)
     cores = torch.empty(ncore, dtype=torch.float32, device="cuda")
-    h.ntt_decompose(dev(A), dims, ranks, iters, 0, 1e-16, cores)
+    e_dec = h.ntt_decompose(dev(A), dims, ranks, iters, 0, 1e-16, cores, want_error=True)
     got = host(cores)
     ref = ora.ntt_decompose(A, ranks, iters, seed=0)
     _cores_check(dims, ranks, got, ref)
@@ -206,6 +206,7 @@ def test_decompose_parity(h, ora, dims, ranks, iters, noise):
     e_gpu = h.ntt_reconstruct(dims, ranks, cores, ref=dev(A), want_error=True)
     e_ora = ora.tt_rel_error(A, ranks, ref)
     assert abs(e_gpu - e_ora) <= 1e-3 * e_ora + 1e-6, (e_gpu, e_ora)
+    assert abs(e_dec - e_gpu) <= 1e-9 + 1e-6 * e_gpu
 
 
 def test_decompose_rank1_exact(h, ora):
