@@ -250,7 +250,7 @@ def run_ours(args):
     clocks = clk.stop()
     launches = h.launch_count - l0
     ms = e0.elapsed_time(e1) / args.steps
-    prof = {c: h.ntt_profile_get(c) for c in range(5)}
+    prof = {c: h.ntt_profile_get(c) for c in range(6)}
     h.ntt_profile_enable(False)
     if dist:
         t = torch.tensor([ms], device="cuda")

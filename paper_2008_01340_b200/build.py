@@ -34,7 +34,8 @@ def nccl_include() -> str:
 
 
 def flags():
-    return ["-O3", "-lineinfo", "-std=c++17", *ARCH, "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",
+    extra = ["-DNTT_WATCHDOG"] if os.environ.get("NTT_WATCHDOG") else []
+    return [*extra, "-O3", "-lineinfo", "-std=c++17", *ARCH, "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",
             f"-I{os.path.join(ROOT, 'include')}", f"-I{nccl_include()}", "--expt-relaxed-constexpr"]
 
 

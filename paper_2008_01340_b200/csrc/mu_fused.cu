@@ -1,9 +1,894 @@
-// mu_fused.cu -- 1-pass fused short-wide MU kernel (placeholder: generic path used).
+// mu_fused.cu -- the 1-pass fused MU kernel for short-wide unfoldings (m <= 40,
+// r <= 8) on sm_100a, plus the parallel-reduction W update it feeds.
+//
+// One pass over X does, per column j (include/ntt.h ntt_nmf_mu; R1-R4):
+//   phase A  S[:,j] = W^T X[:,j]                          (Alg. 6 l.2)
+//            H[:,j] <- H[:,j] o S[:,j] / (G H[:,j] + eps)  (G = W^T W, Alg. 4)
+//   phase B  P += X[:,j] Hn[:,j]^T,  Q += Hn[:,j] Hn[:,j]^T (Alg. 5 l.2 / Alg. 4
+//            for the NEXT iteration's W update)
+// so X is read from HBM once per MU iteration instead of twice (SURVEY s.0 #3).
+//
+// Structure: persistent CTAs (1 per SM), 1 TMA producer warp + 8 consumer warps.
+// The producer streams tiles of 128 columns -- X as four 32-column x MP-row
+// boxes and H as four 32 x 8 boxes, all SWIZZLE_128B -- through an mbarrier
+// ring of `ns` stages.  Each consumer warp owns whole tiles (no CTA-wide syncs
+// in the loop): lane q handles columns 4q..4q+3 in phase A (FFMA2 with scalar
+// broadcast of W), then the warp re-reads its tile for phase B with lanes as
+// (row block rb, 32-column slice cs) -- rows rb+8u hit distinct swizzle phases,
+// so the 128-bit loads are conflict-free -- against a transposed, padded Hn tile
+// read by broadcast.  fp32 FMA inside a tile, fp64 accumulation across tiles,
+// fixed-order CTA reduction into per-CTA fp64 partials (deterministic).
+#include <cuda.h>
+#include <cstdio>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
 #include "mu_fused.h"
 
 namespace ntt {
-bool fused_supported(int64_t, int64_t, int) { return false; }
-int fused_grid(int64_t, int64_t, int, int) { return 0; }
+
+namespace {
+
+constexpr int NW = 8;               // consumer warps
+constexpr int NT = (NW + 1) * 32;   // + 1 TMA producer warp
+constexpr int BN = 128;             // tile columns
+constexpr int HN_FLOATS = 1168;     // per-warp transposed Hn tile (padded)
+constexpr int SMEM_BUDGET = 232448; // 227 KB opt-in
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// try_wait in a C++ loop (not an asm-internal branch loop): the compiler must
+// see the divergent spin to place reconvergence before warp-synchronous code.
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) {
+  }
+}
+#ifdef NTT_WATCHDOG
+__device__ __forceinline__ void mbar_wait_dbg(uint64_t* bar, uint32_t parity, int tag, long long j) {
+  long long t0 = clock64();
+  while (true) {
+    if (mbar_try(bar, parity)) return;
+    if (clock64() - t0 > 4000000000LL) {
+      printf("WATCHDOG tag=%d block=%d thread=%d j=%lld parity=%u\n", tag, blockIdx.x, threadIdx.x, j, parity);
+      __trap();
+    }
+  }
+}
+#define MBAR_WAIT(bar, par, tag, j) mbar_wait_dbg(bar, par, tag, j)
+#else
+#define MBAR_WAIT(bar, par, tag, j) mbar_wait(bar, par)
+#endif
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ float4 lds128(const unsigned char* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+// MU quotient (w * num) / (den + eps) (reading R4) with the 2-ulp fast divide
+__device__ __forceinline__ float mu_q(float w, float num, float den, float eps) {
+  return __fdividef(__fmul_rn(w, num), __fadd_rn(den, eps));
+}
+__device__ __forceinline__ float2 bc(float a) { return make_float2(a, a); }
+
+// transposed per-warp Hn tile: column c (0..127), rank index k (0..7)
+__device__ __forceinline__ int hn_idx(int c, int k) { return c * 8 + k + 4 * (c >> 2) + 4 * (c >> 5); }
+
+template <int R, int UX>
+__global__ void __launch_bounds__(NT, 1)
+k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmH, int m, int64_t n, int r,
+        const float* __restrict__ W, const double* __restrict__ Gpart, int nG, float eps, float* __restrict__ H,
+        double* __restrict__ Ppart, double* __restrict__ Qpart, int mode, int ns, int evict_first) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  constexpr int MP = UX * 8;                 // padded rows (TMA box rows)
+  constexpr uint32_t XB = 4u * MP * 128u;    // X bytes per stage (4 boxes)
+  constexpr uint32_t HB = 4u * 8u * 128u;    // H bytes per stage (4 boxes of 8 rows)
+  constexpr uint32_t SB = XB + HB;
+  unsigned char* stages = smem;
+  float* Ws = reinterpret_cast<float*>(smem + (size_t)ns * SB);  // MP x 8
+  float* Gs = Ws + MP * 8;                                         // 8 x 8
+  float* HnAll = Gs + 64;                                          // NW x HN_FLOATS
+  uint64_t* full = reinterpret_cast<uint64_t*>(HnAll + NW * HN_FLOATS);
+  uint64_t* empty = full + ns;
+  // Tiles issued so far.  Successive rounds of one stage are consumed by
+  // DIFFERENT warps, so before parity-waiting on round k a warp must know round
+  // k-1 completed; the producer only issues round k after waiting for round
+  // k-1's release, hence "issued > j" makes the parity wait unambiguous.
+  uint32_t* issued = reinterpret_cast<uint32_t*>(empty + ns);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool do_update = (mode & kFusedUpdate) != 0;
+  const bool do_acc = (mode & kFusedAcc) != 0;
+
+  // ---- setup: W, G into smem; barriers
+  for (int e = tid; e < MP * 8; e += NT) {
+    int i = e >> 3, k = e & 7;
+    Ws[e] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
+  }
+  if (do_update) {
+    const int rr = r * r;
+    for (int e = tid; e < 64; e += NT) {
+      int k = e >> 3, l = e & 7;
+      double s = 0.0;
+      if (k < r && l < r)
+        for (int b = 0; b < nG; ++b) s += Gpart[(int64_t)b * rr + k * r + l];
+      Gs[e] = (float)s;
+    }
+  }
+  if (tid == 0) {
+    for (int s = 0; s < ns; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    *issued = 0u;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int64_t ntiles = (n + BN - 1) / BN;
+  const int64_t b = blockIdx.x;
+  const int64_t J = (ntiles > b) ? (ntiles - b + gridDim.x - 1) / gridDim.x : 0;
+
+  if (warp == NW) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      uint64_t policy;
+      if (evict_first)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+      else
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
+      for (int64_t j = 0; j < J; ++j) {
+        const int s = (int)(j % ns);
+        const uint32_t ph = (uint32_t)((j / ns) & 1);
+        MBAR_WAIT(&empty[s], ph ^ 1u, 1, j);
+        mbar_expect_tx(&full[s], SB);
+        const int col0 = (int)((b + j * gridDim.x) * BN);
+        unsigned char* st = stages + (size_t)s * SB;
+#pragma unroll
+        for (int bx = 0; bx < 4; ++bx) tma_load_2d(st + bx * MP * 128, &tmX, col0 + bx * 32, 0, &full[s], policy);
+#pragma unroll
+        for (int bx = 0; bx < 4; ++bx) tma_load_2d(st + XB + bx * 1024, &tmH, col0 + bx * 32, 0, &full[s], policy);
+        st_release_u32(issued, (uint32_t)(j + 1));
+      }
+    }
+    return;
+  }
+
+  // ================= consumer warps =================
+  float* Hw = HnAll + warp * HN_FLOATS;
+  const int q = lane, qbox = q >> 3, qch = q & 7;   // phase A: columns 4q..4q+3
+  const int rb = lane & 7, cs = lane >> 3;          // phase B: rows rb+8u, columns 32cs..32cs+31
+  // phase-B accumulators: V4 = (UX+1)*R values per lane (rows rb+8u, u<UX, and Q
+  // row rb), padded to a multiple of 4.  After every tile the 4 lanes sharing rb
+  // (cs = 0..3) reduce-scatter them with two shuffle levels, so each lane keeps
+  // V4/4 of the sums, flat indices [cs*V4/4, cs*V4/4 + V4/4), in fp64.
+  constexpr int V = (UX + 1) * R;
+  constexpr int V4 = (V + 3) / 4 * 4;
+  double accd[V4 / 4];
+#pragma unroll
+  for (int v = 0; v < V4 / 4; ++v) accd[v] = 0.0;
+  const bool h1 = (lane >> 4) & 1, h0 = (lane >> 3) & 1;
+
+  for (int64_t j = warp; j < J; j += NW) {
+    const int s = (int)(j % ns);
+    const uint32_t ph = (uint32_t)((j / ns) & 1);
+    if (lane == 0)
+    {
+#ifdef NTT_WATCHDOG
+      long long t0 = clock64();
+#endif
+      while (ld_acquire_u32(issued) <= (uint32_t)j) {
+        __nanosleep(64);
+#ifdef NTT_WATCHDOG
+        if (clock64() - t0 > 4000000000LL) {
+          printf("WATCHDOG issued block=%d warp=%d j=%lld issued=%u\n", blockIdx.x, warp, (long long)j, *issued);
+          __trap();
+        }
+#endif
+      }
+    }
+    __syncwarp();
+    MBAR_WAIT(&full[s], ph, 2, j);
+    const unsigned char* st = stages + (size_t)s * SB;
+    const int64_t jt = (b + j * gridDim.x) * BN;  // first column of the tile
+
+    // ---------------- phase A ----------------
+    {
+      const unsigned char* hb = st + XB + qbox * 1024;
+      float2 hv[R][2];
+#pragma unroll
+      for (int l = 0; l < R; ++l) {
+        float4 h4 = lds128(hb + l * 128 + ((qch ^ l) << 4));
+        hv[l][0] = f2(h4.x, h4.y);
+        hv[l][1] = f2(h4.z, h4.w);
+      }
+      const int64_t c0 = jt + 4 * q;
+      float2 hn[R][2];
+      if (do_update) {
+        const unsigned char* xb = st + qbox * MP * 128;
+        float2 s2[R][2];
+#pragma unroll
+        for (int k = 0; k < R; ++k) s2[k][0] = s2[k][1] = f2(0.f, 0.f);
+#pragma unroll 4
+        for (int i = 0; i < m; ++i) {
+          float4 x = lds128(xb + i * 128 + ((qch ^ (i & 7)) << 4));
+          const float2 xa = f2(x.x, x.y), xc = f2(x.z, x.w);
+          const float4* wr = reinterpret_cast<const float4*>(Ws + i * 8);
+          float w[8];
+          *reinterpret_cast<float4*>(w) = wr[0];
+          if (R > 4) *reinterpret_cast<float4*>(w + 4) = wr[1];
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            s2[k][0] = __ffma2_rn(bc(w[k]), xa, s2[k][0]);
+            s2[k][1] = __ffma2_rn(bc(w[k]), xc, s2[k][1]);
+          }
+        }
+        // E = G H ; Hn = H S / (E + eps)
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          float2 e0 = f2(0.f, 0.f), e1 = f2(0.f, 0.f);
+#pragma unroll
+          float gk[8];
+          *reinterpret_cast<float4*>(gk) = *reinterpret_cast<const float4*>(Gs + k * 8);
+          if (R > 4) *reinterpret_cast<float4*>(gk + 4) = *reinterpret_cast<const float4*>(Gs + k * 8 + 4);
+#pragma unroll
+          for (int l = 0; l < R; ++l) {
+            const float g = gk[l];
+            e0 = __ffma2_rn(bc(g), hv[l][0], e0);
+            e1 = __ffma2_rn(bc(g), hv[l][1], e1);
+          }
+          hn[k][0].x = mu_q(hv[k][0].x, s2[k][0].x, e0.x, eps);
+          hn[k][0].y = mu_q(hv[k][0].y, s2[k][0].y, e0.y, eps);
+          hn[k][1].x = mu_q(hv[k][1].x, s2[k][1].x, e1.x, eps);
+          hn[k][1].y = mu_q(hv[k][1].y, s2[k][1].y, e1.y, eps);
+          if (k >= r) hn[k][0] = hn[k][1] = f2(0.f, 0.f);  // padded ranks (0/0 when eps = 0)
+        }
+        // columns beyond n: zero (never stored, never accumulated)
+        if (c0 + 3 >= n) {
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            if (c0 + 0 >= n) hn[k][0].x = 0.f;
+            if (c0 + 1 >= n) hn[k][0].y = 0.f;
+            if (c0 + 2 >= n) hn[k][1].x = 0.f;
+            if (c0 + 3 >= n) hn[k][1].y = 0.f;
+          }
+        }
+        // store H (in place; this tile's H was already staged by TMA)
+        if (c0 + 3 < n) {
+#pragma unroll
+          for (int k = 0; k < R; ++k)
+            if (k < r)
+              *reinterpret_cast<float4*>(H + (int64_t)k * n + c0) = make_float4(hn[k][0].x, hn[k][0].y, hn[k][1].x, hn[k][1].y);
+        } else {
+#pragma unroll
+          for (int k = 0; k < R; ++k)
+            if (k < r) {
+              if (c0 + 0 < n) H[(int64_t)k * n + c0 + 0] = hn[k][0].x;
+              if (c0 + 1 < n) H[(int64_t)k * n + c0 + 1] = hn[k][0].y;
+              if (c0 + 2 < n) H[(int64_t)k * n + c0 + 2] = hn[k][1].x;
+            }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          hn[k][0] = hv[k][0];
+          hn[k][1] = hv[k][1];
+        }
+      }
+      if (do_acc) {
+        // transposed Hn tile: Hw[hn_idx(c, k)]
+        float tv[4][8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          tv[0][k] = (k < R) ? hn[k % R][0].x : 0.f;
+          tv[1][k] = (k < R) ? hn[k % R][0].y : 0.f;
+          tv[2][k] = (k < R) ? hn[k % R][1].x : 0.f;
+          tv[3][k] = (k < R) ? hn[k % R][1].y : 0.f;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          float* dst = Hw + hn_idx(4 * q + t, 0);
+          *reinterpret_cast<float4*>(dst) = make_float4(tv[t][0], tv[t][1], tv[t][2], tv[t][3]);
+          if (R > 4) *reinterpret_cast<float4*>(dst + 4) = make_float4(tv[t][4], tv[t][5], tv[t][6], tv[t][7]);
+        }
+      }
+    }
+
+    // ---------------- phase B ----------------
+    if (do_acc) {
+      __syncwarp();
+      const unsigned char* xb = st + cs * MP * 128;
+      float2 acc[V4 / 2];
+#pragma unroll
+      for (int v = 0; v < V4 / 2; ++v) acc[v] = f2(0.f, 0.f);
+#pragma unroll 2
+      for (int s4 = 0; s4 < 8; ++s4) {
+        const int c = 32 * cs + 4 * s4;
+        float2 hq2[4][R / 2];
+        float hq[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float* src = Hw + hn_idx(c + t, 0);
+          float4 a = *reinterpret_cast<const float4*>(src);
+          hq2[t][0] = f2(a.x, a.y);
+          if (R > 2) hq2[t][1 % (R / 2)] = f2(a.z, a.w);
+          if (R > 4) {
+            float4 bq = *reinterpret_cast<const float4*>(src + 4);
+            hq2[t][2 % (R / 2)] = f2(bq.x, bq.y);
+            hq2[t][3 % (R / 2)] = f2(bq.z, bq.w);
+          }
+          hq[t] = src[rb];
+        }
+#pragma unroll
+        for (int u = 0; u < UX; ++u) {
+          const float4 x = lds128(xb + (rb + 8 * u) * 128 + ((s4 ^ rb) << 4));
+          const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int kp = 0; kp < R / 2; ++kp) acc[u * (R / 2) + kp] = __ffma2_rn(bc(xs[t]), hq2[t][kp], acc[u * (R / 2) + kp]);
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+          for (int kp = 0; kp < R / 2; ++kp) acc[UX * (R / 2) + kp] = __ffma2_rn(bc(hq[t]), hq2[t][kp], acc[UX * (R / 2) + kp]);
+      }
+      // reduce-scatter over the 4 lanes with the same rb (xor 16, then xor 8)
+      float a1[V4];
+#pragma unroll
+      for (int v = 0; v < V4 / 2; ++v) {
+        a1[2 * v] = acc[v].x;
+        a1[2 * v + 1] = acc[v].y;
+      }
+      float a2[V4 / 2];
+#pragma unroll
+      for (int v = 0; v < V4 / 2; ++v) {
+        const float send = h1 ? a1[v] : a1[v + V4 / 2];
+        const float keep = h1 ? a1[v + V4 / 2] : a1[v];
+        a2[v] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
+#pragma unroll
+      for (int v = 0; v < V4 / 4; ++v) {
+        const float send = h0 ? a2[v] : a2[v + V4 / 4];
+        const float keep = h0 ? a2[v + V4 / 4] : a2[v];
+        accd[v] += (double)(keep + __shfl_xor_sync(0xffffffffu, send, 8));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  if (!do_acc) return;
+  // ---- fixed-order CTA reduction of the per-thread fp64 partials
+  asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+  // red[w][rb][f], f = u*R + k flat (u = UX is the Q row)
+  double* red = reinterpret_cast<double*>(stages);
+#pragma unroll
+  for (int v = 0; v < V4 / 4; ++v) red[((size_t)warp * 8 + rb) * V4 + cs * (V4 / 4) + v] = accd[v];
+  asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+  const int mr = m * r, rr = r * r;
+  for (int e = tid; e < 8 * V; e += NW * 32) {
+    const int rbe = e / V, f = e % V;
+    const int u = f / R, k = f % R;
+    if (k >= r) continue;
+    const bool isQ = (u == UX);
+    const int row = isQ ? rbe : rbe + 8 * u;
+    if (isQ ? (row >= r) : (row >= m)) continue;
+    double sum = 0.0;
+    for (int w = 0; w < NW; ++w) sum += red[((size_t)w * 8 + rbe) * V4 + f];
+    if (isQ) Qpart[b * rr + row * r + k] = sum;
+    else Ppart[b * mr + row * r + k] = sum;
+  }
+}
+
+
+// ===========================================================================
+// Variant C: CTA-cooperative tiles for 40 < m <= 256 (rank padded to 8).
+// Tile = 32 columns x MP rows (one SWIZZLE_128B box) + the 8 x 32 H box.
+// Phase A splits the m-long dot products across the 8 consumer warps (warp w
+// owns rows [8U w, 8U w + 8U), its W slice in registers), reduces the 8 partial
+// S tiles through smem in fixed order, then 256 threads (k, c) form E = G H and
+// Hn.  Phase B: warp w owns the same rows of P = X Hn^T (lanes = row block x
+// 8-column slice) and row w of Q = Hn Hn^T; rows are disjoint across warps, so
+// per-CTA partials need no cross-warp reduction.
+// ===========================================================================
+constexpr int BNC = 32;
+constexpr int HNC_FLOATS = 32 * 8 + 16;  // transposed Hn tile [c][k] + 4 floats per 8-column group
+
+__device__ __forceinline__ int hnc_idx(int c, int k) { return c * 8 + k + 4 * (c >> 3); }
+
+template <int U>
+__global__ void __launch_bounds__(NT, 1)
+k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmH, int m, int64_t n, int r,
+          const float* __restrict__ W, const double* __restrict__ Gpart, int nG, float eps, float* __restrict__ H,
+          double* __restrict__ Ppart, double* __restrict__ Qpart, int mode, int ns, int evict_first) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  constexpr int MP = 64 * U;                 // padded rows (box rows)
+  constexpr int RW = 8 * U;                  // rows per warp
+  constexpr uint32_t XB = MP * 128u;
+  constexpr uint32_t SB = XB + 1024u;
+  unsigned char* stages = smem;
+  float* Sred = reinterpret_cast<float*>(smem + (size_t)ns * SB);  // [8 warps][8 k][32 c]
+  float* Gs = Sred + 8 * 8 * 32;                                     // 8 x 8
+  float* Hn = Gs + 64;                                               // HNC_FLOATS
+  uint64_t* full = reinterpret_cast<uint64_t*>(Hn + HNC_FLOATS);
+  uint64_t* empty = full + ns;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool do_update = (mode & kFusedUpdate) != 0;
+  const bool do_acc = (mode & kFusedAcc) != 0;
+  if (do_update) {
+    const int rr = r * r;
+    for (int e = tid; e < 64; e += NT) {
+      int k = e >> 3, l = e & 7;
+      double sum = 0.0;
+      if (k < r && l < r)
+        for (int bq = 0; bq < nG; ++bq) sum += Gpart[(int64_t)bq * rr + k * r + l];
+      Gs[e] = (float)sum;
+    }
+  }
+  if (tid == 0) {
+    for (int s = 0; s < ns; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int64_t ntiles = (n + BNC - 1) / BNC;
+  const int64_t b = blockIdx.x;
+  const int64_t J = (ntiles > b) ? (ntiles - b + gridDim.x - 1) / gridDim.x : 0;
+
+  if (warp == NW) {
+    if (lane == 0) {
+      uint64_t policy;
+      if (evict_first)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+      else
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
+      for (int64_t j = 0; j < J; ++j) {
+        const int s = (int)(j % ns);
+        const uint32_t ph = (uint32_t)((j / ns) & 1);
+        MBAR_WAIT(&empty[s], ph ^ 1u, 3, j);
+        mbar_expect_tx(&full[s], SB);
+        const int col0 = (int)((b + j * gridDim.x) * BNC);
+        unsigned char* st = stages + (size_t)s * SB;
+        tma_load_2d(st, &tmX, col0, 0, &full[s], policy);
+        tma_load_2d(st + XB, &tmH, col0, 0, &full[s], policy);
+      }
+    }
+    return;
+  }
+
+  // phase A lane roles: columns 4q..4q+3, ranks 2g, 2g+1 ; W slice in registers
+  const int q = lane & 7, g = lane >> 3;
+  float wr[RW][2];
+#pragma unroll
+  for (int v = 0; v < RW; ++v) {
+    const int i = warp * RW + v;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int k = 2 * g + t;
+      wr[v][t] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
+    }
+  }
+  // phase B lane roles: rows warp*RW + rb + 8u, columns 8cs..8cs+7 ; Q[warp][rb]
+  const int rb = lane & 7, cs = lane >> 3;
+  constexpr int V = U * 8;  // P values per lane per tile (u, k)
+  double accd[V / 4];
+#pragma unroll
+  for (int v = 0; v < V / 4; ++v) accd[v] = 0.0;
+  double qd = 0.0;
+  const bool h1 = (lane >> 4) & 1, h0 = (lane >> 3) & 1;
+  const int kt = tid >> 5, ct = tid & 31;  // (k, c) role in the H update
+
+  for (int64_t j = 0; j < J; ++j) {
+    const int s = (int)(j % ns);
+    const uint32_t ph = (uint32_t)((j / ns) & 1);
+    MBAR_WAIT(&full[s], ph, 4, j);
+    const unsigned char* st = stages + (size_t)s * SB;
+    const int64_t jt = (b + j * gridDim.x) * BNC;
+
+    if (do_update) {
+      // ---- phase A: partial S over this warp's rows
+      float2 sa = f2(0.f, 0.f), sb = f2(0.f, 0.f), sc = f2(0.f, 0.f), sd = f2(0.f, 0.f);
+#pragma unroll
+      for (int v = 0; v < RW; ++v) {
+        const int i = warp * RW + v;
+        const float4 x = lds128(st + i * 128 + ((q ^ (i & 7)) << 4));
+        const float2 x01 = f2(x.x, x.y), x23 = f2(x.z, x.w);
+        sa = __ffma2_rn(bc(wr[v][0]), x01, sa);
+        sb = __ffma2_rn(bc(wr[v][0]), x23, sb);
+        sc = __ffma2_rn(bc(wr[v][1]), x01, sc);
+        sd = __ffma2_rn(bc(wr[v][1]), x23, sd);
+      }
+      float* sr = Sred + (warp * 8 + 2 * g) * 32 + 4 * q;
+      *reinterpret_cast<float4*>(sr) = make_float4(sa.x, sa.y, sb.x, sb.y);
+      *reinterpret_cast<float4*>(sr + 32) = make_float4(sc.x, sc.y, sd.x, sd.y);
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+    {
+      // ---- H update for (k = kt, c = ct)
+      const int64_t col = jt + ct;
+      const float hkc = *reinterpret_cast<const float*>(st + XB + kt * 128 + ((((ct >> 2) ^ kt)) << 4) + (ct & 3) * 4);
+      float hn = 0.0f;
+      if (do_update) {
+        float S = 0.0f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) S += Sred[(w * 8 + kt) * 32 + ct];
+        float e = 0.0f;
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+          const float hl = *reinterpret_cast<const float*>(st + XB + l * 128 + ((((ct >> 2) ^ l)) << 4) + (ct & 3) * 4);
+          e = fmaf(Gs[kt * 8 + l], hl, e);
+        }
+        hn = mu_q(hkc, S, e, eps);
+        if (kt >= r || col >= n) hn = 0.0f;
+        if (kt < r && col < n) H[(int64_t)kt * n + col] = hn;
+      } else {
+        hn = (kt < r && col < n) ? hkc : 0.0f;
+      }
+      if (do_acc) Hn[hnc_idx(ct, kt)] = hn;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+
+    if (do_acc) {
+      // ---- phase B
+      float2 acc[V / 2];
+#pragma unroll
+      for (int v = 0; v < V / 2; ++v) acc[v] = f2(0.f, 0.f);
+      float qa = 0.0f;
+#pragma unroll
+      for (int s4 = 0; s4 < 2; ++s4) {
+        const int c = 8 * cs + 4 * s4;
+        float2 hq2[4][4];
+        float hrb[4], hw[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float* src = Hn + hnc_idx(c + t, 0);
+          const float4 a = *reinterpret_cast<const float4*>(src);
+          const float4 bq = *reinterpret_cast<const float4*>(src + 4);
+          hq2[t][0] = f2(a.x, a.y);
+          hq2[t][1] = f2(a.z, a.w);
+          hq2[t][2] = f2(bq.x, bq.y);
+          hq2[t][3] = f2(bq.z, bq.w);
+          hrb[t] = src[rb];
+          hw[t] = src[warp];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = warp * RW + rb + 8 * u;
+          const float4 x = lds128(st + i * 128 + (((2 * cs + s4) ^ rb) << 4));
+          const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int kp = 0; kp < 4; ++kp) acc[u * 4 + kp] = __ffma2_rn(bc(xs[t]), hq2[t][kp], acc[u * 4 + kp]);
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) qa = fmaf(hw[t], hrb[t], qa);
+      }
+      // reduce-scatter P over the 4 column-slice lanes (xor 16, xor 8)
+      float a1[V];
+#pragma unroll
+      for (int v = 0; v < V / 2; ++v) {
+        a1[2 * v] = acc[v].x;
+        a1[2 * v + 1] = acc[v].y;
+      }
+      float a2[V / 2];
+#pragma unroll
+      for (int v = 0; v < V / 2; ++v) {
+        const float send = h1 ? a1[v] : a1[v + V / 2];
+        const float keep = h1 ? a1[v + V / 2] : a1[v];
+        a2[v] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
+#pragma unroll
+      for (int v = 0; v < V / 4; ++v) {
+        const float send = h0 ? a2[v] : a2[v + V / 4];
+        const float keep = h0 ? a2[v + V / 4] : a2[v];
+        accd[v] += (double)(keep + __shfl_xor_sync(0xffffffffu, send, 8));
+      }
+      qd += (double)qa;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  if (!do_acc) return;
+  // P: lane holds flat f = u*8 + k in [cs*V/4, cs*V/4 + V/4) for rows warp*RW + rb + 8u
+  const int mr = m * r, rr = r * r;
+#pragma unroll
+  for (int v = 0; v < V / 4; ++v) {
+    const int f = cs * (V / 4) + v;
+    const int u = f >> 3, k = f & 7;
+    const int row = warp * RW + rb + 8 * u;
+    if (row < m && k < r) Ppart[b * mr + row * r + k] = accd[v];
+  }
+  // Q[warp][rb]: sum the 4 column slices
+  qd += __shfl_xor_sync(0xffffffffu, qd, 16);
+  qd += __shfl_xor_sync(0xffffffffu, qd, 8);
+  if (cs == 0 && warp < r && rb < r) Qpart[b * rr + warp * r + rb] = qd;
+}
+
+size_t fixed_bytes_c() { return (size_t)8 * 8 * 32 * 4 + 256 + HNC_FLOATS * 4 + 2 * 16 * 8 + 1024; }
+
+int stages_c(int U) {
+  const size_t SB = (size_t)64 * U * 128 + 1024;
+  int ns = (int)((SMEM_BUDGET - fixed_bytes_c()) / SB);
+  return ns > 12 ? 12 : ns;
+}
+
+template <int U>
+cudaError_t launch_c(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_t n, int r, const float* W,
+                     const double* Gpart, int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
+                     int evict_first, cudaStream_t st) {
+  const int ns = stages_c(U);
+  const size_t SB = (size_t)64 * U * 128 + 1024;
+  const size_t smem = (size_t)ns * SB + fixed_bytes_c();
+  cudaError_t e = cudaFuncSetAttribute(k_fused_c<U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_fused_c<U><<<grid, NT, smem, st>>>(mx, mh, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, ns, evict_first);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+cudaError_t get_encode() {
+  if (g_encode) return cudaSuccess;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess) return e;
+  if (q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return cudaSuccess;
+}
+
+cudaError_t make_map(CUtensorMap* map, const float* base, uint64_t cols, uint64_t rows, uint64_t ld_elems,
+                     uint32_t box_rows) {
+  cudaError_t e = get_encode();
+  if (e != cudaSuccess) return e;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld_elems * sizeof(float)};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+int ux_for(int64_t m) { return m <= 8 ? 1 : m <= 16 ? 2 : m <= 32 ? 4 : 5; }
+int rcls_for(int r) { return r <= 2 ? 2 : r <= 4 ? 4 : 8; }
+
+size_t fixed_bytes(int ux) {
+  return (size_t)ux * 8 * 8 * 4 + 256 + (size_t)NW * HN_FLOATS * 4 + 2 * 16 * 8 + 16 + 1024;
+}
+
+int stages_for(int ux) {
+  const size_t SB = 4u * ux * 8 * 128 + 4096;
+  int ns = (int)((SMEM_BUDGET - fixed_bytes(ux)) / SB);
+  if (ns > 16) ns = 16;
+  return ns;
+}
+
+template <int R, int UX>
+cudaError_t launch_t(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_t n, int r, const float* W,
+                     const double* Gpart, int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
+                     int evict_first, cudaStream_t st) {
+  const int ns = stages_for(UX);
+  const size_t SB = 4u * UX * 8 * 128 + 4096;
+  const size_t smem = (size_t)ns * SB + fixed_bytes(UX);
+  cudaError_t e = cudaFuncSetAttribute(k_fused<R, UX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_fused<R, UX><<<grid, NT, smem, st>>>(mx, mh, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, ns, evict_first);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ W update v2 --
+// CTA c owns rows [c*RB, c*RB+RB) with RB*r <= 64 entries; 256 threads = 64
+// entries x 4 chunks of partials; chunk sums combined in order (deterministic).
+template <int R>
+__global__ void __launch_bounds__(256)
+k_wupdate2(float* __restrict__ W, int64_t m, int r, const double* __restrict__ Ppart, int nP,
+           const double* __restrict__ Qpart, int nQ, float eps, double* __restrict__ Gpart) {
+  constexpr int RB = (64 / R) > 0 ? (64 / R) : 1;
+  __shared__ double part[4][64];
+  __shared__ double Qs[R * R];
+  __shared__ double Ps[RB * R];
+  __shared__ float Wn[RB][R];
+  const int t = threadIdx.x, e = t & 63, c = t >> 6;
+  const int rr = r * r;
+  // Q = sum of partials
+  for (int q0 = 0; q0 < rr; q0 += 64) {
+    const int qe = q0 + e;
+    double s = 0.0;
+    if (qe < rr) {
+      const int b0 = (int)((int64_t)nQ * c / 4), b1 = (int)((int64_t)nQ * (c + 1) / 4);
+      for (int bq = b0; bq < b1; ++bq) s += Qpart[(int64_t)bq * rr + qe];
+    }
+    part[c][e] = s;
+    __syncthreads();
+    if (c == 0 && qe < rr) {
+      int kk = qe / r, ll = qe % r;
+      Qs[kk * R + ll] = ((part[0][e] + part[1][e]) + part[2][e]) + part[3][e];
+    }
+    __syncthreads();
+  }
+  // P rows of this CTA
+  const int64_t i0 = (int64_t)blockIdx.x * RB;
+  const int rows = (int)min((int64_t)RB, m - i0);
+  const int64_t mr = m * r;
+  {
+    double s = 0.0;
+    const bool ok = e < rows * r;
+    if (ok) {
+      const int b0 = (int)((int64_t)nP * c / 4), b1 = (int)((int64_t)nP * (c + 1) / 4);
+      const int64_t off = i0 * r + e;
+      for (int bp = b0; bp < b1; ++bp) s += Ppart[(int64_t)bp * mr + off];
+    }
+    part[c][e] = s;
+    __syncthreads();
+    if (c == 0 && ok) {
+      int ii = e / r, kk = e % r;
+      Ps[ii * R + kk] = ((part[0][e] + part[1][e]) + part[2][e]) + part[3][e];
+    }
+    __syncthreads();
+  }
+  if (t < RB) {
+    if (t < rows) {
+      const int64_t i = i0 + t;
+      double w[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) w[k] = (k < r) ? (double)W[i * r + k] : 0.0;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        if (k >= r) {
+          Wn[t][k] = 0.0f;
+          continue;
+        }
+        double d = 0.0;
+#pragma unroll
+        for (int l = 0; l < R; ++l)
+          if (l < r) d += w[l] * Qs[l * R + k];
+        Wn[t][k] = (float)mu_quot(w[k], Ps[t * R + k], d, (double)eps);
+      }
+      for (int k = 0; k < r; ++k) W[i * r + k] = Wn[t][k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < R; ++k) Wn[t][k] = 0.0f;
+    }
+  }
+  __syncthreads();
+  for (int q = t; q < rr; q += 256) {
+    const int k = q / r, l = q % r;
+    double s = 0.0;
+    for (int ii = 0; ii < RB; ++ii) s += (double)Wn[ii][k] * (double)Wn[ii][l];
+    Gpart[(int64_t)blockIdx.x * rr + q] = s;
+  }
+}
+
+int rb2_for(int r) {
+  int R = r <= 2 ? 2 : r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : r <= 32 ? 32 : 64;
+  return (64 / R) > 0 ? 64 / R : 1;
+}
+
+}  // namespace
+
+bool fused_supported(int64_t m, int64_t n, int r, int64_t ldx, const void* X, const void* H) {
+  if (m < 1 || m > 256 || r < 1 || r > 8 || n < 4) return false;
+  if ((n & 3) || (ldx & 3)) return false;
+  if ((reinterpret_cast<uintptr_t>(X) & 15) || (reinterpret_cast<uintptr_t>(H) & 15)) return false;
+  if (n > (int64_t)INT32_MAX - 256) return false;
+  return true;
+}
+
+int fused_grid(int64_t m, int64_t n, int r, int num_sms) {
+  (void)r;
+  int64_t ntiles = m <= 40 ? (n + BN - 1) / BN : (n + BNC - 1) / BNC;
+  return (int)(ntiles < num_sms ? ntiles : num_sms);
+}
+
 size_t fused_scratch_bytes(int64_t, int64_t, int, int) { return 0; }
 void fused_destroy(FusedCtx&) {}
+
+cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int r, const float* W, const double* Gpart,
+                         int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
+                         cudaStream_t st) {
+  const int evict_first = ((double)m * (double)n * 4.0 > 48e6) ? 1 : 0;
+  if (m > 40) {
+    const int U = (int)((m + 63) / 64);
+    CUtensorMap mx, mh;
+    cudaError_t e = make_map(&mx, X, (uint64_t)n, (uint64_t)m, (uint64_t)ldx, (uint32_t)(64 * U));
+    if (e != cudaSuccess) return e;
+    e = make_map(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u);
+    if (e != cudaSuccess) return e;
+#define LC(UU) return launch_c<UU>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st)
+    if (U == 1) LC(1);
+    if (U == 2) LC(2);
+    if (U == 3) LC(3);
+    LC(4);
+#undef LC
+  }
+  const int ux = ux_for(m);
+  CUtensorMap mx, mh;
+  cudaError_t e = make_map(&mx, X, (uint64_t)n, (uint64_t)m, (uint64_t)ldx, (uint32_t)(ux * 8));
+  if (e != cudaSuccess) return e;
+  e = make_map(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u);
+  if (e != cudaSuccess) return e;
+  const int rc = rcls_for(r);
+#define LF(RR, UU) return launch_t<RR, UU>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st)
+  if (rc == 2) {
+    if (ux == 1) LF(2, 1);
+    if (ux == 2) LF(2, 2);
+    if (ux == 4) LF(2, 4);
+    LF(2, 5);
+  }
+  if (rc == 4) {
+    if (ux == 1) LF(4, 1);
+    if (ux == 2) LF(4, 2);
+    if (ux == 4) LF(4, 4);
+    LF(4, 5);
+  }
+  if (ux == 1) LF(8, 1);
+  if (ux == 2) LF(8, 2);
+  if (ux == 4) LF(8, 4);
+  LF(8, 5);
+#undef LF
+}
+
+int wupdate2_ctas(int64_t m, int r) {
+  const int rb = rb2_for(r);
+  return (int)((m + rb - 1) / rb);
+}
+
+cudaError_t launch_wupdate2(float* W, int64_t m, int r, const double* Ppart, int nP, const double* Qpart, int nQ,
+                            float eps, double* Gpart, cudaStream_t st) {
+  const int grid = wupdate2_ctas(m, r);
+#define WU(RR) k_wupdate2<RR><<<grid, 256, 0, st>>>(W, m, r, Ppart, nP, Qpart, nQ, eps, Gpart)
+  if (r <= 2) WU(2);
+  else if (r <= 4) WU(4);
+  else if (r <= 8) WU(8);
+  else if (r <= 16) WU(16);
+  else if (r <= 32) WU(32);
+  else WU(64);
+#undef WU
+  return cudaGetLastError();
+}
+
 }  // namespace ntt

@@ -9,9 +9,29 @@ struct FusedCtx {
   int dummy = 0;
 };
 
-bool fused_supported(int64_t m, int64_t n, int r);
+// Shapes the TMA-fed warp-tile kernel handles: m <= 40 rows, r <= 8, rows of
+// X and H 16-byte aligned (ldx % 4 == 0, n % 4 == 0).
+bool fused_supported(int64_t m, int64_t n, int r, int64_t ldx, const void* X, const void* H);
 int fused_grid(int64_t m, int64_t n, int r, int num_sms);
 size_t fused_scratch_bytes(int64_t m, int64_t n, int r, int grid);
 void fused_destroy(FusedCtx& c);
+
+// mode bits of one fused pass over X
+constexpr int kFusedUpdate = 1;  // phase A: S = W^T X, H <- H o S / (G H + eps), store H
+constexpr int kFusedAcc = 2;     // phase B: per-CTA partials of P = X Hn^T, Q = Hn Hn^T
+
+// One pass over X (m x n, row stride ldx) with the current W (m x r) and
+// G = sum_c Gpart[c] (nG partials).  mode = kFusedAcc alone is the prologue
+// (Hn := H).  Ppart/Qpart: [grid][m*r] / [grid][r*r] fp64.
+cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int r, const float* W,
+                         const double* Gpart, int nG, float eps, float* H, double* Ppart, double* Qpart, int mode,
+                         int grid, cudaStream_t st);
+
+// W update from partials with a parallel fixed-order reduction:
+//   P = sum_b Ppart[b] (nP), Q = sum_b Qpart[b] (nQ), W <- W o P / (W Q + eps);
+//   Gpart[c] = sum over CTA c's rows of Wn^T Wn.  Returns the CTA count via *nG.
+int wupdate2_ctas(int64_t m, int r);
+cudaError_t launch_wupdate2(float* W, int64_t m, int r, const double* Ppart, int nP, const double* Qpart, int nQ,
+                            float eps, double* Gpart, cudaStream_t st);
 
 }  // namespace ntt

@@ -224,24 +224,27 @@ MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, int nranks) {
   p.m = m;
   p.n = n;
   p.r = r;
-  p.fused = fused_supported(m, n, r);
-  p.acc = !p.fused && (m * r <= kMaxAccMR);
+  // shape-level eligibility of the fused TMA kernel; pointer alignment is
+  // re-checked at run time (scratch below is sized for either path).
+  p.fused = fused_supported(m, n, r, n, nullptr, nullptr);
+  p.acc = m * r <= kMaxAccMR;
   p.xp = plan_xht(m, n, num_sms);
   p.qp = plan_xht(r, n, num_sms);
   p.hgrid = hpass_ctas(m, n, r, p.acc, num_sms);
   p.nwup = wupdate_ctas(m, r);
-  p.fgrid = p.fused ? fused_grid(m, n, r, num_sms) : 0;
+  p.fgrid = fused_grid(m, n, r, num_sms);
   int64_t nP = std::max<int64_t>({(int64_t)p.xp.ncs, p.acc ? p.hgrid : 0, (int64_t)p.fgrid, 1});
   int64_t nQ = std::max<int64_t>({(int64_t)p.qp.ncs, p.acc ? p.hgrid : 0, (int64_t)p.fgrid, 1});
+  int64_t nG = std::max<int64_t>({(int64_t)p.nwup, (int64_t)wupdate2_ctas(m, r), 1});
   size_t o = 0;
   p.off_P = o;
   o = align_up(o + sizeof(double) * (size_t)(nP * m * r));
   p.off_Q = o;
   o = align_up(o + sizeof(double) * (size_t)(nQ * r * r));
   p.off_G = o;
-  o = align_up(o + sizeof(double) * (size_t)(std::max(p.nwup, 1) * r * r));
-  p.off_S = o;  // reduced (m r + r r) vector for distributed all-reduce / fused reductions
-  o = align_up(o + sizeof(double) * (size_t)(m * r + r * r) + fused_scratch_bytes(m, n, r, p.fgrid));
+  o = align_up(o + sizeof(double) * (size_t)(nG * r * r));
+  p.off_S = o;  // reduced (m r + r r) vector for the distributed all-reduce
+  o = align_up(o + sizeof(double) * (size_t)(m * r + r * r));
   p.bytes = o;
   (void)nranks;
   return p;
@@ -268,7 +271,29 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
   int nobj = objective_ctas(n);
   if (iters <= 0) return NTT_OK;
 
-  if (p.fused) return fail(h, NTT_ERR_UNSUPPORTED, "fused path not built");
+  if (p.fused && fused_supported(m, n, r, ldx, X, H)) {
+    // 1-pass: prologue P0 = X H0^T, Q0 = H0 H0^T; then per iteration
+    //   W update (reduces the partials)  ->  fused pass (H update + next P, Q).
+    const int fg = p.fgrid;
+    const int nG = wupdate2_ctas(m, r);
+    PLAUNCH(h, 1, 4.0 * (double)(m + r) * (double)n,
+            launch_fused(X, ldx, m, n, r, W, nullptr, 0, eps, H, Ppart, Qpart, kFusedAcc, fg, st));
+    for (int it = 0; it < iters; ++it) {
+      if (dist) {
+        ntt_status s = dist_reduce(h, p, Ppart, fg, Qpart, fg, red);
+        if (s) return s;
+        PLAUNCH(h, 2, 8.0 * (double)(2 * m * r + r * r), launch_wupdate2(W, m, r, red, 1, red + m * r, 1, eps, Gpart, st));
+      } else {
+        PLAUNCH(h, 2, 8.0 * ((double)fg * (m * r + r * r) + m * r),
+                launch_wupdate2(W, m, r, Ppart, fg, Qpart, fg, eps, Gpart, st));
+      }
+      const int mode = kFusedUpdate | ((it + 1 < iters) ? kFusedAcc : 0);
+      PLAUNCH(h, 0, 4.0 * (double)(m + 2 * r) * (double)n,
+              launch_fused(X, ldx, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, fg, st));
+      if (dev_trace) LAUNCH(h, launch_objective(X, ldx, m, n, W, H, r, dev_trace + (int64_t)it * nobj, st));
+    }
+    return NTT_OK;
+  }
 
   // prologue (1-pass) or first W pass: P = X H^T, Q = H H^T
   int nP = 0, nQ = 0;
@@ -288,7 +313,7 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
               launch_wupdate(W, m, r, Ppart, nP, Qpart, nQ, eps, Gpart, st));
     }
     const bool acc_now = p.acc && (it + 1 < iters);
-    PLAUNCH(h, 0, 4.0 * (double)(m + 2 * r) * (double)n,
+    PLAUNCH(h, 5, 4.0 * (double)(m + 2 * r) * (double)n,
             launch_hpass(X, ldx, m, n, W, r, Gpart, p.nwup, eps, H, p.hgrid, acc_now ? Ppart : nullptr,
                            acc_now ? Qpart : nullptr, st));
     if (acc_now) {

@@ -76,7 +76,37 @@ MU_CASES = [
     (300, 257, 32, 6),
     (1, 50, 1, 10),
     (40, 1, 1, 10),
+    # fused 1-pass TMA kernel (m <= 40, r <= 8, n % 4 == 0): every (R, UX) class, ragged last tile
+    (32, 5004, 8, 10),
+    (32, 1 << 16, 8, 10),
+    (6, 10004, 5, 10),
+    (30, 4100, 5, 10),
+    (40, 1000, 8, 10),
+    (16, 28, 3, 10),
+    (8, 132, 2, 10),
+    (15, 388, 4, 10),
+    (5, 120, 1, 10),
+    (24, 640, 7, 10),
+    # fused CTA-cooperative variant (40 < m <= 256, r <= 8 padded to 8)
+    (256, 2052, 8, 10),
+    (256, 1 << 15, 8, 10),
+    (64, 4096, 8, 10),
+    (100, 1000, 5, 10),
+    (200, 4100, 3, 10),
+    (41, 260, 8, 10),
 ]
+
+
+@pytest.mark.parametrize("m,n,r", [(32, 4096, 5), (256, 1024, 5), (6, 1000, 3)])
+def test_nmf_mu_eps_zero_padded_rank(h, ora, m, n, r):
+    """eps = 0 with r < padded kernel rank must not produce 0/0 in the padding."""
+    X, W0, H0 = _mu_inputs(m, n, r, 9)
+    X += 0.5
+    Xd, Wd, Hd = dev(X), dev(W0), dev(H0)
+    h.ntt_nmf_mu(Xd, m, n, n, r, 6, 0.0, Wd, Hd)
+    Wo, Ho = ora.nmf_mu(X, W0.astype(np.float64), H0.astype(np.float64), 6, eps=0.0)
+    assert_close_factor(host(Wd), Wo, what="W eps0")
+    assert_close_factor(host(Hd), Ho, what="H eps0")
 
 
 def _mu_inputs(m, n, r, seed):
@@ -136,9 +166,9 @@ def test_nmf_mu_zero_iterations_is_identity(h):
     assert np.array_equal(host(Wd), W0) and np.array_equal(host(Hd), H0)
 
 
-def test_nmf_mu_scale_invariance_and_determinism(h):
+@pytest.mark.parametrize("m,n,r", [(32, 4096, 8), (256, 2048, 8), (20, 999, 4)])
+def test_nmf_mu_scale_invariance_and_determinism(h, m, n, r):
     """Metamorphic (no oracle): X -> 8X gives W -> 8W, H unchanged; repeat runs bit-identical."""
-    m, n, r = 32, 4096, 8
     X, W0, H0 = _mu_inputs(m, n, r, 4)
     outs = []
     for scale in (1.0, 8.0, 1.0):
