@@ -167,6 +167,11 @@ double ntt_compression_ratio(int32_t d, const int64_t* dims, const int32_t* rank
 ntt_status ntt_profile_enable(ntt_handle h, int enable);
 ntt_status ntt_profile_get(ntt_handle h, int cls, int64_t* launches, double* total_ms,
                            double* total_bytes);
+/* Same, restricted to the launches issued for TT step `step` of ntt_decompose
+ * (1..d-1; d = last-core gather and error pass; 0 = outside ntt_decompose;
+ * -1 = all).                                                                 */
+ntt_status ntt_profile_get_step(ntt_handle h, int cls, int step, int64_t* launches,
+                                double* total_ms, double* total_bytes);
 
 /* ----------------------------------------------------- multi-GPU (NCCL) ----
  * One process per GPU.  Rank 0 calls ntt_get_unique_id and broadcasts the 128

@@ -163,10 +163,11 @@ class Handle:
     def ntt_profile_enable(self, enable: bool = True):
         self._check(lib().ntt_profile_enable(self._h, 1 if enable else 0))
 
-    def ntt_profile_get(self, cls: int):
-        """(launches, total_ms, total_algorithmic_bytes) for kernel class `cls`."""
+    def ntt_profile_get(self, cls: int, step: int = -1):
+        """(launches, total_ms, total_algorithmic_bytes) for kernel class `cls` (optionally one TT step)."""
         n, ms, by = ctypes.c_int64(0), ctypes.c_double(0), ctypes.c_double(0)
-        self._check(lib().ntt_profile_get(self._h, cls, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(by)))
+        self._check(lib().ntt_profile_get_step(self._h, cls, step, ctypes.byref(n), ctypes.byref(ms),
+                                               ctypes.byref(by)))
         return int(n.value), float(ms.value), float(by.value)
 
     def ntt_reconstruct(self, dims, ranks, cores, out=None, ref=None, want_error: bool = False) -> Optional[float]:

@@ -32,6 +32,8 @@ SIGNATURES = {
     "ntt_decompose": (c_int, [c_p, c_p, c_i32, c_p, c_p, c_i32, c_u64, c_f32, c_p, c_p, c_p, c_size]),
     "ntt_profile_enable": (c_int, [c_p, c_int]),
     "ntt_profile_get": (c_int, [c_p, c_int, ctypes.POINTER(c_i64), ctypes.POINTER(c_f64), ctypes.POINTER(c_f64)]),
+    "ntt_profile_get_step": (c_int, [c_p, c_int, c_int, ctypes.POINTER(c_i64), ctypes.POINTER(c_f64),
+                                     ctypes.POINTER(c_f64)]),
     "ntt_reconstruct": (c_int, [c_p, c_i32, c_p, c_p, c_p, c_p, c_p, c_p]),
     "ntt_generate": (c_int, [c_p, c_i32, c_p, c_p, c_p, c_f32, c_u64, c_u64, c_p]),
     "ntt_compression_ratio": (c_f64, [c_i32, c_p, c_p]),

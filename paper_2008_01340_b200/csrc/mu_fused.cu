@@ -255,24 +255,25 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
             s2[k][1] = __ffma2_rn(bc(w[k]), xc, s2[k][1]);
           }
         }
-        // E = G H ; Hn = H S / (E + eps)
+        // E = G H (l outer: 2R independent accumulators) ; Hn = H S / (E + eps)
+        float2 ev[R][2];
+#pragma unroll
+        for (int k = 0; k < R; ++k) ev[k][0] = ev[k][1] = f2(0.f, 0.f);
+#pragma unroll
+        for (int l = 0; l < R; ++l) {
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            const float g = Gs[k * 8 + l];
+            ev[k][0] = __ffma2_rn(bc(g), hv[l][0], ev[k][0]);
+            ev[k][1] = __ffma2_rn(bc(g), hv[l][1], ev[k][1]);
+          }
+        }
 #pragma unroll
         for (int k = 0; k < R; ++k) {
-          float2 e0 = f2(0.f, 0.f), e1 = f2(0.f, 0.f);
-#pragma unroll
-          float gk[8];
-          *reinterpret_cast<float4*>(gk) = *reinterpret_cast<const float4*>(Gs + k * 8);
-          if (R > 4) *reinterpret_cast<float4*>(gk + 4) = *reinterpret_cast<const float4*>(Gs + k * 8 + 4);
-#pragma unroll
-          for (int l = 0; l < R; ++l) {
-            const float g = gk[l];
-            e0 = __ffma2_rn(bc(g), hv[l][0], e0);
-            e1 = __ffma2_rn(bc(g), hv[l][1], e1);
-          }
-          hn[k][0].x = mu_q(hv[k][0].x, s2[k][0].x, e0.x, eps);
-          hn[k][0].y = mu_q(hv[k][0].y, s2[k][0].y, e0.y, eps);
-          hn[k][1].x = mu_q(hv[k][1].x, s2[k][1].x, e1.x, eps);
-          hn[k][1].y = mu_q(hv[k][1].y, s2[k][1].y, e1.y, eps);
+          hn[k][0].x = mu_q(hv[k][0].x, s2[k][0].x, ev[k][0].x, eps);
+          hn[k][0].y = mu_q(hv[k][0].y, s2[k][0].y, ev[k][0].y, eps);
+          hn[k][1].x = mu_q(hv[k][1].x, s2[k][1].x, ev[k][1].x, eps);
+          hn[k][1].y = mu_q(hv[k][1].y, s2[k][1].y, ev[k][1].y, eps);
           if (k >= r) hn[k][0] = hn[k][1] = f2(0.f, 0.f);  // padded ranks (0/0 when eps = 0)
         }
         // columns beyond n: zero (never stored, never accumulated)
@@ -351,15 +352,21 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
           }
           hq[t] = src[rb];
         }
+        float xs[UX][4];
 #pragma unroll
         for (int u = 0; u < UX; ++u) {
           const float4 x = lds128(xb + (rb + 8 * u) * 128 + ((s4 ^ rb) << 4));
-          const float xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-#pragma unroll
-            for (int kp = 0; kp < R / 2; ++kp) acc[u * (R / 2) + kp] = __ffma2_rn(bc(xs[t]), hq2[t][kp], acc[u * (R / 2) + kp]);
+          xs[u][0] = x.x;
+          xs[u][1] = x.y;
+          xs[u][2] = x.z;
+          xs[u][3] = x.w;
         }
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+          for (int u = 0; u < UX; ++u)
+#pragma unroll
+            for (int kp = 0; kp < R / 2; ++kp) acc[u * (R / 2) + kp] = __ffma2_rn(bc(xs[u][t]), hq2[t][kp], acc[u * (R / 2) + kp]);
 #pragma unroll
         for (int t = 0; t < 4; ++t)
 #pragma unroll
@@ -444,7 +451,8 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   float* Sred = reinterpret_cast<float*>(smem + (size_t)ns * SB);  // [8 warps][8 k][32 c]
   float* Gs = Sred + 8 * 8 * 32;                                     // 8 x 8
   float* Hn = Gs + 64;                                               // HNC_FLOATS
-  uint64_t* full = reinterpret_cast<uint64_t*>(Hn + HNC_FLOATS);
+  float* Wc = Hn + HNC_FLOATS;                                       // MP x 8 (W, rank padded)
+  uint64_t* full = reinterpret_cast<uint64_t*>(Wc + MP * 8);
   uint64_t* empty = full + ns;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -459,6 +467,10 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         for (int bq = 0; bq < nG; ++bq) sum += Gpart[(int64_t)bq * rr + k * r + l];
       Gs[e] = (float)sum;
     }
+  }
+  for (int e = tid; e < MP * 8; e += NT) {
+    const int i = e >> 3, k = e & 7;
+    Wc[e] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
   }
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) {
@@ -494,18 +506,8 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     return;
   }
 
-  // phase A lane roles: columns 4q..4q+3, ranks 2g, 2g+1 ; W slice in registers
+  // phase A lane roles: columns 4q..4q+3, ranks 2g, 2g+1 (W pairs by broadcast LDS.64)
   const int q = lane & 7, g = lane >> 3;
-  float wr[RW][2];
-#pragma unroll
-  for (int v = 0; v < RW; ++v) {
-    const int i = warp * RW + v;
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int k = 2 * g + t;
-      wr[v][t] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
-    }
-  }
   // phase B lane roles: rows warp*RW + rb + 8u, columns 8cs..8cs+7 ; Q[warp][rb]
   const int rb = lane & 7, cs = lane >> 3;
   constexpr int V = U * 8;  // P values per lane per tile (u, k)
@@ -531,10 +533,11 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         const int i = warp * RW + v;
         const float4 x = lds128(st + i * 128 + ((q ^ (i & 7)) << 4));
         const float2 x01 = f2(x.x, x.y), x23 = f2(x.z, x.w);
-        sa = __ffma2_rn(bc(wr[v][0]), x01, sa);
-        sb = __ffma2_rn(bc(wr[v][0]), x23, sb);
-        sc = __ffma2_rn(bc(wr[v][1]), x01, sc);
-        sd = __ffma2_rn(bc(wr[v][1]), x23, sd);
+        const float2 wv = *reinterpret_cast<const float2*>(Wc + i * 8 + 2 * g);
+        sa = __ffma2_rn(bc(wv.x), x01, sa);
+        sb = __ffma2_rn(bc(wv.x), x23, sb);
+        sc = __ffma2_rn(bc(wv.y), x01, sc);
+        sd = __ffma2_rn(bc(wv.y), x23, sd);
       }
       float* sr = Sred + (warp * 8 + 2 * g) * 32 + 4 * q;
       *reinterpret_cast<float4*>(sr) = make_float4(sa.x, sa.y, sb.x, sb.y);
@@ -550,12 +553,17 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         float S = 0.0f;
 #pragma unroll
         for (int w = 0; w < NW; ++w) S += Sred[(w * 8 + kt) * 32 + ct];
-        float e = 0.0f;
+        float hl[8];
 #pragma unroll
-        for (int l = 0; l < 8; ++l) {
-          const float hl = *reinterpret_cast<const float*>(st + XB + l * 128 + ((((ct >> 2) ^ l)) << 4) + (ct & 3) * 4);
-          e = fmaf(Gs[kt * 8 + l], hl, e);
+        for (int l = 0; l < 8; ++l)
+          hl[l] = *reinterpret_cast<const float*>(st + XB + l * 128 + ((((ct >> 2) ^ l)) << 4) + (ct & 3) * 4);
+        float e0 = 0.0f, e1 = 0.0f;
+#pragma unroll
+        for (int l = 0; l < 8; l += 2) {
+          e0 = fmaf(Gs[kt * 8 + l], hl[l], e0);
+          e1 = fmaf(Gs[kt * 8 + l + 1], hl[l + 1], e1);
         }
+        const float e = e0 + e1;
         hn = mu_q(hkc, S, e, eps);
         if (kt >= r || col >= n) hn = 0.0f;
         if (kt < r && col < n) H[(int64_t)kt * n + col] = hn;
@@ -589,16 +597,22 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
           hrb[t] = src[rb];
           hw[t] = src[warp];
         }
+        float xs[U][4];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int i = warp * RW + rb + 8 * u;
           const float4 x = lds128(st + i * 128 + (((2 * cs + s4) ^ rb) << 4));
-          const float xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-#pragma unroll
-            for (int kp = 0; kp < 4; ++kp) acc[u * 4 + kp] = __ffma2_rn(bc(xs[t]), hq2[t][kp], acc[u * 4 + kp]);
+          xs[u][0] = x.x;
+          xs[u][1] = x.y;
+          xs[u][2] = x.z;
+          xs[u][3] = x.w;
         }
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int kp = 0; kp < 4; ++kp) acc[u * 4 + kp] = __ffma2_rn(bc(xs[u][t]), hq2[t][kp], acc[u * 4 + kp]);
 #pragma unroll
         for (int t = 0; t < 4; ++t) qa = fmaf(hw[t], hrb[t], qa);
       }
@@ -644,7 +658,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   if (cs == 0 && warp < r && rb < r) Qpart[b * rr + warp * r + rb] = qd;
 }
 
-size_t fixed_bytes_c() { return (size_t)8 * 8 * 32 * 4 + 256 + HNC_FLOATS * 4 + 2 * 16 * 8 + 1024; }
+size_t fixed_bytes_c() { return (size_t)8 * 8 * 32 * 4 + 256 + HNC_FLOATS * 4 + 256 * 8 * 4 + 2 * 16 * 8 + 1024; }
 
 int stages_c(int U) {
   const size_t SB = (size_t)64 * U * 128 + 1024;

@@ -85,8 +85,10 @@ struct ntt_handle_s {
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
+  int cur_step = 0;  // TT step of the launches being recorded (0 outside ntt_decompose)
   struct Rec {
     int cls;
+    int step;
     int ev0;
     double bytes;
   };
@@ -192,7 +194,7 @@ int prof_begin(ntt_handle h) {
 void prof_end(ntt_handle h, int ev0, int cls, double bytes) {
   if (ev0 < 0) return;
   cudaEventRecord(h->ev_pool[ev0 + 1], h->stream);
-  h->recs.push_back({cls, ev0, bytes});
+  h->recs.push_back({cls, h->cur_step, ev0, bytes});
 }
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
@@ -784,6 +786,7 @@ ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t*
     const int64_t m = P.m[l], n = P.ncol[l];
     const int r = (int)s.r[l];
     Hl = hb[(l - 1) & 1];
+    h->cur_step = l;
     LAUNCH(h, launch_fill_uniform(Wd, m * r, seed, stream_w(l), 0, cs));
     if (h->nranks == 1) {
       LAUNCH(h, launch_fill_uniform(Hl, (int64_t)r * n, seed, stream_h(l), 0, cs));
@@ -797,6 +800,7 @@ ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t*
     CU(h, cudaMemcpyAsync(dcores + s.off[l], Wd, sizeof(float) * (size_t)(m * r), cudaMemcpyDeviceToDevice, cs));
     X = Hl;
   }
+  h->cur_step = d;  // last-core gather and the error pass
   // last core G_d[k][i][0] = T_{d-1}[k][i]  (Alg. 2 l.11)
   const int64_t rl = s.r[d - 1], nd = s.dims[d - 1];
   if (h->nranks == 1) {
@@ -827,6 +831,7 @@ ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t*
     if ((st = contract_run(h, P.sl, P.cp, lc, nullptr, 0.0f, 0, dA, es))) return st;
     if ((st = finish_error(h, P.cp, es, h->nranks > 1, rel_err))) return st;
   }
+  h->cur_step = 0;
   if (!cores_dev) {
     CU(h, cudaMemcpyAsync(cores, dcores, sizeof(float) * (size_t)s.cores, cudaMemcpyDeviceToHost, cs));
     CU(h, cudaStreamSynchronize(cs));
@@ -881,12 +886,17 @@ ntt_status ntt_profile_enable(ntt_handle h, int enable) {
 }
 
 ntt_status ntt_profile_get(ntt_handle h, int cls, int64_t* launches, double* total_ms, double* total_bytes) {
+  return ntt_profile_get_step(h, cls, -1, launches, total_ms, total_bytes);
+}
+
+ntt_status ntt_profile_get_step(ntt_handle h, int cls, int step, int64_t* launches, double* total_ms,
+                                double* total_bytes) {
   if (!h || cls < 0 || cls >= NTT_PROF_CLASSES) return NTT_ERR_INVALID_ARG;
   CU(h, cudaStreamSynchronize(h->stream));
   int64_t n = 0;
   double ms = 0.0, by = 0.0;
   for (const auto& r : h->recs) {
-    if (r.cls != cls) continue;
+    if (r.cls != cls || (step >= 0 && r.step != step)) continue;
     float t = 0.0f;
     CU(h, cudaEventElapsedTime(&t, h->ev_pool[r.ev0], h->ev_pool[r.ev0 + 1]));
     ++n;
