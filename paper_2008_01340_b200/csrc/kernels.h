@@ -63,5 +63,7 @@ cudaError_t launch_sum_partials(const double* part, int nparts, int64_t len, dou
 cudaError_t launch_fill_uniform_cols(float* H, int r, int64_t nloc, int64_t b, int64_t nd, int64_t off, int64_t nglob,
                                      uint64_t seed, uint64_t stream, cudaStream_t st);
 // gathered rank-major blocks [g][r][b_g] -> core [r][nd]
+// fixed-order sum of npart (a, b) pairs -> out[0..1]
+cudaError_t launch_sum_pairs(const double* part, int npart, double* out, cudaStream_t st);
 cudaError_t launch_gather_last_core(const float* gath, int64_t r, int64_t nd, int nranks, float* core, cudaStream_t st);
 }  // namespace ntt

@@ -423,35 +423,41 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
 
 // ===========================================================================
 // Variant C: CTA-cooperative tiles for 40 < m <= 256 (rank padded to 8).
-// Tile = 32 columns x MP rows (one SWIZZLE_128B box) + the 8 x 32 H box.
-// Phase A splits the m-long dot products across the 8 consumer warps (warp w
-// owns rows [8U w, 8U w + 8U), its W slice in registers), reduces the 8 partial
-// S tiles through smem in fixed order, then 256 threads (k, c) form E = G H and
-// Hn.  Phase B: warp w owns the same rows of P = X Hn^T (lanes = row block x
-// 8-column slice) and row w of Q = Hn Hn^T; rows are disjoint across warps, so
-// per-CTA partials need no cross-warp reduction.
+// Small CTAs (4 consumer warps + 1 TMA warp, <= 112 KB smem) so TWO CTAs share
+// an SM and one CTA's serial sections (S reduction, H update, barriers) overlap
+// the other's FMA phases.  Tile = 32 columns x MP rows (one SWIZZLE_128B box)
+// + the 8 x 32 H box.  Phase A splits the m-long dot products across the 4
+// warps (warp w owns rows [RW w, RW w + RW)), reduces the partial S tiles
+// through smem in fixed order; 128 threads form E = G H and Hn (2 entries
+// each).  Phase B: warp w owns the same rows of P = X Hn^T in sub-chunks of 32
+// (lanes = row block x 8-column slice, reduce-scatter over the slices, fp64
+// accumulation), and rows 2w, 2w+1 of Q = Hn Hn^T.  Rows are disjoint across
+// warps, so per-CTA partials need no cross-warp reduction.
 // ===========================================================================
 constexpr int BNC = 32;
-constexpr int HNC_FLOATS = 32 * 8 + 16;  // transposed Hn tile [c][k] + 4 floats per 8-column group
+constexpr int NWC = 4;                  // consumer warps per CTA
+constexpr int NTC = (NWC + 1) * 32;
+constexpr int HNC_FLOATS = 32 * 8 + 16; // transposed Hn tile [c][k] + 4 floats per 8-column group
+constexpr int SMEM_C = 113 * 1024;      // two CTAs per SM
 
 __device__ __forceinline__ int hnc_idx(int c, int k) { return c * 8 + k + 4 * (c >> 3); }
 
-template <int U>
-__global__ void __launch_bounds__(NT, 1)
+template <int MP>
+__global__ void __launch_bounds__(NTC, 2)
 k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmH, int m, int64_t n, int r,
           const float* __restrict__ W, const double* __restrict__ Gpart, int nG, float eps, float* __restrict__ H,
           double* __restrict__ Ppart, double* __restrict__ Qpart, int mode, int ns, int evict_first) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  constexpr int MP = 64 * U;                 // padded rows (box rows)
-  constexpr int RW = 8 * U;                  // rows per warp
+  constexpr int RW = MP / NWC;          // rows per warp (32 or 64)
+  constexpr int NCH = RW / 32;          // phase-B sub-chunks of 32 rows
   constexpr uint32_t XB = MP * 128u;
   constexpr uint32_t SB = XB + 1024u;
   unsigned char* stages = smem;
-  float* Sred = reinterpret_cast<float*>(smem + (size_t)ns * SB);  // [8 warps][8 k][32 c]
-  float* Gs = Sred + 8 * 8 * 32;                                     // 8 x 8
+  float* Sred = reinterpret_cast<float*>(smem + (size_t)ns * SB);  // [NWC][8 k][32 c]
+  float* Gs = Sred + NWC * 8 * 32;                                   // 8 x 8
   float* Hn = Gs + 64;                                               // HNC_FLOATS
-  float* Wc = Hn + HNC_FLOATS;                                       // MP x 8 (W, rank padded)
+  float* Wc = Hn + HNC_FLOATS;                                       // MP x 8 (rank padded)
   uint64_t* full = reinterpret_cast<uint64_t*>(Wc + MP * 8);
   uint64_t* empty = full + ns;
 
@@ -460,7 +466,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   const bool do_acc = (mode & kFusedAcc) != 0;
   if (do_update) {
     const int rr = r * r;
-    for (int e = tid; e < 64; e += NT) {
+    for (int e = tid; e < 64; e += NTC) {
       int k = e >> 3, l = e & 7;
       double sum = 0.0;
       if (k < r && l < r)
@@ -468,14 +474,14 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       Gs[e] = (float)sum;
     }
   }
-  for (int e = tid; e < MP * 8; e += NT) {
+  for (int e = tid; e < MP * 8; e += NTC) {
     const int i = e >> 3, k = e & 7;
     Wc[e] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
   }
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NW);
+      mbar_init(&empty[s], NWC);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -485,7 +491,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   const int64_t b = blockIdx.x;
   const int64_t J = (ntiles > b) ? (ntiles - b + gridDim.x - 1) / gridDim.x : 0;
 
-  if (warp == NW) {
+  if (warp == NWC) {
     if (lane == 0) {
       uint64_t policy;
       if (evict_first)
@@ -506,17 +512,16 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     return;
   }
 
-  // phase A lane roles: columns 4q..4q+3, ranks 2g, 2g+1 (W pairs by broadcast LDS.64)
-  const int q = lane & 7, g = lane >> 3;
-  // phase B lane roles: rows warp*RW + rb + 8u, columns 8cs..8cs+7 ; Q[warp][rb]
-  const int rb = lane & 7, cs = lane >> 3;
-  constexpr int V = U * 8;  // P values per lane per tile (u, k)
-  double accd[V / 4];
+  const int q = lane & 7, g = lane >> 3;   // phase A: columns 4q..4q+3, ranks 2g, 2g+1
+  const int rb = lane & 7, cs = lane >> 3; // phase B: rows rb + 8u of a 32-row chunk, columns 8cs..8cs+7
+  double accd[NCH][8];
 #pragma unroll
-  for (int v = 0; v < V / 4; ++v) accd[v] = 0.0;
-  double qd = 0.0;
+  for (int h = 0; h < NCH; ++h)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) accd[h][v] = 0.0;
+  double qd0 = 0.0, qd1 = 0.0;
   const bool h1 = (lane >> 4) & 1, h0 = (lane >> 3) & 1;
-  const int kt = tid >> 5, ct = tid & 31;  // (k, c) role in the H update
+  constexpr int NBAR = NWC * 32;
 
   for (int64_t j = 0; j < J; ++j) {
     const int s = (int)(j % ns);
@@ -528,7 +533,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     if (do_update) {
       // ---- phase A: partial S over this warp's rows
       float2 sa = f2(0.f, 0.f), sb = f2(0.f, 0.f), sc = f2(0.f, 0.f), sd = f2(0.f, 0.f);
-#pragma unroll
+#pragma unroll 8
       for (int v = 0; v < RW; ++v) {
         const int i = warp * RW + v;
         const float4 x = lds128(st + i * 128 + ((q ^ (i & 7)) << 4));
@@ -543,28 +548,29 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       *reinterpret_cast<float4*>(sr) = make_float4(sa.x, sa.y, sb.x, sb.y);
       *reinterpret_cast<float4*>(sr + 32) = make_float4(sc.x, sc.y, sd.x, sd.y);
     }
-    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
-    {
-      // ---- H update for (k = kt, c = ct)
+    asm volatile("bar.sync 1, %0;" ::"r"(NBAR) : "memory");
+    // ---- H update: thread handles (k, c) for k in {kt, kt+4}, c = ct
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int kt = (tid >> 5) + 4 * hh, ct = tid & 31;
       const int64_t col = jt + ct;
-      const float hkc = *reinterpret_cast<const float*>(st + XB + kt * 128 + ((((ct >> 2) ^ kt)) << 4) + (ct & 3) * 4);
-      float hn = 0.0f;
+      const float hkc = *reinterpret_cast<const float*>(st + XB + kt * 128 + (((ct >> 2) ^ kt) << 4) + (ct & 3) * 4);
+      float hn;
       if (do_update) {
         float S = 0.0f;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) S += Sred[(w * 8 + kt) * 32 + ct];
+        for (int w = 0; w < NWC; ++w) S += Sred[(w * 8 + kt) * 32 + ct];
         float hl[8];
 #pragma unroll
         for (int l = 0; l < 8; ++l)
-          hl[l] = *reinterpret_cast<const float*>(st + XB + l * 128 + ((((ct >> 2) ^ l)) << 4) + (ct & 3) * 4);
+          hl[l] = *reinterpret_cast<const float*>(st + XB + l * 128 + (((ct >> 2) ^ l) << 4) + (ct & 3) * 4);
         float e0 = 0.0f, e1 = 0.0f;
 #pragma unroll
         for (int l = 0; l < 8; l += 2) {
           e0 = fmaf(Gs[kt * 8 + l], hl[l], e0);
           e1 = fmaf(Gs[kt * 8 + l + 1], hl[l + 1], e1);
         }
-        const float e = e0 + e1;
-        hn = mu_q(hkc, S, e, eps);
+        hn = mu_q(hkc, S, e0 + e1, eps);
         if (kt >= r || col >= n) hn = 0.0f;
         if (kt < r && col < n) H[(int64_t)kt * n + col] = hn;
       } else {
@@ -572,110 +578,127 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       }
       if (do_acc) Hn[hnc_idx(ct, kt)] = hn;
     }
-    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(NBAR) : "memory");
 
     if (do_acc) {
       // ---- phase B
-      float2 acc[V / 2];
+      {
+        float qa0 = 0.f, qa1 = 0.f;
 #pragma unroll
-      for (int v = 0; v < V / 2; ++v) acc[v] = f2(0.f, 0.f);
-      float qa = 0.0f;
-#pragma unroll
-      for (int s4 = 0; s4 < 2; ++s4) {
-        const int c = 8 * cs + 4 * s4;
-        float2 hq2[4][4];
-        float hrb[4], hw[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const float* src = Hn + hnc_idx(c + t, 0);
-          const float4 a = *reinterpret_cast<const float4*>(src);
-          const float4 bq = *reinterpret_cast<const float4*>(src + 4);
-          hq2[t][0] = f2(a.x, a.y);
-          hq2[t][1] = f2(a.z, a.w);
-          hq2[t][2] = f2(bq.x, bq.y);
-          hq2[t][3] = f2(bq.z, bq.w);
-          hrb[t] = src[rb];
-          hw[t] = src[warp];
+        for (int t = 0; t < 8; ++t) {
+          const float* src = Hn + hnc_idx(8 * cs + t, 0);
+          const float hr = src[rb];
+          qa0 = fmaf(src[2 * warp], hr, qa0);
+          qa1 = fmaf(src[2 * warp + 1], hr, qa1);
         }
-        float xs[U][4];
+        qd0 += (double)qa0;
+        qd1 += (double)qa1;
+      }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int i = warp * RW + rb + 8 * u;
-          const float4 x = lds128(st + i * 128 + (((2 * cs + s4) ^ rb) << 4));
-          xs[u][0] = x.x;
-          xs[u][1] = x.y;
-          xs[u][2] = x.z;
-          xs[u][3] = x.w;
+      for (int h = 0; h < NCH; ++h) {
+        float2 acc[16];
+#pragma unroll
+        for (int v = 0; v < 16; ++v) acc[v] = f2(0.f, 0.f);
+#pragma unroll
+        for (int s4 = 0; s4 < 2; ++s4) {
+          float2 hq2[4][4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float* src = Hn + hnc_idx(8 * cs + 4 * s4 + t, 0);
+            const float4 a = *reinterpret_cast<const float4*>(src);
+            const float4 bq = *reinterpret_cast<const float4*>(src + 4);
+            hq2[t][0] = f2(a.x, a.y);
+            hq2[t][1] = f2(a.z, a.w);
+            hq2[t][2] = f2(bq.x, bq.y);
+            hq2[t][3] = f2(bq.z, bq.w);
+          }
+          float xs[4][4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = warp * RW + 32 * h + rb + 8 * u;
+            const float4 x = lds128(st + i * 128 + (((2 * cs + s4) ^ rb) << 4));
+            xs[u][0] = x.x;
+            xs[u][1] = x.y;
+            xs[u][2] = x.z;
+            xs[u][3] = x.w;
+          }
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int kp = 0; kp < 4; ++kp)
+                acc[u * 4 + kp] = __ffma2_rn(bc(xs[u][t]), hq2[t][kp], acc[u * 4 + kp]);
+        }
+        // reduce-scatter over the 4 column-slice lanes: keep flat f in [8 cs, 8 cs + 8)
+        float a1[32];
+#pragma unroll
+        for (int v = 0; v < 16; ++v) {
+          a1[2 * v] = acc[v].x;
+          a1[2 * v + 1] = acc[v].y;
+        }
+        float a2[16];
+#pragma unroll
+        for (int v = 0; v < 16; ++v) {
+          const float send = h1 ? a1[v] : a1[v + 16];
+          const float keep = h1 ? a1[v + 16] : a1[v];
+          a2[v] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
         }
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int kp = 0; kp < 4; ++kp) acc[u * 4 + kp] = __ffma2_rn(bc(xs[u][t]), hq2[t][kp], acc[u * 4 + kp]);
-#pragma unroll
-        for (int t = 0; t < 4; ++t) qa = fmaf(hw[t], hrb[t], qa);
+        for (int v = 0; v < 8; ++v) {
+          const float send = h0 ? a2[v] : a2[v + 8];
+          const float keep = h0 ? a2[v + 8] : a2[v];
+          accd[h][v] += (double)(keep + __shfl_xor_sync(0xffffffffu, send, 8));
+        }
       }
-      // reduce-scatter P over the 4 column-slice lanes (xor 16, xor 8)
-      float a1[V];
-#pragma unroll
-      for (int v = 0; v < V / 2; ++v) {
-        a1[2 * v] = acc[v].x;
-        a1[2 * v + 1] = acc[v].y;
-      }
-      float a2[V / 2];
-#pragma unroll
-      for (int v = 0; v < V / 2; ++v) {
-        const float send = h1 ? a1[v] : a1[v + V / 2];
-        const float keep = h1 ? a1[v + V / 2] : a1[v];
-        a2[v] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-      }
-#pragma unroll
-      for (int v = 0; v < V / 4; ++v) {
-        const float send = h0 ? a2[v] : a2[v + V / 4];
-        const float keep = h0 ? a2[v + V / 4] : a2[v];
-        accd[v] += (double)(keep + __shfl_xor_sync(0xffffffffu, send, 8));
-      }
-      qd += (double)qa;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 
   if (!do_acc) return;
-  // P: lane holds flat f = u*8 + k in [cs*V/4, cs*V/4 + V/4) for rows warp*RW + rb + 8u
+  // P: lane holds flat f = u*8 + k in [8 cs, 8 cs + 8) of sub-chunk h, rows warp*RW + 32h + rb + 8u
   const int mr = m * r, rr = r * r;
 #pragma unroll
-  for (int v = 0; v < V / 4; ++v) {
-    const int f = cs * (V / 4) + v;
-    const int u = f >> 3, k = f & 7;
-    const int row = warp * RW + rb + 8 * u;
-    if (row < m && k < r) Ppart[b * mr + row * r + k] = accd[v];
+  for (int h = 0; h < NCH; ++h)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const int f = 8 * cs + v;
+      const int u = f >> 3, k = f & 7;
+      const int row = warp * RW + 32 * h + rb + 8 * u;
+      if (row < m && k < r) Ppart[b * mr + row * r + k] = accd[h][v];
+    }
+  // Q rows 2w, 2w+1, column rb: sum the 4 column slices
+  qd0 += __shfl_xor_sync(0xffffffffu, qd0, 16);
+  qd0 += __shfl_xor_sync(0xffffffffu, qd0, 8);
+  qd1 += __shfl_xor_sync(0xffffffffu, qd1, 16);
+  qd1 += __shfl_xor_sync(0xffffffffu, qd1, 8);
+  if (cs == 0 && rb < r) {
+    if (2 * warp < r) Qpart[b * rr + (2 * warp) * r + rb] = qd0;
+    if (2 * warp + 1 < r) Qpart[b * rr + (2 * warp + 1) * r + rb] = qd1;
   }
-  // Q[warp][rb]: sum the 4 column slices
-  qd += __shfl_xor_sync(0xffffffffu, qd, 16);
-  qd += __shfl_xor_sync(0xffffffffu, qd, 8);
-  if (cs == 0 && warp < r && rb < r) Qpart[b * rr + warp * r + rb] = qd;
 }
 
-size_t fixed_bytes_c() { return (size_t)8 * 8 * 32 * 4 + 256 + HNC_FLOATS * 4 + 256 * 8 * 4 + 2 * 16 * 8 + 1024; }
+size_t fixed_bytes_c(int MP) {
+  return (size_t)NWC * 8 * 32 * 4 + 256 + HNC_FLOATS * 4 + (size_t)MP * 8 * 4 + 2 * 16 * 8 + 1024;
+}
 
-int stages_c(int U) {
-  const size_t SB = (size_t)64 * U * 128 + 1024;
-  int ns = (int)((SMEM_BUDGET - fixed_bytes_c()) / SB);
+int stages_c(int MP) {
+  const size_t SB = (size_t)MP * 128 + 1024;
+  int ns = (int)((SMEM_C - fixed_bytes_c(MP)) / SB);
   return ns > 12 ? 12 : ns;
 }
 
-template <int U>
+template <int MP>
 cudaError_t launch_c(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_t n, int r, const float* W,
                      const double* Gpart, int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
                      int evict_first, cudaStream_t st) {
-  const int ns = stages_c(U);
-  const size_t SB = (size_t)64 * U * 128 + 1024;
-  const size_t smem = (size_t)ns * SB + fixed_bytes_c();
-  cudaError_t e = cudaFuncSetAttribute(k_fused_c<U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int ns = stages_c(MP);
+  const size_t SB = (size_t)MP * 128 + 1024;
+  const size_t smem = (size_t)ns * SB + fixed_bytes_c(MP);
+  cudaError_t e = cudaFuncSetAttribute(k_fused_c<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_fused_c<U><<<grid, NT, smem, st>>>(mx, mh, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, ns, evict_first);
+  k_fused_c<MP><<<grid, NTC, smem, st>>>(mx, mh, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, ns, evict_first);
   return cudaGetLastError();
 }
 
@@ -735,14 +758,31 @@ cudaError_t launch_t(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_
 }
 
 // ------------------------------------------------------------ W update v2 --
-// CTA c owns rows [c*RB, c*RB+RB) with RB*r <= 64 entries; 256 threads = 64
-// entries x 4 chunks of partials; chunk sums combined in order (deterministic).
+// CTA c owns rows [c*RB, c*RB+RB) with RB*r <= 64 entries; 1024 threads = 64
+// entries x 16 chunks of partials; each thread sums its chunk with 4
+// independent accumulators (latency hiding), chunks are combined in order --
+// a fixed summation tree, so results are deterministic.
+constexpr int WU2_CH = 16;
+
+__device__ __forceinline__ double chunk_sum(const double* __restrict__ base, int64_t stride, int b0, int b1) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int bq = b0;
+  for (; bq + 3 < b1; bq += 4) {
+    s0 += base[(int64_t)bq * stride];
+    s1 += base[(int64_t)(bq + 1) * stride];
+    s2 += base[(int64_t)(bq + 2) * stride];
+    s3 += base[(int64_t)(bq + 3) * stride];
+  }
+  for (; bq < b1; ++bq) s0 += base[(int64_t)bq * stride];
+  return (s0 + s1) + (s2 + s3);
+}
+
 template <int R>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(64 * WU2_CH)
 k_wupdate2(float* __restrict__ W, int64_t m, int r, const double* __restrict__ Ppart, int nP,
            const double* __restrict__ Qpart, int nQ, float eps, double* __restrict__ Gpart) {
   constexpr int RB = (64 / R) > 0 ? (64 / R) : 1;
-  __shared__ double part[4][64];
+  __shared__ double part[WU2_CH][64];
   __shared__ double Qs[R * R];
   __shared__ double Ps[RB * R];
   __shared__ float Wn[RB][R];
@@ -751,16 +791,18 @@ k_wupdate2(float* __restrict__ W, int64_t m, int r, const double* __restrict__ P
   // Q = sum of partials
   for (int q0 = 0; q0 < rr; q0 += 64) {
     const int qe = q0 + e;
-    double s = 0.0;
+    double sum = 0.0;
     if (qe < rr) {
-      const int b0 = (int)((int64_t)nQ * c / 4), b1 = (int)((int64_t)nQ * (c + 1) / 4);
-      for (int bq = b0; bq < b1; ++bq) s += Qpart[(int64_t)bq * rr + qe];
+      const int b0 = (int)((int64_t)nQ * c / WU2_CH), b1 = (int)((int64_t)nQ * (c + 1) / WU2_CH);
+      sum = chunk_sum(Qpart + qe, rr, b0, b1);
     }
-    part[c][e] = s;
+    part[c][e] = sum;
     __syncthreads();
     if (c == 0 && qe < rr) {
-      int kk = qe / r, ll = qe % r;
-      Qs[kk * R + ll] = ((part[0][e] + part[1][e]) + part[2][e]) + part[3][e];
+      double tot = 0.0;
+#pragma unroll
+      for (int cc = 0; cc < WU2_CH; ++cc) tot += part[cc][e];
+      Qs[(qe / r) * R + (qe % r)] = tot;
     }
     __syncthreads();
   }
@@ -769,18 +811,19 @@ k_wupdate2(float* __restrict__ W, int64_t m, int r, const double* __restrict__ P
   const int rows = (int)min((int64_t)RB, m - i0);
   const int64_t mr = m * r;
   {
-    double s = 0.0;
+    double sum = 0.0;
     const bool ok = e < rows * r;
     if (ok) {
-      const int b0 = (int)((int64_t)nP * c / 4), b1 = (int)((int64_t)nP * (c + 1) / 4);
-      const int64_t off = i0 * r + e;
-      for (int bp = b0; bp < b1; ++bp) s += Ppart[(int64_t)bp * mr + off];
+      const int b0 = (int)((int64_t)nP * c / WU2_CH), b1 = (int)((int64_t)nP * (c + 1) / WU2_CH);
+      sum = chunk_sum(Ppart + i0 * r + e, mr, b0, b1);
     }
-    part[c][e] = s;
+    part[c][e] = sum;
     __syncthreads();
     if (c == 0 && ok) {
-      int ii = e / r, kk = e % r;
-      Ps[ii * R + kk] = ((part[0][e] + part[1][e]) + part[2][e]) + part[3][e];
+      double tot = 0.0;
+#pragma unroll
+      for (int cc = 0; cc < WU2_CH; ++cc) tot += part[cc][e];
+      Ps[(e / r) * R + (e % r)] = tot;
     }
     __syncthreads();
   }
@@ -796,11 +839,11 @@ k_wupdate2(float* __restrict__ W, int64_t m, int r, const double* __restrict__ P
           Wn[t][k] = 0.0f;
           continue;
         }
-        double d = 0.0;
+        double dd = 0.0;
 #pragma unroll
         for (int l = 0; l < R; ++l)
-          if (l < r) d += w[l] * Qs[l * R + k];
-        Wn[t][k] = (float)mu_quot(w[k], Ps[t * R + k], d, (double)eps);
+          if (l < r) dd += w[l] * Qs[l * R + k];
+        Wn[t][k] = (float)mu_quot(w[k], Ps[t * R + k], dd, (double)eps);
       }
       for (int k = 0; k < r; ++k) W[i * r + k] = Wn[t][k];
     } else {
@@ -809,11 +852,11 @@ k_wupdate2(float* __restrict__ W, int64_t m, int r, const double* __restrict__ P
     }
   }
   __syncthreads();
-  for (int q = t; q < rr; q += 256) {
-    const int k = q / r, l = q % r;
-    double s = 0.0;
-    for (int ii = 0; ii < RB; ++ii) s += (double)Wn[ii][k] * (double)Wn[ii][l];
-    Gpart[(int64_t)blockIdx.x * rr + q] = s;
+  for (int qq = t; qq < rr; qq += 64 * WU2_CH) {
+    const int k = qq / r, l = qq % r;
+    double sum = 0.0;
+    for (int ii = 0; ii < RB; ++ii) sum += (double)Wn[ii][k] * (double)Wn[ii][l];
+    Gpart[(int64_t)blockIdx.x * rr + qq] = sum;
   }
 }
 
@@ -834,8 +877,12 @@ bool fused_supported(int64_t m, int64_t n, int r, int64_t ldx, const void* X, co
 
 int fused_grid(int64_t m, int64_t n, int r, int num_sms) {
   (void)r;
-  int64_t ntiles = m <= 40 ? (n + BN - 1) / BN : (n + BNC - 1) / BNC;
-  return (int)(ntiles < num_sms ? ntiles : num_sms);
+  if (m <= 40) {
+    int64_t ntiles = (n + BN - 1) / BN;
+    return (int)(ntiles < num_sms ? ntiles : num_sms);
+  }
+  int64_t ntiles = (n + BNC - 1) / BNC;  // variant C: two CTAs per SM
+  return (int)(ntiles < 2 * num_sms ? ntiles : 2 * num_sms);
 }
 
 size_t fused_scratch_bytes(int64_t, int64_t, int, int) { return 0; }
@@ -846,18 +893,14 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
                          cudaStream_t st) {
   const int evict_first = ((double)m * (double)n * 4.0 > 48e6) ? 1 : 0;
   if (m > 40) {
-    const int U = (int)((m + 63) / 64);
+    const int MPc = m <= 128 ? 128 : 256;
     CUtensorMap mx, mh;
-    cudaError_t e = make_map(&mx, X, (uint64_t)n, (uint64_t)m, (uint64_t)ldx, (uint32_t)(64 * U));
+    cudaError_t e = make_map(&mx, X, (uint64_t)n, (uint64_t)m, (uint64_t)ldx, (uint32_t)MPc);
     if (e != cudaSuccess) return e;
     e = make_map(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u);
     if (e != cudaSuccess) return e;
-#define LC(UU) return launch_c<UU>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st)
-    if (U == 1) LC(1);
-    if (U == 2) LC(2);
-    if (U == 3) LC(3);
-    LC(4);
-#undef LC
+    if (MPc == 128) return launch_c<128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st);
+    return launch_c<256>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st);
   }
   const int ux = ux_for(m);
   CUtensorMap mx, mh;
@@ -894,7 +937,7 @@ int wupdate2_ctas(int64_t m, int r) {
 cudaError_t launch_wupdate2(float* W, int64_t m, int r, const double* Ppart, int nP, const double* Qpart, int nQ,
                             float eps, double* Gpart, cudaStream_t st) {
   const int grid = wupdate2_ctas(m, r);
-#define WU(RR) k_wupdate2<RR><<<grid, 256, 0, st>>>(W, m, r, Ppart, nP, Qpart, nQ, eps, Gpart)
+#define WU(RR) k_wupdate2<RR><<<grid, 64 * WU2_CH, 0, st>>>(W, m, r, Ppart, nP, Qpart, nQ, eps, Gpart)
   if (r <= 2) WU(2);
   else if (r <= 4) WU(4);
   else if (r <= 8) WU(8);

@@ -93,6 +93,21 @@ struct ntt_handle_s {
     double bytes;
   };
   std::vector<Rec> recs;
+  struct Acc {
+    int64_t n = 0;
+    double ms = 0.0, bytes = 0.0;
+  };
+  Acc acc[8][66];
+  // CUDA graph of the last ntt_decompose (replayed when the arguments repeat)
+  bool capturing = false;
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t gev_in = nullptr, gev_out = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<uint64_t> gkey;
+  std::vector<cudaEvent_t> gev_pool;
+  size_t gev_used = 0;
+  std::vector<Rec> grecs;
+  int64_t glaunches = 0;
 };
 
 namespace {
@@ -176,25 +191,53 @@ ntt_status ensure_host_part(ntt_handle h, size_t count) {
   return NTT_OK;
 }
 
+// Events live in two pools: eager launches use ev_pool (recycled by
+// ntt_profile_enable), launches captured into the decompose graph use gev_pool
+// (owned by the graph, re-recorded at every replay).
 int prof_begin(ntt_handle h) {
   if (!h->prof) return -1;
-  if (h->ev_used + 2 > h->ev_pool.size()) {
+  auto& pool = h->capturing ? h->gev_pool : h->ev_pool;
+  size_t& used = h->capturing ? h->gev_used : h->ev_used;
+  if (used + 2 > pool.size()) {
     for (int i = 0; i < 256; ++i) {
       cudaEvent_t e;
       if (cudaEventCreate(&e) != cudaSuccess) return -1;
-      h->ev_pool.push_back(e);
+      pool.push_back(e);
     }
   }
-  int i = (int)h->ev_used;
-  h->ev_used += 2;
-  cudaEventRecord(h->ev_pool[i], h->stream);
+  int i = (int)used;
+  used += 2;
+  // inside stream capture an event record must be EXTERNAL to become a real
+  // record node that re-records (and can be timed) at every graph replay
+  cudaEventRecordWithFlags(pool[i], h->stream, h->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
   return i;
 }
 
 void prof_end(ntt_handle h, int ev0, int cls, double bytes) {
   if (ev0 < 0) return;
-  cudaEventRecord(h->ev_pool[ev0 + 1], h->stream);
-  h->recs.push_back({cls, h->cur_step, ev0, bytes});
+  auto& pool = h->capturing ? h->gev_pool : h->ev_pool;
+  cudaEventRecordWithFlags(pool[ev0 + 1], h->stream, h->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
+  (h->capturing ? h->grecs : h->recs).push_back({cls, h->cur_step, ev0, bytes});
+}
+
+// Fold completed event pairs into the accumulators (stream must be synchronised).
+void prof_fold(ntt_handle h, std::vector<ntt_handle_s::Rec>& recs, std::vector<cudaEvent_t>& pool) {
+  for (const auto& r : recs) {
+    float t = 0.0f;
+    cudaError_t e = cudaEventElapsedTime(&t, pool[r.ev0], pool[r.ev0 + 1]);
+    if (e != cudaSuccess) {
+      static bool warned = false;
+      if (!warned && getenv("NTT_DEBUG")) fprintf(stderr, "ntt profile: cudaEventElapsedTime: %s\n", cudaGetErrorString(e));
+      warned = true;
+      cudaGetLastError();
+      continue;
+    }
+    int step = r.step < 0 ? 0 : (r.step > 65 ? 65 : r.step);
+    auto& a = h->acc[r.cls][step];
+    a.n += 1;
+    a.ms += t;
+    a.bytes += r.bytes;
+  }
 }
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
@@ -471,20 +514,31 @@ ntt_status contract_run(ntt_handle h, const TTShape& s, const ContractPlan& c, c
   return NTT_OK;
 }
 
-// Sum the error partials (fixed order), optionally all-reduce over ranks, return Eq. 3.
-ntt_status finish_error(ntt_handle h, const ContractPlan& c, char* scratch, bool allreduce, double* rel_err) {
+// Sum the error partials (fixed order), optionally all-reduce over ranks, and
+// copy (num, den) to the pinned host landing zone (ensure_host_part(h, 2) first).
+ntt_status finish_error_device(ntt_handle h, const ContractPlan& c, char* scratch, bool allreduce) {
   cudaStream_t cs = h->stream;
   double* part = reinterpret_cast<double*>(scratch + c.off_part);
   double* tot = part + 2 * c.grid;
-  PLAUNCH(h, 4, 0.0, launch_sum_partials(part, c.grid, 2, tot, cs));
+  PLAUNCH(h, 4, 0.0, launch_sum_pairs(part, c.grid, tot, cs));
   if (allreduce) NC(h, g_nccl.AllReduce(tot, tot, 2, ncclFloat64, ncclSum, h->comm, cs));
-  ntt_status st = ensure_host_part(h, 2);
-  if (st) return st;
   CU(h, cudaMemcpyAsync(h->host_part, tot, 2 * sizeof(double), cudaMemcpyDeviceToHost, cs));
-  CU(h, cudaStreamSynchronize(cs));
+  return NTT_OK;
+}
+
+// Eq. 3 from the landed (num, den); the stream must have been synchronised.
+ntt_status finish_error_host(ntt_handle h, double* rel_err) {
   if (h->host_part[1] == 0.0) return fail(h, NTT_ERR_DEGENERATE, "||ref||_F = 0");
   *rel_err = sqrt(h->host_part[0]) / sqrt(h->host_part[1]);
   return NTT_OK;
+}
+
+ntt_status finish_error(ntt_handle h, const ContractPlan& c, char* scratch, bool allreduce, double* rel_err) {
+  ntt_status st = ensure_host_part(h, 2);
+  if (st) return st;
+  if ((st = finish_error_device(h, c, scratch, allreduce))) return st;
+  CU(h, cudaStreamSynchronize(h->stream));
+  return finish_error_host(h, rel_err);
 }
 
 ntt_status contract_stream(ntt_handle h, const TTShape& s, const float* cores, float* out, float noise_amp,
@@ -591,6 +645,11 @@ ntt_status ntt_destroy(ntt_handle h) {
   if (h->host_part) cudaFreeHost(h->host_part);
   if (h->comm && g_nccl.loaded) g_nccl.CommDestroy(h->comm);
   for (auto e : h->ev_pool) cudaEventDestroy(e);
+  for (auto e : h->gev_pool) cudaEventDestroy(e);
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  if (h->gev_in) cudaEventDestroy(h->gev_in);
+  if (h->gev_out) cudaEventDestroy(h->gev_out);
+  if (h->gstream) cudaStreamDestroy(h->gstream);
   delete h;
   return NTT_OK;
 }
@@ -677,7 +736,7 @@ struct DecompPlan {
   int64_t hbuf[2];           // ping-pong H buffer sizes (floats)
   int64_t wmax;              // max m_l r_l
   size_t mu_bytes;
-  size_t off_h0, off_h1, off_w, off_mu, off_cores, off_err, bytes;
+  size_t off_h0, off_h1, off_w, off_mu, off_cores, off_err, off_gath, bytes;
   MuPlan mu[65];
   TTShape sl;        // local shape (last mode = local block) for the error pass
   ContractPlan cp;
@@ -721,7 +780,72 @@ void plan_decompose(const TTShape& s, int num_sms, int nranks, int rank, DecompP
   P->cp = plan_contract(P->sl, num_sms);
   P->off_err = o;
   o = align_up(o + P->cp.bytes);
+  P->off_gath = o;  // last-core all-gather staging (distributed)
+  o = align_up(o + sizeof(float) * (size_t)(s.r[s.d - 1] * s.dims[s.d - 1]));
   P->bytes = o;
+}
+
+// All device work of one ntt_decompose, enqueued on h->stream (graph-capturable:
+// no allocation, no synchronisation, no host reads of device data).
+ntt_status decompose_device(ntt_handle h, const DecompPlan& P, const TTShape& s, const float* dA, float* dcores,
+                            char* ws, int32_t iters, uint64_t seed, float eps, bool want_err) {
+  ntt_status st;
+  cudaStream_t cs = h->stream;
+  const int d = s.d;
+  float* hb[2] = {reinterpret_cast<float*>(ws + P.off_h0), reinterpret_cast<float*>(ws + P.off_h1)};
+  float* Wd = reinterpret_cast<float*>(ws + P.off_w);
+  char* mus = ws + P.off_mu;
+  const float* X = dA;
+  float* Hl = nullptr;
+  for (int l = 1; l < d; ++l) {
+    const int64_t m = P.m[l], n = P.ncol[l];
+    const int r = (int)s.r[l];
+    Hl = hb[(l - 1) & 1];
+    h->cur_step = l;
+    LAUNCH(h, launch_fill_uniform(Wd, m * r, seed, stream_w(l), 0, cs));
+    if (h->nranks == 1) {
+      LAUNCH(h, launch_fill_uniform(Hl, (int64_t)r * n, seed, stream_h(l), 0, cs));
+    } else {
+      // global column index of local column c: (c / b) * n_d + off + c % b  (DESIGN.md s.7)
+      const int64_t nglob = n / P.nloc_last * s.dims[d - 1];
+      LAUNCH(h, launch_fill_uniform_cols(Hl, r, n, P.nloc_last, s.dims[d - 1], P.last_off, nglob, seed,
+                                         stream_h(l), cs));
+    }
+    if ((st = run_mu(h, P.mu[l], X, n, iters, eps, Wd, Hl, mus, nullptr))) return st;
+    CU(h, cudaMemcpyAsync(dcores + s.off[l], Wd, sizeof(float) * (size_t)(m * r), cudaMemcpyDeviceToDevice, cs));
+    X = Hl;
+  }
+  h->cur_step = d;  // last-core gather and the error pass
+  // last core G_d[k][i][0] = T_{d-1}[k][i]  (Alg. 2 l.11)
+  const int64_t rl = s.r[d - 1], nd = s.dims[d - 1];
+  if (h->nranks == 1) {
+    CU(h, cudaMemcpyAsync(dcores + s.off[d], Hl, sizeof(float) * (size_t)(rl * nd), cudaMemcpyDeviceToDevice, cs));
+  } else {
+    // all_gather of the ragged column blocks: one broadcast per rank into a
+    // rank-major staging area, then a permute into the core layout.
+    float* gath = reinterpret_cast<float*>(ws + P.off_gath);
+    NC(h, g_nccl.GroupStart());
+    for (int g = 0; g < h->nranks; ++g) {
+      int64_t og = 0;
+      int64_t bg = ntt_dist_block(nd, h->nranks, g, &og);
+      const float* src = (g == h->rank) ? Hl : gath + rl * og;
+      NC(h, g_nccl.Broadcast(src, gath + rl * og, (size_t)(rl * bg), ncclFloat32, g, h->comm, cs));
+    }
+    NC(h, g_nccl.GroupEnd());
+    LAUNCH(h, launch_gather_last_core(gath, rl, nd, h->nranks, dcores + s.off[d], cs));
+  }
+  if (want_err) {
+    // Eq. 3 of the result against (this rank's block of) A; the local train is
+    // cores 1..d-1 plus this rank's column block of the last core (= H_{d-1}).
+    char* es = ws + P.off_err;
+    float* lc = reinterpret_cast<float*>(es + P.cp.off_cores);
+    CU(h, cudaMemcpyAsync(lc, dcores, sizeof(float) * (size_t)s.off[d], cudaMemcpyDeviceToDevice, cs));
+    CU(h, cudaMemcpyAsync(lc + s.off[d], Hl, sizeof(float) * (size_t)(rl * P.nloc_last), cudaMemcpyDeviceToDevice, cs));
+    if ((st = contract_run(h, P.sl, P.cp, lc, nullptr, 0.0f, 0, dA, es))) return st;
+    if ((st = finish_error_device(h, P.cp, es, h->nranks > 1))) return st;
+  }
+  h->cur_step = 0;
+  return NTT_OK;
 }
 }  // namespace
 
@@ -767,74 +891,93 @@ ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t*
     if ((st = ensure_ws(h, P.bytes))) return st;
     ws = reinterpret_cast<char*>(h->ws);
   }
-  cudaStream_t cs = h->stream;
   const int64_t Nloc = s.N / s.dims[d - 1] * P.nloc_last;
   const float* dA = A;
   if (!is_device_ptr(A)) {
     if ((st = ensure_stage(h, sizeof(float) * (size_t)Nloc))) return st;
     dA = reinterpret_cast<const float*>(h->stage);
-    CU(h, cudaMemcpyAsync((void*)dA, A, sizeof(float) * (size_t)Nloc, cudaMemcpyHostToDevice, cs));
+    CU(h, cudaMemcpyAsync((void*)dA, A, sizeof(float) * (size_t)Nloc, cudaMemcpyHostToDevice, h->stream));
   }
   const bool cores_dev = is_device_ptr(cores);
   float* dcores = cores_dev ? cores : reinterpret_cast<float*>(ws + P.off_cores);
-  float* hb[2] = {reinterpret_cast<float*>(ws + P.off_h0), reinterpret_cast<float*>(ws + P.off_h1)};
-  float* Wd = reinterpret_cast<float*>(ws + P.off_w);
-  char* mus = ws + P.off_mu;
-  const float* X = dA;
-  float* Hl = nullptr;
-  for (int l = 1; l < d; ++l) {
-    const int64_t m = P.m[l], n = P.ncol[l];
-    const int r = (int)s.r[l];
-    Hl = hb[(l - 1) & 1];
-    h->cur_step = l;
-    LAUNCH(h, launch_fill_uniform(Wd, m * r, seed, stream_w(l), 0, cs));
-    if (h->nranks == 1) {
-      LAUNCH(h, launch_fill_uniform(Hl, (int64_t)r * n, seed, stream_h(l), 0, cs));
-    } else {
-      // global column index of local column c: (c / b) * n_d + off + c % b  (DESIGN.md s.7)
-      const int64_t nglob = n / P.nloc_last * s.dims[d - 1];
-      LAUNCH(h, launch_fill_uniform_cols(Hl, r, n, P.nloc_last, s.dims[d - 1], P.last_off, nglob, seed,
-                                         stream_h(l), cs));
-    }
-    if ((st = run_mu(h, P.mu[l], X, n, iters, eps, Wd, Hl, mus, nullptr))) return st;
-    CU(h, cudaMemcpyAsync(dcores + s.off[l], Wd, sizeof(float) * (size_t)(m * r), cudaMemcpyDeviceToDevice, cs));
-    X = Hl;
+  if (rel_err && (st = ensure_host_part(h, 2))) return st;
+
+  // ---- the device part: captured once into a CUDA graph and replayed while
+  // the arguments repeat (NTT_GRAPH=0 disables).  The graph runs on an internal
+  // stream ordered after / before the caller's stream by events.
+  static const bool graphs_on = [] {
+    const char* e = getenv("NTT_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  std::vector<uint64_t> key;
+  if (graphs_on) {
+    key = {(uint64_t)(uintptr_t)dA, (uint64_t)d, (uint64_t)iters, seed, (uint64_t)[](float f) { uint32_t u; memcpy(&u, &f, 4); return u; }(eps),
+           (uint64_t)(uintptr_t)dcores, (uint64_t)(uintptr_t)ws, (uint64_t)(rel_err != nullptr), (uint64_t)h->prof,
+           (uint64_t)(uintptr_t)h->host_part};
+    for (int l = 0; l < d; ++l) key.push_back((uint64_t)s.dims[l]);
+    for (int l = 1; l < d; ++l) key.push_back((uint64_t)s.r[l]);
   }
-  h->cur_step = d;  // last-core gather and the error pass
-  // last core G_d[k][i][0] = T_{d-1}[k][i]  (Alg. 2 l.11)
-  const int64_t rl = s.r[d - 1], nd = s.dims[d - 1];
-  if (h->nranks == 1) {
-    CU(h, cudaMemcpyAsync(dcores + s.off[d], Hl, sizeof(float) * (size_t)(rl * nd), cudaMemcpyDeviceToDevice, cs));
-  } else {
-    // all_gather of the ragged column blocks: one broadcast per rank into a
-    // staging area (rank-major), then a permute into the core layout.
-    float* gath = Wd;  // reuse: needs rl * nd floats <= wmax? not guaranteed -> use mu scratch
-    gath = reinterpret_cast<float*>(mus);
-    NC(h, g_nccl.GroupStart());
-    for (int g = 0; g < h->nranks; ++g) {
-      int64_t og = 0;
-      int64_t bg = ntt_dist_block(nd, h->nranks, g, &og);
-      const float* src = (g == h->rank) ? Hl : nullptr;
-      NC(h, g_nccl.Broadcast(src ? src : gath + rl * og, gath + rl * og, (size_t)(rl * bg), ncclFloat32, g, h->comm,
-                             cs));
+  cudaStream_t user = h->stream;
+  if (graphs_on) {
+    if (!h->gstream) {
+      CU(h, cudaStreamCreateWithFlags(&h->gstream, cudaStreamNonBlocking));
+      CU(h, cudaEventCreateWithFlags(&h->gev_in, cudaEventDisableTiming));
+      CU(h, cudaEventCreateWithFlags(&h->gev_out, cudaEventDisableTiming));
     }
-    NC(h, g_nccl.GroupEnd());
-    LAUNCH(h, launch_gather_last_core(gath, rl, nd, h->nranks, dcores + s.off[d], cs));
+    if (!h->gexec || key != h->gkey) {
+      if (h->gexec) {
+        CU(h, cudaStreamSynchronize(h->gstream));
+        cudaGraphExecDestroy(h->gexec);
+        h->gexec = nullptr;
+      }
+      h->gkey.clear();
+      h->grecs.clear();
+      h->gev_used = 0;
+      const int64_t l0 = h->launches;
+      h->stream = h->gstream;
+      h->capturing = true;
+      cudaError_t e0 = cudaStreamBeginCapture(h->gstream, cudaStreamCaptureModeThreadLocal);
+      ntt_status sd = (e0 == cudaSuccess) ? decompose_device(h, P, s, dA, dcores, ws, iters, seed, eps, rel_err != nullptr)
+                                          : NTT_ERR_CUDA;
+      cudaGraph_t graph = nullptr;
+      cudaError_t e1 = cudaStreamEndCapture(h->gstream, &graph);
+      h->capturing = false;
+      h->stream = user;
+      h->glaunches = h->launches - l0;
+      h->launches = l0;
+      if (e0 != cudaSuccess || sd != NTT_OK || e1 != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        if (sd != NTT_OK) return sd;
+        return fail(h, NTT_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(e0 != cudaSuccess ? e0 : e1));
+      }
+      cudaError_t e2 = cudaGraphInstantiate(&h->gexec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e2 != cudaSuccess) {
+        h->gexec = nullptr;
+        return fail(h, NTT_ERR_CUDA, "graph instantiate failed: %s", cudaGetErrorString(e2));
+      }
+      h->gkey = key;
+    }
+    CU(h, cudaEventRecord(h->gev_in, user));
+    CU(h, cudaStreamWaitEvent(h->gstream, h->gev_in, 0));
+    CU(h, cudaGraphLaunch(h->gexec, h->gstream));
+    CU(h, cudaEventRecord(h->gev_out, h->gstream));
+    CU(h, cudaStreamWaitEvent(user, h->gev_out, 0));
+    h->launches += h->glaunches;
+    if (h->prof) {
+      CU(h, cudaStreamSynchronize(h->gstream));
+      prof_fold(h, h->grecs, h->gev_pool);
+    }
+  } else {
+    if ((st = decompose_device(h, P, s, dA, dcores, ws, iters, seed, eps, rel_err != nullptr))) return st;
   }
   if (rel_err) {
-    // Eq. 3 of the result against (this rank's block of) A; the local train is
-    // cores 1..d-1 plus this rank's column block of the last core (= H_{d-1}).
-    char* es = ws + P.off_err;
-    float* lc = reinterpret_cast<float*>(es + P.cp.off_cores);
-    CU(h, cudaMemcpyAsync(lc, dcores, sizeof(float) * (size_t)s.off[d], cudaMemcpyDeviceToDevice, cs));
-    CU(h, cudaMemcpyAsync(lc + s.off[d], Hl, sizeof(float) * (size_t)(rl * P.nloc_last), cudaMemcpyDeviceToDevice, cs));
-    if ((st = contract_run(h, P.sl, P.cp, lc, nullptr, 0.0f, 0, dA, es))) return st;
-    if ((st = finish_error(h, P.cp, es, h->nranks > 1, rel_err))) return st;
+    CU(h, cudaStreamSynchronize(user));
+    if ((st = finish_error_host(h, rel_err))) return st;
   }
-  h->cur_step = 0;
   if (!cores_dev) {
-    CU(h, cudaMemcpyAsync(cores, dcores, sizeof(float) * (size_t)s.cores, cudaMemcpyDeviceToHost, cs));
-    CU(h, cudaStreamSynchronize(cs));
+    CU(h, cudaMemcpyAsync(cores, dcores, sizeof(float) * (size_t)s.cores, cudaMemcpyDeviceToHost, user));
+    CU(h, cudaStreamSynchronize(user));
   }
   return NTT_OK;
 }
@@ -879,9 +1022,18 @@ double ntt_compression_ratio(int32_t d, const int64_t* dims, const int32_t* rank
 ntt_status ntt_profile_enable(ntt_handle h, int enable) {
   if (!h) return NTT_ERR_INVALID_ARG;
   CU(h, cudaStreamSynchronize(h->stream));
+  if (h->gstream) CU(h, cudaStreamSynchronize(h->gstream));
+  if (h->prof != (enable != 0)) {
+    // the decompose graph records profile events only if captured with profiling on
+    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+    h->gkey.clear();
+  }
   h->prof = enable != 0;
   h->ev_used = 0;
   h->recs.clear();
+  for (auto& row : h->acc)
+    for (auto& a : row) a = ntt_handle_s::Acc();
   return NTT_OK;
 }
 
@@ -893,15 +1045,16 @@ ntt_status ntt_profile_get_step(ntt_handle h, int cls, int step, int64_t* launch
                                 double* total_bytes) {
   if (!h || cls < 0 || cls >= NTT_PROF_CLASSES) return NTT_ERR_INVALID_ARG;
   CU(h, cudaStreamSynchronize(h->stream));
+  prof_fold(h, h->recs, h->ev_pool);
+  h->recs.clear();
+  h->ev_used = 0;
   int64_t n = 0;
   double ms = 0.0, by = 0.0;
-  for (const auto& r : h->recs) {
-    if (r.cls != cls || (step >= 0 && r.step != step)) continue;
-    float t = 0.0f;
-    CU(h, cudaEventElapsedTime(&t, h->ev_pool[r.ev0], h->ev_pool[r.ev0 + 1]));
-    ++n;
-    ms += t;
-    by += r.bytes;
+  for (int l = 0; l < 66; ++l) {
+    if (step >= 0 && l != step) continue;
+    n += h->acc[cls][l].n;
+    ms += h->acc[cls][l].ms;
+    by += h->acc[cls][l].bytes;
   }
   if (launches) *launches = n;
   if (total_ms) *total_ms = ms;

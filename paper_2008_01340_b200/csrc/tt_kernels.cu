@@ -55,34 +55,96 @@ cudaError_t launch_contract_right(const float* G, int rp, int64_t nl, int rl, co
   return cudaGetLastError();
 }
 
-// Streaming kernel: CTA handles rows a of A~ (grid-stride), threads over b.
+// Streaming kernel.  Work item = (block of 32 rows a, block of 1024 columns b);
+// thread owns 4 consecutive columns, keeps R[:, b..b+3] in registers for the
+// whole row block (R is read from L2 once per 32 rows), L rows of the block are
+// staged in smem (broadcast).  A~ (and noise) are formed in fp32; ||ref - A~||^2
+// and ||ref||^2 per thread in fp32 over the 32 rows, then fp64 across items.
+// Persistent grid (<= 8 CTAs/SM) -> one fp64 (num, den) partial per CTA.
 constexpr int TS_THREADS = 256;
+constexpr int TS_RA = 32;
+constexpr int TS_CB = 4 * TS_THREADS;
 
 template <int RK>
 __global__ void __launch_bounds__(TS_THREADS)
 k_tt_stream(const float* __restrict__ L, const float* __restrict__ R, int64_t NL, int64_t NR, int rk,
             float* __restrict__ out, float noise_amp, uint64_t noise_key, const float* __restrict__ ref,
             double* __restrict__ err_part) {
+  __shared__ float Ls[TS_RA][RK];
   __shared__ double red[2][TS_THREADS / 32];
+  // 128-bit paths need NR % 4 == 0 and 16-byte aligned R, ref and out
+  const bool vec = ((NR & 3) == 0) && ((reinterpret_cast<uintptr_t>(R) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(ref) & 15) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  const int64_t ncb = (NR + TS_CB - 1) / TS_CB, nrb = (NL + TS_RA - 1) / TS_RA;
+  const int64_t items = ncb * nrb;
   double num = 0.0, den = 0.0;
-  const int64_t total = NL * NR;
-  for (int64_t t = (int64_t)blockIdx.x * TS_THREADS + threadIdx.x; t < total; t += (int64_t)gridDim.x * TS_THREADS) {
-    const int64_t a = t / NR, b = t - a * NR;
-    float s = 0.0f;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t cb = it % ncb, rbk = it / ncb;
+    const int64_t a0 = rbk * TS_RA;
+    const int rows = (int)min((int64_t)TS_RA, NL - a0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < TS_RA * RK; e += TS_THREADS) {
+      const int aa = e / RK, q = e % RK;
+      Ls[aa][q] = (aa < rows && q < rk) ? L[(a0 + aa) * rk + q] : 0.0f;
+    }
+    __syncthreads();
+    const int64_t b0 = cb * TS_CB + 4 * threadIdx.x;
+    if (b0 >= NR) continue;
+    const bool full4 = vec && (b0 + 3 < NR);
+    float rq[RK][4];
 #pragma unroll
-    for (int q = 0; q < RK; ++q)
-      if (q < rk) s = fmaf(L[a * rk + q], R[(int64_t)q * NR + b], s);
-    if (out) {
-      float v = s;
-      if (noise_amp != 0.0f) v = __fadd_rn(v, __fmul_rn(noise_amp, rng_uniform(noise_key, (uint64_t)t)));
-      out[t] = v;
+    for (int q = 0; q < RK; ++q) {
+      if (q < rk && full4) {
+        const float4 v = *reinterpret_cast<const float4*>(R + (int64_t)q * NR + b0);
+        rq[q][0] = v.x; rq[q][1] = v.y; rq[q][2] = v.z; rq[q][3] = v.w;
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) rq[q][t] = (q < rk && b0 + t < NR) ? R[(int64_t)q * NR + b0 + t] : 0.0f;
+      }
     }
-    if (ref) {
-      float x = ref[t];
-      double e = (double)x - (double)s;
-      num += e * e;
-      den += (double)x * (double)x;
+    float fnum = 0.0f, fden = 0.0f;
+    for (int aa = 0; aa < rows; ++aa) {
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int q = 0; q < RK; ++q) {
+        const float lq = Ls[aa][q];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) v[t] = fmaf(lq, rq[q][t], v[t]);
+      }
+      const int64_t base = (a0 + aa) * NR + b0;
+      if (out) {
+        float o[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          o[t] = (noise_amp != 0.0f) ? __fadd_rn(v[t], __fmul_rn(noise_amp, rng_uniform(noise_key, (uint64_t)(base + t))))
+                                     : v[t];
+        if (full4) {
+          *reinterpret_cast<float4*>(out + base) = make_float4(o[0], o[1], o[2], o[3]);
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (b0 + t < NR) out[base + t] = o[t];
+        }
+      }
+      if (ref) {
+        float x[4];
+        if (full4) {
+          const float4 xv = __ldcs(reinterpret_cast<const float4*>(ref + base));
+          x[0] = xv.x; x[1] = xv.y; x[2] = xv.z; x[3] = xv.w;
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) x[t] = (b0 + t < NR) ? ref[base + t] : 0.0f;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float e = x[t] - ((b0 + t < NR) ? v[t] : 0.0f);
+          fnum = fmaf(e, e, fnum);
+          fden = fmaf(x[t], x[t], fden);
+        }
+      }
     }
+    num += (double)fnum;
+    den += (double)fden;
   }
   if (ref) {
     num = warp_sum(num);
@@ -105,10 +167,9 @@ k_tt_stream(const float* __restrict__ L, const float* __restrict__ R, int64_t NL
 }
 
 int stream_ctas(int64_t NL, int64_t NR, int num_sms) {
-  int64_t total = NL * NR;
-  int64_t g = (total + TS_THREADS - 1) / TS_THREADS;
+  int64_t items = ((NR + TS_CB - 1) / TS_CB) * ((NL + TS_RA - 1) / TS_RA);
   int64_t cap = (int64_t)num_sms * 8;
-  return (int)(g > cap ? cap : (g < 1 ? 1 : g));
+  return (int)(items > cap ? cap : (items < 1 ? 1 : items));
 }
 
 cudaError_t launch_tt_stream(const float* L, const float* R, int64_t NL, int64_t NR, int rk, float* out,
@@ -123,6 +184,36 @@ cudaError_t launch_tt_stream(const float* L, const float* R, int64_t NL, int64_t
   else if (rk <= 32) TS(32);
   else TS(64);
 #undef TS
+  return cudaGetLastError();
+}
+
+// Fixed-order sum of npart (num, den) pairs by one CTA: thread t sums pairs
+// t, t+256, ... in order, then a fixed tree in smem.
+__global__ void __launch_bounds__(256) k_sum_pairs(const double* __restrict__ part, int npart, double* __restrict__ out) {
+  __shared__ double sn[256], sd[256];
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < npart; i += 256) {
+    a += part[2 * i];
+    b += part[2 * i + 1];
+  }
+  sn[threadIdx.x] = a;
+  sd[threadIdx.x] = b;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      sn[threadIdx.x] += sn[threadIdx.x + w];
+      sd[threadIdx.x] += sd[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = sn[0];
+    out[1] = sd[0];
+  }
+}
+
+cudaError_t launch_sum_pairs(const double* part, int npart, double* out, cudaStream_t st) {
+  k_sum_pairs<<<1, 256, 0, st>>>(part, npart, out);
   return cudaGetLastError();
 }
 

@@ -270,7 +270,8 @@ def test_decompose_host_pointers_and_workspace(h, ora):
 
 # ---------------------------------------------------- reconstruct / generate --
 @pytest.mark.parametrize("dims,ranks", [([5, 4, 5, 6], [4, 3, 2]), ([3, 7], [2]), ([4] * 6, [3, 5, 2, 4, 3]),
-                                        ([9, 1, 5, 2], [2, 2, 2])])
+                                        ([9, 1, 5, 2], [2, 2, 2]), ([3, 4], [2]), ([5, 8], [3]), ([7, 3, 16], [2, 3]),
+                                        ([64, 64, 64], [5, 7])])
 def test_reconstruct_parity(h, ora, dims, ranks):
     cores = ni.make_cores(dims, ranks, seed=2).astype(np.float32)
     out = torch.empty(int(np.prod(dims)), dtype=torch.float32, device="cuda")
