@@ -1,0 +1,56 @@
+"""The library's NCCL path (ntt_create_dist) on one GPU (a 1-rank communicator):
+exercises the per-pass all-reduce of the fp64 partials, the global-index H init
+and the last-core gather.  Results must match the single-GPU handle and the
+oracle (parity tolerances of test_gpu_parity)."""
+import numpy as np
+import pytest
+
+import ntt_inputs as ni
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def handles():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2008_01340_b200 as P
+    uid = P.ntt_get_unique_id()
+    hd = P.Handle(0, unique_id=uid, nranks=1, rank=0)
+    assert hd.size == 1 and hd.rank == 0
+    return P.Handle(0), hd
+
+
+@pytest.mark.parametrize("dims,ranks,iters", [([5, 4, 5, 6], [4, 3, 2], 10), ([16, 16, 16, 16], [8, 8, 8], 10),
+                                              ([6] * 6, [5] * 5, 10), ([64, 32, 64], [8, 8], 5)])
+def test_dist_handle_decompose_matches(handles, ora, dims, ranks, iters):
+    h1, hd = handles
+    A = ora.tt_full_f32(dims, ranks, ni.make_cores(dims, ranks, 0), noise_amp=0.3, seed=0)
+    Ad = torch.from_numpy(A).cuda()
+    c1 = torch.empty(ora.cores_size(dims, ranks), device="cuda")
+    cd = torch.empty_like(c1)
+    e1 = h1.ntt_decompose(Ad, dims, ranks, iters, 0, 1e-16, c1, want_error=True)
+    ed = hd.ntt_decompose(Ad, dims, ranks, iters, 0, 1e-16, cd, want_error=True)
+    torch.cuda.synchronize()
+    a, b = c1.cpu().numpy().astype(np.float64), cd.cpu().numpy().astype(np.float64)
+    assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(a)
+    ref = ora.ntt_decompose(A, ranks, iters, seed=0)
+    assert np.linalg.norm(b - ref) <= 1e-4 * np.linalg.norm(ref)
+    assert abs(ed - e1) <= 1e-5 * e1
+
+
+@pytest.mark.parametrize("m,n,r", [(32, 4096, 8), (256, 2048, 8), (100, 700, 16)])
+def test_dist_handle_nmf_mu(handles, ora, m, n, r):
+    h1, hd = handles
+    rng = np.random.default_rng(1)
+    X = rng.random((m, n)).astype(np.float32)
+    W0 = ni.uniform(m * r, 1, 0x202).reshape(m, r).astype(np.float32)
+    H0 = ni.uniform(r * n, 1, 0x203).reshape(r, n).astype(np.float32)
+    Xd = torch.from_numpy(X).cuda()
+    Wd, Hd = torch.from_numpy(W0.copy()).cuda(), torch.from_numpy(H0.copy()).cuda()
+    hd.ntt_nmf_mu(Xd, m, n, n, r, 8, 1e-16, Wd, Hd)
+    Wo, Ho = ora.nmf_mu(X, W0.astype(np.float64), H0.astype(np.float64), 8)
+    W, H = Wd.cpu().numpy(), Hd.cpu().numpy()
+    assert np.linalg.norm(W - Wo) <= 1e-4 * np.linalg.norm(Wo)
+    assert np.linalg.norm(H - Ho) <= 1e-4 * np.linalg.norm(Ho)
