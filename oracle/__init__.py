@@ -72,6 +72,7 @@ def lib():
             "ora_rel_error": (_d, [_p, _p, _i64]),
             "ora_compression_ratio": (_d, [ctypes.c_int, _p, _p]),
             "ora_tt_rel_error_f32": (_d, [ctypes.c_int, _p, _p, _p, _p]),
+            "ora_tt_rel_error_split_f32": (_d, [ctypes.c_int, _p, _p, _p, _p, ctypes.c_int]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -319,6 +320,19 @@ def tt_rel_error(A: np.ndarray, ranks, cores: np.ndarray) -> float:
     D, R = _dims(A.shape), _ranks(ranks)
     C = np.ascontiguousarray(cores, dtype=np.float64)
     return float(lib().ora_tt_rel_error_f32(len(D), _ptr(D), _ptr(R), _ptr(C), _ptr(A)))
+
+
+def tt_rel_error_split(A: np.ndarray, ranks, cores: np.ndarray, k: Optional[int] = None) -> float:
+    """Eq. 3 with the reconstruction formed on the fly from Eq. 1 split at bond k
+    (A~ = L_k R_k, fp64): the full-size evaluation (8 FMAs per element at r_k = 8)."""
+    A = np.ascontiguousarray(A, dtype=np.float32)
+    D, R = _dims(A.shape), _ranks(ranks)
+    C = np.ascontiguousarray(cores, dtype=np.float64)
+    kk = len(D) // 2 if k is None else k
+    v = float(lib().ora_tt_rel_error_split_f32(len(D), _ptr(D), _ptr(R), _ptr(C), _ptr(A), kk))
+    if v < -1.5:
+        raise OracleError("tt_rel_error_split failed")
+    return v
 
 
 def compression_ratio(dims, ranks) -> float:

@@ -164,30 +164,23 @@ int ora_tt_full(int d, const int64_t* dims, const int32_t* inner,
     return ORA_OK;
 }
 
-/* Same contraction, rounded once to fp32 (synthetic inputs are fp32; P:304-305)
- * plus optional additive noise amp*u(seed, noise_stream, flat index) added in
- * fp64 before rounding (reading R12).                                        */
-int ora_tt_full_f32(int d, const int64_t* dims, const int32_t* inner,
-                    const double* cores, double noise_amp, uint64_t seed,
-                    uint64_t noise_stream, float* out) {
-    int64_t N = 1;
-    for (int l = 0; l < d; ++l) N *= dims[l];
+/* Eq. 1 split at bond k (1 <= k < d): A[a, b] = sum_q L[a, q] R[q, b] with
+ * L = G_1 o ... o G_k as (n_1..n_k) x r_k and R = G_{k+1} o ... o G_d as
+ * r_k x (n_{k+1}..n_d), each contracted left to right by ora_tt_full on a
+ * sub-train closed with an identity core.  Caller frees *L and *R.            */
+static int split_LR(int d, const int64_t* dims, const int32_t* inner, const double* cores, int k,
+                    double** Lout, double** Rout, int64_t* NLout, int64_t* NRout, int64_t* rkout) {
     int64_t r[65];
     full_ranks(d, inner, r);
-    if (d < 2) return ORA_ERR_ARG;
-    /* split at the middle bond: A[a, b] = sum_k L[a,k] R[k,b]. L = G1..Gk
-     * (left-to-right), R = G_{k+1}..G_d; both via ora_tt_full on sub-trains. */
-    int k = d / 2;
     int64_t NL = 1, NR = 1;
     for (int l = 0; l < k; ++l) NL *= dims[l];
     for (int l = k; l < d; ++l) NR *= dims[l];
     int64_t rk = r[k];
-    /* left sub-train with trailing rank rk: treat as d'=k+1 train with an
-     * identity last core of shape rk x rk x 1 -> gives L as (NL*rk) vector. */
     double* L = (double*)malloc(sizeof(double) * (size_t)(NL * rk));
     double* R = (double*)malloc(sizeof(double) * (size_t)(rk * NR));
     if (!L || !R) { free(L); free(R); return ORA_ERR_NOMEM; }
     {
+        /* left sub-train: G_1..G_k followed by an identity core rk x rk x 1 */
         int64_t o_end = ora_core_offset(d, dims, inner, k + 1);
         int64_t dl[65];
         int32_t il[65];
@@ -205,7 +198,7 @@ int ora_tt_full_f32(int d, const int64_t* dims, const int32_t* inner,
         if (rc) { free(L); free(R); return rc; }
     }
     {
-        /* right sub-train: identity first core 1 x rk x rk, then G_{k+1}.. */
+        /* right sub-train: an identity core 1 x rk x rk followed by G_{k+1}..G_d */
         int64_t o_beg = ora_core_offset(d, dims, inner, k + 1);
         int64_t o_end = ora_core_offset(d, dims, inner, d) + r[d - 1] * dims[d - 1];
         int64_t dr[65];
@@ -222,6 +215,25 @@ int ora_tt_full_f32(int d, const int64_t* dims, const int32_t* inner,
         free(cr);
         if (rc) { free(L); free(R); return rc; }
     }
+    *Lout = L;
+    *Rout = R;
+    *NLout = NL;
+    *NRout = NR;
+    *rkout = rk;
+    return ORA_OK;
+}
+
+/* Same contraction, rounded once to fp32 (synthetic inputs are fp32; P:304-305)
+ * plus optional additive noise amp*u(seed, noise_stream, flat index) added in
+ * fp64 before rounding (reading R12).  Split at the middle bond k = d/2.      */
+int ora_tt_full_f32(int d, const int64_t* dims, const int32_t* inner,
+                    const double* cores, double noise_amp, uint64_t seed,
+                    uint64_t noise_stream, float* out) {
+    if (d < 2 || d > 64) return ORA_ERR_ARG;
+    double *L, *R;
+    int64_t NL, NR, rk;
+    int rc = split_LR(d, dims, inner, cores, d / 2, &L, &R, &NL, &NR, &rk);
+    if (rc) return rc;
 #pragma omp parallel for schedule(static)
     for (int64_t a = 0; a < NL; ++a)
         for (int64_t b = 0; b < NR; ++b) {
@@ -234,6 +246,39 @@ int ora_tt_full_f32(int d, const int64_t* dims, const int32_t* inner,
     free(L);
     free(R);
     return ORA_OK;
+}
+
+/* Eq. 3 of a TT against fp32 A, the reconstruction formed on the fly
+ * from the bond-k split (fp64, direct differences).  Row sums of A-blocks are
+ * accumulated per row a in order, rows summed in order: a fixed order.
+ * Returns -1 if ||A|| = 0, -2 on allocation failure.                          */
+double ora_tt_rel_error_split_f32(int d, const int64_t* dims, const int32_t* inner, const double* cores,
+                                  const float* A, int k) {
+    if (d < 2 || d > 64 || k < 1 || k >= d) return -3.0;
+    double *L, *R;
+    int64_t NL, NR, rk;
+    if (split_LR(d, dims, inner, cores, k, &L, &R, &NL, &NR, &rk)) return -2.0;
+    double* rn = (double*)malloc(sizeof(double) * (size_t)NL);
+    double* rd = (double*)malloc(sizeof(double) * (size_t)NL);
+    if (!rn || !rd) { free(L); free(R); free(rn); free(rd); return -2.0; }
+#pragma omp parallel for schedule(static)
+    for (int64_t a = 0; a < NL; ++a) {
+        double num = 0.0, den = 0.0;
+        for (int64_t b = 0; b < NR; ++b) {
+            double s = 0.0;
+            for (int64_t q = 0; q < rk; ++q) s += L[a * rk + q] * R[q * NR + b];
+            double x = (double)A[a * NR + b], e = x - s;
+            num += e * e;
+            den += x * x;
+        }
+        rn[a] = num;
+        rd[a] = den;
+    }
+    double num = 0.0, den = 0.0;
+    for (int64_t a = 0; a < NL; ++a) { num += rn[a]; den += rd[a]; }
+    free(L); free(R); free(rn); free(rd);
+    if (den == 0.0) return -1.0;
+    return sqrt(num) / sqrt(den);
 }
 
 /* ------------------------------------------------------------------------ */

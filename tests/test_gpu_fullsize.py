@@ -1,0 +1,122 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (same kernels, same grids), on outputs the oracle can compute: exact first
+MU iteration of config 3 step 1 (W everywhere, H at sampled columns), the full
+config-3 decomposition's Eq. 3 error re-evaluated by the oracle on the GPU's
+cores, config 4 at 10 iterations per step, config 2 at 10 iterations, and a
+config-5 slice at 10 iterations (2-pass path, r = 32).
+
+Tolerances: DESIGN.md readings R14 / R15 (1e-4 on factors, 1e-3 on errors).
+"""
+import numpy as np
+import pytest
+
+import ntt_inputs as ni
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def h():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2008_01340_b200 as P
+    return P.Handle(0)
+
+
+@pytest.fixture(scope="module")
+def config3_A():
+    import oracle
+    w = ni.workloads()["config3"]
+    A = oracle.tt_full_f32(w.dims, w.ranks, ni.make_cores(w.dims, w.ranks, w.seed), noise_amp=w.noise_amp,
+                           seed=w.seed)
+    return w, A
+
+
+def _rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.linalg.norm(a - b) / np.linalg.norm(b), np.abs(a - b).max() / np.abs(b).max()
+
+
+def test_config3_step1_first_iteration_exact(h, ora, config3_A):
+    w, A = config3_A
+    m, n, r = 32, 32 ** 5, 8
+    X = A.reshape(m, n)
+    Xd = torch.from_numpy(X).cuda()
+    Wd = torch.empty(m * r, device="cuda")
+    Hd = torch.empty(r * n, device="cuda")
+    h.ntt_fill_uniform(Wd, m * r, w.seed, ni.stream_w(1))
+    h.ntt_fill_uniform(Hd, r * n, w.seed, ni.stream_h(1))
+    h.ntt_nmf_mu(Xd, m, n, n, r, 1, 1e-16, Wd, Hd)  # fused 1-pass path, bench grid
+    torch.cuda.synchronize()
+    W0 = ni.uniform(m * r, w.seed, ni.stream_w(1)).reshape(m, r)
+    H0 = ni.uniform(r * n, w.seed, ni.stream_h(1)).reshape(r, n)
+    P = ora.xht(X, H0)
+    Q = ora.gram_rows(H0)
+    W1 = ora.w_update(W0, P, Q, 1e-16)
+    fro, mx = _rel(Wd.cpu().numpy().reshape(m, r), W1)
+    assert fro <= TOL and mx <= TOL, (fro, mx)
+    G = ora.gram_cols(W1)
+    rng = np.random.default_rng(0)
+    cols = np.unique(np.concatenate([rng.integers(0, n, 4096), np.arange(n - 300, n), np.arange(0, 300)]))
+    S = ora.wtx_cols(W1, X, cols)
+    H1 = ora.h_update_cols(H0[:, cols], S, G, 1e-16)
+    got = Hd.cpu().numpy().reshape(r, n)[:, cols]
+    fro, mx = _rel(got, H1)
+    assert fro <= TOL and mx <= TOL, (fro, mx)
+
+
+def test_config3_full_decomposition_error(h, ora, config3_A):
+    w, A = config3_A
+    Ad = torch.from_numpy(A.ravel()).cuda()
+    cores = torch.empty(ora.cores_size(w.dims, w.ranks), device="cuda")
+    e_gpu = h.ntt_decompose(Ad, w.dims, w.ranks, w.iters, w.seed, 1e-16, cores, want_error=True)
+    c = cores.cpu().numpy()
+    assert np.all(np.isfinite(c)) and np.all(c >= 0)
+    e_ora = ora.tt_rel_error_split(A, w.ranks, c.astype(np.float64))
+    assert abs(e_gpu - e_ora) <= 1e-3 * e_ora + 1e-6, (e_gpu, e_ora)
+    # noise of amplitude 0.01 * mean: the fit cannot be worse than the noise floor by much
+    assert 0.0 < e_gpu < 0.1
+
+
+def test_config4_ten_iterations_per_step(h, ora):
+    w = ni.workloads()["config4"]
+    A = ora.tt_full_f32(w.dims, w.ranks, ni.make_cores(w.dims, w.ranks, w.seed))
+    cores = torch.empty(ora.cores_size(w.dims, w.ranks), device="cuda")
+    e_gpu = h.ntt_decompose(torch.from_numpy(A.ravel()).cuda(), w.dims, w.ranks, 10, w.seed, 1e-16, cores,
+                            want_error=True)
+    ref = ora.ntt_decompose(A, w.ranks, 10, seed=w.seed)
+    got = cores.cpu().numpy()
+    for l, (g, o) in enumerate(zip(ora.unpack_cores(w.dims, w.ranks, got), ora.unpack_cores(w.dims, w.ranks, ref))):
+        fro, mx = _rel(g, o)
+        assert fro <= TOL and mx <= TOL, (l, fro, mx)
+    e_ora = ora.tt_rel_error_split(A, w.ranks, ref)
+    assert abs(e_gpu - e_ora) <= 1e-3 * e_ora + 1e-6
+
+
+def _factor_input(m, n, r, noise, seed=0):
+    import oracle
+    dims, ranks, cores = ni.make_factor_cores(m, n, r, seed)
+    if noise == "absnormal":
+        X = oracle.tt_full(dims, ranks, cores) + 0.01 * ni.abs_normal(m * n, seed).reshape(m, n)
+        return X.astype(np.float32)
+    return oracle.tt_full_f32(dims, ranks, cores, noise_amp=0.08, seed=seed)
+
+
+@pytest.mark.parametrize("cfg", ["config2", "config5slice"])
+def test_single_nmf_configs_ten_iterations(h, ora, cfg):
+    if cfg == "config2":
+        m, n, r, X = 4096, 4096, 16, _factor_input(4096, 4096, 16, "absnormal")
+    else:
+        m, n, r = 4096, 8192, 32   # config 5's parity slice (SURVEY s.8(d).2)
+        X = _factor_input(m, n, r, "uniform")
+    W0 = ni.uniform(m * r, 0, ni.stream_w(1)).reshape(m, r).astype(np.float32)
+    H0 = ni.uniform(r * n, 0, ni.stream_h(1)).reshape(r, n).astype(np.float32)
+    Wd, Hd = torch.from_numpy(W0.copy()).cuda(), torch.from_numpy(H0.copy()).cuda()
+    h.ntt_nmf_mu(torch.from_numpy(X).cuda(), m, n, n, r, 10, 1e-16, Wd, Hd)
+    Wo, Ho = ora.nmf_mu(X, W0.astype(np.float64), H0.astype(np.float64), 10)
+    for got, ref, nm in ((Wd, Wo, "W"), (Hd, Ho, "H")):
+        fro, mx = _rel(got.cpu().numpy().reshape(ref.shape), ref)
+        assert fro <= TOL and mx <= TOL, (nm, fro, mx)

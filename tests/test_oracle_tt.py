@@ -126,6 +126,14 @@ def test_tt_rel_error_matches_materialised(ora):
     assert ora.rel_error(A, B) == pytest.approx(direct, rel=1e-12)
 
 
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_tt_rel_error_split_matches(ora, k):
+    dims, ranks = [5, 4, 5, 6], [4, 3, 2]
+    A = ora.tt_full_f32(dims, ranks, ni.make_cores(dims, ranks, seed=0), noise_amp=0.3, seed=1)
+    cores2 = ni.make_cores(dims, ranks, seed=5)
+    assert ora.tt_rel_error_split(A, ranks, cores2, k) == pytest.approx(ora.tt_rel_error(A, ranks, cores2), rel=1e-12)
+
+
 def test_core_offsets(ora):
     dims, ranks = [6] * 10, [5] * 9
     assert ora.core_offset(dims, ranks, 1) == 0
