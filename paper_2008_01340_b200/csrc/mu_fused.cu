@@ -20,6 +20,7 @@
 // fixed-order CTA reduction into per-CTA fp64 partials (deterministic).
 #include <cuda.h>
 #include <cstdio>
+#include <cstdlib>
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -702,6 +703,327 @@ cudaError_t launch_c(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_
   return cudaGetLastError();
 }
 
+// ===========================================================================
+// Variant WC: warp-owned 32-column tiles for 40 < m <= 256 (rank padded to 8),
+// no CTA barriers in the loop.  6 consumer warps (<= 2 per SMSP, 255 regs) + 1
+// TMA warp; each warp owns `dpw` ring stages (stage = tile's warp * dpw +
+// round % dpw), so every warp waits only on rounds it consumed itself.
+//   phase A  lanes (q: columns 4q..4q+3, g: ranks 2g, 2g+1) stream all MP rows:
+//            X by 128-bit loads, W as row pairs (one 128-bit broadcast per 2 rows)
+//   H update lane forms E = G H and Hn for its 2 ranks x 4 columns; 128-bit
+//            coalesced stores; Hn into the warp's transposed smem tile
+//   phase B  32-row chunks, lanes (rb, cs: 8-column slice), reduce-scatter over
+//            the slices, per-lane fp32 accumulators for ALL rows (8 values per
+//            chunk) flushed every 32 tiles into the warp's private fp64 global
+//            partial (no atomics: deterministic); Q = Hn Hn^T likewise.
+// ===========================================================================
+constexpr int NWW = 6;
+constexpr int NTW = (NWW + 1) * 32;
+constexpr int WC_FLUSH = 32;
+
+template <int MP>
+__global__ void __launch_bounds__(NTW, 1)
+k_fused_wc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmH, int m, int64_t n, int r,
+           const float* __restrict__ W, const double* __restrict__ Gpart, int nG, float eps, float* __restrict__ H,
+           double* __restrict__ Ppart, double* __restrict__ Qpart, int mode, int dpw, int evict_first) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  constexpr int NCH = MP / 32;
+  constexpr uint32_t XB = MP * 128u;
+  constexpr uint32_t SB = XB + 1024u;
+  const int ns = NWW * dpw;
+  unsigned char* stages = smem;
+  float* Wp = reinterpret_cast<float*>(smem + (size_t)ns * SB);  // [MP/2][4 g][4]: W row pairs
+  float* Gs = Wp + MP * 8;                                         // 8 x 8
+  float* HnAll = Gs + 64;                                          // NWW x HNC_FLOATS
+  uint64_t* full = reinterpret_cast<uint64_t*>(HnAll + NWW * HNC_FLOATS);
+  uint64_t* empty = full + ns;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool do_update = (mode & kFusedUpdate) != 0;
+  const bool do_acc = (mode & kFusedAcc) != 0;
+  if (do_update) {
+    const int rr = r * r;
+    for (int e = tid; e < 64; e += NTW) {
+      int k = e >> 3, l = e & 7;
+      double sum = 0.0;
+      if (k < r && l < r)
+        for (int bq = 0; bq < nG; ++bq) sum += Gpart[(int64_t)bq * rr + k * r + l];
+      Gs[e] = (float)sum;
+    }
+  }
+  for (int e = tid; e < MP * 8; e += NTW) {
+    // Wp[(i/2)*16 + g*4 + (i&1)*2 + t] = W[i][2g + t]
+    const int ip = e >> 4, g = (e >> 2) & 3, w2 = e & 3;
+    const int i = 2 * ip + (w2 >> 1), k = 2 * g + (w2 & 1);
+    Wp[e] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < ns; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int64_t ntiles = (n + BNC - 1) / BNC;
+  const int64_t b = blockIdx.x;
+  const int64_t J = (ntiles > b) ? (ntiles - b + gridDim.x - 1) / gridDim.x : 0;
+
+  if (warp == NWW) {
+    if (lane == 0) {
+      uint64_t policy;
+      if (evict_first)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+      else
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
+      for (int64_t j = 0; j < J; ++j) {
+        const int64_t rnd = j / NWW;
+        const int s = (int)(j % NWW) * dpw + (int)(rnd % dpw);
+        const uint32_t ph = (uint32_t)((rnd / dpw) & 1);
+        MBAR_WAIT(&empty[s], ph ^ 1u, 5, j);
+        mbar_expect_tx(&full[s], SB);
+        const int col0 = (int)((b + j * gridDim.x) * BNC);
+        unsigned char* st = stages + (size_t)s * SB;
+        tma_load_2d(st, &tmX, col0, 0, &full[s], policy);
+        tma_load_2d(st + XB, &tmH, col0, 0, &full[s], policy);
+      }
+    }
+    return;
+  }
+
+  float* Hw = HnAll + warp * HNC_FLOATS;
+  const int q = lane & 7, g = lane >> 3;    // phase A / H update
+  const int rb = lane & 7, cs = lane >> 3;  // phase B
+  const bool h1 = (lane >> 4) & 1, h0 = (lane >> 3) & 1;
+  float accf[NCH][8];
+  float qf[8];
+#pragma unroll
+  for (int h = 0; h < NCH; ++h)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) accf[h][v] = 0.f;
+#pragma unroll
+  for (int v = 0; v < 8; ++v) qf[v] = 0.f;
+  const int mr = m * r, rr = r * r;
+  const int64_t slot = b * NWW + warp;  // this warp's private partial
+  int nflush = 0, since = 0;
+  // flush the fp32 accumulators into the warp's fp64 partial (first flush writes)
+  auto flush = [&]() {
+#pragma unroll
+    for (int h = 0; h < NCH; ++h)
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const int f = 8 * cs + v;  // flat u*8 + k within the chunk
+        const int u = f >> 3, k = f & 7;
+        const int row = 32 * h + rb + 8 * u;
+        if (row < m && k < r) {
+          double* dst = Ppart + slot * mr + row * r + k;
+          *dst = (nflush ? *dst : 0.0) + (double)accf[h][v];
+        }
+        accf[h][v] = 0.f;
+      }
+    // Q[rb][l]: sum the 4 column-slice lanes
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      float t = qf[v];
+      t += __shfl_xor_sync(0xffffffffu, t, 16);
+      t += __shfl_xor_sync(0xffffffffu, t, 8);
+      if (cs == 0 && rb < r && v < r) {
+        double* dst = Qpart + slot * rr + rb * r + v;
+        *dst = (nflush ? *dst : 0.0) + (double)t;
+      }
+      qf[v] = 0.f;
+    }
+    ++nflush;
+    since = 0;
+  };
+
+  for (int64_t j = warp; j < J; j += NWW) {
+    const int64_t rnd = j / NWW;
+    const int s = warp * dpw + (int)(rnd % dpw);
+    const uint32_t ph = (uint32_t)((rnd / dpw) & 1);
+    MBAR_WAIT(&full[s], ph, 6, j);
+    const unsigned char* st = stages + (size_t)s * SB;
+    const int64_t jt = (b + j * gridDim.x) * BNC;
+    const int64_t c0 = jt + 4 * q;
+
+    // ---- phase A + H update (lane: ranks 2g, 2g+1 x columns 4q..4q+3)
+    // (rows 2g, 2g+1 of the H tile are loaded separately: indexing the hv
+    //  register array with the lane-dependent g would spill it to local memory)
+    float hk[2][4];
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      const int k = 2 * g + kk;
+      const float4 t4 = lds128(st + XB + k * 128 + ((q ^ k) << 4));
+      hk[kk][0] = t4.x; hk[kk][1] = t4.y; hk[kk][2] = t4.z; hk[kk][3] = t4.w;
+    }
+    float hn[2][4];
+    if (do_update) {
+      float2 sa = f2(0.f, 0.f), sb = f2(0.f, 0.f), sc = f2(0.f, 0.f), sd = f2(0.f, 0.f);
+#pragma unroll 4
+      for (int ip = 0; ip < MP / 2; ++ip) {
+        const int i = 2 * ip;
+        const float4 x0 = lds128(st + i * 128 + ((q ^ (i & 7)) << 4));
+        const float4 x1 = lds128(st + (i + 1) * 128 + ((q ^ ((i + 1) & 7)) << 4));
+        const float4 wv = *reinterpret_cast<const float4*>(Wp + ip * 16 + g * 4);
+        sa = __ffma2_rn(bc(wv.x), f2(x0.x, x0.y), sa);
+        sb = __ffma2_rn(bc(wv.x), f2(x0.z, x0.w), sb);
+        sc = __ffma2_rn(bc(wv.y), f2(x0.x, x0.y), sc);
+        sd = __ffma2_rn(bc(wv.y), f2(x0.z, x0.w), sd);
+        sa = __ffma2_rn(bc(wv.z), f2(x1.x, x1.y), sa);
+        sb = __ffma2_rn(bc(wv.z), f2(x1.z, x1.w), sb);
+        sc = __ffma2_rn(bc(wv.w), f2(x1.x, x1.y), sc);
+        sd = __ffma2_rn(bc(wv.w), f2(x1.z, x1.w), sd);
+      }
+      const float S[2][4] = {{sa.x, sa.y, sb.x, sb.y}, {sc.x, sc.y, sd.x, sd.y}};
+      float hv[8][4];
+#pragma unroll
+      for (int l = 0; l < 8; ++l) {
+        const float4 t4 = lds128(st + XB + l * 128 + ((q ^ l) << 4));
+        hv[l][0] = t4.x; hv[l][1] = t4.y; hv[l][2] = t4.z; hv[l][3] = t4.w;
+      }
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const int k = 2 * g + kk;
+        float gk[8];
+        *reinterpret_cast<float4*>(gk) = *reinterpret_cast<const float4*>(Gs + k * 8);
+        *reinterpret_cast<float4*>(gk + 4) = *reinterpret_cast<const float4*>(Gs + k * 8 + 4);
+        float2 e01 = f2(0.f, 0.f), e23 = f2(0.f, 0.f);
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+          e01 = __ffma2_rn(bc(gk[l]), f2(hv[l][0], hv[l][1]), e01);
+          e23 = __ffma2_rn(bc(gk[l]), f2(hv[l][2], hv[l][3]), e23);
+        }
+        const float e[4] = {e01.x, e01.y, e23.x, e23.y};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          float v = mu_q(hk[kk][t], S[kk][t], e[t], eps);
+          if (k >= r || c0 + t >= n) v = 0.f;
+          hn[kk][t] = v;
+        }
+        if (k < r) {
+          if (c0 + 3 < n) {
+            *reinterpret_cast<float4*>(H + (int64_t)k * n + c0) = make_float4(hn[kk][0], hn[kk][1], hn[kk][2], hn[kk][3]);
+          } else {
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              if (c0 + t < n) H[(int64_t)k * n + c0 + t] = hn[kk][t];
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int k = 2 * g + kk;
+          hn[kk][t] = (k < r && c0 + t < n) ? hk[kk][t] : 0.f;
+        }
+    }
+
+    if (do_acc) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        *reinterpret_cast<float2*>(Hw + hnc_idx(4 * q + t, 2 * g)) = f2(hn[0][t], hn[1][t]);
+      __syncwarp();
+      // ---- Q rows rb over this lane's 8 columns
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const float* src = Hw + hnc_idx(8 * cs + t, 0);
+        const float4 a = *reinterpret_cast<const float4*>(src);
+        const float4 bq = *reinterpret_cast<const float4*>(src + 4);
+        const float hr = src[rb];
+        qf[0] = fmaf(hr, a.x, qf[0]); qf[1] = fmaf(hr, a.y, qf[1]);
+        qf[2] = fmaf(hr, a.z, qf[2]); qf[3] = fmaf(hr, a.w, qf[3]);
+        qf[4] = fmaf(hr, bq.x, qf[4]); qf[5] = fmaf(hr, bq.y, qf[5]);
+        qf[6] = fmaf(hr, bq.z, qf[6]); qf[7] = fmaf(hr, bq.w, qf[7]);
+      }
+      // ---- phase B: P rows in 32-row chunks
+#pragma unroll
+      for (int h = 0; h < NCH; ++h) {
+        float2 acc[16];
+#pragma unroll
+        for (int v = 0; v < 16; ++v) acc[v] = f2(0.f, 0.f);
+#pragma unroll
+        for (int s4 = 0; s4 < 2; ++s4) {
+          float2 hq2[4][4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float* src = Hw + hnc_idx(8 * cs + 4 * s4 + t, 0);
+            const float4 a = *reinterpret_cast<const float4*>(src);
+            const float4 bq = *reinterpret_cast<const float4*>(src + 4);
+            hq2[t][0] = f2(a.x, a.y);
+            hq2[t][1] = f2(a.z, a.w);
+            hq2[t][2] = f2(bq.x, bq.y);
+            hq2[t][3] = f2(bq.z, bq.w);
+          }
+          float xs[4][4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = 32 * h + rb + 8 * u;
+            const float4 x = lds128(st + i * 128 + (((2 * cs + s4) ^ rb) << 4));
+            xs[u][0] = x.x; xs[u][1] = x.y; xs[u][2] = x.z; xs[u][3] = x.w;
+          }
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int kp = 0; kp < 4; ++kp)
+                acc[u * 4 + kp] = __ffma2_rn(bc(xs[u][t]), hq2[t][kp], acc[u * 4 + kp]);
+        }
+        float a1[32];
+#pragma unroll
+        for (int v = 0; v < 16; ++v) {
+          a1[2 * v] = acc[v].x;
+          a1[2 * v + 1] = acc[v].y;
+        }
+        float a2[16];
+#pragma unroll
+        for (int v = 0; v < 16; ++v) {
+          const float send = h1 ? a1[v] : a1[v + 16];
+          const float keep = h1 ? a1[v + 16] : a1[v];
+          a2[v] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const float send = h0 ? a2[v] : a2[v + 8];
+          const float keep = h0 ? a2[v + 8] : a2[v];
+          accf[h][v] += keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+      }
+      if (++since == WC_FLUSH) flush();
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  if (do_acc) flush();  // final (also writes zeros for warps without tiles)
+}
+
+size_t fixed_bytes_wc(int MP) {
+  return (size_t)MP * 8 * 4 + 256 + (size_t)NWW * HNC_FLOATS * 4 + 2 * 24 * 8 + 1024;
+}
+
+int dpw_wc(int MP) {
+  const size_t SB = (size_t)MP * 128 + 1024;
+  int d = (int)((SMEM_BUDGET - fixed_bytes_wc(MP)) / (SB * NWW));
+  return d > 4 ? 4 : d;
+}
+
+template <int MP>
+cudaError_t launch_wc(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_t n, int r, const float* W,
+                      const double* Gpart, int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
+                      int evict_first, cudaStream_t st) {
+  const int dpw = dpw_wc(MP);
+  const size_t SB = (size_t)MP * 128 + 1024;
+  const size_t smem = (size_t)NWW * dpw * SB + fixed_bytes_wc(MP);
+  cudaError_t e = cudaFuncSetAttribute(k_fused_wc<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_fused_wc<MP><<<grid, NTW, smem, st>>>(mx, mh, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, dpw, evict_first);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
@@ -875,14 +1197,33 @@ bool fused_supported(int64_t m, int64_t n, int r, int64_t ldx, const void* X, co
   return true;
 }
 
+// Variant WC (warp-owned m <= 256 tiles) is kept as an experiment (NTT_FUSED_WC=1);
+// the CTA-cooperative variant C measured faster on config 3 step 2 (DESIGN.md s.6).
+bool use_wc() {
+  static const bool on = [] {
+    const char* e = getenv("NTT_FUSED_WC");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+int fused_partials(int64_t m, int64_t n, int r, int num_sms) {
+  const int g = fused_grid(m, n, r, num_sms);
+  return (m > 40 && use_wc()) ? g * NWW : g;
+}
+
 int fused_grid(int64_t m, int64_t n, int r, int num_sms) {
   (void)r;
   if (m <= 40) {
     int64_t ntiles = (n + BN - 1) / BN;
     return (int)(ntiles < num_sms ? ntiles : num_sms);
   }
-  int64_t ntiles = (n + BNC - 1) / BNC;  // variant C: two CTAs per SM
-  return (int)(ntiles < 2 * num_sms ? ntiles : 2 * num_sms);
+  int64_t ntiles = (n + BNC - 1) / BNC;
+  if (use_wc()) {  // variant WC: one CTA per SM, 6 warp-owned tiles in flight
+    int64_t need = (ntiles + NWW - 1) / NWW;
+    return (int)(need < num_sms ? (need < 1 ? 1 : need) : num_sms);
+  }
+  return (int)(ntiles < 2 * num_sms ? ntiles : 2 * num_sms);  // variant C: two CTAs per SM
 }
 
 size_t fused_scratch_bytes(int64_t, int64_t, int, int) { return 0; }
@@ -892,6 +1233,16 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
                          int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
                          cudaStream_t st) {
   const int evict_first = ((double)m * (double)n * 4.0 > 48e6) ? 1 : 0;
+  if (m > 40 && use_wc()) {
+    const int MPc = m <= 128 ? 128 : 256;
+    CUtensorMap mx, mh;
+    cudaError_t e = make_map(&mx, X, (uint64_t)n, (uint64_t)m, (uint64_t)ldx, (uint32_t)MPc);
+    if (e != cudaSuccess) return e;
+    e = make_map(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u);
+    if (e != cudaSuccess) return e;
+    if (MPc == 128) return launch_wc<128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st);
+    return launch_wc<256>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st);
+  }
   if (m > 40) {
     const int MPc = m <= 128 ? 128 : 256;
     CUtensorMap mx, mh;

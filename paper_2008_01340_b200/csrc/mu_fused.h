@@ -13,6 +13,9 @@ struct FusedCtx {
 // X and H 16-byte aligned (ldx % 4 == 0, n % 4 == 0).
 bool fused_supported(int64_t m, int64_t n, int r, int64_t ldx, const void* X, const void* H);
 int fused_grid(int64_t m, int64_t n, int r, int num_sms);
+// number of (P, Q) partial slots one fused pass writes (>= grid)
+int fused_partials(int64_t m, int64_t n, int r, int num_sms);
+bool use_wc();
 size_t fused_scratch_bytes(int64_t m, int64_t n, int r, int grid);
 void fused_destroy(FusedCtx& c);
 

@@ -261,6 +261,7 @@ struct MuPlan {
   int hgrid;      // H-pass CTAs
   int nwup;       // W-update CTAs
   int fgrid;      // fused kernel CTAs
+  int fparts;     // fused kernel partial slots
   size_t off_P, off_Q, off_G, off_S, bytes;
 };
 
@@ -278,8 +279,9 @@ MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, int nranks) {
   p.hgrid = hpass_ctas(m, n, r, p.acc, num_sms);
   p.nwup = wupdate_ctas(m, r);
   p.fgrid = fused_grid(m, n, r, num_sms);
-  int64_t nP = std::max<int64_t>({(int64_t)p.xp.ncs, p.acc ? p.hgrid : 0, (int64_t)p.fgrid, 1});
-  int64_t nQ = std::max<int64_t>({(int64_t)p.qp.ncs, p.acc ? p.hgrid : 0, (int64_t)p.fgrid, 1});
+  p.fparts = fused_partials(m, n, r, num_sms);
+  int64_t nP = std::max<int64_t>({(int64_t)p.xp.ncs, p.acc ? p.hgrid : 0, (int64_t)p.fparts, 1});
+  int64_t nQ = std::max<int64_t>({(int64_t)p.qp.ncs, p.acc ? p.hgrid : 0, (int64_t)p.fparts, 1});
   int64_t nG = std::max<int64_t>({(int64_t)p.nwup, (int64_t)wupdate2_ctas(m, r), 1});
   size_t o = 0;
   p.off_P = o;
@@ -319,18 +321,18 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
   if (p.fused && fused_supported(m, n, r, ldx, X, H)) {
     // 1-pass: prologue P0 = X H0^T, Q0 = H0 H0^T; then per iteration
     //   W update (reduces the partials)  ->  fused pass (H update + next P, Q).
-    const int fg = p.fgrid;
+    const int fg = p.fgrid, fp = p.fparts;
     const int nG = wupdate2_ctas(m, r);
     PLAUNCH(h, 1, 4.0 * (double)(m + r) * (double)n,
             launch_fused(X, ldx, m, n, r, W, nullptr, 0, eps, H, Ppart, Qpart, kFusedAcc, fg, st));
     for (int it = 0; it < iters; ++it) {
       if (dist) {
-        ntt_status s = dist_reduce(h, p, Ppart, fg, Qpart, fg, red);
+        ntt_status s = dist_reduce(h, p, Ppart, fp, Qpart, fp, red);
         if (s) return s;
         PLAUNCH(h, 2, 8.0 * (double)(2 * m * r + r * r), launch_wupdate2(W, m, r, red, 1, red + m * r, 1, eps, Gpart, st));
       } else {
-        PLAUNCH(h, 2, 8.0 * ((double)fg * (m * r + r * r) + m * r),
-                launch_wupdate2(W, m, r, Ppart, fg, Qpart, fg, eps, Gpart, st));
+        PLAUNCH(h, 2, 8.0 * ((double)fp * (m * r + r * r) + m * r),
+                launch_wupdate2(W, m, r, Ppart, fp, Qpart, fp, eps, Gpart, st));
       }
       const int mode = kFusedUpdate | ((it + 1 < iters) ? kFusedAcc : 0);
       PLAUNCH(h, 0, 4.0 * (double)(m + 2 * r) * (double)n,
