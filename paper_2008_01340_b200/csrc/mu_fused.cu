@@ -112,7 +112,8 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
         const float* __restrict__ W, const double* __restrict__ Gpart, int nG, float eps, float* __restrict__ H,
         double* __restrict__ Ppart, double* __restrict__ Qpart, int mode, int ns, int evict_first) {
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  // keep the shared address space visible to the compiler (LDS/STS, not generic LD/ST)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int MP = UX * 8;                 // padded rows (TMA box rows)
   constexpr uint32_t XB = 4u * MP * 128u;    // X bytes per stage (4 boxes)
   constexpr uint32_t HB = 4u * 8u * 128u;    // H bytes per stage (4 boxes of 8 rows)
@@ -449,7 +450,8 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
           const float* __restrict__ W, const double* __restrict__ Gpart, int nG, float eps, float* __restrict__ H,
           double* __restrict__ Ppart, double* __restrict__ Qpart, int mode, int ns, int evict_first) {
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  // keep the shared address space visible to the compiler (LDS/STS, not generic LD/ST)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int RW = MP / NWC;          // rows per warp (32 or 64)
   constexpr int NCH = RW / 32;          // phase-B sub-chunks of 32 rows
   constexpr uint32_t XB = MP * 128u;
@@ -727,7 +729,8 @@ k_fused_wc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUte
            const float* __restrict__ W, const double* __restrict__ Gpart, int nG, float eps, float* __restrict__ H,
            double* __restrict__ Ppart, double* __restrict__ Qpart, int mode, int dpw, int evict_first) {
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  // keep the shared address space visible to the compiler (LDS/STS, not generic LD/ST)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int NCH = MP / 32;
   constexpr uint32_t XB = MP * 128u;
   constexpr uint32_t SB = XB + 1024u;
