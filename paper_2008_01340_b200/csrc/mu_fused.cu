@@ -106,8 +106,8 @@ __device__ __forceinline__ float2 bc(float a) { return make_float2(a, a); }
 // transposed per-warp Hn tile: column c (0..127), rank index k (0..7)
 __device__ __forceinline__ int hn_idx(int c, int k) { return c * 8 + k + 4 * (c >> 2) + 4 * (c >> 5); }
 
-template <int R, int UX>
-__global__ void __launch_bounds__(NT, 1)
+template <int R, int UX, int NWT, bool HDIRECT>
+__global__ void __launch_bounds__((NWT + 1) * 32, 1)
 k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmH, int m, int64_t n, int r,
         const float* __restrict__ W, const double* __restrict__ Gpart, int nG, float eps, float* __restrict__ H,
         double* __restrict__ Ppart, double* __restrict__ Qpart, int mode, int ns, int evict_first) {
@@ -116,13 +116,17 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int MP = UX * 8;                 // padded rows (TMA box rows)
   constexpr uint32_t XB = 4u * MP * 128u;    // X bytes per stage (4 boxes)
-  constexpr uint32_t HB = 4u * 8u * 128u;    // H bytes per stage (4 boxes of 8 rows)
+  // Small m (UX <= 2): H is NOT staged -- lanes read their H columns with
+  // coalesced 128-bit global loads issued before the stage wait, so stages are
+  // small and many are in flight (H is most of the traffic there).  Larger m:
+  // H rides in the stage as four 32 x 8 TMA boxes.
+  constexpr uint32_t HB = HDIRECT ? 0u : 4u * 8u * 128u;
   constexpr uint32_t SB = XB + HB;
   unsigned char* stages = smem;
   float* Ws = reinterpret_cast<float*>(smem + (size_t)ns * SB);  // MP x 8
   float* Gs = Ws + MP * 8;                                         // 8 x 8
-  float* HnAll = Gs + 64;                                          // NW x HN_FLOATS
-  uint64_t* full = reinterpret_cast<uint64_t*>(HnAll + NW * HN_FLOATS);
+  float* HnAll = Gs + 64;                                          // NWT x HN_FLOATS
+  uint64_t* full = reinterpret_cast<uint64_t*>(HnAll + NWT * HN_FLOATS);
   uint64_t* empty = full + ns;
   // Tiles issued so far.  Successive rounds of one stage are consumed by
   // DIFFERENT warps, so before parity-waiting on round k a warp must know round
@@ -135,13 +139,13 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   const bool do_acc = (mode & kFusedAcc) != 0;
 
   // ---- setup: W, G into smem; barriers
-  for (int e = tid; e < MP * 8; e += NT) {
+  for (int e = tid; e < MP * 8; e += (NWT + 1) * 32) {
     int i = e >> 3, k = e & 7;
     Ws[e] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
   }
   if (do_update) {
     const int rr = r * r;
-    for (int e = tid; e < 64; e += NT) {
+    for (int e = tid; e < 64; e += (NWT + 1) * 32) {
       int k = e >> 3, l = e & 7;
       double s = 0.0;
       if (k < r && l < r)
@@ -163,7 +167,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   const int64_t b = blockIdx.x;
   const int64_t J = (ntiles > b) ? (ntiles - b + gridDim.x - 1) / gridDim.x : 0;
 
-  if (warp == NW) {
+  if (warp == NWT) {
     // ================= TMA producer =================
     if (lane == 0) {
       uint64_t policy;
@@ -180,8 +184,10 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
         unsigned char* st = stages + (size_t)s * SB;
 #pragma unroll
         for (int bx = 0; bx < 4; ++bx) tma_load_2d(st + bx * MP * 128, &tmX, col0 + bx * 32, 0, &full[s], policy);
+        if (!HDIRECT) {
 #pragma unroll
-        for (int bx = 0; bx < 4; ++bx) tma_load_2d(st + XB + bx * 1024, &tmH, col0 + bx * 32, 0, &full[s], policy);
+          for (int bx = 0; bx < 4; ++bx) tma_load_2d(st + XB + bx * 1024, &tmH, col0 + bx * 32, 0, &full[s], policy);
+        }
         st_release_u32(issued, (uint32_t)(j + 1));
       }
     }
@@ -203,40 +209,60 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   for (int v = 0; v < V4 / 4; ++v) accd[v] = 0.0;
   const bool h1 = (lane >> 4) & 1, h0 = (lane >> 3) & 1;
 
-  for (int64_t j = warp; j < J; j += NW) {
+  for (int64_t j = warp; j < J; j += NWT) {
     const int s = (int)(j % ns);
     const uint32_t ph = (uint32_t)((j / ns) & 1);
-    if (lane == 0)
+    const int64_t jt = (b + j * gridDim.x) * BN;  // first column of the tile
+    const int64_t c0 = jt + 4 * q;
+    // H columns 4q..4q+3 of this tile (HDIRECT: independent of the stage, issued first)
+    float2 hv[R][2];
+#pragma unroll
+    for (int l = 0; l < R; ++l) {
+      float4 h4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (HDIRECT && l < r) {
+        const float* hp = H + (int64_t)l * n + c0;
+        if (c0 + 3 < n) {
+          h4 = *reinterpret_cast<const float4*>(hp);
+        } else {
+          if (c0 + 0 < n) h4.x = hp[0];
+          if (c0 + 1 < n) h4.y = hp[1];
+          if (c0 + 2 < n) h4.z = hp[2];
+        }
+      }
+      hv[l][0] = f2(h4.x, h4.y);
+      hv[l][1] = f2(h4.z, h4.w);
+    }
     {
 #ifdef NTT_WATCHDOG
       long long t0 = clock64();
 #endif
-      while (ld_acquire_u32(issued) <= (uint32_t)j) {
-        __nanosleep(64);
+      if (lane == 0) {
+        while (ld_acquire_u32(issued) <= (uint32_t)j) {
+          __nanosleep(64);
 #ifdef NTT_WATCHDOG
-        if (clock64() - t0 > 4000000000LL) {
-          printf("WATCHDOG issued block=%d warp=%d j=%lld issued=%u\n", blockIdx.x, warp, (long long)j, *issued);
-          __trap();
-        }
+          if (clock64() - t0 > 4000000000LL) {
+            printf("WATCHDOG issued block=%d warp=%d j=%lld issued=%u\n", blockIdx.x, warp, (long long)j, *issued);
+            __trap();
+          }
 #endif
+        }
       }
     }
     __syncwarp();
     MBAR_WAIT(&full[s], ph, 2, j);
     const unsigned char* st = stages + (size_t)s * SB;
-    const int64_t jt = (b + j * gridDim.x) * BN;  // first column of the tile
-
-    // ---------------- phase A ----------------
-    {
+    if (!HDIRECT) {
       const unsigned char* hb = st + XB + qbox * 1024;
-      float2 hv[R][2];
 #pragma unroll
       for (int l = 0; l < R; ++l) {
-        float4 h4 = lds128(hb + l * 128 + ((qch ^ l) << 4));
+        const float4 h4 = lds128(hb + l * 128 + ((qch ^ l) << 4));
         hv[l][0] = f2(h4.x, h4.y);
         hv[l][1] = f2(h4.z, h4.w);
       }
-      const int64_t c0 = jt + 4 * q;
+    }
+
+    // ---------------- phase A ----------------
+    {
       float2 hn[R][2];
       if (do_update) {
         const unsigned char* xb = st + qbox * MP * 128;
@@ -401,14 +427,14 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
 
   if (!do_acc) return;
   // ---- fixed-order CTA reduction of the per-thread fp64 partials
-  asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"r"(NWT * 32) : "memory");
   // red[w][rb][f], f = u*R + k flat (u = UX is the Q row)
   double* red = reinterpret_cast<double*>(stages);
 #pragma unroll
   for (int v = 0; v < V4 / 4; ++v) red[((size_t)warp * 8 + rb) * V4 + cs * (V4 / 4) + v] = accd[v];
-  asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"r"(NWT * 32) : "memory");
   const int mr = m * r, rr = r * r;
-  for (int e = tid; e < 8 * V; e += NW * 32) {
+  for (int e = tid; e < 8 * V; e += NWT * 32) {
     const int rbe = e / V, f = e % V;
     const int u = f / R, k = f % R;
     if (k >= r) continue;
@@ -416,7 +442,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
     const int row = isQ ? rbe : rbe + 8 * u;
     if (isQ ? (row >= r) : (row >= m)) continue;
     double sum = 0.0;
-    for (int w = 0; w < NW; ++w) sum += red[((size_t)w * 8 + rbe) * V4 + f];
+    for (int w = 0; w < NWT; ++w) sum += red[((size_t)w * 8 + rbe) * V4 + f];
     if (isQ) Qpart[b * rr + row * r + k] = sum;
     else Ppart[b * mr + row * r + k] = sum;
   }
@@ -1058,27 +1084,27 @@ cudaError_t make_map(CUtensorMap* map, const float* base, uint64_t cols, uint64_
 int ux_for(int64_t m) { return m <= 8 ? 1 : m <= 16 ? 2 : m <= 32 ? 4 : 5; }
 int rcls_for(int r) { return r <= 2 ? 2 : r <= 4 ? 4 : 8; }
 
-size_t fixed_bytes(int ux) {
-  return (size_t)ux * 8 * 8 * 4 + 256 + (size_t)NW * HN_FLOATS * 4 + 2 * 16 * 8 + 16 + 1024;
+size_t fixed_bytes(int ux, int nwt) {
+  return (size_t)ux * 8 * 8 * 4 + 256 + (size_t)nwt * HN_FLOATS * 4 + 2 * 16 * 8 + 16 + 1024;
 }
 
-int stages_for(int ux) {
-  const size_t SB = 4u * ux * 8 * 128 + 4096;
-  int ns = (int)((SMEM_BUDGET - fixed_bytes(ux)) / SB);
+int stages_for(int ux, int nwt, bool hd) {
+  const size_t SB = 4u * ux * 8 * 128 + (hd ? 0 : 4096);
+  int ns = (int)((SMEM_BUDGET - fixed_bytes(ux, nwt)) / SB);
   if (ns > 16) ns = 16;
   return ns;
 }
 
-template <int R, int UX>
+template <int R, int UX, int NWT, bool HD>
 cudaError_t launch_t(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_t n, int r, const float* W,
                      const double* Gpart, int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
                      int evict_first, cudaStream_t st) {
-  const int ns = stages_for(UX);
-  const size_t SB = 4u * UX * 8 * 128 + 4096;
-  const size_t smem = (size_t)ns * SB + fixed_bytes(UX);
-  cudaError_t e = cudaFuncSetAttribute(k_fused<R, UX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int ns = stages_for(UX, NWT, HD);
+  const size_t SB = 4u * UX * 8 * 128 + (HD ? 0 : 4096);
+  const size_t smem = (size_t)ns * SB + fixed_bytes(UX, NWT);
+  cudaError_t e = cudaFuncSetAttribute(k_fused<R, UX, NWT, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_fused<R, UX><<<grid, NT, smem, st>>>(mx, mh, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, ns, evict_first);
+  k_fused<R, UX, NWT, HD><<<grid, (NWT + 1) * 32, smem, st>>>(mx, mh, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, ns, evict_first);
   return cudaGetLastError();
 }
 
@@ -1263,7 +1289,23 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
   e = make_map(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u);
   if (e != cudaSuccess) return e;
   const int rc = rcls_for(r);
-#define LF(RR, UU) return launch_t<RR, UU>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st)
+  // experiment knobs: NTT_W_WARPS=7 (UX >= 4), NTT_W_HDIRECT=0/1 (default: direct H loads
+  // when m <= 16 or r < 8, i.e. when H is a large share of the traffic)
+  static const int w_warps = [] {
+    const char* e = getenv("NTT_W_WARPS");
+    return (e && e[0] == '7') ? 7 : 8;
+  }();
+  static const int w_hd = [] {
+    const char* e = getenv("NTT_W_HDIRECT");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  const bool hd = (w_hd >= 0) ? (w_hd == 1) : (ux <= 2 || r < 8);
+#define LF(RR, UU)                                                                                                              \
+  return (UU >= 4 && w_warps == 7)                                                                                              \
+             ? (hd ? launch_t<RR, UU, 7, true>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st)  \
+                   : launch_t<RR, UU, 7, false>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st)) \
+             : (hd ? launch_t<RR, UU, 8, true>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st)  \
+                   : launch_t<RR, UU, 8, false>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st))
   if (rc == 2) {
     if (ux == 1) LF(2, 1);
     if (ux == 2) LF(2, 2);
