@@ -106,7 +106,7 @@ __device__ __forceinline__ float2 bc(float a) { return make_float2(a, a); }
 // transposed per-warp Hn tile: column c (0..127), rank index k (0..7)
 __device__ __forceinline__ int hn_idx(int c, int k) { return c * 8 + k + 4 * (c >> 2) + 4 * (c >> 5); }
 
-template <int R, int UX, int NWT, bool HDIRECT>
+template <int R, int UX, int NWT, bool HDIRECT, int BNT>
 __global__ void __launch_bounds__((NWT + 1) * 32, 1)
 k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmH, int m, int64_t n, int r,
         const float* __restrict__ W, const double* __restrict__ Gpart, int nG, float eps, float* __restrict__ H,
@@ -115,12 +115,15 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   // keep the shared address space visible to the compiler (LDS/STS, not generic LD/ST)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int MP = UX * 8;                 // padded rows (TMA box rows)
-  constexpr uint32_t XB = 4u * MP * 128u;    // X bytes per stage (4 boxes)
+  constexpr int NB = BNT / 32;               // 32-column boxes per tile
+  constexpr int CPL = BNT / 32;              // phase-A columns per lane (4 or 2)
+  constexpr int SL = BNT / 4;                // phase-B columns per slice lane-group
+  constexpr uint32_t XB = (uint32_t)NB * MP * 128u;
   // Small m (UX <= 2): H is NOT staged -- lanes read their H columns with
   // coalesced 128-bit global loads issued before the stage wait, so stages are
   // small and many are in flight (H is most of the traffic there).  Larger m:
   // H rides in the stage as four 32 x 8 TMA boxes.
-  constexpr uint32_t HB = HDIRECT ? 0u : 4u * 8u * 128u;
+  constexpr uint32_t HB = HDIRECT ? 0u : (uint32_t)NB * 8u * 128u;
   constexpr uint32_t SB = XB + HB;
   unsigned char* stages = smem;
   float* Ws = reinterpret_cast<float*>(smem + (size_t)ns * SB);  // MP x 8
@@ -163,7 +166,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   }
   __syncthreads();
 
-  const int64_t ntiles = (n + BN - 1) / BN;
+  const int64_t ntiles = (n + BNT - 1) / BNT;
   const int64_t b = blockIdx.x;
   const int64_t J = (ntiles > b) ? (ntiles - b + gridDim.x - 1) / gridDim.x : 0;
 
@@ -180,13 +183,13 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
         const uint32_t ph = (uint32_t)((j / ns) & 1);
         MBAR_WAIT(&empty[s], ph ^ 1u, 1, j);
         mbar_expect_tx(&full[s], SB);
-        const int col0 = (int)((b + j * gridDim.x) * BN);
+        const int col0 = (int)((b + j * gridDim.x) * BNT);
         unsigned char* st = stages + (size_t)s * SB;
 #pragma unroll
-        for (int bx = 0; bx < 4; ++bx) tma_load_2d(st + bx * MP * 128, &tmX, col0 + bx * 32, 0, &full[s], policy);
+        for (int bx = 0; bx < NB; ++bx) tma_load_2d(st + bx * MP * 128, &tmX, col0 + bx * 32, 0, &full[s], policy);
         if (!HDIRECT) {
 #pragma unroll
-          for (int bx = 0; bx < 4; ++bx) tma_load_2d(st + XB + bx * 1024, &tmH, col0 + bx * 32, 0, &full[s], policy);
+          for (int bx = 0; bx < NB; ++bx) tma_load_2d(st + XB + bx * 1024, &tmH, col0 + bx * 32, 0, &full[s], policy);
         }
         st_release_u32(issued, (uint32_t)(j + 1));
       }
@@ -196,8 +199,9 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
 
   // ================= consumer warps =================
   float* Hw = HnAll + warp * HN_FLOATS;
-  const int q = lane, qbox = q >> 3, qch = q & 7;   // phase A: columns 4q..4q+3
-  const int rb = lane & 7, cs = lane >> 3;          // phase B: rows rb+8u, columns 32cs..32cs+31
+  // phase A: lane q owns columns cq..cq+CPL-1 (box qbox, 16B chunk qch, float offset qsub)
+  const int q = lane, cq = q * CPL, qbox = cq >> 5, qch = (cq & 31) >> 2, qsub = cq & 3;
+  const int rb = lane & 7, cs = lane >> 3;  // phase B: rows rb+8u, columns cs*SL .. cs*SL+SL-1
   // phase-B accumulators: V4 = (UX+1)*R values per lane (rows rb+8u, u<UX, and Q
   // row rb), padded to a multiple of 4.  After every tile the 4 lanes sharing rb
   // (cs = 0..3) reduce-scatter them with two shuffle levels, so each lane keeps
@@ -212,25 +216,31 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   for (int64_t j = warp; j < J; j += NWT) {
     const int s = (int)(j % ns);
     const uint32_t ph = (uint32_t)((j / ns) & 1);
-    const int64_t jt = (b + j * gridDim.x) * BN;  // first column of the tile
-    const int64_t c0 = jt + 4 * q;
-    // H columns 4q..4q+3 of this tile (HDIRECT: independent of the stage, issued first)
-    float2 hv[R][2];
+    const int64_t jt = (b + j * gridDim.x) * BNT;  // first column of the tile
+    const int64_t c0 = jt + cq;
+    // H columns c0..c0+CPL-1 of this tile (HDIRECT: independent of the stage, issued first)
+    float2 hv[R][CPL / 2];
 #pragma unroll
     for (int l = 0; l < R; ++l) {
-      float4 h4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      float hx[4] = {0.f, 0.f, 0.f, 0.f};
       if (HDIRECT && l < r) {
         const float* hp = H + (int64_t)l * n + c0;
-        if (c0 + 3 < n) {
-          h4 = *reinterpret_cast<const float4*>(hp);
+        if (c0 + CPL - 1 < n) {
+          if (CPL == 4) {
+            const float4 h4 = *reinterpret_cast<const float4*>(hp);
+            hx[0] = h4.x; hx[1] = h4.y; hx[2] = h4.z; hx[3] = h4.w;
+          } else {
+            const float2 h2 = *reinterpret_cast<const float2*>(hp);
+            hx[0] = h2.x; hx[1] = h2.y;
+          }
         } else {
-          if (c0 + 0 < n) h4.x = hp[0];
-          if (c0 + 1 < n) h4.y = hp[1];
-          if (c0 + 2 < n) h4.z = hp[2];
+#pragma unroll
+          for (int t = 0; t < CPL - 1; ++t)
+            if (c0 + t < n) hx[t] = hp[t];
         }
       }
-      hv[l][0] = f2(h4.x, h4.y);
-      hv[l][1] = f2(h4.z, h4.w);
+#pragma unroll
+      for (int p2 = 0; p2 < CPL / 2; ++p2) hv[l][p2] = f2(hx[2 * p2], hx[2 * p2 + 1]);
     }
     {
 #ifdef NTT_WATCHDOG
@@ -255,102 +265,110 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
       const unsigned char* hb = st + XB + qbox * 1024;
 #pragma unroll
       for (int l = 0; l < R; ++l) {
-        const float4 h4 = lds128(hb + l * 128 + ((qch ^ l) << 4));
-        hv[l][0] = f2(h4.x, h4.y);
-        hv[l][1] = f2(h4.z, h4.w);
+        const unsigned char* hp = hb + l * 128 + ((qch ^ l) << 4) + qsub * 4;
+        if (CPL == 4) {
+          const float4 h4 = lds128(hp);
+          hv[l][0] = f2(h4.x, h4.y);
+          hv[l][CPL / 2 - 1] = f2(h4.z, h4.w);
+        } else {
+          hv[l][0] = *reinterpret_cast<const float2*>(hp);
+        }
       }
     }
 
     // ---------------- phase A ----------------
     {
-      float2 hn[R][2];
+      float2 hn[R][CPL / 2];
       if (do_update) {
-        const unsigned char* xb = st + qbox * MP * 128;
-        float2 s2[R][2];
+        const unsigned char* xb = st + qbox * MP * 128 + qsub * 4;
+        float2 s2[R][CPL / 2];
 #pragma unroll
-        for (int k = 0; k < R; ++k) s2[k][0] = s2[k][1] = f2(0.f, 0.f);
+        for (int k = 0; k < R; ++k)
+#pragma unroll
+          for (int p2 = 0; p2 < CPL / 2; ++p2) s2[k][p2] = f2(0.f, 0.f);
 #pragma unroll 4
         for (int i = 0; i < m; ++i) {
-          float4 x = lds128(xb + i * 128 + ((qch ^ (i & 7)) << 4));
-          const float2 xa = f2(x.x, x.y), xc = f2(x.z, x.w);
+          float2 xv[CPL / 2];
+          if (CPL == 4) {
+            const float4 x = lds128(xb + i * 128 + ((qch ^ (i & 7)) << 4));
+            xv[0] = f2(x.x, x.y);
+            xv[CPL / 2 - 1] = f2(x.z, x.w);
+          } else {
+            xv[0] = *reinterpret_cast<const float2*>(xb + i * 128 + ((qch ^ (i & 7)) << 4));
+          }
           const float4* wr = reinterpret_cast<const float4*>(Ws + i * 8);
           float w[8];
           *reinterpret_cast<float4*>(w) = wr[0];
           if (R > 4) *reinterpret_cast<float4*>(w + 4) = wr[1];
 #pragma unroll
-          for (int k = 0; k < R; ++k) {
-            s2[k][0] = __ffma2_rn(bc(w[k]), xa, s2[k][0]);
-            s2[k][1] = __ffma2_rn(bc(w[k]), xc, s2[k][1]);
-          }
-        }
-        // E = G H (l outer: 2R independent accumulators) ; Hn = H S / (E + eps)
-        float2 ev[R][2];
+          for (int k = 0; k < R; ++k)
 #pragma unroll
-        for (int k = 0; k < R; ++k) ev[k][0] = ev[k][1] = f2(0.f, 0.f);
+            for (int p2 = 0; p2 < CPL / 2; ++p2) s2[k][p2] = __ffma2_rn(bc(w[k]), xv[p2], s2[k][p2]);
+        }
+        // E = G H (l outer: independent accumulators) ; Hn = H S / (E + eps)
+        float2 ev[R][CPL / 2];
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+#pragma unroll
+          for (int p2 = 0; p2 < CPL / 2; ++p2) ev[k][p2] = f2(0.f, 0.f);
 #pragma unroll
         for (int l = 0; l < R; ++l) {
 #pragma unroll
           for (int k = 0; k < R; ++k) {
             const float g = Gs[k * 8 + l];
-            ev[k][0] = __ffma2_rn(bc(g), hv[l][0], ev[k][0]);
-            ev[k][1] = __ffma2_rn(bc(g), hv[l][1], ev[k][1]);
+#pragma unroll
+            for (int p2 = 0; p2 < CPL / 2; ++p2) ev[k][p2] = __ffma2_rn(bc(g), hv[l][p2], ev[k][p2]);
           }
         }
 #pragma unroll
-        for (int k = 0; k < R; ++k) {
-          hn[k][0].x = mu_q(hv[k][0].x, s2[k][0].x, ev[k][0].x, eps);
-          hn[k][0].y = mu_q(hv[k][0].y, s2[k][0].y, ev[k][0].y, eps);
-          hn[k][1].x = mu_q(hv[k][1].x, s2[k][1].x, ev[k][1].x, eps);
-          hn[k][1].y = mu_q(hv[k][1].y, s2[k][1].y, ev[k][1].y, eps);
-          if (k >= r) hn[k][0] = hn[k][1] = f2(0.f, 0.f);  // padded ranks (0/0 when eps = 0)
-        }
-        // columns beyond n: zero (never stored, never accumulated)
-        if (c0 + 3 >= n) {
+        for (int k = 0; k < R; ++k)
 #pragma unroll
-          for (int k = 0; k < R; ++k) {
-            if (c0 + 0 >= n) hn[k][0].x = 0.f;
-            if (c0 + 1 >= n) hn[k][0].y = 0.f;
-            if (c0 + 2 >= n) hn[k][1].x = 0.f;
-            if (c0 + 3 >= n) hn[k][1].y = 0.f;
+          for (int p2 = 0; p2 < CPL / 2; ++p2) {
+            float2 v;
+            v.x = mu_q(hv[k][p2].x, s2[k][p2].x, ev[k][p2].x, eps);
+            v.y = mu_q(hv[k][p2].y, s2[k][p2].y, ev[k][p2].y, eps);
+            if (k >= r) v = f2(0.f, 0.f);  // padded ranks (0/0 when eps = 0)
+            // columns beyond n: zero (never stored, never accumulated)
+            if (c0 + 2 * p2 >= n) v.x = 0.f;
+            if (c0 + 2 * p2 + 1 >= n) v.y = 0.f;
+            hn[k][p2] = v;
           }
-        }
-        // store H (in place; this tile's H was already staged by TMA)
-        if (c0 + 3 < n) {
+        // store H (in place; this tile's H was already read)
+        if (c0 + CPL - 1 < n) {
 #pragma unroll
           for (int k = 0; k < R; ++k)
-            if (k < r)
-              *reinterpret_cast<float4*>(H + (int64_t)k * n + c0) = make_float4(hn[k][0].x, hn[k][0].y, hn[k][1].x, hn[k][1].y);
+            if (k < r) {
+              if (CPL == 4)
+                *reinterpret_cast<float4*>(H + (int64_t)k * n + c0) =
+                    make_float4(hn[k][0].x, hn[k][0].y, hn[k][CPL / 2 - 1].x, hn[k][CPL / 2 - 1].y);
+              else
+                *reinterpret_cast<float2*>(H + (int64_t)k * n + c0) = hn[k][0];
+            }
         } else {
 #pragma unroll
           for (int k = 0; k < R; ++k)
             if (k < r) {
-              if (c0 + 0 < n) H[(int64_t)k * n + c0 + 0] = hn[k][0].x;
-              if (c0 + 1 < n) H[(int64_t)k * n + c0 + 1] = hn[k][0].y;
-              if (c0 + 2 < n) H[(int64_t)k * n + c0 + 2] = hn[k][1].x;
+#pragma unroll
+              for (int t = 0; t < CPL - 1; ++t)
+                if (c0 + t < n) H[(int64_t)k * n + c0 + t] = (t & 1) ? hn[k][t >> 1].y : hn[k][t >> 1].x;
             }
         }
       } else {
 #pragma unroll
-        for (int k = 0; k < R; ++k) {
-          hn[k][0] = hv[k][0];
-          hn[k][1] = hv[k][1];
-        }
+        for (int k = 0; k < R; ++k)
+#pragma unroll
+          for (int p2 = 0; p2 < CPL / 2; ++p2) hn[k][p2] = hv[k][p2];
       }
       if (do_acc) {
         // transposed Hn tile: Hw[hn_idx(c, k)]
-        float tv[4][8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          tv[0][k] = (k < R) ? hn[k % R][0].x : 0.f;
-          tv[1][k] = (k < R) ? hn[k % R][0].y : 0.f;
-          tv[2][k] = (k < R) ? hn[k % R][1].x : 0.f;
-          tv[3][k] = (k < R) ? hn[k % R][1].y : 0.f;
-        }
+        for (int t = 0; t < CPL; ++t) {
+          float tv[8];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          float* dst = Hw + hn_idx(4 * q + t, 0);
-          *reinterpret_cast<float4*>(dst) = make_float4(tv[t][0], tv[t][1], tv[t][2], tv[t][3]);
-          if (R > 4) *reinterpret_cast<float4*>(dst + 4) = make_float4(tv[t][4], tv[t][5], tv[t][6], tv[t][7]);
+          for (int k = 0; k < 8; ++k) tv[k] = (k < R) ? ((t & 1) ? hn[k % R][t >> 1].y : hn[k % R][t >> 1].x) : 0.f;
+          float* dst = Hw + hn_idx(cq + t, 0);
+          *reinterpret_cast<float4*>(dst) = make_float4(tv[0], tv[1], tv[2], tv[3]);
+          if (R > 4) *reinterpret_cast<float4*>(dst + 4) = make_float4(tv[4], tv[5], tv[6], tv[7]);
         }
       }
     }
@@ -358,13 +376,14 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
     // ---------------- phase B ----------------
     if (do_acc) {
       __syncwarp();
-      const unsigned char* xb = st + cs * MP * 128;
       float2 acc[V4 / 2];
 #pragma unroll
       for (int v = 0; v < V4 / 2; ++v) acc[v] = f2(0.f, 0.f);
 #pragma unroll 2
-      for (int s4 = 0; s4 < 8; ++s4) {
-        const int c = 32 * cs + 4 * s4;
+      for (int s4 = 0; s4 < SL / 4; ++s4) {
+        const int c = SL * cs + 4 * s4;
+        const unsigned char* xb = st + (c >> 5) * MP * 128;
+        const int chk = (c & 31) >> 2;
         float2 hq2[4][R / 2];
         float hq[4];
 #pragma unroll
@@ -383,7 +402,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
         float xs[UX][4];
 #pragma unroll
         for (int u = 0; u < UX; ++u) {
-          const float4 x = lds128(xb + (rb + 8 * u) * 128 + ((s4 ^ rb) << 4));
+          const float4 x = lds128(xb + (rb + 8 * u) * 128 + ((chk ^ rb) << 4));
           xs[u][0] = x.x;
           xs[u][1] = x.y;
           xs[u][2] = x.z;
@@ -1088,23 +1107,23 @@ size_t fixed_bytes(int ux, int nwt) {
   return (size_t)ux * 8 * 8 * 4 + 256 + (size_t)nwt * HN_FLOATS * 4 + 2 * 16 * 8 + 16 + 1024;
 }
 
-int stages_for(int ux, int nwt, bool hd) {
-  const size_t SB = 4u * ux * 8 * 128 + (hd ? 0 : 4096);
+int stages_for(int ux, int nwt, bool hd, int bnt) {
+  const size_t SB = (size_t)(bnt / 32) * ux * 8 * 128 + (hd ? 0 : (size_t)(bnt / 32) * 1024);
   int ns = (int)((SMEM_BUDGET - fixed_bytes(ux, nwt)) / SB);
-  if (ns > 16) ns = 16;
+  if (ns > 24) ns = 24;
   return ns;
 }
 
-template <int R, int UX, int NWT, bool HD>
+template <int R, int UX, int NWT, bool HD, int BNT>
 cudaError_t launch_t(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_t n, int r, const float* W,
                      const double* Gpart, int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
                      int evict_first, cudaStream_t st) {
-  const int ns = stages_for(UX, NWT, HD);
-  const size_t SB = 4u * UX * 8 * 128 + (HD ? 0 : 4096);
+  const int ns = stages_for(UX, NWT, HD, BNT);
+  const size_t SB = (size_t)(BNT / 32) * UX * 8 * 128 + (HD ? 0 : (size_t)(BNT / 32) * 1024);
   const size_t smem = (size_t)ns * SB + fixed_bytes(UX, NWT);
-  cudaError_t e = cudaFuncSetAttribute(k_fused<R, UX, NWT, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_fused<R, UX, NWT, HD, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_fused<R, UX, NWT, HD><<<grid, (NWT + 1) * 32, smem, st>>>(mx, mh, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, ns, evict_first);
+  k_fused<R, UX, NWT, HD, BNT><<<grid, (NWT + 1) * 32, smem, st>>>(mx, mh, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, ns, evict_first);
   return cudaGetLastError();
 }
 
@@ -1289,11 +1308,11 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
   e = make_map(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u);
   if (e != cudaSuccess) return e;
   const int rc = rcls_for(r);
-  // experiment knobs: NTT_W_WARPS=7 (UX >= 4), NTT_W_HDIRECT=0/1 (default: direct H loads
+  // experiment knobs: NTT_W_BN=64 (64-column tiles for UX >= 4), NTT_W_HDIRECT=0/1 (default: direct H loads
   // when m <= 16 or r < 8, i.e. when H is a large share of the traffic)
-  static const int w_warps = [] {
-    const char* e = getenv("NTT_W_WARPS");
-    return (e && e[0] == '7') ? 7 : 8;
+  static const int w_bn = [] {
+    const char* e = getenv("NTT_W_BN");
+    return (e && e[0] == '6') ? 64 : 128;
   }();
   static const int w_hd = [] {
     const char* e = getenv("NTT_W_HDIRECT");
@@ -1301,11 +1320,11 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
   }();
   const bool hd = (w_hd >= 0) ? (w_hd == 1) : (ux <= 2 || r < 8);
 #define LF(RR, UU)                                                                                                              \
-  return (UU >= 4 && w_warps == 7)                                                                                              \
-             ? (hd ? launch_t<RR, UU, 7, true>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st)  \
-                   : launch_t<RR, UU, 7, false>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st)) \
-             : (hd ? launch_t<RR, UU, 8, true>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st)  \
-                   : launch_t<RR, UU, 8, false>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st))
+  return (UU >= 4 && w_bn == 64)                                                                                                  \
+             ? (hd ? launch_t<RR, UU, 8, true, 64>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st)  \
+                   : launch_t<RR, UU, 8, false, 64>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st)) \
+             : (hd ? launch_t<RR, UU, 8, true, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st) \
+                   : launch_t<RR, UU, 8, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st))
   if (rc == 2) {
     if (ux == 1) LF(2, 1);
     if (ux == 2) LF(2, 2);
