@@ -161,9 +161,10 @@ double ntt_compression_ratio(int32_t d, const int64_t* dims, const int32_t* rank
  * launches, their summed device time in ms and summed algorithmic bytes.
  * Classes: 0 = fused 1-pass X-stream kernel (H update + next X H^T, H H^T),
  * 1 = X H^T pass (incl. the 1-pass prologue), 2 = W update, 3 = TT contraction
- * stream (error / generate), 4 = other, 5 = generic 2-pass H pass.
+ * stream (error / generate), 4 = other, 5 = generic 2-pass H pass, 6 = tensor-core
+ * X H^T pass, 7 = tensor-core W^T X pass (mu_tc.cu, tall / square X).
  * Enabling resets the counters.                                              */
-#define NTT_PROF_CLASSES 6
+#define NTT_PROF_CLASSES 8
 ntt_status ntt_profile_enable(ntt_handle h, int enable);
 ntt_status ntt_profile_get(ntt_handle h, int cls, int64_t* launches, double* total_ms,
                            double* total_bytes);

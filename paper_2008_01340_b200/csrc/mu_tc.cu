@@ -1,0 +1,598 @@
+// mu_tc.cu -- tensor-core (tcgen05, kind::tf32) 2-pass MU iteration for tall /
+// square X (BASELINE configs 2 and 5: m x n = 4096 x 4096 r 16, 32768 x 65536
+// r 32), where the contraction X H^T / W^T X is a real dense GEMM with a long K
+// and FP32 FFMA cannot keep up with HBM (r/2 flop per byte, SURVEY s.0 #4).
+//
+// One MU iteration (include/ntt.h ntt_nmf_mu, readings R1-R4):
+//   pass W   P = X Hcat^T          (Alg. 5 l.2)   k_skinny_tc<R, 0>
+//   W update W <- W o P / (W Q + eps), G = W^T W  (Alg. 4)  k_tc_wupdate
+//   pass H   S = X^T Wcat          (Alg. 6 l.2)   k_skinny_tc<R, 1>
+//   H update H <- H o S / (G H + eps), Q = H H^T          k_tc_hupdate
+//
+// fp32 accuracy from TF32 tensor cores ("3xTF32"): every operand v is split
+// v = hi + lo with hi = v truncated to TF32 (what the tensor core reads from a
+// raw fp32 word) and lo = v - hi (exact in fp32); the products keep
+// hi*hi + hi*lo + lo*hi and drop lo*lo (~2^-22 relative, SURVEY s.8(c) c.4:
+// 3xTF32 drift 2.9e-7 vs the 1e-4 parity bar).  The MMA pair per K step is
+//   D[:, 0:2R] (+)= A_hi * [B_hi | B_lo]      (N = 2R)
+//   D[:, 0:R]  +=   A_lo *  B_hi              (TS, N = R)
+// with A_hi the raw X tile in shared memory (pass W, SS form) or staged in TMEM
+// (pass H, TS form), and A_lo always in TMEM: the converter warps read each X
+// element once (LDS), split it, and store lo (and hi) with tcgen05.st.
+// Measured on B200 (tools/tc_probe.cu): one M=128 K=8 tf32 MMA costs ~138
+// cycles for any N in 8..128, so these passes are MMA-issue-bound at
+// 2 MMAs per 128 x 8 X elements (<= ~15 B/clk/SM), not HBM-bound.  B = [B_hi | B_lo] is prepared by the update kernels
+// (Hcat = [H; lo(H)] (2R x n), WcatT = [W^T; lo(W)^T] (2R x m)).
+// The fp32 accumulator in TMEM is flushed to per-thread fp64 every
+// `flush` K tiles (two-level sums, R13); split-K partials are fp64 and summed
+// in fixed order by the update kernels (deterministic, R16).
+//
+// CTA = 10 warps, persistent (1 CTA / SM): warp 0 TMA producer, warp 1 MMA
+// issuer (one thread), warps 2-5 converters, warps 6-9 epilogue.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "mu_tc.h"
+#include "sm100.cuh"
+
+namespace ntt {
+
+namespace {
+using namespace sm100;
+
+constexpr int TC_BK = 32;     // K elements per stage (one 128-B swizzle row of fp32)
+constexpr int TC_BM = 128;    // D rows per unit (UMMA M)
+constexpr int TC_T = 4;       // TMEM A_lo buffers (32 columns each)
+constexpr int TC_WARPS = 10;
+constexpr int TC_THREADS = TC_WARPS * 32;
+constexpr uint32_t TC_ABYTES = TC_BM * 128u;  // 16 KB A tile per stage
+
+__device__ __forceinline__ float tf32_trunc(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
+__device__ __forceinline__ float tf32_lo(float v) { return __fsub_rn(v, tf32_trunc(v)); }
+
+template <int R>
+struct TcCfg {
+  static constexpr int N1 = 2 * R;                        // [B_hi | B_lo]
+  static constexpr uint32_t BBYTES = (uint32_t)N1 * 128u;  // B tile per stage
+  static constexpr uint32_t SB = TC_ABYTES + BBYTES;
+  static constexpr uint32_t TMEM_D = 0;                   // two accumulators of N1 columns
+  static constexpr uint32_t TMEM_LO = 2 * N1;              // TC_T A_lo buffers of 32 columns
+  static constexpr uint32_t TMEM_HI = TMEM_LO + TC_T * 32;  // TC_T A_hi buffers (MODE 1)
+  static constexpr uint32_t TMEM_COLS = 512u;
+};
+
+// MODE 0: D (Mtot = m rows) = X * Hcat^T, A = X row block [128 rows][32 K] K-major.
+// MODE 1: D (Mtot = n cols) = X^T * WcatT^T, A = X^T from four [32 K rows][32 M cols] boxes; the
+//         converters stage both A_hi and A_lo in TMEM (an MN-major tf32 A read from shared
+//         memory by the SS form gave wrong results on B200 in our probe, so it is not used).
+// Units u = (mb, s): D rows [128 mb, 128 mb + 128), K tiles [s kchunk, (s+1) kchunk).
+// part[(s * Mtot + row) * r + k] (fp64) for row < Mtot, k < r.
+template <int R, int MODE>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+k_skinny_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t Mtot,
+            int64_t ktiles, int nsplit, int64_t kchunk, int ns, int flush, int r, double* __restrict__ part,
+            int evict_first) {
+  using C = TcCfg<R>;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)ns * C::SB);
+  uint64_t* empty = full + ns;
+  uint64_t* lo_full = empty + ns;
+  uint64_t* lo_empty = lo_full + TC_T;
+  uint64_t* acc_full = lo_empty + TC_T;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    tmem_alloc(tmem_slot, C::TMEM_COLS);
+  } else if (warp == 1 && lane == 0) {
+    for (int s = 0; s < ns; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int t = 0; t < TC_T; ++t) {
+      mbar_init(&lo_full[t], 4);
+      mbar_init(&lo_empty[t], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  const int64_t nmb = (Mtot + TC_BM - 1) / TC_BM;
+  const int64_t nunits = nmb * nsplit;
+
+  if (warp == 0) {
+    // ======================= TMA producer =======================
+    if (lane == 0) {
+      prefetch_tmap(&tmA);
+      prefetch_tmap(&tmB);
+      const uint64_t pol = evict_first ? policy_evict_first() : policy_evict_normal();
+      const uint64_t polB = policy_evict_normal();
+      int64_t j = 0;
+      for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int64_t mb = u / nsplit, sp = u % nsplit;
+        const int64_t k0 = sp * kchunk, k1 = ((k0 + kchunk < ktiles) ? k0 + kchunk : ktiles);
+        for (int64_t kt = k0; kt < k1; ++kt, ++j) {
+          const int s = (int)(j % ns);
+          const uint32_t ph = (uint32_t)((j / ns) & 1);
+          mbar_wait(&empty[s], ph ^ 1u);
+          mbar_expect_tx(&full[s], C::SB);
+          unsigned char* st = smem + (size_t)s * C::SB;
+          if (MODE == 0) {
+            tma_load_2d(st, &tmA, (int)(kt * TC_BK), (int)(mb * TC_BM), &full[s], pol);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              tma_load_2d(st + q * 4096, &tmA, (int)(mb * TC_BM + 32 * q), (int)(kt * TC_BK), &full[s], pol);
+          }
+          tma_load_2d(st + TC_ABYTES, &tmB, (int)(kt * TC_BK), 0, &full[s], polB);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer =======================
+    if (lane == 0) {
+      constexpr uint32_t id1 = idesc_tf32(TC_BM, C::N1, false, false);
+      constexpr uint32_t id2 = idesc_tf32(TC_BM, R, false, false);
+      int64_t j = 0, g = 0;
+      for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int64_t sp = u % nsplit;
+        const int64_t k0 = sp * kchunk, k1 = ((k0 + kchunk < ktiles) ? k0 + kchunk : ktiles);
+        for (int64_t kt = k0; kt < k1; ++kt, ++j) {
+          const int64_t i = kt - k0;  // tile index within the unit
+          const bool gfirst = (i % flush) == 0;
+          const bool glast = ((i + 1) % flush) == 0 || kt + 1 == k1;
+          const int a = (int)(g & 1);
+          if (gfirst) {
+            mbar_wait(&acc_empty[a], (uint32_t)(((g >> 1) & 1) ^ 1));
+            tc_fence_after();
+          }
+          const int s = (int)(j % ns);
+          const uint32_t ph = (uint32_t)((j / ns) & 1);
+          const int t = (int)(j % TC_T);
+          const uint32_t pht = (uint32_t)((j / TC_T) & 1);
+          mbar_wait(&full[s], ph);
+          mbar_wait(&lo_full[t], pht);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + (size_t)s * C::SB);
+          const uint32_t sb = sa + TC_ABYTES;
+          const uint32_t dcol = tbase + C::TMEM_D + (uint32_t)a * C::N1;
+#pragma unroll
+          for (int kk = 0; kk < TC_BK / 8; ++kk) {
+            const uint64_t bdesc = umma_desc_sw128(sb + kk * 32, 16, 1024);
+            if (MODE == 0)  // A_hi = the raw X tile in shared memory (K-major)
+              mma_tf32_ss(dcol, umma_desc_sw128(sa + kk * 32, 16, 1024), bdesc, id1, (gfirst && kk == 0) ? 0u : 1u);
+            else            // A_hi = X^T staged in TMEM by the converters
+              mma_tf32_ts(dcol, tbase + C::TMEM_HI + (uint32_t)t * 32 + kk * 8, bdesc, id1, (gfirst && kk == 0) ? 0u : 1u);
+            mma_tf32_ts(dcol, tbase + C::TMEM_LO + (uint32_t)t * 32 + kk * 8, bdesc, id2, 1u);
+          }
+          mma_commit(&empty[s]);
+          mma_commit(&lo_empty[t]);
+          if (glast) {
+            mma_commit(&acc_full[a]);
+            ++g;
+          }
+        }
+      }
+    }
+  } else if (warp < 6) {
+    // ======================= converters: A_lo -> TMEM =======================
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+    int64_t j = 0;
+    for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+      const int64_t sp = u % nsplit;
+      const int64_t k0 = sp * kchunk, k1 = ((k0 + kchunk < ktiles) ? k0 + kchunk : ktiles);
+      for (int64_t kt = k0; kt < k1; ++kt, ++j) {
+        const int s = (int)(j % ns);
+        const uint32_t ph = (uint32_t)((j / ns) & 1);
+        const int t = (int)(j % TC_T);
+        const uint32_t pht = (uint32_t)((j / TC_T) & 1);
+        mbar_wait(&full[s], ph);
+        mbar_wait(&lo_empty[t], pht ^ 1u);
+        tc_fence_after();
+        const unsigned char* st = smem + (size_t)s * C::SB;
+        uint32_t v[32];
+        if (MODE == 0) {
+          // row rho = 32 q + lane of the [128][32] K-major tile
+          const int rho = 32 * q + lane;
+          const unsigned char* row = st + rho * 128;
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) {
+            const float4 x = *reinterpret_cast<const float4*>(row + ((ch ^ (rho & 7)) << 4));
+            v[4 * ch + 0] = __float_as_uint(tf32_lo(x.x));
+            v[4 * ch + 1] = __float_as_uint(tf32_lo(x.y));
+            v[4 * ch + 2] = __float_as_uint(tf32_lo(x.z));
+            v[4 * ch + 3] = __float_as_uint(tf32_lo(x.w));
+          }
+        } else {
+          // column c = lane of box q ([32 K rows][32 cols]); K index = row i
+          const unsigned char* box = st + q * 4096 + (lane & 3) * 4;
+          const int chk = lane >> 2;
+          uint32_t vh[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float x = *reinterpret_cast<const float*>(box + i * 128 + ((chk ^ (i & 7)) << 4));
+            vh[i] = __float_as_uint(x);
+            v[i] = __float_as_uint(tf32_lo(x));
+          }
+          tmem_st32(tbase + C::TMEM_HI + (uint32_t)t * 32 + lane_off, vh);
+        }
+        tmem_st32(tbase + C::TMEM_LO + (uint32_t)t * 32 + lane_off, v);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&lo_full[t]);
+      }
+    }
+  } else {
+    // ======================= epilogue: TMEM -> fp64 partials =======================
+    const int q = warp & 3;
+    const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+    int64_t g = 0;
+    for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+      const int64_t mb = u / nsplit, sp = u % nsplit;
+      const int64_t k0 = sp * kchunk, k1 = ((k0 + kchunk < ktiles) ? k0 + kchunk : ktiles);
+      const int64_t ngr = (k1 - k0 + flush - 1) / flush;
+      double acc[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) acc[k] = 0.0;
+      for (int64_t gi = 0; gi < ngr; ++gi, ++g) {
+        const int a = (int)(g & 1);
+        mbar_wait(&acc_full[a], (uint32_t)((g >> 1) & 1));
+        tc_fence_after();
+        const uint32_t d = tbase + C::TMEM_D + (uint32_t)a * C::N1 + lane_off;
+#pragma unroll
+        for (int c0 = 0; c0 < R; c0 += 16) {
+          uint32_t hi[16], lo[16];
+          tmem_ld16(d + c0, hi);
+          tmem_ld16(d + R + c0, lo);
+          tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 16; ++k) acc[c0 + k] += (double)__uint_as_float(hi[k]) + (double)__uint_as_float(lo[k]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[a]);
+      }
+      const int64_t row = mb * TC_BM + 32 * q + lane;
+      if (row < Mtot) {
+        double* dst = part + ((int64_t)sp * Mtot + row) * r;
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+          if (k < r) dst[k] = acc[k];
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tbase, C::TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------- updates ---
+constexpr int UPD_ROWS = 128;
+
+// W update for TC_ROWS rows per CTA: P = sum_s Ppart[s] (fixed order), Q (r x r,
+// reduced), W <- W o P / (W Q + eps) in fp64 (as k_wupdate), WcatT rows k < r:
+// hi = Wn, rows R + k: lo(Wn); Gpart[cta] = Wn^T Wn over the CTA's rows.
+template <int R>
+__global__ void __launch_bounds__(UPD_ROWS)
+k_tc_wupdate(float* __restrict__ W, int64_t m, int r, const double* __restrict__ Ppart, int nP,
+             const double* __restrict__ Qred, float eps, float* __restrict__ WcatT, int64_t ldw,
+             double* __restrict__ Gpart) {
+  __shared__ double Qs[R * R];
+  __shared__ float Wn[UPD_ROWS][R + 1];
+  const int rr = r * r;
+  for (int t = threadIdx.x; t < R * R; t += blockDim.x) {
+    const int k = t / R, l = t % R;
+    Qs[t] = (k < r && l < r) ? Qred[k * r + l] : 0.0;
+  }
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * UPD_ROWS + threadIdx.x;
+  if (i < m) {
+    const int64_t mr = m * r;
+    double w[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) w[k] = (k < r) ? (double)W[i * r + k] : 0.0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      float wn = 0.0f;
+      if (k < r) {
+        double p = 0.0;
+        for (int b = 0; b < nP; ++b) p += Ppart[(int64_t)b * mr + i * r + k];
+        double d = 0.0;
+#pragma unroll
+        for (int l = 0; l < R; ++l) d += w[l] * Qs[l * R + k];
+        wn = (float)mu_quot(w[k], p, d, (double)eps);
+      }
+      Wn[threadIdx.x][k] = wn;
+    }
+    for (int k = 0; k < r; ++k) W[i * r + k] = Wn[threadIdx.x][k];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const float v = Wn[threadIdx.x][k];
+      WcatT[(int64_t)k * ldw + i] = v;
+      WcatT[(int64_t)(R + k) * ldw + i] = tf32_lo(v);
+    }
+  } else {
+    for (int k = 0; k < R; ++k) Wn[threadIdx.x][k] = 0.0f;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < rr; t += blockDim.x) {
+    const int k = t / r, l = t % r;
+    double s = 0.0;
+    for (int qq = 0; qq < UPD_ROWS; ++qq) s += (double)Wn[qq][k] * (double)Wn[qq][l];
+    Gpart[(int64_t)blockIdx.x * rr + t] = s;
+  }
+}
+
+// H update (or prep: update = false keeps H) for UPD_ROWS columns per CTA:
+// S = sum_s Spart[s][j] (fixed order), E = G H (fp32, G reduced in fp64),
+// H <- H o S / (E + eps); Hcat rows k < r: hi = Hn, rows R + k: lo(Hn);
+// Qpart[cta] = Hn Hn^T over the CTA's columns.
+template <int R>
+__global__ void __launch_bounds__(UPD_ROWS)
+k_tc_hupdate(float* __restrict__ H, int64_t n, int r, const double* __restrict__ Spart, int nS,
+             const double* __restrict__ Gred, float eps, bool update, float* __restrict__ Hcat, int64_t ldh,
+             double* __restrict__ Qpart) {
+  __shared__ float Gs[R * R];
+  __shared__ float Hn[R][UPD_ROWS + 1];
+  const int rr = r * r;
+  if (update)
+    for (int t = threadIdx.x; t < R * R; t += blockDim.x) {
+      const int k = t / R, l = t % R;
+      Gs[t] = (k < r && l < r) ? (float)Gred[k * r + l] : 0.0f;
+    }
+  __syncthreads();
+  const int64_t j = (int64_t)blockIdx.x * UPD_ROWS + threadIdx.x;
+  if (j < n) {
+    float h[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) h[k] = (k < r) ? H[(int64_t)k * n + j] : 0.0f;
+    const int64_t nr = n * r;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      float hn = h[k];
+      if (update && k < r) {
+        double sd = 0.0;
+        for (int b = 0; b < nS; ++b) sd += Spart[(int64_t)b * nr + j * r + k];
+        float e = 0.0f;
+#pragma unroll
+        for (int l = 0; l < R; ++l) e = fmaf(Gs[k * R + l], h[l], e);
+        hn = mu_quot(h[k], (float)sd, e, eps);
+      }
+      if (k >= r) hn = 0.0f;
+      Hn[k][threadIdx.x] = hn;
+      if (update && k < r) H[(int64_t)k * n + j] = hn;
+      Hcat[(int64_t)k * ldh + j] = hn;
+      Hcat[(int64_t)(R + k) * ldh + j] = tf32_lo(hn);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < R; ++k) Hn[k][threadIdx.x] = 0.0f;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < rr; t += blockDim.x) {
+    const int k = t / r, l = t % r;
+    double s = 0.0;
+    for (int c = 0; c < UPD_ROWS; ++c) s += (double)Hn[k][c] * (double)Hn[l][c];
+    Qpart[(int64_t)blockIdx.x * rr + t] = s;
+  }
+}
+
+__global__ void k_tc_sum(const double* __restrict__ part, int nparts, int len, double* __restrict__ out) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < len; t += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nparts; ++b) s += part[(int64_t)b * len + t];
+    out[t] = s;
+  }
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 g_enc = nullptr;
+
+cudaError_t enc() {
+  if (g_enc) return cudaSuccess;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult qr;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr);
+  if (e != cudaSuccess) return e;
+  if (qr != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+  g_enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return cudaSuccess;
+}
+
+cudaError_t map2d(CUtensorMap* map, const float* base, uint64_t cols, uint64_t rows, uint64_t ld, uint32_t bc,
+                  uint32_t br) {
+  cudaError_t e = enc();
+  if (e != cudaSuccess) return e;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * sizeof(float)};
+  cuuint32_t box[2] = {bc, br};
+  cuuint32_t es[2] = {1, 1};
+  CUresult res = g_enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return res == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+int rcls(int r) { return r <= 16 ? 16 : 32; }
+
+template <int R>
+int tc_stages() {
+  int s = (int)((227u * 1024u - 2048u) / TcCfg<R>::SB);
+  return std::min(s, 8);
+}
+template <int R>
+size_t tc_smem(int ns) {
+  return (size_t)ns * TcCfg<R>::SB + 2048;
+}
+
+// split-K choice: units = nmb * nsplit spread over `grid` persistent CTAs;
+// smallest nsplit whose wave efficiency is >= 0.9 with >= 8 K tiles per unit.
+void pick_split(int64_t nmb, int64_t ktiles, int grid, int* nsplit, int64_t* kchunk) {
+  int best = 1;
+  double beff = -1.0;
+  for (int s = 1; s <= 64; ++s) {
+    int64_t kc = (ktiles + s - 1) / s;
+    if (s > 1 && kc < 8) break;
+    int64_t ns = (ktiles + kc - 1) / kc;
+    int64_t units = nmb * ns;
+    int64_t waves = (units + grid - 1) / grid;
+    double eff = (double)units / (double)(waves * grid);
+    if (eff > beff + 1e-9) {
+      beff = eff;
+      best = (int)ns;
+    }
+    if (eff >= 0.9) break;
+  }
+  *nsplit = best;
+  *kchunk = (ktiles + best - 1) / best;
+}
+
+template <int R, int MODE>
+cudaError_t launch_skinny(const CUtensorMap& ma, const CUtensorMap& mb, int64_t Mtot, int64_t ktiles, int nsplit,
+                          int64_t kchunk, int grid, int r, double* part, int evict_first, cudaStream_t st) {
+  const int ns = tc_stages<R>();
+  const size_t sm = tc_smem<R>(ns);
+  cudaError_t e = cudaFuncSetAttribute(k_skinny_tc<R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  k_skinny_tc<R, MODE><<<grid, TC_THREADS, sm, st>>>(ma, mb, Mtot, ktiles, nsplit, kchunk, ns, 32, r, part,
+                                                     evict_first);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- public ----
+bool tc_supported(int64_t m, int64_t n, int r, int64_t ldx, const void* X) {
+  if (r < 1 || r > 32) return false;
+  if (m < 256 || n < 256) return false;  // short-wide unfoldings take the fused 1-pass kernels
+  if ((ldx & 3) != 0) return false;
+  if ((reinterpret_cast<uintptr_t>(X) & 15) != 0) return false;
+  return true;
+}
+
+TcPlan plan_tc(int64_t m, int64_t n, int r, int num_sms) {
+  TcPlan p;
+  p.m = m;
+  p.n = n;
+  p.r = r;
+  p.R = rcls(r);
+  p.grid = num_sms;
+  p.ldh = (n + 3) & ~int64_t(3);
+  p.ldw = (m + 3) & ~int64_t(3);
+  pick_split((m + TC_BM - 1) / TC_BM, (n + TC_BK - 1) / TC_BK, num_sms, &p.splitW, &p.kchW);
+  pick_split((n + TC_BM - 1) / TC_BM, (m + TC_BK - 1) / TC_BK, num_sms, &p.splitH, &p.kchH);
+  p.nG = (int)((m + UPD_ROWS - 1) / UPD_ROWS);
+  p.nQ = (int)((n + UPD_ROWS - 1) / UPD_ROWS);
+  size_t o = 0;
+  auto take = [&](size_t b) {
+    size_t at = o;
+    o = (o + b + 255) & ~size_t(255);
+    return at;
+  };
+  p.off_hcat = take(sizeof(float) * (size_t)(2 * p.R) * p.ldh);
+  p.off_wcat = take(sizeof(float) * (size_t)(2 * p.R) * p.ldw);
+  p.off_P = take(sizeof(double) * (size_t)p.splitW * m * r);
+  p.off_S = take(sizeof(double) * (size_t)p.splitH * n * r);
+  p.off_G = take(sizeof(double) * (size_t)p.nG * r * r);
+  p.off_Q = take(sizeof(double) * (size_t)p.nQ * r * r);
+  p.off_Gred = take(sizeof(double) * (size_t)r * r);
+  p.off_Qred = take(sizeof(double) * (size_t)r * r);
+  p.bytes = o;
+  return p;
+}
+
+cudaError_t tc_prepare(const TcPlan& p, const float* X, int64_t ldx, float* H, char* ws, TcMaps* maps,
+                       cudaStream_t st) {
+  float* Hcat = reinterpret_cast<float*>(ws + p.off_hcat);
+  float* Wcat = reinterpret_cast<float*>(ws + p.off_wcat);
+  cudaError_t e;
+  const uint32_t N1 = 2u * (uint32_t)p.R;
+  if ((e = map2d(&maps->xw, X, p.n, p.m, ldx, 32, TC_BM))) return e;
+  if ((e = map2d(&maps->xh, X, p.n, p.m, ldx, 32, 32))) return e;
+  if ((e = map2d(&maps->hcat, Hcat, p.n, N1, p.ldh, 32, N1))) return e;
+  if ((e = map2d(&maps->wcat, Wcat, p.m, N1, p.ldw, 32, N1))) return e;
+  // zero the padded rank rows once (never written afterwards)
+  if ((e = cudaMemsetAsync(Hcat, 0, sizeof(float) * (size_t)N1 * p.ldh, st))) return e;
+  if ((e = cudaMemsetAsync(Wcat, 0, sizeof(float) * (size_t)N1 * p.ldw, st))) return e;
+  double* Qpart = reinterpret_cast<double*>(ws + p.off_Q);
+  const unsigned g = (unsigned)p.nQ;
+  if (p.R == 16)
+    k_tc_hupdate<16><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, nullptr, 0, nullptr, 0.f, false, Hcat, p.ldh, Qpart);
+  else
+    k_tc_hupdate<32><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, nullptr, 0, nullptr, 0.f, false, Hcat, p.ldh, Qpart);
+  return cudaGetLastError();
+}
+
+cudaError_t tc_sum_Q(const TcPlan& p, char* ws, cudaStream_t st) {
+  const int len = p.r * p.r;
+  k_tc_sum<<<(len + 127) / 128, 128, 0, st>>>(reinterpret_cast<double*>(ws + p.off_Q), p.nQ, len,
+                                              reinterpret_cast<double*>(ws + p.off_Qred));
+  return cudaGetLastError();
+}
+
+cudaError_t tc_pass_w(const TcPlan& p, const TcMaps& mp, char* ws, int evict_first, cudaStream_t st) {
+  double* P = reinterpret_cast<double*>(ws + p.off_P);
+  const int64_t kt = (p.n + TC_BK - 1) / TC_BK;
+  if (p.R == 16) return launch_skinny<16, 0>(mp.xw, mp.hcat, p.m, kt, p.splitW, p.kchW, p.grid, p.r, P, evict_first, st);
+  return launch_skinny<32, 0>(mp.xw, mp.hcat, p.m, kt, p.splitW, p.kchW, p.grid, p.r, P, evict_first, st);
+}
+
+cudaError_t tc_wupdate(const TcPlan& p, float* W, float eps, char* ws, cudaStream_t st) {
+  const double* P = reinterpret_cast<const double*>(ws + p.off_P);
+  const double* Qr = reinterpret_cast<const double*>(ws + p.off_Qred);
+  float* Wcat = reinterpret_cast<float*>(ws + p.off_wcat);
+  double* G = reinterpret_cast<double*>(ws + p.off_G);
+  const unsigned g = (unsigned)p.nG;
+  if (p.R == 16)
+    k_tc_wupdate<16><<<g, UPD_ROWS, 0, st>>>(W, p.m, p.r, P, p.splitW, Qr, eps, Wcat, p.ldw, G);
+  else
+    k_tc_wupdate<32><<<g, UPD_ROWS, 0, st>>>(W, p.m, p.r, P, p.splitW, Qr, eps, Wcat, p.ldw, G);
+  cudaError_t e = cudaGetLastError();
+  if (e) return e;
+  const int len = p.r * p.r;
+  k_tc_sum<<<(len + 127) / 128, 128, 0, st>>>(G, p.nG, len, reinterpret_cast<double*>(ws + p.off_Gred));
+  return cudaGetLastError();
+}
+
+cudaError_t tc_pass_h(const TcPlan& p, const TcMaps& mp, char* ws, int evict_first, cudaStream_t st) {
+  double* S = reinterpret_cast<double*>(ws + p.off_S);
+  const int64_t kt = (p.m + TC_BK - 1) / TC_BK;
+  if (p.R == 16) return launch_skinny<16, 1>(mp.xh, mp.wcat, p.n, kt, p.splitH, p.kchH, p.grid, p.r, S, evict_first, st);
+  return launch_skinny<32, 1>(mp.xh, mp.wcat, p.n, kt, p.splitH, p.kchH, p.grid, p.r, S, evict_first, st);
+}
+
+cudaError_t tc_hupdate(const TcPlan& p, float* H, float eps, char* ws, cudaStream_t st) {
+  const double* S = reinterpret_cast<const double*>(ws + p.off_S);
+  const double* Gr = reinterpret_cast<const double*>(ws + p.off_Gred);
+  float* Hcat = reinterpret_cast<float*>(ws + p.off_hcat);
+  double* Q = reinterpret_cast<double*>(ws + p.off_Q);
+  const unsigned g = (unsigned)p.nQ;
+  if (p.R == 16)
+    k_tc_hupdate<16><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, S, p.splitH, Gr, eps, true, Hcat, p.ldh, Q);
+  else
+    k_tc_hupdate<32><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, S, p.splitH, Gr, eps, true, Hcat, p.ldh, Q);
+  return cudaGetLastError();
+}
+
+}  // namespace ntt

@@ -1,0 +1,44 @@
+// mu_tc.h -- tensor-core (tcgen05 kind::tf32, 3xTF32) 2-pass MU iteration for
+// tall / square X (mu_tc.cu).  Internal to libntt.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ntt {
+
+struct TcPlan {
+  int64_t m = 0, n = 0;
+  int r = 0, R = 0;      // rank and its padded class (16 or 32)
+  int grid = 0;          // persistent CTAs of the GEMM passes
+  int64_t ldh = 0, ldw = 0;
+  int splitW = 1, splitH = 1;   // split-K factors of the two passes
+  int64_t kchW = 0, kchH = 0;   // K tiles (of 32) per split
+  int nG = 0, nQ = 0;           // Gram partial counts (W update CTAs, H update CTAs)
+  size_t off_hcat = 0, off_wcat = 0, off_P = 0, off_S = 0, off_G = 0, off_Q = 0, off_Gred = 0, off_Qred = 0;
+  size_t bytes = 0;
+};
+
+struct TcMaps {
+  CUtensorMap xw, xh, hcat, wcat;
+};
+
+// Shapes the TC path takes: r <= 32, m, n >= 256, X 16-byte aligned with ldx % 4 == 0.
+bool tc_supported(int64_t m, int64_t n, int r, int64_t ldx, const void* X);
+TcPlan plan_tc(int64_t m, int64_t n, int r, int num_sms);
+
+// Tensor maps, Hcat = [H; lo(H)] and Q partials of the initial H.
+cudaError_t tc_prepare(const TcPlan& p, const float* X, int64_t ldx, float* H, char* ws, TcMaps* maps,
+                       cudaStream_t st);
+// Q = sum of the H-side Gram partials (fixed order)
+cudaError_t tc_sum_Q(const TcPlan& p, char* ws, cudaStream_t st);
+// split-K partials of P = X H^T
+cudaError_t tc_pass_w(const TcPlan& p, const TcMaps& mp, char* ws, int evict_first, cudaStream_t st);
+// W <- W o P / (W Q + eps); Wcat; G = W^T W (reduced)
+cudaError_t tc_wupdate(const TcPlan& p, float* W, float eps, char* ws, cudaStream_t st);
+// split-K partials of S = W^T X
+cudaError_t tc_pass_h(const TcPlan& p, const TcMaps& mp, char* ws, int evict_first, cudaStream_t st);
+// H <- H o S / (G H + eps); Hcat; Q partials of the new H
+cudaError_t tc_hupdate(const TcPlan& p, float* H, float eps, char* ws, cudaStream_t st);
+
+}  // namespace ntt

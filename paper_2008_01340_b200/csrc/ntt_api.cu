@@ -18,6 +18,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "mu_fused.h"
+#include "mu_tc.h"
 
 using namespace ntt;
 
@@ -67,6 +68,7 @@ struct ntt_handle_s {
   int device = 0;
   cudaStream_t stream = nullptr;
   int num_sms = 148;
+  int64_t l2_bytes = 126 << 20;
   std::string err;
   int64_t launches = 0;
   // internal scratch (grown, never shrunk)
@@ -262,7 +264,9 @@ struct MuPlan {
   int nwup;       // W-update CTAs
   int fgrid;      // fused kernel CTAs
   int fparts;     // fused kernel partial slots
-  size_t off_P, off_Q, off_G, off_S, bytes;
+  bool tc;        // tensor-core 2-pass path (mu_tc.cu) for tall / square X
+  TcPlan tp;
+  size_t off_P, off_Q, off_G, off_S, off_tc, bytes;
 };
 
 MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, int nranks) {
@@ -292,6 +296,13 @@ MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, int nranks) {
   o = align_up(o + sizeof(double) * (size_t)(nG * r * r));
   p.off_S = o;  // reduced (m r + r r) vector for the distributed all-reduce
   o = align_up(o + sizeof(double) * (size_t)(m * r + r * r));
+  // shape-level eligibility of the tensor-core path (alignment re-checked at run time)
+  p.tc = nranks == 1 && !p.fused && tc_supported(m, n, r, n, nullptr) && !getenv("NTT_NO_TC");
+  p.off_tc = o;
+  if (p.tc) {
+    p.tp = plan_tc(m, n, r, num_sms);
+    o = align_up(o + p.tp.bytes);
+  }
   p.bytes = o;
   (void)nranks;
   return p;
@@ -337,6 +348,26 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
       const int mode = kFusedUpdate | ((it + 1 < iters) ? kFusedAcc : 0);
       PLAUNCH(h, 0, 4.0 * (double)(m + 2 * r) * (double)n,
               launch_fused(X, ldx, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, fg, st));
+      if (dev_trace) LAUNCH(h, launch_objective(X, ldx, m, n, W, H, r, dev_trace + (int64_t)it * nobj, st));
+    }
+    return NTT_OK;
+  }
+
+  if (p.tc && !dist && tc_supported(m, n, r, ldx, X)) {
+    // tensor-core 2-pass iteration (mu_tc.cu): X > L2 streams evict-first
+    const TcPlan& tp = p.tp;
+    char* tws = scratch + p.off_tc;
+    const int ef = (double)m * (double)ldx * 4.0 > 0.6 * (double)h->l2_bytes ? 1 : 0;
+    TcMaps maps;
+    LAUNCH(h, tc_prepare(tp, X, ldx, H, tws, &maps, st));
+    for (int it = 0; it < iters; ++it) {
+      LAUNCH(h, tc_sum_Q(tp, tws, st));
+      PLAUNCH(h, 6, 4.0 * (double)(m + 2 * tp.R) * (double)n, tc_pass_w(tp, maps, tws, ef, st));
+      PLAUNCH(h, 2, 8.0 * (double)tp.splitW * m * r + 8.0 * m * r + 4.0 * 2 * tp.R * m,
+              tc_wupdate(tp, W, eps, tws, st));
+      PLAUNCH(h, 7, 4.0 * (double)(n + 2 * tp.R) * (double)m, tc_pass_h(tp, maps, tws, ef, st));
+      PLAUNCH(h, 4, 8.0 * (double)tp.splitH * n * r + 4.0 * (3 * tp.R + r) * (double)n,
+              tc_hupdate(tp, H, eps, tws, st));
       if (dev_trace) LAUNCH(h, launch_objective(X, ldx, m, n, W, H, r, dev_trace + (int64_t)it * nobj, st));
     }
     return NTT_OK;
@@ -623,6 +654,7 @@ static ntt_status create_common(ntt_handle* out, int device, void* stream) {
   h->device = device;
   h->stream = reinterpret_cast<cudaStream_t>(stream);
   h->num_sms = prop.multiProcessorCount;
+  h->l2_bytes = prop.l2CacheSize;
   *out = h;
   return NTT_OK;
 }

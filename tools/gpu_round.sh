@@ -1,0 +1,3 @@
+timeout 600 python -m pytest tests/test_gpu_tc.py -q 2>&1 | tail -5
+timeout 300 python tools/bench_nmf.py config2 20 2>&1 | tail -1
+timeout 300 python tools/bench_nmf.py config5 5 2>&1 | tail -1
