@@ -174,6 +174,13 @@ ntt_status ntt_profile_get(ntt_handle h, int cls, int64_t* launches, double* tot
 ntt_status ntt_profile_get_step(ntt_handle h, int cls, int step, int64_t* launches,
                                 double* total_ms, double* total_bytes);
 
+/* Diagnostics: with NTT_PERSIST_TRACE set when the handle is created, the
+ * persistent fused MU kernel records, per pass p, 4 globaltimer stamps of CTA 0
+ * (pass start, partials written, after barrier 1, after barrier 2) at
+ * [4p .. 4p+3] of the returned host-readable array (4096 passes max; pass 0 is
+ * the prologue).  NULL otherwise.  Synchronises the handle's stream.         */
+const unsigned long long* ntt_debug_persist_trace(ntt_handle h);
+
 /* ----------------------------------------------------- multi-GPU (NCCL) ----
  * One process per GPU.  Rank 0 calls ntt_get_unique_id and broadcasts the 128
  * bytes (e.g. over a torch process group); every rank then calls

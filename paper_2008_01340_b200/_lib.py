@@ -42,6 +42,7 @@ SIGNATURES = {
     "ntt_dist_rank": (c_int, [c_p]),
     "ntt_dist_size": (c_int, [c_p]),
     "ntt_dist_block": (c_i64, [c_i64, c_int, c_int, ctypes.POINTER(c_i64)]),
+    "ntt_debug_persist_trace": (ctypes.POINTER(ctypes.c_uint64), [c_p]),
 }
 
 _lib = None

@@ -21,6 +21,7 @@
 #include <cuda.h>
 #include <cstdio>
 #include <cstdlib>
+#include <utility>
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -106,11 +107,158 @@ __device__ __forceinline__ float2 bc(float a) { return make_float2(a, a); }
 // transposed per-warp Hn tile: column c (0..127), rank index k (0..7)
 __device__ __forceinline__ int hn_idx(int c, int k) { return c * 8 + k + 4 * (c >> 2) + 4 * (c >> 5); }
 
+// ---------------------------------------------------------------------------
+// Persistent mode (PersistArgs.iters > 0): ONE cooperative launch runs the whole
+// MU loop of a TT step -- the acc-only prologue pass (P0 = X H0^T, Q0 = H0 H0^T)
+// and `iters` fused passes.  Between passes every CTA writes its fp64 (P, Q)
+// partial ([P (m r) | Q (r r)], L doubles) to part[cta], then
+//   grid barrier -> CTA b sums slice b of the L entries over all CTAs (fixed
+//   order) into red -> grid barrier -> every CTA computes the SAME W update
+//   W <- W o P / (W Q + eps) (fp64, reading R4) and G = W^T W in its own smem.
+// This replaces the per-iteration W-update launch and the pass launch (~20 us of
+// launch/ramp/partial traffic per iteration on small TT steps).
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void pstamp(const PersistArgs& pa, int it, int ph) {
+  if (pa.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    pa.trace[it * 4 + ph] = t;
+  }
+}
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// grid-wide barrier over co-resident CTAs (cooperative launch).  The proxy fence
+// orders this thread's generic global writes (H) before later TMA (async-proxy)
+// reads of the same data by any CTA.
+__device__ __forceinline__ void grid_sync(unsigned* ctr, unsigned& epoch) {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  epoch += gridDim.x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    while (ld_acquire_gpu(ctr) < epoch) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Reduce the per-CTA partials and apply the W update in every CTA (see above).
+// Ws: [i * 8 + k] (rows >= m stay zero), Gs: [k * 8 + l]; scr: >= (L + 16) doubles + m*8 floats
+// + 256 doubles of smem.  Global reads are issued in independent batches (L2 latency is ~1 us).
+__device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int r, float eps, float* Ws, float* Gs,
+                             double* scr, int it) {
+  const int L = m * r + r * r;
+  const int T = blockDim.x, tid = threadIdx.x;
+  pstamp(pa, it, 1);
+  if (gridDim.x > 1) {
+    grid_sync(pa.ctr, epoch);
+    pstamp(pa, it, 2);
+    const int G = gridDim.x;
+    const int SL = (L + G - 1) / G;
+    const int e0 = blockIdx.x * SL;
+    const int ne = min(L, e0 + SL) - e0;
+    if (ne > 0) {
+      int C = T / ne;
+      C = C < 1 ? 1 : (C > 32 ? 32 : C);
+      for (int t = tid; t < ne * C; t += T) {
+        const int e = t % ne, c = t / ne;
+        const int g0 = (int)((int64_t)G * c / C), g1 = (int)((int64_t)G * (c + 1) / C);
+        const double* src = pa.part + e0 + e;
+        double a[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = 0.0;
+        for (int g = g0; g < g1; g += 8) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (g + q < g1) a[q] += __ldcg(src + (int64_t)(g + q) * L);
+        }
+        scr[c * ne + e] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+      }
+      __syncthreads();
+      for (int e = tid; e < ne; e += T) {
+        double sv = 0.0;
+        for (int c = 0; c < C; ++c) sv += scr[c * ne + e];
+        __stcg(pa.red + e0 + e, sv);
+      }
+    }
+    grid_sync(pa.ctr, epoch);
+  } else {
+    __syncthreads();  // single CTA: its own partial is the sum
+  }
+  pstamp(pa, it, 3);
+  const double* srcv = gridDim.x > 1 ? pa.red : pa.part;
+  for (int e0 = 0; e0 < L; e0 += 8 * T) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = e0 + q * T + tid;
+      v[q] = e < L ? __ldcg(srcv + e) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = e0 + q * T + tid;
+      if (e < L) scr[e] = v[q];
+    }
+  }
+  __syncthreads();
+  double* P = scr;           // m x r
+  double* Q = scr + m * r;   // r x r
+  float* Wn = reinterpret_cast<float*>(scr + L + 16);
+  double* Gp = scr + L + 16 + (m * 8 + 1) / 2 + 8;  // [C][64] Gram chunk partials
+  for (int e = tid; e < m * 8; e += T) {
+    const int i = e >> 3, k = e & 7;
+    float v = 0.0f;
+    if (k < r) {
+      double d = 0.0;
+      for (int l = 0; l < r; ++l) d += (double)Ws[i * 8 + l] * Q[l * r + k];
+      v = (float)mu_quot((double)Ws[i * 8 + k], P[i * r + k], d, (double)eps);
+    }
+    Wn[e] = v;
+  }
+  __syncthreads();
+  for (int e = tid; e < m * 8; e += T) Ws[e] = Wn[e];
+  // G = Wn^T Wn: 64 entries x C row chunks (fixed order), then combine
+  const int GC = T / 64 < 1 ? 1 : (T / 64 > 4 ? 4 : T / 64);
+  for (int t = tid; t < 64 * GC; t += T) {
+    const int e = t & 63, c = t >> 6;
+    const int k = e >> 3, l = e & 7;
+    const int i0 = m * c / GC, i1 = m * (c + 1) / GC;
+    double s0 = 0.0, s1 = 0.0;
+    if (k < r && l < r) {
+      int i = i0;
+      for (; i + 1 < i1; i += 2) {
+        s0 += (double)Wn[i * 8 + k] * (double)Wn[i * 8 + l];
+        s1 += (double)Wn[(i + 1) * 8 + k] * (double)Wn[(i + 1) * 8 + l];
+      }
+      if (i < i1) s0 += (double)Wn[i * 8 + k] * (double)Wn[i * 8 + l];
+    }
+    Gp[c * 64 + e] = s0 + s1;
+  }
+  __syncthreads();
+  for (int e = tid; e < 64; e += T) {
+    double sg = 0.0;
+    for (int c = 0; c < GC; ++c) sg += Gp[c * 64 + e];
+    Gs[e] = (float)sg;
+  }
+  if (blockIdx.x == 0)
+    for (int e = tid; e < m * r; e += T) pa.Wout[e] = Wn[(e / r) * 8 + (e % r)];
+  __syncthreads();
+}
+
 template <int R, int UX, int NWT, bool HDIRECT, int BNT>
 __global__ void __launch_bounds__((NWT + 1) * 32, 1)
 k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmH, int m, int64_t n, int r,
         const float* __restrict__ W, const double* __restrict__ Gpart, int nG, float eps, float* __restrict__ H,
-        double* __restrict__ Ppart, double* __restrict__ Qpart, int mode, int ns, int evict_first) {
+        double* __restrict__ Ppart, double* __restrict__ Qpart, int mode, int ns, int evict_first,
+        PersistArgs pa) {
   extern __shared__ unsigned char smem_raw[];
   // keep the shared address space visible to the compiler (LDS/STS, not generic LD/ST)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -138,15 +286,14 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   uint32_t* issued = reinterpret_cast<uint32_t*>(empty + ns);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const bool do_update = (mode & kFusedUpdate) != 0;
-  const bool do_acc = (mode & kFusedAcc) != 0;
+  const bool persist = pa.iters > 0;
 
   // ---- setup: W, G into smem; barriers
   for (int e = tid; e < MP * 8; e += (NWT + 1) * 32) {
     int i = e >> 3, k = e & 7;
     Ws[e] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
   }
-  if (do_update) {
+  if (!persist && (mode & kFusedUpdate)) {
     const int rr = r * r;
     for (int e = tid; e < 64; e += (NWT + 1) * 32) {
       int k = e >> 3, l = e & 7;
@@ -170,6 +317,15 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   const int64_t b = blockIdx.x;
   const int64_t J = (ntiles > b) ? (ntiles - b + gridDim.x - 1) / gridDim.x : 0;
 
+  unsigned epoch = 0;
+  const int nit = persist ? pa.iters + 1 : 1;
+  for (int it = 0; it < nit; ++it) {
+  // persistent: pass 0 = acc-only prologue, passes 1..iters update (+ acc except the last)
+  const int md = persist ? (it == 0 ? kFusedAcc : (kFusedUpdate | (it < pa.iters ? kFusedAcc : 0))) : mode;
+  const bool do_update = (md & kFusedUpdate) != 0;
+  const bool do_acc = (md & kFusedAcc) != 0;
+  const int64_t pbase = (int64_t)it * J;  // ring position of this pass's first tile
+  pstamp(pa, it, 0);
   if (warp == NWT) {
     // ================= TMA producer =================
     if (lane == 0) {
@@ -179,8 +335,9 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
       else
         asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
       for (int64_t j = 0; j < J; ++j) {
-        const int s = (int)(j % ns);
-        const uint32_t ph = (uint32_t)((j / ns) & 1);
+        const int64_t pos = pbase + j;
+        const int s = (int)(pos % ns);
+        const uint32_t ph = (uint32_t)((pos / ns) & 1);
         MBAR_WAIT(&empty[s], ph ^ 1u, 1, j);
         mbar_expect_tx(&full[s], SB);
         const int col0 = (int)((b + j * gridDim.x) * BNT);
@@ -191,11 +348,10 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
 #pragma unroll
           for (int bx = 0; bx < NB; ++bx) tma_load_2d(st + XB + bx * 1024, &tmH, col0 + bx * 32, 0, &full[s], policy);
         }
-        st_release_u32(issued, (uint32_t)(j + 1));
+        st_release_u32(issued, (uint32_t)(pos + 1));
       }
     }
-    return;
-  }
+  } else {
 
   // ================= consumer warps =================
   float* Hw = HnAll + warp * HN_FLOATS;
@@ -214,8 +370,9 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   const bool h1 = (lane >> 4) & 1, h0 = (lane >> 3) & 1;
 
   for (int64_t j = warp; j < J; j += NWT) {
-    const int s = (int)(j % ns);
-    const uint32_t ph = (uint32_t)((j / ns) & 1);
+    const int64_t pos = pbase + j;
+    const int s = (int)(pos % ns);
+    const uint32_t ph = (uint32_t)((pos / ns) & 1);
     const int64_t jt = (b + j * gridDim.x) * BNT;  // first column of the tile
     const int64_t c0 = jt + cq;
     // H columns c0..c0+CPL-1 of this tile (HDIRECT: independent of the stage, issued first)
@@ -247,7 +404,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
       long long t0 = clock64();
 #endif
       if (lane == 0) {
-        while (ld_acquire_u32(issued) <= (uint32_t)j) {
+        while (ld_acquire_u32(issued) <= (uint32_t)pos) {
           __nanosleep(64);
 #ifdef NTT_WATCHDOG
           if (clock64() - t0 > 4000000000LL) {
@@ -444,7 +601,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 
-  if (!do_acc) return;
+  if (do_acc) {
   // ---- fixed-order CTA reduction of the per-thread fp64 partials
   asm volatile("bar.sync 1, %0;" ::"r"(NWT * 32) : "memory");
   // red[w][rb][f], f = u*R + k flat (u = UX is the Q row)
@@ -453,6 +610,8 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   for (int v = 0; v < V4 / 4; ++v) red[((size_t)warp * 8 + rb) * V4 + cs * (V4 / 4) + v] = accd[v];
   asm volatile("bar.sync 1, %0;" ::"r"(NWT * 32) : "memory");
   const int mr = m * r, rr = r * r;
+  double* Pb = persist ? pa.part + b * (mr + rr) : Ppart + b * mr;
+  double* Qb = persist ? pa.part + b * (mr + rr) + mr : Qpart + b * rr;
   for (int e = tid; e < 8 * V; e += NWT * 32) {
     const int rbe = e / V, f = e % V;
     const int u = f / R, k = f % R;
@@ -462,9 +621,14 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
     if (isQ ? (row >= r) : (row >= m)) continue;
     double sum = 0.0;
     for (int w = 0; w < NWT; ++w) sum += red[((size_t)w * 8 + rbe) * V4 + f];
-    if (isQ) Qpart[b * rr + row * r + k] = sum;
-    else Ppart[b * mr + row * r + k] = sum;
+    if (isQ) Qb[row * r + k] = sum;
+    else Pb[row * r + k] = sum;
   }
+  }
+  }  // consumer warps
+  if (!persist || !do_acc) break;
+  persist_step(pa, epoch, m, r, eps, Ws, Gs, reinterpret_cast<double*>(stages), it);
+  }  // passes
 }
 
 
@@ -493,7 +657,8 @@ template <int MP>
 __global__ void __launch_bounds__(NTC, 2)
 k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmH, int m, int64_t n, int r,
           const float* __restrict__ W, const double* __restrict__ Gpart, int nG, float eps, float* __restrict__ H,
-          double* __restrict__ Ppart, double* __restrict__ Qpart, int mode, int ns, int evict_first) {
+          double* __restrict__ Ppart, double* __restrict__ Qpart, int mode, int ns, int evict_first,
+          PersistArgs pa) {
   extern __shared__ unsigned char smem_raw[];
   // keep the shared address space visible to the compiler (LDS/STS, not generic LD/ST)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -510,9 +675,8 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   uint64_t* empty = full + ns;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const bool do_update = (mode & kFusedUpdate) != 0;
-  const bool do_acc = (mode & kFusedAcc) != 0;
-  if (do_update) {
+  const bool persist = pa.iters > 0;
+  if (!persist && (mode & kFusedUpdate)) {
     const int rr = r * r;
     for (int e = tid; e < 64; e += NTC) {
       int k = e >> 3, l = e & 7;
@@ -539,6 +703,14 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   const int64_t b = blockIdx.x;
   const int64_t J = (ntiles > b) ? (ntiles - b + gridDim.x - 1) / gridDim.x : 0;
 
+  unsigned epoch = 0;
+  const int nit = persist ? pa.iters + 1 : 1;
+  for (int it = 0; it < nit; ++it) {
+  const int md = persist ? (it == 0 ? kFusedAcc : (kFusedUpdate | (it < pa.iters ? kFusedAcc : 0))) : mode;
+  const bool do_update = (md & kFusedUpdate) != 0;
+  const bool do_acc = (md & kFusedAcc) != 0;
+  const int64_t pbase = (int64_t)it * J;
+  pstamp(pa, it, 0);
   if (warp == NWC) {
     if (lane == 0) {
       uint64_t policy;
@@ -547,8 +719,9 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       else
         asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
       for (int64_t j = 0; j < J; ++j) {
-        const int s = (int)(j % ns);
-        const uint32_t ph = (uint32_t)((j / ns) & 1);
+        const int64_t pos = pbase + j;
+        const int s = (int)(pos % ns);
+        const uint32_t ph = (uint32_t)((pos / ns) & 1);
         MBAR_WAIT(&empty[s], ph ^ 1u, 3, j);
         mbar_expect_tx(&full[s], SB);
         const int col0 = (int)((b + j * gridDim.x) * BNC);
@@ -557,8 +730,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         tma_load_2d(st + XB, &tmH, col0, 0, &full[s], policy);
       }
     }
-    return;
-  }
+  } else {
 
   const int q = lane & 7, g = lane >> 3;   // phase A: columns 4q..4q+3, ranks 2g, 2g+1
   const int rb = lane & 7, cs = lane >> 3; // phase B: rows rb + 8u of a 32-row chunk, columns 8cs..8cs+7
@@ -572,8 +744,9 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   constexpr int NBAR = NWC * 32;
 
   for (int64_t j = 0; j < J; ++j) {
-    const int s = (int)(j % ns);
-    const uint32_t ph = (uint32_t)((j / ns) & 1);
+    const int64_t pos = pbase + j;
+    const int s = (int)(pos % ns);
+    const uint32_t ph = (uint32_t)((pos / ns) & 1);
     MBAR_WAIT(&full[s], ph, 4, j);
     const unsigned char* st = stages + (size_t)s * SB;
     const int64_t jt = (b + j * gridDim.x) * BNC;
@@ -704,9 +877,11 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 
-  if (!do_acc) return;
+  if (do_acc) {
   // P: lane holds flat f = u*8 + k in [8 cs, 8 cs + 8) of sub-chunk h, rows warp*RW + 32h + rb + 8u
   const int mr = m * r, rr = r * r;
+  double* Pb = persist ? pa.part + b * (mr + rr) : Ppart + b * mr;
+  double* Qb = persist ? pa.part + b * (mr + rr) + mr : Qpart + b * rr;
 #pragma unroll
   for (int h = 0; h < NCH; ++h)
 #pragma unroll
@@ -714,7 +889,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       const int f = 8 * cs + v;
       const int u = f >> 3, k = f & 7;
       const int row = warp * RW + 32 * h + rb + 8 * u;
-      if (row < m && k < r) Ppart[b * mr + row * r + k] = accd[h][v];
+      if (row < m && k < r) Pb[row * r + k] = accd[h][v];
     }
   // Q rows 2w, 2w+1, column rb: sum the 4 column slices
   qd0 += __shfl_xor_sync(0xffffffffu, qd0, 16);
@@ -722,9 +897,14 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   qd1 += __shfl_xor_sync(0xffffffffu, qd1, 16);
   qd1 += __shfl_xor_sync(0xffffffffu, qd1, 8);
   if (cs == 0 && rb < r) {
-    if (2 * warp < r) Qpart[b * rr + (2 * warp) * r + rb] = qd0;
-    if (2 * warp + 1 < r) Qpart[b * rr + (2 * warp + 1) * r + rb] = qd1;
+    if (2 * warp < r) Qb[(2 * warp) * r + rb] = qd0;
+    if (2 * warp + 1 < r) Qb[(2 * warp + 1) * r + rb] = qd1;
   }
+  }
+  }  // consumer warps
+  if (!persist || !do_acc) break;
+  persist_step(pa, epoch, m, r, eps, Wc, Gs, reinterpret_cast<double*>(stages), it);
+  }  // passes
 }
 
 size_t fixed_bytes_c(int MP) {
@@ -737,17 +917,34 @@ int stages_c(int MP) {
   return ns > 12 ? 12 : ns;
 }
 
+// cooperative launch (all CTAs co-resident) for the persistent mode, plain otherwise
+template <typename... KArgs, typename... Args>
+cudaError_t launch_maybe_coop(void (*kern)(KArgs...), int grid, int threads, size_t smem, cudaStream_t st,
+                              bool coop, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = coop ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 template <int MP>
 cudaError_t launch_c(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_t n, int r, const float* W,
                      const double* Gpart, int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
-                     int evict_first, cudaStream_t st) {
+                     int evict_first, const PersistArgs& pa, cudaStream_t st) {
   const int ns = stages_c(MP);
   const size_t SB = (size_t)MP * 128 + 1024;
   const size_t smem = (size_t)ns * SB + fixed_bytes_c(MP);
   cudaError_t e = cudaFuncSetAttribute(k_fused_c<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_fused_c<MP><<<grid, NTC, smem, st>>>(mx, mh, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, ns, evict_first);
-  return cudaGetLastError();
+  return launch_maybe_coop(k_fused_c<MP>, grid, NTC, smem, st, pa.iters > 0, mx, mh, m, n, r, W, Gpart, nG, eps, H,
+                           Ppart, Qpart, mode, ns, evict_first, pa);
 }
 
 // ===========================================================================
@@ -1117,14 +1314,14 @@ int stages_for(int ux, int nwt, bool hd, int bnt) {
 template <int R, int UX, int NWT, bool HD, int BNT>
 cudaError_t launch_t(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_t n, int r, const float* W,
                      const double* Gpart, int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
-                     int evict_first, cudaStream_t st) {
+                     int evict_first, const PersistArgs& pa, cudaStream_t st) {
   const int ns = stages_for(UX, NWT, HD, BNT);
   const size_t SB = (size_t)(BNT / 32) * UX * 8 * 128 + (HD ? 0 : (size_t)(BNT / 32) * 1024);
   const size_t smem = (size_t)ns * SB + fixed_bytes(UX, NWT);
   cudaError_t e = cudaFuncSetAttribute(k_fused<R, UX, NWT, HD, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_fused<R, UX, NWT, HD, BNT><<<grid, (NWT + 1) * 32, smem, st>>>(mx, mh, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, ns, evict_first);
-  return cudaGetLastError();
+  return launch_maybe_coop(k_fused<R, UX, NWT, HD, BNT>, grid, (NWT + 1) * 32, smem, st, pa.iters > 0, mx, mh, m, n, r,
+                           W, Gpart, nG, eps, H, Ppart, Qpart, mode, ns, evict_first, pa);
 }
 
 // ------------------------------------------------------------ W update v2 --
@@ -1279,7 +1476,9 @@ void fused_destroy(FusedCtx&) {}
 
 cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int r, const float* W, const double* Gpart,
                          int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
-                         cudaStream_t st) {
+                         cudaStream_t st, const PersistArgs* pap) {
+  const PersistArgs pa = pap ? *pap : PersistArgs{0, nullptr, nullptr, nullptr, nullptr, nullptr};
+  if (pa.iters > 0 && m > 40 && use_wc()) return cudaErrorNotSupported;
   const int evict_first = ((double)m * (double)n * 4.0 > 48e6) ? 1 : 0;
   if (m > 40 && use_wc()) {
     const int MPc = m <= 128 ? 128 : 256;
@@ -1298,8 +1497,8 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
     if (e != cudaSuccess) return e;
     e = make_map(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u);
     if (e != cudaSuccess) return e;
-    if (MPc == 128) return launch_c<128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st);
-    return launch_c<256>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st);
+    if (MPc == 128) return launch_c<128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
+    return launch_c<256>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
   }
   const int ux = ux_for(m);
   CUtensorMap mx, mh;
@@ -1321,10 +1520,10 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
   const bool hd = (w_hd >= 0) ? (w_hd == 1) : (ux <= 2 || r < 8);
 #define LF(RR, UU)                                                                                                              \
   return (UU >= 4 && w_bn == 64)                                                                                                  \
-             ? (hd ? launch_t<RR, UU, 8, true, 64>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st)  \
-                   : launch_t<RR, UU, 8, false, 64>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st)) \
-             : (hd ? launch_t<RR, UU, 8, true, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st) \
-                   : launch_t<RR, UU, 8, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st))
+             ? (hd ? launch_t<RR, UU, 8, true, 64>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st)  \
+                   : launch_t<RR, UU, 8, false, 64>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st)) \
+             : (hd ? launch_t<RR, UU, 8, true, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st) \
+                   : launch_t<RR, UU, 8, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st))
   if (rc == 2) {
     if (ux == 1) LF(2, 1);
     if (ux == 2) LF(2, 2);

@@ -23,12 +23,25 @@ void fused_destroy(FusedCtx& c);
 constexpr int kFusedUpdate = 1;  // phase A: S = W^T X, H <- H o S / (G H + eps), store H
 constexpr int kFusedAcc = 2;     // phase B: per-CTA partials of P = X Hn^T, Q = Hn Hn^T
 
+// Persistent mode (iters > 0): one cooperative launch runs the acc-only prologue
+// and `iters` fused passes of a TT step, reducing the per-CTA partials and
+// updating W inside the kernel (mu_fused.cu, persist_step).  part: [grid][m r + r r]
+// fp64, red: [m r + r r] fp64, ctr: zeroed grid-barrier counter, Wout: W (m x r).
+struct PersistArgs {
+  int iters;
+  double* part;
+  double* red;
+  unsigned* ctr;
+  float* Wout;
+  unsigned long long* trace;  // nullable: per pass 4 globaltimer stamps of CTA 0 (diagnostics)
+};
+
 // One pass over X (m x n, row stride ldx) with the current W (m x r) and
 // G = sum_c Gpart[c] (nG partials).  mode = kFusedAcc alone is the prologue
 // (Hn := H).  Ppart/Qpart: [grid][m*r] / [grid][r*r] fp64.
 cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int r, const float* W,
                          const double* Gpart, int nG, float eps, float* H, double* Ppart, double* Qpart, int mode,
-                         int grid, cudaStream_t st);
+                         int grid, cudaStream_t st, const PersistArgs* persist = nullptr);
 
 // W update from partials with a parallel fixed-order reduction:
 //   P = sum_b Ppart[b] (nP), Q = sum_b Qpart[b] (nQ), W <- W o P / (W Q + eps);

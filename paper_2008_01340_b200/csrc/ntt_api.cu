@@ -69,6 +69,7 @@ struct ntt_handle_s {
   cudaStream_t stream = nullptr;
   int num_sms = 148;
   int64_t l2_bytes = 126 << 20;
+  unsigned long long* ptrace = nullptr;  // persistent-kernel phase stamps (NTT_PERSIST_TRACE)
   std::string err;
   int64_t launches = 0;
   // internal scratch (grown, never shrunk)
@@ -266,7 +267,8 @@ struct MuPlan {
   int fparts;     // fused kernel partial slots
   bool tc;        // tensor-core 2-pass path (mu_tc.cu) for tall / square X
   TcPlan tp;
-  size_t off_P, off_Q, off_G, off_S, off_tc, bytes;
+  bool persist;   // fused path as one persistent cooperative launch per call
+  size_t off_P, off_Q, off_G, off_S, off_tc, off_pp, off_red, off_ctr, bytes;
 };
 
 MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, int nranks) {
@@ -303,6 +305,13 @@ MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, int nranks) {
     p.tp = plan_tc(m, n, r, num_sms);
     o = align_up(o + p.tp.bytes);
   }
+  p.persist = nranks == 1 && p.fused && !use_wc() && !getenv("NTT_NO_PERSIST");
+  p.off_pp = o;
+  if (p.persist) o = align_up(o + sizeof(double) * (size_t)p.fgrid * (size_t)(m * r + r * r));
+  p.off_red = o;
+  if (p.persist) o = align_up(o + sizeof(double) * (size_t)(m * r + r * r));
+  p.off_ctr = o;
+  if (p.persist) o = align_up(o + 64);
   p.bytes = o;
   (void)nranks;
   return p;
@@ -329,6 +338,20 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
   int nobj = objective_ctas(n);
   if (iters <= 0) return NTT_OK;
 
+  if (p.fused && p.persist && !dist && !dev_trace && fused_supported(m, n, r, ldx, X, H)) {
+    // whole MU loop of this call in one cooperative launch (mu_fused.cu persist_step)
+    PersistArgs pa;
+    pa.iters = iters;
+    pa.part = reinterpret_cast<double*>(scratch + p.off_pp);
+    pa.red = reinterpret_cast<double*>(scratch + p.off_red);
+    pa.ctr = reinterpret_cast<unsigned*>(scratch + p.off_ctr);
+    pa.Wout = W;
+    pa.trace = h->ptrace;  // diagnostics (NTT_PERSIST_TRACE), else null
+    CU(h, cudaMemsetAsync(pa.ctr, 0, 64, st));
+    PLAUNCH(h, 0, (double)iters * 4.0 * (double)(m + 2 * r) * (double)n + 4.0 * (double)(m + r) * (double)n,
+            launch_fused(X, ldx, m, n, r, W, nullptr, 0, eps, H, nullptr, nullptr, 0, p.fgrid, st, &pa));
+    return NTT_OK;
+  }
   if (p.fused && fused_supported(m, n, r, ldx, X, H)) {
     // 1-pass: prologue P0 = X H0^T, Q0 = H0 H0^T; then per iteration
     //   W update (reduces the partials)  ->  fused pass (H update + next P, Q).
@@ -655,6 +678,7 @@ static ntt_status create_common(ntt_handle* out, int device, void* stream) {
   h->stream = reinterpret_cast<cudaStream_t>(stream);
   h->num_sms = prop.multiProcessorCount;
   h->l2_bytes = prop.l2CacheSize;
+  if (getenv("NTT_PERSIST_TRACE")) cudaMallocManaged(&h->ptrace, sizeof(unsigned long long) * 4 * 4096);
   *out = h;
   return NTT_OK;
 }
@@ -675,6 +699,7 @@ ntt_status ntt_destroy(ntt_handle h) {
   cudaStreamSynchronize(h->stream);
   fused_destroy(h->fused);
   if (h->ws) cudaFree(h->ws);
+  if (h->ptrace) cudaFree(h->ptrace);
   if (h->stage) cudaFree(h->stage);
   if (h->host_part) cudaFreeHost(h->host_part);
   if (h->comm && g_nccl.loaded) g_nccl.CommDestroy(h->comm);
@@ -1139,3 +1164,9 @@ int ntt_dist_rank(ntt_handle h) { return h ? h->rank : -1; }
 int ntt_dist_size(ntt_handle h) { return h ? h->nranks : -1; }
 
 }  // extern "C"
+
+extern "C" const unsigned long long* ntt_debug_persist_trace(ntt_handle h) {
+  if (!h) return nullptr;
+  cudaStreamSynchronize(h->stream);
+  return h->ptrace;
+}
