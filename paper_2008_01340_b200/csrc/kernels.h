@@ -36,6 +36,12 @@ cudaError_t launch_hpass(const float* X, int64_t ldx, int64_t m, int64_t n, cons
                          const double* Gpart, int nG, float eps, float* H, int grid, double* Ppart,
                          double* Qpart, cudaStream_t st);
 
+// tiny mode (mu_tiny.cu): the whole MU loop of a small X (m n <= 48k, m <= 512,
+// r <= 16) in one CTA from shared memory
+bool tiny_supported(int64_t m, int64_t n, int r);
+cudaError_t launch_tiny(const float* X, int64_t ldx, int64_t m, int64_t n, int r, int iters, float eps, float* W,
+                        float* H, cudaStream_t st);
+
 // 1/2 ||X - W H||^2 partial sums (fp64), one per CTA; returns number of partials.
 int objective_ctas(int64_t n);
 cudaError_t launch_objective(const float* X, int64_t ldx, int64_t m, int64_t n, const float* W,

@@ -86,6 +86,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// L2 prefetch of one TMA box (no smem, no barrier): deepens the HBM pipeline
+// beyond the shared-memory ring
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(c0), "r"(c1)
+               : "memory");
+}
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
@@ -106,6 +112,11 @@ __device__ __forceinline__ float2 bc(float a) { return make_float2(a, a); }
 
 // transposed per-warp Hn tile: column c (0..127), rank index k (0..7)
 __device__ __forceinline__ int hn_idx(int c, int k) { return c * 8 + k + 4 * (c >> 2) + 4 * (c >> 5); }
+// transposed Hn tile stored over the stage's (already consumed) H boxes: 8 floats
+// per column, row rho(c) = c ^ (((c >> 2) + c / SL) & 3) -- conflict-free phase-B
+// reads (the 4 column slices land in distinct bank groups), 2-way phase-A writes.
+template <int SL>
+__device__ __forceinline__ int hn_sw(int c, int k) { return ((c ^ (((c >> 2) + c / SL) & 3)) << 3) + k; }
 
 // ---------------------------------------------------------------------------
 // Persistent mode (PersistArgs.iters > 0): ONE cooperative launch runs the whole
@@ -276,8 +287,9 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   unsigned char* stages = smem;
   float* Ws = reinterpret_cast<float*>(smem + (size_t)ns * SB);  // MP x 8
   float* Gs = Ws + MP * 8;                                         // 8 x 8
-  float* HnAll = Gs + 64;                                          // NWT x HN_FLOATS
-  uint64_t* full = reinterpret_cast<uint64_t*>(HnAll + NWT * HN_FLOATS);
+  // HDIRECT: per-warp padded Hn tiles; otherwise Hn overwrites the stage's H boxes
+  float* HnAll = Gs + 64;                                          // NWT x HN_FLOATS (HDIRECT)
+  uint64_t* full = reinterpret_cast<uint64_t*>(HnAll + (HDIRECT ? NWT * HN_FLOATS : 0));
   uint64_t* empty = full + ns;
   // Tiles issued so far.  Successive rounds of one stage are consumed by
   // DIFFERENT warps, so before parity-waiting on round k a warp must know round
@@ -330,14 +342,25 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
     // ================= TMA producer =================
     if (lane == 0) {
       uint64_t policy;
-      if (evict_first)
+      if (evict_first & 1)
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
       else
         asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
+      const int pf = (evict_first >> 8) & 255;  // L2 prefetch distance (tiles)
+      for (int64_t j = 0; j < pf && j < J; ++j) {
+        const int c = (int)((b + j * gridDim.x) * BNT);
+#pragma unroll
+        for (int bx = 0; bx < NB; ++bx) tma_prefetch_2d(&tmX, c + bx * 32, 0);
+      }
       for (int64_t j = 0; j < J; ++j) {
         const int64_t pos = pbase + j;
         const int s = (int)(pos % ns);
         const uint32_t ph = (uint32_t)((pos / ns) & 1);
+        if (pf && j + pf < J) {
+          const int c = (int)((b + (j + pf) * gridDim.x) * BNT);
+#pragma unroll
+          for (int bx = 0; bx < NB; ++bx) tma_prefetch_2d(&tmX, c + bx * 32, 0);
+        }
         MBAR_WAIT(&empty[s], ph ^ 1u, 1, j);
         mbar_expect_tx(&full[s], SB);
         const int col0 = (int)((b + j * gridDim.x) * BNT);
@@ -354,7 +377,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   } else {
 
   // ================= consumer warps =================
-  float* Hw = HnAll + warp * HN_FLOATS;
+  float* HwDirect = HnAll + warp * HN_FLOATS;
   // phase A: lane q owns columns cq..cq+CPL-1 (box qbox, 16B chunk qch, float offset qsub)
   const int q = lane, cq = q * CPL, qbox = cq >> 5, qch = (cq & 31) >> 2, qsub = cq & 3;
   const int rb = lane & 7, cs = lane >> 3;  // phase B: rows rb+8u, columns cs*SL .. cs*SL+SL-1
@@ -418,6 +441,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
     __syncwarp();
     MBAR_WAIT(&full[s], ph, 2, j);
     const unsigned char* st = stages + (size_t)s * SB;
+    float* Hw = HDIRECT ? HwDirect : reinterpret_cast<float*>(stages + (size_t)s * SB + XB);
     if (!HDIRECT) {
       const unsigned char* hb = st + XB + qbox * 1024;
 #pragma unroll
@@ -517,13 +541,14 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
           for (int p2 = 0; p2 < CPL / 2; ++p2) hn[k][p2] = hv[k][p2];
       }
       if (do_acc) {
-        // transposed Hn tile: Hw[hn_idx(c, k)]
+        // transposed Hn tile: Hw[hn_idx(c, k)] (HDIRECT) or over the H boxes (all lanes have read H)
+        if (!HDIRECT) __syncwarp();
 #pragma unroll
         for (int t = 0; t < CPL; ++t) {
           float tv[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k) tv[k] = (k < R) ? ((t & 1) ? hn[k % R][t >> 1].y : hn[k % R][t >> 1].x) : 0.f;
-          float* dst = Hw + hn_idx(cq + t, 0);
+          float* dst = Hw + (HDIRECT ? hn_idx(cq + t, 0) : hn_sw<SL>(cq + t, 0));
           *reinterpret_cast<float4*>(dst) = make_float4(tv[0], tv[1], tv[2], tv[3]);
           if (R > 4) *reinterpret_cast<float4*>(dst + 4) = make_float4(tv[4], tv[5], tv[6], tv[7]);
         }
@@ -545,7 +570,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
         float hq[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-          const float* src = Hw + hn_idx(c + t, 0);
+          const float* src = Hw + (HDIRECT ? hn_idx(c + t, 0) : hn_sw<SL>(c + t, 0));
           float4 a = *reinterpret_cast<const float4*>(src);
           hq2[t][0] = f2(a.x, a.y);
           if (R > 2) hq2[t][1 % (R / 2)] = f2(a.z, a.w);
@@ -597,6 +622,9 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
         accd[v] += (double)(keep + __shfl_xor_sync(0xffffffffu, send, 8));
       }
     }
+    // Hn was written over the stage with generic stores: order them before the
+    // producer's next TMA (async-proxy) write into this stage
+    if (!HDIRECT && do_acc) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
@@ -714,14 +742,17 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   if (warp == NWC) {
     if (lane == 0) {
       uint64_t policy;
-      if (evict_first)
+      if (evict_first & 1)
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
       else
         asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
+      const int pf = (evict_first >> 8) & 255;  // L2 prefetch distance (tiles)
+      for (int64_t j = 0; j < pf && j < J; ++j) tma_prefetch_2d(&tmX, (int)((b + j * gridDim.x) * BNC), 0);
       for (int64_t j = 0; j < J; ++j) {
         const int64_t pos = pbase + j;
         const int s = (int)(pos % ns);
         const uint32_t ph = (uint32_t)((pos / ns) & 1);
+        if (pf && j + pf < J) tma_prefetch_2d(&tmX, (int)((b + (j + pf) * gridDim.x) * BNC), 0);
         MBAR_WAIT(&empty[s], ph ^ 1u, 3, j);
         mbar_expect_tx(&full[s], SB);
         const int col0 = (int)((b + j * gridDim.x) * BNC);
@@ -1019,7 +1050,7 @@ k_fused_wc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUte
   if (warp == NWW) {
     if (lane == 0) {
       uint64_t policy;
-      if (evict_first)
+      if (evict_first & 1)
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
       else
         asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
@@ -1300,13 +1331,13 @@ cudaError_t make_map(CUtensorMap* map, const float* base, uint64_t cols, uint64_
 int ux_for(int64_t m) { return m <= 8 ? 1 : m <= 16 ? 2 : m <= 32 ? 4 : 5; }
 int rcls_for(int r) { return r <= 2 ? 2 : r <= 4 ? 4 : 8; }
 
-size_t fixed_bytes(int ux, int nwt) {
-  return (size_t)ux * 8 * 8 * 4 + 256 + (size_t)nwt * HN_FLOATS * 4 + 2 * 16 * 8 + 16 + 1024;
+size_t fixed_bytes(int ux, int nwt, bool hd) {
+  return (size_t)ux * 8 * 8 * 4 + 256 + (hd ? (size_t)nwt * HN_FLOATS * 4 : 0) + 2 * 24 * 8 + 16 + 1024;
 }
 
 int stages_for(int ux, int nwt, bool hd, int bnt) {
   const size_t SB = (size_t)(bnt / 32) * ux * 8 * 128 + (hd ? 0 : (size_t)(bnt / 32) * 1024);
-  int ns = (int)((SMEM_BUDGET - fixed_bytes(ux, nwt)) / SB);
+  int ns = (int)((SMEM_BUDGET - fixed_bytes(ux, nwt, hd)) / SB);
   if (ns > 24) ns = 24;
   return ns;
 }
@@ -1317,7 +1348,7 @@ cudaError_t launch_t(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_
                      int evict_first, const PersistArgs& pa, cudaStream_t st) {
   const int ns = stages_for(UX, NWT, HD, BNT);
   const size_t SB = (size_t)(BNT / 32) * UX * 8 * 128 + (HD ? 0 : (size_t)(BNT / 32) * 1024);
-  const size_t smem = (size_t)ns * SB + fixed_bytes(UX, NWT);
+  const size_t smem = (size_t)ns * SB + fixed_bytes(UX, NWT, HD);
   cudaError_t e = cudaFuncSetAttribute(k_fused<R, UX, NWT, HD, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_maybe_coop(k_fused<R, UX, NWT, HD, BNT>, grid, (NWT + 1) * 32, smem, st, pa.iters > 0, mx, mh, m, n, r,
@@ -1479,7 +1510,12 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
                          cudaStream_t st, const PersistArgs* pap) {
   const PersistArgs pa = pap ? *pap : PersistArgs{0, nullptr, nullptr, nullptr, nullptr, nullptr};
   if (pa.iters > 0 && m > 40 && use_wc()) return cudaErrorNotSupported;
-  const int evict_first = ((double)m * (double)n * 4.0 > 48e6) ? 1 : 0;
+  static const int pf_env = [] {
+    const char* e = getenv("NTT_PF");
+    return e ? atoi(e) : -1;
+  }();
+  const int pf_tiles = pf_env >= 0 ? pf_env : 0;
+  const int evict_first = (((double)m * (double)n * 4.0 > 48e6) ? 1 : 0) | ((pf_tiles & 255) << 8);
   if (m > 40 && use_wc()) {
     const int MPc = m <= 128 ? 128 : 256;
     CUtensorMap mx, mh;
@@ -1538,6 +1574,14 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
   }
   if (ux == 1) LF(8, 1);
   if (ux == 2) LF(8, 2);
+  static const int w_nwt = [] {
+    const char* e = getenv("NTT_W_NWT");
+    return e ? atoi(e) : 7;  // 7 consumer warps measured ~6% faster than 8 on config 3 step 1
+  }();
+  if (ux == 4 && !hd && w_bn == 128 && w_nwt == 6)
+    return launch_t<8, 4, 6, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
+  if (ux == 4 && !hd && w_bn == 128 && w_nwt == 7)
+    return launch_t<8, 4, 7, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
   if (ux == 4) LF(8, 4);
   LF(8, 5);
 #undef LF

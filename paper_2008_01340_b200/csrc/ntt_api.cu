@@ -268,6 +268,7 @@ struct MuPlan {
   bool tc;        // tensor-core 2-pass path (mu_tc.cu) for tall / square X
   TcPlan tp;
   bool persist;   // fused path as one persistent cooperative launch per call
+  bool tiny;      // whole MU loop in one CTA from shared memory (mu_tiny.cu)
   size_t off_P, off_Q, off_G, off_S, off_tc, off_pp, off_red, off_ctr, bytes;
 };
 
@@ -306,6 +307,7 @@ MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, int nranks) {
     o = align_up(o + p.tp.bytes);
   }
   p.persist = nranks == 1 && p.fused && !use_wc() && !getenv("NTT_NO_PERSIST");
+  p.tiny = nranks == 1 && tiny_supported(m, n, r) && !getenv("NTT_NO_TINY");
   p.off_pp = o;
   if (p.persist) o = align_up(o + sizeof(double) * (size_t)p.fgrid * (size_t)(m * r + r * r));
   p.off_red = o;
@@ -338,6 +340,12 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
   int nobj = objective_ctas(n);
   if (iters <= 0) return NTT_OK;
 
+  if (p.tiny && !dist && !dev_trace) {
+    // tiny mode: every iteration in one CTA from shared memory (mu_tiny.cu)
+    PLAUNCH(h, 0, (double)iters * 4.0 * (double)(m + 2 * r) * (double)n,
+            launch_tiny(X, ldx, m, n, r, iters, eps, W, H, st));
+    return NTT_OK;
+  }
   if (p.fused && p.persist && !dist && !dev_trace && fused_supported(m, n, r, ldx, X, H)) {
     // whole MU loop of this call in one cooperative launch (mu_fused.cu persist_step)
     PersistArgs pa;
