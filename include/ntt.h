@@ -195,6 +195,20 @@ const unsigned long long* ntt_debug_persist_trace(ntt_handle h);
 ntt_status ntt_get_unique_id(void* id128);
 ntt_status ntt_create_dist(ntt_handle* out, int device, void* cuda_stream, const void* id128,
                            int nranks, int rank);
+/* 2-D pr x pc process grid for the plain NMF (Alg. 5 / Alg. 6, P:268-292;
+ * SURVEY s.8(e)): rank = ga * pc + gb.  ntt_nmf_mu on such a handle takes the
+ * LOCAL blocks: X = X[rows of block ga, columns of block gb] (m x n are the
+ * local extents, blocks from ntt_dist_block over pr resp. pc parts), W = the
+ * m x r rows of block ga (replicated over grid row ga), H = the r x n columns of
+ * block gb (replicated over grid column gb).  Per iteration: all-reduce of
+ * (X H^T, H H^T) over the grid row, of W^T W and of the W^T X block over the grid
+ * column (fp64 payloads).  X never moves.  pr > 1 needs the tensor-core path
+ * (r <= 32, m, n >= 256, 16-byte aligned X) else NTT_ERR_UNSUPPORTED.
+ * ntt_create_dist(.., nranks, rank) == ntt_create_dist_grid(.., 1, nranks).  */
+ntt_status ntt_create_dist_grid(ntt_handle* out, int device, void* cuda_stream, const void* id128,
+                                int nranks, int rank, int pr, int pc);
+/* grid shape and this rank's position; returns 0 (or -1 for a null handle) */
+int ntt_dist_grid(ntt_handle h, int* pr, int* pc, int* ga, int* gb);
 int ntt_dist_rank(ntt_handle h);
 int ntt_dist_size(ntt_handle h);
 /* Local extent of the last mode on `rank` for a global extent n_d over p ranks. */

@@ -93,7 +93,7 @@ class Handle:
     """Owns an ntt_handle bound to (device, stream)."""
 
     def __init__(self, device: int = 0, stream: Optional[int] = None, unique_id: Optional[bytes] = None,
-                 nranks: int = 1, rank: int = 0):
+                 nranks: int = 1, rank: int = 0, grid: Optional[tuple] = None):
         self._h = ctypes.c_void_p()
         if stream is None:
             try:
@@ -105,7 +105,9 @@ class Handle:
             st = lib().ntt_create(ctypes.byref(self._h), device, ctypes.c_void_p(stream))
         else:
             idb = ctypes.create_string_buffer(unique_id, 128)
-            st = lib().ntt_create_dist(ctypes.byref(self._h), device, ctypes.c_void_p(stream), idb, nranks, rank)
+            pr, pc = grid if grid is not None else (1, nranks)
+            st = lib().ntt_create_dist_grid(ctypes.byref(self._h), device, ctypes.c_void_p(stream), idb, nranks, rank,
+                                            pr, pc)
         if st != 0:
             raise NttError(st, f"ntt_create failed ({lib().ntt_status_string(st).decode()})")
 
@@ -139,6 +141,13 @@ class Handle:
     @property
     def size(self) -> int:
         return int(lib().ntt_dist_size(self._h))
+
+    @property
+    def grid(self):
+        """(pr, pc, ga, gb): process-grid shape and this rank's (row, column) position."""
+        v = [ctypes.c_int() for _ in range(4)]
+        lib().ntt_dist_grid(self._h, *[ctypes.byref(x) for x in v])
+        return tuple(int(x.value) for x in v)
 
     def last_error(self) -> str:
         return lib().ntt_last_error(self._h).decode()

@@ -39,6 +39,9 @@ SIGNATURES = {
     "ntt_compression_ratio": (c_f64, [c_i32, c_p, c_p]),
     "ntt_get_unique_id": (c_int, [c_p]),
     "ntt_create_dist": (c_int, [ctypes.POINTER(c_p), c_int, c_p, c_p, c_int, c_int]),
+    "ntt_create_dist_grid": (c_int, [ctypes.POINTER(c_p), c_int, c_p, c_p, c_int, c_int, c_int, c_int]),
+    "ntt_dist_grid": (c_int, [c_p, ctypes.POINTER(c_int), ctypes.POINTER(c_int), ctypes.POINTER(c_int),
+                              ctypes.POINTER(c_int)]),
     "ntt_dist_rank": (c_int, [c_p]),
     "ntt_dist_size": (c_int, [c_p]),
     "ntt_dist_block": (c_i64, [c_i64, c_int, c_int, ctypes.POINTER(c_i64)]),

@@ -36,7 +36,7 @@ cudaError_t launch_hpass(const float* X, int64_t ldx, int64_t m, int64_t n, cons
                          const double* Gpart, int nG, float eps, float* H, int grid, double* Ppart,
                          double* Qpart, cudaStream_t st);
 
-// tiny mode (mu_tiny.cu): the whole MU loop of a small X (m n <= 48k, m <= 512,
+// tiny mode (mu_tiny.cu): the whole MU loop of a small X (m n <= 48k, m <= 64,
 // r <= 16) in one CTA from shared memory
 bool tiny_supported(int64_t m, int64_t n, int r);
 cudaError_t launch_tiny(const float* X, int64_t ldx, int64_t m, int64_t n, int r, int iters, float eps, float* W,

@@ -518,6 +518,8 @@ TcPlan plan_tc(int64_t m, int64_t n, int r, int num_sms) {
   p.off_Q = take(sizeof(double) * (size_t)p.nQ * r * r);
   p.off_Gred = take(sizeof(double) * (size_t)r * r);
   p.off_Qred = take(sizeof(double) * (size_t)r * r);
+  p.off_red = take(sizeof(double) * (size_t)(m * r + r * r));  // distributed: [P | Q] all-reduce payload
+  p.off_Sred = take(sizeof(double) * (size_t)n * r);          // distributed: W^T X block payload
   p.bytes = o;
   return p;
 }
@@ -559,15 +561,19 @@ cudaError_t tc_pass_w(const TcPlan& p, const TcMaps& mp, char* ws, int evict_fir
 }
 
 cudaError_t tc_wupdate(const TcPlan& p, float* W, float eps, char* ws, cudaStream_t st) {
-  const double* P = reinterpret_cast<const double*>(ws + p.off_P);
-  const double* Qr = reinterpret_cast<const double*>(ws + p.off_Qred);
+  return tc_wupdate_ex(p, W, eps, ws, reinterpret_cast<const double*>(ws + p.off_P), p.splitW,
+                       reinterpret_cast<const double*>(ws + p.off_Qred), st);
+}
+
+cudaError_t tc_wupdate_ex(const TcPlan& p, float* W, float eps, char* ws, const double* P, int nP, const double* Qr,
+                          cudaStream_t st) {
   float* Wcat = reinterpret_cast<float*>(ws + p.off_wcat);
   double* G = reinterpret_cast<double*>(ws + p.off_G);
   const unsigned g = (unsigned)p.nG;
   if (p.R == 16)
-    k_tc_wupdate<16><<<g, UPD_ROWS, 0, st>>>(W, p.m, p.r, P, p.splitW, Qr, eps, Wcat, p.ldw, G);
+    k_tc_wupdate<16><<<g, UPD_ROWS, 0, st>>>(W, p.m, p.r, P, nP, Qr, eps, Wcat, p.ldw, G);
   else
-    k_tc_wupdate<32><<<g, UPD_ROWS, 0, st>>>(W, p.m, p.r, P, p.splitW, Qr, eps, Wcat, p.ldw, G);
+    k_tc_wupdate<32><<<g, UPD_ROWS, 0, st>>>(W, p.m, p.r, P, nP, Qr, eps, Wcat, p.ldw, G);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
   const int len = p.r * p.r;
@@ -583,15 +589,37 @@ cudaError_t tc_pass_h(const TcPlan& p, const TcMaps& mp, char* ws, int evict_fir
 }
 
 cudaError_t tc_hupdate(const TcPlan& p, float* H, float eps, char* ws, cudaStream_t st) {
-  const double* S = reinterpret_cast<const double*>(ws + p.off_S);
+  return tc_hupdate_ex(p, H, eps, ws, reinterpret_cast<const double*>(ws + p.off_S), p.splitH, st);
+}
+
+cudaError_t tc_hupdate_ex(const TcPlan& p, float* H, float eps, char* ws, const double* S, int nS, cudaStream_t st) {
   const double* Gr = reinterpret_cast<const double*>(ws + p.off_Gred);
   float* Hcat = reinterpret_cast<float*>(ws + p.off_hcat);
   double* Q = reinterpret_cast<double*>(ws + p.off_Q);
   const unsigned g = (unsigned)p.nQ;
   if (p.R == 16)
-    k_tc_hupdate<16><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, S, p.splitH, Gr, eps, true, Hcat, p.ldh, Q);
+    k_tc_hupdate<16><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, S, nS, Gr, eps, true, Hcat, p.ldh, Q);
   else
-    k_tc_hupdate<32><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, S, p.splitH, Gr, eps, true, Hcat, p.ldh, Q);
+    k_tc_hupdate<32><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, S, nS, Gr, eps, true, Hcat, p.ldh, Q);
+  return cudaGetLastError();
+}
+
+// distributed: red = [sum of the P split partials | Q]  (payload of the grid-row all-reduce)
+cudaError_t tc_reduce_PQ(const TcPlan& p, char* ws, cudaStream_t st) {
+  double* red = reinterpret_cast<double*>(ws + p.off_red);
+  const int64_t mr = p.m * p.r;
+  k_tc_sum<<<(unsigned)std::min<int64_t>((mr + 255) / 256, 1184), 256, 0, st>>>(
+      reinterpret_cast<const double*>(ws + p.off_P), p.splitW, (int)mr, red);
+  cudaError_t e = cudaGetLastError();
+  if (e) return e;
+  return cudaMemcpyAsync(red + mr, ws + p.off_Qred, sizeof(double) * p.r * p.r, cudaMemcpyDeviceToDevice, st);
+}
+
+// distributed: Sred = sum of the S split partials (payload of the grid-column all-reduce)
+cudaError_t tc_reduce_S(const TcPlan& p, char* ws, cudaStream_t st) {
+  const int64_t nr = p.n * p.r;
+  k_tc_sum<<<(unsigned)std::min<int64_t>((nr + 255) / 256, 1184), 256, 0, st>>>(
+      reinterpret_cast<const double*>(ws + p.off_S), p.splitH, (int)nr, reinterpret_cast<double*>(ws + p.off_Sred));
   return cudaGetLastError();
 }
 

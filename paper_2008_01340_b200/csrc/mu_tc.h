@@ -16,6 +16,7 @@ struct TcPlan {
   int64_t kchW = 0, kchH = 0;   // K tiles (of 32) per split
   int nG = 0, nQ = 0;           // Gram partial counts (W update CTAs, H update CTAs)
   size_t off_hcat = 0, off_wcat = 0, off_P = 0, off_S = 0, off_G = 0, off_Q = 0, off_Gred = 0, off_Qred = 0;
+  size_t off_red = 0, off_Sred = 0;  // distributed all-reduce payloads (fp64)
   size_t bytes = 0;
 };
 
@@ -40,5 +41,13 @@ cudaError_t tc_wupdate(const TcPlan& p, float* W, float eps, char* ws, cudaStrea
 cudaError_t tc_pass_h(const TcPlan& p, const TcMaps& mp, char* ws, int evict_first, cudaStream_t st);
 // H <- H o S / (G H + eps); Hcat; Q partials of the new H
 cudaError_t tc_hupdate(const TcPlan& p, float* H, float eps, char* ws, cudaStream_t st);
+
+// explicit-operand forms (distributed path: P / S already reduced, nP = nS = 1)
+cudaError_t tc_wupdate_ex(const TcPlan& p, float* W, float eps, char* ws, const double* P, int nP, const double* Q,
+                          cudaStream_t st);
+cudaError_t tc_hupdate_ex(const TcPlan& p, float* H, float eps, char* ws, const double* S, int nS, cudaStream_t st);
+// distributed payloads: ws+off_red = [P (m r) | Q (r r)], ws+off_Sred = S (n r); G (local) at ws+off_Gred
+cudaError_t tc_reduce_PQ(const TcPlan& p, char* ws, cudaStream_t st);
+cudaError_t tc_reduce_S(const TcPlan& p, char* ws, cudaStream_t st);
 
 }  // namespace ntt

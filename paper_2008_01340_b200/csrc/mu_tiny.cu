@@ -2,7 +2,7 @@
 // small unfolding (X of at most ~40k entries: config 1's steps, the tail steps of
 // configs 3 and 4) in ONE CTA, with X, W, H and the r x r Grams resident in shared
 // memory.  Per iteration (include/ntt.h ntt_nmf_mu, readings R1-R4):
-//   P = X H^T, Q = H H^T         fp32 over 64-column blocks, fp64 across (R13)
+//   P = X H^T, Q = H H^T         warp per row, fp32 per lane over 64 columns, fp64 across (R13)
 //   W <- W o P / (W Q + eps)     fp64 quotient, rounded to fp32 (as k_wupdate)
 //   G = W^T W                    fp64
 //   H <- H o (W^T X) / (G H + eps)   per column, fp32 (as k_hpass)
@@ -18,7 +18,7 @@ namespace ntt {
 namespace {
 
 constexpr int TINY_THREADS = 512;
-constexpr int TINY_BLK = 64;  // columns per fp32 partial block
+constexpr int TINY_BLK = 64;  // fp32 partial block: 32 lanes x 64 columns
 
 template <int R>
 struct TinyLayout {
@@ -33,7 +33,7 @@ struct TinyLayout {
     o = al(o + sizeof(double) * (size_t)m * R);       // P
     o = al(o + sizeof(double) * (size_t)R * R);       // Q
     o = al(o + sizeof(float) * (size_t)R * R);        // G (fp32 for E = G H)
-    o = al(o + sizeof(double) * (size_t)nch * (m * R + R * R));  // chunk partials
+    o = al(o + sizeof(double) * (size_t)nch * (m * R + R * R));  // chunk partials (n <= 256)
     return o;
   }
 };
@@ -79,19 +79,13 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
   const int EP = m * R, EQ = R * R, E = EP + EQ;
   const int nblk = (n + TINY_BLK - 1) / TINY_BLK;
   for (int it = 0; it < iters; ++it) {
-    // ---- P = X H^T and Q = H H^T: entry e x chunk c; chunk c owns 64-column blocks
-    //      [c*nblk/nch, (c+1)*nblk/nch); fp32 inside a block, fp64 across blocks
+    if (n <= 256) {
+    // ---- short rows: P = X H^T and Q = H H^T entry-parallel, entry e x chunk c of
+    //      64-column blocks, fp32 inside a block, fp64 across
     for (int t = tid; t < E * nch; t += T) {
       const int e = t % E, c = t / E;
-      const float* a;
-      const float* bv;
-      if (e < EP) {
-        a = Xs + (e / R) * n;
-        bv = Hs + (e % R) * n;
-      } else {
-        a = Hs + ((e - EP) / R) * n;
-        bv = Hs + ((e - EP) % R) * n;
-      }
+      const float* a = e < EP ? Xs + (e / R) * n : Hs + ((e - EP) / R) * n;
+      const float* bv = e < EP ? Hs + (e % R) * n : Hs + ((e - EP) % R) * n;
       const int b0 = nblk * c / nch, b1 = nblk * (c + 1) / nch;
       double acc = 0.0;
       for (int bk = b0; bk < b1; ++bk) {
@@ -109,12 +103,54 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
     }
     __syncthreads();
     for (int e = tid; e < E; e += T) {
-      double s = 0.0;
-      for (int c = 0; c < nch; ++c) s += part[c * E + e];
-      if (e < EP) P[e] = s;
-      else Q[e - EP] = s;
+      double sv = 0.0;
+      for (int c = 0; c < nch; ++c) sv += part[c * E + e];
+      if (e < EP) P[e] = sv;
+      else Q[e - EP] = sv;
     }
     __syncthreads();
+    } else {
+    // ---- long rows: P = X H^T and Q = H H^T: one warp per row task (X row i, then H row k);
+    //      lanes stride the columns (conflict-free), fp32 per lane over <= 64
+    //      columns, fp64 across, fixed-order butterfly over the lanes
+    {
+      const int warp = tid >> 5, lane = tid & 31, nw = T >> 5;
+      for (int task = warp; task < m + R; task += nw) {
+        const float* a = task < m ? Xs + (int64_t)task * n : Hs + (int64_t)(task - m) * n;
+        double acc[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) acc[k] = 0.0;
+        for (int j0 = 0; j0 < n; j0 += 32 * TINY_BLK) {
+          float s[R];
+#pragma unroll
+          for (int k = 0; k < R; ++k) s[k] = 0.0f;
+          const int j1 = min(n, j0 + 32 * TINY_BLK);
+          for (int j = j0 + lane; j < j1; j += 32) {
+            const float x = a[j];
+#pragma unroll
+            for (int k = 0; k < R; ++k) s[k] = fmaf(x, Hs[k * n + j], s[k]);
+          }
+#pragma unroll
+          for (int k = 0; k < R; ++k) acc[k] += (double)s[k];
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          double v = acc[k];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          acc[k] = v;
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            if (task < m) P[task * R + k] = acc[k];
+            else Q[(task - m) * R + k] = acc[k];
+          }
+        }
+      }
+    }
+    __syncthreads();
+    }
     // ---- W update (fp64, R4)
     for (int e = tid; e < EP; e += T) {
       const int i = e / R, k = e % R;
@@ -186,8 +222,10 @@ cudaError_t launch_tiny_t(const float* X, int64_t ldx, int m, int n, int r, int 
 
 }  // namespace
 
+// measured on B200: faster than the persistent fused kernel for m <= 64 (config 1,
+// config 4 steps 7-9); config 3 step 5 (256 x 32) stays on the fused path
 bool tiny_supported(int64_t m, int64_t n, int r) {
-  if (r < 1 || r > 16 || m < 1 || n < 1 || m > 512) return false;
+  if (r < 1 || r > 16 || m < 1 || n < 1 || m > 64) return false;
   const int R = r <= 4 ? 4 : (r <= 8 ? 8 : 16);
   if (m * n > 48 * 1024) return false;
   size_t b = R == 4 ? TinyLayout<4>::bytes((int)m, (int)n, tiny_nch((int)m, r, (int)n))

@@ -33,6 +33,7 @@ struct NcclApi {
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 NcclApi g_nccl;
@@ -56,6 +57,7 @@ bool load_nccl() {
   SYM(Broadcast, "ncclBroadcast")
   SYM(GroupStart, "ncclGroupStart")
   SYM(GroupEnd, "ncclGroupEnd")
+  SYM(CommSplit, "ncclCommSplit")
   SYM(GetErrorString, "ncclGetErrorString")
 #undef SYM
   g_nccl.loaded = true;
@@ -82,6 +84,11 @@ struct ntt_handle_s {
   size_t host_part_count = 0;
   // distributed
   int nranks = 1, rank = 0;
+  // 2-D pr x pc process grid for the plain NMF (SURVEY s.8(e)); rank = ga * pc + gb.
+  // comm_row: the pc ranks of grid row ga (same X row block / W block),
+  // comm_col: the pr ranks of grid column gb (same X column block / H block).
+  int pr = 1, pc = 1, ga = 0, gb = 0;
+  ncclComm_t comm_row = nullptr, comm_col = nullptr;
   ncclComm_t comm = nullptr;
   FusedCtx fused;
   // profiling (ntt_profile_enable)
@@ -300,7 +307,7 @@ MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, int nranks) {
   p.off_S = o;  // reduced (m r + r r) vector for the distributed all-reduce
   o = align_up(o + sizeof(double) * (size_t)(m * r + r * r));
   // shape-level eligibility of the tensor-core path (alignment re-checked at run time)
-  p.tc = nranks == 1 && !p.fused && tc_supported(m, n, r, n, nullptr) && !getenv("NTT_NO_TC");
+  p.tc = !p.fused && tc_supported(m, n, r, n, nullptr) && !getenv("NTT_NO_TC");
   p.off_tc = o;
   if (p.tc) {
     p.tp = plan_tc(m, n, r, num_sms);
@@ -384,25 +391,49 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
     return NTT_OK;
   }
 
-  if (p.tc && !dist && tc_supported(m, n, r, ldx, X)) {
-    // tensor-core 2-pass iteration (mu_tc.cu): X > L2 streams evict-first
+  if (p.tc && tc_supported(m, n, r, ldx, X)) {
+    // tensor-core 2-pass iteration (mu_tc.cu): X > L2 streams evict-first.
+    // Distributed (2-D grid, DESIGN.md s.7): the local partials are reduced and
+    // all-reduced over the grid row (P = X H^T, Q = H H^T) and the grid column
+    // (G = W^T W, S = W^T X); the updates then run redundantly per group.
     const TcPlan& tp = p.tp;
     char* tws = scratch + p.off_tc;
     const int ef = (double)m * (double)ldx * 4.0 > 0.6 * (double)h->l2_bytes ? 1 : 0;
+    double* red = reinterpret_cast<double*>(tws + tp.off_red);
+    double* gred = reinterpret_cast<double*>(tws + tp.off_Gred);
+    double* sred = reinterpret_cast<double*>(tws + tp.off_Sred);
     TcMaps maps;
     LAUNCH(h, tc_prepare(tp, X, ldx, H, tws, &maps, st));
     for (int it = 0; it < iters; ++it) {
       LAUNCH(h, tc_sum_Q(tp, tws, st));
       PLAUNCH(h, 6, 4.0 * (double)(m + 2 * tp.R) * (double)n, tc_pass_w(tp, maps, tws, ef, st));
-      PLAUNCH(h, 2, 8.0 * (double)tp.splitW * m * r + 8.0 * m * r + 4.0 * 2 * tp.R * m,
-              tc_wupdate(tp, W, eps, tws, st));
+      if (dist) {
+        LAUNCH(h, tc_reduce_PQ(tp, tws, st));
+        NC(h, g_nccl.AllReduce(red, red, (size_t)(m * r + r * r), ncclFloat64, ncclSum, h->comm_row, st));
+        PLAUNCH(h, 2, 8.0 * (double)(2 * m * r + r * r) + 4.0 * 2 * tp.R * m,
+                tc_wupdate_ex(tp, W, eps, tws, red, 1, red + m * r, st));
+        NC(h, g_nccl.AllReduce(gred, gred, (size_t)(r * r), ncclFloat64, ncclSum, h->comm_col, st));
+      } else {
+        PLAUNCH(h, 2, 8.0 * (double)tp.splitW * m * r + 8.0 * m * r + 4.0 * 2 * tp.R * m,
+                tc_wupdate(tp, W, eps, tws, st));
+      }
       PLAUNCH(h, 7, 4.0 * (double)(n + 2 * tp.R) * (double)m, tc_pass_h(tp, maps, tws, ef, st));
-      PLAUNCH(h, 4, 8.0 * (double)tp.splitH * n * r + 4.0 * (3 * tp.R + r) * (double)n,
-              tc_hupdate(tp, H, eps, tws, st));
+      if (dist) {
+        LAUNCH(h, tc_reduce_S(tp, tws, st));
+        NC(h, g_nccl.AllReduce(sred, sred, (size_t)(n * r), ncclFloat64, ncclSum, h->comm_col, st));
+        PLAUNCH(h, 4, 8.0 * (double)n * r + 4.0 * (3 * tp.R + r) * (double)n, tc_hupdate_ex(tp, H, eps, tws, sred, 1, st));
+      } else {
+        PLAUNCH(h, 4, 8.0 * (double)tp.splitH * n * r + 4.0 * (3 * tp.R + r) * (double)n,
+                tc_hupdate(tp, H, eps, tws, st));
+      }
       if (dev_trace) LAUNCH(h, launch_objective(X, ldx, m, n, W, H, r, dev_trace + (int64_t)it * nobj, st));
     }
     return NTT_OK;
   }
+  if (h->pr > 1)
+    return fail(h, NTT_ERR_UNSUPPORTED,
+                "2-D grid (pr = %d) NMF needs the tensor-core path: r <= 32, local m, n >= 256, 16-byte aligned X "
+                "(got m=%lld n=%lld r=%d)", h->pr, (long long)m, (long long)n, r);
 
   // prologue (1-pass) or first W pass: P = X H^T, Q = H H^T
   int nP = 0, nQ = 0;
@@ -710,6 +741,8 @@ ntt_status ntt_destroy(ntt_handle h) {
   if (h->ptrace) cudaFree(h->ptrace);
   if (h->stage) cudaFree(h->stage);
   if (h->host_part) cudaFreeHost(h->host_part);
+  if (h->comm_row && g_nccl.loaded) g_nccl.CommDestroy(h->comm_row);
+  if (h->comm_col && g_nccl.loaded) g_nccl.CommDestroy(h->comm_col);
   if (h->comm && g_nccl.loaded) g_nccl.CommDestroy(h->comm);
   for (auto e : h->ev_pool) cudaEventDestroy(e);
   for (auto e : h->gev_pool) cudaEventDestroy(e);
@@ -937,6 +970,9 @@ ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t*
   if (!A || !cores) return fail(h, NTT_ERR_INVALID_ARG, "null A or cores");
   if (iters < 0) return fail(h, NTT_ERR_INVALID_ARG, "iters < 0");
   if (!(eps >= 0.0f)) return fail(h, NTT_ERR_INVALID_ARG, "eps must be >= 0");
+  if (h->pr > 1)
+    return fail(h, NTT_ERR_UNSUPPORTED, "ntt_decompose partitions the last tensor mode: use a 1 x p grid (pr = %d)",
+                h->pr);
   TTShape s;
   ntt_status st = check_tt(h, d, dims, ranks, &s, true);
   if (st) return st;
@@ -1150,7 +1186,13 @@ ntt_status ntt_get_unique_id(void* id128) {
 }
 
 ntt_status ntt_create_dist(ntt_handle* out, int device, void* cuda_stream, const void* id128, int nranks, int rank) {
+  return ntt_create_dist_grid(out, device, cuda_stream, id128, nranks, rank, 1, nranks);
+}
+
+ntt_status ntt_create_dist_grid(ntt_handle* out, int device, void* cuda_stream, const void* id128, int nranks, int rank,
+                                int pr, int pc) {
   if (!out || !id128 || nranks < 1 || rank < 0 || rank >= nranks) return NTT_ERR_INVALID_ARG;
+  if (pr < 1 || pc < 1 || pr * pc != nranks) return NTT_ERR_INVALID_ARG;
   if (!load_nccl()) return NTT_ERR_UNSUPPORTED;
   ntt_status s = create_common(out, device, cuda_stream);
   if (s) return s;
@@ -1165,7 +1207,28 @@ ntt_status ntt_create_dist(ntt_handle* out, int device, void* cuda_stream, const
   }
   h->nranks = nranks;
   h->rank = rank;
+  h->pr = pr;
+  h->pc = pc;
+  h->ga = rank / pc;
+  h->gb = rank % pc;
+  // row / column communicators (Alg. 5 / Alg. 6 groups)
+  ncclResult_t r1 = g_nccl.CommSplit(h->comm, h->ga, h->gb, &h->comm_row, nullptr);
+  ncclResult_t r2 = (r1 == ncclSuccess) ? g_nccl.CommSplit(h->comm, h->gb, h->ga, &h->comm_col, nullptr) : r1;
+  if (r2 != ncclSuccess) {
+    ntt_destroy(h);
+    *out = nullptr;
+    return NTT_ERR_NCCL;
+  }
   return NTT_OK;
+}
+
+int ntt_dist_grid(ntt_handle h, int* pr, int* pc, int* ga, int* gb) {
+  if (!h) return -1;
+  if (pr) *pr = h->pr;
+  if (pc) *pc = h->pc;
+  if (ga) *ga = h->ga;
+  if (gb) *gb = h->gb;
+  return 0;
 }
 
 int ntt_dist_rank(ntt_handle h) { return h ? h->rank : -1; }

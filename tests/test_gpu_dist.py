@@ -54,3 +54,39 @@ def test_dist_handle_nmf_mu(handles, ora, m, n, r):
     W, H = Wd.cpu().numpy(), Hd.cpu().numpy()
     assert np.linalg.norm(W - Wo) <= 1e-4 * np.linalg.norm(Wo)
     assert np.linalg.norm(H - Ho) <= 1e-4 * np.linalg.norm(Ho)
+
+
+@pytest.mark.parametrize("m,n,r", [(512, 1024, 16), (1000, 776, 32)])
+def test_grid_handle_tc_nmf_matches(handles, ora, m, n, r):
+    """2-D grid handle (1 x 1 on one GPU): the tensor-core NMF path with the grid-row /
+    grid-column NCCL all-reduces must be bit-identical to the single-GPU path (the
+    split partials are summed in the same order) and match the oracle."""
+    import paper_2008_01340_b200 as P
+    h1, _ = handles
+    hg = P.Handle(0, unique_id=P.ntt_get_unique_id(), nranks=1, rank=0, grid=(1, 1))
+    assert hg.grid == (1, 1, 0, 0)
+    rng = np.random.default_rng(2)
+    X = (rng.random((m, r)) @ rng.random((r, n)) + 0.01 * rng.random((m, n))).astype(np.float32)
+    W0 = ni.uniform(m * r, 2, 0x202).reshape(m, r).astype(np.float32)
+    H0 = ni.uniform(r * n, 2, 0x203).reshape(r, n).astype(np.float32)
+    Xd = torch.from_numpy(X).cuda()
+    outs = []
+    for h in (h1, hg):
+        Wd, Hd = torch.from_numpy(W0.copy()).cuda(), torch.from_numpy(H0.copy()).cuda()
+        h.ntt_profile_enable(True)
+        h.ntt_nmf_mu(Xd, m, n, n, r, 6, 1e-16, Wd, Hd)
+        assert h.ntt_profile_get(6)[0] == 6, "tensor-core path not taken"
+        h.ntt_profile_enable(False)
+        outs.append((Wd.cpu().numpy(), Hd.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    Wo, Ho = ora.nmf_mu(X, W0.astype(np.float64), H0.astype(np.float64), 6)
+    assert np.linalg.norm(outs[1][0] - Wo) <= 1e-4 * np.linalg.norm(Wo)
+    assert np.linalg.norm(outs[1][1] - Ho) <= 1e-4 * np.linalg.norm(Ho)
+
+
+def test_grid_handle_rejects_bad_grid():
+    import paper_2008_01340_b200 as P
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    with pytest.raises(P.NttError):
+        P.Handle(0, unique_id=P.ntt_get_unique_id(), nranks=1, rank=0, grid=(2, 1))
