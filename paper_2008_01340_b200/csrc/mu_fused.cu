@@ -291,11 +291,15 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   float* HnAll = Gs + 64;                                          // NWT x HN_FLOATS (HDIRECT)
   uint64_t* full = reinterpret_cast<uint64_t*>(HnAll + (HDIRECT ? NWT * HN_FLOATS : 0));
   uint64_t* empty = full + ns;
-  // Tiles issued so far.  Successive rounds of one stage are consumed by
-  // DIFFERENT warps, so before parity-waiting on round k a warp must know round
-  // k-1 completed; the producer only issues round k after waiting for round
-  // k-1's release, hence "issued > j" makes the parity wait unambiguous.
+  // Dynamic stage assignment (no head-of-line blocking between the warp-owned
+  // tiles): the producer loads tile `pos` into ANY free stage s (bit s of
+  // free_mask, set again by the consuming warp when it is done), records
+  // slot[pos % 32] = s | parity << 8 and then publishes issued = pos + 1
+  // (release); the consumer reads its slot after acquiring `issued`.  At most ns
+  // tiles are issued-but-unreleased, so a 32-entry slot ring cannot be overrun.
   uint32_t* issued = reinterpret_cast<uint32_t*>(empty + ns);
+  uint32_t* free_mask = issued + 1;
+  uint32_t* slot = issued + 2;  // [32]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool persist = pa.iters > 0;
@@ -321,9 +325,11 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
       mbar_init(&empty[s], 1);
     }
     *issued = 0u;
+    *free_mask = (ns >= 32) ? 0xffffffffu : ((1u << ns) - 1u);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  uint32_t par_mask = 0u;  // producer: parity of the next fill of each stage
 
   const int64_t ntiles = (n + BNT - 1) / BNT;
   const int64_t b = blockIdx.x;
@@ -354,15 +360,20 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
       }
       for (int64_t j = 0; j < J; ++j) {
         const int64_t pos = pbase + j;
-        const int s = (int)(pos % ns);
-        const uint32_t ph = (uint32_t)((pos / ns) & 1);
         if (pf && j + pf < J) {
           const int c = (int)((b + (j + pf) * gridDim.x) * BNT);
 #pragma unroll
           for (int bx = 0; bx < NB; ++bx) tma_prefetch_2d(&tmX, c + bx * 32, 0);
         }
-        MBAR_WAIT(&empty[s], ph ^ 1u, 1, j);
-        mbar_expect_tx(&full[s], SB);
+        uint32_t fm;
+        while ((fm = ld_acquire_u32(free_mask)) == 0u) {
+        }
+        const int s = __ffs(fm) - 1;
+        atomicAnd(free_mask, ~(1u << s));
+        const uint32_t ph = (par_mask >> s) & 1u;
+        par_mask ^= 1u << s;
+        slot[pos & 31] = (uint32_t)s | (ph << 8);
+        mbar_expect_tx(&full[s], XB + (HDIRECT ? 0u : HB));
         const int col0 = (int)((b + j * gridDim.x) * BNT);
         unsigned char* st = stages + (size_t)s * SB;
 #pragma unroll
@@ -394,8 +405,6 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
 
   for (int64_t j = warp; j < J; j += NWT) {
     const int64_t pos = pbase + j;
-    const int s = (int)(pos % ns);
-    const uint32_t ph = (uint32_t)((pos / ns) & 1);
     const int64_t jt = (b + j * gridDim.x) * BNT;  // first column of the tile
     const int64_t c0 = jt + cq;
     // H columns c0..c0+CPL-1 of this tile (HDIRECT: independent of the stage, issued first)
@@ -439,6 +448,9 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
       }
     }
     __syncwarp();
+    const uint32_t so = __shfl_sync(0xffffffffu, lane == 0 ? *reinterpret_cast<volatile uint32_t*>(slot + (pos & 31)) : 0u, 0);
+    const int s = (int)(so & 255u);
+    const uint32_t ph = so >> 8;
     MBAR_WAIT(&full[s], ph, 2, j);
     const unsigned char* st = stages + (size_t)s * SB;
     float* Hw = HDIRECT ? HwDirect : reinterpret_cast<float*>(stages + (size_t)s * SB + XB);
@@ -626,7 +638,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
     // producer's next TMA (async-proxy) write into this stage
     if (!HDIRECT && do_acc) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (lane == 0) asm volatile("red.release.cta.shared::cta.or.b32 [%0], %1;" ::"r"(smem_u32(free_mask)), "r"(1u << s) : "memory");
   }
 
   if (do_acc) {
@@ -1332,7 +1344,7 @@ int ux_for(int64_t m) { return m <= 8 ? 1 : m <= 16 ? 2 : m <= 32 ? 4 : 5; }
 int rcls_for(int r) { return r <= 2 ? 2 : r <= 4 ? 4 : 8; }
 
 size_t fixed_bytes(int ux, int nwt, bool hd) {
-  return (size_t)ux * 8 * 8 * 4 + 256 + (hd ? (size_t)nwt * HN_FLOATS * 4 : 0) + 2 * 24 * 8 + 16 + 1024;
+  return (size_t)ux * 8 * 8 * 4 + 256 + (hd ? (size_t)nwt * HN_FLOATS * 4 : 0) + 2 * 24 * 8 + 160 + 1024;
 }
 
 int stages_for(int ux, int nwt, bool hd, int bnt) {
@@ -1576,10 +1588,12 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
   if (ux == 2) LF(8, 2);
   static const int w_nwt = [] {
     const char* e = getenv("NTT_W_NWT");
-    return e ? atoi(e) : 7;  // 7 consumer warps measured ~6% faster than 8 on config 3 step 1
+    return e ? atoi(e) : 8;
   }();
   if (ux == 4 && !hd && w_bn == 128 && w_nwt == 6)
     return launch_t<8, 4, 6, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
+  if (ux == 4 && !hd && w_bn == 128 && w_nwt == 9)
+    return launch_t<8, 4, 9, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
   if (ux == 4 && !hd && w_bn == 128 && w_nwt == 7)
     return launch_t<8, 4, 7, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
   if (ux == 4) LF(8, 4);
