@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--iters", type=int, default=None, help="override MU iterations per TT step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-other", action="store_true", help="skip the configs 1, 2, 4, 5 side measurements")
     return ap.parse_args()
 
 
@@ -186,6 +187,63 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------- other BASELINE workloads ---
+def other_workloads(h, P, ni, torch, steps=2):
+    """nTT wall time of configs 1 and 4 and MU iterations/s of the single-NMF configs 2 and
+    5 (1-GPU slice 32768 x 65536, SURVEY s.8(d) d.2) on device-generated synthetic inputs.
+    Reported beside the headline workload (config 3); not part of its timed region."""
+    import numpy as np
+    out = {}
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    for name in ("config1", "config4"):
+        w = ni.workloads()[name]
+        cores0 = torch.from_numpy(ni.make_cores(w.dims, w.ranks, w.seed).astype(np.float32)).cuda()
+        A = torch.empty(w.numel, device="cuda")
+        h.ntt_generate(w.dims, w.ranks, cores0, w.noise_amp, w.seed, ni.STREAM_NOISE, A)
+        cores = torch.empty(P.cores_size(w.dims, w.ranks), device="cuda")
+        err = h.ntt_decompose(A, w.dims, w.ranks, w.iters, w.seed, 1e-16, cores, want_error=True)
+        e0, e1 = ev(), ev()
+        e0.record()
+        for _ in range(steps):
+            h.ntt_decompose(A, w.dims, w.ranks, w.iters, w.seed, 1e-16, cores)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        its = (len(w.dims) - 1) * w.iters
+        out[name] = {"ntt_wall_ms": ms, "mu_iter_per_s": its / (ms / 1e3), "rel_error": err,
+                     "dims": w.dims, "ranks": w.ranks, "iters_per_step": w.iters}
+        del A, cores
+    for name, rows, iters in (("config2", None, 20), ("config5", 32768, 3)):
+        w = ni.workloads()[name]
+        m, n = w.dims
+        r = w.ranks[0]
+        if rows:
+            m = rows
+        dims, ranks, cores = ni.make_factor_cores(m, n, r, w.seed)
+        X = torch.empty(m * n, device="cuda")
+        h.ntt_generate(dims, ranks, torch.from_numpy(cores.astype(np.float32)).cuda(), w.noise_amp or 0.01, w.seed,
+                       ni.STREAM_NOISE, X)
+        W = torch.empty(m * r, device="cuda")
+        H = torch.empty(r * n, device="cuda")
+        h.ntt_fill_uniform(W, m * r, w.seed, ni.stream_w(1))
+        h.ntt_fill_uniform(H, r * n, w.seed, ni.stream_h(1))
+        h.ntt_nmf_mu(X, m, n, n, r, 1, 1e-16, W, H)
+        e0, e1 = ev(), ev()
+        e0.record()
+        h.ntt_nmf_mu(X, m, n, n, r, iters, 1e-16, W, H)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / iters
+        alg = 4.0 * n * (2 * m + 3 * r)  # 2-pass algorithmic bytes per iteration
+        out[name] = {"mu_iter_per_s": 1e3 / ms, "ms_per_iter": ms, "m": m, "n": n, "r": r, "timed_iters": iters,
+                     "effective_GBps": alg / (ms / 1e3) / 1e9,
+                     "path": "tcgen05 kind::tf32 3xTF32 2-pass (mu_tc.cu)",
+                     "note": "config 5 on the 1-GPU row slice (SURVEY s.8(d)); inputs X = W0 H0 + noise on device"}
+        del X, W, H
+        torch.cuda.empty_cache()
+    return out
+
+
 # ------------------------------------------------------------------- ours ---
 def run_ours(args):
     import numpy as np
@@ -324,6 +382,8 @@ def run_ours(args):
         "clocks": clocks,
         "e2e": e2e,
     }
+    if ws == 1 and not args.no_other:
+        line["other_workloads"] = other_workloads(h, P, ni, torch)
     if rk == 0 and ws == 1 and not args.no_cpu:
         t, threads, desc = oracle_sample_time(dims, ranks, iters)
         line["cpu_baseline"] = {"value": its / t, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc}

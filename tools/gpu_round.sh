@@ -1,4 +1,3 @@
-timeout 600 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
-NTT_W_BN=64 timeout 300 python tools/persist_trace.py 2>&1 | head -1
-timeout 600 python bench.py --no-e2e > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc $?"; python -c "
-import json; d=json.load(open('gpurun_out/bench.json')); print(d['value'], d['ms_per_step'], d['roofline']['frac'], d['clocks']); print({k:round(list(v.values())[0]['ms_per_step'],2) for k,v in d['roofline']['per_tt_step'].items()})"
+set -x
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_r1b.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_launch.log 2>&1; echo "ncu launch rc $?"
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_fused -c 2 -o gpurun_out/bench_full python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu > gpurun_out/ncu_full_bench.log 2>&1; echo "ncu full rc $?"
