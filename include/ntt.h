@@ -178,7 +178,8 @@ ntt_status ntt_profile_get_step(ntt_handle h, int cls, int step, int64_t* launch
  * persistent fused MU kernel records, per pass p, 4 globaltimer stamps of CTA 0
  * (pass start, partials written, after barrier 1, after barrier 2) at
  * [4p .. 4p+3] of the returned host-readable array (4096 passes max; pass 0 is
- * the prologue).  NULL otherwise.  Synchronises the handle's stream.         */
+ * the prologue), and for pass 1 of every CTA c < 1024 its start at [17408 + c]
+ * and end at [16384 + c].  NULL otherwise.  Synchronises the handle's stream. */
 const unsigned long long* ntt_debug_persist_trace(ntt_handle h);
 
 /* ----------------------------------------------------- multi-GPU (NCCL) ----

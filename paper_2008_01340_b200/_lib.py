@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libntt.so")
+LIB_PATH = os.environ.get("NTT_LIB") or os.path.join(_HERE, "libntt.so")  # NTT_LIB: experiment builds
 
 c_i32, c_i64, c_u64, c_f32, c_f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float, ctypes.c_double
 c_p = ctypes.c_void_p

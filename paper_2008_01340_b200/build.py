@@ -15,8 +15,10 @@ import sysconfig
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "build_obj")
-LIB = os.path.join(PKG, "libntt.so")
+# experiment builds: NTT_NVCC_DEFS="-DFOO=1" NTT_LIB_OUT=/path/libntt_x.so (own object dir)
+_VARIANT = os.environ.get("NTT_LIB_OUT")
+OBJ = os.path.join(PKG, "build_obj" + ("_" + os.path.basename(_VARIANT).replace(".so", "") if _VARIANT else ""))
+LIB = _VARIANT or os.path.join(PKG, "libntt.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -35,6 +37,7 @@ def nccl_include() -> str:
 
 def flags():
     extra = ["-DNTT_WATCHDOG"] if os.environ.get("NTT_WATCHDOG") else []
+    extra += os.environ.get("NTT_NVCC_DEFS", "").split()
     return [*extra, "-O3", "-lineinfo", "-std=c++17", *ARCH, "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",
             f"-I{os.path.join(ROOT, 'include')}", f"-I{nccl_include()}", "--expt-relaxed-constexpr"]
 

@@ -131,10 +131,13 @@ __device__ __forceinline__ int hn_sw(int c, int k) { return ((c ^ (((c >> 2) + c
 // ---------------------------------------------------------------------------
 
 __device__ __forceinline__ void pstamp(const PersistArgs& pa, int it, int ph) {
-  if (pa.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (pa.trace && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    pa.trace[it * 4 + ph] = t;
+    if (blockIdx.x == 0) pa.trace[it * 4 + ph] = t;
+    // per-CTA end of pass 1 (load-balance diagnostics): [16384 + cta], start of pass 1: [17408 + cta]
+    if (it == 1 && ph == 1 && blockIdx.x < 1024) pa.trace[16384 + blockIdx.x] = t;
+    if (it == 1 && ph == 0 && blockIdx.x < 1024) pa.trace[17408 + blockIdx.x] = t;
   }
 }
 
@@ -402,6 +405,21 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
 #pragma unroll
   for (int v = 0; v < V4 / 4; ++v) accd[v] = 0.0;
   const bool h1 = (lane >> 4) & 1, h0 = (lane >> 3) & 1;
+  // phase-B fp32 accumulators live across RS tiles; the reduce-scatter + fp64 fold
+  // runs every RS tiles (and after the warp's last tile): <= RS * SL / 4 fp32 terms
+#ifndef NTT_RS
+#define NTT_RS 1
+#endif
+  constexpr int RS = NTT_RS;
+  float2 acc[V4 / 2];
+#pragma unroll
+  for (int v = 0; v < V4 / 2; ++v) acc[v] = f2(0.f, 0.f);
+  int ntile = 0;
+  // swizzle offsets: phase A row i reads chunk (qch ^ (i & 7)), phase B chunk (s4 ^ rb)
+  int offA[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) offA[t] = ((qch ^ t) << 4);
+  (void)offA;
 
   for (int64_t j = warp; j < J; j += NWT) {
     const int64_t pos = pbase + j;
@@ -470,6 +488,8 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
     }
 
     // ---------------- phase A ----------------
+    const bool masked = (r < R) || (jt + BNT > n);  // warp-uniform
+    (void)masked;
     {
       float2 hn[R][CPL / 2];
       if (do_update) {
@@ -479,15 +499,26 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
         for (int k = 0; k < R; ++k)
 #pragma unroll
           for (int p2 = 0; p2 < CPL / 2; ++p2) s2[k][p2] = f2(0.f, 0.f);
+#ifndef NTT_PA_FULL
+#define NTT_PA_FULL 0
+#endif
+#if NTT_PA_FULL
+        // all MP rows: rows >= m are zero in the TMA tile (OOB fill) and in Ws
+#pragma unroll
+        for (int i = 0; i < MP; ++i) {
+          const int offi = offA[i & 7];
+#else
 #pragma unroll 4
         for (int i = 0; i < m; ++i) {
+          const int offi = (qch ^ (i & 7)) << 4;
+#endif
           float2 xv[CPL / 2];
           if (CPL == 4) {
-            const float4 x = lds128(xb + i * 128 + ((qch ^ (i & 7)) << 4));
+            const float4 x = lds128(xb + offi + i * 128);
             xv[0] = f2(x.x, x.y);
             xv[CPL / 2 - 1] = f2(x.z, x.w);
           } else {
-            xv[0] = *reinterpret_cast<const float2*>(xb + i * 128 + ((qch ^ (i & 7)) << 4));
+            xv[0] = *reinterpret_cast<const float2*>(xb + offi + i * 128);
           }
           const float4* wr = reinterpret_cast<const float4*>(Ws + i * 8);
           float w[8];
@@ -504,11 +535,24 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
         for (int k = 0; k < R; ++k)
 #pragma unroll
           for (int p2 = 0; p2 < CPL / 2; ++p2) ev[k][p2] = f2(0.f, 0.f);
+#ifndef NTT_GSYM
+#define NTT_GSYM 1
+#endif
 #pragma unroll
         for (int l = 0; l < R; ++l) {
+#if NTT_GSYM
+          // G = W^T W is symmetric: G[k][l] = Gs[l * 8 + k], read as two 128-bit words
+          float gl[8];
+          *reinterpret_cast<float4*>(gl) = *reinterpret_cast<const float4*>(Gs + l * 8);
+          if (R > 4) *reinterpret_cast<float4*>(gl + 4) = *reinterpret_cast<const float4*>(Gs + l * 8 + 4);
+#endif
 #pragma unroll
           for (int k = 0; k < R; ++k) {
+#if NTT_GSYM
+            const float g = gl[k];
+#else
             const float g = Gs[k * 8 + l];
+#endif
 #pragma unroll
             for (int p2 = 0; p2 < CPL / 2; ++p2) ev[k][p2] = __ffma2_rn(bc(g), hv[l][p2], ev[k][p2]);
           }
@@ -520,10 +564,15 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
             float2 v;
             v.x = mu_q(hv[k][p2].x, s2[k][p2].x, ev[k][p2].x, eps);
             v.y = mu_q(hv[k][p2].y, s2[k][p2].y, ev[k][p2].y, eps);
-            if (k >= r) v = f2(0.f, 0.f);  // padded ranks (0/0 when eps = 0)
-            // columns beyond n: zero (never stored, never accumulated)
-            if (c0 + 2 * p2 >= n) v.x = 0.f;
-            if (c0 + 2 * p2 + 1 >= n) v.y = 0.f;
+#ifndef NTT_MASKB
+#define NTT_MASKB 0
+#endif
+            if (!NTT_MASKB || masked) {
+              if (k >= r) v = f2(0.f, 0.f);  // padded ranks (0/0 when eps = 0)
+              // columns beyond n: zero (never stored, never accumulated)
+              if (c0 + 2 * p2 >= n) v.x = 0.f;
+              if (c0 + 2 * p2 + 1 >= n) v.y = 0.f;
+            }
             hn[k][p2] = v;
           }
         // store H (in place; this tile's H was already read)
@@ -570,9 +619,6 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
     // ---------------- phase B ----------------
     if (do_acc) {
       __syncwarp();
-      float2 acc[V4 / 2];
-#pragma unroll
-      for (int v = 0; v < V4 / 2; ++v) acc[v] = f2(0.f, 0.f);
 #pragma unroll 2
       for (int s4 = 0; s4 < SL / 4; ++s4) {
         const int c = SL * cs + 4 * s4;
@@ -613,6 +659,10 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
 #pragma unroll
           for (int kp = 0; kp < R / 2; ++kp) acc[UX * (R / 2) + kp] = __ffma2_rn(bc(hq[t]), hq2[t][kp], acc[UX * (R / 2) + kp]);
       }
+      ++ntile;
+    }
+    if (do_acc && (ntile == RS || j + NWT >= J)) {
+      ntile = 0;
       // reduce-scatter over the 4 lanes with the same rb (xor 16, then xor 8)
       float a1[V4];
 #pragma unroll
@@ -633,6 +683,8 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
         const float keep = h0 ? a2[v + V4 / 4] : a2[v];
         accd[v] += (double)(keep + __shfl_xor_sync(0xffffffffu, send, 8));
       }
+#pragma unroll
+      for (int v = 0; v < V4 / 2; ++v) acc[v] = f2(0.f, 0.f);
     }
     // Hn was written over the stage with generic stores: order them before the
     // producer's next TMA (async-proxy) write into this stage
@@ -744,6 +796,8 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   const int64_t J = (ntiles > b) ? (ntiles - b + gridDim.x - 1) / gridDim.x : 0;
 
   unsigned epoch = 0;
+  int ring_s = 0;          // ring stage / parity of the next tile (continues across passes;
+  uint32_t ring_ph = 0;    // incremental: a 64-bit pos % ns was a division call per tile)
   const int nit = persist ? pa.iters + 1 : 1;
   for (int it = 0; it < nit; ++it) {
   const int md = persist ? (it == 0 ? kFusedAcc : (kFusedUpdate | (it < pa.iters ? kFusedAcc : 0))) : mode;
@@ -761,9 +815,12 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       const int pf = (evict_first >> 8) & 255;  // L2 prefetch distance (tiles)
       for (int64_t j = 0; j < pf && j < J; ++j) tma_prefetch_2d(&tmX, (int)((b + j * gridDim.x) * BNC), 0);
       for (int64_t j = 0; j < J; ++j) {
-        const int64_t pos = pbase + j;
-        const int s = (int)(pos % ns);
-        const uint32_t ph = (uint32_t)((pos / ns) & 1);
+        const int s = ring_s;
+        const uint32_t ph = ring_ph;
+        if (++ring_s == ns) {
+          ring_s = 0;
+          ring_ph ^= 1u;
+        }
         if (pf && j + pf < J) tma_prefetch_2d(&tmX, (int)((b + (j + pf) * gridDim.x) * BNC), 0);
         MBAR_WAIT(&empty[s], ph ^ 1u, 3, j);
         mbar_expect_tx(&full[s], SB);
@@ -787,9 +844,12 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   constexpr int NBAR = NWC * 32;
 
   for (int64_t j = 0; j < J; ++j) {
-    const int64_t pos = pbase + j;
-    const int s = (int)(pos % ns);
-    const uint32_t ph = (uint32_t)((pos / ns) & 1);
+    const int s = ring_s;
+    const uint32_t ph = ring_ph;
+    if (++ring_s == ns) {
+      ring_s = 0;
+      ring_ph ^= 1u;
+    }
     MBAR_WAIT(&full[s], ph, 4, j);
     const unsigned char* st = stages + (size_t)s * SB;
     const int64_t jt = (b + j * gridDim.x) * BNC;

@@ -717,7 +717,7 @@ static ntt_status create_common(ntt_handle* out, int device, void* stream) {
   h->stream = reinterpret_cast<cudaStream_t>(stream);
   h->num_sms = prop.multiProcessorCount;
   h->l2_bytes = prop.l2CacheSize;
-  if (getenv("NTT_PERSIST_TRACE")) cudaMallocManaged(&h->ptrace, sizeof(unsigned long long) * 4 * 4096);
+  if (getenv("NTT_PERSIST_TRACE")) cudaMallocManaged(&h->ptrace, sizeof(unsigned long long) * (4 * 4096 + 2048));
   *out = h;
   return NTT_OK;
 }
