@@ -296,13 +296,15 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   uint64_t* empty = full + ns;
   // Dynamic stage assignment (no head-of-line blocking between the warp-owned
   // tiles): the producer loads tile `pos` into ANY free stage s (bit s of
-  // free_mask, set again by the consuming warp when it is done), records
-  // slot[pos % 32] = s | parity << 8 and then publishes issued = pos + 1
-  // (release); the consumer reads its slot after acquiring `issued`.  At most ns
-  // tiles are issued-but-unreleased, so a 32-entry slot ring cannot be overrun.
+  // free_mask, set again by the consuming warp when it is done), tags the stage
+  // tag[s] = pos << 1 | fill parity and then publishes issued = pos + 1
+  // (release).  The consumer, after acquiring `issued`, finds the stage whose tag
+  // holds its pos (one ballot over the <= 24 tags).  A stage's tag cannot change
+  // before its consumer releases it, so there is no overrun however far the
+  // other warps run ahead (a 32-entry pos % 32 slot ring could be overwritten).
   uint32_t* issued = reinterpret_cast<uint32_t*>(empty + ns);
   uint32_t* free_mask = issued + 1;
-  uint32_t* slot = issued + 2;  // [32]
+  uint32_t* tag = issued + 2;  // [ns <= 24]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool persist = pa.iters > 0;
@@ -329,6 +331,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
     }
     *issued = 0u;
     *free_mask = (ns >= 32) ? 0xffffffffu : ((1u << ns) - 1u);
+    for (int q = 0; q < ns; ++q) tag[q] = 0xffffffffu;  // never a valid pos << 1 | parity
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -375,7 +378,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
         atomicAnd(free_mask, ~(1u << s));
         const uint32_t ph = (par_mask >> s) & 1u;
         par_mask ^= 1u << s;
-        slot[pos & 31] = (uint32_t)s | (ph << 8);
+        tag[s] = ((uint32_t)pos << 1) | ph;
         mbar_expect_tx(&full[s], XB + (HDIRECT ? 0u : HB));
         const int col0 = (int)((b + j * gridDim.x) * BNT);
         unsigned char* st = stages + (size_t)s * SB;
@@ -421,18 +424,17 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   for (int t = 0; t < 8; ++t) offA[t] = ((qch ^ t) << 4);
   (void)offA;
 
-  for (int64_t j = warp; j < J; j += NWT) {
-    const int64_t pos = pbase + j;
-    const int64_t jt = (b + j * gridDim.x) * BNT;  // first column of the tile
-    const int64_t c0 = jt + cq;
-    // H columns c0..c0+CPL-1 of this tile (HDIRECT: independent of the stage, issued first)
-    float2 hv[R][CPL / 2];
+  // HDIRECT: this lane's H columns of a tile, loaded ONE TILE AHEAD (software
+  // pipelined: the global-load latency overlaps the previous tile's work; each
+  // tile's H is only read and written by its owning warp, so the early read is safe)
+  auto load_h = [&](int64_t jj, float2 (&dst)[R][CPL / 2]) {
+    const int64_t cc = (b + jj * gridDim.x) * BNT + cq;
 #pragma unroll
     for (int l = 0; l < R; ++l) {
       float hx[4] = {0.f, 0.f, 0.f, 0.f};
-      if (HDIRECT && l < r) {
-        const float* hp = H + (int64_t)l * n + c0;
-        if (c0 + CPL - 1 < n) {
+      if (l < r && jj < J) {
+        const float* hp = H + (int64_t)l * n + cc;
+        if (cc + CPL - 1 < n) {
           if (CPL == 4) {
             const float4 h4 = *reinterpret_cast<const float4*>(hp);
             hx[0] = h4.x; hx[1] = h4.y; hx[2] = h4.z; hx[3] = h4.w;
@@ -443,12 +445,26 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
         } else {
 #pragma unroll
           for (int t = 0; t < CPL - 1; ++t)
-            if (c0 + t < n) hx[t] = hp[t];
+            if (cc + t < n) hx[t] = hp[t];
         }
       }
 #pragma unroll
-      for (int p2 = 0; p2 < CPL / 2; ++p2) hv[l][p2] = f2(hx[2 * p2], hx[2 * p2 + 1]);
+      for (int p2 = 0; p2 < CPL / 2; ++p2) dst[l][p2] = f2(hx[2 * p2], hx[2 * p2 + 1]);
     }
+  };
+  float2 hnext[R][CPL / 2];
+  if (HDIRECT) load_h(warp, hnext);
+
+  for (int64_t j = warp; j < J; j += NWT) {
+    const int64_t pos = pbase + j;
+    const int64_t jt = (b + j * gridDim.x) * BNT;  // first column of the tile
+    const int64_t c0 = jt + cq;
+    float2 hv[R][CPL / 2];
+#pragma unroll
+    for (int l = 0; l < R; ++l)
+#pragma unroll
+      for (int p2 = 0; p2 < CPL / 2; ++p2) hv[l][p2] = HDIRECT ? hnext[l][p2] : f2(0.f, 0.f);
+    if (HDIRECT) load_h(j + NWT, hnext);
     {
 #ifdef NTT_WATCHDOG
       long long t0 = clock64();
@@ -466,9 +482,10 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
       }
     }
     __syncwarp();
-    const uint32_t so = __shfl_sync(0xffffffffu, lane == 0 ? *reinterpret_cast<volatile uint32_t*>(slot + (pos & 31)) : 0u, 0);
-    const int s = (int)(so & 255u);
-    const uint32_t ph = so >> 8;
+    const uint32_t tg = lane < ns ? *reinterpret_cast<volatile uint32_t*>(tag + lane) : 0xffffffffu;
+    const unsigned hit = __ballot_sync(0xffffffffu, (tg >> 1) == (uint32_t)pos && lane < ns);
+    const int s = __ffs(hit) - 1;
+    const uint32_t ph = __shfl_sync(0xffffffffu, tg, s) & 1u;
     MBAR_WAIT(&full[s], ph, 2, j);
     const unsigned char* st = stages + (size_t)s * SB;
     float* Hw = HDIRECT ? HwDirect : reinterpret_cast<float*>(stages + (size_t)s * SB + XB);
@@ -745,8 +762,8 @@ constexpr int SMEM_C = 113 * 1024;      // two CTAs per SM
 
 __device__ __forceinline__ int hnc_idx(int c, int k) { return c * 8 + k + 4 * (c >> 3); }
 
-template <int MP>
-__global__ void __launch_bounds__(NTC, 2)
+template <int MP, int NW>
+__global__ void __launch_bounds__((NW + 1) * 32, NW == 4 ? 2 : 1)
 k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmH, int m, int64_t n, int r,
           const float* __restrict__ W, const double* __restrict__ Gpart, int nG, float eps, float* __restrict__ H,
           double* __restrict__ Ppart, double* __restrict__ Qpart, int mode, int ns, int evict_first,
@@ -754,13 +771,18 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   extern __shared__ unsigned char smem_raw[];
   // keep the shared address space visible to the compiler (LDS/STS, not generic LD/ST)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  constexpr int RW = MP / NWC;          // rows per warp (32 or 64)
+  constexpr int RW = MP / NW;           // rows per warp (32 or 64)
   constexpr int NCH = RW / 32;          // phase-B sub-chunks of 32 rows
+  static_assert(RW >= 32 && RW % 32 == 0, "k_fused_c: at least 32 rows per consumer warp");
+  constexpr int HH = 256 / (NW * 32);   // H-update (k, c) pairs per thread
+  constexpr int QR = 8 / NW;            // Q rows per warp
+  constexpr bool WREG = (RW == 32);     // W rows of this warp kept in registers
+  constexpr int NTHR = (NW + 1) * 32;
   constexpr uint32_t XB = MP * 128u;
   constexpr uint32_t SB = XB + 1024u;
   unsigned char* stages = smem;
-  float* Sred = reinterpret_cast<float*>(smem + (size_t)ns * SB);  // [NWC][8 k][32 c]
-  float* Gs = Sred + NWC * 8 * 32;                                   // 8 x 8
+  float* Sred = reinterpret_cast<float*>(smem + (size_t)ns * SB);  // [NW][8 k][32 c]
+  float* Gs = Sred + NW * 8 * 32;                                    // 8 x 8
   float* Hn = Gs + 64;                                               // HNC_FLOATS
   float* Wc = Hn + HNC_FLOATS;                                       // MP x 8 (rank padded)
   uint64_t* full = reinterpret_cast<uint64_t*>(Wc + MP * 8);
@@ -770,7 +792,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   const bool persist = pa.iters > 0;
   if (!persist && (mode & kFusedUpdate)) {
     const int rr = r * r;
-    for (int e = tid; e < 64; e += NTC) {
+    for (int e = tid; e < 64; e += NTHR) {
       int k = e >> 3, l = e & 7;
       double sum = 0.0;
       if (k < r && l < r)
@@ -778,14 +800,14 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       Gs[e] = (float)sum;
     }
   }
-  for (int e = tid; e < MP * 8; e += NTC) {
+  for (int e = tid; e < MP * 8; e += NTHR) {
     const int i = e >> 3, k = e & 7;
     Wc[e] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
   }
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NWC);
+      mbar_init(&empty[s], NW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -805,7 +827,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   const bool do_acc = (md & kFusedAcc) != 0;
   const int64_t pbase = (int64_t)it * J;
   pstamp(pa, it, 0);
-  if (warp == NWC) {
+  if (warp == NW) {
     if (lane == 0) {
       uint64_t policy;
       if (evict_first & 1)
@@ -839,9 +861,17 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   for (int h = 0; h < NCH; ++h)
 #pragma unroll
     for (int v = 0; v < 8; ++v) accd[h][v] = 0.0;
-  double qd0 = 0.0, qd1 = 0.0;
+  double qd[QR];
+#pragma unroll
+  for (int qq = 0; qq < QR; ++qq) qd[qq] = 0.0;
   const bool h1 = (lane >> 4) & 1, h0 = (lane >> 3) & 1;
-  constexpr int NBAR = NWC * 32;
+  constexpr int NBAR = NW * 32;
+  // this warp's W rows (ranks 2g, 2g+1) in registers when it owns 32 rows
+  float2 wreg[WREG ? 32 : 1];
+  if constexpr (WREG) {
+#pragma unroll
+    for (int v = 0; v < 32; ++v) wreg[v] = *reinterpret_cast<const float2*>(Wc + (warp * RW + v) * 8 + 2 * g);
+  }
 
   for (int64_t j = 0; j < J; ++j) {
     const int s = ring_s;
@@ -857,12 +887,14 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     if (do_update) {
       // ---- phase A: partial S over this warp's rows
       float2 sa = f2(0.f, 0.f), sb = f2(0.f, 0.f), sc = f2(0.f, 0.f), sd = f2(0.f, 0.f);
-#pragma unroll 8
+#pragma unroll WREG ? 32 : 8
       for (int v = 0; v < RW; ++v) {
         const int i = warp * RW + v;
         const float4 x = lds128(st + i * 128 + ((q ^ (i & 7)) << 4));
         const float2 x01 = f2(x.x, x.y), x23 = f2(x.z, x.w);
-        const float2 wv = *reinterpret_cast<const float2*>(Wc + i * 8 + 2 * g);
+        float2 wv;
+        if constexpr (WREG) wv = wreg[v];
+        else wv = *reinterpret_cast<const float2*>(Wc + i * 8 + 2 * g);
         sa = __ffma2_rn(bc(wv.x), x01, sa);
         sb = __ffma2_rn(bc(wv.x), x23, sb);
         sc = __ffma2_rn(bc(wv.y), x01, sc);
@@ -875,15 +907,15 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     asm volatile("bar.sync 1, %0;" ::"r"(NBAR) : "memory");
     // ---- H update: thread handles (k, c) for k in {kt, kt+4}, c = ct
 #pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      const int kt = (tid >> 5) + 4 * hh, ct = tid & 31;
+    for (int hh = 0; hh < HH; ++hh) {
+      const int kt = (tid >> 5) + NW * hh, ct = tid & 31;
       const int64_t col = jt + ct;
       const float hkc = *reinterpret_cast<const float*>(st + XB + kt * 128 + (((ct >> 2) ^ kt) << 4) + (ct & 3) * 4);
       float hn;
       if (do_update) {
         float S = 0.0f;
 #pragma unroll
-        for (int w = 0; w < NWC; ++w) S += Sred[(w * 8 + kt) * 32 + ct];
+        for (int w = 0; w < NW; ++w) S += Sred[(w * 8 + kt) * 32 + ct];
         float hl[8];
 #pragma unroll
         for (int l = 0; l < 8; ++l)
@@ -907,16 +939,18 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     if (do_acc) {
       // ---- phase B
       {
-        float qa0 = 0.f, qa1 = 0.f;
+        float qa[QR];
+#pragma unroll
+        for (int qq = 0; qq < QR; ++qq) qa[qq] = 0.f;
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
           const float* src = Hn + hnc_idx(8 * cs + t, 0);
           const float hr = src[rb];
-          qa0 = fmaf(src[2 * warp], hr, qa0);
-          qa1 = fmaf(src[2 * warp + 1], hr, qa1);
+#pragma unroll
+          for (int qq = 0; qq < QR; ++qq) qa[qq] = fmaf(src[QR * warp + qq], hr, qa[qq]);
         }
-        qd0 += (double)qa0;
-        qd1 += (double)qa1;
+#pragma unroll
+        for (int qq = 0; qq < QR; ++qq) qd[qq] += (double)qa[qq];
       }
 #pragma unroll
       for (int h = 0; h < NCH; ++h) {
@@ -994,14 +1028,12 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       const int row = warp * RW + 32 * h + rb + 8 * u;
       if (row < m && k < r) Pb[row * r + k] = accd[h][v];
     }
-  // Q rows 2w, 2w+1, column rb: sum the 4 column slices
-  qd0 += __shfl_xor_sync(0xffffffffu, qd0, 16);
-  qd0 += __shfl_xor_sync(0xffffffffu, qd0, 8);
-  qd1 += __shfl_xor_sync(0xffffffffu, qd1, 16);
-  qd1 += __shfl_xor_sync(0xffffffffu, qd1, 8);
-  if (cs == 0 && rb < r) {
-    if (2 * warp < r) Qb[(2 * warp) * r + rb] = qd0;
-    if (2 * warp + 1 < r) Qb[(2 * warp + 1) * r + rb] = qd1;
+  // Q rows QR w + qq, column rb: sum the 4 column slices
+#pragma unroll
+  for (int qq = 0; qq < QR; ++qq) {
+    qd[qq] += __shfl_xor_sync(0xffffffffu, qd[qq], 16);
+    qd[qq] += __shfl_xor_sync(0xffffffffu, qd[qq], 8);
+    if (cs == 0 && rb < r && QR * warp + qq < r) Qb[(QR * warp + qq) * r + rb] = qd[qq];
   }
   }
   }  // consumer warps
@@ -1010,13 +1042,14 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   }  // passes
 }
 
-size_t fixed_bytes_c(int MP) {
-  return (size_t)NWC * 8 * 32 * 4 + 256 + HNC_FLOATS * 4 + (size_t)MP * 8 * 4 + 2 * 16 * 8 + 1024;
+size_t fixed_bytes_c(int MP, int NW) {
+  return (size_t)NW * 8 * 32 * 4 + 256 + HNC_FLOATS * 4 + (size_t)MP * 8 * 4 + 2 * 16 * 8 + 1024;
 }
 
-int stages_c(int MP) {
+int stages_c(int MP, int NW) {
   const size_t SB = (size_t)MP * 128 + 1024;
-  int ns = (int)((SMEM_C - fixed_bytes_c(MP)) / SB);
+  const size_t budget = NW == 4 ? (size_t)SMEM_C : (size_t)SMEM_BUDGET;  // 2 CTAs / SM or 1
+  int ns = (int)((budget - fixed_bytes_c(MP, NW)) / SB);
   return ns > 12 ? 12 : ns;
 }
 
@@ -1037,17 +1070,26 @@ cudaError_t launch_maybe_coop(void (*kern)(KArgs...), int grid, int threads, siz
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
-template <int MP>
+template <int MP, int NW>
 cudaError_t launch_c(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_t n, int r, const float* W,
                      const double* Gpart, int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
                      int evict_first, const PersistArgs& pa, cudaStream_t st) {
-  const int ns = stages_c(MP);
+  const int ns = stages_c(MP, NW);
   const size_t SB = (size_t)MP * 128 + 1024;
-  const size_t smem = (size_t)ns * SB + fixed_bytes_c(MP);
-  cudaError_t e = cudaFuncSetAttribute(k_fused_c<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = (size_t)ns * SB + fixed_bytes_c(MP, NW);
+  cudaError_t e = cudaFuncSetAttribute(k_fused_c<MP, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_maybe_coop(k_fused_c<MP>, grid, NTC, smem, st, pa.iters > 0, mx, mh, m, n, r, W, Gpart, nG, eps, H,
-                           Ppart, Qpart, mode, ns, evict_first, pa);
+  return launch_maybe_coop(k_fused_c<MP, NW>, grid, (NW + 1) * 32, smem, st, pa.iters > 0, mx, mh, m, n, r, W, Gpart,
+                           nG, eps, H, Ppart, Qpart, mode, ns, evict_first, pa);
+}
+
+// 8 consumer warps, 1 CTA / SM, W rows in registers for m > 128 (NTT_C_NW=4: the 2-CTA variant)
+int c_nw(int MP) {
+  static const int env = [] {
+    const char* e = getenv("NTT_C_NW");
+    return e ? atoi(e) : 4;  // the 8-warp variant measured slower (502 vs 362 us/iter, step 2)
+  }();
+  return (MP == 256 && env == 8) ? 8 : 4;
 }
 
 // ===========================================================================
@@ -1571,7 +1613,8 @@ int fused_grid(int64_t m, int64_t n, int r, int num_sms) {
     int64_t need = (ntiles + NWW - 1) / NWW;
     return (int)(need < num_sms ? (need < 1 ? 1 : need) : num_sms);
   }
-  return (int)(ntiles < 2 * num_sms ? ntiles : 2 * num_sms);  // variant C: two CTAs per SM
+  const int cps = c_nw(m <= 128 ? 128 : 256) == 8 ? 1 : 2;  // variant C: CTAs per SM
+  return (int)(ntiles < cps * num_sms ? ntiles : cps * num_sms);
 }
 
 size_t fused_scratch_bytes(int64_t, int64_t, int, int) { return 0; }
@@ -1605,8 +1648,10 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
     if (e != cudaSuccess) return e;
     e = make_map(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u);
     if (e != cudaSuccess) return e;
-    if (MPc == 128) return launch_c<128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
-    return launch_c<256>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
+    if (MPc == 128) return launch_c<128, 4>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
+    if (c_nw(256) == 8)
+      return launch_c<256, 8>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
+    return launch_c<256, 4>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
   }
   const int ux = ux_for(m);
   CUtensorMap mx, mh;
