@@ -120,3 +120,34 @@ def test_single_nmf_configs_ten_iterations(h, ora, cfg):
     for got, ref, nm in ((Wd, Wo, "W"), (Hd, Ho, "H")):
         fro, mx = _rel(got.cpu().numpy().reshape(ref.shape), ref)
         assert fro <= TOL and mx <= TOL, (nm, fro, mx)
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("m,n,r,iters", [(6, 6 ** 9, 5, 40), (32, 1 << 22, 8, 30), (256, 1 << 18, 8, 30)])
+def test_persistent_long_runs(h, m, n, r, iters):
+    """Long persistent launches (many passes, many tiles per warp, warps drifting far
+    apart): must terminate, be bit-reproducible, and agree with the per-pass
+    (non-persistent) launches to rounding.  Regression test for a stage-slot ring
+    overrun that hung config 4 step 1 (DESIGN.md s.9)."""
+    import os
+    g = torch.Generator(device="cuda").manual_seed(3)
+    X = torch.rand(m * n, device="cuda", generator=g)
+    W0 = torch.rand(m * r, device="cuda", generator=g)
+    H0 = torch.rand(r * n, device="cuda", generator=g)
+    outs = []
+    for persist in (True, True, False):
+        if persist:
+            os.environ.pop("NTT_NO_PERSIST", None)
+        else:
+            os.environ["NTT_NO_PERSIST"] = "1"
+        W, H = W0.clone(), H0.clone()
+        try:
+            h.ntt_nmf_mu(X, m, n, n, r, iters, 1e-16, W, H)
+            torch.cuda.synchronize()
+        finally:
+            os.environ.pop("NTT_NO_PERSIST", None)
+        outs.append((W.cpu().numpy().astype(np.float64), H.cpu().numpy().astype(np.float64)))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    for a, b in zip(outs[0], outs[2]):
+        assert np.all(np.isfinite(a))
+        assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(b)
