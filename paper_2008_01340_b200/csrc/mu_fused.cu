@@ -167,8 +167,14 @@ __device__ __forceinline__ void grid_sync(unsigned* ctr, unsigned& epoch) {
 // Reduce the per-CTA partials and apply the W update in every CTA (see above).
 // Ws: [i * 8 + k] (rows >= m stay zero), Gs: [k * 8 + l]; scr: >= (L + 16) doubles + m*8 floats
 // + 256 doubles of smem.  Global reads are issued in independent batches (L2 latency is ~1 us).
+// W layout in smem: row-major [i * 8 + k], or (pairs) [i/2][k/2][i%2][k%2] so that a
+// lane reading ranks (2g, 2g+1) of rows (i, i+1) issues one 128-bit load (k_fused_c)
+__device__ __forceinline__ int widx(int i, int k, bool pairs) {
+  return pairs ? ((i >> 1) << 4) + ((k >> 1) << 2) + ((i & 1) << 1) + (k & 1) : (i << 3) + k;
+}
+
 __device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int r, float eps, float* Ws, float* Gs,
-                             double* scr, int it) {
+                             double* scr, int it, bool pairs = false) {
   const int L = m * r + r * r;
   const int T = blockDim.x, tid = threadIdx.x;
   pstamp(pa, it, 1);
@@ -232,13 +238,13 @@ __device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int 
     float v = 0.0f;
     if (k < r) {
       double d = 0.0;
-      for (int l = 0; l < r; ++l) d += (double)Ws[i * 8 + l] * Q[l * r + k];
-      v = (float)mu_quot((double)Ws[i * 8 + k], P[i * r + k], d, (double)eps);
+      for (int l = 0; l < r; ++l) d += (double)Ws[widx(i, l, pairs)] * Q[l * r + k];
+      v = (float)mu_quot((double)Ws[widx(i, k, pairs)], P[i * r + k], d, (double)eps);
     }
     Wn[e] = v;
   }
   __syncthreads();
-  for (int e = tid; e < m * 8; e += T) Ws[e] = Wn[e];
+  for (int e = tid; e < m * 8; e += T) Ws[widx(e >> 3, e & 7, pairs)] = Wn[e];
   // G = Wn^T Wn: 64 entries x C row chunks (fixed order), then combine
   const int GC = T / 64 < 1 ? 1 : (T / 64 > 4 ? 4 : T / 64);
   for (int t = tid; t < 64 * GC; t += T) {
@@ -800,9 +806,10 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       Gs[e] = (float)sum;
     }
   }
+  constexpr bool WPAIR = !WREG;  // W in row-pair layout (one 128-bit load per 2 rows in phase A)
   for (int e = tid; e < MP * 8; e += NTHR) {
     const int i = e >> 3, k = e & 7;
-    Wc[e] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
+    Wc[widx(i, k, WPAIR)] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
   }
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) {
@@ -870,7 +877,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   float2 wreg[WREG ? 32 : 1];
   if constexpr (WREG) {
 #pragma unroll
-    for (int v = 0; v < 32; ++v) wreg[v] = *reinterpret_cast<const float2*>(Wc + (warp * RW + v) * 8 + 2 * g);
+    for (int v = 0; v < 32; ++v) wreg[v] = *reinterpret_cast<const float2*>(Wc + widx(warp * RW + v, 2 * g, false));
   }
 
   for (int64_t j = 0; j < J; ++j) {
@@ -887,18 +894,35 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     if (do_update) {
       // ---- phase A: partial S over this warp's rows
       float2 sa = f2(0.f, 0.f), sb = f2(0.f, 0.f), sc = f2(0.f, 0.f), sd = f2(0.f, 0.f);
-#pragma unroll WREG ? 32 : 8
-      for (int v = 0; v < RW; ++v) {
-        const int i = warp * RW + v;
-        const float4 x = lds128(st + i * 128 + ((q ^ (i & 7)) << 4));
-        const float2 x01 = f2(x.x, x.y), x23 = f2(x.z, x.w);
-        float2 wv;
-        if constexpr (WREG) wv = wreg[v];
-        else wv = *reinterpret_cast<const float2*>(Wc + i * 8 + 2 * g);
-        sa = __ffma2_rn(bc(wv.x), x01, sa);
-        sb = __ffma2_rn(bc(wv.x), x23, sb);
-        sc = __ffma2_rn(bc(wv.y), x01, sc);
-        sd = __ffma2_rn(bc(wv.y), x23, sd);
+      if constexpr (WREG) {
+#pragma unroll
+        for (int v = 0; v < RW; ++v) {
+          const int i = warp * RW + v;
+          const float4 x = lds128(st + i * 128 + ((q ^ (i & 7)) << 4));
+          const float2 x01 = f2(x.x, x.y), x23 = f2(x.z, x.w);
+          const float2 wv = wreg[v & 31];
+          sa = __ffma2_rn(bc(wv.x), x01, sa);
+          sb = __ffma2_rn(bc(wv.x), x23, sb);
+          sc = __ffma2_rn(bc(wv.y), x01, sc);
+          sd = __ffma2_rn(bc(wv.y), x23, sd);
+        }
+      } else {
+#pragma unroll 4
+        for (int v = 0; v < RW; v += 2) {
+          const int i = warp * RW + v;
+          const float4 xa = lds128(st + i * 128 + ((q ^ (i & 7)) << 4));
+          const float4 xb = lds128(st + (i + 1) * 128 + ((q ^ ((i + 1) & 7)) << 4));
+          // W[i][2g], W[i][2g+1], W[i+1][2g], W[i+1][2g+1]
+          const float4 w4 = *reinterpret_cast<const float4*>(Wc + widx(i, 2 * g, true));
+          sa = __ffma2_rn(bc(w4.x), f2(xa.x, xa.y), sa);
+          sb = __ffma2_rn(bc(w4.x), f2(xa.z, xa.w), sb);
+          sc = __ffma2_rn(bc(w4.y), f2(xa.x, xa.y), sc);
+          sd = __ffma2_rn(bc(w4.y), f2(xa.z, xa.w), sd);
+          sa = __ffma2_rn(bc(w4.z), f2(xb.x, xb.y), sa);
+          sb = __ffma2_rn(bc(w4.z), f2(xb.z, xb.w), sb);
+          sc = __ffma2_rn(bc(w4.w), f2(xb.x, xb.y), sc);
+          sd = __ffma2_rn(bc(w4.w), f2(xb.z, xb.w), sd);
+        }
       }
       float* sr = Sred + (warp * 8 + 2 * g) * 32 + 4 * q;
       *reinterpret_cast<float4*>(sr) = make_float4(sa.x, sa.y, sb.x, sb.y);
@@ -1038,7 +1062,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   }
   }  // consumer warps
   if (!persist || !do_acc) break;
-  persist_step(pa, epoch, m, r, eps, Wc, Gs, reinterpret_cast<double*>(stages), it);
+  persist_step(pa, epoch, m, r, eps, Wc, Gs, reinterpret_cast<double*>(stages), it, WPAIR);
   }  // passes
 }
 
