@@ -339,3 +339,57 @@ def compression_ratio(dims, ranks) -> float:
     """Eq. 4 (P:448-451)."""
     D, R = _dims(dims), _ranks(ranks)
     return float(lib().ora_compression_ratio(len(D), _ptr(D), _ptr(R)))
+
+
+# ------------------------------------------- SVD rank rule (SURVEY s.8(f) f2) --
+def svd_tail_rank(X: np.ndarray, tt_eps: float, rmax: Optional[int] = None) -> int:
+    """Alg. 2 l.5-6 and section III-A: r = the smallest k in
+    [1, N], N = min(m, n), with sqrt(s_{k+1}^2 + ... + s_N^2) / sqrt(s_1^2 + ... + s_N^2)
+    <= eps.  Singular values by LAPACK (numpy.linalg.svd -- a library primitive used
+    as one step, SURVEY s.8(c)); the tail sums are accumulated from the smallest
+    value up.  Optional cap rmax (reading R21).  An all-zero X gives r = 1."""
+    s = np.linalg.svd(np.asarray(X, dtype=np.float64), compute_uv=False)
+    e = s * s
+    N = e.size
+    tot = float(e.sum())
+    if tot == 0.0:
+        return 1
+    # tail[k] = sum_{i > k} e_i (1-based k), k = 1..N
+    asc = np.cumsum(e[::-1])          # asc[j-1] = sum of the j smallest
+    r = N
+    for k in range(1, N + 1):
+        tail = float(asc[N - k - 1]) if k < N else 0.0
+        if np.sqrt(tail / tot) <= tt_eps:
+            r = k
+            break
+    return min(r, rmax) if rmax else r
+
+
+def ntt_decompose_eps(A: np.ndarray, tt_eps: float, iters: int, seed: int = 0, eps: float = 1e-16,
+                      max_ranks: Optional[Sequence[int]] = None):
+    """Alg. 2 with the SVD rank rule of l.5-6 at every step (ranks chosen
+    from the current unfolding X_l = reshape(H_{l-1})) and MU NMF (R1-R4); inits as
+    ntt_decompose (streams 0x200 + 2l / 0x201 + 2l).  Returns (ranks, packed fp64 cores)."""
+    A = np.ascontiguousarray(A, dtype=np.float32)
+    dims = list(A.shape)
+    d = len(dims)
+    T = A.reshape(-1)
+    rprev = 1
+    ranks, cores = [], []
+    rest = T.size
+    for l in range(1, d):
+        m = rprev * dims[l - 1]
+        rest //= dims[l - 1]
+        n = rest
+        X = T.reshape(m, n)
+        cap = min(m, n, max_ranks[l - 1]) if max_ranks else min(m, n)
+        r = svd_tail_rank(X, tt_eps, cap)
+        W0 = fill_uniform(m * r, seed, stream_w(l)).reshape(m, r)
+        H0 = fill_uniform(r * n, seed, stream_h(l)).reshape(r, n)
+        W, H = nmf_mu(X, W0, H0, iters, eps)
+        cores.append(W.reshape(-1))
+        ranks.append(r)
+        T = H.reshape(-1)
+        rprev = r
+    cores.append(T)
+    return ranks, np.concatenate(cores)
