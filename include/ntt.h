@@ -132,6 +132,31 @@ ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t*
                          const int32_t* ranks, int32_t iters, uint64_t seed, float eps,
                          float* cores, double* rel_err, void* workspace, size_t workspace_bytes);
 
+/* ------------------------------------------- eps-driven nTT (SVD rank rule) --
+ * Alg. 2 with the rank rule of l.5-6 (section III-A): at every
+ * step the rank is r_l = the smallest k in [1, N], N = min(m, n) of the current
+ * unfolding X_l, with sqrt(s_{k+1}^2 + ... + s_N^2) / sqrt(s_1^2 + ... + s_N^2)
+ * <= tt_eps, capped at max_ranks[l-1] (nullable; default and hard limit 64); then
+ * MU NMF with that rank as in ntt_decompose (same inits, eps, iters).  The squared
+ * singular values are the eigenvalues of the fp64 Gram matrix of X_l (computed on
+ * the device: split-K Gram, Householder tridiagonalisation and bisection), so the
+ * rule is exact for tt_eps >= ~1e-7 (reading R21); each step needs
+ * min(m, n) <= 512 (else NTT_ERR_UNSUPPORTED).  The call synchronises once per step
+ * (the next step's shapes depend on the chosen rank).
+ *   cores : packed output (device or host) with room for cores_capacity floats;
+ *           the layout is ntt_decompose's for the chosen ranks (NTT_ERR_WORKSPACE if
+ *           the capacity is too small -- ranks_out is filled either way).
+ *   ranks_out : d-1 chosen inner ranks (host).  rel_err: nullable, Eq. 3.
+ * Single-GPU handles only (NTT_ERR_UNSUPPORTED on a distributed handle).      */
+ntt_status ntt_decompose_eps(ntt_handle h, const float* A, int32_t d, const int64_t* dims, double tt_eps,
+                             const int32_t* max_ranks, int32_t iters, uint64_t seed, float eps, float* cores,
+                             int64_t cores_capacity, int32_t* ranks_out, double* rel_err);
+/* The rank rule alone on a device matrix X (m x n, row stride ldx,
+ * min(m, n) <= 512): *rank = r for tt_eps; eig (nullable host, min(m, n)
+ * doubles) receives the squared singular values in ascending order.            */
+ntt_status ntt_rank_rule(ntt_handle h, const float* X, int64_t m, int64_t n, int64_t ldx, double tt_eps,
+                         int32_t* rank, double* eig);
+
 /* --------------------------------------------------- reconstruction / error
  * Contract a TT (Eq. 1):  A~ = G_1 o G_2 o ... o G_d, and/or the
  * relative error of Eq. 3: ||ref - A~||_F / ||ref||_F by direct

@@ -185,6 +185,25 @@ class Handle:
                                           _ptr(ref), ctypes.byref(err) if err is not None else None))
         return float(err.value) if want_error else None
 
+    def ntt_decompose_eps(self, A, dims, tt_eps: float, iters: int, seed: int, eps: float, cores,
+                          cores_capacity: int, max_ranks=None, want_error: bool = False):
+        """Alg. 2 with the SVD rank rule (l.5-6); returns (ranks, rel_err or None)."""
+        d = len(dims)
+        rk = (ctypes.c_int32 * max(d - 1, 1))()
+        err = ctypes.c_double(-1.0) if want_error else None
+        mr = _i32arr(max_ranks) if max_ranks is not None else None
+        self._check(lib().ntt_decompose_eps(self._h, _ptr(A), d, _i64arr(dims), tt_eps, mr, iters, seed, eps,
+                                            _ptr(cores), cores_capacity, rk,
+                                            ctypes.byref(err) if err is not None else None))
+        return [int(x) for x in rk][: d - 1], (float(err.value) if want_error else None)
+
+    def ntt_rank_rule(self, X, m: int, n: int, ldx: int, tt_eps: float, want_eig: bool = False):
+        """SVD rank rule on a device matrix; returns (rank, eigenvalues ascending or None)."""
+        r = ctypes.c_int32()
+        eig = (ctypes.c_double * min(m, n))() if want_eig else None
+        self._check(lib().ntt_rank_rule(self._h, _ptr(X), m, n, ldx, tt_eps, ctypes.byref(r), eig))
+        return int(r.value), (list(eig) if want_eig else None)
+
     def ntt_generate(self, dims, ranks, cores, noise_amp: float, seed: int, noise_stream: int, out):
         self._check(lib().ntt_generate(self._h, len(dims), _i64arr(dims), _i32arr(ranks), _ptr(cores), noise_amp,
                                        seed, noise_stream, _ptr(out)))

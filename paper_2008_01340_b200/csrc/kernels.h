@@ -42,6 +42,13 @@ bool tiny_supported(int64_t m, int64_t n, int r);
 cudaError_t launch_tiny(const float* X, int64_t ldx, int64_t m, int64_t n, int r, int iters, float eps, float* W,
                         float* H, cudaStream_t st);
 
+// SVD rank rule of Alg. 2 l.5-6 (tt_rank.cu): Gram of X (min(m, n) <= 512) -> eigenvalues
+// (Householder + bisection, one CTA) -> r = smallest k with tail energy <= tt_eps.
+// Writes d_rank[0] (and the N eigenvalues ascending to d_eig when non-null).
+size_t rank_rule_bytes(int64_t N, int64_t T, int num_sms);
+cudaError_t launch_rank_rule(const float* X, int64_t m, int64_t n, int64_t ldx, double tt_eps, char* ws,
+                             int num_sms, int* d_rank, double* d_eig, cudaStream_t st);
+
 // 1/2 ||X - W H||^2 partial sums (fp64), one per CTA; returns number of partials.
 int objective_ctas(int64_t n);
 cudaError_t launch_objective(const float* X, int64_t ldx, int64_t m, int64_t n, const float* W,

@@ -1085,6 +1085,145 @@ ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t*
   return NTT_OK;
 }
 
+ntt_status ntt_decompose_eps(ntt_handle h, const float* A, int32_t d, const int64_t* dims, double tt_eps,
+                             const int32_t* max_ranks, int32_t iters, uint64_t seed, float eps, float* cores,
+                             int64_t cores_capacity, int32_t* ranks_out, double* rel_err) {
+  if (!h) return NTT_ERR_INVALID_ARG;
+  if (!A || !cores || !ranks_out) return fail(h, NTT_ERR_INVALID_ARG, "null A, cores or ranks_out");
+  if (iters < 0) return fail(h, NTT_ERR_INVALID_ARG, "iters < 0");
+  if (!(eps >= 0.0f)) return fail(h, NTT_ERR_INVALID_ARG, "eps must be >= 0");
+  if (!(tt_eps >= 0.0)) return fail(h, NTT_ERR_INVALID_ARG, "tt_eps must be >= 0");
+  if (h->nranks > 1)
+    return fail(h, NTT_ERR_UNSUPPORTED, "ntt_decompose_eps runs on a single-GPU handle (rank rule per step)");
+  // ---- shape, caps (upper bounds of the data-dependent ranks) and workspace plan
+  TTShape s0;
+  std::vector<int32_t> ones((size_t)std::max(d - 1, 1), 1);
+  ntt_status st = check_tt(h, d, dims, ones.data(), &s0, false);
+  if (st) return st;
+  int64_t cap[65], mcap[65], ncol[65];
+  cap[0] = 1;
+  int64_t rest = s0.N;
+  size_t hbuf[2] = {1, 1}, wmax = 1, mu_bytes = 0, rk_bytes = 0, cores_cap = 0;
+  for (int l = 1; l < d; ++l) {
+    mcap[l] = cap[l - 1] * s0.dims[l - 1];
+    rest /= s0.dims[l - 1];
+    ncol[l] = rest;
+    int64_t c = std::min<int64_t>({(int64_t)kMaxRank, mcap[l], ncol[l]});
+    if (max_ranks) {
+      if (max_ranks[l - 1] < 1) return fail(h, NTT_ERR_RANK, "max_ranks[%d] < 1", l - 1);
+      c = std::min<int64_t>(c, max_ranks[l - 1]);
+    }
+    cap[l] = c;
+    hbuf[(l - 1) & 1] = std::max(hbuf[(l - 1) & 1], (size_t)(c * ncol[l]));
+    wmax = std::max(wmax, (size_t)(mcap[l] * c));
+    cores_cap += (size_t)(mcap[l] * c);
+    // run_mu scratch for every (r_{l-1}, r_l) the rule may pick
+    for (int64_t rp = 1; rp <= cap[l - 1]; ++rp)
+      for (int64_t r = 1; r <= c && r <= rp * s0.dims[l - 1]; ++r)
+        mu_bytes = std::max(mu_bytes, plan_mu(rp * s0.dims[l - 1], ncol[l], (int)r, h->num_sms, 1).bytes);
+    // rank-rule scratch for every Gram size the step can see (min(m, n) <= 512 is checked per step)
+    const int64_t nmax = std::min<int64_t>({mcap[l], ncol[l], 512});
+    for (int64_t Nn = 1; Nn <= nmax; ++Nn)
+      rk_bytes = std::max(rk_bytes, rank_rule_bytes(Nn, std::max(mcap[l], ncol[l]), h->num_sms));
+  }
+  cores_cap += (size_t)(cap[d - 1] * s0.dims[d - 1]);
+  size_t o = 0;
+  const size_t off_h0 = o;
+  o = align_up(o + sizeof(float) * hbuf[0]);
+  const size_t off_h1 = o;
+  o = align_up(o + sizeof(float) * hbuf[1]);
+  const size_t off_w = o;
+  o = align_up(o + sizeof(float) * wmax);
+  const size_t off_c = o;
+  o = align_up(o + sizeof(float) * cores_cap);
+  const size_t off_mu = o;
+  o = align_up(o + mu_bytes);
+  const size_t off_rk = o;
+  o = align_up(o + rk_bytes);
+  const size_t off_int = o;
+  o = align_up(o + 64);
+  CU(h, cudaSetDevice(h->device));
+  if ((st = ensure_ws(h, o))) return st;
+  char* ws = reinterpret_cast<char*>(h->ws);
+  cudaStream_t cs = h->stream;
+  const float* dA = A;
+  if (!is_device_ptr(A)) {
+    if ((st = ensure_stage(h, sizeof(float) * (size_t)s0.N))) return st;
+    dA = reinterpret_cast<const float*>(h->stage);
+    CU(h, cudaMemcpyAsync((void*)dA, A, sizeof(float) * (size_t)s0.N, cudaMemcpyHostToDevice, cs));
+  }
+  float* hb[2] = {reinterpret_cast<float*>(ws + off_h0), reinterpret_cast<float*>(ws + off_h1)};
+  float* Wd = reinterpret_cast<float*>(ws + off_w);
+  float* dcores = reinterpret_cast<float*>(ws + off_c);
+  int* d_rank = reinterpret_cast<int*>(ws + off_int);
+  // ---- the sweep: rank rule on the current unfolding, then MU NMF with that rank (Alg. 2 l.4-9)
+  const float* X = dA;
+  float* Hl = nullptr;
+  int64_t rprev = 1, coff = 0;
+  for (int l = 1; l < d; ++l) {
+    const int64_t m = rprev * s0.dims[l - 1], n = ncol[l];
+    h->cur_step = l;
+    if (std::min(m, n) > 512)
+      return fail(h, NTT_ERR_UNSUPPORTED, "rank rule needs min(m, n) <= 512 (step %d: %lld x %lld)", l,
+                  (long long)m, (long long)n);
+    LAUNCH(h, launch_rank_rule(X, m, n, n, tt_eps, ws + off_rk, h->num_sms, d_rank, nullptr, cs));
+    int rk = 1;
+    CU(h, cudaMemcpyAsync(&rk, d_rank, sizeof(int), cudaMemcpyDeviceToHost, cs));
+    CU(h, cudaStreamSynchronize(cs));
+    const int r = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)rk, cap[l], m, n}));
+    ranks_out[l - 1] = r;
+    Hl = hb[(l - 1) & 1];
+    LAUNCH(h, launch_fill_uniform(Wd, m * r, seed, stream_w(l), 0, cs));
+    LAUNCH(h, launch_fill_uniform(Hl, (int64_t)r * n, seed, stream_h(l), 0, cs));
+    MuPlan p = plan_mu(m, n, r, h->num_sms, 1);
+    if (p.bytes > mu_bytes) return fail(h, NTT_ERR_WORKSPACE, "internal: MU scratch plan exceeded");
+    if ((st = run_mu(h, p, X, n, iters, eps, Wd, Hl, ws + off_mu, nullptr))) return st;
+    CU(h, cudaMemcpyAsync(dcores + coff, Wd, sizeof(float) * (size_t)(m * r), cudaMemcpyDeviceToDevice, cs));
+    coff += m * r;
+    X = Hl;
+    rprev = r;
+  }
+  h->cur_step = 0;
+  const int64_t ncl = rprev * s0.dims[d - 1];
+  CU(h, cudaMemcpyAsync(dcores + coff, Hl, sizeof(float) * (size_t)ncl, cudaMemcpyDeviceToDevice, cs));
+  coff += ncl;
+  if (coff > cores_capacity)
+    return fail(h, NTT_ERR_WORKSPACE, "cores_capacity %lld < %lld floats for the chosen ranks",
+                (long long)cores_capacity, (long long)coff);
+  CU(h, cudaMemcpyAsync(cores, dcores, sizeof(float) * (size_t)coff, cudaMemcpyDefault, cs));
+  CU(h, cudaStreamSynchronize(cs));
+  if (rel_err) {
+    TTShape s;
+    if ((st = check_tt(h, d, dims, ranks_out, &s, true))) return st;
+    if ((st = contract_stream(h, s, cores, nullptr, 0.0f, 0, A, rel_err))) return st;
+  }
+  return NTT_OK;
+}
+
+ntt_status ntt_rank_rule(ntt_handle h, const float* X, int64_t m, int64_t n, int64_t ldx, double tt_eps,
+                         int32_t* rank, double* eig) {
+  if (!h || !X || !rank) return NTT_ERR_INVALID_ARG;
+  if (m < 1 || n < 1 || ldx < n) return fail(h, NTT_ERR_INVALID_ARG, "bad shape");
+  if (!(tt_eps >= 0.0)) return fail(h, NTT_ERR_INVALID_ARG, "tt_eps must be >= 0");
+  if (std::min(m, n) > 512) return fail(h, NTT_ERR_UNSUPPORTED, "rank rule needs min(m, n) <= 512");
+  if (!is_device_ptr(X)) return fail(h, NTT_ERR_INVALID_ARG, "X must be device memory");
+  CU(h, cudaSetDevice(h->device));
+  const int64_t N = std::min(m, n);
+  const size_t rb = align_up(rank_rule_bytes(N, std::max(m, n), h->num_sms));
+  ntt_status st = ensure_ws(h, rb + align_up(64) + align_up(sizeof(double) * (size_t)N));
+  if (st) return st;
+  char* ws = reinterpret_cast<char*>(h->ws);
+  int* d_rank = reinterpret_cast<int*>(ws + rb);
+  double* d_eig = reinterpret_cast<double*>(ws + rb + align_up(64));
+  LAUNCH(h, launch_rank_rule(X, m, n, ldx, tt_eps, ws, h->num_sms, d_rank, d_eig, h->stream));
+  int rk = 0;
+  CU(h, cudaMemcpyAsync(&rk, d_rank, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  if (eig) CU(h, cudaMemcpyAsync(eig, d_eig, sizeof(double) * (size_t)N, cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  *rank = rk;
+  return NTT_OK;
+}
+
 ntt_status ntt_reconstruct(ntt_handle h, int32_t d, const int64_t* dims, const int32_t* ranks, const float* cores,
                            float* out, const float* ref, double* rel_err) {
   if (!h) return NTT_ERR_INVALID_ARG;

@@ -1,0 +1,298 @@
+// tt_rank.cu -- the SVD rank rule of Alg. 2 l.5-6 (section III-A P:194;
+// SURVEY s.8(f) f2) on the GPU:
+//   r_l = smallest k in [1, N] with sqrt(s_{k+1}^2 + ... + s_N^2) / sqrt(sum s_i^2) <= eps
+// for the current unfolding X (m x n, N = min(m, n)).  The squared singular values
+// are the eigenvalues of the Gram matrix C = X X^T (m <= 512; padded with m - n
+// zeros when n < m) or C = X^T X (n <= 512 < m):
+//   k_gram         split-K tiles of C, fp64 FMA on the fp32 inputs (exact products), fixed order
+//   k_gram_sum     fixed-order sum of the split partials, symmetric fill
+//   k_eig_rank     ONE CTA: Householder tridiagonalisation of C (fp64, matrix in global /
+//                  L2), Sturm-count bisection for every eigenvalue, then the tail rule
+// Gram-based eigenvalues carry an absolute error ~1e-16 * trace(C), so the rule is
+// exact for eps >= ~1e-7 (reading R21).  Deterministic (fixed reduction orders).
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ntt {
+
+namespace {
+
+constexpr int GT = 32;   // Gram output tile (GT x GT)
+constexpr int GK = 32;   // columns of the long dimension per smem block
+
+// C tile (ta, tb) (tb >= ta) over the split's range of the long index t:
+// u_t[a] = X[a * sa + t * st]  (X X^T: sa = ldx, st = 1;  X^T X: sa = 1, st = ldx)
+__global__ void __launch_bounds__(256)
+k_gram(const float* __restrict__ X, int64_t sa, int64_t st, int N, int64_t T, int ntile, int64_t chunk,
+       double* __restrict__ part) {
+  __shared__ float As[GT][GK + 1];
+  __shared__ float Bs[GT][GK + 1];
+  // upper-triangular tile index -> (ta, tb)
+  int tix = blockIdx.x, ta = 0;
+  while (tix >= ntile - ta) {
+    tix -= ntile - ta;
+    ++ta;
+  }
+  const int tb = ta + tix;
+  const int split = blockIdx.y;
+  const int64_t t0 = (int64_t)split * chunk, t1 = min(T, t0 + chunk);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 2 x 2 outputs per thread
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (int64_t tb0 = t0; tb0 < t1; tb0 += GK) {
+    for (int e = threadIdx.x; e < GT * GK; e += 256) {
+      // XX^T: consecutive threads along t (contiguous); X^T X: along a (contiguous)
+      int i, k;
+      if (st == 1) {
+        i = e / GK;
+        k = e % GK;
+      } else {
+        i = e % GT;
+        k = e / GT;
+      }
+      const int64_t t = tb0 + k;
+      const int a = ta * GT + i, bb = tb * GT + i;
+      As[i][k] = (t < t1 && a < N) ? X[(int64_t)a * sa + t * st] : 0.0f;
+      Bs[i][k] = (t < t1 && bb < N) ? X[(int64_t)bb * sa + t * st] : 0.0f;
+    }
+    __syncthreads();
+    // fp64 FMA: the product of two fp32 values is exact in fp64, so the Gram (and the
+    // eigenvalues) carry ~1e-16 relative error instead of fp32's ~1e-7
+#pragma unroll 8
+    for (int k = 0; k < GK; ++k) {
+      const double a0 = As[ty][k], a1 = As[ty + 16][k];
+      const double b0 = Bs[tx][k], b1 = Bs[tx + 16][k];
+      acc[0][0] = fma(a0, b0, acc[0][0]);
+      acc[0][1] = fma(a0, b1, acc[0][1]);
+      acc[1][0] = fma(a1, b0, acc[1][0]);
+      acc[1][1] = fma(a1, b1, acc[1][1]);
+    }
+    __syncthreads();
+  }
+  // part[split][tile][GT][GT]
+  const int tile = blockIdx.x;
+  double* dst = part + ((int64_t)split * gridDim.x + tile) * (GT * GT);
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) dst[(ty + 16 * u) * GT + tx + 16 * v] = acc[u][v];
+}
+
+__global__ void k_gram_sum(const double* __restrict__ part, int nsplit, int ntile, int N, double* __restrict__ C) {
+  const int nut = ntile * (ntile + 1) / 2;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)nut * GT * GT;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int tix = (int)(e / (GT * GT));
+    const int w = (int)(e % (GT * GT));
+    const int tile = tix;
+    int ta = 0;
+    while (tix >= ntile - ta) {
+      tix -= ntile - ta;
+      ++ta;
+    }
+    const int tb = ta + tix;
+    const int a = ta * GT + w / GT, b = tb * GT + w % GT;
+    if (a >= N || b >= N) continue;
+    double s = 0.0;
+    for (int sp = 0; sp < nsplit; ++sp) s += part[((int64_t)sp * nut + tile) * (GT * GT) + w];
+    C[(int64_t)a * N + b] = s;
+    C[(int64_t)b * N + a] = s;
+  }
+}
+
+// ---------------------------------------------------------------- eigen + rule
+constexpr int ET = 1024;
+
+__device__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = (threadIdx.x < (int)(blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+    s = warp_sum(s);
+    if (threadIdx.x == 0) red[32] = s;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+// number of eigenvalues of the symmetric tridiagonal (d, e) strictly below x
+__device__ int sturm_count(const double* d, const double* e2, int N, double x) {
+  int c = 0;
+  double q = d[0] - x;
+  if (q < 0.0) ++c;
+  for (int i = 1; i < N; ++i) {
+    if (q == 0.0) q = 1e-300;
+    q = (d[i] - x) - e2[i - 1] / q;
+    if (q < 0.0) ++c;
+  }
+  return c;
+}
+
+// One CTA.  C: N x N symmetric (destroyed).  v, p: N doubles scratch (global).
+// out: eig[N] ascending (optional), rank[0] = r for tt_eps.
+__global__ void __launch_bounds__(ET)
+k_eig_rank(double* __restrict__ C, int N, double* __restrict__ vg, double* __restrict__ pg, double tt_eps,
+           double* __restrict__ eig, int* __restrict__ rank_out) {
+  extern __shared__ double sm[];
+  double* d = sm;           // N
+  double* e = d + N;        // N
+  double* e2 = e + N;       // N
+  double* lam = e2 + N;     // N
+  double* red = lam + N;    // 33
+  const int tid = threadIdx.x, T = blockDim.x;
+  // ---- Householder tridiagonalisation, H = I - 2 v v^T with ||v|| = 1
+  for (int k = 0; k + 2 < N; ++k) {
+    const int L = N - k - 1;        // trailing size
+    double* A = C + (int64_t)(k + 1) * N + (k + 1);  // A'[i][j] = A[i * N + j]
+    // x = C[k+1 .. N-1][k]
+    double xs = 0.0;
+    for (int i = tid; i < L; i += T) {
+      const double xi = C[(int64_t)(k + 1 + i) * N + k];
+      vg[i] = xi;
+      xs += xi * xi;
+    }
+    const double nx2 = block_sum(xs, red);
+    const double x0 = vg[0];
+    const double nx = sqrt(nx2);
+    const double alpha = (x0 > 0.0) ? -nx : nx;
+    // v = x - alpha e1, ||v||^2 = nx2 - 2 alpha x0 + alpha^2
+    const double nv2 = nx2 - 2.0 * alpha * x0 + alpha * alpha;
+    if (tid == 0) {
+      d[k] = C[(int64_t)k * N + k];
+      e[k] = (nx2 > 0.0) ? alpha : 0.0;
+    }
+    if (nv2 <= 0.0 || nx2 == 0.0) {  // already reduced
+      __syncthreads();
+      if (tid == 0) e[k] = vg[0];
+      __syncthreads();
+      continue;
+    }
+    const double inv = 1.0 / sqrt(nv2);
+    __syncthreads();
+    for (int i = tid; i < L; i += T) vg[i] = (i == 0 ? vg[0] - alpha : vg[i]) * inv;
+    __syncthreads();
+    // p = A' v (warp per row, lanes over columns)
+    const int w = tid >> 5, ln = tid & 31, nw = T >> 5;
+    for (int i = w; i < L; i += nw) {
+      double s = 0.0;
+      for (int j = ln; j < L; j += 32) s += A[(int64_t)i * N + j] * vg[j];
+      s = warp_sum(s);
+      if (ln == 0) pg[i] = s;
+    }
+    __syncthreads();
+    double kp = 0.0;
+    for (int i = tid; i < L; i += T) kp += vg[i] * pg[i];
+    const double K = block_sum(kp, red);
+    for (int i = tid; i < L; i += T) pg[i] = pg[i] - K * vg[i];  // w = p - K v
+    __syncthreads();
+    // A' -= 2 (v w^T + w v^T)
+    for (int q = tid; q < L * L; q += T) {  // L <= 511: 32-bit index math
+      const int i = q / L, j = q - i * L;
+      A[(int64_t)i * N + j] -= 2.0 * (vg[i] * pg[j] + pg[i] * vg[j]);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (N >= 2) {
+      d[N - 2] = C[(int64_t)(N - 2) * N + (N - 2)];
+      e[N - 2] = C[(int64_t)(N - 1) * N + (N - 2)];
+    }
+    d[N - 1] = C[(int64_t)(N - 1) * N + (N - 1)];
+  }
+  __syncthreads();
+  for (int i = tid; i < N - 1; i += T) e2[i] = e[i] * e[i];
+  __syncthreads();
+  // ---- Gershgorin bounds, then bisection for eigenvalue index i (ascending)
+  double gl = 1e300, gu = -1e300;
+  if (tid == 0) {
+    for (int i = 0; i < N; ++i) {
+      const double rad = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < N ? fabs(e[i]) : 0.0);
+      gl = fmin(gl, d[i] - rad);
+      gu = fmax(gu, d[i] + rad);
+    }
+    red[0] = gl;
+    red[1] = gu;
+  }
+  __syncthreads();
+  gl = red[0];
+  gu = red[1];
+  const double span = fmax(gu - gl, 1e-300);
+  for (int i = tid; i < N; i += T) {
+    double lo = gl - 1e-12 * span, hi = gu + 1e-12 * span;
+    for (int it = 0; it < 200 && hi - lo > 1e-15 * fmax(fabs(lo), fabs(hi)) + 1e-300; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      if (sturm_count(d, e2, N, mid) <= i) lo = mid;
+      else hi = mid;
+    }
+    lam[i] = fmax(0.5 * (lo + hi), 0.0);  // PSD: clamp round-off negatives
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // tail after k (descending order) = sum of the N - k smallest, accumulated from the smallest
+    double tot = 0.0;
+    for (int i = 0; i < N; ++i) tot += lam[i];
+    int r = N;
+    if (tot <= 0.0) {
+      r = 1;
+    } else {
+      double asc = 0.0;  // sum of the j smallest
+      // k = N - j: condition sqrt(asc_j / tot) <= eps; smallest k <=> largest j
+      int best = 0;
+      for (int j = 1; j < N; ++j) {
+        asc += lam[j - 1];
+        if (sqrt(asc / tot) <= tt_eps) best = j;
+        else break;
+      }
+      r = N - best;
+    }
+    rank_out[0] = r;
+  }
+  if (eig)
+    for (int i = tid; i < N; i += T) eig[i] = lam[i];
+}
+
+}  // namespace
+
+size_t rank_rule_bytes(int64_t N, int64_t T, int num_sms) {
+  const int ntile = (int)((N + GT - 1) / GT);
+  const int nut = ntile * (ntile + 1) / 2;
+  int64_t nsplit = (2 * num_sms + nut - 1) / nut;
+  const int64_t ch = (T + nsplit - 1) / nsplit;
+  nsplit = (T + ch - 1) / ch;
+  return sizeof(double) * ((size_t)nsplit * nut * GT * GT + (size_t)N * N + 4 * (size_t)N + 64) + 64;
+}
+
+cudaError_t launch_rank_rule(const float* X, int64_t m, int64_t n, int64_t ldx, double tt_eps, char* ws,
+                             int num_sms, int* d_rank, double* d_eig, cudaStream_t st) {
+  const bool rows = m <= n;  // C = X X^T (N = m) or X^T X (N = n)
+  const int N = (int)(rows ? m : n);
+  const int64_t T = rows ? n : m;
+  const int64_t sa = rows ? ldx : 1, stt = rows ? 1 : ldx;
+  const int ntile = (N + GT - 1) / GT;
+  const int nut = ntile * (ntile + 1) / 2;
+  int64_t nsplit = (2 * num_sms + nut - 1) / nut;
+  int64_t chunk = (T + nsplit - 1) / nsplit;
+  chunk = (chunk + GK - 1) / GK * GK;
+  nsplit = (T + chunk - 1) / chunk;
+  double* part = reinterpret_cast<double*>(ws);
+  double* C = part + (size_t)nsplit * nut * GT * GT;
+  double* vg = C + (size_t)N * N;
+  double* pg = vg + N;
+  k_gram<<<dim3((unsigned)nut, (unsigned)nsplit), 256, 0, st>>>(X, sa, stt, N, T, ntile, chunk, part);
+  cudaError_t e = cudaGetLastError();
+  if (e) return e;
+  k_gram_sum<<<256, 256, 0, st>>>(part, (int)nsplit, ntile, N, C);
+  if ((e = cudaGetLastError())) return e;
+  const size_t sm = sizeof(double) * (4 * (size_t)N + 40);
+  e = cudaFuncSetAttribute(k_eig_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e) return e;
+  k_eig_rank<<<1, ET, sm, st>>>(C, N, vg, pg, tt_eps, d_eig, d_rank);
+  return cudaGetLastError();
+}
+
+}  // namespace ntt
