@@ -658,7 +658,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
           if (R > 4) {
             float4 bq = *reinterpret_cast<const float4*>(src + 4);
             hq2[t][2 % (R / 2)] = f2(bq.x, bq.y);
-            hq2[t][3 % (R / 2)] = f2(bq.z, bq.w);
+            if (R > 6) hq2[t][3 % (R / 2)] = f2(bq.z, bq.w);
           }
           hq[t] = src[rb];
         }
@@ -1070,9 +1070,17 @@ size_t fixed_bytes_c(int MP, int NW) {
   return (size_t)NW * 8 * 32 * 4 + 256 + HNC_FLOATS * 4 + (size_t)MP * 8 * 4 + 2 * 16 * 8 + 1024;
 }
 
+bool c_one_cta() {  // experiment: NTT_C_1CTA=1 runs the 4-warp variant at 1 CTA / SM with a deeper ring
+  static const bool on = [] {
+    const char* e = getenv("NTT_C_1CTA");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 int stages_c(int MP, int NW) {
   const size_t SB = (size_t)MP * 128 + 1024;
-  const size_t budget = NW == 4 ? (size_t)SMEM_C : (size_t)SMEM_BUDGET;  // 2 CTAs / SM or 1
+  const size_t budget = (NW == 4 && !c_one_cta()) ? (size_t)SMEM_C : (size_t)SMEM_BUDGET;  // 2 CTAs / SM or 1
   int ns = (int)((budget - fixed_bytes_c(MP, NW)) / SB);
   return ns > 12 ? 12 : ns;
 }
@@ -1467,7 +1475,7 @@ cudaError_t make_map(CUtensorMap* map, const float* base, uint64_t cols, uint64_
 }
 
 int ux_for(int64_t m) { return m <= 8 ? 1 : m <= 16 ? 2 : m <= 32 ? 4 : 5; }
-int rcls_for(int r) { return r <= 2 ? 2 : r <= 4 ? 4 : 8; }
+int rcls_for(int r) { return r <= 2 ? 2 : r <= 4 ? 4 : r <= 6 ? 6 : 8; }
 
 size_t fixed_bytes(int ux, int nwt, bool hd) {
   return (size_t)ux * 8 * 8 * 4 + 256 + (hd ? (size_t)nwt * HN_FLOATS * 4 : 0) + 2 * 24 * 8 + 160 + 1024;
@@ -1637,7 +1645,7 @@ int fused_grid(int64_t m, int64_t n, int r, int num_sms) {
     int64_t need = (ntiles + NWW - 1) / NWW;
     return (int)(need < num_sms ? (need < 1 ? 1 : need) : num_sms);
   }
-  const int cps = c_nw(m <= 128 ? 128 : 256) == 8 ? 1 : 2;  // variant C: CTAs per SM
+  const int cps = (c_nw(m <= 128 ? 128 : 256) == 8 || c_one_cta()) ? 1 : 2;  // variant C: CTAs per SM
   return (int)(ntiles < cps * num_sms ? ntiles : cps * num_sms);
 }
 
@@ -1706,6 +1714,12 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
     if (ux == 2) LF(2, 2);
     if (ux == 4) LF(2, 4);
     LF(2, 5);
+  }
+  if (rc == 6) {  // r = 5, 6 (config 4): less padded work than the R = 8 class
+    if (ux == 1) LF(6, 1);
+    if (ux == 2) LF(6, 2);
+    if (ux == 4) LF(6, 4);
+    LF(6, 5);
   }
   if (rc == 4) {
     if (ux == 1) LF(4, 1);
