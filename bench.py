@@ -308,7 +308,7 @@ def run_ours(args):
     clocks = clk.stop()
     launches = h.launch_count - l0
     ms = e0.elapsed_time(e1) / args.steps
-    step_prof = {(c, l): h.ntt_profile_get(c, l) for c in range(6) for l in range(0, d + 1)}
+    step_prof = {(c, l): h.ntt_profile_get(c, l) for c in range(8) for l in range(0, d + 1)}
     h.ntt_profile_enable(False)
     if dist:
         t = torch.tensor([ms], device="cuda")
@@ -355,7 +355,7 @@ def run_ours(args):
     per_step = {}
     for l in range(1, d + 1):
         ent = {}
-        for c, nm in enumerate(["xstream", "xht", "wupdate", "ttstream", "other", "hpass2"]):
+        for c, nm in enumerate(["xstream", "xht", "wupdate", "ttstream", "other", "hpass2", "tc_xht", "tc_wtx"]):
             k, t, by = step_prof[(c, l)]
             if k:
                 ent[nm] = {"launches_per_step": k // args.steps, "ms_per_step": t / args.steps,

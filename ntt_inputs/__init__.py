@@ -140,4 +140,7 @@ def workloads() -> dict:
         "config5": Workload("config5", "nmf", [131072, 65536], [32], 100, noise="uniform", noise_amp=0.08,
                             note="X = W0 H0 + 0.08 u (1% of mean 8); 1-GPU slice 32768 rows",
                             extra={"slice_rows": 32768}),
+        # SURVEY s.8(f) f3: the paper's strong-scaling tensor shape, synthetic
+        "paper256": Workload("paper256", "ntt", [256] * 4, [10, 10, 10], 100, noise="uniform", noise_amp=0.625,
+                             note="256^4 (16 GiB) TT ranks 10 + 1% uniform noise (0.01 * mean 62.5 * u)"),
     }

@@ -361,40 +361,57 @@ k_tc_hupdate(float* __restrict__ H, int64_t n, int r, const double* __restrict__
       const int k = t / R, l = t % R;
       Gs[t] = (k < r && l < r) ? (float)Gred[k * r + l] : 0.0f;
     }
-  __syncthreads();
-  const int64_t j = (int64_t)blockIdx.x * UPD_ROWS + threadIdx.x;
-  if (j < n) {
-    float h[R];
+  // grid-stride over 128-column blocks; Q partial of this CTA accumulated in fp64 in
+  // block order (fixed, so deterministic), one entry per thread (rr <= 1024)
+  double qacc[(R * R + UPD_ROWS - 1) / UPD_ROWS];
 #pragma unroll
-    for (int k = 0; k < R; ++k) h[k] = (k < r) ? H[(int64_t)k * n + j] : 0.0f;
-    const int64_t nr = n * r;
+  for (int u = 0; u < (R * R + UPD_ROWS - 1) / UPD_ROWS; ++u) qacc[u] = 0.0;
+  const int64_t nblk = (n + UPD_ROWS - 1) / UPD_ROWS;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    __syncthreads();
+    const int64_t j = blk * UPD_ROWS + threadIdx.x;
+    if (j < n) {
+      float h[R];
 #pragma unroll
-    for (int k = 0; k < R; ++k) {
-      float hn = h[k];
-      if (update && k < r) {
-        double sd = 0.0;
-        for (int b = 0; b < nS; ++b) sd += Spart[(int64_t)b * nr + j * r + k];
-        float e = 0.0f;
+      for (int k = 0; k < R; ++k) h[k] = (k < r) ? H[(int64_t)k * n + j] : 0.0f;
+      const int64_t nr = n * r;
 #pragma unroll
-        for (int l = 0; l < R; ++l) e = fmaf(Gs[k * R + l], h[l], e);
-        hn = mu_quot(h[k], (float)sd, e, eps);
+      for (int k = 0; k < R; ++k) {
+        float hn = h[k];
+        if (update && k < r) {
+          double sd = 0.0;
+          for (int b = 0; b < nS; ++b) sd += Spart[(int64_t)b * nr + j * r + k];
+          float e = 0.0f;
+#pragma unroll
+          for (int l = 0; l < R; ++l) e = fmaf(Gs[k * R + l], h[l], e);
+          hn = mu_quot(h[k], (float)sd, e, eps);
+        }
+        if (k >= r) hn = 0.0f;
+        Hn[k][threadIdx.x] = hn;
+        if (update && k < r) H[(int64_t)k * n + j] = hn;
+        Hcat[(int64_t)k * ldh + j] = hn;
+        Hcat[(int64_t)(R + k) * ldh + j] = tf32_lo(hn);
       }
-      if (k >= r) hn = 0.0f;
-      Hn[k][threadIdx.x] = hn;
-      if (update && k < r) H[(int64_t)k * n + j] = hn;
-      Hcat[(int64_t)k * ldh + j] = hn;
-      Hcat[(int64_t)(R + k) * ldh + j] = tf32_lo(hn);
-    }
-  } else {
+    } else {
 #pragma unroll
-    for (int k = 0; k < R; ++k) Hn[k][threadIdx.x] = 0.0f;
+      for (int k = 0; k < R; ++k) Hn[k][threadIdx.x] = 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < (R * R + UPD_ROWS - 1) / UPD_ROWS; ++u) {
+      const int t = threadIdx.x + u * UPD_ROWS;
+      if (t < rr) {
+        const int k = t / r, l = t % r;
+        double sq = 0.0;
+        for (int c = 0; c < UPD_ROWS; ++c) sq += (double)Hn[k][c] * (double)Hn[l][c];
+        qacc[u] += sq;
+      }
+    }
   }
-  __syncthreads();
-  for (int t = threadIdx.x; t < rr; t += blockDim.x) {
-    const int k = t / r, l = t % r;
-    double s = 0.0;
-    for (int c = 0; c < UPD_ROWS; ++c) s += (double)Hn[k][c] * (double)Hn[l][c];
-    Qpart[(int64_t)blockIdx.x * rr + t] = s;
+#pragma unroll
+  for (int u = 0; u < (R * R + UPD_ROWS - 1) / UPD_ROWS; ++u) {
+    const int t = threadIdx.x + u * UPD_ROWS;
+    if (t < rr) Qpart[(int64_t)blockIdx.x * rr + t] = qacc[u];
   }
 }
 
@@ -503,7 +520,7 @@ TcPlan plan_tc(int64_t m, int64_t n, int r, int num_sms) {
   pick_split((m + TC_BM - 1) / TC_BM, (n + TC_BK - 1) / TC_BK, num_sms, &p.splitW, &p.kchW);
   pick_split((n + TC_BM - 1) / TC_BM, (m + TC_BK - 1) / TC_BK, num_sms, &p.splitH, &p.kchH);
   p.nG = (int)((m + UPD_ROWS - 1) / UPD_ROWS);
-  p.nQ = (int)((n + UPD_ROWS - 1) / UPD_ROWS);
+  p.nQ = (int)std::min<int64_t>((n + UPD_ROWS - 1) / UPD_ROWS, 4 * num_sms);  // H-update CTAs (grid-stride)
   size_t o = 0;
   auto take = [&](size_t b) {
     size_t at = o;
