@@ -121,13 +121,12 @@ k_skinny_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       prefetch_tmap(&tmB);
       const uint64_t pol = evict_first ? policy_evict_first() : policy_evict_normal();
       const uint64_t polB = policy_evict_normal();
-      int64_t j = 0;
+      int s = 0;
+      uint32_t ph = 0;  // ring position, incremental (no 64-bit division per stage)
       for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
         const int64_t mb = u / nsplit, sp = u % nsplit;
         const int64_t k0 = sp * kchunk, k1 = ((k0 + kchunk < ktiles) ? k0 + kchunk : ktiles);
-        for (int64_t kt = k0; kt < k1; ++kt, ++j) {
-          const int s = (int)(j % ns);
-          const uint32_t ph = (uint32_t)((j / ns) & 1);
+        for (int64_t kt = k0; kt < k1; ++kt, s = (s + 1 == ns) ? 0 : s + 1, ph ^= (s == 0) ? 1u : 0u) {
           mbar_wait(&empty[s], ph ^ 1u);
           mbar_expect_tx(&full[s], C::SB);
           unsigned char* st = smem + (size_t)s * C::SB;
@@ -147,11 +146,14 @@ k_skinny_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     if (lane == 0) {
       constexpr uint32_t id1 = idesc_tf32(TC_BM, C::N1, false, false);
       constexpr uint32_t id2 = idesc_tf32(TC_BM, R, false, false);
-      int64_t j = 0, g = 0;
+      int64_t g = 0;
+      int s = 0, t = 0;
+      uint32_t ph = 0, pht = 0;
       for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
         const int64_t sp = u % nsplit;
         const int64_t k0 = sp * kchunk, k1 = ((k0 + kchunk < ktiles) ? k0 + kchunk : ktiles);
-        for (int64_t kt = k0; kt < k1; ++kt, ++j) {
+        for (int64_t kt = k0; kt < k1; ++kt, s = (s + 1 == ns) ? 0 : s + 1, ph ^= (s == 0) ? 1u : 0u,
+                     t = (t + 1) & (TC_T - 1), pht ^= (t == 0) ? 1u : 0u) {
           const int64_t i = kt - k0;  // tile index within the unit
           const bool gfirst = (i % flush) == 0;
           const bool glast = ((i + 1) % flush) == 0 || kt + 1 == k1;
@@ -160,10 +162,6 @@ k_skinny_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             mbar_wait(&acc_empty[a], (uint32_t)(((g >> 1) & 1) ^ 1));
             tc_fence_after();
           }
-          const int s = (int)(j % ns);
-          const uint32_t ph = (uint32_t)((j / ns) & 1);
-          const int t = (int)(j % TC_T);
-          const uint32_t pht = (uint32_t)((j / TC_T) & 1);
           mbar_wait(&full[s], ph);
           mbar_wait(&lo_full[t], pht);
           tc_fence_after();
@@ -192,15 +190,13 @@ k_skinny_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     // ======================= converters: A_lo -> TMEM =======================
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const uint32_t lane_off = (uint32_t)(32 * q) << 16;
-    int64_t j = 0;
+    int s = 0, t = 0;
+    uint32_t ph = 0, pht = 0;
     for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
       const int64_t sp = u % nsplit;
       const int64_t k0 = sp * kchunk, k1 = ((k0 + kchunk < ktiles) ? k0 + kchunk : ktiles);
-      for (int64_t kt = k0; kt < k1; ++kt, ++j) {
-        const int s = (int)(j % ns);
-        const uint32_t ph = (uint32_t)((j / ns) & 1);
-        const int t = (int)(j % TC_T);
-        const uint32_t pht = (uint32_t)((j / TC_T) & 1);
+      for (int64_t kt = k0; kt < k1; ++kt, s = (s + 1 == ns) ? 0 : s + 1, ph ^= (s == 0) ? 1u : 0u,
+                   t = (t + 1) & (TC_T - 1), pht ^= (t == 0) ? 1u : 0u) {
         mbar_wait(&full[s], ph);
         mbar_wait(&lo_empty[t], pht ^ 1u);
         tc_fence_after();
