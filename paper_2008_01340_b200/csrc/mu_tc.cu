@@ -322,11 +322,13 @@ k_tc_wupdate(float* __restrict__ W, int64_t m, int r, const double* __restrict__
       Wn[threadIdx.x][k] = wn;
     }
     for (int k = 0; k < r; ++k) W[i * r + k] = Wn[threadIdx.x][k];
+    if (WcatT) {
 #pragma unroll
-    for (int k = 0; k < R; ++k) {
-      const float v = Wn[threadIdx.x][k];
-      WcatT[(int64_t)k * ldw + i] = v;
-      WcatT[(int64_t)(R + k) * ldw + i] = tf32_lo(v);
+      for (int k = 0; k < R; ++k) {
+        const float v = Wn[threadIdx.x][k];
+        WcatT[(int64_t)k * ldw + i] = v;
+        WcatT[(int64_t)(R + k) * ldw + i] = tf32_lo(v);
+      }
     }
   } else {
     for (int k = 0; k < R; ++k) Wn[threadIdx.x][k] = 0.0f;
@@ -385,8 +387,10 @@ k_tc_hupdate(float* __restrict__ H, int64_t n, int r, const double* __restrict__
         if (k >= r) hn = 0.0f;
         Hn[k][threadIdx.x] = hn;
         if (update && k < r) H[(int64_t)k * n + j] = hn;
-        Hcat[(int64_t)k * ldh + j] = hn;
-        Hcat[(int64_t)(R + k) * ldh + j] = tf32_lo(hn);
+        if (Hcat) {
+          Hcat[(int64_t)k * ldh + j] = hn;
+          Hcat[(int64_t)(R + k) * ldh + j] = tf32_lo(hn);
+        }
       }
     } else {
 #pragma unroll
@@ -533,6 +537,22 @@ TcPlan plan_tc(int64_t m, int64_t n, int r, int num_sms) {
   p.off_Qred = take(sizeof(double) * (size_t)r * r);
   p.off_red = take(sizeof(double) * (size_t)(m * r + r * r));  // distributed: [P | Q] all-reduce payload
   p.off_Sred = take(sizeof(double) * (size_t)n * r);          // distributed: W^T X block payload
+  // fp16x2 variant (mu_tc16.cu): default unless NTT_TC16=0
+  {
+    const char* e = getenv("NTT_TC16");
+    p.f16 = !(e && e[0] == '0');
+  }
+  p.ldh16 = (n + 7) & ~int64_t(7);
+  p.ldw16 = (m + 7) & ~int64_t(7);
+  pick_split((m + TC_BM - 1) / TC_BM, (n + 63) / 64, num_sms, &p.splitW16, &p.kchW16);
+  pick_split((n + TC_BM - 1) / TC_BM, (m + 63) / 64, num_sms, &p.splitH16, &p.kchH16);
+  if (p.f16) {  // the split partial buffers must hold either variant's split count
+    p.off_P = take(sizeof(double) * (size_t)std::max(p.splitW, p.splitW16) * m * r);
+    p.off_S = take(sizeof(double) * (size_t)std::max(p.splitH, p.splitH16) * n * r);
+  }
+  p.off_h16 = take(2 * sizeof(uint16_t) * (size_t)(2 * p.R) * p.ldh16);
+  p.off_w16 = take(2 * sizeof(uint16_t) * (size_t)(2 * p.R) * p.ldw16);
+  p.off_scales = take(256);
   p.bytes = o;
   return p;
 }
@@ -574,13 +594,13 @@ cudaError_t tc_pass_w(const TcPlan& p, const TcMaps& mp, char* ws, int evict_fir
 }
 
 cudaError_t tc_wupdate(const TcPlan& p, float* W, float eps, char* ws, cudaStream_t st) {
-  return tc_wupdate_ex(p, W, eps, ws, reinterpret_cast<const double*>(ws + p.off_P), p.splitW,
+  return tc_wupdate_ex(p, W, eps, ws, reinterpret_cast<const double*>(ws + p.off_P), p.f16 ? p.splitW16 : p.splitW,
                        reinterpret_cast<const double*>(ws + p.off_Qred), st);
 }
 
 cudaError_t tc_wupdate_ex(const TcPlan& p, float* W, float eps, char* ws, const double* P, int nP, const double* Qr,
                           cudaStream_t st) {
-  float* Wcat = reinterpret_cast<float*>(ws + p.off_wcat);
+  float* Wcat = p.f16 ? nullptr : reinterpret_cast<float*>(ws + p.off_wcat);
   double* G = reinterpret_cast<double*>(ws + p.off_G);
   const unsigned g = (unsigned)p.nG;
   if (p.R == 16)
@@ -602,12 +622,12 @@ cudaError_t tc_pass_h(const TcPlan& p, const TcMaps& mp, char* ws, int evict_fir
 }
 
 cudaError_t tc_hupdate(const TcPlan& p, float* H, float eps, char* ws, cudaStream_t st) {
-  return tc_hupdate_ex(p, H, eps, ws, reinterpret_cast<const double*>(ws + p.off_S), p.splitH, st);
+  return tc_hupdate_ex(p, H, eps, ws, reinterpret_cast<const double*>(ws + p.off_S), p.f16 ? p.splitH16 : p.splitH, st);
 }
 
 cudaError_t tc_hupdate_ex(const TcPlan& p, float* H, float eps, char* ws, const double* S, int nS, cudaStream_t st) {
   const double* Gr = reinterpret_cast<const double*>(ws + p.off_Gred);
-  float* Hcat = reinterpret_cast<float*>(ws + p.off_hcat);
+  float* Hcat = p.f16 ? nullptr : reinterpret_cast<float*>(ws + p.off_hcat);
   double* Q = reinterpret_cast<double*>(ws + p.off_Q);
   const unsigned g = (unsigned)p.nQ;
   if (p.R == 16)
@@ -622,7 +642,7 @@ cudaError_t tc_reduce_PQ(const TcPlan& p, char* ws, cudaStream_t st) {
   double* red = reinterpret_cast<double*>(ws + p.off_red);
   const int64_t mr = p.m * p.r;
   k_tc_sum<<<(unsigned)std::min<int64_t>((mr + 255) / 256, 1184), 256, 0, st>>>(
-      reinterpret_cast<const double*>(ws + p.off_P), p.splitW, (int)mr, red);
+      reinterpret_cast<const double*>(ws + p.off_P), p.f16 ? p.splitW16 : p.splitW, (int)mr, red);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
   return cudaMemcpyAsync(red + mr, ws + p.off_Qred, sizeof(double) * p.r * p.r, cudaMemcpyDeviceToDevice, st);
@@ -632,7 +652,8 @@ cudaError_t tc_reduce_PQ(const TcPlan& p, char* ws, cudaStream_t st) {
 cudaError_t tc_reduce_S(const TcPlan& p, char* ws, cudaStream_t st) {
   const int64_t nr = p.n * p.r;
   k_tc_sum<<<(unsigned)std::min<int64_t>((nr + 255) / 256, 1184), 256, 0, st>>>(
-      reinterpret_cast<const double*>(ws + p.off_S), p.splitH, (int)nr, reinterpret_cast<double*>(ws + p.off_Sred));
+      reinterpret_cast<const double*>(ws + p.off_S), p.f16 ? p.splitH16 : p.splitH, (int)nr,
+      reinterpret_cast<double*>(ws + p.off_Sred));
   return cudaGetLastError();
 }
 

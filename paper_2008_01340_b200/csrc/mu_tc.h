@@ -17,11 +17,18 @@ struct TcPlan {
   int nG = 0, nQ = 0;           // Gram partial counts (W update CTAs, H update CTAs)
   size_t off_hcat = 0, off_wcat = 0, off_P = 0, off_S = 0, off_G = 0, off_Q = 0, off_Gred = 0, off_Qred = 0;
   size_t off_red = 0, off_Sred = 0;  // distributed all-reduce payloads (fp64)
+  // fp16x2 variant (mu_tc16.cu)
+  bool f16 = false;
+  int64_t ldh16 = 0, ldw16 = 0;
+  int splitW16 = 1, splitH16 = 1;
+  int64_t kchW16 = 0, kchH16 = 0;
+  size_t off_h16 = 0, off_w16 = 0, off_scales = 0;
   size_t bytes = 0;
 };
 
 struct TcMaps {
   CUtensorMap xw, xh, hcat, wcat;
+  CUtensorMap xw16, xh16, hcat16, wcat16;
 };
 
 // Shapes the TC path takes: r <= 32, m, n >= 256, X 16-byte aligned with ldx % 4 == 0.
@@ -49,5 +56,13 @@ cudaError_t tc_hupdate_ex(const TcPlan& p, float* H, float eps, char* ws, const 
 // distributed payloads: ws+off_red = [P (m r) | Q (r r)], ws+off_Sred = S (n r); G (local) at ws+off_Gred
 cudaError_t tc_reduce_PQ(const TcPlan& p, char* ws, cudaStream_t st);
 cudaError_t tc_reduce_S(const TcPlan& p, char* ws, cudaStream_t st);
+
+// fp16x2 variant (mu_tc16.cu): scales, fp16 operand parts and the two passes
+cudaError_t tc16_prepare(const TcPlan& p, const float* X, int64_t ldx, float* H, char* ws, TcMaps* maps,
+                         cudaStream_t st);
+cudaError_t tc16_pack_h(const TcPlan& p, const float* H, char* ws, cudaStream_t st);
+cudaError_t tc16_pack_w(const TcPlan& p, const float* W, char* ws, cudaStream_t st);
+cudaError_t tc16_pass_w(const TcPlan& p, const TcMaps& mp, char* ws, int evict_first, cudaStream_t st);
+cudaError_t tc16_pass_h(const TcPlan& p, const TcMaps& mp, char* ws, int evict_first, cudaStream_t st);
 
 }  // namespace ntt

@@ -404,9 +404,14 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
     double* sred = reinterpret_cast<double*>(tws + tp.off_Sred);
     TcMaps maps;
     LAUNCH(h, tc_prepare(tp, X, ldx, H, tws, &maps, st));
+    if (tp.f16) {
+      LAUNCH(h, tc16_prepare(tp, X, ldx, H, tws, &maps, st));
+      LAUNCH(h, tc16_pack_h(tp, H, tws, st));
+    }
     for (int it = 0; it < iters; ++it) {
       LAUNCH(h, tc_sum_Q(tp, tws, st));
-      PLAUNCH(h, 6, 4.0 * (double)(m + 2 * tp.R) * (double)n, tc_pass_w(tp, maps, tws, ef, st));
+      PLAUNCH(h, 6, 4.0 * (double)(m + 2 * tp.R) * (double)n,
+              tp.f16 ? tc16_pass_w(tp, maps, tws, ef, st) : tc_pass_w(tp, maps, tws, ef, st));
       if (dist) {
         LAUNCH(h, tc_reduce_PQ(tp, tws, st));
         NC(h, g_nccl.AllReduce(red, red, (size_t)(m * r + r * r), ncclFloat64, ncclSum, h->comm_row, st));
@@ -417,7 +422,9 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
         PLAUNCH(h, 2, 8.0 * (double)tp.splitW * m * r + 8.0 * m * r + 4.0 * 2 * tp.R * m,
                 tc_wupdate(tp, W, eps, tws, st));
       }
-      PLAUNCH(h, 7, 4.0 * (double)(n + 2 * tp.R) * (double)m, tc_pass_h(tp, maps, tws, ef, st));
+      if (tp.f16) LAUNCH(h, tc16_pack_w(tp, W, tws, st));
+      PLAUNCH(h, 7, 4.0 * (double)(n + 2 * tp.R) * (double)m,
+              tp.f16 ? tc16_pass_h(tp, maps, tws, ef, st) : tc_pass_h(tp, maps, tws, ef, st));
       if (dist) {
         LAUNCH(h, tc_reduce_S(tp, tws, st));
         NC(h, g_nccl.AllReduce(sred, sred, (size_t)(n * r), ncclFloat64, ncclSum, h->comm_col, st));
@@ -426,6 +433,7 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
         PLAUNCH(h, 4, 8.0 * (double)tp.splitH * n * r + 4.0 * (3 * tp.R + r) * (double)n,
                 tc_hupdate(tp, H, eps, tws, st));
       }
+      if (tp.f16) LAUNCH(h, tc16_pack_h(tp, H, tws, st));
       if (dev_trace) LAUNCH(h, launch_objective(X, ldx, m, n, W, H, r, dev_trace + (int64_t)it * nobj, st));
     }
     return NTT_OK;
