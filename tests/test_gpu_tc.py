@@ -105,3 +105,28 @@ def test_tc_leading_dimension(h, ora):
     for g, o in ((host(Wd), Wo), (host(Hd), Ho)):
         fro, mx = rel(g, o)
         assert fro <= TOL and mx <= TOL, (fro, mx)
+
+
+@pytest.mark.parametrize("variant", ["0", "1"])
+@pytest.mark.parametrize("m,n,r,wide", [(1000, 776, 32, False), (512, 1024, 16, True), (2048, 1536, 24, True)])
+def test_tc_variants_parity(h, ora, variant, m, n, r, wide):
+    """Both tensor-core variants (NTT_TC16=0: 3xTF32, =1: fp16x2 with power-of-two
+    scales) match the oracle; `wide` spreads X over ~9 decades (row and column
+    scales 1e-4 .. 1e4) to exercise the fp16 scaling and subnormal floor."""
+    import os
+    X, W0, H0 = inputs(m, n, r, 17 + m)
+    if wide:
+        rng = np.random.default_rng(5)
+        X = (X * 10.0 ** rng.uniform(-2, 2, (m, 1)) * 10.0 ** rng.uniform(-2, 2, (1, n))).astype(np.float32)
+    os.environ["NTT_TC16"] = variant
+    try:
+        Xd, Wd, Hd = dev(X), dev(W0), dev(H0)
+        h.ntt_nmf_mu(Xd, m, n, n, r, 8, 1e-16, Wd, Hd)
+        Wg, Hg = host(Wd), host(Hd)
+    finally:
+        os.environ.pop("NTT_TC16", None)
+    Wo, Ho = ora.nmf_mu(X, W0.astype(np.float64), H0.astype(np.float64), 8, eps=1e-16)
+    for name, g, o in (("W", Wg, Wo), ("H", Hg, Ho)):
+        fro, mx = rel(g, o)
+        assert np.all(np.isfinite(g)) and np.all(g >= 0), name
+        assert fro <= TOL and mx <= TOL, f"{name} variant {variant}: rel fro {fro:.3e}, rel max {mx:.3e}"
