@@ -23,7 +23,8 @@ def handles():
 
 
 @pytest.mark.parametrize("dims,ranks,iters", [([5, 4, 5, 6], [4, 3, 2], 10), ([16, 16, 16, 16], [8, 8, 8], 10),
-                                              ([6] * 6, [5] * 5, 10), ([64, 32, 64], [8, 8], 5)])
+                                              ([6] * 6, [5] * 5, 10), ([64, 32, 64], [8, 8], 5),
+                                              ([20, 30, 40, 30], [10, 12, 9], 5)])
 def test_dist_handle_decompose_matches(handles, ora, dims, ranks, iters):
     h1, hd = handles
     A = ora.tt_full_f32(dims, ranks, ni.make_cores(dims, ranks, 0), noise_amp=0.3, seed=0)

@@ -220,6 +220,9 @@ NTT_CASES = [
     ([6] * 7, [5] * 6, 10, 0.0),             # config-4-like, 6^7
     ([16, 16, 16, 16], [8, 8, 8], 10, 1.0),
     ([7, 3, 11], [3, 5], 10, 0.0),
+    # r > 8: step 2 (300 x 1200, r 12) takes the tensor-core path, steps 1 and 3 the generic one
+    ([20, 30, 40, 30], [10, 12, 9], 10, 0.2),
+    ([32, 16, 64, 8], [16, 24, 8], 6, 0.0),
 ]
 
 
