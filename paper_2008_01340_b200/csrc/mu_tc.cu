@@ -293,7 +293,7 @@ template <int R>
 __global__ void __launch_bounds__(UPD_ROWS)
 k_tc_wupdate(float* __restrict__ W, int64_t m, int r, const double* __restrict__ Ppart, int nP,
              const double* __restrict__ Qred, float eps, float* __restrict__ WcatT, int64_t ldw,
-             double* __restrict__ Gpart) {
+             double* __restrict__ Gpart, unsigned* __restrict__ maxw) {
   __shared__ double Qs[R * R];
   __shared__ float Wn[UPD_ROWS][R + 1];
   const int rr = r * r;
@@ -322,6 +322,11 @@ k_tc_wupdate(float* __restrict__ W, int64_t m, int r, const double* __restrict__
       Wn[threadIdx.x][k] = wn;
     }
     for (int k = 0; k < r; ++k) W[i * r + k] = Wn[threadIdx.x][k];
+    if (maxw) {  // max |W| for the fp16x2 scale (fp16 variant); order-independent
+      float mx = 0.0f;
+      for (int k = 0; k < r; ++k) mx = fmaxf(mx, Wn[threadIdx.x][k]);
+      atomicMax(maxw, __float_as_uint(mx));
+    }
     if (WcatT) {
 #pragma unroll
       for (int k = 0; k < R; ++k) {
@@ -350,7 +355,8 @@ template <int R>
 __global__ void __launch_bounds__(UPD_ROWS)
 k_tc_hupdate(float* __restrict__ H, int64_t n, int r, const double* __restrict__ Spart, int nS,
              const double* __restrict__ Gred, float eps, bool update, float* __restrict__ Hcat, int64_t ldh,
-             double* __restrict__ Qpart) {
+             double* __restrict__ Qpart, unsigned* __restrict__ maxh) {
+  float hmax = 0.0f;
   __shared__ float Gs[R * R];
   __shared__ float Hn[R][UPD_ROWS + 1];
   const int rr = r * r;
@@ -385,6 +391,7 @@ k_tc_hupdate(float* __restrict__ H, int64_t n, int r, const double* __restrict__
           hn = mu_quot(h[k], (float)sd, e, eps);
         }
         if (k >= r) hn = 0.0f;
+        hmax = fmaxf(hmax, hn);
         Hn[k][threadIdx.x] = hn;
         if (update && k < r) H[(int64_t)k * n + j] = hn;
         if (Hcat) {
@@ -412,6 +419,10 @@ k_tc_hupdate(float* __restrict__ H, int64_t n, int r, const double* __restrict__
   for (int u = 0; u < (R * R + UPD_ROWS - 1) / UPD_ROWS; ++u) {
     const int t = threadIdx.x + u * UPD_ROWS;
     if (t < rr) Qpart[(int64_t)blockIdx.x * rr + t] = qacc[u];
+  }
+  if (maxh) {  // max |H| for the fp16x2 scale (fp16 variant)
+    for (int o = 16; o > 0; o >>= 1) hmax = fmaxf(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(maxh, __float_as_uint(hmax));
   }
 }
 
@@ -573,9 +584,11 @@ cudaError_t tc_prepare(const TcPlan& p, const float* X, int64_t ldx, float* H, c
   double* Qpart = reinterpret_cast<double*>(ws + p.off_Q);
   const unsigned g = (unsigned)p.nQ;
   if (p.R == 16)
-    k_tc_hupdate<16><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, nullptr, 0, nullptr, 0.f, false, Hcat, p.ldh, Qpart);
+    k_tc_hupdate<16><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, nullptr, 0, nullptr, 0.f, false, Hcat, p.ldh, Qpart,
+                                             nullptr);
   else
-    k_tc_hupdate<32><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, nullptr, 0, nullptr, 0.f, false, Hcat, p.ldh, Qpart);
+    k_tc_hupdate<32><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, nullptr, 0, nullptr, 0.f, false, Hcat, p.ldh, Qpart,
+                                             nullptr);
   return cudaGetLastError();
 }
 
@@ -593,20 +606,26 @@ cudaError_t tc_pass_w(const TcPlan& p, const TcMaps& mp, char* ws, int evict_fir
   return launch_skinny<32, 0>(mp.xw, mp.hcat, p.m, kt, p.splitW, p.kchW, p.grid, p.r, P, evict_first, st);
 }
 
-cudaError_t tc_wupdate(const TcPlan& p, float* W, float eps, char* ws, cudaStream_t st) {
+cudaError_t tc_wupdate(const TcPlan& p, float* W, float eps, char* ws, cudaStream_t st, int it) {
   return tc_wupdate_ex(p, W, eps, ws, reinterpret_cast<const double*>(ws + p.off_P), p.f16 ? p.splitW16 : p.splitW,
-                       reinterpret_cast<const double*>(ws + p.off_Qred), st);
+                       reinterpret_cast<const double*>(ws + p.off_Qred), st, it);
+}
+
+// fp16 variant max words (unsigned, after the 64-byte scale block): [0] X, [1 + (it & 1)] H, [3 + (it & 1)] W
+static unsigned* tc_maxw(const TcPlan& p, char* ws, int slot) {
+  return p.f16 ? reinterpret_cast<unsigned*>(ws + p.off_scales + 64) + slot : nullptr;
 }
 
 cudaError_t tc_wupdate_ex(const TcPlan& p, float* W, float eps, char* ws, const double* P, int nP, const double* Qr,
-                          cudaStream_t st) {
+                          cudaStream_t st, int it) {
   float* Wcat = p.f16 ? nullptr : reinterpret_cast<float*>(ws + p.off_wcat);
+  unsigned* mxw = tc_maxw(p, ws, 3 + (it & 1));
   double* G = reinterpret_cast<double*>(ws + p.off_G);
   const unsigned g = (unsigned)p.nG;
   if (p.R == 16)
-    k_tc_wupdate<16><<<g, UPD_ROWS, 0, st>>>(W, p.m, p.r, P, nP, Qr, eps, Wcat, p.ldw, G);
+    k_tc_wupdate<16><<<g, UPD_ROWS, 0, st>>>(W, p.m, p.r, P, nP, Qr, eps, Wcat, p.ldw, G, mxw);
   else
-    k_tc_wupdate<32><<<g, UPD_ROWS, 0, st>>>(W, p.m, p.r, P, nP, Qr, eps, Wcat, p.ldw, G);
+    k_tc_wupdate<32><<<g, UPD_ROWS, 0, st>>>(W, p.m, p.r, P, nP, Qr, eps, Wcat, p.ldw, G, mxw);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
   const int len = p.r * p.r;
@@ -621,19 +640,22 @@ cudaError_t tc_pass_h(const TcPlan& p, const TcMaps& mp, char* ws, int evict_fir
   return launch_skinny<32, 1>(mp.xh, mp.wcat, p.n, kt, p.splitH, p.kchH, p.grid, p.r, S, evict_first, st);
 }
 
-cudaError_t tc_hupdate(const TcPlan& p, float* H, float eps, char* ws, cudaStream_t st) {
-  return tc_hupdate_ex(p, H, eps, ws, reinterpret_cast<const double*>(ws + p.off_S), p.f16 ? p.splitH16 : p.splitH, st);
+cudaError_t tc_hupdate(const TcPlan& p, float* H, float eps, char* ws, cudaStream_t st, int it) {
+  return tc_hupdate_ex(p, H, eps, ws, reinterpret_cast<const double*>(ws + p.off_S), p.f16 ? p.splitH16 : p.splitH, st,
+                       it);
 }
 
-cudaError_t tc_hupdate_ex(const TcPlan& p, float* H, float eps, char* ws, const double* S, int nS, cudaStream_t st) {
+cudaError_t tc_hupdate_ex(const TcPlan& p, float* H, float eps, char* ws, const double* S, int nS, cudaStream_t st,
+                          int it) {
+  unsigned* mxh = tc_maxw(p, ws, 1 + (it & 1));
   const double* Gr = reinterpret_cast<const double*>(ws + p.off_Gred);
   float* Hcat = p.f16 ? nullptr : reinterpret_cast<float*>(ws + p.off_hcat);
   double* Q = reinterpret_cast<double*>(ws + p.off_Q);
   const unsigned g = (unsigned)p.nQ;
   if (p.R == 16)
-    k_tc_hupdate<16><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, S, nS, Gr, eps, true, Hcat, p.ldh, Q);
+    k_tc_hupdate<16><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, S, nS, Gr, eps, true, Hcat, p.ldh, Q, mxh);
   else
-    k_tc_hupdate<32><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, S, nS, Gr, eps, true, Hcat, p.ldh, Q);
+    k_tc_hupdate<32><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, S, nS, Gr, eps, true, Hcat, p.ldh, Q, mxh);
   return cudaGetLastError();
 }
 

@@ -43,16 +43,17 @@ cudaError_t tc_sum_Q(const TcPlan& p, char* ws, cudaStream_t st);
 // split-K partials of P = X H^T
 cudaError_t tc_pass_w(const TcPlan& p, const TcMaps& mp, char* ws, int evict_first, cudaStream_t st);
 // W <- W o P / (W Q + eps); Wcat; G = W^T W (reduced)
-cudaError_t tc_wupdate(const TcPlan& p, float* W, float eps, char* ws, cudaStream_t st);
+cudaError_t tc_wupdate(const TcPlan& p, float* W, float eps, char* ws, cudaStream_t st, int it = 0);
 // split-K partials of S = W^T X
 cudaError_t tc_pass_h(const TcPlan& p, const TcMaps& mp, char* ws, int evict_first, cudaStream_t st);
 // H <- H o S / (G H + eps); Hcat; Q partials of the new H
-cudaError_t tc_hupdate(const TcPlan& p, float* H, float eps, char* ws, cudaStream_t st);
+cudaError_t tc_hupdate(const TcPlan& p, float* H, float eps, char* ws, cudaStream_t st, int it = 0);
 
 // explicit-operand forms (distributed path: P / S already reduced, nP = nS = 1)
 cudaError_t tc_wupdate_ex(const TcPlan& p, float* W, float eps, char* ws, const double* P, int nP, const double* Q,
-                          cudaStream_t st);
-cudaError_t tc_hupdate_ex(const TcPlan& p, float* H, float eps, char* ws, const double* S, int nS, cudaStream_t st);
+                          cudaStream_t st, int it = 0);
+cudaError_t tc_hupdate_ex(const TcPlan& p, float* H, float eps, char* ws, const double* S, int nS, cudaStream_t st,
+                          int it = 0);
 // distributed payloads: ws+off_red = [P (m r) | Q (r r)], ws+off_Sred = S (n r); G (local) at ws+off_Gred
 cudaError_t tc_reduce_PQ(const TcPlan& p, char* ws, cudaStream_t st);
 cudaError_t tc_reduce_S(const TcPlan& p, char* ws, cudaStream_t st);
@@ -60,8 +61,10 @@ cudaError_t tc_reduce_S(const TcPlan& p, char* ws, cudaStream_t st);
 // fp16x2 variant (mu_tc16.cu): scales, fp16 operand parts and the two passes
 cudaError_t tc16_prepare(const TcPlan& p, const float* X, int64_t ldx, float* H, char* ws, TcMaps* maps,
                          cudaStream_t st);
-cudaError_t tc16_pack_h(const TcPlan& p, const float* H, char* ws, cudaStream_t st);
-cudaError_t tc16_pack_w(const TcPlan& p, const float* W, char* ws, cudaStream_t st);
+// it: iteration (-1 = the initial H of tc16_prepare); the max of the factor comes from
+// the update kernel of the same iteration (parity slot), the other slot is reset
+cudaError_t tc16_pack_h(const TcPlan& p, const float* H, char* ws, cudaStream_t st, int it);
+cudaError_t tc16_pack_w(const TcPlan& p, const float* W, char* ws, cudaStream_t st, int it);
 cudaError_t tc16_pass_w(const TcPlan& p, const TcMaps& mp, char* ws, int evict_first, cudaStream_t st);
 cudaError_t tc16_pass_h(const TcPlan& p, const TcMaps& mp, char* ws, int evict_first, cudaStream_t st);
 

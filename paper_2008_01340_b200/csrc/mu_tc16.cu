@@ -316,9 +316,12 @@ __device__ __forceinline__ float pow2_scale(unsigned maxbits) {
 // dst[k][j] = fp16(F[k][j] s), dst[R + k][j] = fp16(F[k][j] s - hi); scales[sidx] = s
 __global__ void k_pack16(const float* __restrict__ F, int r, int64_t len, bool transposed, int R,
                          const unsigned* __restrict__ maxbits, __half* __restrict__ dst, int64_t ldd,
-                         float* __restrict__ scales, int sidx) {
+                         float* __restrict__ scales, int sidx, unsigned* __restrict__ reset) {
   const float s = pow2_scale(*maxbits);
-  if (blockIdx.x == 0 && threadIdx.x == 0) scales[sidx] = s;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    scales[sidx] = s;
+    *reset = 0u;  // the next update's max slot (the other parity)
+  }
   // j (the long index) over threads / CTAs, k in an inner loop: no division per element
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (int64_t)gridDim.x * blockDim.x) {
     for (int k = 0; k < r; ++k) {
@@ -397,31 +400,33 @@ cudaError_t tc16_prepare(const TcPlan& p, const float* X, int64_t ldx, float* H,
   if ((e = map2d_t(&maps->wcat16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, W16, p.m, N1, p.ldw16, 64, N1))) return e;
   if ((e = cudaMemsetAsync(H16, 0, sizeof(__half) * (size_t)N1 * p.ldh16, st))) return e;
   if ((e = cudaMemsetAsync(W16, 0, sizeof(__half) * (size_t)N1 * p.ldw16, st))) return e;
-  if ((e = cudaMemsetAsync(mx, 0, 16, st))) return e;
+  if ((e = cudaMemsetAsync(mx, 0, 32, st))) return e;
   k_absmax<<<4 * p.grid, 256, 0, st>>>(X, p.m, p.n, ldx, mx);
   k_scale_init<<<1, 32, 0, st>>>(scales, mx);
   return cudaGetLastError();
 }
 
-// fp16 parts of H (r x n) -> Hcat16, scale at scales[1]
-cudaError_t tc16_pack_h(const TcPlan& p, const float* H, char* ws, cudaStream_t st) {
-  unsigned* mx = reinterpret_cast<unsigned*>(ws + p.off_scales + 64) + 1;
-  cudaError_t e = cudaMemsetAsync(mx, 0, 4, st);
-  if (e) return e;
-  k_absmax<<<2 * p.grid, 256, 0, st>>>(H, p.r, p.n, p.n, mx);
-  k_pack16<<<4 * p.grid, 256, 0, st>>>(H, p.r, p.n, false, p.R, mx, reinterpret_cast<__half*>(ws + p.off_h16), p.ldh16,
-                                       reinterpret_cast<float*>(ws + p.off_scales), 1);
+// fp16 parts of H (r x n) -> Hcat16, scale at scales[1].  it = -1: the initial H (its max
+// is computed here); otherwise k_tc_hupdate of iteration `it` left max|H| in slot 1 + (it & 1).
+cudaError_t tc16_pack_h(const TcPlan& p, const float* H, char* ws, cudaStream_t st, int it) {
+  unsigned* mx = reinterpret_cast<unsigned*>(ws + p.off_scales + 64);
+  unsigned* cur = mx + 1 + (it & 1);
+  if (it < 0) {
+    k_absmax<<<2 * p.grid, 256, 0, st>>>(H, p.r, p.n, p.n, cur);
+    cudaError_t e = cudaGetLastError();
+    if (e) return e;
+  }
+  k_pack16<<<4 * p.grid, 256, 0, st>>>(H, p.r, p.n, false, p.R, cur, reinterpret_cast<__half*>(ws + p.off_h16), p.ldh16,
+                                       reinterpret_cast<float*>(ws + p.off_scales), 1, mx + 1 + ((it + 1) & 1));
   return cudaGetLastError();
 }
 
-// fp16 parts of W (m x r) transposed -> WcatT16, scale at scales[2]
-cudaError_t tc16_pack_w(const TcPlan& p, const float* W, char* ws, cudaStream_t st) {
-  unsigned* mx = reinterpret_cast<unsigned*>(ws + p.off_scales + 64) + 2;
-  cudaError_t e = cudaMemsetAsync(mx, 0, 4, st);
-  if (e) return e;
-  k_absmax<<<2 * p.grid, 256, 0, st>>>(W, p.m, p.r, p.r, mx);
-  k_pack16<<<4 * p.grid, 256, 0, st>>>(W, p.r, p.m, true, p.R, mx, reinterpret_cast<__half*>(ws + p.off_w16), p.ldw16,
-                                       reinterpret_cast<float*>(ws + p.off_scales), 2);
+// fp16 parts of W (m x r) transposed -> WcatT16, scale at scales[2]; max|W| from k_tc_wupdate
+cudaError_t tc16_pack_w(const TcPlan& p, const float* W, char* ws, cudaStream_t st, int it) {
+  unsigned* mx = reinterpret_cast<unsigned*>(ws + p.off_scales + 64);
+  k_pack16<<<4 * p.grid, 256, 0, st>>>(W, p.r, p.m, true, p.R, mx + 3 + (it & 1),
+                                       reinterpret_cast<__half*>(ws + p.off_w16), p.ldw16,
+                                       reinterpret_cast<float*>(ws + p.off_scales), 2, mx + 3 + ((it + 1) & 1));
   return cudaGetLastError();
 }
 

@@ -406,7 +406,7 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
     LAUNCH(h, tc_prepare(tp, X, ldx, H, tws, &maps, st));
     if (tp.f16) {
       LAUNCH(h, tc16_prepare(tp, X, ldx, H, tws, &maps, st));
-      LAUNCH(h, tc16_pack_h(tp, H, tws, st));
+      LAUNCH(h, tc16_pack_h(tp, H, tws, st, -1));
     }
     for (int it = 0; it < iters; ++it) {
       LAUNCH(h, tc_sum_Q(tp, tws, st));
@@ -416,24 +416,24 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
         LAUNCH(h, tc_reduce_PQ(tp, tws, st));
         NC(h, g_nccl.AllReduce(red, red, (size_t)(m * r + r * r), ncclFloat64, ncclSum, h->comm_row, st));
         PLAUNCH(h, 2, 8.0 * (double)(2 * m * r + r * r) + 4.0 * 2 * tp.R * m,
-                tc_wupdate_ex(tp, W, eps, tws, red, 1, red + m * r, st));
+                tc_wupdate_ex(tp, W, eps, tws, red, 1, red + m * r, st, it));
         NC(h, g_nccl.AllReduce(gred, gred, (size_t)(r * r), ncclFloat64, ncclSum, h->comm_col, st));
       } else {
         PLAUNCH(h, 2, 8.0 * (double)tp.splitW * m * r + 8.0 * m * r + 4.0 * 2 * tp.R * m,
-                tc_wupdate(tp, W, eps, tws, st));
+                tc_wupdate(tp, W, eps, tws, st, it));
       }
-      if (tp.f16) LAUNCH(h, tc16_pack_w(tp, W, tws, st));
+      if (tp.f16) LAUNCH(h, tc16_pack_w(tp, W, tws, st, it));
       PLAUNCH(h, 7, 4.0 * (double)(n + 2 * tp.R) * (double)m,
               tp.f16 ? tc16_pass_h(tp, maps, tws, ef, st) : tc_pass_h(tp, maps, tws, ef, st));
       if (dist) {
         LAUNCH(h, tc_reduce_S(tp, tws, st));
         NC(h, g_nccl.AllReduce(sred, sred, (size_t)(n * r), ncclFloat64, ncclSum, h->comm_col, st));
-        PLAUNCH(h, 4, 8.0 * (double)n * r + 4.0 * (3 * tp.R + r) * (double)n, tc_hupdate_ex(tp, H, eps, tws, sred, 1, st));
+        PLAUNCH(h, 4, 8.0 * (double)n * r + 4.0 * (3 * tp.R + r) * (double)n, tc_hupdate_ex(tp, H, eps, tws, sred, 1, st, it));
       } else {
         PLAUNCH(h, 4, 8.0 * (double)tp.splitH * n * r + 4.0 * (3 * tp.R + r) * (double)n,
-                tc_hupdate(tp, H, eps, tws, st));
+                tc_hupdate(tp, H, eps, tws, st, it));
       }
-      if (tp.f16) LAUNCH(h, tc16_pack_h(tp, H, tws, st));
+      if (tp.f16) LAUNCH(h, tc16_pack_h(tp, H, tws, st, it));
       if (dev_trace) LAUNCH(h, launch_objective(X, ldx, m, n, W, H, r, dev_trace + (int64_t)it * nobj, st));
     }
     return NTT_OK;
