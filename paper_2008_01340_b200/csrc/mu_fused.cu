@@ -86,12 +86,6 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
-// L2 prefetch of one TMA box (no smem, no barrier): deepens the HBM pipeline
-// beyond the shared-memory ring
-__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(c0), "r"(c1)
-               : "memory");
-}
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
@@ -360,23 +354,12 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
     // ================= TMA producer =================
     if (lane == 0) {
       uint64_t policy;
-      if (evict_first & 1)
+      if (evict_first)
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
       else
         asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
-      const int pf = (evict_first >> 8) & 255;  // L2 prefetch distance (tiles)
-      for (int64_t j = 0; j < pf && j < J; ++j) {
-        const int c = (int)((b + j * gridDim.x) * BNT);
-#pragma unroll
-        for (int bx = 0; bx < NB; ++bx) tma_prefetch_2d(&tmX, c + bx * 32, 0);
-      }
       for (int64_t j = 0; j < J; ++j) {
         const int64_t pos = pbase + j;
-        if (pf && j + pf < J) {
-          const int c = (int)((b + (j + pf) * gridDim.x) * BNT);
-#pragma unroll
-          for (int bx = 0; bx < NB; ++bx) tma_prefetch_2d(&tmX, c + bx * 32, 0);
-        }
         uint32_t fm;
         while ((fm = ld_acquire_u32(free_mask)) == 0u) {
         }
@@ -416,19 +399,12 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   const bool h1 = (lane >> 4) & 1, h0 = (lane >> 3) & 1;
   // phase-B fp32 accumulators live across RS tiles; the reduce-scatter + fp64 fold
   // runs every RS tiles (and after the warp's last tile): <= RS * SL / 4 fp32 terms
-#ifndef NTT_RS
-#define NTT_RS 1
-#endif
-  constexpr int RS = NTT_RS;
+  constexpr int RS = 1;  // reduce-scatter every tile (4 measured within noise, more registers)
   float2 acc[V4 / 2];
 #pragma unroll
   for (int v = 0; v < V4 / 2; ++v) acc[v] = f2(0.f, 0.f);
   int ntile = 0;
   // swizzle offsets: phase A row i reads chunk (qch ^ (i & 7)), phase B chunk (s4 ^ rb)
-  int offA[8];
-#pragma unroll
-  for (int t = 0; t < 8; ++t) offA[t] = ((qch ^ t) << 4);
-  (void)offA;
 
   // HDIRECT: this lane's H columns of a tile, loaded ONE TILE AHEAD (software
   // pipelined: the global-load latency overlaps the previous tile's work; each
@@ -511,8 +487,6 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
     }
 
     // ---------------- phase A ----------------
-    const bool masked = (r < R) || (jt + BNT > n);  // warp-uniform
-    (void)masked;
     {
       float2 hn[R][CPL / 2];
       if (do_update) {
@@ -522,19 +496,9 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
         for (int k = 0; k < R; ++k)
 #pragma unroll
           for (int p2 = 0; p2 < CPL / 2; ++p2) s2[k][p2] = f2(0.f, 0.f);
-#ifndef NTT_PA_FULL
-#define NTT_PA_FULL 0
-#endif
-#if NTT_PA_FULL
-        // all MP rows: rows >= m are zero in the TMA tile (OOB fill) and in Ws
-#pragma unroll
-        for (int i = 0; i < MP; ++i) {
-          const int offi = offA[i & 7];
-#else
 #pragma unroll 4
         for (int i = 0; i < m; ++i) {
           const int offi = (qch ^ (i & 7)) << 4;
-#endif
           float2 xv[CPL / 2];
           if (CPL == 4) {
             const float4 x = lds128(xb + offi + i * 128);
@@ -558,24 +522,15 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
         for (int k = 0; k < R; ++k)
 #pragma unroll
           for (int p2 = 0; p2 < CPL / 2; ++p2) ev[k][p2] = f2(0.f, 0.f);
-#ifndef NTT_GSYM
-#define NTT_GSYM 1
-#endif
 #pragma unroll
         for (int l = 0; l < R; ++l) {
-#if NTT_GSYM
           // G = W^T W is symmetric: G[k][l] = Gs[l * 8 + k], read as two 128-bit words
           float gl[8];
           *reinterpret_cast<float4*>(gl) = *reinterpret_cast<const float4*>(Gs + l * 8);
           if (R > 4) *reinterpret_cast<float4*>(gl + 4) = *reinterpret_cast<const float4*>(Gs + l * 8 + 4);
-#endif
 #pragma unroll
           for (int k = 0; k < R; ++k) {
-#if NTT_GSYM
             const float g = gl[k];
-#else
-            const float g = Gs[k * 8 + l];
-#endif
 #pragma unroll
             for (int p2 = 0; p2 < CPL / 2; ++p2) ev[k][p2] = __ffma2_rn(bc(g), hv[l][p2], ev[k][p2]);
           }
@@ -587,15 +542,10 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
             float2 v;
             v.x = mu_q(hv[k][p2].x, s2[k][p2].x, ev[k][p2].x, eps);
             v.y = mu_q(hv[k][p2].y, s2[k][p2].y, ev[k][p2].y, eps);
-#ifndef NTT_MASKB
-#define NTT_MASKB 0
-#endif
-            if (!NTT_MASKB || masked) {
-              if (k >= r) v = f2(0.f, 0.f);  // padded ranks (0/0 when eps = 0)
-              // columns beyond n: zero (never stored, never accumulated)
-              if (c0 + 2 * p2 >= n) v.x = 0.f;
-              if (c0 + 2 * p2 + 1 >= n) v.y = 0.f;
-            }
+            if (k >= r) v = f2(0.f, 0.f);  // padded ranks (0/0 when eps = 0)
+            // columns beyond n: zero (never stored, never accumulated)
+            if (c0 + 2 * p2 >= n) v.x = 0.f;
+            if (c0 + 2 * p2 + 1 >= n) v.y = 0.f;
             hn[k][p2] = v;
           }
         // store H (in place; this tile's H was already read)
@@ -837,12 +787,10 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   if (warp == NW) {
     if (lane == 0) {
       uint64_t policy;
-      if (evict_first & 1)
+      if (evict_first)
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
       else
         asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
-      const int pf = (evict_first >> 8) & 255;  // L2 prefetch distance (tiles)
-      for (int64_t j = 0; j < pf && j < J; ++j) tma_prefetch_2d(&tmX, (int)((b + j * gridDim.x) * BNC), 0);
       for (int64_t j = 0; j < J; ++j) {
         const int s = ring_s;
         const uint32_t ph = ring_ph;
@@ -850,7 +798,6 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
           ring_s = 0;
           ring_ph ^= 1u;
         }
-        if (pf && j + pf < J) tma_prefetch_2d(&tmX, (int)((b + (j + pf) * gridDim.x) * BNC), 0);
         MBAR_WAIT(&empty[s], ph ^ 1u, 3, j);
         mbar_expect_tx(&full[s], SB);
         const int col0 = (int)((b + j * gridDim.x) * BNC);
@@ -1196,7 +1143,7 @@ k_fused_wc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUte
   if (warp == NWW) {
     if (lane == 0) {
       uint64_t policy;
-      if (evict_first & 1)
+      if (evict_first)
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
       else
         asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
@@ -1657,12 +1604,7 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
                          cudaStream_t st, const PersistArgs* pap) {
   const PersistArgs pa = pap ? *pap : PersistArgs{0, nullptr, nullptr, nullptr, nullptr, nullptr};
   if (pa.iters > 0 && m > 40 && use_wc()) return cudaErrorNotSupported;
-  static const int pf_env = [] {
-    const char* e = getenv("NTT_PF");
-    return e ? atoi(e) : -1;
-  }();
-  const int pf_tiles = pf_env >= 0 ? pf_env : 0;
-  const int evict_first = (((double)m * (double)n * 4.0 > 48e6) ? 1 : 0) | ((pf_tiles & 255) << 8);
+  const int evict_first = ((double)m * (double)n * 4.0 > 48e6) ? 1 : 0;
   if (m > 40 && use_wc()) {
     const int MPc = m <= 128 ? 128 : 256;
     CUtensorMap mx, mh;

@@ -1,3 +1,5 @@
-timeout 600 python -m pytest tests/test_gpu_tc.py tests/test_gpu_dist.py tests/test_gpu_fullsize.py -x -q 2>&1 | tail -1
-timeout 300 python tools/bench_nmf.py config2 20 2>&1 | tail -1 > gpurun_out/c2_16.json
-timeout 300 python tools/bench_nmf.py config5 5 2>&1 | tail -1 > gpurun_out/c5_16.json
+set -x
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?"; tail -2 gpurun_out/pytest_gpu.log
+timeout 300 python __graft_entry__.py --smoke > gpurun_out/smoke.log 2>&1; echo "smoke rc $?"; tail -1 gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; echo "bench rc $?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_r1c.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-other > gpurun_out/ncu_launch.log 2>&1; echo "ncu launch rc $?"
