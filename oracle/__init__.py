@@ -393,3 +393,77 @@ def ntt_decompose_eps(A: np.ndarray, tt_eps: float, iters: int, seed: int = 0, e
         rprev = r
     cores.append(T)
     return ranks, np.concatenate(cores)
+
+
+# ------------------------------------------------- BCD NMF (SURVEY s.8(f) f1) --
+def _spec(M: np.ndarray) -> float:
+    """Spectral norm of a symmetric PSD r x r Gram (LAPACK eigvalsh, a library primitive)."""
+    return float(np.linalg.eigvalsh(np.asarray(M, np.float64))[-1]) if M.size else 0.0
+
+
+def nmf_bcd(X: np.ndarray, W0: np.ndarray, H0: np.ndarray, iters: int, delta: float = 0.9999,
+            trace: bool = False):
+    """Alg. 3 (distBCDnmf) on one process, fp64, with readings
+    R22-R27 (DESIGN.md s.3):
+      init  W_m = W0 sqrt(||X||_F)/||W0||_F, H_m = H0 sqrt(||X||_F)/||H0||_F; W = W_m, H = H_m;
+            Q = H H^T, P = X H^T, t = 1, obj = 1/2 ||X||_F^2, L_W(prev) = ||Q||_2, L_H(prev) = ||W^T W||_2
+      loop  W  = max(0, W_m - (W_m Q - P) / L_W),  L_W = ||Q||_2           (l.6-8)
+            column L1 normalisation of W: c_k = sum_i W[i][k] (> 0): W[:, k] /= c_k,
+            H_m[k, :] *= c_k, H_prev[k, :] *= c_k, W_prev[:, k] /= c_k     (l.9; WH invariant)
+            G  = W^T W,  L_H = ||G||_2                                      (l.10)
+            H  = max(0, H_m - (G H_m - W^T X) / L_H)                        (l.11-14)
+            Q = H H^T, P = X H^T, obj_new = 1/2 ||X - W H||_F^2             (l.15-16)
+            obj_new >= obj: correction -- back to the last accepted (W_prev, H_prev),
+                W_m = W_prev, H_m = H_prev, t = 1, Q, P from H_prev         (l.17-20)
+            else extrapolation: t+ = (1 + sqrt(1 + 4 t^2)) / 2, w = (t - 1) / t+,
+                w_W = min(w, delta sqrt(L_W_prev / L_W)), w_H = min(w, delta sqrt(L_H_prev / L_H)),
+                W_m = W + w_W (W - W_prev), H_m = H + w_H (H - H_prev),
+                W_prev, H_prev = W, H; L_*_prev = L_*; t = t+; obj = obj_new  (l.21-27)
+    Returns (W, H) = the last accepted iterates, or (W, H, accepted-objective trace)."""
+    X = np.asarray(X, dtype=np.float64)
+    m, n = X.shape
+    W0 = np.asarray(W0, dtype=np.float64)
+    H0 = np.asarray(H0, dtype=np.float64)
+    r = W0.shape[1]
+    nx = np.linalg.norm(X)
+    if nx == 0.0:
+        raise ValueError("||X|| = 0 (DegenerateInputError, S:330)")
+    Wm = W0 * (np.sqrt(nx) / np.linalg.norm(W0))
+    Hm = H0 * (np.sqrt(nx) / np.linalg.norm(H0))
+    Wp, Hp = Wm.copy(), Hm.copy()
+    Q, P = Hp @ Hp.T, X @ Hp.T
+    t, obj = 1.0, 0.5 * nx * nx
+    LWp, LHp = _spec(Q), _spec(Wp.T @ Wp)
+    tr = []
+    for _ in range(iters):
+        LW = _spec(Q)
+        W = np.maximum(0.0, Wm - (Wm @ Q - P) / LW) if LW > 0 else Wm.copy()
+        c = W.sum(axis=0)
+        nz = c > 0
+        W[:, nz] /= c[nz]
+        Hm = Hm.copy()
+        Hp = Hp.copy()
+        Wp = Wp.copy()
+        Hm[nz, :] *= c[nz, None]
+        Hp[nz, :] *= c[nz, None]
+        Wp[:, nz] /= c[nz]
+        G = W.T @ W
+        LH = _spec(G)
+        H = np.maximum(0.0, Hm - (G @ Hm - W.T @ X) / LH) if LH > 0 else Hm.copy()
+        obj_new = 0.5 * float(np.sum((X - W @ H) ** 2))
+        if obj_new >= obj:          # correction
+            Wm, Hm, t = Wp.copy(), Hp.copy(), 1.0
+            Q, P = Hp @ Hp.T, X @ Hp.T
+        else:                       # extrapolation
+            tp = (1.0 + np.sqrt(1.0 + 4.0 * t * t)) / 2.0
+            w = (t - 1.0) / tp
+            wW = min(w, delta * np.sqrt(LWp / LW))
+            wH = min(w, delta * np.sqrt(LHp / LH))
+            Wm = W + wW * (W - Wp)
+            Hm = H + wH * (H - Hp)
+            Wp, Hp = W, H
+            LWp, LHp = LW, LH
+            t, obj = tp, obj_new
+            Q, P = H @ H.T, X @ H.T
+        tr.append(obj)
+    return (Wp, Hp, np.array(tr)) if trace else (Wp, Hp)
