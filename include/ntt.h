@@ -157,6 +157,25 @@ ntt_status ntt_decompose_eps(ntt_handle h, const float* A, int32_t d, const int6
 ntt_status ntt_rank_rule(ntt_handle h, const float* X, int64_t m, int64_t n, int64_t ldx, double tt_eps,
                          int32_t* rank, double* eig);
 
+/* --------------------------------------------------------------- BCD NMF
+ * The paper's alternative NMF (Alg. 3, distBCDnmf, P:196-240, P:254, P:294;
+ * SURVEY s.8(f) f1) with readings R22-R27 (DESIGN.md s.3): prox-linear block
+ * steps W = max(0, W_m - (W_m Q - P)/L_W), H = max(0, H_m - (G H_m - W^T X)/L_H)
+ * with L = spectral norm of the r x r Gram (Q = H H^T, G = W^T W), column L1
+ * normalisation of W compensated into H, Nesterov extrapolation with weights
+ * min((t-1)/t+, delta sqrt(L_prev/L)), and a correction (return to the last
+ * accepted iterates, t = 1) whenever the objective 1/2 ||X - W H||_F^2 (Gram
+ * identity, fp64 sums) does not decrease.
+ *   X : DEVICE, m x n row-major, row stride ldx >= n.
+ *   W : DEVICE, m x r (in: W0, out: last accepted W).  H: DEVICE, r x n (in/out).
+ *       W0 and H0 are rescaled to Frobenius norm sqrt(||X||_F) first (R22).
+ *   delta in [0, 1) (paper: 0.9999).  objective_trace: nullable HOST, iters
+ *   doubles: the accepted objective after every iteration.
+ * Single-GPU handles, 1 <= r <= min(m, n, 32) (else NTT_ERR_RANK);
+ * NTT_ERR_DEGENERATE if ||X||_F = 0.  One host synchronisation per iteration. */
+ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64_t ldx, int32_t r, int32_t iters,
+                       double delta, float* W, float* H, double* objective_trace);
+
 /* --------------------------------------------------- reconstruction / error
  * Contract a TT (Eq. 1):  A~ = G_1 o G_2 o ... o G_d, and/or the
  * relative error of Eq. 3: ||ref - A~||_F / ||ref||_F by direct

@@ -161,6 +161,13 @@ class Handle:
         self._check(lib().ntt_nmf_mu(self._h, _ptr(X), m, n, ldx, r, iters, eps, _ptr(W), _ptr(H), tr))
         return list(tr)[:iters] if trace else None
 
+    def ntt_nmf_bcd(self, X, m: int, n: int, ldx: int, r: int, iters: int, W, H, delta: float = 0.9999,
+                    trace: bool = False):
+        """Alg. 3 BCD NMF on device buffers (W, H in/out); returns the accepted-objective trace if asked."""
+        tr = (ctypes.c_double * max(1, iters))() if trace else None
+        self._check(lib().ntt_nmf_bcd(self._h, _ptr(X), m, n, ldx, r, iters, delta, _ptr(W), _ptr(H), tr))
+        return list(tr)[:iters] if trace else None
+
     def ntt_decompose(self, A, dims, ranks, iters: int, seed: int, eps: float, cores, workspace=None,
                       workspace_bytes: int = 0, want_error: bool = False) -> Optional[float]:
         err = ctypes.c_double(-1.0) if want_error else None

@@ -49,6 +49,25 @@ size_t rank_rule_bytes(int64_t N, int64_t T, int num_sms);
 cudaError_t launch_rank_rule(const float* X, int64_t m, int64_t n, int64_t ldx, double tt_eps, char* ws,
                              int num_sms, int* d_rank, double* d_eig, cudaStream_t st);
 
+cudaError_t launch_sym_eig(double* C, int N, double* scratch, double* eig, int* rank_dummy, cudaStream_t st);
+
+// BCD NMF building blocks (bcd.cu, Alg. 3)
+int bcd_w_ctas(int64_t m);
+cudaError_t launch_bcd_w(const float* Wm, int64_t m, int r, const double* P, const double* Q, const double* LW,
+                         float* W, double* cpart, cudaStream_t st);
+cudaError_t launch_bcd_wnorm(float* W, float* Wp, int64_t m, int r, const double* c, double* Gpart, cudaStream_t st);
+cudaError_t launch_bcd_hnorm(float* Hm, float* Hp, int r, int64_t n, const double* c, cudaStream_t st);
+cudaError_t launch_bcd_h(const float* X, int64_t ldx, int64_t m, int64_t n, const float* W, int r, const double* G,
+                         const double* LH, const float* Hm, float* H, int num_sms, cudaStream_t st);
+cudaError_t launch_bcd_obj(double xx, const float* W, const double* P, int64_t m, int r, const double* G,
+                           const double* Q, double* out, cudaStream_t st);
+cudaError_t launch_bcd_extrap(float* V, float* Vm, float* Vp, int64_t cnt, double w, cudaStream_t st);
+cudaError_t launch_scale_copy(const float* src, float* a, float* b, int64_t cnt, const double* num, const double* den,
+                              cudaStream_t st);
+int sumsq_ctas();
+cudaError_t launch_sumsq(const float* v, int64_t rows, int64_t cols, int64_t ld, double* part, cudaStream_t st);
+cudaError_t launch_copy_last(const double* eig, int N, double* out, cudaStream_t st);
+
 // 1/2 ||X - W H||^2 partial sums (fp64), one per CTA; returns number of partials.
 int objective_ctas(int64_t n);
 cudaError_t launch_objective(const float* X, int64_t ldx, int64_t m, int64_t n, const float* W,

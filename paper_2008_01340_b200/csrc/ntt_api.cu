@@ -1093,6 +1093,136 @@ ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t*
   return NTT_OK;
 }
 
+ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64_t ldx, int32_t r, int32_t iters,
+                       double delta, float* W, float* H, double* objective_trace) {
+  if (!h) return NTT_ERR_INVALID_ARG;
+  if (!X || !W || !H) return fail(h, NTT_ERR_INVALID_ARG, "null X, W or H");
+  if (m < 1 || n < 1 || ldx < n) return fail(h, NTT_ERR_INVALID_ARG, "bad shape m=%lld n=%lld ldx=%lld",
+                                              (long long)m, (long long)n, (long long)ldx);
+  if (iters < 0) return fail(h, NTT_ERR_INVALID_ARG, "iters < 0");
+  if (!(delta >= 0.0 && delta < 1.0)) return fail(h, NTT_ERR_INVALID_ARG, "delta must be in [0, 1)");
+  if (r < 1 || r > 32 || r > std::min(m, n)) return fail(h, NTT_ERR_RANK, "BCD needs 1 <= r <= min(m, n, 32)");
+  if (h->nranks > 1) return fail(h, NTT_ERR_UNSUPPORTED, "ntt_nmf_bcd runs on a single-GPU handle");
+  if (!is_device_ptr(X) || !is_device_ptr(W) || !is_device_ptr(H))
+    return fail(h, NTT_ERR_INVALID_ARG, "ntt_nmf_bcd takes device buffers");
+  CU(h, cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  const XhtPlan xp = plan_xht(m, n, h->num_sms), qp = plan_xht(r, n, h->num_sms);
+  const int nwc = bcd_w_ctas(m);
+  size_t o = 0;
+  auto take = [&](size_t b) {
+    size_t at = o;
+    o = align_up(o + b);
+    return at;
+  };
+  const size_t oWm = take(sizeof(float) * m * r), oWp = take(sizeof(float) * m * r);
+  const size_t oHm = take(sizeof(float) * r * n), oHp = take(sizeof(float) * r * n);
+  const size_t oP0 = take(sizeof(double) * m * r), oP1 = take(sizeof(double) * m * r);
+  const size_t oQ0 = take(sizeof(double) * r * r), oQ1 = take(sizeof(double) * r * r);
+  const size_t oG = take(sizeof(double) * r * r), oC = take(sizeof(double) * r);
+  const size_t oPp = take(sizeof(double) * (size_t)xp.ncs * m * r), oQp = take(sizeof(double) * (size_t)qp.ncs * r * r);
+  const size_t oCp = take(sizeof(double) * (size_t)nwc * r), oGp = take(sizeof(double) * (size_t)nwc * r * r);
+  const size_t oE = take(sizeof(double) * (r * r + 3 * r + 8)), oSq = take(sizeof(double) * sumsq_ctas());
+  const size_t oSc = take(sizeof(double) * 16);
+  ntt_status s = ensure_ws(h, o);
+  if (s) return s;
+  char* ws = reinterpret_cast<char*>(h->ws);
+  float* Wm = reinterpret_cast<float*>(ws + oWm);
+  float* Wp = reinterpret_cast<float*>(ws + oWp);
+  float* Hm = reinterpret_cast<float*>(ws + oHm);
+  float* Hp = reinterpret_cast<float*>(ws + oHp);
+  double* Pc = reinterpret_cast<double*>(ws + oP0);  // X H_prev^T of the accepted H
+  double* Pn = reinterpret_cast<double*>(ws + oP1);
+  double* Qc = reinterpret_cast<double*>(ws + oQ0);
+  double* Qn = reinterpret_cast<double*>(ws + oQ1);
+  double* G = reinterpret_cast<double*>(ws + oG);
+  double* c = reinterpret_cast<double*>(ws + oC);
+  double* Ppart = reinterpret_cast<double*>(ws + oPp);
+  double* Qpart = reinterpret_cast<double*>(ws + oQp);
+  double* cpart = reinterpret_cast<double*>(ws + oCp);
+  double* Gpart = reinterpret_cast<double*>(ws + oGp);
+  double* E = reinterpret_cast<double*>(ws + oE);     // eigen scratch: [C r*r][v, p 2r][eig r][rank int]
+  double* sq = reinterpret_cast<double*>(ws + oSq);
+  double* sc = reinterpret_cast<double*>(ws + oSc);   // [0] ||X||^2 [1] ||W0||^2 [2] ||H0||^2 [3] L_W [4] L_H [5] obj
+  int* rk_dummy = reinterpret_cast<int*>(E + r * r + 3 * r);
+  auto spec = [&](const double* M, double* out) -> ntt_status {  // spectral norm of an r x r Gram
+    CU(h, cudaMemcpyAsync(E, M, sizeof(double) * r * r, cudaMemcpyDeviceToDevice, st));
+    LAUNCH(h, launch_sym_eig(E, r, E + r * r, E + r * r + 2 * r, rk_dummy, st));
+    LAUNCH(h, launch_copy_last(E + r * r + 2 * r, r, out, st));
+    return NTT_OK;
+  };
+  auto xht_pq = [&](const float* Hs, double* P, double* Q) -> ntt_status {  // P = X H^T, Q = H H^T
+    LAUNCH(h, launch_xht_partial(X, ldx, m, n, Hs, n, r, xp, Ppart, st));
+    LAUNCH(h, launch_sum_partials(Ppart, xp.ncs, m * r, P, st));
+    LAUNCH(h, launch_xht_partial(Hs, n, r, n, Hs, n, r, qp, Qpart, st));
+    LAUNCH(h, launch_sum_partials(Qpart, qp.ncs, (int64_t)r * r, Q, st));
+    return NTT_OK;
+  };
+  // ---- init (Alg. 3 l.1-4, R22, R25)
+  LAUNCH(h, launch_sumsq(X, m, n, ldx, sq, st));
+  LAUNCH(h, launch_sum_partials(sq, sumsq_ctas(), 1, sc + 0, st));
+  LAUNCH(h, launch_sumsq(W, m, r, r, sq, st));
+  LAUNCH(h, launch_sum_partials(sq, sumsq_ctas(), 1, sc + 1, st));
+  LAUNCH(h, launch_sumsq(H, r, n, n, sq, st));
+  LAUNCH(h, launch_sum_partials(sq, sumsq_ctas(), 1, sc + 2, st));
+  LAUNCH(h, launch_scale_copy(W, Wm, Wp, m * r, sc + 0, sc + 1, st));
+  LAUNCH(h, launch_scale_copy(H, Hm, Hp, (int64_t)r * n, sc + 0, sc + 2, st));
+  if ((s = xht_pq(Hp, Pc, Qc))) return s;
+  LAUNCH(h, launch_bcd_wnorm(Wp, Wp, m, r, nullptr, Gpart, st));  // G of W_prev (no normalisation)
+  LAUNCH(h, launch_sum_partials(Gpart, nwc, (int64_t)r * r, G, st));
+  if ((s = spec(Qc, sc + 3))) return s;
+  if ((s = spec(G, sc + 4))) return s;
+  double hs[6];
+  CU(h, cudaMemcpyAsync(hs, sc, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  CU(h, cudaStreamSynchronize(st));
+  const double xx = hs[0];
+  if (!(xx > 0.0)) return fail(h, NTT_ERR_DEGENERATE, "||X|| = 0");
+  double LWp = hs[3], LHp = hs[4], t = 1.0, obj = 0.5 * xx;
+  for (int it = 0; it < iters; ++it) {
+    // W step (l.6-8), column L1 normalisation with compensation (l.9, R24), G and L_H (l.10)
+    if ((s = spec(Qc, sc + 3))) return s;
+    LAUNCH(h, launch_bcd_w(Wm, m, r, Pc, Qc, sc + 3, W, cpart, st));
+    LAUNCH(h, launch_sum_partials(cpart, nwc, r, c, st));
+    LAUNCH(h, launch_bcd_wnorm(W, Wp, m, r, c, Gpart, st));
+    LAUNCH(h, launch_bcd_hnorm(Hm, Hp, r, n, c, st));
+    LAUNCH(h, launch_sum_partials(Gpart, nwc, (int64_t)r * r, G, st));
+    if ((s = spec(G, sc + 4))) return s;
+    // H step (l.11-14), then X H^T, H H^T and the objective of the candidate (l.15-16)
+    LAUNCH(h, launch_bcd_h(X, ldx, m, n, W, r, G, sc + 4, Hm, H, h->num_sms, st));
+    if ((s = xht_pq(H, Pn, Qn))) return s;
+    LAUNCH(h, launch_bcd_obj(xx, W, Pn, m, r, G, Qn, sc + 5, st));
+    CU(h, cudaMemcpyAsync(hs, sc, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    CU(h, cudaStreamSynchronize(st));
+    const double LW = hs[3], LH = hs[4], obj_new = hs[5];
+    if (obj_new >= obj) {
+      // correction (l.17-20, R26): back to the last accepted iterates, no extrapolation
+      CU(h, cudaMemcpyAsync(Wm, Wp, sizeof(float) * m * r, cudaMemcpyDeviceToDevice, st));
+      CU(h, cudaMemcpyAsync(Hm, Hp, sizeof(float) * r * n, cudaMemcpyDeviceToDevice, st));
+      t = 1.0;
+      if ((s = xht_pq(Hp, Pc, Qc))) return s;
+    } else {
+      // extrapolation (l.21-27, R27)
+      const double tp = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
+      const double w = (t - 1.0) / tp;
+      const double wW = std::min(w, delta * sqrt(LWp / LW)), wH = std::min(w, delta * sqrt(LHp / LH));
+      LAUNCH(h, launch_bcd_extrap(W, Wm, Wp, m * r, wW, st));
+      LAUNCH(h, launch_bcd_extrap(H, Hm, Hp, (int64_t)r * n, wH, st));
+      std::swap(Pc, Pn);
+      std::swap(Qc, Qn);
+      LWp = LW;
+      LHp = LH;
+      t = tp;
+      obj = obj_new;
+    }
+    if (objective_trace) objective_trace[it] = obj;
+  }
+  // return the last accepted iterates
+  CU(h, cudaMemcpyAsync(W, Wp, sizeof(float) * m * r, cudaMemcpyDeviceToDevice, st));
+  CU(h, cudaMemcpyAsync(H, Hp, sizeof(float) * r * n, cudaMemcpyDeviceToDevice, st));
+  CU(h, cudaStreamSynchronize(st));
+  return NTT_OK;
+}
+
 ntt_status ntt_decompose_eps(ntt_handle h, const float* A, int32_t d, const int64_t* dims, double tt_eps,
                              const int32_t* max_ranks, int32_t iters, uint64_t seed, float eps, float* cores,
                              int64_t cores_capacity, int32_t* ranks_out, double* rel_err) {

@@ -1,0 +1,124 @@
+"""GPU parity of the BCD NMF (Alg. 3; readings R22-R27; SURVEY s.8(f) f1)
+against oracle.nmf_bcd.
+
+Both sides start from the same fp32 inputs; the GPU stores W, H in fp32 (fp64 sums and
+r x r matrices), the oracle is fp64 throughout.  Tolerances: factors 1e-4 relative to their
+max entry, accepted objective 1e-5 relative, over a bounded number of iterations (the
+accept / correct branch of l.17 is decided by the objective; the inputs keep clear
+decreases in that window, so both sides take the same branches — checked)."""
+import numpy as np
+import pytest
+
+import ntt_inputs as ni
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def h():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2008_01340_b200 as P
+    return P.Handle(0)
+
+
+def case(m, n, r, seed, lowrank=0):
+    rng = np.random.default_rng(seed)
+    if lowrank:
+        X = rng.random((m, lowrank)) @ rng.random((lowrank, n)) + 0.01 * rng.random((m, n))
+    else:
+        X = rng.random((m, n))
+    X = X.astype(np.float32)
+    W0 = ni.uniform(m * r, seed, ni.stream_w(1)).reshape(m, r).astype(np.float32)
+    H0 = ni.uniform(r * n, seed, ni.stream_h(1)).reshape(r, n).astype(np.float32)
+    return X, W0, H0
+
+
+def run_gpu(h, X, W0, H0, iters, delta=0.9999):
+    m, n = X.shape
+    r = W0.shape[1]
+    Xd = torch.from_numpy(X.ravel()).cuda()
+    Wd = torch.from_numpy(W0.ravel().copy()).cuda()
+    Hd = torch.from_numpy(H0.ravel().copy()).cuda()
+    tr = h.ntt_nmf_bcd(Xd, m, n, n, r, iters, Wd, Hd, delta=delta, trace=True)
+    return Wd.cpu().numpy().reshape(m, r), Hd.cpu().numpy().reshape(r, n), np.array(tr)
+
+
+def branches(tr, obj0):
+    prev = np.concatenate([[obj0], tr[:-1]])
+    return tr < prev        # True = accepted (extrapolation), False = correction
+
+
+@pytest.mark.parametrize("m,n,r,iters,lr", [
+    (40, 300, 4, 15, 0), (257, 1000, 8, 15, 0), (100, 2000, 16, 12, 6), (513, 777, 32, 10, 0),
+    (3000, 64, 5, 15, 3), (1, 50, 1, 8, 0), (7, 7, 7, 10, 0)])
+def test_bcd_parity(h, ora, m, n, r, iters, lr):
+    X, W0, H0 = case(m, n, r, m * 7 + n + r, lr)
+    Wg, Hg, trg = run_gpu(h, X, W0, H0, iters)
+    Wo, Ho, tro = ora.nmf_bcd(X.astype(np.float64), W0, H0, iters, trace=True)
+    obj0 = 0.5 * float(np.sum(X.astype(np.float64) ** 2))
+    assert np.array_equal(branches(trg, obj0), branches(tro, obj0))
+    # the GPU evaluates the objective by the Gram identity (fp32 chunk products in X H^T):
+    # its rounding scales with ||X||^2 = 2 obj0, hence the absolute term
+    assert np.abs(trg - tro).max() <= 1e-5 * tro.max() + 1e-6 * obj0
+    assert np.abs(Wg - Wo).max() <= 1e-4 * np.abs(Wo).max()
+    assert np.abs(Hg - Ho).max() <= 1e-4 * np.abs(Ho).max()
+    assert Wg.min() >= 0 and Hg.min() >= 0
+
+
+def test_bcd_zero_iterations_rescales(h, ora):
+    X, W0, H0 = case(30, 70, 3, 1)
+    Wg, Hg, _ = run_gpu(h, X, W0, H0, 0)
+    Wo, Ho = ora.nmf_bcd(X.astype(np.float64), W0, H0, 0)
+    assert np.allclose(Wg, Wo, rtol=1e-6, atol=0) and np.allclose(Hg, Ho, rtol=1e-6, atol=0)
+    nx = np.linalg.norm(X.astype(np.float64))
+    assert abs(np.linalg.norm(Wg.astype(np.float64)) - np.sqrt(nx)) <= 1e-6 * np.sqrt(nx)
+
+
+def test_bcd_delta_zero(h, ora):
+    """delta = 0 switches extrapolation off (w_W = w_H = 0): plain prox-linear BCD."""
+    X, W0, H0 = case(64, 200, 6, 5)
+    Wg, Hg, trg = run_gpu(h, X, W0, H0, 12, delta=0.0)
+    Wo, Ho, tro = ora.nmf_bcd(X.astype(np.float64), W0, H0, 12, delta=0.0, trace=True)
+    assert np.abs(trg - tro).max() <= 1e-5 * tro.max() + 1e-6 * 0.5 * float(np.sum(X.astype(np.float64) ** 2))
+    assert np.abs(Wg - Wo).max() <= 1e-4 * np.abs(Wo).max()
+    assert np.abs(Hg - Ho).max() <= 1e-4 * np.abs(Ho).max()
+
+
+def test_bcd_errors(h):
+    import paper_2008_01340_b200 as P
+    X = torch.rand(20 * 40, device="cuda")
+    W = torch.rand(20 * 33, device="cuda")
+    H = torch.rand(33 * 40, device="cuda")
+    with pytest.raises(P.NttError):
+        h.ntt_nmf_bcd(X, 20, 40, 40, 33, 5, W, H)          # r > 32
+    with pytest.raises(P.NttError):
+        h.ntt_nmf_bcd(X, 20, 40, 40, 4, 5, W, H, delta=1.0)
+    Z = torch.zeros(20 * 40, device="cuda")
+    with pytest.raises(P.NttError):
+        h.ntt_nmf_bcd(Z, 20, 40, 40, 4, 5, W, H)            # ||X|| = 0
+
+
+def test_bcd_fullsize_properties(h):
+    """Config-2 size (4096 x 4096, r = 16): accepted objective non-increasing, factors
+    non-negative, trace = 1/2 ||X - W H||_F^2 of the returned factors, and lower error
+    than the same number of MU iterations from the same start (the paper's claim)."""
+    m = n = 4096
+    r, iters = 16, 40
+    g = torch.Generator(device="cuda").manual_seed(2)
+    Wt = torch.rand(m, r, device="cuda", generator=g)
+    Ht = torch.rand(r, n, device="cuda", generator=g)
+    X = (Wt @ Ht + 0.1 * torch.rand(m, n, device="cuda", generator=g)).contiguous()
+    W0 = torch.rand(m * r, device="cuda", generator=g)
+    H0 = torch.rand(r * n, device="cuda", generator=g)
+    W, H = W0.clone(), H0.clone()
+    tr = np.array(h.ntt_nmf_bcd(X.view(-1), m, n, n, r, iters, W, H, trace=True))
+    assert np.all(np.diff(tr) <= 0) and W.min() >= 0 and H.min() >= 0
+    Xd = X.double()
+    res = 0.5 * float(((Xd - W.view(m, r).double() @ H.view(r, n).double()) ** 2).sum())
+    assert abs(res - tr[-1]) <= 1e-4 * tr[-1]
+    Wm, Hm = W0.clone(), H0.clone()
+    h.ntt_nmf_mu(X.view(-1), m, n, n, r, iters, 1e-16, Wm, Hm)
+    res_mu = 0.5 * float(((Xd - Wm.view(m, r).double() @ Hm.view(r, n).double()) ** 2).sum())
+    assert res < res_mu
