@@ -7,12 +7,18 @@
 //   k_bcd_w      W = max(0, W_m - (W_m Q - P) / L_W), per row; column L1 partials
 //   k_bcd_wnorm  W[:,k] /= c_k, W_prev[:,k] /= c_k (and G partials of the new W)
 //   k_bcd_hnorm  H_m[k,:] *= c_k, H_prev[k,:] *= c_k
-//   k_bcd_h      S = W^T X (fp32 per 128-row chunk, fp64 across), E = G H_m,
-//                H = max(0, H_m - (E - S) / L_H), per column
-//   k_bcd_obj    1/2 (||X||^2 - 2 <W, X H^T> + <W^T W, H H^T>) in fp64 (Gram identity)
-//   k_bcd_extrap V_m = V + w (V - V_prev), V_prev = V
-// The host drives the iteration (one 40-byte read-back per iteration for the
-// correction / extrapolation decision, as Alg. 3 l.17 branches on the objective).
+//   k_bcd_spart  split-K partials of S = W^T X (FFMA path; the tensor-core path
+//                produces the same [split][j][k] layout with k_skinny_tc16<R, 1>)
+//   k_bcd_hup    S = sum of the partials, E = G H_m, H = max(0, H_m - (E - S) / L_H)
+//   k_bcd_psum_dot  P = X H^T from its split partials, with per-CTA partials of <W, P>
+//   k_spec_norm  ||M||_2 of an r x r Gram (repeated squaring + Rayleigh quotient)
+//   k_bcd_decide 1/2 (||X||^2 - 2 <W, X H^T> + <W^T W, H H^T>) in fp64 (Gram identity, R25),
+//                the l.17 branch and the extrapolation weights, on the device
+//   k_bcd_commit V_m = V + w (V - V_prev), V_prev = V (accepted) or V_m = V_prev (correction)
+//   k_bcd_commit_pq  P, Q = those of the new H (accepted) or of the rescaled H_prev
+// Every decision stays on the device (state block `bs`, below), so one iteration is
+// a fixed launch sequence the host captures once in a CUDA graph and replays.
+#include <algorithm>
 #include <cstdint>
 
 #include "common.cuh"
@@ -45,7 +51,8 @@ k_bcd_w(const float* __restrict__ Wm, int64_t m, int r, const double* __restrict
     double v = 0.0;
     if (i < m && k < r) {
       double g = -P[i * r + k];
-      for (int l = 0; l < r; ++l) g += w[l] * Qs[l * R + k];
+#pragma unroll
+      for (int l = 0; l < R; ++l) g += w[l] * Qs[l * R + k];  // Qs zero-padded beyond r
       v = L > 0.0 ? fmax(0.0, w[k] - g / L) : w[k];
       const float vf = (float)v;
       W[i * r + k] = vf;
@@ -65,8 +72,9 @@ k_bcd_w(const float* __restrict__ Wm, int64_t m, int r, const double* __restrict
 template <int R>
 __global__ void __launch_bounds__(BROWS)
 k_bcd_wnorm(float* __restrict__ W, float* __restrict__ Wp, int64_t m, int r, const double* __restrict__ c,
-            double* __restrict__ Gpart) {
+            double* __restrict__ Gpart, unsigned* __restrict__ maxw) {
   __shared__ float Wn[BROWS][R + 1];
+  float mx = 0.0f;
   const int64_t i = (int64_t)blockIdx.x * BROWS + threadIdx.x;
 #pragma unroll
   for (int k = 0; k < R; ++k) {
@@ -80,7 +88,12 @@ k_bcd_wnorm(float* __restrict__ W, float* __restrict__ Wp, int64_t m, int r, con
         Wp[i * r + k] = (float)((double)Wp[i * r + k] / ck);
       }
     }
+    mx = fmaxf(mx, v);
     Wn[threadIdx.x][k] = v;
+  }
+  if (maxw) {  // max W for the fp16x2 scale of the W^T X pass (order-independent)
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(maxw, __float_as_uint(mx));
   }
   __syncthreads();
   const int rr = r * r;
@@ -108,89 +121,316 @@ __global__ void k_bcd_hnorm(float* __restrict__ Hm, float* __restrict__ Hp, int 
 constexpr int BH_BN = 128;
 constexpr int BH_MCH = 128;
 
+// Spart[s][j][k] = sum_{i in rows of split s} W[i][k] X[i][j]; fp32 per 128-row chunk,
+// fp64 across chunks.  Grid: (column tiles, splits).
 template <int R>
 __global__ void __launch_bounds__(BH_BN)
-k_bcd_h(const float* __restrict__ X, int64_t ldx, int64_t m, int64_t n, const float* __restrict__ W, int r,
-        const double* __restrict__ G, const double* __restrict__ LH, const float* __restrict__ Hm,
-        float* __restrict__ H) {
+k_bcd_spart(const float* __restrict__ X, int64_t ldx, int64_t m, int64_t n, const float* __restrict__ W, int r,
+            int64_t rows_per_split, double* __restrict__ Spart) {
   __shared__ float Ws[BH_MCH * R];
+  const int64_t j = (int64_t)blockIdx.x * BH_BN + threadIdx.x;
+  const bool valid = j < n;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_split;
+  const int64_t r1 = min(m, r0 + rows_per_split);
+  double Sd[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) Sd[k] = 0.0;
+  for (int64_t c0 = r0; c0 < r1; c0 += BH_MCH) {
+    const int rows = (int)min((int64_t)BH_MCH, r1 - c0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < BH_MCH * R; e += blockDim.x) {
+      const int ii = e / R, kk = e % R;
+      Ws[e] = (ii < rows && kk < r) ? W[(c0 + ii) * r + kk] : 0.0f;
+    }
+    __syncthreads();
+    float S[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) S[k] = 0.0f;
+    if (valid)
+      for (int ii = 0; ii < rows; ++ii) {
+        const float x = X[(c0 + ii) * ldx + j];
+#pragma unroll
+        for (int k = 0; k < R; ++k) S[k] = fmaf(Ws[ii * R + k], x, S[k]);
+      }
+#pragma unroll
+    for (int k = 0; k < R; ++k) Sd[k] += (double)S[k];
+  }
+  if (valid) {
+    double* o = Spart + ((int64_t)blockIdx.y * n + j) * r;
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if (k < r) o[k] = Sd[k];
+  }
+}
+
+// H = max(0, H_m - (G H_m - S) / L_H) per column j, S = sum_s Spart[s][j][:] (fixed order).
+// The 128 columns of a block own a contiguous run of 128 r doubles in every split: each
+// thread sums fixed elements of that run over the splits (coalesced), then reads its column
+// back from shared memory.
+template <int R>
+__global__ void __launch_bounds__(BH_BN)
+k_bcd_hup(const double* __restrict__ Spart, int nS, int64_t n, int r, const double* __restrict__ G,
+          const double* __restrict__ LH, const float* __restrict__ Hm, float* __restrict__ H,
+          unsigned* __restrict__ maxh) {
   __shared__ double Gs[R * R];
+  __shared__ double Ss[BH_BN * R];
   for (int t = threadIdx.x; t < R * R; t += blockDim.x) {
     const int k = t / R, l = t % R;
     Gs[t] = (k < r && l < r) ? G[k * r + l] : 0.0;
   }
   const double L = *LH;
-  const int64_t ntiles = (n + BH_BN - 1) / BH_BN;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t j = tile * BH_BN + threadIdx.x;
-    const bool valid = j < n;
-    double Sd[R];
+  const int64_t nr = n * r;
+  float mx = 0.0f;
+  for (int64_t blk = blockIdx.x; blk * BH_BN < n; blk += gridDim.x) {
+    const int64_t j0 = blk * BH_BN;
+    const int cols = (int)min((int64_t)BH_BN, n - j0);
+    const int len = cols * r;
+    double acc[R];
 #pragma unroll
-    for (int k = 0; k < R; ++k) Sd[k] = 0.0;
-    for (int64_t c0 = 0; c0 < m; c0 += BH_MCH) {
-      const int rows = (int)min((int64_t)BH_MCH, m - c0);
-      __syncthreads();
-      for (int e = threadIdx.x; e < BH_MCH * R; e += blockDim.x) {
-        const int ii = e / R, kk = e % R;
-        Ws[e] = (ii < rows && kk < r) ? W[(c0 + ii) * r + kk] : 0.0f;
+    for (int q = 0; q < R; ++q) acc[q] = 0.0;
+    for (int b = 0; b < nS; ++b) {
+      const double* src = Spart + (int64_t)b * nr + j0 * r;
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int e = threadIdx.x + q * BH_BN;
+        if (e < len) acc[q] += src[e];
       }
-      __syncthreads();
-      float S[R];
-#pragma unroll
-      for (int k = 0; k < R; ++k) S[k] = 0.0f;
-      if (valid)
-        for (int ii = 0; ii < rows; ++ii) {
-          const float x = X[(c0 + ii) * ldx + j];
-#pragma unroll
-          for (int k = 0; k < R; ++k) S[k] = fmaf(Ws[ii * R + k], x, S[k]);
-        }
-#pragma unroll
-      for (int k = 0; k < R; ++k) Sd[k] += (double)S[k];
     }
-    if (valid) {
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int e = threadIdx.x + q * BH_BN;
+      if (e < len) Ss[e] = acc[q];
+    }
+    __syncthreads();
+    if (threadIdx.x < cols) {
+      const int64_t j = j0 + threadIdx.x;
       double hm[R];
 #pragma unroll
       for (int k = 0; k < R; ++k) hm[k] = (k < r) ? (double)Hm[(int64_t)k * n + j] : 0.0;
 #pragma unroll
       for (int k = 0; k < R; ++k) {
-        if (k >= r) continue;
-        double e = -Sd[k];
+        if (k < r) {
+          double e = -Ss[threadIdx.x * r + k];
 #pragma unroll
-        for (int l = 0; l < R; ++l) e += Gs[k * R + l] * hm[l];
-        const double v = L > 0.0 ? fmax(0.0, hm[k] - e / L) : hm[k];
-        H[(int64_t)k * n + j] = (float)v;
+          for (int l = 0; l < R; ++l) e += Gs[k * R + l] * hm[l];
+          const double v = L > 0.0 ? fmax(0.0, hm[k] - e / L) : hm[k];
+          const float vf = (float)v;
+          H[(int64_t)k * n + j] = vf;
+          mx = fmaxf(mx, vf);
+        }
       }
+    }
+  }
+  if (maxh) {
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(maxh, __float_as_uint(mx));
+  }
+}
+
+// P = sum_b Ppart[b] (fixed order) and the per-CTA partials of <W, P> (for the objective)
+__global__ void __launch_bounds__(256)
+k_bcd_psum_dot(const double* __restrict__ part, int nparts, int64_t len, const float* __restrict__ W,
+               double* __restrict__ P, double* __restrict__ dotpart) {
+  __shared__ double red[8];
+  double d = 0.0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < len; t += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nparts; ++b) s += part[(int64_t)b * len + t];
+    P[t] = s;
+    if (W) d += (double)W[t] * s;
+  }
+  if (!dotpart) return;
+  d = warp_sum(d);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = d;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    dotpart[blockIdx.x] = t;
+  }
+}
+
+// lambda_max of a symmetric PSD r x r matrix M (r <= 32; the Lipschitz constants of R23).
+// Repeated squaring A <- A^2 / max diag(A^2) drives A to the scaled projector onto the top
+// eigenspace (stopped when A no longer changes, at most 64 squarings = M^(2^64)); the Rayleigh
+// quotient of M on the column of A with the largest diagonal entry is then lambda_max with an
+// error quadratic in the eigenvector error.  One CTA of 1024 threads, thread (i, j) owns A[i][j].
+__global__ void __launch_bounds__(1024) k_spec_norm(const double* __restrict__ M, int r, double* __restrict__ out) {
+  __shared__ double A[32][33];
+  __shared__ double Ms[32][33];
+  __shared__ double red[32];
+  __shared__ double bc[2];
+  const int t = threadIdx.x, i = t >> 5, j = t & 31, lane = t & 31, w = t >> 5;
+  const bool in = i < r && j < r;
+  const double mv = in ? M[i * r + j] : 0.0;
+  Ms[i][j] = mv;
+  if (t < 32) red[t] = (t < r) ? M[t * r + t] : 0.0;
+  __syncthreads();
+  if (t < 32) {
+    double d = red[t];
+    for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+    if (t == 0) bc[0] = d;
+  }
+  __syncthreads();
+  const double d0 = bc[0];
+  if (!(d0 > 0.0)) {  // PSD with a zero diagonal: M = 0
+    if (t == 0) *out = 0.0;
+    return;
+  }
+  A[i][j] = mv / d0;
+  __syncthreads();
+  for (int it = 0; it < 64; ++it) {
+    double c = 0.0;
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) c += A[i][k] * A[k][j];
+    __syncthreads();
+    if (i == j) red[i] = c;
+    __syncthreads();
+    if (t < 32) {
+      double d = red[t];
+      for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+      if (t == 0) bc[0] = d;
+    }
+    __syncthreads();
+    const double an = c / bc[0];
+    double diff = fabs(an - A[i][j]);
+    A[i][j] = an;
+    for (int o = 16; o > 0; o >>= 1) diff = fmax(diff, __shfl_xor_sync(0xffffffffu, diff, o));
+    if (lane == 0) red[w] = diff;
+    __syncthreads();
+    if (t < 32) {
+      double d = red[t];
+      for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+      if (t == 0) bc[1] = d;
+    }
+    __syncthreads();
+    if (bc[1] <= 1e-15) break;
+  }
+  // column with the largest diagonal entry (lowest index on ties)
+  if (t < 32) {
+    double d = (t < r) ? A[t][t] : -1.0;
+    int idx = t;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, d, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (od > d || (od == d && oi < idx)) {
+        d = od;
+        idx = oi;
+      }
+    }
+    if (t == 0) bc[0] = (double)idx;
+  }
+  __syncthreads();
+  const int jc = (int)bc[0];
+  const double vi = A[i][jc], vj = A[j][jc];
+  double num = in ? vi * Ms[i][j] * vj : 0.0;
+  double den = (in && i == j) ? vi * vi : 0.0;
+  num = warp_sum(num);
+  den = warp_sum(den);
+  __syncthreads();
+  if (lane == 0) {
+    A[w][0] = num;
+    A[w][1] = den;
+  }
+  __syncthreads();
+  if (t == 0) {
+    double sn = 0.0, sd = 0.0;
+    for (int q = 0; q < 32; ++q) {
+      sn += A[q][0];
+      sd += A[q][1];
+    }
+    *out = sd > 0.0 ? sn / sd : 0.0;
+  }
+}
+
+// l.17-27 on the device: accept (extrapolate) or correct; trace[it] = accepted objective
+// (one warp) obj_new = 1/2 (||X||^2 - 2 <W, X H^T> + <W^T W, H H^T>) (Gram identity, R25) from
+// the <W, P> partials of k_bcd_psum_dot; then the branch; clears the two fp16 max slots
+__global__ void k_bcd_decide(double* __restrict__ bs, double* __restrict__ trace, const double* __restrict__ dotpart,
+                             int ndot, const double* __restrict__ G, const double* __restrict__ Q, int rr,
+                             unsigned* __restrict__ mxslots) {
+  double s1 = 0.0, s2 = 0.0;
+  for (int q = threadIdx.x; q < ndot; q += 32) s1 += dotpart[q];
+  for (int q = threadIdx.x; q < rr; q += 32) s2 += G[q] * Q[q];
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  if (threadIdx.x != 0) return;
+  if (mxslots) {
+    mxslots[0] = 0u;
+    mxslots[1] = 0u;
+  }
+  bs[BS_OBJNEW] = 0.5 * (bs[BS_XX] - 2.0 * s1 + s2);
+  const double obj_new = bs[BS_OBJNEW], obj = bs[BS_OBJ], t = bs[BS_T];
+  if (obj_new < obj) {
+    const double tp = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
+    const double w = (t - 1.0) / tp;
+    const double LW = bs[BS_LW], LH = bs[BS_LH], dl = bs[BS_DELTA];
+    bs[BS_WW] = fmin(w, dl * sqrt(bs[BS_LWP] / LW));  // fmin drops a NaN ratio (0/0) as min() does
+    bs[BS_WH] = fmin(w, dl * sqrt(bs[BS_LHP] / LH));
+    bs[BS_ACC] = 1.0;
+    bs[BS_LWP] = LW;
+    bs[BS_LHP] = LH;
+    bs[BS_T] = tp;
+    bs[BS_OBJ] = obj_new;
+  } else {
+    bs[BS_ACC] = 0.0;
+    bs[BS_T] = 1.0;
+  }
+  const int it = (int)bs[BS_IT];
+  if (trace) trace[it] = bs[BS_OBJ];
+  bs[BS_IT] = (double)(it + 1);
+}
+
+// accepted: V_m = V + w (V - V_prev), V_prev = V;  correction: V_m = V_prev
+__global__ void k_bcd_commit(const float* __restrict__ V, float* __restrict__ Vm, float* __restrict__ Vp, int64_t cnt,
+                             const double* __restrict__ bs, int widx) {
+  const bool acc = bs[BS_ACC] != 0.0;
+  const double w = bs[widx];
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += (int64_t)gridDim.x * blockDim.x) {
+    if (acc) {
+      const double v = V[e], vp = Vp[e];
+      Vm[e] = (float)(v + w * (v - vp));
+      Vp[e] = (float)v;
+    } else {
+      Vm[e] = Vp[e];
     }
   }
 }
 
-// out[0] = 1/2 (xx - 2 <W, P> + <G, Q>) with W fp32 m x r, P fp64 m x r, G, Q fp64 r x r
-__global__ void k_bcd_obj(double xx, const float* __restrict__ W, const double* __restrict__ P, int64_t m, int r,
-                          const double* __restrict__ G, const double* __restrict__ Q, double* __restrict__ out) {
-  __shared__ double red[32];
-  double s = 0.0;
-  for (int64_t e = threadIdx.x; e < m * r; e += blockDim.x) s += (double)W[e] * P[e];
-  double g = 0.0;
-  for (int e = threadIdx.x; e < r * r; e += blockDim.x) g += G[e] * Q[e];
-  double v = -2.0 * s + g;
-  v = warp_sum(v);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    out[0] = 0.5 * (xx + t);
+// accepted: P = X H^T, Q = H H^T of the new H (Pn, Qn).  Correction: H_prev was rescaled
+// by c in l.9 (rows k x c_k), so X H_prev^T = P diag(c) and H_prev H_prev^T = diag(c) Q diag(c)
+// (R26: the same matrices the oracle recomputes from H_prev, without another pass over X)
+__global__ void k_bcd_commit_pq(double* __restrict__ Pc, const double* __restrict__ Pn, int64_t m, int r,
+                                double* __restrict__ Qc, const double* __restrict__ Qn, const double* __restrict__ c,
+                                const double* __restrict__ bs) {
+  const bool acc = bs[BS_ACC] != 0.0;
+  const int64_t mr = m * r, tot = mr + (int64_t)r * r;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < mr) {
+      const int k = (int)(e % r);
+      if (acc) Pc[e] = Pn[e];
+      else if (c[k] > 0.0) Pc[e] *= c[k];
+    } else {
+      const int64_t q = e - mr;
+      const int k = (int)(q / r), l = (int)(q % r);
+      if (acc) Qc[q] = Qn[q];
+      else Qc[q] *= (c[k] > 0.0 ? c[k] : 1.0) * (c[l] > 0.0 ? c[l] : 1.0);
+    }
   }
 }
 
-__global__ void k_bcd_extrap(float* __restrict__ V, float* __restrict__ Vm, float* __restrict__ Vp, int64_t cnt,
-                             double w) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += (int64_t)gridDim.x * blockDim.x) {
-    const double v = V[e], vp = Vp[e];
-    Vm[e] = (float)(v + w * (v - vp));
-    Vp[e] = (float)v;
-  }
+__global__ void k_bcd_init(double* __restrict__ bs, double delta) {
+  if (threadIdx.x != 0) return;
+  bs[BS_OBJ] = 0.5 * bs[BS_XX];
+  bs[BS_T] = 1.0;
+  bs[BS_LWP] = bs[BS_LW];
+  bs[BS_LHP] = bs[BS_LH];
+  bs[BS_DELTA] = delta;
+  bs[BS_IT] = 0.0;
+  bs[BS_ACC] = 0.0;
 }
+
 
 __global__ void k_scale_copy(const float* __restrict__ src, float* __restrict__ a, float* __restrict__ b, int64_t cnt,
                              const double* __restrict__ num, const double* __restrict__ den) {
@@ -242,13 +482,14 @@ cudaError_t launch_bcd_w(const float* Wm, int64_t m, int r, const double* P, con
   return cudaGetLastError();
 }
 
-cudaError_t launch_bcd_wnorm(float* W, float* Wp, int64_t m, int r, const double* c, double* Gpart, cudaStream_t st) {
+cudaError_t launch_bcd_wnorm(float* W, float* Wp, int64_t m, int r, const double* c, double* Gpart, unsigned* maxw,
+                             cudaStream_t st) {
   const unsigned g = (unsigned)bcd_w_ctas(m);
   switch (rcls_bcd(r)) {
-    case 4: k_bcd_wnorm<4><<<g, BROWS, 0, st>>>(W, Wp, m, r, c, Gpart); break;
-    case 8: k_bcd_wnorm<8><<<g, BROWS, 0, st>>>(W, Wp, m, r, c, Gpart); break;
-    case 16: k_bcd_wnorm<16><<<g, BROWS, 0, st>>>(W, Wp, m, r, c, Gpart); break;
-    default: k_bcd_wnorm<32><<<g, BROWS, 0, st>>>(W, Wp, m, r, c, Gpart); break;
+    case 4: k_bcd_wnorm<4><<<g, BROWS, 0, st>>>(W, Wp, m, r, c, Gpart, maxw); break;
+    case 8: k_bcd_wnorm<8><<<g, BROWS, 0, st>>>(W, Wp, m, r, c, Gpart, maxw); break;
+    case 16: k_bcd_wnorm<16><<<g, BROWS, 0, st>>>(W, Wp, m, r, c, Gpart, maxw); break;
+    default: k_bcd_wnorm<32><<<g, BROWS, 0, st>>>(W, Wp, m, r, c, Gpart, maxw); break;
   }
   return cudaGetLastError();
 }
@@ -258,27 +499,80 @@ cudaError_t launch_bcd_hnorm(float* Hm, float* Hp, int r, int64_t n, const doubl
   return cudaGetLastError();
 }
 
-cudaError_t launch_bcd_h(const float* X, int64_t ldx, int64_t m, int64_t n, const float* W, int r, const double* G,
-                         const double* LH, const float* Hm, float* H, int num_sms, cudaStream_t st) {
-  int64_t g = (n + BH_BN - 1) / BH_BN;
-  if (g > 8 * num_sms) g = 8 * num_sms;
+int bcd_spart_splits(int64_t m, int64_t n, int num_sms) {
+  const int64_t tiles = (n + BH_BN - 1) / BH_BN, chunks = (m + BH_MCH - 1) / BH_MCH;
+  int64_t s = (4 * (int64_t)num_sms + tiles - 1) / tiles;  // >= 4 CTAs of 128 threads per SM
+  s = std::max<int64_t>(1, std::min<int64_t>(s, chunks));
+  return (int)std::min<int64_t>(s, 64);
+}
+
+cudaError_t launch_bcd_spart(const float* X, int64_t ldx, int64_t m, int64_t n, const float* W, int r, int nsplit,
+                             double* Spart, cudaStream_t st) {
+  const int64_t chunks = (m + BH_MCH - 1) / BH_MCH;
+  const int64_t rps = ((chunks + nsplit - 1) / nsplit) * BH_MCH;
+  const dim3 g((unsigned)((n + BH_BN - 1) / BH_BN), (unsigned)nsplit);
   switch (rcls_bcd(r)) {
-    case 4: k_bcd_h<4><<<(unsigned)g, BH_BN, 0, st>>>(X, ldx, m, n, W, r, G, LH, Hm, H); break;
-    case 8: k_bcd_h<8><<<(unsigned)g, BH_BN, 0, st>>>(X, ldx, m, n, W, r, G, LH, Hm, H); break;
-    case 16: k_bcd_h<16><<<(unsigned)g, BH_BN, 0, st>>>(X, ldx, m, n, W, r, G, LH, Hm, H); break;
-    default: k_bcd_h<32><<<(unsigned)g, BH_BN, 0, st>>>(X, ldx, m, n, W, r, G, LH, Hm, H); break;
+    case 4: k_bcd_spart<4><<<g, BH_BN, 0, st>>>(X, ldx, m, n, W, r, rps, Spart); break;
+    case 8: k_bcd_spart<8><<<g, BH_BN, 0, st>>>(X, ldx, m, n, W, r, rps, Spart); break;
+    case 16: k_bcd_spart<16><<<g, BH_BN, 0, st>>>(X, ldx, m, n, W, r, rps, Spart); break;
+    default: k_bcd_spart<32><<<g, BH_BN, 0, st>>>(X, ldx, m, n, W, r, rps, Spart); break;
   }
   return cudaGetLastError();
 }
 
-cudaError_t launch_bcd_obj(double xx, const float* W, const double* P, int64_t m, int r, const double* G,
-                           const double* Q, double* out, cudaStream_t st) {
-  k_bcd_obj<<<1, 1024, 0, st>>>(xx, W, P, m, r, G, Q, out);
+cudaError_t launch_bcd_hup(const double* Spart, int nS, int64_t n, int r, const double* G, const double* LH,
+                           const float* Hm, float* H, unsigned* maxh, int num_sms, cudaStream_t st) {
+  int64_t g = (n + BH_BN - 1) / BH_BN;
+  if (g > 4 * num_sms) g = 4 * num_sms;
+  switch (rcls_bcd(r)) {
+    case 4: k_bcd_hup<4><<<(unsigned)g, BH_BN, 0, st>>>(Spart, nS, n, r, G, LH, Hm, H, maxh); break;
+    case 8: k_bcd_hup<8><<<(unsigned)g, BH_BN, 0, st>>>(Spart, nS, n, r, G, LH, Hm, H, maxh); break;
+    case 16: k_bcd_hup<16><<<(unsigned)g, BH_BN, 0, st>>>(Spart, nS, n, r, G, LH, Hm, H, maxh); break;
+    default: k_bcd_hup<32><<<(unsigned)g, BH_BN, 0, st>>>(Spart, nS, n, r, G, LH, Hm, H, maxh); break;
+  }
   return cudaGetLastError();
 }
 
-cudaError_t launch_bcd_extrap(float* V, float* Vm, float* Vp, int64_t cnt, double w, cudaStream_t st) {
-  k_bcd_extrap<<<1184, 256, 0, st>>>(V, Vm, Vp, cnt, w);
+int bcd_dot_ctas(int64_t len, int num_sms) {
+  const int64_t g = (len + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 2 * (int64_t)num_sms));
+}
+
+cudaError_t launch_bcd_psum_dot(const double* part, int nparts, int64_t len, const float* W, double* P,
+                                double* dotpart, int num_sms, cudaStream_t st) {
+  k_bcd_psum_dot<<<(unsigned)bcd_dot_ctas(len, num_sms), 256, 0, st>>>(part, nparts, len, W, P, dotpart);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spec_norm(const double* M, int r, double* out, cudaStream_t st) {
+  if (r > 32) return cudaErrorInvalidValue;
+  k_spec_norm<<<1, 1024, 0, st>>>(M, r, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bcd_init(double* bs, double delta, cudaStream_t st) {
+  k_bcd_init<<<1, 32, 0, st>>>(bs, delta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bcd_decide(double* bs, double* trace, const double* dotpart, int ndot, const double* G,
+                              const double* Q, int r, unsigned* mxslots, cudaStream_t st) {
+  k_bcd_decide<<<1, 32, 0, st>>>(bs, trace, dotpart, ndot, G, Q, r * r, mxslots);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bcd_commit(const float* V, float* Vm, float* Vp, int64_t cnt, const double* bs, int widx,
+                              cudaStream_t st) {
+  const int64_t g = std::min<int64_t>(1184, (cnt + 255) / 256);
+  k_bcd_commit<<<(unsigned)std::max<int64_t>(g, 1), 256, 0, st>>>(V, Vm, Vp, cnt, bs, widx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bcd_commit_pq(double* Pc, const double* Pn, int64_t m, int r, double* Qc, const double* Qn,
+                                 const double* c, const double* bs, cudaStream_t st) {
+  const int64_t tot = m * r + (int64_t)r * r;
+  const int64_t g = std::min<int64_t>(1184, (tot + 255) / 256);
+  k_bcd_commit_pq<<<(unsigned)g, 256, 0, st>>>(Pc, Pn, m, r, Qc, Qn, c, bs);
   return cudaGetLastError();
 }
 

@@ -51,17 +51,47 @@ cudaError_t launch_rank_rule(const float* X, int64_t m, int64_t n, int64_t ldx, 
 
 cudaError_t launch_sym_eig(double* C, int N, double* scratch, double* eig, int* rank_dummy, cudaStream_t st);
 
-// BCD NMF building blocks (bcd.cu, Alg. 3)
+// BCD NMF building blocks (bcd.cu, Alg. 3).  Device state block (doubles):
+enum BcdState {
+  BS_XX = 0,      // ||X||_F^2
+  BS_W0 = 1,      // ||W0||_F^2
+  BS_H0 = 2,      // ||H0||_F^2
+  BS_LW = 3,      // L_W of this iteration (||H_prev H_prev^T||_2)
+  BS_LH = 4,      // L_H of this iteration (||W^T W||_2)
+  BS_OBJNEW = 5,  // objective of the candidate (W, H)
+  BS_OBJ = 6,     // last accepted objective
+  BS_T = 7,       // extrapolation t
+  BS_LWP = 8,     // L_W, L_H of the last accepted iteration
+  BS_LHP = 9,
+  BS_ACC = 10,    // 1 = accepted (extrapolation), 0 = correction
+  BS_WW = 11,     // extrapolation weights w_W, w_H
+  BS_WH = 12,
+  BS_IT = 13,     // iteration counter (trace index)
+  BS_DELTA = 14,
+  BS_COUNT = 16
+};
 int bcd_w_ctas(int64_t m);
 cudaError_t launch_bcd_w(const float* Wm, int64_t m, int r, const double* P, const double* Q, const double* LW,
                          float* W, double* cpart, cudaStream_t st);
-cudaError_t launch_bcd_wnorm(float* W, float* Wp, int64_t m, int r, const double* c, double* Gpart, cudaStream_t st);
+cudaError_t launch_bcd_wnorm(float* W, float* Wp, int64_t m, int r, const double* c, double* Gpart, unsigned* maxw,
+                             cudaStream_t st);
 cudaError_t launch_bcd_hnorm(float* Hm, float* Hp, int r, int64_t n, const double* c, cudaStream_t st);
-cudaError_t launch_bcd_h(const float* X, int64_t ldx, int64_t m, int64_t n, const float* W, int r, const double* G,
-                         const double* LH, const float* Hm, float* H, int num_sms, cudaStream_t st);
-cudaError_t launch_bcd_obj(double xx, const float* W, const double* P, int64_t m, int r, const double* G,
-                           const double* Q, double* out, cudaStream_t st);
-cudaError_t launch_bcd_extrap(float* V, float* Vm, float* Vp, int64_t cnt, double w, cudaStream_t st);
+int bcd_spart_splits(int64_t m, int64_t n, int num_sms);
+cudaError_t launch_bcd_spart(const float* X, int64_t ldx, int64_t m, int64_t n, const float* W, int r, int nsplit,
+                             double* Spart, cudaStream_t st);
+cudaError_t launch_bcd_hup(const double* Spart, int nS, int64_t n, int r, const double* G, const double* LH,
+                           const float* Hm, float* H, unsigned* maxh, int num_sms, cudaStream_t st);
+int bcd_dot_ctas(int64_t len, int num_sms);
+cudaError_t launch_bcd_psum_dot(const double* part, int nparts, int64_t len, const float* W, double* P,
+                                double* dotpart, int num_sms, cudaStream_t st);
+cudaError_t launch_spec_norm(const double* M, int r, double* out, cudaStream_t st);
+cudaError_t launch_bcd_init(double* bs, double delta, cudaStream_t st);
+cudaError_t launch_bcd_decide(double* bs, double* trace, const double* dotpart, int ndot, const double* G,
+                              const double* Q, int r, unsigned* mxslots, cudaStream_t st);
+cudaError_t launch_bcd_commit(const float* V, float* Vm, float* Vp, int64_t cnt, const double* bs, int widx,
+                              cudaStream_t st);
+cudaError_t launch_bcd_commit_pq(double* Pc, const double* Pn, int64_t m, int r, double* Qc, const double* Qn,
+                                 const double* c, const double* bs, cudaStream_t st);
 cudaError_t launch_scale_copy(const float* src, float* a, float* b, int64_t cnt, const double* num, const double* den,
                               cudaStream_t st);
 int sumsq_ctas();

@@ -382,7 +382,22 @@ __global__ void k_sum_partials(const double* __restrict__ part, int nparts, int6
   }
 }
 
+// few outputs, many partials: one warp per output, lanes take every 32nd partial, then a fixed
+// shuffle tree (deterministic; avoids a serial chain of nparts dependent-latency loads)
+__global__ void k_sum_partials_warp(const double* __restrict__ part, int nparts, int64_t len, double* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= len) return;
+  double s = 0.0;
+  for (int b = threadIdx.x & 31; b < nparts; b += 32) s += part[(int64_t)b * len + t];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) out[t] = s;
+}
+
 cudaError_t launch_sum_partials(const double* part, int nparts, int64_t len, double* out, cudaStream_t st) {
+  if (nparts >= 8 && len <= 4096) {
+    k_sum_partials_warp<<<(unsigned)((len + 7) / 8), 256, 0, st>>>(part, nparts, len, out);
+    return cudaGetLastError();
+  }
   int64_t g = (len + 255) / 256;
   if (g > 1184) g = 1184;
   if (g < 1) g = 1;

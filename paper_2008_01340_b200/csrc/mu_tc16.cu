@@ -373,12 +373,12 @@ int t16_stages() {
 template <int R, int MODE>
 cudaError_t launch16(const CUtensorMap& ma, const CUtensorMap& mb, int64_t Mtot, int64_t ktiles, int nsplit,
                      int64_t kchunk, int grid, int r, double* part, const float* scales, int sidx, int ef,
-                     cudaStream_t st) {
+                     cudaStream_t st, int flush) {
   const int ns = t16_stages<R>();
   const size_t sm = (size_t)ns * T16Cfg<R>::SB + 2048;
   cudaError_t e = cudaFuncSetAttribute(k_skinny_tc16<R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  k_skinny_tc16<R, MODE><<<grid, T16_THREADS, sm, st>>>(ma, mb, Mtot, ktiles, nsplit, kchunk, ns, 16, r, part,
+  k_skinny_tc16<R, MODE><<<grid, T16_THREADS, sm, st>>>(ma, mb, Mtot, ktiles, nsplit, kchunk, ns, flush, r, part,
                                                         scales, sidx, ef);
   return cudaGetLastError();
 }
@@ -430,20 +430,56 @@ cudaError_t tc16_pack_w(const TcPlan& p, const float* W, char* ws, cudaStream_t 
   return cudaGetLastError();
 }
 
-cudaError_t tc16_pass_w(const TcPlan& p, const TcMaps& mp, char* ws, int ef, cudaStream_t st) {
+// BCD (bcd.cu) slots: 5 = max H (k_bcd_hup), 6 = max W (k_bcd_wnorm), both cleared by
+// k_bcd_decide; 7 = the self-contained "fresh" packs below; 4 = a reset target nobody reads
+// while BCD runs (the MU W slot, unused there).
+unsigned* tc16_max_slot(const TcPlan& p, char* ws, int slot) {
+  return reinterpret_cast<unsigned*>(ws + p.off_scales + 64) + slot;
+}
+
+cudaError_t tc16_pack_h_slot(const TcPlan& p, const float* H, char* ws, cudaStream_t st, int slot) {
+  k_pack16<<<4 * p.grid, 256, 0, st>>>(H, p.r, p.n, false, p.R, tc16_max_slot(p, ws, slot),
+                                       reinterpret_cast<__half*>(ws + p.off_h16), p.ldh16,
+                                       reinterpret_cast<float*>(ws + p.off_scales), 1, tc16_max_slot(p, ws, 4));
+  return cudaGetLastError();
+}
+
+cudaError_t tc16_pack_w_slot(const TcPlan& p, const float* W, char* ws, cudaStream_t st, int slot) {
+  k_pack16<<<4 * p.grid, 256, 0, st>>>(W, p.r, p.m, true, p.R, tc16_max_slot(p, ws, slot),
+                                       reinterpret_cast<__half*>(ws + p.off_w16), p.ldw16,
+                                       reinterpret_cast<float*>(ws + p.off_scales), 2, tc16_max_slot(p, ws, 4));
+  return cudaGetLastError();
+}
+
+// fp16 parts of an arbitrary factor with its max computed here (slot 7, cleared first)
+cudaError_t tc16_pack_h_fresh(const TcPlan& p, const float* H, char* ws, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(tc16_max_slot(p, ws, 7), 0, sizeof(unsigned), st);
+  if (e) return e;
+  k_absmax<<<2 * p.grid, 256, 0, st>>>(H, 1, (int64_t)p.r * p.n, (int64_t)p.r * p.n, tc16_max_slot(p, ws, 7));
+  return tc16_pack_h_slot(p, H, ws, st, 7);
+}
+
+cudaError_t tc16_pack_w_fresh(const TcPlan& p, const float* W, char* ws, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(tc16_max_slot(p, ws, 7), 0, sizeof(unsigned), st);
+  if (e) return e;
+  k_absmax<<<2 * p.grid, 256, 0, st>>>(W, 1, p.m * p.r, p.m * p.r, tc16_max_slot(p, ws, 7));
+  return tc16_pack_w_slot(p, W, ws, st, 7);
+}
+
+cudaError_t tc16_pass_w(const TcPlan& p, const TcMaps& mp, char* ws, int ef, cudaStream_t st, int flush) {
   double* P = reinterpret_cast<double*>(ws + p.off_P);
   const float* sc = reinterpret_cast<const float*>(ws + p.off_scales);
   const int64_t kt = (p.n + T16_BK - 1) / T16_BK;
-  if (p.R == 16) return launch16<16, 0>(mp.xw16, mp.hcat16, p.m, kt, p.splitW16, p.kchW16, p.grid, p.r, P, sc, 1, ef, st);
-  return launch16<32, 0>(mp.xw16, mp.hcat16, p.m, kt, p.splitW16, p.kchW16, p.grid, p.r, P, sc, 1, ef, st);
+  if (p.R == 16) return launch16<16, 0>(mp.xw16, mp.hcat16, p.m, kt, p.splitW16, p.kchW16, p.grid, p.r, P, sc, 1, ef, st, flush);
+  return launch16<32, 0>(mp.xw16, mp.hcat16, p.m, kt, p.splitW16, p.kchW16, p.grid, p.r, P, sc, 1, ef, st, flush);
 }
 
-cudaError_t tc16_pass_h(const TcPlan& p, const TcMaps& mp, char* ws, int ef, cudaStream_t st) {
+cudaError_t tc16_pass_h(const TcPlan& p, const TcMaps& mp, char* ws, int ef, cudaStream_t st, int flush) {
   double* S = reinterpret_cast<double*>(ws + p.off_S);
   const float* sc = reinterpret_cast<const float*>(ws + p.off_scales);
   const int64_t kt = (p.m + T16_BK - 1) / T16_BK;
-  if (p.R == 16) return launch16<16, 1>(mp.xh16, mp.wcat16, p.n, kt, p.splitH16, p.kchH16, p.grid, p.r, S, sc, 2, ef, st);
-  return launch16<32, 1>(mp.xh16, mp.wcat16, p.n, kt, p.splitH16, p.kchH16, p.grid, p.r, S, sc, 2, ef, st);
+  if (p.R == 16) return launch16<16, 1>(mp.xh16, mp.wcat16, p.n, kt, p.splitH16, p.kchH16, p.grid, p.r, S, sc, 2, ef, st, flush);
+  return launch16<32, 1>(mp.xh16, mp.wcat16, p.n, kt, p.splitH16, p.kchH16, p.grid, p.r, S, sc, 2, ef, st, flush);
 }
 
 }  // namespace ntt

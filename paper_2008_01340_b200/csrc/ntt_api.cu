@@ -1093,6 +1093,12 @@ ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t*
   return NTT_OK;
 }
 
+// BCD NMF (Alg. 3, readings R22-R27).  Every branch of the iteration is decided on the
+// device (bcd.cu, state block BcdState), so one iteration is a fixed launch sequence:
+// captured once into a CUDA graph and replayed `iters` times (NTT_BCD_GRAPH=0: eager).
+// The two passes over X per iteration (S = W^T X for the H step, P = X H^T for the
+// objective and the next W step) run on the fp16x2 tensor-core kernels of the MU path
+// where those take the shape (mu_tc16.cu), else on FFMA kernels.
 ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64_t ldx, int32_t r, int32_t iters,
                        double delta, float* W, float* H, double* objective_trace) {
   if (!h) return NTT_ERR_INVALID_ARG;
@@ -1107,8 +1113,15 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
     return fail(h, NTT_ERR_INVALID_ARG, "ntt_nmf_bcd takes device buffers");
   CU(h, cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
+  bool tc = tc_supported(m, n, r, ldx, X) && !getenv("NTT_NO_TC");
+  TcPlan tp;
+  if (tc) {
+    tp = plan_tc(m, n, r, h->num_sms);
+    tc = tp.f16;
+  }
   const XhtPlan xp = plan_xht(m, n, h->num_sms), qp = plan_xht(r, n, h->num_sms);
   const int nwc = bcd_w_ctas(m);
+  const int nS = tc ? tp.splitH16 : bcd_spart_splits(m, n, h->num_sms);
   size_t o = 0;
   auto take = [&](size_t b) {
     size_t at = o;
@@ -1120,10 +1133,14 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   const size_t oP0 = take(sizeof(double) * m * r), oP1 = take(sizeof(double) * m * r);
   const size_t oQ0 = take(sizeof(double) * r * r), oQ1 = take(sizeof(double) * r * r);
   const size_t oG = take(sizeof(double) * r * r), oC = take(sizeof(double) * r);
-  const size_t oPp = take(sizeof(double) * (size_t)xp.ncs * m * r), oQp = take(sizeof(double) * (size_t)qp.ncs * r * r);
+  const size_t oPp = tc ? 0 : take(sizeof(double) * (size_t)xp.ncs * m * r);
+  const size_t oSp = tc ? 0 : take(sizeof(double) * (size_t)nS * n * r);
+  const size_t oQp = take(sizeof(double) * (size_t)qp.ncs * r * r);
   const size_t oCp = take(sizeof(double) * (size_t)nwc * r), oGp = take(sizeof(double) * (size_t)nwc * r * r);
-  const size_t oE = take(sizeof(double) * (r * r + 3 * r + 8)), oSq = take(sizeof(double) * sumsq_ctas());
-  const size_t oSc = take(sizeof(double) * 16);
+  const int ndot = bcd_dot_ctas(m * r, h->num_sms);
+  const size_t oD = take(sizeof(double) * ndot), oSq = take(sizeof(double) * sumsq_ctas());
+  const size_t oBs = take(sizeof(double) * BS_COUNT), oTr = take(sizeof(double) * std::max(iters, 1));
+  const size_t oTc = tc ? take(tp.bytes) : 0;
   ntt_status s = ensure_ws(h, o);
   if (s) return s;
   char* ws = reinterpret_cast<char*>(h->ws);
@@ -1131,94 +1148,140 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   float* Wp = reinterpret_cast<float*>(ws + oWp);
   float* Hm = reinterpret_cast<float*>(ws + oHm);
   float* Hp = reinterpret_cast<float*>(ws + oHp);
-  double* Pc = reinterpret_cast<double*>(ws + oP0);  // X H_prev^T of the accepted H
-  double* Pn = reinterpret_cast<double*>(ws + oP1);
+  double* Pc = reinterpret_cast<double*>(ws + oP0);  // X H_prev^T, H_prev H_prev^T (accepted H)
+  double* Pn = reinterpret_cast<double*>(ws + oP1);  // the same for the candidate H
   double* Qc = reinterpret_cast<double*>(ws + oQ0);
   double* Qn = reinterpret_cast<double*>(ws + oQ1);
   double* G = reinterpret_cast<double*>(ws + oG);
   double* c = reinterpret_cast<double*>(ws + oC);
-  double* Ppart = reinterpret_cast<double*>(ws + oPp);
   double* Qpart = reinterpret_cast<double*>(ws + oQp);
   double* cpart = reinterpret_cast<double*>(ws + oCp);
   double* Gpart = reinterpret_cast<double*>(ws + oGp);
-  double* E = reinterpret_cast<double*>(ws + oE);     // eigen scratch: [C r*r][v, p 2r][eig r][rank int]
+  double* dotpart = reinterpret_cast<double*>(ws + oD);  // per-CTA partials of <W, X H^T>
   double* sq = reinterpret_cast<double*>(ws + oSq);
-  double* sc = reinterpret_cast<double*>(ws + oSc);   // [0] ||X||^2 [1] ||W0||^2 [2] ||H0||^2 [3] L_W [4] L_H [5] obj
-  int* rk_dummy = reinterpret_cast<int*>(E + r * r + 3 * r);
+  double* bs = reinterpret_cast<double*>(ws + oBs);
+  double* dtrace = reinterpret_cast<double*>(ws + oTr);
+  char* tws = ws + oTc;
+  double* Ppart = tc ? reinterpret_cast<double*>(tws + tp.off_P) : reinterpret_cast<double*>(ws + oPp);
+  double* Spart = tc ? reinterpret_cast<double*>(tws + tp.off_S) : reinterpret_cast<double*>(ws + oSp);
+  const int nP = tc ? tp.splitW16 : xp.ncs;
+  TcMaps maps;
+  unsigned* mxh = tc ? tc16_max_slot(tp, tws, 5) : nullptr;  // max H, then max W (slot 6)
+  unsigned* mxw = tc ? tc16_max_slot(tp, tws, 6) : nullptr;
+  const double xbytes = 4.0 * (double)m * (double)n;
+  const char* fe = getenv("NTT_BCD_FLUSH");
+  const int bflush = fe ? std::max(1, atoi(fe)) : 4;
+  const int bef = (double)m * (double)ldx * 4.0 > 0.6 * (double)h->l2_bytes ? 1 : 0;  // X > L2: evict-first
   auto spec = [&](const double* M, double* out) -> ntt_status {  // spectral norm of an r x r Gram
-    CU(h, cudaMemcpyAsync(E, M, sizeof(double) * r * r, cudaMemcpyDeviceToDevice, st));
-    LAUNCH(h, launch_sym_eig(E, r, E + r * r, E + r * r + 2 * r, rk_dummy, st));
-    LAUNCH(h, launch_copy_last(E + r * r + 2 * r, r, out, st));
+    LAUNCH(h, launch_spec_norm(M, r, out, st));
     return NTT_OK;
   };
-  auto xht_pq = [&](const float* Hs, double* P, double* Q) -> ntt_status {  // P = X H^T, Q = H H^T
-    LAUNCH(h, launch_xht_partial(X, ldx, m, n, Hs, n, r, xp, Ppart, st));
-    LAUNCH(h, launch_sum_partials(Ppart, xp.ncs, m * r, P, st));
+  // P = X H^T, Q = H H^T; in the iteration also the <W, P> partials of the objective, and
+  // the fp16 scale of H from the max k_bcd_hup left in slot 5
+  auto pq = [&](const float* Hs, double* P, double* Q, bool in_iter) -> ntt_status {
+    if (tc) {
+      if (in_iter) LAUNCH(h, tc16_pack_h_slot(tp, Hs, tws, st, 5));
+      else LAUNCH(h, tc16_pack_h_fresh(tp, Hs, tws, st));
+      PLAUNCH(h, 6, xbytes, tc16_pass_w(tp, maps, tws, bef, st, bflush));
+    } else {
+      PLAUNCH(h, 1, xbytes, launch_xht_partial(X, ldx, m, n, Hs, n, r, xp, Ppart, st));
+    }
+    LAUNCH(h, launch_bcd_psum_dot(Ppart, nP, m * r, in_iter ? W : nullptr, P, in_iter ? dotpart : nullptr,
+                                  h->num_sms, st));
     LAUNCH(h, launch_xht_partial(Hs, n, r, n, Hs, n, r, qp, Qpart, st));
     LAUNCH(h, launch_sum_partials(Qpart, qp.ncs, (int64_t)r * r, Q, st));
     return NTT_OK;
   };
-  // ---- init (Alg. 3 l.1-4, R22, R25)
+  // ---- init (Alg. 3 l.1-4, R22, R23)
+  CU(h, cudaMemsetAsync(bs, 0, sizeof(double) * BS_COUNT, st));
   LAUNCH(h, launch_sumsq(X, m, n, ldx, sq, st));
-  LAUNCH(h, launch_sum_partials(sq, sumsq_ctas(), 1, sc + 0, st));
+  LAUNCH(h, launch_sum_partials(sq, sumsq_ctas(), 1, bs + BS_XX, st));
   LAUNCH(h, launch_sumsq(W, m, r, r, sq, st));
-  LAUNCH(h, launch_sum_partials(sq, sumsq_ctas(), 1, sc + 1, st));
+  LAUNCH(h, launch_sum_partials(sq, sumsq_ctas(), 1, bs + BS_W0, st));
   LAUNCH(h, launch_sumsq(H, r, n, n, sq, st));
-  LAUNCH(h, launch_sum_partials(sq, sumsq_ctas(), 1, sc + 2, st));
-  LAUNCH(h, launch_scale_copy(W, Wm, Wp, m * r, sc + 0, sc + 1, st));
-  LAUNCH(h, launch_scale_copy(H, Hm, Hp, (int64_t)r * n, sc + 0, sc + 2, st));
-  if ((s = xht_pq(Hp, Pc, Qc))) return s;
-  LAUNCH(h, launch_bcd_wnorm(Wp, Wp, m, r, nullptr, Gpart, st));  // G of W_prev (no normalisation)
-  LAUNCH(h, launch_sum_partials(Gpart, nwc, (int64_t)r * r, G, st));
-  if ((s = spec(Qc, sc + 3))) return s;
-  if ((s = spec(G, sc + 4))) return s;
-  double hs[6];
-  CU(h, cudaMemcpyAsync(hs, sc, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  LAUNCH(h, launch_sum_partials(sq, sumsq_ctas(), 1, bs + BS_H0, st));
+  double xx = 0.0;
+  CU(h, cudaMemcpyAsync(&xx, bs + BS_XX, sizeof(double), cudaMemcpyDeviceToHost, st));
   CU(h, cudaStreamSynchronize(st));
-  const double xx = hs[0];
   if (!(xx > 0.0)) return fail(h, NTT_ERR_DEGENERATE, "||X|| = 0");
-  double LWp = hs[3], LHp = hs[4], t = 1.0, obj = 0.5 * xx;
-  for (int it = 0; it < iters; ++it) {
-    // W step (l.6-8), column L1 normalisation with compensation (l.9, R24), G and L_H (l.10)
-    if ((s = spec(Qc, sc + 3))) return s;
-    LAUNCH(h, launch_bcd_w(Wm, m, r, Pc, Qc, sc + 3, W, cpart, st));
-    LAUNCH(h, launch_sum_partials(cpart, nwc, r, c, st));
-    LAUNCH(h, launch_bcd_wnorm(W, Wp, m, r, c, Gpart, st));
-    LAUNCH(h, launch_bcd_hnorm(Hm, Hp, r, n, c, st));
-    LAUNCH(h, launch_sum_partials(Gpart, nwc, (int64_t)r * r, G, st));
-    if ((s = spec(G, sc + 4))) return s;
-    // H step (l.11-14), then X H^T, H H^T and the objective of the candidate (l.15-16)
-    LAUNCH(h, launch_bcd_h(X, ldx, m, n, W, r, G, sc + 4, Hm, H, h->num_sms, st));
-    if ((s = xht_pq(H, Pn, Qn))) return s;
-    LAUNCH(h, launch_bcd_obj(xx, W, Pn, m, r, G, Qn, sc + 5, st));
-    CU(h, cudaMemcpyAsync(hs, sc, sizeof(hs), cudaMemcpyDeviceToHost, st));
-    CU(h, cudaStreamSynchronize(st));
-    const double LW = hs[3], LH = hs[4], obj_new = hs[5];
-    if (obj_new >= obj) {
-      // correction (l.17-20, R26): back to the last accepted iterates, no extrapolation
-      CU(h, cudaMemcpyAsync(Wm, Wp, sizeof(float) * m * r, cudaMemcpyDeviceToDevice, st));
-      CU(h, cudaMemcpyAsync(Hm, Hp, sizeof(float) * r * n, cudaMemcpyDeviceToDevice, st));
-      t = 1.0;
-      if ((s = xht_pq(Hp, Pc, Qc))) return s;
-    } else {
-      // extrapolation (l.21-27, R27)
-      const double tp = (1.0 + sqrt(1.0 + 4.0 * t * t)) / 2.0;
-      const double w = (t - 1.0) / tp;
-      const double wW = std::min(w, delta * sqrt(LWp / LW)), wH = std::min(w, delta * sqrt(LHp / LH));
-      LAUNCH(h, launch_bcd_extrap(W, Wm, Wp, m * r, wW, st));
-      LAUNCH(h, launch_bcd_extrap(H, Hm, Hp, (int64_t)r * n, wH, st));
-      std::swap(Pc, Pn);
-      std::swap(Qc, Qn);
-      LWp = LW;
-      LHp = LH;
-      t = tp;
-      obj = obj_new;
-    }
-    if (objective_trace) objective_trace[it] = obj;
+  LAUNCH(h, launch_scale_copy(W, Wm, Wp, m * r, bs + BS_XX, bs + BS_W0, st));
+  LAUNCH(h, launch_scale_copy(H, Hm, Hp, (int64_t)r * n, bs + BS_XX, bs + BS_H0, st));
+  if (tc) {
+    LAUNCH(h, tc_prepare(tp, X, ldx, Hp, tws, &maps, st));
+    LAUNCH(h, tc16_prepare(tp, X, ldx, Hp, tws, &maps, st));
   }
-  // return the last accepted iterates
+  if ((s = pq(Hp, Pc, Qc, false))) return s;
+  LAUNCH(h, launch_bcd_wnorm(Wp, Wp, m, r, nullptr, Gpart, nullptr, st));  // W_prev^T W_prev (no normalisation)
+  LAUNCH(h, launch_sum_partials(Gpart, nwc, (int64_t)r * r, G, st));
+  if ((s = spec(Qc, bs + BS_LW))) return s;
+  if ((s = spec(G, bs + BS_LH))) return s;
+  LAUNCH(h, launch_bcd_init(bs, delta, st));
+  // ---- one iteration (l.5-27), a fixed launch sequence
+  auto iteration = [&]() -> ntt_status {
+    if ((s = spec(Qc, bs + BS_LW))) return s;                                    // l.7
+    LAUNCH(h, launch_bcd_w(Wm, m, r, Pc, Qc, bs + BS_LW, W, cpart, st));          // l.6-8
+    LAUNCH(h, launch_sum_partials(cpart, nwc, r, c, st));
+    LAUNCH(h, launch_bcd_wnorm(W, Wp, m, r, c, Gpart, mxw, st));                  // l.9 (R24)
+    LAUNCH(h, launch_bcd_hnorm(Hm, Hp, r, n, c, st));
+    LAUNCH(h, launch_sum_partials(Gpart, nwc, (int64_t)r * r, G, st));             // l.10
+    if ((s = spec(G, bs + BS_LH))) return s;
+    if (tc) {                                                                     // S = W^T X
+      LAUNCH(h, tc16_pack_w_slot(tp, W, tws, st, 6));
+      PLAUNCH(h, 7, xbytes, tc16_pass_h(tp, maps, tws, bef, st, bflush));
+    } else {
+      PLAUNCH(h, 5, xbytes, launch_bcd_spart(X, ldx, m, n, W, r, nS, Spart, st));
+    }
+    LAUNCH(h, launch_bcd_hup(Spart, nS, n, r, G, bs + BS_LH, Hm, H, mxh, h->num_sms, st));  // l.11-14
+    if ((s = pq(H, Pn, Qn, true))) return s;                                               // l.15
+    LAUNCH(h, launch_bcd_decide(bs, dtrace, dotpart, ndot, G, Qn, r, mxh, st));             // l.16-17 (R25)
+    LAUNCH(h, launch_bcd_commit(W, Wm, Wp, m * r, bs, BS_WW, st));                    // l.18-27
+    LAUNCH(h, launch_bcd_commit(H, Hm, Hp, (int64_t)r * n, bs, BS_WH, st));
+    LAUNCH(h, launch_bcd_commit_pq(Pc, Pn, m, r, Qc, Qn, c, bs, st));
+    return NTT_OK;
+  };
+  const char* ge = getenv("NTT_BCD_GRAPH");
+  const bool graph = iters >= 2 && !h->prof && !(ge && ge[0] == '0');
+  if (graph) {
+    if (!h->gstream) {
+      CU(h, cudaStreamCreateWithFlags(&h->gstream, cudaStreamNonBlocking));
+      CU(h, cudaEventCreateWithFlags(&h->gev_in, cudaEventDisableTiming));
+      CU(h, cudaEventCreateWithFlags(&h->gev_out, cudaEventDisableTiming));
+    }
+    CU(h, cudaEventRecord(h->gev_in, st));
+    CU(h, cudaStreamWaitEvent(h->gstream, h->gev_in, 0));
+    const int64_t l0 = h->launches;
+    st = h->gstream;
+    cudaError_t e0 = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+    ntt_status si = e0 == cudaSuccess ? iteration() : NTT_ERR_CUDA;
+    cudaGraph_t g = nullptr;
+    cudaError_t e1 = cudaStreamEndCapture(st, &g);
+    const int64_t per_it = h->launches - l0;
+    if (e0 != cudaSuccess || si != NTT_OK || e1 != cudaSuccess) {
+      if (g) cudaGraphDestroy(g);
+      if (si != NTT_OK) return si;
+      return fail(h, NTT_ERR_CUDA, "BCD graph capture failed: %s", cudaGetErrorString(e0 ? e0 : e1));
+    }
+    cudaGraphExec_t ge_ = nullptr;
+    cudaError_t e2 = cudaGraphInstantiate(&ge_, g, 0);
+    cudaGraphDestroy(g);
+    if (e2 != cudaSuccess) return fail(h, NTT_ERR_CUDA, "BCD graph instantiate: %s", cudaGetErrorString(e2));
+    cudaError_t el = cudaSuccess;
+    for (int it = 0; it < iters && el == cudaSuccess; ++it) el = cudaGraphLaunch(ge_, st);
+    cudaGraphExecDestroy(ge_);
+    if (el != cudaSuccess) return fail(h, NTT_ERR_CUDA, "BCD graph launch: %s", cudaGetErrorString(el));
+    h->launches = l0 + per_it * iters;
+    CU(h, cudaEventRecord(h->gev_out, st));
+    st = h->stream;
+    CU(h, cudaStreamWaitEvent(st, h->gev_out, 0));
+  } else {
+    for (int it = 0; it < iters; ++it)
+      if ((s = iteration())) return s;
+  }
+  // the last accepted iterates (l.28)
   CU(h, cudaMemcpyAsync(W, Wp, sizeof(float) * m * r, cudaMemcpyDeviceToDevice, st));
   CU(h, cudaMemcpyAsync(H, Hp, sizeof(float) * r * n, cudaMemcpyDeviceToDevice, st));
+  if (objective_trace && iters > 0)
+    CU(h, cudaMemcpyAsync(objective_trace, dtrace, sizeof(double) * iters, cudaMemcpyDeviceToHost, st));
   CU(h, cudaStreamSynchronize(st));
   return NTT_OK;
 }

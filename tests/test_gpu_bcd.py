@@ -59,9 +59,11 @@ def test_bcd_parity(h, ora, m, n, r, iters, lr):
     Wo, Ho, tro = ora.nmf_bcd(X.astype(np.float64), W0, H0, iters, trace=True)
     obj0 = 0.5 * float(np.sum(X.astype(np.float64) ** 2))
     assert np.array_equal(branches(trg, obj0), branches(tro, obj0))
-    # the GPU evaluates the objective by the Gram identity (fp32 chunk products in X H^T):
-    # its rounding scales with ||X||^2 = 2 obj0, hence the absolute term
-    assert np.abs(trg - tro).max() <= 1e-5 * tro.max() + 1e-6 * obj0
+    # the GPU evaluates the objective by the Gram identity from X H^T, whose contraction runs
+    # in fp32 chunks (FFMA) or fp16x2 parts with fp32 tensor-core accumulation (m, n >= 256):
+    # a ~1e-6-relative error in <W, X H^T> scales with ||X||^2 = 2 obj0, hence the
+    # ||X||^2-relative term (R25).
+    assert np.abs(trg - tro).max() <= 1e-5 * tro.max() + 1e-5 * obj0
     assert np.abs(Wg - Wo).max() <= 1e-4 * np.abs(Wo).max()
     assert np.abs(Hg - Ho).max() <= 1e-4 * np.abs(Ho).max()
     assert Wg.min() >= 0 and Hg.min() >= 0
@@ -81,7 +83,7 @@ def test_bcd_delta_zero(h, ora):
     X, W0, H0 = case(64, 200, 6, 5)
     Wg, Hg, trg = run_gpu(h, X, W0, H0, 12, delta=0.0)
     Wo, Ho, tro = ora.nmf_bcd(X.astype(np.float64), W0, H0, 12, delta=0.0, trace=True)
-    assert np.abs(trg - tro).max() <= 1e-5 * tro.max() + 1e-6 * 0.5 * float(np.sum(X.astype(np.float64) ** 2))
+    assert np.abs(trg - tro).max() <= 1e-5 * tro.max() + 1e-5 * 0.5 * float(np.sum(X.astype(np.float64) ** 2))
     assert np.abs(Wg - Wo).max() <= 1e-4 * np.abs(Wo).max()
     assert np.abs(Hg - Ho).max() <= 1e-4 * np.abs(Ho).max()
 
@@ -117,7 +119,8 @@ def test_bcd_fullsize_properties(h):
     assert np.all(np.diff(tr) <= 0) and W.min() >= 0 and H.min() >= 0
     Xd = X.double()
     res = 0.5 * float(((Xd - W.view(m, r).double() @ H.view(r, n).double()) ** 2).sum())
-    assert abs(res - tr[-1]) <= 1e-4 * tr[-1]
+    obj0 = 0.5 * float((Xd ** 2).sum())
+    assert abs(res - tr[-1]) <= 1e-5 * obj0      # Gram-identity objective (R25)
     Wm, Hm = W0.clone(), H0.clone()
     h.ntt_nmf_mu(X.view(-1), m, n, n, r, iters, 1e-16, Wm, Hm)
     res_mu = 0.5 * float(((Xd - Wm.view(m, r).double() @ Hm.view(r, n).double()) ** 2).sum())
