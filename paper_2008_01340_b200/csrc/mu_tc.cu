@@ -295,16 +295,44 @@ k_tc_wupdate(float* __restrict__ W, int64_t m, int r, const double* __restrict__
              const double* __restrict__ Qred, float eps, float* __restrict__ WcatT, int64_t ldw,
              double* __restrict__ Gpart, unsigned* __restrict__ maxw) {
   __shared__ double Qs[R * R];
-  __shared__ float Wn[UPD_ROWS][R + 1];
+  // the CTA's rows own a contiguous run of rows * r doubles in every split partial: summed
+  // coalesced (thread t: elements t + 128 q) into Ps, which later holds Wn (same storage)
+  __shared__ __align__(16) unsigned char ubuf[UPD_ROWS * R * sizeof(double)];
+  double(*Ps) = reinterpret_cast<double*>(ubuf);
+  float(*Wn)[R + 1] = reinterpret_cast<float(*)[R + 1]>(ubuf);
   const int rr = r * r;
   for (int t = threadIdx.x; t < R * R; t += blockDim.x) {
     const int k = t / R, l = t % R;
     Qs[t] = (k < r && l < r) ? Qred[k * r + l] : 0.0;
   }
-  __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * UPD_ROWS + threadIdx.x;
-  if (i < m) {
+  const int64_t i0 = (int64_t)blockIdx.x * UPD_ROWS;
+  const int64_t i = i0 + threadIdx.x;
+  {
+    const int len = (int)(min((int64_t)UPD_ROWS, m - i0) * r);
     const int64_t mr = m * r;
+    double acc[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) acc[q] = 0.0;
+    for (int b = 0; b < nP; ++b) {
+      const double* src = Ppart + (int64_t)b * mr + i0 * r;
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int e = threadIdx.x + q * UPD_ROWS;
+        if (e < len) acc[q] += src[e];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int e = threadIdx.x + q * UPD_ROWS;
+      if (e < len) Ps[e] = acc[q];
+    }
+  }
+  __syncthreads();
+  double pv[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) pv[k] = (i < m && k < r) ? Ps[threadIdx.x * r + k] : 0.0;
+  __syncthreads();  // Ps -> Wn
+  if (i < m) {
     double w[R];
 #pragma unroll
     for (int k = 0; k < R; ++k) w[k] = (k < r) ? (double)W[i * r + k] : 0.0;
@@ -312,8 +340,7 @@ k_tc_wupdate(float* __restrict__ W, int64_t m, int r, const double* __restrict__
     for (int k = 0; k < R; ++k) {
       float wn = 0.0f;
       if (k < r) {
-        double p = 0.0;
-        for (int b = 0; b < nP; ++b) p += Ppart[(int64_t)b * mr + i * r + k];
+        const double p = pv[k];
         double d = 0.0;
 #pragma unroll
         for (int l = 0; l < R; ++l) d += w[l] * Qs[l * R + k];
@@ -358,7 +385,11 @@ k_tc_hupdate(float* __restrict__ H, int64_t n, int r, const double* __restrict__
              double* __restrict__ Qpart, unsigned* __restrict__ maxh) {
   float hmax = 0.0f;
   __shared__ float Gs[R * R];
-  __shared__ float Hn[R][UPD_ROWS + 1];
+  // S of the block's 128 columns (a contiguous run of cols * r doubles per split), summed
+  // coalesced into Ss, which later holds Hn (same storage)
+  __shared__ __align__(16) unsigned char ubuf[UPD_ROWS * R * sizeof(double)];
+  double* Ss = reinterpret_cast<double*>(ubuf);
+  float(*Hn)[UPD_ROWS + 1] = reinterpret_cast<float(*)[UPD_ROWS + 1]>(ubuf);
   const int rr = r * r;
   if (update)
     for (int t = threadIdx.x; t < R * R; t += blockDim.x) {
@@ -374,17 +405,40 @@ k_tc_hupdate(float* __restrict__ H, int64_t n, int r, const double* __restrict__
   for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     __syncthreads();
     const int64_t j = blk * UPD_ROWS + threadIdx.x;
+    double sv[R];
+    if (update) {
+      const int len = (int)(min((int64_t)UPD_ROWS, n - blk * UPD_ROWS) * r);
+      const int64_t nr = n * r;
+      double acc[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) acc[q] = 0.0;
+      for (int b = 0; b < nS; ++b) {
+        const double* src = Spart + (int64_t)b * nr + blk * UPD_ROWS * r;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int e = threadIdx.x + q * UPD_ROWS;
+          if (e < len) acc[q] += src[e];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int e = threadIdx.x + q * UPD_ROWS;
+        if (e < len) Ss[e] = acc[q];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < R; ++k) sv[k] = (j < n && k < r) ? Ss[threadIdx.x * r + k] : 0.0;
+      __syncthreads();  // Ss -> Hn
+    }
     if (j < n) {
       float h[R];
 #pragma unroll
       for (int k = 0; k < R; ++k) h[k] = (k < r) ? H[(int64_t)k * n + j] : 0.0f;
-      const int64_t nr = n * r;
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         float hn = h[k];
         if (update && k < r) {
-          double sd = 0.0;
-          for (int b = 0; b < nS; ++b) sd += Spart[(int64_t)b * nr + j * r + k];
+          const double sd = sv[k];
           float e = 0.0f;
 #pragma unroll
           for (int l = 0; l < R; ++l) e = fmaf(Gs[k * R + l], h[l], e);
