@@ -237,9 +237,26 @@ def other_workloads(h, P, ni, torch, steps=2):
         alg = 4.0 * n * (2 * m + 3 * r)  # 2-pass algorithmic bytes per iteration
         out[name] = {"mu_iter_per_s": 1e3 / ms, "ms_per_iter": ms, "m": m, "n": n, "r": r, "timed_iters": iters,
                      "effective_GBps": alg / (ms / 1e3) / 1e9,
-                     "path": "tcgen05 kind::tf32 3xTF32 2-pass (mu_tc.cu)",
+                     "path": "tcgen05 kind::f16 fp16x2 2-pass (mu_tc16.cu)",
                      "note": "config 5 on the 1-GPU row slice (SURVEY s.8(d)); inputs X = W0 H0 + noise on device"}
-        del X, W, H
+        # BCD NMF (Alg. 3, SURVEY s.8(f) f1) on the same X: two passes over X per iteration
+        h.ntt_fill_uniform(W, m * r, w.seed, ni.stream_w(1))
+        h.ntt_fill_uniform(H, r * n, w.seed, ni.stream_h(1))
+        W0, H0 = W.clone(), H.clone()
+        h.ntt_nmf_bcd(X, m, n, n, r, 2, W, H)
+        W.copy_(W0)
+        H.copy_(H0)
+        e0, e1 = ev(), ev()
+        e0.record()
+        tr = h.ntt_nmf_bcd(X, m, n, n, r, iters, W, H, trace=True)
+        e1.record()
+        torch.cuda.synchronize()
+        msb = e0.elapsed_time(e1) / iters
+        out[name]["bcd"] = {"iter_per_s": 1e3 / msb, "ms_per_iter": msb, "timed_iters": iters,
+                            "effective_GBps_2xX": 8.0 * m * n / (msb / 1e3) / 1e9,
+                            "rel_error_after": float((2.0 * tr[-1]) ** 0.5 / float(torch.linalg.norm(X))),
+                            "path": "ntt_nmf_bcd: one CUDA graph per iteration, fp16x2 tcgen05 X passes (bcd.cu)"}
+        del X, W, H, W0, H0
         torch.cuda.empty_cache()
     return out
 
