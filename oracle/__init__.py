@@ -467,3 +467,42 @@ def nmf_bcd(X: np.ndarray, W0: np.ndarray, H0: np.ndarray, iters: int, delta: fl
             Q, P = H @ H.T, X @ H.T
         tr.append(obj)
     return (Wp, Hp, np.array(tr)) if trace else (Wp, Hp)
+
+
+# ---------------------------------------------- TT-SVD baseline (SURVEY s.8(f) f4) --
+def tt_svd(A: np.ndarray, tt_eps: float, max_ranks: Optional[Sequence[int]] = None):
+    """Unconstrained TT by sequential truncated SVDs (TT-SVD, the baseline the paper compares
+    nTT against: P:78), reading R28 (DESIGN.md s.3): at step l the current
+    matrix X_l (r_{l-1} n_l x prod_{i>l} n_i, as Alg. 2 l.4) is factored by LAPACK's SVD
+    (numpy.linalg.svd, a library primitive), r_l is chosen by the same tail rule as the nTT
+    sweep (svd_tail_rank, Alg. 2 l.5-6, capped by max_ranks), core l = U[:, :r_l] and
+    X_{l+1} = reshape(diag(s[:r_l]) V^T[:r_l]); the last core is X_d.  Sign convention (the
+    SVD fixes singular vectors only up to sign): the largest-magnitude entry of every kept
+    column of U is positive (lowest index on ties), the matching row of V^T flips with it.
+    Returns (ranks, packed fp64 cores, per-step discarded energies sum_{i > r_l} s_i^2)."""
+    A = np.asarray(A, dtype=np.float64)
+    dims = list(A.shape)
+    d = len(dims)
+    T = A.reshape(-1)
+    rprev, rest = 1, T.size
+    ranks, cores, tails = [], [], []
+    for l in range(1, d):
+        m = rprev * dims[l - 1]
+        rest //= dims[l - 1]
+        X = T.reshape(m, rest)
+        cap = min(m, rest, max_ranks[l - 1]) if max_ranks else min(m, rest)
+        r = svd_tail_rank(X, tt_eps, cap)
+        U, s, Vt = np.linalg.svd(X, full_matrices=False)
+        U, s, Vt = U[:, :r].copy(), s.copy(), Vt[:r].copy()
+        for k in range(r):
+            i = int(np.argmax(np.abs(U[:, k])))
+            if U[i, k] < 0:
+                U[:, k] = -U[:, k]
+                Vt[k] = -Vt[k]
+        tails.append(float(np.sum(s[r:] ** 2)))
+        cores.append(U.reshape(-1))
+        ranks.append(r)
+        T = (s[:r, None] * Vt).reshape(-1)
+        rprev = r
+    cores.append(T)
+    return ranks, np.concatenate(cores), np.array(tails)
