@@ -157,6 +157,20 @@ ntt_status ntt_decompose_eps(ntt_handle h, const float* A, int32_t d, const int6
 ntt_status ntt_rank_rule(ntt_handle h, const float* X, int64_t m, int64_t n, int64_t ldx, double tt_eps,
                          int32_t* rank, double* eig);
 
+/* ------------------------------------------------------------ TT-SVD baseline
+ * The unconstrained TT the paper compares nTT against (TT-SVD, P:78, P:88,
+ * P:453; SURVEY s.8(f) f4; reading R28): the same sweep and the same rank rule
+ * as ntt_decompose_eps (Alg. 2 l.4-6), with the NMF of each step replaced by the
+ * truncated SVD of X_l: core l = U_r (left singular vectors, signs fixed so the
+ * largest-magnitude entry of every column is positive), X_{l+1} = reshape(S_r V_r^T).
+ * Singular vectors come from the fp64 Gram of the smaller side (Householder +
+ * bisection + inverse iteration + Rayleigh-Ritz in one CTA), so min(m, n) <= 512
+ * per step (else NTT_ERR_UNSUPPORTED) and ranks <= 64 (max_ranks caps further).
+ * Cores may be negative.  Arguments, layouts and errors as ntt_decompose_eps.   */
+ntt_status ntt_tt_svd(ntt_handle h, const float* A, int32_t d, const int64_t* dims, double tt_eps,
+                      const int32_t* max_ranks, float* cores, int64_t cores_capacity, int32_t* ranks_out,
+                      double* rel_err);
+
 /* --------------------------------------------------------------- BCD NMF
  * The paper's alternative NMF (Alg. 3, distBCDnmf, P:196-240, P:254, P:294;
  * SURVEY s.8(f) f1) with readings R22-R27 (DESIGN.md s.3): prox-linear block

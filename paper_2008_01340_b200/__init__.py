@@ -204,6 +204,17 @@ class Handle:
                                             ctypes.byref(err) if err is not None else None))
         return [int(x) for x in rk][: d - 1], (float(err.value) if want_error else None)
 
+    def ntt_tt_svd(self, A, dims, tt_eps: float, cores, cores_capacity: int, max_ranks=None,
+                   want_error: bool = False):
+        """TT-SVD baseline (f4) with the rank rule; returns (ranks, rel_err or None)."""
+        d = len(dims)
+        rk = (ctypes.c_int32 * max(d - 1, 1))()
+        err = ctypes.c_double(-1.0) if want_error else None
+        mr = _i32arr(max_ranks) if max_ranks is not None else None
+        self._check(lib().ntt_tt_svd(self._h, _ptr(A), d, _i64arr(dims), tt_eps, mr, _ptr(cores), cores_capacity, rk,
+                                     ctypes.byref(err) if err is not None else None))
+        return [int(x) for x in rk][: d - 1], (float(err.value) if want_error else None)
+
     def ntt_rank_rule(self, X, m: int, n: int, ldx: int, tt_eps: float, want_eig: bool = False):
         """SVD rank rule on a device matrix; returns (rank, eigenvalues ascending or None)."""
         r = ctypes.c_int32()

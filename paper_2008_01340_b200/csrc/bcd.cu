@@ -467,7 +467,7 @@ __global__ void k_copy_last(const double* __restrict__ eig, int N, double* __res
   if (threadIdx.x == 0) out[0] = eig[N - 1];
 }
 
-int rcls_bcd(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : 32; }
+int rcls_bcd(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : r <= 32 ? 32 : 64; }
 
 }  // namespace
 
@@ -518,7 +518,8 @@ cudaError_t launch_bcd_spart(const float* X, int64_t ldx, int64_t m, int64_t n, 
     case 4: k_bcd_spart<4><<<g, BH_BN, 0, st>>>(X, ldx, m, n, W, r, rps, Spart); break;
     case 8: k_bcd_spart<8><<<g, BH_BN, 0, st>>>(X, ldx, m, n, W, r, rps, Spart); break;
     case 16: k_bcd_spart<16><<<g, BH_BN, 0, st>>>(X, ldx, m, n, W, r, rps, Spart); break;
-    default: k_bcd_spart<32><<<g, BH_BN, 0, st>>>(X, ldx, m, n, W, r, rps, Spart); break;
+    case 32: k_bcd_spart<32><<<g, BH_BN, 0, st>>>(X, ldx, m, n, W, r, rps, Spart); break;
+    default: k_bcd_spart<64><<<g, BH_BN, 0, st>>>(X, ldx, m, n, W, r, rps, Spart); break;  // TT-SVD (r <= 64)
   }
   return cudaGetLastError();
 }

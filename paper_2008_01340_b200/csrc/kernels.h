@@ -50,6 +50,22 @@ cudaError_t launch_rank_rule(const float* X, int64_t m, int64_t n, int64_t ldx, 
                              int num_sms, int* d_rank, double* d_eig, cudaStream_t st);
 
 cudaError_t launch_sym_eig(double* C, int N, double* scratch, double* eig, int* rank_dummy, cudaStream_t st);
+// fp64 Gram of X (X X^T if m <= n else X^T X) into ws (partials, then C = *Cout, N x N);
+// needs rank_rule_bytes(min(m, n), max(m, n), num_sms)
+cudaError_t launch_gram(const float* X, int64_t m, int64_t n, int64_t ldx, char* ws, int num_sms, double** Cout,
+                        cudaStream_t st);
+
+// TT-SVD baseline (tt_svd.cu, SURVEY s.8(f) f4): eigenvectors of the top r eigenvalues of a
+// symmetric PSD C (N <= 512, r <= 64 chosen by the tail rule and capped at rcap)
+size_t svd_eig_bytes(int64_t N);
+cudaError_t launch_svd_eig(double* C, int N, char* ws, double tt_eps, int rcap, double* eig_asc, double* lam,
+                           int* d_rank, double* U, cudaStream_t st);
+cudaError_t launch_sign_cols(const double* M, int64_t rows, int r, const double* scale, float* out, double* sgn,
+                             cudaStream_t st);
+cudaError_t launch_rows_from_spart(const double* Spart, int nS, int64_t n, int r, float* Xn, cudaStream_t st);
+cudaError_t launch_v_rows(const double* V, int64_t n, int r, const double* mult, const double* sgn, float* out,
+                          cudaStream_t st);
+cudaError_t launch_sing(const double* lam, int r, double* s, double* inv, cudaStream_t st);
 
 // BCD NMF building blocks (bcd.cu, Alg. 3).  Device state block (doubles):
 enum BcdState {

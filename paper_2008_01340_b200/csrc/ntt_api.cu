@@ -1401,6 +1401,154 @@ ntt_status ntt_decompose_eps(ntt_handle h, const float* A, int32_t d, const int6
   return NTT_OK;
 }
 
+// TT-SVD baseline (SURVEY s.8(f) f4, reading R28; tt_svd.cu).  Same sweep, shapes and rank
+// rule as ntt_decompose_eps; the NMF of each step is replaced by the truncated SVD.
+ntt_status ntt_tt_svd(ntt_handle h, const float* A, int32_t d, const int64_t* dims, double tt_eps,
+                      const int32_t* max_ranks, float* cores, int64_t cores_capacity, int32_t* ranks_out,
+                      double* rel_err) {
+  if (!h) return NTT_ERR_INVALID_ARG;
+  if (!A || !cores || !ranks_out) return fail(h, NTT_ERR_INVALID_ARG, "null A, cores or ranks_out");
+  if (!(tt_eps >= 0.0)) return fail(h, NTT_ERR_INVALID_ARG, "tt_eps must be >= 0");
+  if (h->nranks > 1) return fail(h, NTT_ERR_UNSUPPORTED, "ntt_tt_svd runs on a single-GPU handle");
+  TTShape s0;
+  std::vector<int32_t> ones((size_t)std::max(d - 1, 1), 1);
+  ntt_status st = check_tt(h, d, dims, ones.data(), &s0, false);
+  if (st) return st;
+  int64_t cap[65], mcap[65], ncol[65];
+  cap[0] = 1;
+  int64_t rest = s0.N;
+  size_t hbuf[2] = {1, 1}, cores_cap = 0, stepb = 0;
+  for (int l = 1; l < d; ++l) {
+    mcap[l] = cap[l - 1] * s0.dims[l - 1];
+    rest /= s0.dims[l - 1];
+    ncol[l] = rest;
+    int64_t c = std::min<int64_t>({(int64_t)kMaxRank, mcap[l], ncol[l]});
+    if (max_ranks) {
+      if (max_ranks[l - 1] < 1) return fail(h, NTT_ERR_RANK, "max_ranks[%d] < 1", l - 1);
+      c = std::min<int64_t>(c, max_ranks[l - 1]);
+    }
+    cap[l] = c;
+    hbuf[(l - 1) & 1] = std::max(hbuf[(l - 1) & 1], (size_t)(c * ncol[l]));
+    cores_cap += (size_t)(mcap[l] * c);
+    // per-step scratch for every m the previous rank allows
+    for (int64_t rp = 1; rp <= cap[l - 1]; ++rp) {
+      const int64_t m = rp * s0.dims[l - 1], n = ncol[l], N = std::min(m, n);
+      if (N > 512) continue;  // rejected at run time
+      size_t b = align_up(rank_rule_bytes(N, std::max(m, n), h->num_sms)) + align_up(svd_eig_bytes(N)) +
+                 align_up(sizeof(double) * (size_t)N * 64) + align_up(sizeof(double) * (size_t)(N + 64 * 4 + 8));
+      if (m <= n) {
+        b += align_up(sizeof(double) * (size_t)bcd_spart_splits(m, n, h->num_sms) * n * c);
+      } else {
+        const XhtPlan xp = plan_xht(m, n, h->num_sms);
+        b += align_up(sizeof(double) * (size_t)xp.ncs * m * c) + align_up(sizeof(double) * (size_t)m * c) +
+             align_up(sizeof(float) * (size_t)c * n);
+      }
+      stepb = std::max(stepb, b);
+    }
+  }
+  cores_cap += (size_t)(cap[d - 1] * s0.dims[d - 1]);
+  size_t o = 0;
+  const size_t off_h0 = o;
+  o = align_up(o + sizeof(float) * hbuf[0]);
+  const size_t off_h1 = o;
+  o = align_up(o + sizeof(float) * hbuf[1]);
+  const size_t off_c = o;
+  o = align_up(o + sizeof(float) * cores_cap);
+  const size_t off_step = o;
+  o = align_up(o + stepb);
+  CU(h, cudaSetDevice(h->device));
+  if ((st = ensure_ws(h, o))) return st;
+  char* ws = reinterpret_cast<char*>(h->ws);
+  cudaStream_t cs = h->stream;
+  const float* dA = A;
+  if (!is_device_ptr(A)) {
+    if ((st = ensure_stage(h, sizeof(float) * (size_t)s0.N))) return st;
+    dA = reinterpret_cast<const float*>(h->stage);
+    CU(h, cudaMemcpyAsync((void*)dA, A, sizeof(float) * (size_t)s0.N, cudaMemcpyHostToDevice, cs));
+  }
+  float* hb[2] = {reinterpret_cast<float*>(ws + off_h0), reinterpret_cast<float*>(ws + off_h1)};
+  float* dcores = reinterpret_cast<float*>(ws + off_c);
+  const float* X = dA;
+  float* Xn = nullptr;
+  int64_t rprev = 1, coff = 0;
+  for (int l = 1; l < d; ++l) {
+    const int64_t m = rprev * s0.dims[l - 1], n = ncol[l], N = std::min(m, n);
+    h->cur_step = l;
+    if (N > 512)
+      return fail(h, NTT_ERR_UNSUPPORTED, "TT-SVD needs min(m, n) <= 512 (step %d: %lld x %lld)", l, (long long)m,
+                  (long long)n);
+    const int rcap = (int)std::min<int64_t>(cap[l], N);
+    // step scratch
+    char* sp = ws + off_step;
+    size_t so = 0;
+    auto take = [&](size_t b) {
+      char* at = sp + so;
+      so = align_up(so + b);
+      return at;
+    };
+    char* gws = take(rank_rule_bytes(N, std::max(m, n), h->num_sms));
+    char* ews = take(svd_eig_bytes(N));
+    double* Uv = reinterpret_cast<double*>(take(sizeof(double) * (size_t)N * 64));
+    double* small = reinterpret_cast<double*>(take(sizeof(double) * (size_t)(N + 64 * 4 + 8)));
+    double* eig = small;
+    double* lam = eig + N;
+    double* sv = lam + 64;
+    double* inv = sv + 64;
+    double* sgn = inv + 64;
+    int* d_rank = reinterpret_cast<int*>(sgn + 64);
+    double* C = nullptr;
+    LAUNCH(h, launch_gram(X, m, n, n, gws, h->num_sms, &C, cs));
+    LAUNCH(h, launch_svd_eig(C, (int)N, ews, tt_eps, rcap, eig, lam, d_rank, Uv, cs));
+    int rk = 1;
+    CU(h, cudaMemcpyAsync(&rk, d_rank, sizeof(int), cudaMemcpyDeviceToHost, cs));
+    CU(h, cudaStreamSynchronize(cs));
+    const int r = std::max(1, std::min(rk, rcap));
+    ranks_out[l - 1] = r;
+    Xn = hb[(l - 1) & 1];
+    float* core = dcores + coff;
+    if (m <= n) {
+      // core = U_r with the sign convention, X' = core^T X
+      const int nS = bcd_spart_splits(m, n, h->num_sms);
+      double* Spart = reinterpret_cast<double*>(take(sizeof(double) * (size_t)nS * n * r));
+      LAUNCH(h, launch_sign_cols(Uv, m, r, nullptr, core, sgn, cs));
+      LAUNCH(h, launch_bcd_spart(X, n, m, n, core, r, nS, Spart, cs));
+      LAUNCH(h, launch_rows_from_spart(Spart, nS, n, r, Xn, cs));
+    } else {
+      // V_r = Uv (n x r): core = X V_r diag(1/s) with signs, X' = diag(sgn s) V_r^T
+      const XhtPlan xp = plan_xht(m, n, h->num_sms);
+      double* Ppart = reinterpret_cast<double*>(take(sizeof(double) * (size_t)xp.ncs * m * r));
+      double* P = reinterpret_cast<double*>(take(sizeof(double) * (size_t)m * r));
+      float* Vt = reinterpret_cast<float*>(take(sizeof(float) * (size_t)r * n));
+      if (so > stepb) return fail(h, NTT_ERR_WORKSPACE, "internal: TT-SVD step scratch exceeded");
+      LAUNCH(h, launch_sing(lam, r, sv, inv, cs));
+      LAUNCH(h, launch_v_rows(Uv, n, r, nullptr, nullptr, Vt, cs));
+      LAUNCH(h, launch_xht_partial(X, n, m, n, Vt, n, r, xp, Ppart, cs));
+      LAUNCH(h, launch_sum_partials(Ppart, xp.ncs, m * r, P, cs));
+      LAUNCH(h, launch_sign_cols(P, m, r, inv, core, sgn, cs));
+      LAUNCH(h, launch_v_rows(Uv, n, r, sv, sgn, Xn, cs));
+    }
+    if (so > stepb) return fail(h, NTT_ERR_WORKSPACE, "internal: TT-SVD step scratch exceeded");
+    coff += m * r;
+    X = Xn;
+    rprev = r;
+  }
+  h->cur_step = 0;
+  const int64_t ncl = rprev * s0.dims[d - 1];
+  CU(h, cudaMemcpyAsync(dcores + coff, Xn, sizeof(float) * (size_t)ncl, cudaMemcpyDeviceToDevice, cs));
+  coff += ncl;
+  if (coff > cores_capacity)
+    return fail(h, NTT_ERR_WORKSPACE, "cores_capacity %lld < %lld floats for the chosen ranks",
+                (long long)cores_capacity, (long long)coff);
+  CU(h, cudaMemcpyAsync(cores, dcores, sizeof(float) * (size_t)coff, cudaMemcpyDefault, cs));
+  CU(h, cudaStreamSynchronize(cs));
+  if (rel_err) {
+    TTShape s;
+    if ((st = check_tt(h, d, dims, ranks_out, &s, true))) return st;
+    if ((st = contract_stream(h, s, cores, nullptr, 0.0f, 0, A, rel_err))) return st;
+  }
+  return NTT_OK;
+}
+
 ntt_status ntt_rank_rule(ntt_handle h, const float* X, int64_t m, int64_t n, int64_t ldx, double tt_eps,
                          int32_t* rank, double* eig) {
   if (!h || !X || !rank) return NTT_ERR_INVALID_ARG;

@@ -267,8 +267,8 @@ size_t rank_rule_bytes(int64_t N, int64_t T, int num_sms) {
   return sizeof(double) * ((size_t)nsplit * nut * GT * GT + (size_t)N * N + 4 * (size_t)N + 64) + 64;
 }
 
-cudaError_t launch_rank_rule(const float* X, int64_t m, int64_t n, int64_t ldx, double tt_eps, char* ws,
-                             int num_sms, int* d_rank, double* d_eig, cudaStream_t st) {
+cudaError_t launch_gram(const float* X, int64_t m, int64_t n, int64_t ldx, char* ws, int num_sms, double** Cout,
+                        cudaStream_t st) {
   const bool rows = m <= n;  // C = X X^T (N = m) or X^T X (N = n)
   const int N = (int)(rows ? m : n);
   const int64_t T = rows ? n : m;
@@ -281,13 +281,22 @@ cudaError_t launch_rank_rule(const float* X, int64_t m, int64_t n, int64_t ldx, 
   nsplit = (T + chunk - 1) / chunk;
   double* part = reinterpret_cast<double*>(ws);
   double* C = part + (size_t)nsplit * nut * GT * GT;
-  double* vg = C + (size_t)N * N;
-  double* pg = vg + N;
+  *Cout = C;
   k_gram<<<dim3((unsigned)nut, (unsigned)nsplit), 256, 0, st>>>(X, sa, stt, N, T, ntile, chunk, part);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
   k_gram_sum<<<256, 256, 0, st>>>(part, (int)nsplit, ntile, N, C);
-  if ((e = cudaGetLastError())) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rank_rule(const float* X, int64_t m, int64_t n, int64_t ldx, double tt_eps, char* ws,
+                             int num_sms, int* d_rank, double* d_eig, cudaStream_t st) {
+  const int N = (int)(m <= n ? m : n);
+  double* C = nullptr;
+  cudaError_t e = launch_gram(X, m, n, ldx, ws, num_sms, &C, st);
+  if (e) return e;
+  double* vg = C + (size_t)N * N;
+  double* pg = vg + N;
   const size_t sm = sizeof(double) * (4 * (size_t)N + 40);
   e = cudaFuncSetAttribute(k_eig_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e) return e;
