@@ -24,11 +24,14 @@ constexpr int GK = 32;   // columns of the long dimension per smem block
 
 // C tile (ta, tb) (tb >= ta) over the split's range of the long index t:
 // u_t[a] = X[a * sa + t * st]  (X X^T: sa = ldx, st = 1;  X^T X: sa = 1, st = ldx)
-__global__ void __launch_bounds__(256)
+// 64 threads, 4 x 4 outputs each (rows ty + 8u, columns tx + 8v): 8 shared loads per 16
+// fp64 FMAs, so the FP64 pipe, not shared memory, sets the rate.
+constexpr int GTH = 64;
+__global__ void __launch_bounds__(GTH)
 k_gram(const float* __restrict__ X, int64_t sa, int64_t st, int N, int64_t T, int ntile, int64_t chunk,
        double* __restrict__ part) {
-  __shared__ float As[GT][GK + 1];
-  __shared__ float Bs[GT][GK + 1];
+  __shared__ float As[GK][GT + 1];
+  __shared__ float Bs[GK][GT + 1];
   // upper-triangular tile index -> (ta, tb)
   int tix = blockIdx.x, ta = 0;
   while (tix >= ntile - ta) {
@@ -38,10 +41,14 @@ k_gram(const float* __restrict__ X, int64_t sa, int64_t st, int N, int64_t T, in
   const int tb = ta + tix;
   const int split = blockIdx.y;
   const int64_t t0 = (int64_t)split * chunk, t1 = min(T, t0 + chunk);
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 2 x 2 outputs per thread
-  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+  double acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
   for (int64_t tb0 = t0; tb0 < t1; tb0 += GK) {
-    for (int e = threadIdx.x; e < GT * GK; e += 256) {
+    for (int e = threadIdx.x; e < GT * GK; e += GTH) {
       // XX^T: consecutive threads along t (contiguous); X^T X: along a (contiguous)
       int i, k;
       if (st == 1) {
@@ -53,20 +60,23 @@ k_gram(const float* __restrict__ X, int64_t sa, int64_t st, int N, int64_t T, in
       }
       const int64_t t = tb0 + k;
       const int a = ta * GT + i, bb = tb * GT + i;
-      As[i][k] = (t < t1 && a < N) ? X[(int64_t)a * sa + t * st] : 0.0f;
-      Bs[i][k] = (t < t1 && bb < N) ? X[(int64_t)bb * sa + t * st] : 0.0f;
+      As[k][i] = (t < t1 && a < N) ? X[(int64_t)a * sa + t * st] : 0.0f;
+      Bs[k][i] = (t < t1 && bb < N) ? X[(int64_t)bb * sa + t * st] : 0.0f;
     }
     __syncthreads();
     // fp64 FMA: the product of two fp32 values is exact in fp64, so the Gram (and the
     // eigenvalues) carry ~1e-16 relative error instead of fp32's ~1e-7
-#pragma unroll 8
+#pragma unroll 4
     for (int k = 0; k < GK; ++k) {
-      const double a0 = As[ty][k], a1 = As[ty + 16][k];
-      const double b0 = Bs[tx][k], b1 = Bs[tx + 16][k];
-      acc[0][0] = fma(a0, b0, acc[0][0]);
-      acc[0][1] = fma(a0, b1, acc[0][1]);
-      acc[1][0] = fma(a1, b0, acc[1][0]);
-      acc[1][1] = fma(a1, b1, acc[1][1]);
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = As[k][ty + 8 * u];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) b[v] = Bs[k][tx + 8 * v];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
     }
     __syncthreads();
   }
@@ -74,15 +84,18 @@ k_gram(const float* __restrict__ X, int64_t sa, int64_t st, int N, int64_t T, in
   const int tile = blockIdx.x;
   double* dst = part + ((int64_t)split * gridDim.x + tile) * (GT * GT);
 #pragma unroll
-  for (int u = 0; u < 2; ++u)
+  for (int u = 0; u < 4; ++u)
 #pragma unroll
-    for (int v = 0; v < 2; ++v) dst[(ty + 16 * u) * GT + tx + 16 * v] = acc[u][v];
+    for (int v = 0; v < 4; ++v) dst[(ty + 8 * u) * GT + tx + 8 * v] = acc[u][v];
 }
 
+// one warp per entry of the upper tiles: lanes take every 32nd split, fixed shuffle tree
 __global__ void k_gram_sum(const double* __restrict__ part, int nsplit, int ntile, int N, double* __restrict__ C) {
   const int nut = ntile * (ntile + 1) / 2;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)nut * GT * GT;
-       e += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t nent = (int64_t)nut * GT * GT;
+  const int lane = threadIdx.x & 31;
+  for (int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < nent;
+       e += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     int tix = (int)(e / (GT * GT));
     const int w = (int)(e % (GT * GT));
     const int tile = tix;
@@ -93,11 +106,14 @@ __global__ void k_gram_sum(const double* __restrict__ part, int nsplit, int ntil
     }
     const int tb = ta + tix;
     const int a = ta * GT + w / GT, b = tb * GT + w % GT;
-    if (a >= N || b >= N) continue;
+    if (a >= N || b >= N) continue;  // warp-uniform
     double s = 0.0;
-    for (int sp = 0; sp < nsplit; ++sp) s += part[((int64_t)sp * nut + tile) * (GT * GT) + w];
-    C[(int64_t)a * N + b] = s;
-    C[(int64_t)b * N + a] = s;
+    for (int sp = lane; sp < nsplit; sp += 32) s += part[((int64_t)sp * nut + tile) * (GT * GT) + w];
+    s = warp_sum(s);
+    if (lane == 0) {
+      C[(int64_t)a * N + b] = s;
+      C[(int64_t)b * N + a] = s;
+    }
   }
 }
 
@@ -261,8 +277,9 @@ k_eig_rank(double* __restrict__ C, int N, double* __restrict__ vg, double* __res
 size_t rank_rule_bytes(int64_t N, int64_t T, int num_sms) {
   const int ntile = (int)((N + GT - 1) / GT);
   const int nut = ntile * (ntile + 1) / 2;
-  int64_t nsplit = (2 * num_sms + nut - 1) / nut;
-  const int64_t ch = (T + nsplit - 1) / nsplit;
+  int64_t nsplit = (8 * num_sms + nut - 1) / nut;
+  int64_t ch = (T + nsplit - 1) / nsplit;
+  ch = (ch + GK - 1) / GK * GK;
   nsplit = (T + ch - 1) / ch;
   return sizeof(double) * ((size_t)nsplit * nut * GT * GT + (size_t)N * N + 4 * (size_t)N + 64) + 64;
 }
@@ -275,17 +292,17 @@ cudaError_t launch_gram(const float* X, int64_t m, int64_t n, int64_t ldx, char*
   const int64_t sa = rows ? ldx : 1, stt = rows ? 1 : ldx;
   const int ntile = (N + GT - 1) / GT;
   const int nut = ntile * (ntile + 1) / 2;
-  int64_t nsplit = (2 * num_sms + nut - 1) / nut;
+  int64_t nsplit = (8 * num_sms + nut - 1) / nut;
   int64_t chunk = (T + nsplit - 1) / nsplit;
   chunk = (chunk + GK - 1) / GK * GK;
   nsplit = (T + chunk - 1) / chunk;
   double* part = reinterpret_cast<double*>(ws);
   double* C = part + (size_t)nsplit * nut * GT * GT;
   *Cout = C;
-  k_gram<<<dim3((unsigned)nut, (unsigned)nsplit), 256, 0, st>>>(X, sa, stt, N, T, ntile, chunk, part);
+  k_gram<<<dim3((unsigned)nut, (unsigned)nsplit), GTH, 0, st>>>(X, sa, stt, N, T, ntile, chunk, part);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
-  k_gram_sum<<<256, 256, 0, st>>>(part, (int)nsplit, ntile, N, C);
+  k_gram_sum<<<1184, 256, 0, st>>>(part, (int)nsplit, ntile, N, C);
   return cudaGetLastError();
 }
 

@@ -463,14 +463,24 @@ __global__ void __launch_bounds__(256) k_sign_cols(const double* __restrict__ M,
   for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) out[i * r + k] = (float)(M[i * r + k] * s);
 }
 
-// X'[k][j] = sum_s Spart[s][j][k] (fixed order)
+// X'[k][j] = sum_s Spart[s][j][k] (fixed order): thread j reads its r contiguous doubles per
+// split, writes row k coalesced across j
+template <int R>
 __global__ void k_rows_from_spart(const double* __restrict__ Spart, int nS, int64_t n, int r, float* __restrict__ Xn) {
   const int64_t nr = n * r;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nr; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = t / n, j = t - k * n;
-    double s = 0.0;
-    for (int b = 0; b < nS; ++b) s += Spart[(int64_t)b * nr + j * r + k];
-    Xn[t] = (float)s;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    double acc[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc[k] = 0.0;
+    for (int b = 0; b < nS; ++b) {
+      const double* src = Spart + (int64_t)b * nr + j * r;
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        if (k < r) acc[k] += src[k];
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if (k < r) Xn[(int64_t)k * n + j] = (float)acc[k];
   }
 }
 
@@ -528,8 +538,11 @@ cudaError_t launch_sign_cols(const double* M, int64_t rows, int r, const double*
 }
 
 cudaError_t launch_rows_from_spart(const double* Spart, int nS, int64_t n, int r, float* Xn, cudaStream_t st) {
-  const int64_t g = std::min<int64_t>(1184, (n * r + 255) / 256);
-  k_rows_from_spart<<<(unsigned)std::max<int64_t>(g, 1), 256, 0, st>>>(Spart, nS, n, r, Xn);
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(1184, (n + 127) / 128));
+  if (r <= 8) k_rows_from_spart<8><<<g, 128, 0, st>>>(Spart, nS, n, r, Xn);
+  else if (r <= 16) k_rows_from_spart<16><<<g, 128, 0, st>>>(Spart, nS, n, r, Xn);
+  else if (r <= 32) k_rows_from_spart<32><<<g, 128, 0, st>>>(Spart, nS, n, r, Xn);
+  else k_rows_from_spart<64><<<g, 128, 0, st>>>(Spart, nS, n, r, Xn);
   return cudaGetLastError();
 }
 
