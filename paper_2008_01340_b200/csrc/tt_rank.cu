@@ -30,8 +30,9 @@ constexpr int GTH = 64;
 __global__ void __launch_bounds__(GTH)
 k_gram(const float* __restrict__ X, int64_t sa, int64_t st, int N, int64_t T, int ntile, int64_t chunk,
        double* __restrict__ part) {
-  __shared__ float As[GK][GT + 1];
-  __shared__ float Bs[GK][GT + 1];
+  // fp64 in shared memory: each element is converted once when staged, not per use
+  __shared__ double As[GK][GT + 1];
+  __shared__ double Bs[GK][GT + 1];
   // upper-triangular tile index -> (ta, tb)
   int tix = blockIdx.x, ta = 0;
   while (tix >= ntile - ta) {
@@ -60,8 +61,8 @@ k_gram(const float* __restrict__ X, int64_t sa, int64_t st, int N, int64_t T, in
       }
       const int64_t t = tb0 + k;
       const int a = ta * GT + i, bb = tb * GT + i;
-      As[k][i] = (t < t1 && a < N) ? X[(int64_t)a * sa + t * st] : 0.0f;
-      Bs[k][i] = (t < t1 && bb < N) ? X[(int64_t)bb * sa + t * st] : 0.0f;
+      As[k][i] = (t < t1 && a < N) ? (double)X[(int64_t)a * sa + t * st] : 0.0;
+      Bs[k][i] = (t < t1 && bb < N) ? (double)X[(int64_t)bb * sa + t * st] : 0.0;
     }
     __syncthreads();
     // fp64 FMA: the product of two fp32 values is exact in fp64, so the Gram (and the
