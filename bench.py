@@ -258,7 +258,55 @@ def other_workloads(h, P, ni, torch, steps=2):
                             "path": "ntt_nmf_bcd: one CUDA graph per iteration, fp16x2 tcgen05 X passes (bcd.cu)"}
         del X, W, H, W0, H0
         torch.cuda.empty_cache()
+    # TT-SVD baseline (SURVEY s.8(f) f4) at the nTT ranks of configs 3 and 4
+    for name in ("config3", "config4"):
+        w = ni.workloads()[name]
+        cores0 = torch.from_numpy(ni.make_cores(w.dims, w.ranks, w.seed).astype(np.float32)).cuda()
+        A = torch.empty(w.numel, device="cuda")
+        h.ntt_generate(w.dims, w.ranks, cores0, w.noise_amp, w.seed, ni.STREAM_NOISE, A)
+        cap = P.cores_size(w.dims, [64] * (len(w.dims) - 1))
+        cores = torch.empty(cap, device="cuda")
+        ranks, err = h.ntt_tt_svd(A, w.dims, 0.0, cores, cap, max_ranks=w.ranks, want_error=True)
+        e0, e1 = ev(), ev()
+        e0.record()
+        for _ in range(steps):
+            h.ntt_tt_svd(A, w.dims, 0.0, cores, cap, max_ranks=w.ranks)
+        e1.record()
+        torch.cuda.synchronize()
+        row = {"ttsvd_ms": e0.elapsed_time(e1) / steps, "ranks": ranks, "rel_error": err,
+               "path": "ntt_tt_svd: fp64 Gram + one-CTA eigensolver per step (tt_svd.cu)"}
+        out.setdefault(name, {})["ttsvd"] = row
+        del A, cores
+        torch.cuda.empty_cache()
     return out
+
+
+def cpu_baseline_other(other, ni):
+    """The oracle timed beside the NEXT-row workloads (cpu_baseline leg): 2 iterations of
+    oracle.nmf_bcd on a config-2-shaped X, and oracle.tt_svd on a config-4-shaped tensor
+    (numpy fp64 / LAPACK; inputs of the same shape, seeded uniform values)."""
+    import numpy as np
+    import oracle
+    rng = np.random.default_rng(0)
+    if "config2" in other and "bcd" in other["config2"]:
+        m, n, r = other["config2"]["m"], other["config2"]["n"], other["config2"]["r"]
+        X = rng.random((m, n))
+        t0 = time.perf_counter()
+        oracle.nmf_bcd(X, rng.random((m, r)), rng.random((r, n)), 2)
+        dt = (time.perf_counter() - t0) / 2
+        other["config2"]["bcd"]["cpu_baseline"] = {
+            "value": 1.0 / dt, "unit": "BCD-iter/s", "kind": "oracle",
+            "sample": "2 iterations of oracle.nmf_bcd (numpy fp64) on a 4096 x 4096 X"}
+        del X
+    if "config4" in other and "ttsvd" in other["config4"]:
+        w = ni.workloads()["config4"]
+        A = rng.random(w.dims)
+        t0 = time.perf_counter()
+        oracle.tt_svd(A, 0.0, w.ranks)
+        other["config4"]["ttsvd"]["cpu_baseline"] = {
+            "value": (time.perf_counter() - t0) * 1e3, "unit": "ms", "kind": "oracle",
+            "sample": "one oracle.tt_svd (LAPACK SVD per step, fp64) of a 6^10 tensor at ranks 5"}
+        del A
 
 
 # ------------------------------------------------------------------- ours ---
@@ -404,6 +452,8 @@ def run_ours(args):
     if rk == 0 and ws == 1 and not args.no_cpu:
         t, threads, desc = oracle_sample_time(dims, ranks, iters)
         line["cpu_baseline"] = {"value": its / t, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc}
+        if "other_workloads" in line:
+            cpu_baseline_other(line["other_workloads"], ni)
     if rk == 0:
         print(json.dumps(line))
     if dist:
