@@ -213,7 +213,7 @@ def other_workloads(h, P, ni, torch, steps=2):
         out[name] = {"ntt_wall_ms": ms, "mu_iter_per_s": its / (ms / 1e3), "rel_error": err,
                      "dims": w.dims, "ranks": w.ranks, "iters_per_step": w.iters}
         del A, cores
-    for name, rows, iters in (("config2", None, 20), ("config5", 32768, 3)):
+    for name, rows, iters in (("config2", None, 20), ("config5", 32768, 10)):
         w = ni.workloads()[name]
         m, n = w.dims
         r = w.ranks[0]
