@@ -160,7 +160,9 @@ k_eig_rank(double* __restrict__ C, int N, double* __restrict__ vg, double* __res
   double* e = d + N;        // N
   double* e2 = e + N;       // N
   double* lam = e2 + N;     // N
-  double* red = lam + N;    // 33
+  vg = lam + N;             // N: Householder vector and p, in shared memory
+  pg = vg + N;              // N (the global vg / pg arguments are not used)
+  double* red = pg + N;     // 33
   const int tid = threadIdx.x, T = blockDim.x;
   // ---- Householder tridiagonalisation, H = I - 2 v v^T with ||v|| = 1
   for (int k = 0; k + 2 < N; ++k) {
@@ -315,7 +317,7 @@ cudaError_t launch_rank_rule(const float* X, int64_t m, int64_t n, int64_t ldx, 
   if (e) return e;
   double* vg = C + (size_t)N * N;
   double* pg = vg + N;
-  const size_t sm = sizeof(double) * (4 * (size_t)N + 40);
+  const size_t sm = sizeof(double) * (6 * (size_t)N + 40);
   e = cudaFuncSetAttribute(k_eig_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e) return e;
   k_eig_rank<<<1, ET, sm, st>>>(C, N, vg, pg, tt_eps, d_eig, d_rank);
@@ -325,7 +327,7 @@ cudaError_t launch_rank_rule(const float* X, int64_t m, int64_t n, int64_t ldx, 
 // eigenvalues (ascending) of a symmetric fp64 N x N matrix C (destroyed), N <= 512;
 // scratch: 2 N doubles; eig: N doubles; rank_dummy: one int (the rank rule output, unused)
 cudaError_t launch_sym_eig(double* C, int N, double* scratch, double* eig, int* rank_dummy, cudaStream_t st) {
-  const size_t sm = sizeof(double) * (4 * (size_t)N + 40);
+  const size_t sm = sizeof(double) * (6 * (size_t)N + 40);
   cudaError_t e = cudaFuncSetAttribute(k_eig_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e) return e;
   k_eig_rank<<<1, ET, sm, st>>>(C, N, scratch, scratch + N, 1.0, eig, rank_dummy);

@@ -73,7 +73,9 @@ k_svd_eig(double* __restrict__ C, int N, double* __restrict__ Vh, double* __rest
   double* e = d + N;                   // N
   double* e2 = e + N;                  // N
   double* lam = e2 + N;                // N
-  double* red = lam + N;               // 40
+  vg = lam + N;                        // N: the Householder vector, in shared memory
+  pg = vg + N;                         // N (the global vg / pg arguments are not used)
+  double* red = pg + N;                // 40
   double* B = red + 40;                // RMAX x (RMAX + 1)
   double* Q = B + RMAX * (RMAX + 1);   // RMAX x (RMAX + 1)
   double* dots = Q + RMAX * (RMAX + 1);  // RMAX
@@ -524,7 +526,7 @@ cudaError_t launch_svd_eig(double* C, int N, char* ws, double tt_eps, int rcap, 
   double* work = pg + N;
   double* Y = work + 6 * (size_t)N * RMAX;
   double* Z = Y + (size_t)N * RMAX;
-  const size_t sm = sizeof(double) * (4 * (size_t)N + 40 + 2 * RMAX * (RMAX + 1) + RMAX + RMAX) + sizeof(int) * (2 * RMAX + 8);
+  const size_t sm = sizeof(double) * (6 * (size_t)N + 40 + 2 * RMAX * (RMAX + 1) + RMAX + RMAX) + sizeof(int) * (2 * RMAX + 8);
   cudaError_t e = cudaFuncSetAttribute(k_svd_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e) return e;
   k_svd_eig<<<1, ST, sm, st>>>(C, N, Vh, vg, pg, work, Y, Z, tt_eps, rcap, eig_asc, lam, d_rank, U);
