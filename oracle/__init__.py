@@ -506,3 +506,28 @@ def tt_svd(A: np.ndarray, tt_eps: float, max_ranks: Optional[Sequence[int]] = No
         rprev = r
     cores.append(T)
     return ranks, np.concatenate(cores), np.array(tails)
+
+
+def ntt_decompose_bcd(A: np.ndarray, ranks, iters: int, seed: int = 0, delta: float = 0.9999) -> np.ndarray:
+    """Alg. 2 with fixed ranks and the paper's own NMF, BCD (Alg. 3 via nmf_bcd,
+    readings R22-R27), at every step: inits W0, H0 from the streams of R20 (as ntt_decompose),
+    core l = W_l, next X = reshape(H_l) (Alg. 2 l.8-10).  Returns packed fp64 cores."""
+    A = np.asarray(A, dtype=np.float64)
+    dims = list(A.shape)
+    d = len(dims)
+    T = A.reshape(-1)
+    rprev, rest = 1, T.size
+    cores = []
+    for l in range(1, d):
+        m = rprev * dims[l - 1]
+        rest //= dims[l - 1]
+        r = int(ranks[l - 1])
+        X = T.reshape(m, rest)
+        W0 = fill_uniform(m * r, seed, stream_w(l)).reshape(m, r)
+        H0 = fill_uniform(r * rest, seed, stream_h(l)).reshape(r, rest)
+        W, H = nmf_bcd(X, W0, H0, iters, delta)
+        cores.append(W.reshape(-1))
+        T = H.reshape(-1)
+        rprev = r
+    cores.append(T)
+    return np.concatenate(cores)
