@@ -157,6 +157,14 @@ ntt_status ntt_decompose_eps(ntt_handle h, const float* A, int32_t d, const int6
 ntt_status ntt_rank_rule(ntt_handle h, const float* X, int64_t m, int64_t n, int64_t ldx, double tt_eps,
                          int32_t* rank, double* eig);
 
+/* nTT with the BCD NMF at every step (Alg. 2 with Alg. 3 as its NMF):
+ * fixed ranks (<= 32), W_l, H_l initialised as ntt_decompose (R20), `iters` BCD
+ * iterations per step (R22-R27, delta as ntt_nmf_bcd), core l = the last accepted
+ * W_l, next unfolding = the last accepted H_l.  A and cores: device or host;
+ * layouts, rel_err and errors as ntt_decompose.  Single-GPU handles.          */
+ntt_status ntt_decompose_bcd(ntt_handle h, const float* A, int32_t d, const int64_t* dims, const int32_t* ranks,
+                             int32_t iters, uint64_t seed, double delta, float* cores, double* rel_err);
+
 /* ------------------------------------------------------------ TT-SVD baseline
  * The unconstrained TT the paper compares nTT against (TT-SVD, P:78, P:88,
  * P:453; SURVEY s.8(f) f4; reading R28): the same sweep and the same rank rule

@@ -204,6 +204,14 @@ class Handle:
                                             ctypes.byref(err) if err is not None else None))
         return [int(x) for x in rk][: d - 1], (float(err.value) if want_error else None)
 
+    def ntt_decompose_bcd(self, A, dims, ranks, iters: int, seed: int, cores, delta: float = 0.9999,
+                          want_error: bool = False) -> Optional[float]:
+        """Alg. 2 with the BCD NMF (Alg. 3) at every step; returns rel_err if asked."""
+        err = ctypes.c_double(-1.0) if want_error else None
+        self._check(lib().ntt_decompose_bcd(self._h, _ptr(A), len(dims), _i64arr(dims), _i32arr(ranks), iters, seed,
+                                            delta, _ptr(cores), ctypes.byref(err) if err is not None else None))
+        return float(err.value) if want_error else None
+
     def ntt_tt_svd(self, A, dims, tt_eps: float, cores, cores_capacity: int, max_ranks=None,
                    want_error: bool = False):
         """TT-SVD baseline (f4) with the rank rule; returns (ranks, rel_err or None)."""

@@ -38,6 +38,7 @@ SIGNATURES = {
     "ntt_decompose_eps": (c_int, [c_p, c_p, c_i32, c_p, c_f64, c_p, c_i32, c_u64, c_f32, c_p, c_i64, c_p, c_p]),
     "ntt_nmf_bcd": (c_int, [c_p, c_p, c_i64, c_i64, c_i64, c_i32, c_i32, c_f64, c_p, c_p, c_p]),
     "ntt_tt_svd": (c_int, [c_p, c_p, c_i32, c_p, c_f64, c_p, c_p, c_i64, c_p, c_p]),
+    "ntt_decompose_bcd": (c_int, [c_p, c_p, c_i32, c_p, c_p, c_i32, c_u64, c_f64, c_p, c_p]),
     "ntt_rank_rule": (c_int, [c_p, c_p, c_i64, c_i64, c_i64, c_f64, ctypes.POINTER(c_i32), c_p]),
     "ntt_generate": (c_int, [c_p, c_i32, c_p, c_p, c_p, c_f32, c_u64, c_u64, c_p]),
     "ntt_compression_ratio": (c_f64, [c_i32, c_p, c_p]),

@@ -1401,6 +1401,77 @@ ntt_status ntt_decompose_eps(ntt_handle h, const float* A, int32_t d, const int6
   return NTT_OK;
 }
 
+// nTT sweep with the paper's BCD NMF at every step (Alg. 2 + Alg. 3).  Sweep buffers are
+// stream-ordered allocations of their own, so the BCD calls may grow the handle workspace.
+ntt_status ntt_decompose_bcd(ntt_handle h, const float* A, int32_t d, const int64_t* dims, const int32_t* ranks,
+                             int32_t iters, uint64_t seed, double delta, float* cores, double* rel_err) {
+  if (!h) return NTT_ERR_INVALID_ARG;
+  if (!A || !cores) return fail(h, NTT_ERR_INVALID_ARG, "null A or cores");
+  if (iters < 0) return fail(h, NTT_ERR_INVALID_ARG, "iters < 0");
+  if (!(delta >= 0.0 && delta < 1.0)) return fail(h, NTT_ERR_INVALID_ARG, "delta must be in [0, 1)");
+  if (h->nranks > 1) return fail(h, NTT_ERR_UNSUPPORTED, "ntt_decompose_bcd runs on a single-GPU handle");
+  TTShape s;
+  ntt_status st = check_tt(h, d, dims, ranks, &s, true);
+  if (st) return st;
+  for (int l = 0; l + 1 < d; ++l)
+    if (ranks[l] > 32) return fail(h, NTT_ERR_RANK, "BCD sweep needs ranks <= 32 (rank %d = %d)", l, ranks[l]);
+  CU(h, cudaSetDevice(h->device));
+  cudaStream_t cs = h->stream;
+  size_t hmax = 1, wmax = 1;
+  {
+    int64_t rest = s.N, rp = 1;
+    for (int l = 1; l < d; ++l) {
+      rest /= s.dims[l - 1];
+      hmax = std::max(hmax, (size_t)(ranks[l - 1] * rest));
+      wmax = std::max(wmax, (size_t)(rp * s.dims[l - 1] * ranks[l - 1]));
+      rp = ranks[l - 1];
+    }
+  }
+  const float* dA = A;
+  if (!is_device_ptr(A)) {
+    if ((st = ensure_stage(h, sizeof(float) * (size_t)s.N))) return st;
+    dA = reinterpret_cast<const float*>(h->stage);
+    CU(h, cudaMemcpyAsync((void*)dA, A, sizeof(float) * (size_t)s.N, cudaMemcpyHostToDevice, cs));
+  }
+  float* buf = nullptr;
+  const size_t nfl = 2 * hmax + wmax + (size_t)s.cores;
+  CU(h, cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(float) * nfl, cs));
+  struct Free {
+    float* p;
+    cudaStream_t st;
+    ~Free() { cudaFreeAsync(p, st); }
+  } fr{buf, cs};
+  float* hb[2] = {buf, buf + hmax};
+  float* Wd = buf + 2 * hmax;
+  float* dcores = Wd + wmax;
+  const float* X = dA;
+  float* Hl = nullptr;
+  int64_t rprev = 1, coff = 0, rest = s.N;
+  for (int l = 1; l < d; ++l) {
+    const int64_t m = rprev * s.dims[l - 1];
+    rest /= s.dims[l - 1];
+    const int r = ranks[l - 1];
+    h->cur_step = l;
+    Hl = hb[(l - 1) & 1];
+    LAUNCH(h, launch_fill_uniform(Wd, m * r, seed, stream_w(l), 0, cs));
+    LAUNCH(h, launch_fill_uniform(Hl, (int64_t)r * rest, seed, stream_h(l), 0, cs));
+    if ((st = ntt_nmf_bcd(h, X, m, rest, rest, r, iters, delta, Wd, Hl, nullptr))) return st;
+    CU(h, cudaMemcpyAsync(dcores + coff, Wd, sizeof(float) * (size_t)(m * r), cudaMemcpyDeviceToDevice, cs));
+    coff += m * r;
+    X = Hl;
+    rprev = r;
+  }
+  h->cur_step = 0;
+  const int64_t ncl = rprev * s.dims[d - 1];
+  CU(h, cudaMemcpyAsync(dcores + coff, Hl, sizeof(float) * (size_t)ncl, cudaMemcpyDeviceToDevice, cs));
+  CU(h, cudaMemcpyAsync(cores, dcores, sizeof(float) * (size_t)s.cores, cudaMemcpyDefault, cs));
+  CU(h, cudaStreamSynchronize(cs));
+  if (rel_err) {
+    if ((st = contract_stream(h, s, cores, nullptr, 0.0f, 0, A, rel_err))) return st;
+  }
+  return NTT_OK;
+}
+
 // TT-SVD baseline (SURVEY s.8(f) f4, reading R28; tt_svd.cu).  Same sweep, shapes and rank
 // rule as ntt_decompose_eps; the NMF of each step is replaced by the truncated SVD.
 ntt_status ntt_tt_svd(ntt_handle h, const float* A, int32_t d, const int64_t* dims, double tt_eps,

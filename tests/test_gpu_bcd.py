@@ -125,3 +125,23 @@ def test_bcd_fullsize_properties(h):
     h.ntt_nmf_mu(X.view(-1), m, n, n, r, iters, 1e-16, Wm, Hm)
     res_mu = 0.5 * float(((Xd - Wm.view(m, r).double() @ Hm.view(r, n).double()) ** 2).sum())
     assert res < res_mu
+
+
+@pytest.mark.parametrize("dims,ranks,iters", [((5, 4, 5, 6), (4, 3, 2), 10), ((6, 6, 6, 6, 6), (5, 5, 5, 5), 8),
+                                              ((300, 20, 40), (12, 9), 6)])
+def test_ntt_bcd_sweep_parity(h, ora, dims, ranks, iters):
+    """nTT with BCD at every step (Alg. 2 + Alg. 3) against oracle.ntt_decompose_bcd: cores
+    1e-4 relative per core (R14), Eq. 3 error within 1e-3 (R15)."""
+    import paper_2008_01340_b200 as P
+    rng = np.random.default_rng(sum(dims))
+    A = (ora.tt_full(list(dims), list(ranks), rng.random(ora.cores_size(list(dims), list(ranks))))
+         + 0.01 * rng.random(dims)).astype(np.float32)
+    cores = torch.empty(P.cores_size(list(dims), list(ranks)), device="cuda")
+    err = h.ntt_decompose_bcd(torch.from_numpy(A.ravel()).cuda(), list(dims), list(ranks), iters, 0, cores,
+                              want_error=True)
+    co = ora.ntt_decompose_bcd(A, list(ranks), iters)
+    cg = cores.cpu().numpy().astype(np.float64)
+    for Gg, Go in zip(ora.unpack_cores(list(dims), list(ranks), cg), ora.unpack_cores(list(dims), list(ranks), co)):
+        assert np.abs(Gg - Go).max() <= 1e-4 * np.abs(Go).max()
+    e_ora = ora.rel_error(A, ora.tt_full(list(dims), list(ranks), co))
+    assert abs(err - e_ora) <= 1e-3 * e_ora + 1e-6
