@@ -6,7 +6,7 @@
 // Kernels (any m x n, r <= 32; fp32 storage, fp64 for every sum and small matrix):
 //   k_bcd_w      W = max(0, W_m - (W_m Q - P) / L_W), per row; column L1 partials
 //   k_bcd_wnorm  W[:,k] /= c_k, W_prev[:,k] /= c_k (and G partials of the new W)
-//   k_bcd_hnorm  H_m[k,:] *= c_k, H_prev[k,:] *= c_k
+//   k_bcd_hscale the same for H through row-scale vectors of H_m and H_prev (no H traffic)
 //   k_bcd_spart  split-K partials of S = W^T X (FFMA path; the tensor-core path
 //                produces the same [split][j][k] layout with k_skinny_tc16<R, 1>)
 //   k_bcd_hup    S = sum of the partials, E = G H_m, H = max(0, H_m - (E - S) / L_H)
@@ -105,16 +105,13 @@ k_bcd_wnorm(float* __restrict__ W, float* __restrict__ Wp, int64_t m, int r, con
   }
 }
 
-__global__ void k_bcd_hnorm(float* __restrict__ Hm, float* __restrict__ Hp, int r, int64_t n,
-                            const double* __restrict__ c) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)r * n;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int k = (int)(e / n);
-    const double ck = c[k];
-    if (ck > 0.0) {
-      Hm[e] = (float)((double)Hm[e] * ck);
-      Hp[e] = (float)((double)Hp[e] * ck);
-    }
+// l.9 compensation on the H side without touching H: the logical H_m and H_prev are
+// diag(sH[0..r)) Hm and diag(sH[R..R+r)) Hp (sH: [2][32]); their rows scale by c_k
+__global__ void k_bcd_hscale(double* __restrict__ sH, int r, const double* __restrict__ c) {
+  const int k = threadIdx.x;
+  if (k < r && c[k] > 0.0) {
+    sH[k] *= c[k];
+    sH[32 + k] *= c[k];
   }
 }
 
@@ -163,6 +160,62 @@ k_bcd_spart(const float* __restrict__ X, int64_t ldx, int64_t m, int64_t n, cons
   }
 }
 
+// S = W^T X and the H step in one pass when the rows are not split (short-wide X): thread j
+// owns column j, S in fp32 per 128-row chunk and fp64 across (as k_bcd_spart), then
+// H[:, j] = max(0, Hm - (G Hm - S) / L_H) with Hm = diag(sHm) Hm_stored, no S partials
+template <int R>
+__global__ void __launch_bounds__(BH_BN)
+k_bcd_shup(const float* __restrict__ X, int64_t ldx, int64_t m, int64_t n, const float* __restrict__ W, int r,
+           const double* __restrict__ G, const double* __restrict__ LH, const float* __restrict__ Hm,
+           const double* __restrict__ sHm, float* __restrict__ H) {
+  __shared__ float Ws[BH_MCH * R];
+  __shared__ double Gs[R * R];
+  for (int t = threadIdx.x; t < R * R; t += blockDim.x) {
+    const int k = t / R, l = t % R;
+    Gs[t] = (k < r && l < r) ? G[k * r + l] : 0.0;
+  }
+  const double L = *LH;
+  const int64_t j = (int64_t)blockIdx.x * BH_BN + threadIdx.x;
+  const bool valid = j < n;
+  double Sd[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) Sd[k] = 0.0;
+  for (int64_t c0 = 0; c0 < m; c0 += BH_MCH) {
+    const int rows = (int)min((int64_t)BH_MCH, m - c0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < BH_MCH * R; e += blockDim.x) {
+      const int ii = e / R, kk = e % R;
+      Ws[e] = (ii < rows && kk < r) ? W[(c0 + ii) * r + kk] : 0.0f;
+    }
+    __syncthreads();
+    float S[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) S[k] = 0.0f;
+    if (valid)
+      for (int ii = 0; ii < rows; ++ii) {
+        const float x = X[(c0 + ii) * ldx + j];
+#pragma unroll
+        for (int k = 0; k < R; ++k) S[k] = fmaf(Ws[ii * R + k], x, S[k]);
+      }
+#pragma unroll
+    for (int k = 0; k < R; ++k) Sd[k] += (double)S[k];
+  }
+  if (!valid) return;
+  double hm[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) hm[k] = (k < r) ? (double)Hm[(int64_t)k * n + j] * sHm[k] : 0.0;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    if (k < r) {
+      double e = -Sd[k];
+#pragma unroll
+      for (int l = 0; l < R; ++l) e += Gs[k * R + l] * hm[l];
+      const double v = L > 0.0 ? fmax(0.0, hm[k] - e / L) : hm[k];
+      H[(int64_t)k * n + j] = (float)v;
+    }
+  }
+}
+
 // H = max(0, H_m - (G H_m - S) / L_H) per column j, S = sum_s Spart[s][j][:] (fixed order).
 // The 128 columns of a block own a contiguous run of 128 r doubles in every split: each
 // thread sums fixed elements of that run over the splits (coalesced), then reads its column
@@ -170,8 +223,8 @@ k_bcd_spart(const float* __restrict__ X, int64_t ldx, int64_t m, int64_t n, cons
 template <int R>
 __global__ void __launch_bounds__(BH_BN)
 k_bcd_hup(const double* __restrict__ Spart, int nS, int64_t n, int r, const double* __restrict__ G,
-          const double* __restrict__ LH, const float* __restrict__ Hm, float* __restrict__ H,
-          unsigned* __restrict__ maxh) {
+          const double* __restrict__ LH, const float* __restrict__ Hm, const double* __restrict__ sHm,
+          float* __restrict__ H, unsigned* __restrict__ maxh) {
   __shared__ double Gs[R * R];
   __shared__ double Ss[BH_BN * R];
   for (int t = threadIdx.x; t < R * R; t += blockDim.x) {
@@ -207,7 +260,7 @@ k_bcd_hup(const double* __restrict__ Spart, int nS, int64_t n, int r, const doub
       const int64_t j = j0 + threadIdx.x;
       double hm[R];
 #pragma unroll
-      for (int k = 0; k < R; ++k) hm[k] = (k < r) ? (double)Hm[(int64_t)k * n + j] : 0.0;
+      for (int k = 0; k < R; ++k) hm[k] = (k < r) ? (double)Hm[(int64_t)k * n + j] * sHm[k] : 0.0;
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         if (k < r) {
@@ -401,13 +454,51 @@ __global__ void k_bcd_commit(const float* __restrict__ V, float* __restrict__ Vm
   }
 }
 
+// H side of l.18-27 with the scale vectors: Hp = diag(sHp) Hp_stored.  Accepted:
+// Hm = H + w_H (H - Hp), Hp = H; correction: Hm = Hp.  Element e is (k = e / n, j).
+__global__ void k_bcd_commit_h(const float* __restrict__ H, float* __restrict__ Hm, float* __restrict__ Hp, int r,
+                               int64_t n, const double* __restrict__ sH, const double* __restrict__ bs) {
+  const bool acc = bs[BS_ACC] != 0.0;
+  const double w = bs[BS_WH];
+  for (int k = blockIdx.y; k < r; k += gridDim.y) {
+    const double sp = sH[32 + k];
+    const int64_t base = (int64_t)k * n;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+      const double vp = (double)Hp[base + j] * sp;
+      if (acc) {
+        const double v = H[base + j];
+        Hm[base + j] = (float)(v + w * (v - vp));
+        Hp[base + j] = (float)v;
+      } else {
+        Hm[base + j] = (float)vp;
+      }
+    }
+  }
+}
+
+// out[k][j] = sH[32 + k] Hp[k][j] (the logical H_prev, returned at the end) or, with init,
+// sH[0..64) = 1
+__global__ void k_bcd_hout(const float* __restrict__ Hp, int r, int64_t n, double* __restrict__ sH,
+                           float* __restrict__ out, int init) {
+  if (init) {
+    if (blockIdx.x == 0 && threadIdx.x < 64) sH[threadIdx.x] = 1.0;
+    return;
+  }
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)r * n; e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = (float)((double)Hp[e] * sH[32 + (int)(e / n)]);
+}
+
 // accepted: P = X H^T, Q = H H^T of the new H (Pn, Qn).  Correction: H_prev was rescaled
 // by c in l.9 (rows k x c_k), so X H_prev^T = P diag(c) and H_prev H_prev^T = diag(c) Q diag(c)
 // (R26: the same matrices the oracle recomputes from H_prev, without another pass over X)
 __global__ void k_bcd_commit_pq(double* __restrict__ Pc, const double* __restrict__ Pn, int64_t m, int r,
                                 double* __restrict__ Qc, const double* __restrict__ Qn, const double* __restrict__ c,
-                                const double* __restrict__ bs) {
+                                const double* __restrict__ bs, double* __restrict__ sH) {
   const bool acc = bs[BS_ACC] != 0.0;
+  if (blockIdx.x == 0 && threadIdx.x < 32) {  // Hm is stored fresh; Hp too when accepted
+    sH[threadIdx.x] = 1.0;
+    if (acc) sH[32 + threadIdx.x] = 1.0;
+  }
   const int64_t mr = m * r, tot = mr + (int64_t)r * r;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
     if (e < mr) {
@@ -497,8 +588,32 @@ cudaError_t launch_bcd_wnorm(float* W, float* Wp, int64_t m, int r, const double
   return cudaGetLastError();
 }
 
-cudaError_t launch_bcd_hnorm(float* Hm, float* Hp, int r, int64_t n, const double* c, cudaStream_t st) {
-  k_bcd_hnorm<<<1184, 256, 0, st>>>(Hm, Hp, r, n, c);
+cudaError_t launch_bcd_hscale(double* sH, int r, const double* c, cudaStream_t st) {
+  k_bcd_hscale<<<1, 32, 0, st>>>(sH, r, c);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bcd_commit_h(const float* H, float* Hm, float* Hp, int r, int64_t n, const double* sH,
+                                const double* bs, cudaStream_t st) {
+  const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 1184 / std::max(r, 1) + 1));
+  k_bcd_commit_h<<<dim3((unsigned)gx, (unsigned)r), 256, 0, st>>>(H, Hm, Hp, r, n, sH, bs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bcd_shup(const float* X, int64_t ldx, int64_t m, int64_t n, const float* W, int r, const double* G,
+                            const double* LH, const float* Hm, const double* sHm, float* H, cudaStream_t st) {
+  const unsigned g = (unsigned)((n + BH_BN - 1) / BH_BN);
+  switch (rcls_bcd(r)) {
+    case 4: k_bcd_shup<4><<<g, BH_BN, 0, st>>>(X, ldx, m, n, W, r, G, LH, Hm, sHm, H); break;
+    case 8: k_bcd_shup<8><<<g, BH_BN, 0, st>>>(X, ldx, m, n, W, r, G, LH, Hm, sHm, H); break;
+    case 16: k_bcd_shup<16><<<g, BH_BN, 0, st>>>(X, ldx, m, n, W, r, G, LH, Hm, sHm, H); break;
+    default: k_bcd_shup<32><<<g, BH_BN, 0, st>>>(X, ldx, m, n, W, r, G, LH, Hm, sHm, H); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bcd_hout(const float* Hp, int r, int64_t n, double* sH, float* out, int init, cudaStream_t st) {
+  k_bcd_hout<<<init ? 1 : 1184, 256, 0, st>>>(Hp, r, n, sH, out, init);
   return cudaGetLastError();
 }
 
@@ -525,14 +640,14 @@ cudaError_t launch_bcd_spart(const float* X, int64_t ldx, int64_t m, int64_t n, 
 }
 
 cudaError_t launch_bcd_hup(const double* Spart, int nS, int64_t n, int r, const double* G, const double* LH,
-                           const float* Hm, float* H, unsigned* maxh, int num_sms, cudaStream_t st) {
+                           const float* Hm, const double* sHm, float* H, unsigned* maxh, int num_sms, cudaStream_t st) {
   int64_t g = (n + BH_BN - 1) / BH_BN;
   if (g > 4 * num_sms) g = 4 * num_sms;
   switch (rcls_bcd(r)) {
-    case 4: k_bcd_hup<4><<<(unsigned)g, BH_BN, 0, st>>>(Spart, nS, n, r, G, LH, Hm, H, maxh); break;
-    case 8: k_bcd_hup<8><<<(unsigned)g, BH_BN, 0, st>>>(Spart, nS, n, r, G, LH, Hm, H, maxh); break;
-    case 16: k_bcd_hup<16><<<(unsigned)g, BH_BN, 0, st>>>(Spart, nS, n, r, G, LH, Hm, H, maxh); break;
-    default: k_bcd_hup<32><<<(unsigned)g, BH_BN, 0, st>>>(Spart, nS, n, r, G, LH, Hm, H, maxh); break;
+    case 4: k_bcd_hup<4><<<(unsigned)g, BH_BN, 0, st>>>(Spart, nS, n, r, G, LH, Hm, sHm, H, maxh); break;
+    case 8: k_bcd_hup<8><<<(unsigned)g, BH_BN, 0, st>>>(Spart, nS, n, r, G, LH, Hm, sHm, H, maxh); break;
+    case 16: k_bcd_hup<16><<<(unsigned)g, BH_BN, 0, st>>>(Spart, nS, n, r, G, LH, Hm, sHm, H, maxh); break;
+    default: k_bcd_hup<32><<<(unsigned)g, BH_BN, 0, st>>>(Spart, nS, n, r, G, LH, Hm, sHm, H, maxh); break;
   }
   return cudaGetLastError();
 }
@@ -573,10 +688,10 @@ cudaError_t launch_bcd_commit(const float* V, float* Vm, float* Vp, int64_t cnt,
 }
 
 cudaError_t launch_bcd_commit_pq(double* Pc, const double* Pn, int64_t m, int r, double* Qc, const double* Qn,
-                                 const double* c, const double* bs, cudaStream_t st) {
+                                 const double* c, const double* bs, double* sH, cudaStream_t st) {
   const int64_t tot = m * r + (int64_t)r * r;
   const int64_t g = std::min<int64_t>(1184, (tot + 255) / 256);
-  k_bcd_commit_pq<<<(unsigned)g, 256, 0, st>>>(Pc, Pn, m, r, Qc, Qn, c, bs);
+  k_bcd_commit_pq<<<(unsigned)g, 256, 0, st>>>(Pc, Pn, m, r, Qc, Qn, c, bs, sH);
   return cudaGetLastError();
 }
 

@@ -91,12 +91,17 @@ cudaError_t launch_bcd_w(const float* Wm, int64_t m, int r, const double* P, con
                          float* W, double* cpart, cudaStream_t st);
 cudaError_t launch_bcd_wnorm(float* W, float* Wp, int64_t m, int r, const double* c, double* Gpart, unsigned* maxw,
                              cudaStream_t st);
-cudaError_t launch_bcd_hnorm(float* Hm, float* Hp, int r, int64_t n, const double* c, cudaStream_t st);
+cudaError_t launch_bcd_hscale(double* sH, int r, const double* c, cudaStream_t st);
+cudaError_t launch_bcd_hout(const float* Hp, int r, int64_t n, double* sH, float* out, int init, cudaStream_t st);
+cudaError_t launch_bcd_commit_h(const float* H, float* Hm, float* Hp, int r, int64_t n, const double* sH,
+                                const double* bs, cudaStream_t st);
+cudaError_t launch_bcd_shup(const float* X, int64_t ldx, int64_t m, int64_t n, const float* W, int r, const double* G,
+                            const double* LH, const float* Hm, const double* sHm, float* H, cudaStream_t st);
 int bcd_spart_splits(int64_t m, int64_t n, int num_sms);
 cudaError_t launch_bcd_spart(const float* X, int64_t ldx, int64_t m, int64_t n, const float* W, int r, int nsplit,
                              double* Spart, cudaStream_t st);
 cudaError_t launch_bcd_hup(const double* Spart, int nS, int64_t n, int r, const double* G, const double* LH,
-                           const float* Hm, float* H, unsigned* maxh, int num_sms, cudaStream_t st);
+                           const float* Hm, const double* sHm, float* H, unsigned* maxh, int num_sms, cudaStream_t st);
 int bcd_dot_ctas(int64_t len, int num_sms);
 cudaError_t launch_bcd_psum_dot(const double* part, int nparts, int64_t len, const float* W, double* P,
                                 double* dotpart, int num_sms, cudaStream_t st);
@@ -107,7 +112,7 @@ cudaError_t launch_bcd_decide(double* bs, double* trace, const double* dotpart, 
 cudaError_t launch_bcd_commit(const float* V, float* Vm, float* Vp, int64_t cnt, const double* bs, int widx,
                               cudaStream_t st);
 cudaError_t launch_bcd_commit_pq(double* Pc, const double* Pn, int64_t m, int r, double* Qc, const double* Qn,
-                                 const double* c, const double* bs, cudaStream_t st);
+                                 const double* c, const double* bs, double* sH, cudaStream_t st);
 cudaError_t launch_scale_copy(const float* src, float* a, float* b, int64_t cnt, const double* num, const double* den,
                               cudaStream_t st);
 int sumsq_ctas();

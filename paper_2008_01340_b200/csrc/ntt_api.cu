@@ -1122,6 +1122,9 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   const XhtPlan xp = plan_xht(m, n, h->num_sms), qp = plan_xht(r, n, h->num_sms);
   const int nwc = bcd_w_ctas(m);
   const int nS = tc ? tp.splitH16 : bcd_spart_splits(m, n, h->num_sms);
+  // short-wide X (r <= 8, m <= 256): P, Q from the 1-pass fused kernel's acc-only mode
+  const bool fa = !tc && fused_supported(m, n, r, ldx, X, H) && !getenv("NTT_BCD_NO_FUSED");
+  const int fparts = fa ? fused_partials(m, n, r, h->num_sms) : 0;
   size_t o = 0;
   auto take = [&](size_t b) {
     size_t at = o;
@@ -1133,9 +1136,10 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   const size_t oP0 = take(sizeof(double) * m * r), oP1 = take(sizeof(double) * m * r);
   const size_t oQ0 = take(sizeof(double) * r * r), oQ1 = take(sizeof(double) * r * r);
   const size_t oG = take(sizeof(double) * r * r), oC = take(sizeof(double) * r);
-  const size_t oPp = tc ? 0 : take(sizeof(double) * (size_t)xp.ncs * m * r);
-  const size_t oSp = tc ? 0 : take(sizeof(double) * (size_t)nS * n * r);
-  const size_t oQp = take(sizeof(double) * (size_t)qp.ncs * r * r);
+  const size_t oPp = tc ? 0 : take(sizeof(double) * (size_t)std::max(xp.ncs, fparts) * m * r);
+  const size_t oSp = (tc || nS == 1) ? 0 : take(sizeof(double) * (size_t)nS * n * r);
+  const size_t oQp = take(sizeof(double) * (size_t)std::max(qp.ncs, fparts) * r * r);
+  const size_t oSH = take(sizeof(double) * 64);  // row scales of H_m, H_prev (k_bcd_hscale)
   const size_t oCp = take(sizeof(double) * (size_t)nwc * r), oGp = take(sizeof(double) * (size_t)nwc * r * r);
   const int ndot = bcd_dot_ctas(m * r, h->num_sms);
   const size_t oD = take(sizeof(double) * ndot), oSq = take(sizeof(double) * sumsq_ctas());
@@ -1164,7 +1168,8 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   char* tws = ws + oTc;
   double* Ppart = tc ? reinterpret_cast<double*>(tws + tp.off_P) : reinterpret_cast<double*>(ws + oPp);
   double* Spart = tc ? reinterpret_cast<double*>(tws + tp.off_S) : reinterpret_cast<double*>(ws + oSp);
-  const int nP = tc ? tp.splitW16 : xp.ncs;
+  const int nP = tc ? tp.splitW16 : fa ? fparts : xp.ncs;
+  double* sH = reinterpret_cast<double*>(ws + oSH);
   TcMaps maps;
   unsigned* mxh = tc ? tc16_max_slot(tp, tws, 5) : nullptr;  // max H, then max W (slot 6)
   unsigned* mxw = tc ? tc16_max_slot(tp, tws, 6) : nullptr;
@@ -1183,13 +1188,17 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
       if (in_iter) LAUNCH(h, tc16_pack_h_slot(tp, Hs, tws, st, 5));
       else LAUNCH(h, tc16_pack_h_fresh(tp, Hs, tws, st));
       PLAUNCH(h, 6, xbytes, tc16_pass_w(tp, maps, tws, bef, st, bflush));
+    } else if (fa) {  // one pass: P = X H^T and Q = H H^T partials per CTA
+      PLAUNCH(h, 1, xbytes + 4.0 * r * (double)n,
+              launch_fused(X, ldx, m, n, r, W, nullptr, 0, 0.0f, const_cast<float*>(Hs), Ppart, Qpart, kFusedAcc,
+                           fused_grid(m, n, r, h->num_sms), st));
     } else {
       PLAUNCH(h, 1, xbytes, launch_xht_partial(X, ldx, m, n, Hs, n, r, xp, Ppart, st));
     }
     LAUNCH(h, launch_bcd_psum_dot(Ppart, nP, m * r, in_iter ? W : nullptr, P, in_iter ? dotpart : nullptr,
                                   h->num_sms, st));
-    LAUNCH(h, launch_xht_partial(Hs, n, r, n, Hs, n, r, qp, Qpart, st));
-    LAUNCH(h, launch_sum_partials(Qpart, qp.ncs, (int64_t)r * r, Q, st));
+    if (!fa) LAUNCH(h, launch_xht_partial(Hs, n, r, n, Hs, n, r, qp, Qpart, st));
+    LAUNCH(h, launch_sum_partials(Qpart, fa ? fparts : qp.ncs, (int64_t)r * r, Q, st));
     return NTT_OK;
   };
   // ---- init (Alg. 3 l.1-4, R22, R23)
@@ -1206,6 +1215,7 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   if (!(xx > 0.0)) return fail(h, NTT_ERR_DEGENERATE, "||X|| = 0");
   LAUNCH(h, launch_scale_copy(W, Wm, Wp, m * r, bs + BS_XX, bs + BS_W0, st));
   LAUNCH(h, launch_scale_copy(H, Hm, Hp, (int64_t)r * n, bs + BS_XX, bs + BS_H0, st));
+  LAUNCH(h, launch_bcd_hout(Hp, r, n, sH, nullptr, 1, st));  // sH = 1
   if (tc) {
     LAUNCH(h, tc_prepare(tp, X, ldx, Hp, tws, &maps, st));
     LAUNCH(h, tc16_prepare(tp, X, ldx, Hp, tws, &maps, st));
@@ -1222,21 +1232,24 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
     LAUNCH(h, launch_bcd_w(Wm, m, r, Pc, Qc, bs + BS_LW, W, cpart, st));          // l.6-8
     LAUNCH(h, launch_sum_partials(cpart, nwc, r, c, st));
     LAUNCH(h, launch_bcd_wnorm(W, Wp, m, r, c, Gpart, mxw, st));                  // l.9 (R24)
-    LAUNCH(h, launch_bcd_hnorm(Hm, Hp, r, n, c, st));
+    LAUNCH(h, launch_bcd_hscale(sH, r, c, st));
     LAUNCH(h, launch_sum_partials(Gpart, nwc, (int64_t)r * r, G, st));             // l.10
     if ((s = spec(G, bs + BS_LH))) return s;
     if (tc) {                                                                     // S = W^T X
       LAUNCH(h, tc16_pack_w_slot(tp, W, tws, st, 6));
       PLAUNCH(h, 7, xbytes, tc16_pass_h(tp, maps, tws, bef, st, bflush));
-    } else {
-      PLAUNCH(h, 5, xbytes, launch_bcd_spart(X, ldx, m, n, W, r, nS, Spart, st));
     }
-    LAUNCH(h, launch_bcd_hup(Spart, nS, n, r, G, bs + BS_LH, Hm, H, mxh, h->num_sms, st));  // l.11-14
+    if (!tc && nS == 1) {  // S and the H step in one pass (l.11-14)
+      PLAUNCH(h, 5, xbytes + 8.0 * r * (double)n, launch_bcd_shup(X, ldx, m, n, W, r, G, bs + BS_LH, Hm, sH, H, st));
+    } else {
+      if (!tc) PLAUNCH(h, 5, xbytes, launch_bcd_spart(X, ldx, m, n, W, r, nS, Spart, st));
+      LAUNCH(h, launch_bcd_hup(Spart, nS, n, r, G, bs + BS_LH, Hm, sH, H, mxh, h->num_sms, st));  // l.11-14
+    }
     if ((s = pq(H, Pn, Qn, true))) return s;                                               // l.15
     LAUNCH(h, launch_bcd_decide(bs, dtrace, dotpart, ndot, G, Qn, r, mxh, st));             // l.16-17 (R25)
     LAUNCH(h, launch_bcd_commit(W, Wm, Wp, m * r, bs, BS_WW, st));                    // l.18-27
-    LAUNCH(h, launch_bcd_commit(H, Hm, Hp, (int64_t)r * n, bs, BS_WH, st));
-    LAUNCH(h, launch_bcd_commit_pq(Pc, Pn, m, r, Qc, Qn, c, bs, st));
+    LAUNCH(h, launch_bcd_commit_h(H, Hm, Hp, r, n, sH, bs, st));
+    LAUNCH(h, launch_bcd_commit_pq(Pc, Pn, m, r, Qc, Qn, c, bs, sH, st));
     return NTT_OK;
   };
   const char* ge = getenv("NTT_BCD_GRAPH");
@@ -1279,7 +1292,7 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   }
   // the last accepted iterates (l.28)
   CU(h, cudaMemcpyAsync(W, Wp, sizeof(float) * m * r, cudaMemcpyDeviceToDevice, st));
-  CU(h, cudaMemcpyAsync(H, Hp, sizeof(float) * r * n, cudaMemcpyDeviceToDevice, st));
+  LAUNCH(h, launch_bcd_hout(Hp, r, n, sH, H, 0, st));  // logical H_prev = diag(sHp) Hp
   if (objective_trace && iters > 0)
     CU(h, cudaMemcpyAsync(objective_trace, dtrace, sizeof(double) * iters, cudaMemcpyDeviceToHost, st));
   CU(h, cudaStreamSynchronize(st));
