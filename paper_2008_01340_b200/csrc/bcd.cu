@@ -308,13 +308,16 @@ k_bcd_psum_dot(const double* __restrict__ part, int nparts, int64_t len, const f
 // Repeated squaring A <- A^2 / max diag(A^2) drives A to the scaled projector onto the top
 // eigenspace (stopped when A stops changing, at most 64 squarings = M^(2^64)); the Rayleigh
 // quotient of M on the column of A with the largest diagonal entry is then lambda_max with an
-// error quadratic in the eigenvector error.  One CTA of 1024 threads, thread (i, j) owns A[i][j].
-__global__ void __launch_bounds__(1024) k_spec_norm(const double* __restrict__ M, int r, double* __restrict__ out) {
-  __shared__ double A[32][33];
-  __shared__ double Ms[32][33];
+// error quadratic in the eigenvector error.  One CTA of RP^2 threads (RP = 8, 16, 32 >= r),
+// thread (i, j) owns A[i][j]: small ranks pay for 2 warps, not 32.
+template <int RP>
+__global__ void __launch_bounds__(RP * RP) k_spec_norm(const double* __restrict__ M, int r, double* __restrict__ out) {
+  constexpr int NW = RP * RP / 32;
+  __shared__ double A[RP][RP + 1];
+  __shared__ double Ms[RP][RP + 1];
   __shared__ double red[32];
   __shared__ double bc[2];
-  const int t = threadIdx.x, i = t >> 5, j = t & 31, lane = t & 31, w = t >> 5;
+  const int t = threadIdx.x, i = t / RP, j = t % RP, lane = t & 31, w = t >> 5;
   const bool in = i < r && j < r;
   const double mv = in ? M[i * r + j] : 0.0;
   Ms[i][j] = mv;
@@ -336,12 +339,12 @@ __global__ void __launch_bounds__(1024) k_spec_norm(const double* __restrict__ M
   for (int it = 0; it < 64; ++it) {
     double c = 0.0;
 #pragma unroll 8
-    for (int k = 0; k < 32; ++k) c += A[i][k] * A[k][j];
+    for (int k = 0; k < RP; ++k) c += A[i][k] * A[k][j];
     __syncthreads();
     if (i == j) red[i] = c;
     __syncthreads();
     if (t < 32) {
-      double d = red[t];
+      double d = (t < RP) ? red[t] : 0.0;
       for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
       if (t == 0) bc[0] = d;
     }
@@ -353,7 +356,7 @@ __global__ void __launch_bounds__(1024) k_spec_norm(const double* __restrict__ M
     if (lane == 0) red[w] = diff;
     __syncthreads();
     if (t < 32) {
-      double d = red[t];
+      double d = (t < NW) ? red[t] : 0.0;
       for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
       if (t == 0) bc[1] = d;
     }
@@ -386,15 +389,15 @@ __global__ void __launch_bounds__(1024) k_spec_norm(const double* __restrict__ M
   den = warp_sum(den);
   __syncthreads();
   if (lane == 0) {
-    A[w][0] = num;
-    A[w][1] = den;
+    red[w] = num;
+    A[w][0] = den;
   }
   __syncthreads();
   if (t == 0) {
     double sn = 0.0, sd = 0.0;
-    for (int q = 0; q < 32; ++q) {
-      sn += A[q][0];
-      sd += A[q][1];
+    for (int q = 0; q < NW; ++q) {
+      sn += red[q];
+      sd += A[q][0];
     }
     *out = sd > 0.0 ? sn / sd : 0.0;
   }
@@ -665,7 +668,9 @@ cudaError_t launch_bcd_psum_dot(const double* part, int nparts, int64_t len, con
 
 cudaError_t launch_spec_norm(const double* M, int r, double* out, cudaStream_t st) {
   if (r > 32) return cudaErrorInvalidValue;
-  k_spec_norm<<<1, 1024, 0, st>>>(M, r, out);
+  if (r <= 8) k_spec_norm<8><<<1, 64, 0, st>>>(M, r, out);
+  else if (r <= 16) k_spec_norm<16><<<1, 256, 0, st>>>(M, r, out);
+  else k_spec_norm<32><<<1, 1024, 0, st>>>(M, r, out);
   return cudaGetLastError();
 }
 
