@@ -58,3 +58,28 @@ for name in which:
     print(json.dumps(row), flush=True)
     del X, W, H, W0, H0
     torch.cuda.empty_cache()
+
+# nTT sweeps with BCD at every step (ntt_decompose_bcd) next to the MU sweep, configs 3 and 4
+if len(sys.argv) > 3 and sys.argv[3] == "sweep":
+    for name in ("config3", "config4"):
+        w = ni.workloads()[name]
+        cores0 = torch.from_numpy(ni.make_cores(w.dims, w.ranks, w.seed).astype(np.float32)).cuda()
+        A = torch.empty(w.numel, device="cuda")
+        h.ntt_generate(w.dims, w.ranks, cores0, w.noise_amp, w.seed, ni.STREAM_NOISE, A)
+        cores = torch.empty(P.cores_size(w.dims, w.ranks), device="cuda")
+        row = {"workload": name, "iters_per_step": w.iters}
+        for alg in ("bcd", "mu"):
+            f = (lambda: h.ntt_decompose_bcd(A, w.dims, w.ranks, w.iters, w.seed, cores, want_error=True)) \
+                if alg == "bcd" else \
+                (lambda: h.ntt_decompose(A, w.dims, w.ranks, w.iters, w.seed, 1e-16, cores, want_error=True))
+            f()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            err = f()
+            e1.record()
+            torch.cuda.synchronize()
+            row[alg] = {"wall_ms": e0.elapsed_time(e1), "rel_err": err}
+        print(json.dumps(row), flush=True)
+        del A, cores
+        torch.cuda.empty_cache()

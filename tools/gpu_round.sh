@@ -1,4 +1,2 @@
 set -x
-timeout 600 python -m pytest tests/test_gpu_bcd.py -q > gpurun_out/pytest_bcd.log 2>&1; echo "bcd rc $?"; grep -E "^E  |passed|failed" gpurun_out/pytest_bcd.log | head -30
-timeout 900 python tools/bench_bcd.py config2 20 sweep 2>&1 | tail -3
-timeout 900 python tools/bench_bcd.py config5 20 2>&1 | tail -1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_fused_c -c 1 -o gpurun_out/fused_c_step2 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-other > gpurun_out/ncu_fc.log 2>&1; echo "ncu rc $?"; tail -3 gpurun_out/ncu_fc.log
