@@ -272,6 +272,8 @@ struct MuPlan {
   int nwup;       // W-update CTAs
   int fgrid;      // fused kernel CTAs
   int fparts;     // fused kernel partial slots
+  bool small = false;  // m <= 8: register-resident pass (mu_small.cu)
+  int sgrid = 0;       // its CTAs (= partial slots)
   bool tc;        // tensor-core 2-pass path (mu_tc.cu) for tall / square X
   TcPlan tp;
   bool persist;   // fused path as one persistent cooperative launch per call
@@ -294,6 +296,15 @@ MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, int nranks) {
   p.nwup = wupdate_ctas(m, r);
   p.fgrid = fused_grid(m, n, r, num_sms);
   p.fparts = fused_partials(m, n, r, num_sms);
+  // m <= 8: the register-resident pass of mu_small.cu (opt-in, NTT_SMALL=1: on config 4
+  // step 1 it ties the persistent warp-tile kernel at 3.27 TB/s -- both are held by an
+  // uneven DRAM channel load, DESIGN.md s.6 -- and adds a W-update launch per iteration)
+  {
+    const char* se = getenv("NTT_SMALL");
+    p.small = small_supported(m, n, r, n, nullptr, nullptr) && se && se[0] == '1';
+  }
+  p.sgrid = small_grid(n, num_sms);
+  if (p.small) p.fparts = std::max(p.fparts, p.sgrid);
   int64_t nP = std::max<int64_t>({(int64_t)p.xp.ncs, p.acc ? p.hgrid : 0, (int64_t)p.fparts, 1});
   int64_t nQ = std::max<int64_t>({(int64_t)p.qp.ncs, p.acc ? p.hgrid : 0, (int64_t)p.fparts, 1});
   int64_t nG = std::max<int64_t>({(int64_t)p.nwup, (int64_t)wupdate2_ctas(m, r), 1});
@@ -351,6 +362,29 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
     // tiny mode: every iteration in one CTA from shared memory (mu_tiny.cu)
     PLAUNCH(h, 0, (double)iters * 4.0 * (double)(m + 2 * r) * (double)n,
             launch_tiny(X, ldx, m, n, r, iters, eps, W, H, st));
+    return NTT_OK;
+  }
+  if (p.small && small_supported(m, n, r, ldx, X, H)) {
+    // 1-pass with the register-resident small-m pass: prologue P0, Q0; then per iteration
+    // W update (reduces the partials) -> pass (H update + next P, Q)
+    const int fg = p.sgrid;
+    const int nG = wupdate2_ctas(m, r);
+    PLAUNCH(h, 1, 4.0 * (double)(m + r) * (double)n,
+            launch_small(X, ldx, m, n, r, W, nullptr, 0, eps, H, Ppart, Qpart, kFusedAcc, fg, st));
+    for (int it = 0; it < iters; ++it) {
+      if (dist) {
+        ntt_status s = dist_reduce(h, p, Ppart, fg, Qpart, fg, red);
+        if (s) return s;
+        PLAUNCH(h, 2, 8.0 * (double)(2 * m * r + r * r), launch_wupdate2(W, m, r, red, 1, red + m * r, 1, eps, Gpart, st));
+      } else {
+        PLAUNCH(h, 2, 8.0 * ((double)fg * (m * r + r * r) + m * r),
+                launch_wupdate2(W, m, r, Ppart, fg, Qpart, fg, eps, Gpart, st));
+      }
+      const int mode = kFusedUpdate | ((it + 1 < iters) ? kFusedAcc : 0);
+      PLAUNCH(h, 0, 4.0 * (double)(m + 2 * r) * (double)n,
+              launch_small(X, ldx, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, fg, st));
+      if (dev_trace) LAUNCH(h, launch_objective(X, ldx, m, n, W, H, r, dev_trace + (int64_t)it * nobj, st));
+    }
     return NTT_OK;
   }
   if (p.fused && p.persist && !dist && !dev_trace && fused_supported(m, n, r, ldx, X, H)) {

@@ -303,3 +303,16 @@ def test_generate_matches_oracle_generator(h, ora):
     h.ntt_generate(dims, ranks, dev(cores.astype(np.float32)), 0.25, 5, 0x300, out)
     ref = ora.tt_full_f32(dims, ranks, cores, noise_amp=0.25, seed=5).ravel()
     assert np.allclose(host(out), ref, rtol=2e-6, atol=0)
+
+
+@pytest.mark.parametrize("m,n,r", [(2, 4100, 2), (4, 60000, 4), (6, 70004, 5), (8, 1 << 16, 3), (1, 1024, 1),
+                                   (6, 800, 6), (7, 4000, 4)])
+def test_nmf_mu_small_path_parity(h, ora, m, n, r, monkeypatch):
+    """The register-resident m <= 8 pass (mu_small.cu, NTT_SMALL=1) against the oracle."""
+    monkeypatch.setenv("NTT_SMALL", "1")
+    X, W0, H0 = _mu_inputs(m, n, r, m * 11 + n)
+    Xd, Wd, Hd = dev(X), dev(W0), dev(H0)
+    h.ntt_nmf_mu(Xd, m, n, n, r, 10, 1e-16, Wd, Hd)
+    Wo, Ho = ora.nmf_mu(X, W0.astype(np.float64), H0.astype(np.float64), 10, eps=1e-16)
+    assert_close_factor(host(Wd), Wo, what=f"small W {m}x{n} r{r}")
+    assert_close_factor(host(Hd), Ho, what=f"small H {m}x{n} r{r}")
