@@ -86,6 +86,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// one 3-D box {32 cols, rows, blocks} = `blocks` consecutive 32-column boxes in one transaction
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
@@ -354,10 +363,11 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
     // ================= TMA producer =================
     if (lane == 0) {
       uint64_t policy;
-      if (evict_first)
+      if (evict_first & 1)
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
       else
         asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
+      const bool x3d = (evict_first & 2) != 0;  // tmX is the 3-D map: the tile's NB boxes in one transaction
       for (int64_t j = 0; j < J; ++j) {
         const int64_t pos = pbase + j;
         uint32_t fm;
@@ -371,11 +381,19 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
         mbar_expect_tx(&full[s], XB + (HDIRECT ? 0u : HB));
         const int col0 = (int)((b + j * gridDim.x) * BNT);
         unsigned char* st = stages + (size_t)s * SB;
+        if (x3d) {
+          tma_load_3d(st, &tmX, 0, 0, col0 >> 5, &full[s], policy);
+        } else {
 #pragma unroll
-        for (int bx = 0; bx < NB; ++bx) tma_load_2d(st + bx * MP * 128, &tmX, col0 + bx * 32, 0, &full[s], policy);
+          for (int bx = 0; bx < NB; ++bx) tma_load_2d(st + bx * MP * 128, &tmX, col0 + bx * 32, 0, &full[s], policy);
+        }
         if (!HDIRECT) {
+          if (x3d) {
+            tma_load_3d(st + XB, &tmH, 0, 0, col0 >> 5, &full[s], policy);
+          } else {
 #pragma unroll
-          for (int bx = 0; bx < NB; ++bx) tma_load_2d(st + XB + bx * 1024, &tmH, col0 + bx * 32, 0, &full[s], policy);
+            for (int bx = 0; bx < NB; ++bx) tma_load_2d(st + XB + bx * 1024, &tmH, col0 + bx * 32, 0, &full[s], policy);
+          }
         }
         st_release_u32(issued, (uint32_t)(pos + 1));
       }
@@ -1421,6 +1439,25 @@ cudaError_t make_map(CUtensorMap* map, const float* base, uint64_t cols, uint64_
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// X as {32 cols, rows, n / 32 column blocks} (block stride 128 B): a box {32, rows, blocks}
+// lands in shared memory exactly as `blocks` 2-D boxes of 32 columns (same 128B swizzle,
+// rows = 8), but as ONE transaction -- config 4's 8-row boxes are 1 KB each, in the
+// small-transaction regime of the TMA engine (tools/tmabench.cu: 1 KB segments stream at
+// well under half the rate of 4 KB ones).  Requires n % 32 == 0.
+cudaError_t make_map3(CUtensorMap* map, const float* base, uint64_t cols, uint64_t rows, uint64_t ld_elems,
+                      uint32_t box_rows, uint32_t blocks) {
+  cudaError_t e = get_encode();
+  if (e != cudaSuccess) return e;
+  cuuint64_t dims[3] = {32, rows, cols / 32};
+  cuuint64_t strides[2] = {ld_elems * sizeof(float), 32 * sizeof(float)};
+  cuuint32_t box[3] = {32, box_rows, blocks};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 int ux_for(int64_t m) { return m <= 8 ? 1 : m <= 16 ? 2 : m <= 32 ? 4 : 5; }
 int rcls_for(int r) { return r <= 2 ? 2 : r <= 4 ? 4 : r <= 6 ? 6 : 8; }
 
@@ -1629,9 +1666,18 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
   }
   const int ux = ux_for(m);
   CUtensorMap mx, mh;
-  cudaError_t e = make_map(&mx, X, (uint64_t)n, (uint64_t)m, (uint64_t)ldx, (uint32_t)(ux * 8));
-  if (e != cudaSuccess) return e;
-  e = make_map(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u);
+  static const bool x3d_on = [] {
+    const char* e = getenv("NTT_X3D");
+    return !(e && e[0] == '0');
+  }();
+  int ef = evict_first;
+  cudaError_t e;
+  if (ux == 1 && (n % 32) == 0 && x3d_on) {  // 8-row X tiles: one 3-D box per 128-column tile
+    e = make_map3(&mx, X, (uint64_t)n, (uint64_t)m, (uint64_t)ldx, 8u, 4u);
+    ef |= 2;
+  } else {
+    e = make_map(&mx, X, (uint64_t)n, (uint64_t)m, (uint64_t)ldx, (uint32_t)(ux * 8));
+  }
   if (e != cudaSuccess) return e;
   const int rc = rcls_for(r);
   // experiment knobs: NTT_W_BN=64 (64-column tiles for UX >= 4), NTT_W_HDIRECT=0/1 (default: direct H loads
@@ -1644,13 +1690,19 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
     const char* e = getenv("NTT_W_HDIRECT");
     return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
-  const bool hd = (w_hd >= 0) ? (w_hd == 1) : (ux <= 2 || r < 8);
+  // with the 3-D maps (m <= 8) staging H through TMA beats the lanes' direct loads: config 4 step 1
+  // 59.4 -> 53.7 ms (the direct loads cannot keep enough bytes in flight, tools/membench.cu)
+  const bool hd = (w_hd >= 0) ? (w_hd == 1) : ((ef & 2) ? false : (ux <= 2 || r < 8));
+  // H boxes (staged path): 3-D as well when X uses the 3-D map (block stride 128 B of row pitch n)
+  e = (ef & 2) && !hd && (n % 32) == 0 ? make_map3(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u, 4u)
+                                       : make_map(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u);
+  if (e != cudaSuccess) return e;
 #define LF(RR, UU)                                                                                                              \
   return (UU >= 4 && w_bn == 64)                                                                                                  \
-             ? (hd ? launch_t<RR, UU, 8, true, 64>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st)  \
-                   : launch_t<RR, UU, 8, false, 64>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st)) \
-             : (hd ? launch_t<RR, UU, 8, true, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st) \
-                   : launch_t<RR, UU, 8, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st))
+             ? (hd ? launch_t<RR, UU, 8, true, 64>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, ef, pa, st)  \
+                   : launch_t<RR, UU, 8, false, 64>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, ef, pa, st)) \
+             : (hd ? launch_t<RR, UU, 8, true, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, ef, pa, st) \
+                   : launch_t<RR, UU, 8, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, ef, pa, st))
   if (rc == 2) {
     if (ux == 1) LF(2, 1);
     if (ux == 2) LF(2, 2);
@@ -1676,11 +1728,11 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
     return e ? atoi(e) : 8;
   }();
   if (ux == 4 && !hd && w_bn == 128 && w_nwt == 6)
-    return launch_t<8, 4, 6, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
+    return launch_t<8, 4, 6, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, ef, pa, st);
   if (ux == 4 && !hd && w_bn == 128 && w_nwt == 9)
-    return launch_t<8, 4, 9, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
+    return launch_t<8, 4, 9, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, ef, pa, st);
   if (ux == 4 && !hd && w_bn == 128 && w_nwt == 7)
-    return launch_t<8, 4, 7, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
+    return launch_t<8, 4, 7, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, ef, pa, st);
   if (ux == 4) LF(8, 4);
   LF(8, 5);
 #undef LF
