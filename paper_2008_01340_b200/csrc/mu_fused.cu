@@ -1668,12 +1668,17 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
   CUtensorMap mx, mh;
   static const bool x3d_on = [] {
     const char* e = getenv("NTT_X3D");
-    return !(e && e[0] == '0');
+    const char* b = getenv("NTT_W_BN");  // the 3-D box spans 4 blocks: 128-column tiles only
+    return !(e && e[0] == '0') && !(b && b[0] == '6');
   }();
   int ef = evict_first;
   cudaError_t e;
-  if (ux == 1 && (n % 32) == 0 && x3d_on) {  // 8-row X tiles: one 3-D box per 128-column tile
-    e = make_map3(&mx, X, (uint64_t)n, (uint64_t)m, (uint64_t)ldx, 8u, 4u);
+  static const int x3d_max_ux = [] {
+    const char* e = getenv("NTT_X3D_UX");
+    return e ? atoi(e) : 5;
+  }();
+  if (ux <= x3d_max_ux && (n % 32) == 0 && x3d_on) {  // one 3-D box per 128-column tile
+    e = make_map3(&mx, X, (uint64_t)n, (uint64_t)m, (uint64_t)ldx, (uint32_t)(ux * 8), 4u);
     ef |= 2;
   } else {
     e = make_map(&mx, X, (uint64_t)n, (uint64_t)m, (uint64_t)ldx, (uint32_t)(ux * 8));
@@ -1692,7 +1697,7 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
   }();
   // with the 3-D maps (m <= 8) staging H through TMA beats the lanes' direct loads: config 4 step 1
   // 59.4 -> 53.7 ms (the direct loads cannot keep enough bytes in flight, tools/membench.cu)
-  const bool hd = (w_hd >= 0) ? (w_hd == 1) : ((ef & 2) ? false : (ux <= 2 || r < 8));
+  const bool hd = (w_hd >= 0) ? (w_hd == 1) : ((ef & 2) && ux == 1 ? false : (ux <= 2 || r < 8));
   // H boxes (staged path): 3-D as well when X uses the 3-D map (block stride 128 B of row pitch n)
   e = (ef & 2) && !hd && (n % 32) == 0 ? make_map3(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u, 4u)
                                        : make_map(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u);
