@@ -1695,9 +1695,10 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
     const char* e = getenv("NTT_W_HDIRECT");
     return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
-  // with the 3-D maps (m <= 8) staging H through TMA beats the lanes' direct loads: config 4 step 1
-  // 59.4 -> 53.7 ms (the direct loads cannot keep enough bytes in flight, tools/membench.cu)
-  const bool hd = (w_hd >= 0) ? (w_hd == 1) : ((ef & 2) && ux == 1 ? false : (ux <= 2 || r < 8));
+  // with the 3-D maps staging H through TMA (one 4 KB box per tile) beats the lanes' direct
+  // loads, which cannot keep enough bytes in flight (tools/membench.cu): config 4 step 1
+  // 59.4 -> 53.7 ms, steps 2-5 -2 to -5 %
+  const bool hd = (w_hd >= 0) ? (w_hd == 1) : ((ef & 2) ? false : (ux <= 2 || r < 8));
   // H boxes (staged path): 3-D as well when X uses the 3-D map (block stride 128 B of row pitch n)
   e = (ef & 2) && !hd && (n % 32) == 0 ? make_map3(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u, 4u)
                                        : make_map(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u);
