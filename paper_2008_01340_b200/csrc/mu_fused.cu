@@ -452,6 +452,17 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
       for (int p2 = 0; p2 < CPL / 2; ++p2) dst[l][p2] = f2(hx[2 * p2], hx[2 * p2 + 1]);
     }
   };
+  // BCD mode (PersistArgs::bcdL): row scales of H_m, 1 / L_H, output buffer
+  const bool bcd = pa.bcdL != nullptr;
+  float bsh[R];
+  float binvL = 0.f;
+#pragma unroll
+  for (int l = 0; l < R; ++l) bsh[l] = (bcd && l < r) ? (float)pa.bcdS[l] : 1.f;
+  if (bcd) {
+    const double L = *pa.bcdL;
+    binvL = L > 0.0 ? (float)(1.0 / L) : 0.f;
+  }
+  float* const Ho = (bcd && pa.Hout) ? pa.Hout : H;
   float2 hnext[R][CPL / 2];
   if (HDIRECT) load_h(warp, hnext);
 
@@ -502,6 +513,12 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
           hv[l][0] = *reinterpret_cast<const float2*>(hp);
         }
       }
+    }
+    if (bcd) {  // H_m = diag(sH) H_m stored (bcd.cu's l.9 compensation)
+#pragma unroll
+      for (int l = 0; l < R; ++l)
+#pragma unroll
+        for (int p2 = 0; p2 < CPL / 2; ++p2) hv[l][p2] = f2(hv[l][p2].x * bsh[l], hv[l][p2].y * bsh[l]);
     }
 
     // ---------------- phase A ----------------
@@ -558,24 +575,29 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
 #pragma unroll
           for (int p2 = 0; p2 < CPL / 2; ++p2) {
             float2 v;
-            v.x = mu_q(hv[k][p2].x, s2[k][p2].x, ev[k][p2].x, eps);
-            v.y = mu_q(hv[k][p2].y, s2[k][p2].y, ev[k][p2].y, eps);
+            if (bcd) {  // prox-linear step (Alg. 3 l.14): max(0, H_m - (G H_m - S) / L_H)
+              v.x = fmaxf(0.f, fmaf(-(ev[k][p2].x - s2[k][p2].x), binvL, hv[k][p2].x));
+              v.y = fmaxf(0.f, fmaf(-(ev[k][p2].y - s2[k][p2].y), binvL, hv[k][p2].y));
+            } else {
+              v.x = mu_q(hv[k][p2].x, s2[k][p2].x, ev[k][p2].x, eps);
+              v.y = mu_q(hv[k][p2].y, s2[k][p2].y, ev[k][p2].y, eps);
+            }
             if (k >= r) v = f2(0.f, 0.f);  // padded ranks (0/0 when eps = 0)
             // columns beyond n: zero (never stored, never accumulated)
             if (c0 + 2 * p2 >= n) v.x = 0.f;
             if (c0 + 2 * p2 + 1 >= n) v.y = 0.f;
             hn[k][p2] = v;
           }
-        // store H (in place; this tile's H was already read)
+        // store H (in place -- this tile's H was already read -- or to Hout for BCD)
         if (c0 + CPL - 1 < n) {
 #pragma unroll
           for (int k = 0; k < R; ++k)
             if (k < r) {
               if (CPL == 4)
-                *reinterpret_cast<float4*>(H + (int64_t)k * n + c0) =
+                *reinterpret_cast<float4*>(Ho + (int64_t)k * n + c0) =
                     make_float4(hn[k][0].x, hn[k][0].y, hn[k][CPL / 2 - 1].x, hn[k][CPL / 2 - 1].y);
               else
-                *reinterpret_cast<float2*>(H + (int64_t)k * n + c0) = hn[k][0];
+                *reinterpret_cast<float2*>(Ho + (int64_t)k * n + c0) = hn[k][0];
             }
         } else {
 #pragma unroll
@@ -583,7 +605,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
             if (k < r) {
 #pragma unroll
               for (int t = 0; t < CPL - 1; ++t)
-                if (c0 + t < n) H[(int64_t)k * n + c0 + t] = (t & 1) ? hn[k][t >> 1].y : hn[k][t >> 1].x;
+                if (c0 + t < n) Ho[(int64_t)k * n + c0 + t] = (t & 1) ? hn[k][t >> 1].y : hn[k][t >> 1].x;
             }
         }
       } else {

@@ -34,6 +34,12 @@ struct PersistArgs {
   unsigned* ctr;
   float* Wout;
   unsigned long long* trace;  // nullable: per pass 4 globaltimer stamps of CTA 0 (diagnostics)
+  // BCD H step instead of the MU rule (non-persistent k_fused, m <= 40; bcd.cu, Alg. 3 l.11-14):
+  // H is then H_m (rows scaled by bcdS[k]) and Hn = max(0, H_m - (G H_m - W^T X) / *bcdL) is
+  // stored to Hout (P, Q partials of Hn as usual)
+  const double* bcdL = nullptr;
+  const double* bcdS = nullptr;
+  float* Hout = nullptr;
 };
 
 // One pass over X (m x n, row stride ldx) with the current W (m x r) and

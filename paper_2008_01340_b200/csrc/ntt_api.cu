@@ -1159,6 +1159,8 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   // short-wide X (r <= 8, m <= 256): P, Q from the 1-pass fused kernel's acc-only mode
   const bool fa = !tc && fused_supported(m, n, r, ldx, X, H) && !getenv("NTT_BCD_NO_FUSED");
   const int fparts = fa ? fused_partials(m, n, r, h->num_sms) : 0;
+  // m <= 40 (k_fused, not the CTA-cooperative k_fused_c): the whole H half-iteration in one pass
+  const bool f1 = fa && m <= 40 && !getenv("NTT_BCD_NO_1PASS");
   size_t o = 0;
   auto take = [&](size_t b) {
     size_t at = o;
@@ -1273,13 +1275,30 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
       LAUNCH(h, tc16_pack_w_slot(tp, W, tws, st, 6));
       PLAUNCH(h, 7, xbytes, tc16_pass_h(tp, maps, tws, bef, st, bflush));
     }
-    if (!tc && nS == 1) {  // S and the H step in one pass (l.11-14)
-      PLAUNCH(h, 5, xbytes + 8.0 * r * (double)n, launch_bcd_shup(X, ldx, m, n, W, r, G, bs + BS_LH, Hm, sH, H, st));
+    if (f1) {  // ONE pass (m <= 40): S, the H step, and P, Q of the new H (l.11-15), k_fused in BCD mode
+      PersistArgs pa;
+      pa.iters = 0;
+      pa.part = pa.red = nullptr;
+      pa.ctr = nullptr;
+      pa.Wout = nullptr;
+      pa.trace = nullptr;
+      pa.bcdL = bs + BS_LH;
+      pa.bcdS = sH;
+      pa.Hout = H;
+      PLAUNCH(h, 0, xbytes + 8.0 * r * (double)n,
+              launch_fused(X, ldx, m, n, r, W, G, 1, 0.0f, Hm, Ppart, Qpart, kFusedUpdate | kFusedAcc,
+                           fused_grid(m, n, r, h->num_sms), st, &pa));
+      LAUNCH(h, launch_bcd_psum_dot(Ppart, fparts, m * r, W, Pn, dotpart, h->num_sms, st));
+      LAUNCH(h, launch_sum_partials(Qpart, fparts, (int64_t)r * r, Qn, st));
     } else {
-      if (!tc) PLAUNCH(h, 5, xbytes, launch_bcd_spart(X, ldx, m, n, W, r, nS, Spart, st));
-      LAUNCH(h, launch_bcd_hup(Spart, nS, n, r, G, bs + BS_LH, Hm, sH, H, mxh, h->num_sms, st));  // l.11-14
+      if (!tc && nS == 1) {  // S and the H step in one pass (l.11-14)
+        PLAUNCH(h, 5, xbytes + 8.0 * r * (double)n, launch_bcd_shup(X, ldx, m, n, W, r, G, bs + BS_LH, Hm, sH, H, st));
+      } else {
+        if (!tc) PLAUNCH(h, 5, xbytes, launch_bcd_spart(X, ldx, m, n, W, r, nS, Spart, st));
+        LAUNCH(h, launch_bcd_hup(Spart, nS, n, r, G, bs + BS_LH, Hm, sH, H, mxh, h->num_sms, st));  // l.11-14
+      }
+      if ((s = pq(H, Pn, Qn, true))) return s;                                               // l.15
     }
-    if ((s = pq(H, Pn, Qn, true))) return s;                                               // l.15
     LAUNCH(h, launch_bcd_decide(bs, dtrace, dotpart, ndot, G, Qn, r, mxh, st));             // l.16-17 (R25)
     LAUNCH(h, launch_bcd_commit(W, Wm, Wp, m * r, bs, BS_WW, st));                    // l.18-27
     LAUNCH(h, launch_bcd_commit_h(H, Hm, Hp, r, n, sH, bs, st));
