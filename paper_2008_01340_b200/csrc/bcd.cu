@@ -308,67 +308,76 @@ k_bcd_psum_dot(const double* __restrict__ part, int nparts, int64_t len, const f
 // Repeated squaring A <- A^2 / max diag(A^2) drives A to the scaled projector onto the top
 // eigenspace (stopped when A stops changing, at most 64 squarings = M^(2^64)); the Rayleigh
 // quotient of M on the column of A with the largest diagonal entry is then lambda_max with an
-// error quadratic in the eigenvector error.  One CTA of RP^2 threads (RP = 8, 16, 32 >= r),
-// thread (i, j) owns A[i][j]: small ranks pay for 2 warps, not 32.
+// error quadratic in the eigenvector error.  Runs on the whole CTA (blockDim >= RP^2, a multiple
+// of 32; thread (i, j) = (t / RP, t % RP) owns A[i][j]); the result is returned to every thread.
 template <int RP>
-__global__ void __launch_bounds__(RP * RP) k_spec_norm(const double* __restrict__ M, int r, double* __restrict__ out) {
-  constexpr int NW = RP * RP / 32;
-  __shared__ double A[RP][RP + 1];
-  __shared__ double Ms[RP][RP + 1];
-  __shared__ double red[32];
-  __shared__ double bc[2];
-  const int t = threadIdx.x, i = t / RP, j = t % RP, lane = t & 31, w = t >> 5;
-  const bool in = i < r && j < r;
+struct SpecSmem {
+  double A[RP][RP + 1];
+  double Ms[RP][RP + 1];
+  double red[32];
+  double red2[32];
+  double bc[2];
+};
+
+template <int RP>
+__device__ double spec_dev(const double* __restrict__ M, int r, SpecSmem<RP>& S) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5, NWB = blockDim.x >> 5;
+  const bool act = t < RP * RP;
+  const int i = act ? t / RP : 0, j = act ? t % RP : 0;
+  const bool in = act && i < r && j < r;
   const double mv = in ? M[i * r + j] : 0.0;
-  Ms[i][j] = mv;
-  if (t < 32) red[t] = (t < r) ? M[t * r + t] : 0.0;
+  __syncthreads();  // S may be reused from a previous call
+  if (act) S.Ms[i][j] = mv;
+  if (t < 32) S.red[t] = (t < r) ? M[t * r + t] : 0.0;
   __syncthreads();
   if (t < 32) {
-    double d = red[t];
+    double d = S.red[t];
     for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
-    if (t == 0) bc[0] = d;
+    if (t == 0) S.bc[0] = d;
   }
   __syncthreads();
-  const double d0 = bc[0];
-  if (!(d0 > 0.0)) {  // PSD with a zero diagonal: M = 0
-    if (t == 0) *out = 0.0;
-    return;
-  }
-  A[i][j] = mv / d0;
+  const double d0 = S.bc[0];
+  if (!(d0 > 0.0)) return 0.0;  // PSD with a zero diagonal: M = 0 (uniform branch)
+  if (act) S.A[i][j] = mv / d0;
   __syncthreads();
   for (int it = 0; it < 64; ++it) {
     double c = 0.0;
+    if (act) {
 #pragma unroll 8
-    for (int k = 0; k < RP; ++k) c += A[i][k] * A[k][j];
-    __syncthreads();
-    if (i == j) red[i] = c;
-    __syncthreads();
-    if (t < 32) {
-      double d = (t < RP) ? red[t] : 0.0;
-      for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
-      if (t == 0) bc[0] = d;
+      for (int k = 0; k < RP; ++k) c += S.A[i][k] * S.A[k][j];
     }
     __syncthreads();
-    const double an = c / bc[0];
-    double diff = fabs(an - A[i][j]);
-    A[i][j] = an;
-    for (int o = 16; o > 0; o >>= 1) diff = fmax(diff, __shfl_xor_sync(0xffffffffu, diff, o));
-    if (lane == 0) red[w] = diff;
+    if (act && i == j) S.red[i] = c;
     __syncthreads();
     if (t < 32) {
-      double d = (t < NW) ? red[t] : 0.0;
+      double d = (t < RP) ? S.red[t] : 0.0;
       for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
-      if (t == 0) bc[1] = d;
+      if (t == 0) S.bc[0] = d;
+    }
+    __syncthreads();
+    double diff = 0.0;
+    if (act) {
+      const double an = c / S.bc[0];
+      diff = fabs(an - S.A[i][j]);
+      S.A[i][j] = an;
+    }
+    for (int o = 16; o > 0; o >>= 1) diff = fmax(diff, __shfl_xor_sync(0xffffffffu, diff, o));
+    if (lane == 0) S.red[w] = diff;
+    __syncthreads();
+    if (t < 32) {
+      double d = (t < NWB) ? S.red[t] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+      if (t == 0) S.bc[1] = d;
     }
     __syncthreads();
     // A entries are O(1) (max diagonal 1); a change <= 1e-12 means the non-top eigen-components
     // left are <= ~1e-12 (or within 1e-12 of lambda_max), and the Rayleigh quotient's error is
     // quadratic in them.  (A tighter stop would chase the ~1e-15 rounding noise of A^2.)
-    if (bc[1] <= 1e-12) break;
+    if (S.bc[1] <= 1e-12) break;
   }
   // column with the largest diagonal entry (lowest index on ties)
   if (t < 32) {
-    double d = (t < r) ? A[t][t] : -1.0;
+    double d = (t < r) ? S.A[t][t] : -1.0;
     int idx = t;
     for (int o = 16; o > 0; o >>= 1) {
       const double od = __shfl_xor_sync(0xffffffffu, d, o);
@@ -378,28 +387,223 @@ __global__ void __launch_bounds__(RP * RP) k_spec_norm(const double* __restrict_
         idx = oi;
       }
     }
-    if (t == 0) bc[0] = (double)idx;
+    if (t == 0) S.bc[0] = (double)idx;
   }
   __syncthreads();
-  const int jc = (int)bc[0];
-  const double vi = A[i][jc], vj = A[j][jc];
-  double num = in ? vi * Ms[i][j] * vj : 0.0;
+  const int jc = (int)S.bc[0];
+  const double vi = act ? S.A[i][jc] : 0.0, vj = act ? S.A[j][jc] : 0.0;
+  double num = in ? vi * S.Ms[i][j] * vj : 0.0;
   double den = (in && i == j) ? vi * vi : 0.0;
   num = warp_sum(num);
   den = warp_sum(den);
   __syncthreads();
   if (lane == 0) {
-    red[w] = num;
-    A[w][0] = den;
+    S.red[w] = num;
+    S.red2[w] = den;
   }
   __syncthreads();
   if (t == 0) {
     double sn = 0.0, sd = 0.0;
-    for (int q = 0; q < NW; ++q) {
-      sn += red[q];
-      sd += A[q][0];
+    for (int q = 0; q < NWB; ++q) {
+      sn += S.red[q];
+      sd += S.red2[q];
     }
-    *out = sd > 0.0 ? sn / sd : 0.0;
+    S.bc[0] = sd > 0.0 ? sn / sd : 0.0;
+  }
+  __syncthreads();
+  return S.bc[0];
+}
+
+template <int RP>
+__global__ void __launch_bounds__(RP * RP) k_spec_norm(const double* __restrict__ M, int r, double* __restrict__ out) {
+  __shared__ SpecSmem<RP> S;
+  const double v = spec_dev<RP>(M, r, S);
+  if (threadIdx.x == 0) *out = v;
+}
+
+// ---- one-CTA stages for small W (m r <= 8192, r <= 16): the whole W side of an iteration
+// and everything after the H pass except the H commit, so an iteration is 4-5 launches
+constexpr int WS_T = 256;
+
+// W side (l.5-10): L_W = ||Q||_2, W step, column L1 normalisation (W, W_prev; H_m, H_prev
+// through their row scales), G = W^T W, L_H = ||G||_2.  Dynamic smem: m * RP floats.
+template <int RP>
+__global__ void __launch_bounds__(WS_T) k_bcd_wside(const float* __restrict__ Wm, float* __restrict__ W,
+                                                    float* __restrict__ Wp, int m, int r, const double* __restrict__ Pc,
+                                                    const double* __restrict__ Qc, double* __restrict__ bs,
+                                                    double* __restrict__ c_out, double* __restrict__ G_out,
+                                                    double* __restrict__ sH) {
+  __shared__ SpecSmem<RP> S;
+  __shared__ double Qs[RP * RP];
+  __shared__ double cw[WS_T / 32][RP];
+  __shared__ double cs[RP];
+  __shared__ double Gp[WS_T];
+  extern __shared__ float Wsm[];  // m x RP (the new W)
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  // the previous iteration's H commit stored H_m afresh (and H_prev when it accepted)
+  if (t < 32) {
+    sH[t] = 1.0;
+    if (bs[BS_ACC] != 0.0) sH[32 + t] = 1.0;
+  }
+  const double LW = spec_dev<RP>(Qc, r, S);  // l.7
+  if (t == 0) bs[BS_LW] = LW;
+  for (int e = t; e < RP * RP; e += WS_T) {
+    const int k = e / RP, l = e % RP;
+    Qs[e] = (k < r && l < r) ? Qc[k * r + l] : 0.0;
+  }
+  __syncthreads();
+  double csum[RP];
+#pragma unroll
+  for (int k = 0; k < RP; ++k) csum[k] = 0.0;
+  for (int i = t; i < m; i += WS_T) {  // l.6-8, one row per thread
+    double wv[RP];
+#pragma unroll
+    for (int k = 0; k < RP; ++k) wv[k] = (k < r) ? (double)Wm[i * r + k] : 0.0;
+#pragma unroll
+    for (int k = 0; k < RP; ++k) {
+      float vf = 0.0f;
+      if (k < r) {
+        double g = -Pc[i * r + k];
+#pragma unroll
+        for (int l = 0; l < RP; ++l) g += wv[l] * Qs[l * RP + k];
+        const double v = LW > 0.0 ? fmax(0.0, wv[k] - g / LW) : wv[k];
+        vf = (float)v;
+        csum[k] += (double)vf;
+      }
+      Wsm[i * RP + k] = vf;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < RP; ++k) {
+    const double v = warp_sum(csum[k]);
+    if (lane == 0) cw[w][k] = v;
+  }
+  __syncthreads();
+  if (t < RP) {
+    double sum = 0.0;
+    for (int q = 0; q < WS_T / 32; ++q) sum += cw[q][t];
+    cs[t] = sum;
+    if (t < r) c_out[t] = sum;
+  }
+  __syncthreads();
+  for (int e = t; e < m * r; e += WS_T) {  // l.9 (R24)
+    const int i = e / r, k = e % r;
+    const double ck = cs[k];
+    float v = Wsm[i * RP + k];
+    if (ck > 0.0) {
+      v = (float)((double)v / ck);
+      Wp[e] = (float)((double)Wp[e] / ck);
+    }
+    Wsm[i * RP + k] = v;
+    W[e] = v;
+  }
+  if (t < r && cs[t] > 0.0) {
+    sH[t] *= cs[t];
+    sH[32 + t] *= cs[t];
+  }
+  __syncthreads();
+  constexpr int NE = RP * RP;
+  constexpr int SPL = WS_T / NE >= 1 ? WS_T / NE : 1;  // row slices per G entry
+  if (t < NE * SPL) {  // l.10: G = W^T W, fixed order
+    const int e = t % NE, sl = t / NE, k = e / RP, l = e % RP;
+    double g = 0.0;
+    if (k < r && l < r)
+      for (int i = sl; i < m; i += SPL) g += (double)Wsm[i * RP + k] * (double)Wsm[i * RP + l];
+    Gp[t] = g;
+  }
+  __syncthreads();
+  if (t < NE) {
+    double g = 0.0;
+    for (int sl = 0; sl < SPL; ++sl) g += Gp[sl * NE + t];
+    const int k = t / RP, l = t % RP;
+    if (k < r && l < r) G_out[k * r + l] = g;
+  }
+  __syncthreads();
+  const double LH = spec_dev<RP>(G_out, r, S);
+  if (t == 0) bs[BS_LH] = LH;
+}
+
+// After the H pass (l.15-27): P, Q of the candidate from their partials, the Gram-identity
+// objective, the branch (as k_bcd_decide), and the W / P / Q commits.  Dynamic smem: m r doubles.
+template <int RP>
+__global__ void __launch_bounds__(WS_T) k_bcd_post(const double* __restrict__ Ppart, int nP,
+                                                   const double* __restrict__ Qpart, int nQ, int m, int r,
+                                                   const float* __restrict__ W, float* __restrict__ Wm,
+                                                   float* __restrict__ Wp, double* __restrict__ Pc,
+                                                   double* __restrict__ Qc, const double* __restrict__ c,
+                                                   const double* __restrict__ G, double* __restrict__ bs,
+                                                   double* __restrict__ trace) {
+  extern __shared__ double Pn[];  // m r
+  __shared__ double Qn[RP * RP];
+  __shared__ double red[32], red2[32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int mr = m * r, rr = r * r;
+  double dot = 0.0, gq = 0.0;
+  for (int e = t; e < mr; e += WS_T) {
+    double sv = 0.0;
+    for (int b = 0; b < nP; ++b) sv += Ppart[(int64_t)b * mr + e];
+    Pn[e] = sv;
+    dot += (double)W[e] * sv;
+  }
+  for (int e = t; e < rr; e += WS_T) {
+    double sv = 0.0;
+    for (int b = 0; b < nQ; ++b) sv += Qpart[(int64_t)b * rr + e];
+    Qn[e] = sv;
+    gq += G[e] * sv;
+  }
+  dot = warp_sum(dot);
+  gq = warp_sum(gq);
+  if (lane == 0) {
+    red[w] = dot;
+    red2[w] = gq;
+  }
+  __syncthreads();
+  if (t == 0) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int q = 0; q < WS_T / 32; ++q) {
+      s1 += red[q];
+      s2 += red2[q];
+    }
+    bs[BS_OBJNEW] = 0.5 * (bs[BS_XX] - 2.0 * s1 + s2);  // R25
+    const double obj_new = bs[BS_OBJNEW], obj = bs[BS_OBJ], tt = bs[BS_T];
+    if (obj_new < obj) {  // l.21-27
+      const double tp = (1.0 + sqrt(1.0 + 4.0 * tt * tt)) / 2.0;
+      const double wgt = (tt - 1.0) / tp;
+      const double LW = bs[BS_LW], LH = bs[BS_LH], dl = bs[BS_DELTA];
+      bs[BS_WW] = fmin(wgt, dl * sqrt(bs[BS_LWP] / LW));
+      bs[BS_WH] = fmin(wgt, dl * sqrt(bs[BS_LHP] / LH));
+      bs[BS_ACC] = 1.0;
+      bs[BS_LWP] = LW;
+      bs[BS_LHP] = LH;
+      bs[BS_T] = tp;
+      bs[BS_OBJ] = obj_new;
+    } else {  // l.17-20
+      bs[BS_ACC] = 0.0;
+      bs[BS_T] = 1.0;
+    }
+    const int it = (int)bs[BS_IT];
+    if (trace) trace[it] = bs[BS_OBJ];
+    bs[BS_IT] = (double)(it + 1);
+  }
+  __syncthreads();
+  const bool acc = bs[BS_ACC] != 0.0;
+  const double wW = bs[BS_WW];
+  for (int e = t; e < mr; e += WS_T) {
+    const int k = e % r;
+    if (acc) {
+      const double v = W[e], vp = Wp[e];
+      Wm[e] = (float)(v + wW * (v - vp));
+      Wp[e] = (float)v;
+      Pc[e] = Pn[e];
+    } else {
+      Wm[e] = Wp[e];
+      if (c[k] > 0.0) Pc[e] *= c[k];
+    }
+  }
+  for (int e = t; e < rr; e += WS_T) {
+    const int k = e / r, l = e % r;
+    if (acc) Qc[e] = Qn[e];
+    else Qc[e] *= (c[k] > 0.0 ? c[k] : 1.0) * (c[l] > 0.0 ? c[l] : 1.0);
   }
 }
 
@@ -482,13 +686,15 @@ __global__ void k_bcd_commit_h(const float* __restrict__ H, float* __restrict__ 
 // out[k][j] = sH[32 + k] Hp[k][j] (the logical H_prev, returned at the end) or, with init,
 // sH[0..64) = 1
 __global__ void k_bcd_hout(const float* __restrict__ Hp, int r, int64_t n, double* __restrict__ sH,
-                           float* __restrict__ out, int init) {
+                           float* __restrict__ out, int init, const double* __restrict__ bs) {
   if (init) {
     if (blockIdx.x == 0 && threadIdx.x < 64) sH[threadIdx.x] = 1.0;
     return;
   }
+  // after an accepted last iteration H_prev was stored afresh (its scale restarts at 1)
+  const bool fresh = bs && bs[BS_ACC] != 0.0;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)r * n; e += (int64_t)gridDim.x * blockDim.x)
-    out[e] = (float)((double)Hp[e] * sH[32 + (int)(e / n)]);
+    out[e] = fresh ? Hp[e] : (float)((double)Hp[e] * sH[32 + (int)(e / n)]);
 }
 
 // accepted: P = X H^T, Q = H H^T of the new H (Pn, Qn).  Correction: H_prev was rescaled
@@ -615,8 +821,37 @@ cudaError_t launch_bcd_shup(const float* X, int64_t ldx, int64_t m, int64_t n, c
   return cudaGetLastError();
 }
 
-cudaError_t launch_bcd_hout(const float* Hp, int r, int64_t n, double* sH, float* out, int init, cudaStream_t st) {
-  k_bcd_hout<<<init ? 1 : 1184, 256, 0, st>>>(Hp, r, n, sH, out, init);
+cudaError_t launch_bcd_hout(const float* Hp, int r, int64_t n, double* sH, float* out, int init, const double* bs,
+                            cudaStream_t st) {
+  k_bcd_hout<<<init ? 1 : 1184, 256, 0, st>>>(Hp, r, n, sH, out, init, bs);
+  return cudaGetLastError();
+}
+
+bool bcd_cta_ok(int64_t m, int r) { return r <= 16 && m * (r <= 8 ? 8 : 16) <= 8192; }
+
+cudaError_t launch_bcd_wside(const float* Wm, float* W, float* Wp, int m, int r, const double* Pc, const double* Qc,
+                             double* bs, double* c, double* G, double* sH, cudaStream_t st) {
+  if (r <= 8) {
+    const size_t sm = sizeof(float) * (size_t)m * 8;
+    k_bcd_wside<8><<<1, WS_T, sm, st>>>(Wm, W, Wp, m, r, Pc, Qc, bs, c, G, sH);
+  } else {
+    const size_t sm = sizeof(float) * (size_t)m * 16;
+    k_bcd_wside<16><<<1, WS_T, sm, st>>>(Wm, W, Wp, m, r, Pc, Qc, bs, c, G, sH);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bcd_post(const double* Ppart, int nP, const double* Qpart, int nQ, int m, int r, const float* W,
+                            float* Wm, float* Wp, double* Pc, double* Qc, const double* c, const double* G, double* bs,
+                            double* trace, cudaStream_t st) {
+  const size_t sm = sizeof(double) * (size_t)m * r;
+  if (sm > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(r <= 8 ? k_bcd_post<8> : k_bcd_post<16>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e) return e;
+  }
+  if (r <= 8) k_bcd_post<8><<<1, WS_T, sm, st>>>(Ppart, nP, Qpart, nQ, m, r, W, Wm, Wp, Pc, Qc, c, G, bs, trace);
+  else k_bcd_post<16><<<1, WS_T, sm, st>>>(Ppart, nP, Qpart, nQ, m, r, W, Wm, Wp, Pc, Qc, c, G, bs, trace);
   return cudaGetLastError();
 }
 

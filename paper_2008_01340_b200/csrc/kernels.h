@@ -100,7 +100,15 @@ cudaError_t launch_bcd_w(const float* Wm, int64_t m, int r, const double* P, con
 cudaError_t launch_bcd_wnorm(float* W, float* Wp, int64_t m, int r, const double* c, double* Gpart, unsigned* maxw,
                              cudaStream_t st);
 cudaError_t launch_bcd_hscale(double* sH, int r, const double* c, cudaStream_t st);
-cudaError_t launch_bcd_hout(const float* Hp, int r, int64_t n, double* sH, float* out, int init, cudaStream_t st);
+cudaError_t launch_bcd_hout(const float* Hp, int r, int64_t n, double* sH, float* out, int init, const double* bs,
+                            cudaStream_t st);
+// one-CTA W side / post-pass stages for small W (bcd_cta_ok: r <= 16, m * rclass <= 8192)
+bool bcd_cta_ok(int64_t m, int r);
+cudaError_t launch_bcd_wside(const float* Wm, float* W, float* Wp, int m, int r, const double* Pc, const double* Qc,
+                             double* bs, double* c, double* G, double* sH, cudaStream_t st);
+cudaError_t launch_bcd_post(const double* Ppart, int nP, const double* Qpart, int nQ, int m, int r, const float* W,
+                            float* Wm, float* Wp, double* Pc, double* Qc, const double* c, const double* G, double* bs,
+                            double* trace, cudaStream_t st);
 cudaError_t launch_bcd_commit_h(const float* H, float* Hm, float* Hp, int r, int64_t n, const double* sH,
                                 const double* bs, cudaStream_t st);
 cudaError_t launch_bcd_shup(const float* X, int64_t ldx, int64_t m, int64_t n, const float* W, int r, const double* G,

@@ -1251,7 +1251,7 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   if (!(xx > 0.0)) return fail(h, NTT_ERR_DEGENERATE, "||X|| = 0");
   LAUNCH(h, launch_scale_copy(W, Wm, Wp, m * r, bs + BS_XX, bs + BS_W0, st));
   LAUNCH(h, launch_scale_copy(H, Hm, Hp, (int64_t)r * n, bs + BS_XX, bs + BS_H0, st));
-  LAUNCH(h, launch_bcd_hout(Hp, r, n, sH, nullptr, 1, st));  // sH = 1
+  LAUNCH(h, launch_bcd_hout(Hp, r, n, sH, nullptr, 1, nullptr, st));  // sH = 1
   if (tc) {
     LAUNCH(h, tc_prepare(tp, X, ldx, Hp, tws, &maps, st));
     LAUNCH(h, tc16_prepare(tp, X, ldx, Hp, tws, &maps, st));
@@ -1263,7 +1263,49 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   if ((s = spec(G, bs + BS_LH))) return s;
   LAUNCH(h, launch_bcd_init(bs, delta, st));
   // ---- one iteration (l.5-27), a fixed launch sequence
+  // small W (non-TC): one-CTA stages for the W side and for everything after the H pass
+  const bool cta = !tc && bcd_cta_ok(m, r) && !getenv("NTT_BCD_NO_CTA");
+  auto iteration_cta = [&]() -> ntt_status {
+    LAUNCH(h, launch_bcd_wside(Wm, W, Wp, (int)m, r, Pc, Qc, bs, c, G, sH, st));  // l.5-10
+    int nPp = nP, nQp = qp.ncs;
+    if (f1) {  // l.11-15 in one pass
+      PersistArgs pa;
+      pa.iters = 0;
+      pa.part = pa.red = nullptr;
+      pa.ctr = nullptr;
+      pa.Wout = nullptr;
+      pa.trace = nullptr;
+      pa.bcdL = bs + BS_LH;
+      pa.bcdS = sH;
+      pa.Hout = H;
+      PLAUNCH(h, 0, xbytes + 8.0 * r * (double)n,
+              launch_fused(X, ldx, m, n, r, W, G, 1, 0.0f, Hm, Ppart, Qpart, kFusedUpdate | kFusedAcc,
+                           fused_grid(m, n, r, h->num_sms), st, &pa));
+      nPp = nQp = fparts;
+    } else {
+      if (nS == 1) {
+        PLAUNCH(h, 5, xbytes + 8.0 * r * (double)n, launch_bcd_shup(X, ldx, m, n, W, r, G, bs + BS_LH, Hm, sH, H, st));
+      } else {
+        PLAUNCH(h, 5, xbytes, launch_bcd_spart(X, ldx, m, n, W, r, nS, Spart, st));
+        LAUNCH(h, launch_bcd_hup(Spart, nS, n, r, G, bs + BS_LH, Hm, sH, H, nullptr, h->num_sms, st));
+      }
+      if (fa) {
+        PLAUNCH(h, 1, xbytes + 4.0 * r * (double)n,
+                launch_fused(X, ldx, m, n, r, W, nullptr, 0, 0.0f, H, Ppart, Qpart, kFusedAcc,
+                             fused_grid(m, n, r, h->num_sms), st));
+        nPp = nQp = fparts;
+      } else {
+        PLAUNCH(h, 1, xbytes, launch_xht_partial(X, ldx, m, n, H, n, r, xp, Ppart, st));
+        LAUNCH(h, launch_xht_partial(H, n, r, n, H, n, r, qp, Qpart, st));
+        nPp = xp.ncs;
+      }
+    }
+    LAUNCH(h, launch_bcd_post(Ppart, nPp, Qpart, nQp, (int)m, r, W, Wm, Wp, Pc, Qc, c, G, bs, dtrace, st));
+    LAUNCH(h, launch_bcd_commit_h(H, Hm, Hp, r, n, sH, bs, st));  // l.18-27 (H side)
+    return NTT_OK;
+  };
   auto iteration = [&]() -> ntt_status {
+    if (cta) return iteration_cta();
     if ((s = spec(Qc, bs + BS_LW))) return s;                                    // l.7
     LAUNCH(h, launch_bcd_w(Wm, m, r, Pc, Qc, bs + BS_LW, W, cpart, st));          // l.6-8
     LAUNCH(h, launch_sum_partials(cpart, nwc, r, c, st));
@@ -1345,7 +1387,7 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   }
   // the last accepted iterates (l.28)
   CU(h, cudaMemcpyAsync(W, Wp, sizeof(float) * m * r, cudaMemcpyDeviceToDevice, st));
-  LAUNCH(h, launch_bcd_hout(Hp, r, n, sH, H, 0, st));  // logical H_prev = diag(sHp) Hp
+  LAUNCH(h, launch_bcd_hout(Hp, r, n, sH, H, 0, bs, st));  // logical H_prev = diag(sHp) Hp
   if (objective_trace && iters > 0)
     CU(h, cudaMemcpyAsync(objective_trace, dtrace, sizeof(double) * iters, cudaMemcpyDeviceToHost, st));
   CU(h, cudaStreamSynchronize(st));
