@@ -145,3 +145,21 @@ def test_ntt_bcd_sweep_parity(h, ora, dims, ranks, iters):
         assert np.abs(Gg - Go).max() <= 1e-4 * np.abs(Go).max()
     e_ora = ora.rel_error(A, ora.tt_full(list(dims), list(ranks), co))
     assert abs(err - e_ora) <= 1e-3 * e_ora + 1e-6
+
+
+def test_ntt_bcd_sweep_host_buffers_and_errors(h, ora):
+    """Host A / host cores through ntt_decompose_bcd (staged by the library) equal the device
+    call bit for bit; ranks > 32 and delta outside [0, 1) are rejected."""
+    import paper_2008_01340_b200 as P
+    dims, ranks = [5, 4, 5, 6], [4, 3, 2]
+    rng = np.random.default_rng(3)
+    A = rng.random(dims).astype(np.float32)
+    cd = torch.empty(P.cores_size(dims, ranks), device="cuda")
+    e_dev = h.ntt_decompose_bcd(torch.from_numpy(A.ravel()).cuda(), dims, ranks, 5, 0, cd, want_error=True)
+    ch = np.empty(P.cores_size(dims, ranks), dtype=np.float32)
+    e_host = h.ntt_decompose_bcd(np.ascontiguousarray(A.ravel()), dims, ranks, 5, 0, ch, want_error=True)
+    assert np.array_equal(cd.cpu().numpy(), ch) and e_dev == e_host
+    with pytest.raises(P.NttError):
+        h.ntt_decompose_bcd(torch.from_numpy(A.ravel()).cuda(), dims, [4, 33, 2], 5, 0, cd)
+    with pytest.raises(P.NttError):
+        h.ntt_decompose_bcd(torch.from_numpy(A.ravel()).cuda(), dims, ranks, 5, 0, cd, delta=1.5)

@@ -101,3 +101,17 @@ def test_ttsvd_unsupported(h):
     cores = torch.empty(10 ** 6, device="cuda")
     with pytest.raises(P.NttError):
         h.ntt_tt_svd(A, [600, 700], 0.1, cores, 10 ** 6)
+
+
+def test_ttsvd_host_buffers(h, ora):
+    """Host A and host cores (staged by the library) give the same result as device buffers."""
+    import paper_2008_01340_b200 as P
+    A = rand_tt((6, 5, 7, 4), (3, 4, 2), 5, 0.01)
+    dims = list(A.shape)
+    cap = P.cores_size(dims, [64] * 3)
+    cd = torch.empty(cap, device="cuda")
+    rd, ed = h.ntt_tt_svd(torch.from_numpy(A.ravel()).cuda(), dims, 0.05, cd, cap, want_error=True)
+    ch = np.empty(cap, dtype=np.float32)
+    rh, eh = h.ntt_tt_svd(np.ascontiguousarray(A.ravel()), dims, 0.05, ch, cap, want_error=True)
+    k = P.cores_size(dims, rd)
+    assert rd == rh and ed == eh and np.array_equal(cd.cpu().numpy()[:k], ch[:k])
