@@ -786,6 +786,12 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool persist = pa.iters > 0;
+  // BCD mode (PersistArgs::bcdL; see k_fused): row scales of H_m (smem), 1 / L_H, output buffer
+  const bool bcd = pa.bcdL != nullptr;
+  __shared__ float bsh[8];
+  if (tid < 8) bsh[tid] = (bcd && tid < r) ? (float)pa.bcdS[tid] : 1.f;
+  const float binvL = (bcd && *pa.bcdL > 0.0) ? (float)(1.0 / *pa.bcdL) : 0.f;
+  float* const Ho = (bcd && pa.Hout) ? pa.Hout : H;
   if (!persist && (mode & kFusedUpdate)) {
     const int rr = r * r;
     for (int e = tid; e < 64; e += NTHR) {
@@ -931,15 +937,22 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 #pragma unroll
         for (int l = 0; l < 8; ++l)
           hl[l] = *reinterpret_cast<const float*>(st + XB + l * 128 + (((ct >> 2) ^ l) << 4) + (ct & 3) * 4);
+        if (bcd) {
+#pragma unroll
+          for (int l = 0; l < 8; ++l) hl[l] *= bsh[l];
+        }
         float e0 = 0.0f, e1 = 0.0f;
 #pragma unroll
         for (int l = 0; l < 8; l += 2) {
           e0 = fmaf(Gs[kt * 8 + l], hl[l], e0);
           e1 = fmaf(Gs[kt * 8 + l + 1], hl[l + 1], e1);
         }
-        hn = mu_q(hkc, S, e0 + e1, eps);
+        if (bcd)  // prox-linear step (Alg. 3 l.14) on H_m = diag(sH) H_m stored
+          hn = fmaxf(0.f, fmaf(-((e0 + e1) - S), binvL, hkc * bsh[kt]));
+        else
+          hn = mu_q(hkc, S, e0 + e1, eps);
         if (kt >= r || col >= n) hn = 0.0f;
-        if (kt < r && col < n) H[(int64_t)kt * n + col] = hn;
+        if (kt < r && col < n) Ho[(int64_t)kt * n + col] = hn;
       } else {
         hn = (kt < r && col < n) ? hkc : 0.0f;
       }

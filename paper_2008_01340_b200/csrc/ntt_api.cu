@@ -80,6 +80,8 @@ struct ntt_handle_s {
   // staging for host buffers
   void* stage = nullptr;
   size_t stage_bytes = 0;
+  void* sweep = nullptr;  // ntt_decompose_bcd's H / W / cores buffers (kept across calls)
+  size_t sweep_bytes = 0;
   double* host_part = nullptr;  // pinned host landing zone for small reductions
   size_t host_part_count = 0;
   // distributed
@@ -782,6 +784,7 @@ ntt_status ntt_destroy(ntt_handle h) {
   if (h->ws) cudaFree(h->ws);
   if (h->ptrace) cudaFree(h->ptrace);
   if (h->stage) cudaFree(h->stage);
+  if (h->sweep) cudaFree(h->sweep);
   if (h->host_part) cudaFreeHost(h->host_part);
   if (h->comm_row && g_nccl.loaded) g_nccl.CommDestroy(h->comm_row);
   if (h->comm_col && g_nccl.loaded) g_nccl.CommDestroy(h->comm_col);
@@ -1147,7 +1150,18 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
     return fail(h, NTT_ERR_INVALID_ARG, "ntt_nmf_bcd takes device buffers");
   CU(h, cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
-  bool tc = tc_supported(m, n, r, ldx, X) && !getenv("NTT_NO_TC");
+  // one-pass fused kernels in BCD mode where they win (r <= 8): always for m <= 40 (k_fused);
+  // for 40 < m <= 256 (k_fused_c, non-persistent) measured on config 3's shapes against the
+  // tensor-core 2-pass path: 256 x 2^20 57 vs 88 ms / 100 it, 256 x 2^10 5.7 vs 7.5, but
+  // 256 x 2^15 19 vs 9.5 (per-launch CTA imbalance at ~3.5 tiles per CTA) -- so large or small n
+  static const int f1_max = [] {
+    const char* e = getenv("NTT_BCD_1PASS_M");
+    return e ? atoi(e) : 256;
+  }();
+  const bool f1_n = m <= 40 || n >= (int64_t(1) << 18) || n <= 4096;
+  const bool f1_shape = m <= f1_max && f1_n && fused_supported(m, n, r, ldx, X, H) && !use_wc() &&
+                        !getenv("NTT_BCD_NO_1PASS") && !getenv("NTT_BCD_NO_FUSED");
+  bool tc = !f1_shape && tc_supported(m, n, r, ldx, X) && !getenv("NTT_NO_TC");
   TcPlan tp;
   if (tc) {
     tp = plan_tc(m, n, r, h->num_sms);
@@ -1159,8 +1173,7 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   // short-wide X (r <= 8, m <= 256): P, Q from the 1-pass fused kernel's acc-only mode
   const bool fa = !tc && fused_supported(m, n, r, ldx, X, H) && !getenv("NTT_BCD_NO_FUSED");
   const int fparts = fa ? fused_partials(m, n, r, h->num_sms) : 0;
-  // m <= 40 (k_fused, not the CTA-cooperative k_fused_c): the whole H half-iteration in one pass
-  const bool f1 = fa && m <= 40 && !getenv("NTT_BCD_NO_1PASS");
+  const bool f1 = fa && f1_shape;  // the whole H half-iteration in one pass
   size_t o = 0;
   auto take = [&](size_t b) {
     size_t at = o;
@@ -1543,12 +1556,15 @@ ntt_status ntt_decompose_bcd(ntt_handle h, const float* A, int32_t d, const int6
   }
   float* buf = nullptr;
   const size_t nfl = 2 * hmax + wmax + (size_t)s.cores;
-  CU(h, cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(float) * nfl, cs));
-  struct Free {
-    float* p;
-    cudaStream_t st;
-    ~Free() { cudaFreeAsync(p, st); }
-  } fr{buf, cs};
+  if (h->sweep_bytes < sizeof(float) * nfl) {  // grown once, reused by later calls
+    CU(h, cudaStreamSynchronize(cs));
+    if (h->sweep) CU(h, cudaFree(h->sweep));
+    h->sweep = nullptr;
+    h->sweep_bytes = 0;
+    CU(h, cudaMalloc(&h->sweep, sizeof(float) * nfl));
+    h->sweep_bytes = sizeof(float) * nfl;
+  }
+  buf = reinterpret_cast<float*>(h->sweep);
   float* hb[2] = {buf, buf + hmax};
   float* Wd = buf + 2 * hmax;
   float* dcores = Wd + wmax;
