@@ -662,22 +662,46 @@ __global__ void k_bcd_commit(const float* __restrict__ V, float* __restrict__ Vm
 }
 
 // H side of l.18-27 with the scale vectors: Hp = diag(sHp) Hp_stored.  Accepted:
-// Hm = H + w_H (H - Hp), Hp = H; correction: Hm = Hp.  Element e is (k = e / n, j).
+// Hm = H + w_H (H - Hp), Hp = H; correction: Hm = Hp.  Rows k over blockIdx.y; float4 columns
+// when n % 4 == 0 (16-byte accesses: a streaming kernel needs the bytes in flight)
 __global__ void k_bcd_commit_h(const float* __restrict__ H, float* __restrict__ Hm, float* __restrict__ Hp, int r,
                                int64_t n, const double* __restrict__ sH, const double* __restrict__ bs) {
   const bool acc = bs[BS_ACC] != 0.0;
   const double w = bs[BS_WH];
+  const bool v4 = (n & 3) == 0;
   for (int k = blockIdx.y; k < r; k += gridDim.y) {
     const double sp = sH[32 + k];
     const int64_t base = (int64_t)k * n;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-      const double vp = (double)Hp[base + j] * sp;
-      if (acc) {
-        const double v = H[base + j];
-        Hm[base + j] = (float)(v + w * (v - vp));
-        Hp[base + j] = (float)v;
-      } else {
-        Hm[base + j] = (float)vp;
+    if (v4) {
+      const float4* H4 = reinterpret_cast<const float4*>(H + base);
+      float4* Hm4 = reinterpret_cast<float4*>(Hm + base);
+      float4* Hp4 = reinterpret_cast<float4*>(Hp + base);
+      for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n / 4; j += (int64_t)gridDim.x * blockDim.x) {
+        const float4 p4 = __ldcs(Hp4 + j);
+        if (acc) {
+          const float4 h4 = __ldcs(H4 + j);
+          float4 m4;
+          m4.x = (float)((double)h4.x + w * ((double)h4.x - (double)p4.x * sp));
+          m4.y = (float)((double)h4.y + w * ((double)h4.y - (double)p4.y * sp));
+          m4.z = (float)((double)h4.z + w * ((double)h4.z - (double)p4.z * sp));
+          m4.w = (float)((double)h4.w + w * ((double)h4.w - (double)p4.w * sp));
+          Hm4[j] = m4;
+          Hp4[j] = h4;
+        } else {
+          Hm4[j] = make_float4((float)((double)p4.x * sp), (float)((double)p4.y * sp), (float)((double)p4.z * sp),
+                               (float)((double)p4.w * sp));
+        }
+      }
+    } else {
+      for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const double vp = (double)Hp[base + j] * sp;
+        if (acc) {
+          const double v = H[base + j];
+          Hm[base + j] = (float)(v + w * (v - vp));
+          Hp[base + j] = (float)v;
+        } else {
+          Hm[base + j] = (float)vp;
+        }
       }
     }
   }
@@ -804,7 +828,8 @@ cudaError_t launch_bcd_hscale(double* sH, int r, const double* c, cudaStream_t s
 
 cudaError_t launch_bcd_commit_h(const float* H, float* Hm, float* Hp, int r, int64_t n, const double* sH,
                                 const double* bs, cudaStream_t st) {
-  const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 1184 / std::max(r, 1) + 1));
+  const int64_t per = (n & 3) == 0 ? n / 4 : n;
+  const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((per + 255) / 256, 2368 / std::max(r, 1) + 1));
   k_bcd_commit_h<<<dim3((unsigned)gx, (unsigned)r), 256, 0, st>>>(H, Hm, Hp, r, n, sH, bs);
   return cudaGetLastError();
 }
