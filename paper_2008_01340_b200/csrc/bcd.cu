@@ -440,11 +440,15 @@ __global__ void __launch_bounds__(WS_T) k_bcd_wside(const float* __restrict__ Wm
   __shared__ double Gp[WS_T];
   extern __shared__ float Wsm[];  // m x RP (the new W)
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  // the previous iteration's H commit stored H_m afresh (and H_prev when it accepted)
+  // the previous iteration's H commit stored H_m afresh (and H_prev when it accepted: copied, or
+  // in the one-pass path by swapping the roles of the two H buffers -- done here, in thread 0)
+  const bool prev_acc = bs[BS_ACC] != 0.0;
   if (t < 32) {
     sH[t] = 1.0;
-    if (bs[BS_ACC] != 0.0) sH[32 + t] = 1.0;
+    if (prev_acc) sH[32 + t] = 1.0;
   }
+  __syncthreads();
+  if (t == 0 && prev_acc) bs[BS_ROLE] = 1.0 - bs[BS_ROLE];
   const double LW = spec_dev<RP>(Qc, r, S);  // l.7
   if (t == 0) bs[BS_LW] = LW;
   for (int e = t; e < RP * RP; e += WS_T) {
@@ -707,6 +711,67 @@ __global__ void k_bcd_commit_h(const float* __restrict__ H, float* __restrict__ 
   }
 }
 
+// Role-swapped variant of the H commit (one-pass path): the candidate lives in B[role], H_prev
+// in B[1 - role].  Accepted: Hm = H + w_H (H - Hp) and the roles swap (k_bcd_wside flips
+// BS_ROLE), so H_prev := H costs nothing; correction: Hm = Hp.  3 H-sized streams instead of 4.
+__global__ void k_bcd_commit_h_role(const float* __restrict__ B0, const float* __restrict__ B1, float* __restrict__ Hm,
+                                    int r, int64_t n, const double* __restrict__ sH, const double* __restrict__ bs) {
+  const bool acc = bs[BS_ACC] != 0.0;
+  const bool role = bs[BS_ROLE] != 0.0;
+  const float* __restrict__ Hc = role ? B1 : B0;
+  const float* __restrict__ Hp = role ? B0 : B1;
+  const double w = bs[BS_WH];
+  const bool v4 = (n & 3) == 0;
+  for (int k = blockIdx.y; k < r; k += gridDim.y) {
+    const double sp = sH[32 + k];
+    const int64_t base = (int64_t)k * n;
+    if (v4) {
+      const float4* H4 = reinterpret_cast<const float4*>(Hc + base);
+      const float4* P4 = reinterpret_cast<const float4*>(Hp + base);
+      float4* M4 = reinterpret_cast<float4*>(Hm + base);
+      for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n / 4; j += (int64_t)gridDim.x * blockDim.x) {
+        const float4 p4 = __ldcs(P4 + j);
+        float4 m4;
+        if (acc) {
+          const float4 h4 = __ldcs(H4 + j);
+          m4.x = (float)((double)h4.x + w * ((double)h4.x - (double)p4.x * sp));
+          m4.y = (float)((double)h4.y + w * ((double)h4.y - (double)p4.y * sp));
+          m4.z = (float)((double)h4.z + w * ((double)h4.z - (double)p4.z * sp));
+          m4.w = (float)((double)h4.w + w * ((double)h4.w - (double)p4.w * sp));
+        } else {
+          m4 = make_float4((float)((double)p4.x * sp), (float)((double)p4.y * sp), (float)((double)p4.z * sp),
+                           (float)((double)p4.w * sp));
+        }
+        M4[j] = m4;
+      }
+    } else {
+      for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const double vp = (double)Hp[base + j] * sp;
+        if (acc) {
+          const double v = Hc[base + j];
+          Hm[base + j] = (float)(v + w * (v - vp));
+        } else {
+          Hm[base + j] = (float)vp;
+        }
+      }
+    }
+  }
+}
+
+// final logical H_prev of the role-swapped path into B0 (the caller's H): after an accepted last
+// iteration it is the candidate (pending swap, scale 1), otherwise B[1 - role] with its scale
+__global__ void k_bcd_hout_role(float* __restrict__ B0, const float* __restrict__ B1, int r, int64_t n,
+                                const double* __restrict__ sH, const double* __restrict__ bs) {
+  const bool acc = bs[BS_ACC] != 0.0;
+  const bool role = bs[BS_ROLE] != 0.0;
+  const bool in_b1 = acc ? role : !role;
+  const float* src = in_b1 ? B1 : B0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)r * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const float v = src[e];
+    B0[e] = acc ? v : (float)((double)v * sH[32 + (int)(e / n)]);
+  }
+}
+
 // out[k][j] = sH[32 + k] Hp[k][j] (the logical H_prev, returned at the end) or, with init,
 // sH[0..64) = 1
 __global__ void k_bcd_hout(const float* __restrict__ Hp, int r, int64_t n, double* __restrict__ sH,
@@ -877,6 +942,20 @@ cudaError_t launch_bcd_post(const double* Ppart, int nP, const double* Qpart, in
   }
   if (r <= 8) k_bcd_post<8><<<1, WS_T, sm, st>>>(Ppart, nP, Qpart, nQ, m, r, W, Wm, Wp, Pc, Qc, c, G, bs, trace);
   else k_bcd_post<16><<<1, WS_T, sm, st>>>(Ppart, nP, Qpart, nQ, m, r, W, Wm, Wp, Pc, Qc, c, G, bs, trace);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bcd_commit_h_role(float* B0, float* B1, float* Hm, int r, int64_t n, const double* sH,
+                                     const double* bs, cudaStream_t st) {
+  const int64_t per = (n & 3) == 0 ? n / 4 : n;
+  const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((per + 255) / 256, 2368 / std::max(r, 1) + 1));
+  k_bcd_commit_h_role<<<dim3((unsigned)gx, (unsigned)r), 256, 0, st>>>(B0, B1, Hm, r, n, sH, bs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bcd_hout_role(float* B0, float* B1, int r, int64_t n, const double* sH, const double* bs,
+                                 cudaStream_t st) {
+  k_bcd_hout_role<<<1184, 256, 0, st>>>(B0, B1, r, n, sH, bs);
   return cudaGetLastError();
 }
 

@@ -92,6 +92,7 @@ enum BcdState {
   BS_WH = 12,
   BS_IT = 13,     // iteration counter (trace index)
   BS_DELTA = 14,
+  BS_ROLE = 15,   // one-pass path: which of (H, H_prev's buffer) holds the candidate (0 / 1)
   BS_COUNT = 16
 };
 int bcd_w_ctas(int64_t m);
@@ -100,6 +101,11 @@ cudaError_t launch_bcd_w(const float* Wm, int64_t m, int r, const double* P, con
 cudaError_t launch_bcd_wnorm(float* W, float* Wp, int64_t m, int r, const double* c, double* Gpart, unsigned* maxw,
                              cudaStream_t st);
 cudaError_t launch_bcd_hscale(double* sH, int r, const double* c, cudaStream_t st);
+// role-swapped H buffers (one-pass path): B[role] holds the candidate, B[1 - role] H_prev
+cudaError_t launch_bcd_commit_h_role(float* B0, float* B1, float* Hm, int r, int64_t n, const double* sH,
+                                     const double* bs, cudaStream_t st);
+cudaError_t launch_bcd_hout_role(float* B0, float* B1, int r, int64_t n, const double* sH, const double* bs,
+                                 cudaStream_t st);
 cudaError_t launch_bcd_hout(const float* Hp, int r, int64_t n, double* sH, float* out, int init, const double* bs,
                             cudaStream_t st);
 // one-CTA W side / post-pass stages for small W (bcd_cta_ok: r <= 16, m * rclass <= 8192)

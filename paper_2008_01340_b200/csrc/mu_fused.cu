@@ -462,7 +462,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
     const double L = *pa.bcdL;
     binvL = L > 0.0 ? (float)(1.0 / L) : 0.f;
   }
-  float* const Ho = (bcd && pa.Hout) ? pa.Hout : H;
+  float* const Ho = (bcd && pa.Hout) ? ((pa.bcdRole && *pa.bcdRole != 0.0) ? pa.Hout2 : pa.Hout) : H;
   float2 hnext[R][CPL / 2];
   if (HDIRECT) load_h(warp, hnext);
 
@@ -791,7 +791,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   __shared__ float bsh[8];
   if (tid < 8) bsh[tid] = (bcd && tid < r) ? (float)pa.bcdS[tid] : 1.f;
   const float binvL = (bcd && *pa.bcdL > 0.0) ? (float)(1.0 / *pa.bcdL) : 0.f;
-  float* const Ho = (bcd && pa.Hout) ? pa.Hout : H;
+  float* const Ho = (bcd && pa.Hout) ? ((pa.bcdRole && *pa.bcdRole != 0.0) ? pa.Hout2 : pa.Hout) : H;
   if (!persist && (mode & kFusedUpdate)) {
     const int rr = r * r;
     for (int e = tid; e < 64; e += NTHR) {

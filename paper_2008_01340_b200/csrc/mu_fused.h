@@ -40,6 +40,8 @@ struct PersistArgs {
   const double* bcdL = nullptr;
   const double* bcdS = nullptr;
   float* Hout = nullptr;
+  float* Hout2 = nullptr;           // with bcdRole: Hn goes to (*bcdRole != 0 ? Hout2 : Hout)
+  const double* bcdRole = nullptr;
 };
 
 // One pass over X (m x n, row stride ldx) with the current W (m x r) and

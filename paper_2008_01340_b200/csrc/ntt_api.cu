@@ -1290,7 +1290,9 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
       pa.trace = nullptr;
       pa.bcdL = bs + BS_LH;
       pa.bcdS = sH;
-      pa.Hout = H;
+      pa.Hout = H;  // the two H buffers swap roles on acceptance (k_bcd_commit_h_role)
+      pa.Hout2 = Hp;
+      pa.bcdRole = bs + BS_ROLE;
       PLAUNCH(h, 0, xbytes + 8.0 * r * (double)n,
               launch_fused(X, ldx, m, n, r, W, G, 1, 0.0f, Hm, Ppart, Qpart, kFusedUpdate | kFusedAcc,
                            fused_grid(m, n, r, h->num_sms), st, &pa));
@@ -1314,7 +1316,8 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
       }
     }
     LAUNCH(h, launch_bcd_post(Ppart, nPp, Qpart, nQp, (int)m, r, W, Wm, Wp, Pc, Qc, c, G, bs, dtrace, st));
-    LAUNCH(h, launch_bcd_commit_h(H, Hm, Hp, r, n, sH, bs, st));  // l.18-27 (H side)
+    if (f1) LAUNCH(h, launch_bcd_commit_h_role(H, Hp, Hm, r, n, sH, bs, st));  // l.18-27 (H side)
+    else LAUNCH(h, launch_bcd_commit_h(H, Hm, Hp, r, n, sH, bs, st));
     return NTT_OK;
   };
   auto iteration = [&]() -> ntt_status {
@@ -1400,7 +1403,8 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   }
   // the last accepted iterates (l.28)
   CU(h, cudaMemcpyAsync(W, Wp, sizeof(float) * m * r, cudaMemcpyDeviceToDevice, st));
-  LAUNCH(h, launch_bcd_hout(Hp, r, n, sH, H, 0, bs, st));  // logical H_prev = diag(sHp) Hp
+  if (cta && f1) LAUNCH(h, launch_bcd_hout_role(H, Hp, r, n, sH, bs, st));  // logical H_prev (role-swapped)
+  else LAUNCH(h, launch_bcd_hout(Hp, r, n, sH, H, 0, bs, st));        // logical H_prev = diag(sHp) Hp
   if (objective_trace && iters > 0)
     CU(h, cudaMemcpyAsync(objective_trace, dtrace, sizeof(double) * iters, cudaMemcpyDeviceToHost, st));
   CU(h, cudaStreamSynchronize(st));
