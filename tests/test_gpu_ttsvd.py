@@ -115,3 +115,12 @@ def test_ttsvd_host_buffers(h, ora):
     rh, eh = h.ntt_tt_svd(np.ascontiguousarray(A.ravel()), dims, 0.05, ch, cap, want_error=True)
     k = P.cores_size(dims, rd)
     assert rd == rh and ed == eh and np.array_equal(cd.cpu().numpy()[:k], ch[:k])
+
+
+def test_ttsvd_large_ranks(h, ora):
+    """Ranks above 32 (the 64-rank classes of the X' = U^T X kernel and the eigensolver's
+    64-vector Rayleigh-Ritz) on an exact TT of ranks (40, 30) + small noise."""
+    A = rand_tt((48, 50, 40), (40, 30), 21, 1e-3)
+    ranks, cores, err = run(h, A, 1e-3)
+    compare(ora, A, 1e-3, ranks, cores, err)
+    assert ranks == [40, 30]
