@@ -60,12 +60,17 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uin
 }
 
 // split (a, b) = (K index 2p, 2p + 1) into packed hi / lo fp16 pairs (low half = lower K)
+// (packed fp32x2 / f16x2 conversions: per component the same IEEE round-to-nearest operations as
+// the scalar form -- scale, round to fp16, exact back-conversion, subtract, round -- so the parts
+// are bit-identical; half the converter-warp instructions)
 __device__ __forceinline__ void split2(float a, float b, float s, uint32_t& hi, uint32_t& lo) {
-  const float as = a * s, bs = b * s;
-  const __half ha = __float2half_rn(as), hb = __float2half_rn(bs);
-  const __half la = __float2half_rn(as - __half2float(ha)), lb = __float2half_rn(bs - __half2float(hb));
-  hi = (uint32_t)__half_as_ushort(ha) | ((uint32_t)__half_as_ushort(hb) << 16);
-  lo = (uint32_t)__half_as_ushort(la) | ((uint32_t)__half_as_ushort(lb) << 16);
+  const float2 v = __fmul2_rn(make_float2(a, b), make_float2(s, s));
+  const __half2 h = __floats2half2_rn(v.x, v.y);
+  const float2 hf = __half22float2(h);
+  const float2 d = __fadd2_rn(v, make_float2(-hf.x, -hf.y));
+  const __half2 l = __floats2half2_rn(d.x, d.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
 // MODE 0: D (Mtot = m) = X Bcat^T, A = X rows: two [128 rows][32 cols] boxes per stage.
