@@ -37,6 +37,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "kernels.h"
 #include "mu_tc.h"
 #include "sm100.cuh"
 
@@ -647,10 +648,10 @@ cudaError_t tc_prepare(const TcPlan& p, const float* X, int64_t ldx, float* H, c
 }
 
 cudaError_t tc_sum_Q(const TcPlan& p, char* ws, cudaStream_t st) {
-  const int len = p.r * p.r;
-  k_tc_sum<<<(len + 127) / 128, 128, 0, st>>>(reinterpret_cast<double*>(ws + p.off_Q), p.nQ, len,
-                                              reinterpret_cast<double*>(ws + p.off_Qred));
-  return cudaGetLastError();
+  // r^2 entries over nQ (up to 4 x 148) partials: one warp per entry (launch_sum_partials), not
+  // one thread walking every partial (88 us on config 5)
+  return launch_sum_partials(reinterpret_cast<double*>(ws + p.off_Q), p.nQ, (int64_t)p.r * p.r,
+                             reinterpret_cast<double*>(ws + p.off_Qred), st);
 }
 
 cudaError_t tc_pass_w(const TcPlan& p, const TcMaps& mp, char* ws, int evict_first, cudaStream_t st) {
@@ -682,9 +683,7 @@ cudaError_t tc_wupdate_ex(const TcPlan& p, float* W, float eps, char* ws, const 
     k_tc_wupdate<32><<<g, UPD_ROWS, 0, st>>>(W, p.m, p.r, P, nP, Qr, eps, Wcat, p.ldw, G, mxw);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
-  const int len = p.r * p.r;
-  k_tc_sum<<<(len + 127) / 128, 128, 0, st>>>(G, p.nG, len, reinterpret_cast<double*>(ws + p.off_Gred));
-  return cudaGetLastError();
+  return launch_sum_partials(G, p.nG, (int64_t)p.r * p.r, reinterpret_cast<double*>(ws + p.off_Gred), st);
 }
 
 cudaError_t tc_pass_h(const TcPlan& p, const TcMaps& mp, char* ws, int evict_first, cudaStream_t st) {
