@@ -296,11 +296,11 @@ k_tc_wupdate(float* __restrict__ W, int64_t m, int r, const double* __restrict__
              const double* __restrict__ Qred, float eps, float* __restrict__ WcatT, int64_t ldw,
              double* __restrict__ Gpart, unsigned* __restrict__ maxw) {
   __shared__ double Qs[R * R];
+  __shared__ float Wn[UPD_ROWS][R + 1];
   // the CTA's rows own a contiguous run of rows * r doubles in every split partial: summed
-  // coalesced (thread t: elements t + 128 q) into Ps, which later holds Wn (same storage)
-  __shared__ __align__(16) unsigned char ubuf[UPD_ROWS * R * sizeof(double)];
-  double(*Ps) = reinterpret_cast<double*>(ubuf);
-  float(*Wn)[R + 1] = reinterpret_cast<float(*)[R + 1]>(ubuf);
+  // coalesced (thread t: elements t + 128 q, in split order) straight into shared memory (no
+  // register staging: fewer registers, more CTAs per SM for this latency-bound kernel)
+  extern __shared__ double Ps[];  // UPD_ROWS * r
   const int rr = r * r;
   for (int t = threadIdx.x; t < R * R; t += blockDim.x) {
     const int k = t / R, l = t % R;
@@ -311,28 +311,13 @@ k_tc_wupdate(float* __restrict__ W, int64_t m, int r, const double* __restrict__
   {
     const int len = (int)(min((int64_t)UPD_ROWS, m - i0) * r);
     const int64_t mr = m * r;
-    double acc[R];
-#pragma unroll
-    for (int q = 0; q < R; ++q) acc[q] = 0.0;
+    for (int e = threadIdx.x; e < len; e += UPD_ROWS) Ps[e] = 0.0;
     for (int b = 0; b < nP; ++b) {
       const double* src = Ppart + (int64_t)b * mr + i0 * r;
-#pragma unroll
-      for (int q = 0; q < R; ++q) {
-        const int e = threadIdx.x + q * UPD_ROWS;
-        if (e < len) acc[q] += src[e];
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const int e = threadIdx.x + q * UPD_ROWS;
-      if (e < len) Ps[e] = acc[q];
+      for (int e = threadIdx.x; e < len; e += UPD_ROWS) Ps[e] += src[e];
     }
   }
   __syncthreads();
-  double pv[R];
-#pragma unroll
-  for (int k = 0; k < R; ++k) pv[k] = (i < m && k < r) ? Ps[threadIdx.x * r + k] : 0.0;
-  __syncthreads();  // Ps -> Wn
   if (i < m) {
     double w[R];
 #pragma unroll
@@ -341,7 +326,7 @@ k_tc_wupdate(float* __restrict__ W, int64_t m, int r, const double* __restrict__
     for (int k = 0; k < R; ++k) {
       float wn = 0.0f;
       if (k < r) {
-        const double p = pv[k];
+        const double p = Ps[threadIdx.x * r + k];
         double d = 0.0;
 #pragma unroll
         for (int l = 0; l < R; ++l) d += w[l] * Qs[l * R + k];
@@ -386,11 +371,10 @@ k_tc_hupdate(float* __restrict__ H, int64_t n, int r, const double* __restrict__
              double* __restrict__ Qpart, unsigned* __restrict__ maxh) {
   float hmax = 0.0f;
   __shared__ float Gs[R * R];
+  __shared__ float Hn[R][UPD_ROWS + 1];
   // S of the block's 128 columns (a contiguous run of cols * r doubles per split), summed
-  // coalesced into Ss, which later holds Hn (same storage)
-  __shared__ __align__(16) unsigned char ubuf[UPD_ROWS * R * sizeof(double)];
-  double* Ss = reinterpret_cast<double*>(ubuf);
-  float(*Hn)[UPD_ROWS + 1] = reinterpret_cast<float(*)[UPD_ROWS + 1]>(ubuf);
+  // coalesced straight into shared memory in split order (no register staging)
+  extern __shared__ double Ss[];  // UPD_ROWS * r
   const int rr = r * r;
   if (update)
     for (int t = threadIdx.x; t < R * R; t += blockDim.x) {
@@ -406,30 +390,15 @@ k_tc_hupdate(float* __restrict__ H, int64_t n, int r, const double* __restrict__
   for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     __syncthreads();
     const int64_t j = blk * UPD_ROWS + threadIdx.x;
-    double sv[R];
     if (update) {
       const int len = (int)(min((int64_t)UPD_ROWS, n - blk * UPD_ROWS) * r);
       const int64_t nr = n * r;
-      double acc[R];
-#pragma unroll
-      for (int q = 0; q < R; ++q) acc[q] = 0.0;
+      for (int e = threadIdx.x; e < len; e += UPD_ROWS) Ss[e] = 0.0;
       for (int b = 0; b < nS; ++b) {
         const double* src = Spart + (int64_t)b * nr + blk * UPD_ROWS * r;
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
-          const int e = threadIdx.x + q * UPD_ROWS;
-          if (e < len) acc[q] += src[e];
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < R; ++q) {
-        const int e = threadIdx.x + q * UPD_ROWS;
-        if (e < len) Ss[e] = acc[q];
+        for (int e = threadIdx.x; e < len; e += UPD_ROWS) Ss[e] += src[e];
       }
       __syncthreads();
-#pragma unroll
-      for (int k = 0; k < R; ++k) sv[k] = (j < n && k < r) ? Ss[threadIdx.x * r + k] : 0.0;
-      __syncthreads();  // Ss -> Hn
     }
     if (j < n) {
       float h[R];
@@ -439,7 +408,7 @@ k_tc_hupdate(float* __restrict__ H, int64_t n, int r, const double* __restrict__
       for (int k = 0; k < R; ++k) {
         float hn = h[k];
         if (update && k < r) {
-          const double sd = sv[k];
+          const double sd = Ss[threadIdx.x * r + k];
           float e = 0.0f;
 #pragma unroll
           for (int l = 0; l < R; ++l) e = fmaf(Gs[k * R + l], h[l], e);
@@ -677,10 +646,16 @@ cudaError_t tc_wupdate_ex(const TcPlan& p, float* W, float eps, char* ws, const 
   unsigned* mxw = tc_maxw(p, ws, 3 + (it & 1));
   double* G = reinterpret_cast<double*>(ws + p.off_G);
   const unsigned g = (unsigned)p.nG;
+  const size_t dsm = sizeof(double) * UPD_ROWS * p.r;  // <= 32 KB (+ ~25 KB static: opt in above 48 KB)
+  {
+    cudaError_t ea = p.R == 16 ? cudaFuncSetAttribute(k_tc_wupdate<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm)
+                               : cudaFuncSetAttribute(k_tc_wupdate<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+    if (ea) return ea;
+  }
   if (p.R == 16)
-    k_tc_wupdate<16><<<g, UPD_ROWS, 0, st>>>(W, p.m, p.r, P, nP, Qr, eps, Wcat, p.ldw, G, mxw);
+    k_tc_wupdate<16><<<g, UPD_ROWS, dsm, st>>>(W, p.m, p.r, P, nP, Qr, eps, Wcat, p.ldw, G, mxw);
   else
-    k_tc_wupdate<32><<<g, UPD_ROWS, 0, st>>>(W, p.m, p.r, P, nP, Qr, eps, Wcat, p.ldw, G, mxw);
+    k_tc_wupdate<32><<<g, UPD_ROWS, dsm, st>>>(W, p.m, p.r, P, nP, Qr, eps, Wcat, p.ldw, G, mxw);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
   return launch_sum_partials(G, p.nG, (int64_t)p.r * p.r, reinterpret_cast<double*>(ws + p.off_Gred), st);
@@ -705,10 +680,18 @@ cudaError_t tc_hupdate_ex(const TcPlan& p, float* H, float eps, char* ws, const 
   float* Hcat = p.f16 ? nullptr : reinterpret_cast<float*>(ws + p.off_hcat);
   double* Q = reinterpret_cast<double*>(ws + p.off_Q);
   const unsigned g = (unsigned)p.nQ;
+  {
+    const int dsm = (int)(sizeof(double) * UPD_ROWS * p.r);
+    cudaError_t ea = p.R == 16 ? cudaFuncSetAttribute(k_tc_hupdate<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm)
+                               : cudaFuncSetAttribute(k_tc_hupdate<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);
+    if (ea) return ea;
+  }
   if (p.R == 16)
-    k_tc_hupdate<16><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, S, nS, Gr, eps, true, Hcat, p.ldh, Q, mxh);
+    k_tc_hupdate<16><<<g, UPD_ROWS, sizeof(double) * UPD_ROWS * p.r, st>>>(H, p.n, p.r, S, nS, Gr, eps, true, Hcat,
+                                                                            p.ldh, Q, mxh);
   else
-    k_tc_hupdate<32><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, S, nS, Gr, eps, true, Hcat, p.ldh, Q, mxh);
+    k_tc_hupdate<32><<<g, UPD_ROWS, sizeof(double) * UPD_ROWS * p.r, st>>>(H, p.n, p.r, S, nS, Gr, eps, true, Hcat,
+                                                                            p.ldh, Q, mxh);
   return cudaGetLastError();
 }
 
