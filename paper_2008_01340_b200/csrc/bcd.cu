@@ -238,22 +238,11 @@ k_bcd_hup(const double* __restrict__ Spart, int nS, int64_t n, int r, const doub
     const int64_t j0 = blk * BH_BN;
     const int cols = (int)min((int64_t)BH_BN, n - j0);
     const int len = cols * r;
-    double acc[R];
-#pragma unroll
-    for (int q = 0; q < R; ++q) acc[q] = 0.0;
-    for (int b = 0; b < nS; ++b) {
+    __syncthreads();  // the previous block's readers are done with Ss
+    for (int e = threadIdx.x; e < len; e += BH_BN) Ss[e] = 0.0;
+    for (int b = 0; b < nS; ++b) {  // split order, straight into shared memory (few registers)
       const double* src = Spart + (int64_t)b * nr + j0 * r;
-#pragma unroll
-      for (int q = 0; q < R; ++q) {
-        const int e = threadIdx.x + q * BH_BN;
-        if (e < len) acc[q] += src[e];
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const int e = threadIdx.x + q * BH_BN;
-      if (e < len) Ss[e] = acc[q];
+      for (int e = threadIdx.x; e < len; e += BH_BN) Ss[e] += src[e];
     }
     __syncthreads();
     if (threadIdx.x < cols) {

@@ -115,6 +115,9 @@ struct ntt_handle_s {
   cudaStream_t gstream = nullptr;
   cudaEvent_t gev_in = nullptr, gev_out = nullptr;
   cudaGraphExec_t gexec = nullptr;
+  cudaGraphExec_t bcd_exec = nullptr;  // ntt_nmf_bcd's one-iteration graph, reused while its key matches
+  std::string bcd_key;
+  int64_t bcd_per_it = 0;
   std::vector<uint64_t> gkey;
   std::vector<cudaEvent_t> gev_pool;
   size_t gev_used = 0;
@@ -792,6 +795,7 @@ ntt_status ntt_destroy(ntt_handle h) {
   for (auto e : h->ev_pool) cudaEventDestroy(e);
   for (auto e : h->gev_pool) cudaEventDestroy(e);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  if (h->bcd_exec) cudaGraphExecDestroy(h->bcd_exec);
   if (h->gev_in) cudaEventDestroy(h->gev_in);
   if (h->gev_out) cudaEventDestroy(h->gev_out);
   if (h->gstream) cudaStreamDestroy(h->gstream);
@@ -1375,25 +1379,39 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
     CU(h, cudaStreamWaitEvent(h->gstream, h->gev_in, 0));
     const int64_t l0 = h->launches;
     st = h->gstream;
-    cudaError_t e0 = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
-    ntt_status si = e0 == cudaSuccess ? iteration() : NTT_ERR_CUDA;
-    cudaGraph_t g = nullptr;
-    cudaError_t e1 = cudaStreamEndCapture(st, &g);
-    const int64_t per_it = h->launches - l0;
-    if (e0 != cudaSuccess || si != NTT_OK || e1 != cudaSuccess) {
-      if (g) cudaGraphDestroy(g);
-      if (si != NTT_OK) return si;
-      return fail(h, NTT_ERR_CUDA, "BCD graph capture failed: %s", cudaGetErrorString(e0 ? e0 : e1));
+    // the graph bakes in pointers, sizes and tensor maps: reuse it while they are unchanged
+    char kb[256];
+    snprintf(kb, sizeof(kb), "%p %p %p %p %lld %lld %lld %d", (const void*)X, (void*)W, (void*)H, (void*)h->ws,
+             (long long)m, (long long)n, (long long)ldx, r);
+    if (!h->bcd_exec || h->bcd_key != kb) {
+      if (h->bcd_exec) {
+        cudaGraphExecDestroy(h->bcd_exec);
+        h->bcd_exec = nullptr;
+        h->bcd_key.clear();
+      }
+      cudaError_t e0 = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+      ntt_status si = e0 == cudaSuccess ? iteration() : NTT_ERR_CUDA;
+      cudaGraph_t g = nullptr;
+      cudaError_t e1 = cudaStreamEndCapture(st, &g);
+      h->bcd_per_it = h->launches - l0;
+      h->launches = l0;
+      if (e0 != cudaSuccess || si != NTT_OK || e1 != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        if (si != NTT_OK) return si;
+        return fail(h, NTT_ERR_CUDA, "BCD graph capture failed: %s", cudaGetErrorString(e0 ? e0 : e1));
+      }
+      cudaError_t e2 = cudaGraphInstantiate(&h->bcd_exec, g, 0);
+      cudaGraphDestroy(g);
+      if (e2 != cudaSuccess) {
+        h->bcd_exec = nullptr;
+        return fail(h, NTT_ERR_CUDA, "BCD graph instantiate: %s", cudaGetErrorString(e2));
+      }
+      h->bcd_key = kb;
     }
-    cudaGraphExec_t ge_ = nullptr;
-    cudaError_t e2 = cudaGraphInstantiate(&ge_, g, 0);
-    cudaGraphDestroy(g);
-    if (e2 != cudaSuccess) return fail(h, NTT_ERR_CUDA, "BCD graph instantiate: %s", cudaGetErrorString(e2));
     cudaError_t el = cudaSuccess;
-    for (int it = 0; it < iters && el == cudaSuccess; ++it) el = cudaGraphLaunch(ge_, st);
-    cudaGraphExecDestroy(ge_);
+    for (int it = 0; it < iters && el == cudaSuccess; ++it) el = cudaGraphLaunch(h->bcd_exec, st);
     if (el != cudaSuccess) return fail(h, NTT_ERR_CUDA, "BCD graph launch: %s", cudaGetErrorString(el));
-    h->launches = l0 + per_it * iters;
+    h->launches = l0 + h->bcd_per_it * iters;
     CU(h, cudaEventRecord(h->gev_out, st));
     st = h->stream;
     CU(h, cudaStreamWaitEvent(st, h->gev_out, 0));
