@@ -841,10 +841,6 @@ __global__ void k_sumsq(const float* __restrict__ v, int64_t rows, int64_t cols,
   }
 }
 
-__global__ void k_copy_last(const double* __restrict__ eig, int N, double* __restrict__ out) {
-  if (threadIdx.x == 0) out[0] = eig[N - 1];
-}
-
 int rcls_bcd(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : r <= 32 ? 32 : 64; }
 
 }  // namespace
@@ -1038,11 +1034,6 @@ int sumsq_ctas() { return 1184; }
 
 cudaError_t launch_sumsq(const float* v, int64_t rows, int64_t cols, int64_t ld, double* part, cudaStream_t st) {
   k_sumsq<<<1184, 256, 0, st>>>(v, rows, cols, ld, part);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_copy_last(const double* eig, int N, double* out, cudaStream_t st) {
-  k_copy_last<<<1, 32, 0, st>>>(eig, N, out);
   return cudaGetLastError();
 }
 

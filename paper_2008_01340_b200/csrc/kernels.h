@@ -57,7 +57,6 @@ size_t rank_rule_bytes(int64_t N, int64_t T, int num_sms);
 cudaError_t launch_rank_rule(const float* X, int64_t m, int64_t n, int64_t ldx, double tt_eps, char* ws,
                              int num_sms, int* d_rank, double* d_eig, cudaStream_t st);
 
-cudaError_t launch_sym_eig(double* C, int N, double* scratch, double* eig, int* rank_dummy, cudaStream_t st);
 // fp64 Gram of X (X X^T if m <= n else X^T X) into ws (partials, then C = *Cout, N x N);
 // needs rank_rule_bytes(min(m, n), max(m, n), num_sms)
 cudaError_t launch_gram(const float* X, int64_t m, int64_t n, int64_t ldx, char* ws, int num_sms, double** Cout,
@@ -139,7 +138,6 @@ cudaError_t launch_scale_copy(const float* src, float* a, float* b, int64_t cnt,
                               cudaStream_t st);
 int sumsq_ctas();
 cudaError_t launch_sumsq(const float* v, int64_t rows, int64_t cols, int64_t ld, double* part, cudaStream_t st);
-cudaError_t launch_copy_last(const double* eig, int N, double* out, cudaStream_t st);
 
 // 1/2 ||X - W H||^2 partial sums (fp64), one per CTA; returns number of partials.
 int objective_ctas(int64_t n);

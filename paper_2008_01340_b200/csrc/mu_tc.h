@@ -71,7 +71,6 @@ unsigned* tc16_max_slot(const TcPlan& p, char* ws, int slot);
 cudaError_t tc16_pack_h_slot(const TcPlan& p, const float* H, char* ws, cudaStream_t st, int slot);
 cudaError_t tc16_pack_w_slot(const TcPlan& p, const float* W, char* ws, cudaStream_t st, int slot);
 cudaError_t tc16_pack_h_fresh(const TcPlan& p, const float* H, char* ws, cudaStream_t st);
-cudaError_t tc16_pack_w_fresh(const TcPlan& p, const float* W, char* ws, cudaStream_t st);
 // flush: K tiles (of 64) accumulated in fp32 in TMEM before the fp64 flush (MU: 16; BCD uses
 // a shorter interval because its objective takes a difference of large terms, R25)
 cudaError_t tc16_pass_w(const TcPlan& p, const TcMaps& mp, char* ws, int evict_first, cudaStream_t st,

@@ -464,13 +464,6 @@ cudaError_t tc16_pack_h_fresh(const TcPlan& p, const float* H, char* ws, cudaStr
   return tc16_pack_h_slot(p, H, ws, st, 7);
 }
 
-cudaError_t tc16_pack_w_fresh(const TcPlan& p, const float* W, char* ws, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(tc16_max_slot(p, ws, 7), 0, sizeof(unsigned), st);
-  if (e) return e;
-  k_absmax<<<2 * p.grid, 256, 0, st>>>(W, 1, p.m * p.r, p.m * p.r, tc16_max_slot(p, ws, 7));
-  return tc16_pack_w_slot(p, W, ws, st, 7);
-}
-
 cudaError_t tc16_pass_w(const TcPlan& p, const TcMaps& mp, char* ws, int ef, cudaStream_t st, int flush) {
   double* P = reinterpret_cast<double*>(ws + p.off_P);
   const float* sc = reinterpret_cast<const float*>(ws + p.off_scales);

@@ -324,14 +324,4 @@ cudaError_t launch_rank_rule(const float* X, int64_t m, int64_t n, int64_t ldx, 
   return cudaGetLastError();
 }
 
-// eigenvalues (ascending) of a symmetric fp64 N x N matrix C (destroyed), N <= 512;
-// scratch: 2 N doubles; eig: N doubles; rank_dummy: one int (the rank rule output, unused)
-cudaError_t launch_sym_eig(double* C, int N, double* scratch, double* eig, int* rank_dummy, cudaStream_t st) {
-  const size_t sm = sizeof(double) * (6 * (size_t)N + 40);
-  cudaError_t e = cudaFuncSetAttribute(k_eig_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e) return e;
-  k_eig_rank<<<1, ET, sm, st>>>(C, N, scratch, scratch + N, 1.0, eig, rank_dummy);
-  return cudaGetLastError();
-}
-
 }  // namespace ntt
