@@ -16,6 +16,12 @@
 //                the l.17 branch and the extrapolation weights, on the device
 //   k_bcd_commit V_m = V + w (V - V_prev), V_prev = V (accepted) or V_m = V_prev (correction)
 //   k_bcd_commit_pq  P, Q = those of the new H (accepted) or of the rescaled H_prev
+//   k_bcd_commit_h(_role)  the H side of the commit (float4 streams; the role variant swaps
+//                the candidate / H_prev buffers instead of copying)
+//   k_bcd_wside / k_bcd_post  one-CTA forms of the W side and of everything after the H pass
+//                for small W (m r <= 8192, r <= 16)
+// The X passes themselves are the MU kernels: k_fused / k_fused_c in their BCD mode (one pass
+// per H half-iteration), their acc-only mode, or the fp16x2 tensor-core passes.
 // Every decision stays on the device (state block `bs`, below), so one iteration is
 // a fixed launch sequence the host captures once in a CUDA graph and replays.
 #include <algorithm>
