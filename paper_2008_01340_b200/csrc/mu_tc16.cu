@@ -323,13 +323,15 @@ __global__ void k_pack16(const float* __restrict__ F, int r, int64_t len, bool t
                          const unsigned* __restrict__ maxbits, __half* __restrict__ dst, int64_t ldd,
                          float* __restrict__ scales, int sidx, unsigned* __restrict__ reset) {
   const float s = pow2_scale(*maxbits);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
     scales[sidx] = s;
     *reset = 0u;  // the next update's max slot (the other parity)
   }
-  // j (the long index) over threads / CTAs, k in an inner loop: no division per element
+  // j (the long index) over threads / CTAs, k in an inner loop over this CTA row's chunk of 8
+  // ranks (blockIdx.y): no division per element, and r / 8 times the threads of one k loop
+  const int k0 = 8 * blockIdx.y, k1 = min(r, k0 + 8);
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (int64_t)gridDim.x * blockDim.x) {
-    for (int k = 0; k < r; ++k) {
+    for (int k = k0; k < k1; ++k) {
       const float v = (transposed ? F[j * r + k] : F[(int64_t)k * len + j]) * s;
       const __half h = __float2half_rn(v);
       dst[(int64_t)k * ldd + j] = h;
@@ -421,7 +423,7 @@ cudaError_t tc16_pack_h(const TcPlan& p, const float* H, char* ws, cudaStream_t 
     cudaError_t e = cudaGetLastError();
     if (e) return e;
   }
-  k_pack16<<<4 * p.grid, 256, 0, st>>>(H, p.r, p.n, false, p.R, cur, reinterpret_cast<__half*>(ws + p.off_h16), p.ldh16,
+  k_pack16<<<dim3(4 * p.grid, (p.r + 7) / 8), 256, 0, st>>>(H, p.r, p.n, false, p.R, cur, reinterpret_cast<__half*>(ws + p.off_h16), p.ldh16,
                                        reinterpret_cast<float*>(ws + p.off_scales), 1, mx + 1 + ((it + 1) & 1));
   return cudaGetLastError();
 }
@@ -429,7 +431,7 @@ cudaError_t tc16_pack_h(const TcPlan& p, const float* H, char* ws, cudaStream_t 
 // fp16 parts of W (m x r) transposed -> WcatT16, scale at scales[2]; max|W| from k_tc_wupdate
 cudaError_t tc16_pack_w(const TcPlan& p, const float* W, char* ws, cudaStream_t st, int it) {
   unsigned* mx = reinterpret_cast<unsigned*>(ws + p.off_scales + 64);
-  k_pack16<<<4 * p.grid, 256, 0, st>>>(W, p.r, p.m, true, p.R, mx + 3 + (it & 1),
+  k_pack16<<<dim3(4 * p.grid, (p.r + 7) / 8), 256, 0, st>>>(W, p.r, p.m, true, p.R, mx + 3 + (it & 1),
                                        reinterpret_cast<__half*>(ws + p.off_w16), p.ldw16,
                                        reinterpret_cast<float*>(ws + p.off_scales), 2, mx + 3 + ((it + 1) & 1));
   return cudaGetLastError();
@@ -443,14 +445,14 @@ unsigned* tc16_max_slot(const TcPlan& p, char* ws, int slot) {
 }
 
 cudaError_t tc16_pack_h_slot(const TcPlan& p, const float* H, char* ws, cudaStream_t st, int slot) {
-  k_pack16<<<4 * p.grid, 256, 0, st>>>(H, p.r, p.n, false, p.R, tc16_max_slot(p, ws, slot),
+  k_pack16<<<dim3(4 * p.grid, (p.r + 7) / 8), 256, 0, st>>>(H, p.r, p.n, false, p.R, tc16_max_slot(p, ws, slot),
                                        reinterpret_cast<__half*>(ws + p.off_h16), p.ldh16,
                                        reinterpret_cast<float*>(ws + p.off_scales), 1, tc16_max_slot(p, ws, 4));
   return cudaGetLastError();
 }
 
 cudaError_t tc16_pack_w_slot(const TcPlan& p, const float* W, char* ws, cudaStream_t st, int slot) {
-  k_pack16<<<4 * p.grid, 256, 0, st>>>(W, p.r, p.m, true, p.R, tc16_max_slot(p, ws, slot),
+  k_pack16<<<dim3(4 * p.grid, (p.r + 7) / 8), 256, 0, st>>>(W, p.r, p.m, true, p.R, tc16_max_slot(p, ws, slot),
                                        reinterpret_cast<__half*>(ws + p.off_w16), p.ldw16,
                                        reinterpret_cast<float*>(ws + p.off_scales), 2, tc16_max_slot(p, ws, 4));
   return cudaGetLastError();
