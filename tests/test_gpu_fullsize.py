@@ -151,3 +151,53 @@ def test_persistent_long_runs(h, m, n, r, iters):
     for a, b in zip(outs[0], outs[2]):
         assert np.all(np.isfinite(a))
         assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(b)
+
+
+@pytest.mark.timeout(300)
+def test_bcd_config5_slice_properties(h):
+    """BCD (f1) at the config-5 slice size (32768 x 65536, r 32: tensor-core passes, the large-W
+    kernels): accepted objective non-increasing, factors non-negative, and the last accepted
+    objective equal to 1/2 ||X - W H||^2 of the returned factors within 1e-5 ||X||^2 (R25)."""
+    import ntt_inputs as ni2
+    w = ni2.workloads()["config5"]
+    m, n, r = 32768, w.dims[1], w.ranks[0]
+    dims, ranks, cores = ni2.make_factor_cores(m, n, r, 0)
+    X = torch.empty(m * n, device="cuda")
+    h.ntt_generate(dims, ranks, torch.from_numpy(cores.astype(np.float32)).cuda(), w.noise_amp or 0.01, 0,
+                   ni2.STREAM_NOISE, X)
+    W = torch.empty(m * r, device="cuda")
+    H = torch.empty(r * n, device="cuda")
+    h.ntt_fill_uniform(W, m * r, 0, ni2.stream_w(1))
+    h.ntt_fill_uniform(H, r * n, 0, ni2.stream_h(1))
+    tr = np.array(h.ntt_nmf_bcd(X, m, n, n, r, 10, W, H, trace=True))
+    assert np.all(np.diff(tr) <= 0) and float(W.min()) >= 0 and float(H.min()) >= 0
+    Xm = X.view(m, n)
+    res = 0.0
+    for i0 in range(0, m, 4096):  # fp64 residual in row blocks
+        blk = Xm[i0:i0 + 4096].double() - W.view(m, r)[i0:i0 + 4096].double() @ H.view(r, n).double()
+        res += float((blk * blk).sum())
+        del blk
+    obj0 = 0.5 * float((Xm.double() ** 2).sum())
+    assert abs(0.5 * res - tr[-1]) <= 1e-5 * obj0
+
+
+@pytest.mark.timeout(300)
+def test_ttsvd_config3_properties(h, config3_A):
+    """TT-SVD (f4) at config 3's full size (32^6, ranks capped at 8), checked through properties
+    that hold at any size: left-orthonormal cores (U^T U = I for every core but the last) and
+    the library's Eq. 3 error equal to the oracle's error of the same cores (R15)."""
+    import oracle
+    import paper_2008_01340_b200 as P
+    w, A = config3_A
+    cap = P.cores_size(w.dims, [64] * (len(w.dims) - 1))
+    cores = torch.empty(cap, device="cuda")
+    ranks, err = h.ntt_tt_svd(torch.from_numpy(A.ravel()).cuda(), w.dims, 0.0, cores, cap, max_ranks=w.ranks,
+                              want_error=True)
+    assert ranks == list(w.ranks)
+    c = cores[: P.cores_size(w.dims, ranks)].cpu().numpy().astype(np.float64)
+    parts = oracle.unpack_cores(w.dims, ranks, c)
+    for G in parts[:-1]:
+        M = G.reshape(-1, G.shape[-1])
+        assert np.abs(M.T @ M - np.eye(M.shape[1])).max() <= 1e-5
+    e_ora = oracle.tt_rel_error_split(A, ranks, c)
+    assert abs(err - e_ora) <= 1e-3 * e_ora + 1e-6
