@@ -275,6 +275,18 @@ def other_workloads(h, P, ni, torch, steps=2):
         torch.cuda.synchronize()
         row = {"ttsvd_ms": e0.elapsed_time(e1) / steps, "ranks": ranks, "rel_error": err,
                "path": "ntt_tt_svd: fp64 Gram + one-CTA eigensolver per step (tt_svd.cu)"}
+        # nTT with the paper's BCD NMF at every step (Alg. 2 + Alg. 3, SURVEY s.8(f) f1) at the same ranks
+        bc = torch.empty(P.cores_size(w.dims, w.ranks), device="cuda")
+        h.ntt_decompose_bcd(A, w.dims, w.ranks, w.iters, w.seed, bc)
+        e0, e1 = ev(), ev()
+        e0.record()
+        errb = h.ntt_decompose_bcd(A, w.dims, w.ranks, w.iters, w.seed, bc, want_error=True)
+        e1.record()
+        torch.cuda.synchronize()
+        out.setdefault(name, {})["bcd_sweep"] = {"ntt_wall_ms": e0.elapsed_time(e1), "rel_error": errb,
+                                                 "iters_per_step": w.iters,
+                                                 "path": "ntt_decompose_bcd: BCD NMF (Alg. 3) at every TT step"}
+        del bc
         out.setdefault(name, {})["ttsvd"] = row
         del A, cores
         torch.cuda.empty_cache()

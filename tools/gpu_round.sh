@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_fullsize.py -q -k "bcd_config5 or ttsvd_config3" 2>&1 | grep -E "^E  |passed|failed" | head -10
+SECONDS=0; timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; echo "bench rc $? ${SECONDS}s"
