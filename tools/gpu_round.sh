@@ -1,4 +1,3 @@
-set -x
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?"; tail -1 gpurun_out/pytest_gpu.log
-timeout 300 python __graft_entry__.py --smoke > gpurun_out/smoke.log 2>&1; echo "smoke rc $?"; tail -1 gpurun_out/smoke.log
-timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; echo "bench rc $?"
+timeout 900 python -m pytest tests/test_gpu_bcd.py -q 2>&1 | grep -E "^E  |passed|failed" | head -6
+timeout 600 python tools/bcd_steps4.py 2>&1 | grep bcd
+NTT_BCD_GRAPH=0 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/bcd_small2.csv python tools/bcd_small_prof.py > /dev/null 2>&1; echo rc $?
