@@ -802,7 +802,15 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       Gs[e] = (float)sum;
     }
   }
-  constexpr bool WPAIR = !WREG;  // W in row-pair layout (one 128-bit load per 2 rows in phase A)
+#ifdef NTT_FC_PAIR_A
+  constexpr bool COLA = false;
+#else
+  // phase A with lane = column and all 8 ranks per lane: X by conflict-free LDS.32 (1 wavefront
+  // per row) and W by two warp-uniform LDS.128; the (4 columns x 2 ranks) lane layout read X
+  // by 128-bit loads that 4 lanes share, which cost 4 wavefronts per row (tools/ldsbench.cu)
+  constexpr bool COLA = !WREG;
+#endif
+  constexpr bool WPAIR = !WREG && !COLA;  // W in row-pair layout (one 128-bit load per 2 rows in phase A)
   for (int e = tid; e < MP * 8; e += NTHR) {
     const int i = e >> 3, k = e & 7;
     Wc[widx(i, k, WPAIR)] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
@@ -887,7 +895,30 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     if (do_update) {
       // ---- phase A: partial S over this warp's rows
       float2 sa = f2(0.f, 0.f), sb = f2(0.f, 0.f), sc = f2(0.f, 0.f), sd = f2(0.f, 0.f);
-      if constexpr (WREG) {
+      if constexpr (COLA) {
+        // sa..sd = S[k][lane] for k = (0,1), (2,3), (4,5), (6,7)
+        const unsigned char* xb = st + (size_t)(warp * RW) * 128 + (lane & 3) * 4;
+        const float* wb = Wc + warp * RW * 8;
+#pragma unroll 8
+        for (int v = 0; v < RW; ++v) {
+          const float x = *reinterpret_cast<const float*>(xb + v * 128 + (((lane >> 2) ^ (v & 7)) << 4));
+          const float4 wa = *reinterpret_cast<const float4*>(wb + v * 8);
+          const float4 wc = *reinterpret_cast<const float4*>(wb + v * 8 + 4);
+          sa = __ffma2_rn(f2(wa.x, wa.y), bc(x), sa);
+          sb = __ffma2_rn(f2(wa.z, wa.w), bc(x), sb);
+          sc = __ffma2_rn(f2(wc.x, wc.y), bc(x), sc);
+          sd = __ffma2_rn(f2(wc.z, wc.w), bc(x), sd);
+        }
+        float* sr = Sred + warp * 8 * 32 + lane;
+        sr[0] = sa.x;
+        sr[32] = sa.y;
+        sr[64] = sb.x;
+        sr[96] = sb.y;
+        sr[128] = sc.x;
+        sr[160] = sc.y;
+        sr[192] = sd.x;
+        sr[224] = sd.y;
+      } else if constexpr (WREG) {
 #pragma unroll
         for (int v = 0; v < RW; ++v) {
           const int i = warp * RW + v;
@@ -917,9 +948,11 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
           sd = __ffma2_rn(bc(w4.w), f2(xb.z, xb.w), sd);
         }
       }
-      float* sr = Sred + (warp * 8 + 2 * g) * 32 + 4 * q;
-      *reinterpret_cast<float4*>(sr) = make_float4(sa.x, sa.y, sb.x, sb.y);
-      *reinterpret_cast<float4*>(sr + 32) = make_float4(sc.x, sc.y, sd.x, sd.y);
+      if constexpr (!COLA) {
+        float* sr = Sred + (warp * 8 + 2 * g) * 32 + 4 * q;
+        *reinterpret_cast<float4*>(sr) = make_float4(sa.x, sa.y, sb.x, sb.y);
+        *reinterpret_cast<float4*>(sr + 32) = make_float4(sc.x, sc.y, sd.x, sd.y);
+      }
     }
     asm volatile("bar.sync 1, %0;" ::"r"(NBAR) : "memory");
     // ---- H update: thread handles (k, c) for k in {kt, kt+4}, c = ct
