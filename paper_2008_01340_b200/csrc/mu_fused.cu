@@ -805,9 +805,10 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 #ifdef NTT_FC_PAIR_A
   constexpr bool COLA = false;
 #else
-  // phase A with lane = column and all 8 ranks per lane: X by conflict-free LDS.32 (1 wavefront
-  // per row) and W by two warp-uniform LDS.128; the (4 columns x 2 ranks) lane layout read X
-  // by 128-bit loads that 4 lanes share, which cost 4 wavefronts per row (tools/ldsbench.cu)
+  // phase A with lanes = (2 columns, 4 ranks): X by LDS.64 (one 128-byte row per warp) and W
+  // by one half-warp-uniform LDS.128 per row; the (4 columns x 2 ranks) lane layout read X by
+  // 128-bit loads that 4 lanes share (4 wavefronts per row, tools/ldsbench.cu), and the
+  // (1 column x 8 ranks) layout spent 2 x 2 wavefronts per row on uniform LDS.128s of W
   constexpr bool COLA = !WREG;
 #endif
   constexpr bool WPAIR = !WREG && !COLA;  // W in row-pair layout (one 128-bit load per 2 rows in phase A)
@@ -896,28 +897,25 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       // ---- phase A: partial S over this warp's rows
       float2 sa = f2(0.f, 0.f), sb = f2(0.f, 0.f), sc = f2(0.f, 0.f), sd = f2(0.f, 0.f);
       if constexpr (COLA) {
-        // sa..sd = S[k][lane] for k = (0,1), (2,3), (4,5), (6,7)
-        const unsigned char* xb = st + (size_t)(warp * RW) * 128 + (lane & 3) * 4;
-        const float* wb = Wc + warp * RW * 8;
+        // lane = (cp = lane & 15: columns 2cp, 2cp+1; kh = lane >> 4: ranks 4kh..4kh+3);
+        // sa..sd = S[4kh + 0..3][2cp..2cp+1]
+        const int cp = lane & 15, kh = lane >> 4;
+        const unsigned char* xb = st + (size_t)(warp * RW) * 128 + (cp & 1) * 8;
+        const float* wb = Wc + warp * RW * 8 + 4 * kh;
 #pragma unroll 8
         for (int v = 0; v < RW; ++v) {
-          const float x = *reinterpret_cast<const float*>(xb + v * 128 + (((lane >> 2) ^ (v & 7)) << 4));
-          const float4 wa = *reinterpret_cast<const float4*>(wb + v * 8);
-          const float4 wc = *reinterpret_cast<const float4*>(wb + v * 8 + 4);
-          sa = __ffma2_rn(f2(wa.x, wa.y), bc(x), sa);
-          sb = __ffma2_rn(f2(wa.z, wa.w), bc(x), sb);
-          sc = __ffma2_rn(f2(wc.x, wc.y), bc(x), sc);
-          sd = __ffma2_rn(f2(wc.z, wc.w), bc(x), sd);
+          const float2 x = *reinterpret_cast<const float2*>(xb + v * 128 + (((cp >> 1) ^ (v & 7)) << 4));
+          const float4 w = *reinterpret_cast<const float4*>(wb + v * 8);
+          sa = __ffma2_rn(bc(w.x), x, sa);
+          sb = __ffma2_rn(bc(w.y), x, sb);
+          sc = __ffma2_rn(bc(w.z), x, sc);
+          sd = __ffma2_rn(bc(w.w), x, sd);
         }
-        float* sr = Sred + warp * 8 * 32 + lane;
-        sr[0] = sa.x;
-        sr[32] = sa.y;
-        sr[64] = sb.x;
-        sr[96] = sb.y;
-        sr[128] = sc.x;
-        sr[160] = sc.y;
-        sr[192] = sd.x;
-        sr[224] = sd.y;
+        float* sr = Sred + (warp * 8 + 4 * kh) * 32 + 2 * cp;
+        *reinterpret_cast<float2*>(sr) = sa;
+        *reinterpret_cast<float2*>(sr + 32) = sb;
+        *reinterpret_cast<float2*>(sr + 64) = sc;
+        *reinterpret_cast<float2*>(sr + 96) = sd;
       } else if constexpr (WREG) {
 #pragma unroll
         for (int v = 0; v < RW; ++v) {
