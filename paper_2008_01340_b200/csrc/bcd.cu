@@ -121,6 +121,7 @@ __global__ void k_bcd_hscale(double* __restrict__ sH, int r, const double* __res
   if (k < r && c[k] > 0.0) {
     sH[k] *= c[k];
     sH[32 + k] *= c[k];
+    sH[64 + k] *= c[k];
   }
 }
 
@@ -442,7 +443,17 @@ __global__ void __launch_bounds__(WS_T) k_bcd_wside(const float* __restrict__ Wm
   // in the one-pass path by swapping the roles of the two H buffers -- done here, in thread 0)
   const bool prev_acc = bs[BS_ACC] != 0.0;
   if (t < 32) {
-    sH[t] = 1.0;
+    if (bs[BS_FOLD] != 0.0) {
+      // no H commit: the pass reads H_m = diag(a) B[1 - role] - diag(b) B[role] (after the swap
+      // below).  Accepted: H_m = H + w_H (H - diag(s_p) H_prev) with H fresh in B[1 - role] and
+      // the old H_prev in B[role]; correction: H_m = diag(s_p) H_prev.
+      const double sp = sH[32 + t], wh = bs[BS_WH];
+      sH[t] = prev_acc ? 1.0 + wh : sp;
+      sH[64 + t] = prev_acc ? wh * sp : 0.0;
+    } else {
+      sH[t] = 1.0;
+      sH[64 + t] = 0.0;
+    }
     if (prev_acc) sH[32 + t] = 1.0;
   }
   __syncthreads();
@@ -502,6 +513,7 @@ __global__ void __launch_bounds__(WS_T) k_bcd_wside(const float* __restrict__ Wm
   if (t < r && cs[t] > 0.0) {
     sH[t] *= cs[t];
     sH[32 + t] *= cs[t];
+    sH[64 + t] *= cs[t];
   }
   __syncthreads();
   constexpr int NE = RP * RP;
@@ -775,7 +787,7 @@ __global__ void k_bcd_hout_role(float* __restrict__ B0, const float* __restrict_
 __global__ void k_bcd_hout(const float* __restrict__ Hp, int r, int64_t n, double* __restrict__ sH,
                            float* __restrict__ out, int init, const double* __restrict__ bs) {
   if (init) {
-    if (blockIdx.x == 0 && threadIdx.x < 64) sH[threadIdx.x] = 1.0;
+    if (blockIdx.x == 0 && threadIdx.x < 96) sH[threadIdx.x] = threadIdx.x < 64 ? 1.0 : 0.0;
     return;
   }
   // after an accepted last iteration H_prev was stored afresh (its scale restarts at 1)
@@ -810,8 +822,9 @@ __global__ void k_bcd_commit_pq(double* __restrict__ Pc, const double* __restric
   }
 }
 
-__global__ void k_bcd_init(double* __restrict__ bs, double delta) {
+__global__ void k_bcd_init(double* __restrict__ bs, double delta, double fold) {
   if (threadIdx.x != 0) return;
+  bs[BS_FOLD] = fold;
   bs[BS_OBJ] = 0.5 * bs[BS_XX];
   bs[BS_T] = 1.0;
   bs[BS_LWP] = bs[BS_LW];
@@ -1007,8 +1020,8 @@ cudaError_t launch_spec_norm(const double* M, int r, double* out, cudaStream_t s
   return cudaGetLastError();
 }
 
-cudaError_t launch_bcd_init(double* bs, double delta, cudaStream_t st) {
-  k_bcd_init<<<1, 32, 0, st>>>(bs, delta);
+cudaError_t launch_bcd_init(double* bs, double delta, bool fold, cudaStream_t st) {
+  k_bcd_init<<<1, 32, 0, st>>>(bs, delta, fold ? 1.0 : 0.0);
   return cudaGetLastError();
 }
 

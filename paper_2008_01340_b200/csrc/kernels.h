@@ -92,7 +92,8 @@ enum BcdState {
   BS_IT = 13,     // iteration counter (trace index)
   BS_DELTA = 14,
   BS_ROLE = 15,   // one-pass path: which of (H, H_prev's buffer) holds the candidate (0 / 1)
-  BS_COUNT = 16
+  BS_FOLD = 16,   // one-pass path: H_m is read as a H_prev - b H_prev2 inside the pass (no H commit)
+  BS_COUNT = 17
 };
 int bcd_w_ctas(int64_t m);
 cudaError_t launch_bcd_w(const float* Wm, int64_t m, int r, const double* P, const double* Q, const double* LW,
@@ -127,7 +128,7 @@ int bcd_dot_ctas(int64_t len, int num_sms);
 cudaError_t launch_bcd_psum_dot(const double* part, int nparts, int64_t len, const float* W, double* P,
                                 double* dotpart, int num_sms, cudaStream_t st);
 cudaError_t launch_spec_norm(const double* M, int r, double* out, cudaStream_t st);
-cudaError_t launch_bcd_init(double* bs, double delta, cudaStream_t st);
+cudaError_t launch_bcd_init(double* bs, double delta, bool fold, cudaStream_t st);
 cudaError_t launch_bcd_decide(double* bs, double* trace, const double* dotpart, int ndot, const double* G,
                               const double* Q, int r, unsigned* mxslots, cudaStream_t st);
 cudaError_t launch_bcd_commit(const float* V, float* Vm, float* Vp, int64_t cnt, const double* bs, int widx,

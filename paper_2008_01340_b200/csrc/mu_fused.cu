@@ -276,9 +276,10 @@ __device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int 
   __syncthreads();
 }
 
-template <int R, int UX, int NWT, bool HDIRECT, int BNT>
+template <int R, int UX, int NWT, bool HDIRECT, int BNT, bool FOLD>
 __global__ void __launch_bounds__((NWT + 1) * 32, 1)
-k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmH, int m, int64_t n, int r,
+k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmH,
+        const __grid_constant__ CUtensorMap tmH2, int m, int64_t n, int r,
         const float* __restrict__ W, const double* __restrict__ Gpart, int nG, float eps, float* __restrict__ H,
         double* __restrict__ Ppart, double* __restrict__ Qpart, int mode, int ns, int evict_first,
         PersistArgs pa) {
@@ -295,7 +296,9 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   // small and many are in flight (H is most of the traffic there).  Larger m:
   // H rides in the stage as four 32 x 8 TMA boxes.
   constexpr uint32_t HB = HDIRECT ? 0u : (uint32_t)NB * 8u * 128u;
-  constexpr uint32_t SB = XB + HB;
+  // FOLD (BCD one-pass, PersistArgs::bcdFold): a second set of H boxes per stage, B[role]
+  static_assert(!(FOLD && HDIRECT), "k_fused: the H_m fold needs staged H");
+  constexpr uint32_t SB = XB + HB * (FOLD ? 2u : 1u);
   unsigned char* stages = smem;
   float* Ws = reinterpret_cast<float*>(smem + (size_t)ns * SB);  // MP x 8
   float* Gs = Ws + MP * 8;                                         // 8 x 8
@@ -317,6 +320,12 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool persist = pa.iters > 0;
+  // FOLD: H_m = diag(a) B[1 - role] - diag(b) B[role] (B = tmH, tmH2 over Hout, Hout2); the
+  // second box set is loaded only when some b_k != 0 (after an accepted iteration)
+  const bool role1 = FOLD && *pa.bcdRole != 0.0;
+  bool ext = false;
+  if (FOLD)
+    for (int l = 0; l < r; ++l) ext |= pa.bcdS[64 + l] != 0.0;
 
   // ---- setup: W, G into smem; barriers
   for (int e = tid; e < MP * 8; e += (NWT + 1) * 32) {
@@ -378,7 +387,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
         const uint32_t ph = (par_mask >> s) & 1u;
         par_mask ^= 1u << s;
         tag[s] = ((uint32_t)pos << 1) | ph;
-        mbar_expect_tx(&full[s], XB + (HDIRECT ? 0u : HB));
+        mbar_expect_tx(&full[s], XB + (HDIRECT ? 0u : HB) + (FOLD && ext ? HB : 0u));
         const int col0 = (int)((b + j * gridDim.x) * BNT);
         unsigned char* st = stages + (size_t)s * SB;
         if (x3d) {
@@ -388,11 +397,19 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
           for (int bx = 0; bx < NB; ++bx) tma_load_2d(st + bx * MP * 128, &tmX, col0 + bx * 32, 0, &full[s], policy);
         }
         if (!HDIRECT) {
+          // FOLD: H_prev = B[1 - role] into the usual boxes, B[role] (H_prev2) after them
+          const CUtensorMap* mp = (FOLD && !role1) ? &tmH2 : &tmH;
+          const CUtensorMap* mq = role1 ? &tmH2 : &tmH;
           if (x3d) {
-            tma_load_3d(st + XB, &tmH, 0, 0, col0 >> 5, &full[s], policy);
+            tma_load_3d(st + XB, mp, 0, 0, col0 >> 5, &full[s], policy);
+            if (FOLD && ext) tma_load_3d(st + XB + HB, mq, 0, 0, col0 >> 5, &full[s], policy);
           } else {
 #pragma unroll
-            for (int bx = 0; bx < NB; ++bx) tma_load_2d(st + XB + bx * 1024, &tmH, col0 + bx * 32, 0, &full[s], policy);
+            for (int bx = 0; bx < NB; ++bx) tma_load_2d(st + XB + bx * 1024, mp, col0 + bx * 32, 0, &full[s], policy);
+            if (FOLD && ext)
+#pragma unroll
+              for (int bx = 0; bx < NB; ++bx)
+                tma_load_2d(st + XB + HB + bx * 1024, mq, col0 + bx * 32, 0, &full[s], policy);
           }
         }
         st_release_u32(issued, (uint32_t)(pos + 1));
@@ -454,10 +471,13 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   };
   // BCD mode (PersistArgs::bcdL): row scales of H_m, 1 / L_H, output buffer
   const bool bcd = pa.bcdL != nullptr;
-  float bsh[R];
+  float bsh[R], bq[R];
   float binvL = 0.f;
 #pragma unroll
-  for (int l = 0; l < R; ++l) bsh[l] = (bcd && l < r) ? (float)pa.bcdS[l] : 1.f;
+  for (int l = 0; l < R; ++l) {
+    bsh[l] = (bcd && l < r) ? (float)pa.bcdS[l] : 1.f;
+    bq[l] = (FOLD && l < r) ? (float)pa.bcdS[64 + l] : 0.f;
+  }
   if (bcd) {
     const double L = *pa.bcdL;
     binvL = L > 0.0 ? (float)(1.0 / L) : 0.f;
@@ -514,7 +534,24 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
         }
       }
     }
-    if (bcd) {  // H_m = diag(sH) H_m stored (bcd.cu's l.9 compensation)
+    if (FOLD && ext) {  // H_m = a H_prev - b H_prev2 (bcd.cu k_bcd_wside, BS_FOLD)
+      const unsigned char* qb = st + XB + HB + qbox * 1024;
+#pragma unroll
+      for (int l = 0; l < R; ++l) {
+        const unsigned char* qp = qb + l * 128 + ((qch ^ l) << 4) + qsub * 4;
+        float2 hq[CPL / 2];
+        if (CPL == 4) {
+          const float4 q4 = lds128(qp);
+          hq[0] = f2(q4.x, q4.y);
+          hq[CPL / 2 - 1] = f2(q4.z, q4.w);
+        } else {
+          hq[0] = *reinterpret_cast<const float2*>(qp);
+        }
+#pragma unroll
+        for (int p2 = 0; p2 < CPL / 2; ++p2)
+          hv[l][p2] = f2(fmaf(bsh[l], hv[l][p2].x, -bq[l] * hq[p2].x), fmaf(bsh[l], hv[l][p2].y, -bq[l] * hq[p2].y));
+      }
+    } else if (bcd) {  // H_m = diag(sH) H_m stored (bcd.cu's l.9 compensation)
 #pragma unroll
       for (int l = 0; l < R; ++l)
 #pragma unroll
@@ -1538,17 +1575,19 @@ int stages_for(int ux, int nwt, bool hd, int bnt) {
   return ns;
 }
 
-template <int R, int UX, int NWT, bool HD, int BNT>
+template <int R, int UX, int NWT, bool HD, int BNT, bool FOLD = false>
 cudaError_t launch_t(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_t n, int r, const float* W,
                      const double* Gpart, int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
-                     int evict_first, const PersistArgs& pa, cudaStream_t st) {
-  const int ns = stages_for(UX, NWT, HD, BNT);
-  const size_t SB = (size_t)(BNT / 32) * UX * 8 * 128 + (HD ? 0 : (size_t)(BNT / 32) * 1024);
+                     int evict_first, const PersistArgs& pa, cudaStream_t st, const CUtensorMap* mh2 = nullptr) {
+  const size_t HBs = HD ? 0 : (size_t)(BNT / 32) * 1024;
+  const size_t SB = (size_t)(BNT / 32) * UX * 8 * 128 + HBs * (FOLD ? 2 : 1);
+  int ns = FOLD ? (int)((SMEM_BUDGET - fixed_bytes(UX, NWT, HD)) / SB) : stages_for(UX, NWT, HD, BNT);
+  if (ns > 24) ns = 24;
   const size_t smem = (size_t)ns * SB + fixed_bytes(UX, NWT, HD);
-  cudaError_t e = cudaFuncSetAttribute(k_fused<R, UX, NWT, HD, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_fused<R, UX, NWT, HD, BNT, FOLD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_maybe_coop(k_fused<R, UX, NWT, HD, BNT>, grid, (NWT + 1) * 32, smem, st, pa.iters > 0, mx, mh, m, n, r,
-                           W, Gpart, nG, eps, H, Ppart, Qpart, mode, ns, evict_first, pa);
+  return launch_maybe_coop(k_fused<R, UX, NWT, HD, BNT, FOLD>, grid, (NWT + 1) * 32, smem, st, pa.iters > 0, mx, mh,
+                           mh2 ? *mh2 : mh, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, ns, evict_first, pa);
 }
 
 // ------------------------------------------------------------ W update v2 --
@@ -1702,6 +1741,51 @@ int fused_grid(int64_t m, int64_t n, int r, int num_sms) {
 size_t fused_scratch_bytes(int64_t, int64_t, int, int) { return 0; }
 void fused_destroy(FusedCtx&) {}
 
+struct FusedPlan {
+  bool x3d;  // X (and staged H) through 3-D maps: one box per 128-column tile
+  bool hd;   // lanes load H directly (no H boxes in the stage)
+  int bn;    // tile width (columns)
+};
+
+// the k_fused variant launch_fused picks for m <= 40 (environment knobs: DESIGN.md s.6)
+FusedPlan fused_plan(int64_t m, int64_t n, int r) {
+  static const bool x3d_on = [] {
+    const char* e = getenv("NTT_X3D");
+    const char* b = getenv("NTT_W_BN");  // the 3-D box spans 4 blocks: 128-column tiles only
+    return !(e && e[0] == '0') && !(b && b[0] == '6');
+  }();
+  static const int x3d_max_ux = [] {
+    const char* e = getenv("NTT_X3D_UX");
+    return e ? atoi(e) : 5;
+  }();
+  // experiment knobs: NTT_W_BN=64 (64-column tiles for UX >= 4), NTT_W_HDIRECT=0/1 (default: direct H loads
+  // when m <= 16 or r < 8, i.e. when H is a large share of the traffic)
+  static const int w_bn = [] {
+    const char* e = getenv("NTT_W_BN");
+    return (e && e[0] == '6') ? 64 : 128;
+  }();
+  static const int w_hd = [] {
+    const char* e = getenv("NTT_W_HDIRECT");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  const int ux = ux_for(m);
+  FusedPlan p;
+  p.x3d = ux <= x3d_max_ux && (n % 32) == 0 && x3d_on;
+  // with the 3-D maps staging H through TMA (one 4 KB box per tile) beats the lanes' direct
+  // loads, which cannot keep enough bytes in flight (tools/membench.cu): config 4 step 1
+  // 59.4 -> 53.7 ms, steps 2-5 -2 to -5 %
+  p.hd = (w_hd >= 0) ? (w_hd == 1) : (p.x3d ? false : (ux <= 2 || r < 8));
+  p.bn = (ux >= 4 && w_bn == 64) ? 64 : 128;
+  return p;
+}
+
+bool fused_fold_ok(int64_t m, int64_t n, int r, int64_t ldx, const void* X, const void* H0, const void* H1) {
+  if (m > 40 || !fused_supported(m, n, r, ldx, X, H0) || !fused_supported(m, n, r, ldx, X, H1)) return false;
+  if ((reinterpret_cast<uintptr_t>(H0) & 15) || (reinterpret_cast<uintptr_t>(H1) & 15) || (n & 3)) return false;
+  const FusedPlan p = fused_plan(m, n, r);
+  return !p.hd && p.bn == 128;
+}
+
 cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int r, const float* W, const double* Gpart,
                          int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
                          cudaStream_t st, const PersistArgs* pap) {
@@ -1731,19 +1815,11 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
     return launch_c<256, 4>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
   }
   const int ux = ux_for(m);
-  CUtensorMap mx, mh;
-  static const bool x3d_on = [] {
-    const char* e = getenv("NTT_X3D");
-    const char* b = getenv("NTT_W_BN");  // the 3-D box spans 4 blocks: 128-column tiles only
-    return !(e && e[0] == '0') && !(b && b[0] == '6');
-  }();
+  CUtensorMap mx, mh, mb0, mb1;
+  const FusedPlan fp = fused_plan(m, n, r);
   int ef = evict_first;
   cudaError_t e;
-  static const int x3d_max_ux = [] {
-    const char* e = getenv("NTT_X3D_UX");
-    return e ? atoi(e) : 5;
-  }();
-  if (ux <= x3d_max_ux && (n % 32) == 0 && x3d_on) {  // one 3-D box per 128-column tile
+  if (fp.x3d) {  // one 3-D box per 128-column tile
     e = make_map3(&mx, X, (uint64_t)n, (uint64_t)m, (uint64_t)ldx, (uint32_t)(ux * 8), 4u);
     ef |= 2;
   } else {
@@ -1751,24 +1827,45 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
   }
   if (e != cudaSuccess) return e;
   const int rc = rcls_for(r);
-  // experiment knobs: NTT_W_BN=64 (64-column tiles for UX >= 4), NTT_W_HDIRECT=0/1 (default: direct H loads
-  // when m <= 16 or r < 8, i.e. when H is a large share of the traffic)
-  static const int w_bn = [] {
-    const char* e = getenv("NTT_W_BN");
-    return (e && e[0] == '6') ? 64 : 128;
-  }();
-  static const int w_hd = [] {
-    const char* e = getenv("NTT_W_HDIRECT");
-    return e ? (e[0] == '1' ? 1 : 0) : -1;
-  }();
-  // with the 3-D maps staging H through TMA (one 4 KB box per tile) beats the lanes' direct
-  // loads, which cannot keep enough bytes in flight (tools/membench.cu): config 4 step 1
-  // 59.4 -> 53.7 ms, steps 2-5 -2 to -5 %
-  const bool hd = (w_hd >= 0) ? (w_hd == 1) : ((ef & 2) ? false : (ux <= 2 || r < 8));
+  const int w_bn = fp.bn;
+  const bool hd = fp.hd;
   // H boxes (staged path): 3-D as well when X uses the 3-D map (block stride 128 B of row pitch n)
-  e = (ef & 2) && !hd && (n % 32) == 0 ? make_map3(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u, 4u)
-                                       : make_map(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u);
+  auto hmap = [&](CUtensorMap* mp, const float* base) {
+    return (ef & 2) && !hd && (n % 32) == 0 ? make_map3(mp, base, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u, 4u)
+                                            : make_map(mp, base, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u);
+  };
+  e = hmap(&mh, H);
   if (e != cudaSuccess) return e;
+  if (pa.bcdFold) {  // BCD H_m fold: both H buffers (fused_fold_ok() said this variant runs)
+    if (hd || w_bn != 128 || !pa.Hout || !pa.Hout2 || !pa.bcdRole) return cudaErrorNotSupported;
+    if ((e = hmap(&mb0, pa.Hout)) != cudaSuccess) return e;
+    if ((e = hmap(&mb1, pa.Hout2)) != cudaSuccess) return e;
+#define LFF(RR, UU) \
+  return launch_t<RR, UU, 8, false, 128, true>(mx, mb0, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, ef, pa, st, &mb1)
+    if (rc == 2) {
+      if (ux == 1) LFF(2, 1);
+      if (ux == 2) LFF(2, 2);
+      if (ux == 4) LFF(2, 4);
+      LFF(2, 5);
+    }
+    if (rc == 6) {
+      if (ux == 1) LFF(6, 1);
+      if (ux == 2) LFF(6, 2);
+      if (ux == 4) LFF(6, 4);
+      LFF(6, 5);
+    }
+    if (rc == 4) {
+      if (ux == 1) LFF(4, 1);
+      if (ux == 2) LFF(4, 2);
+      if (ux == 4) LFF(4, 4);
+      LFF(4, 5);
+    }
+    if (ux == 1) LFF(8, 1);
+    if (ux == 2) LFF(8, 2);
+    if (ux == 4) LFF(8, 4);
+    LFF(8, 5);
+#undef LFF
+  }
 #define LF(RR, UU)                                                                                                              \
   return (UU >= 4 && w_bn == 64)                                                                                                  \
              ? (hd ? launch_t<RR, UU, 8, true, 64>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, ef, pa, st)  \

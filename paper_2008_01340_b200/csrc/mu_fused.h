@@ -42,11 +42,17 @@ struct PersistArgs {
   float* Hout = nullptr;
   float* Hout2 = nullptr;           // with bcdRole: Hn goes to (*bcdRole != 0 ? Hout2 : Hout)
   const double* bcdRole = nullptr;
+  // with bcdRole: H_m = diag(bcdS[0..r)) B[1 - role] - diag(bcdS[64..64+r)) B[role], B = (Hout,
+  // Hout2), formed inside the pass (k_fused with staged H only; see fused_fold_ok)
+  bool bcdFold = false;
 };
 
 // One pass over X (m x n, row stride ldx) with the current W (m x r) and
 // G = sum_c Gpart[c] (nG partials).  mode = kFusedAcc alone is the prologue
 // (Hn := H).  Ppart/Qpart: [grid][m*r] / [grid][r*r] fp64.
+// whether launch_fused runs the BCD H_m fold (PersistArgs::bcdFold) for this shape and buffers
+bool fused_fold_ok(int64_t m, int64_t n, int r, int64_t ldx, const void* X, const void* H0, const void* H1);
+
 cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int r, const float* W,
                          const double* Gpart, int nG, float eps, float* H, double* Ppart, double* Qpart, int mode,
                          int grid, cudaStream_t st, const PersistArgs* persist = nullptr);

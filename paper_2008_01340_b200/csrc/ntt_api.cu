@@ -1192,7 +1192,7 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   const size_t oPp = tc ? 0 : take(sizeof(double) * (size_t)std::max(xp.ncs, fparts) * m * r);
   const size_t oSp = (tc || nS == 1) ? 0 : take(sizeof(double) * (size_t)nS * n * r);
   const size_t oQp = take(sizeof(double) * (size_t)std::max(qp.ncs, fparts) * r * r);
-  const size_t oSH = take(sizeof(double) * 64);  // row scales of H_m, H_prev (k_bcd_hscale)
+  const size_t oSH = take(sizeof(double) * 96);  // row scales of H_m, H_prev, H_prev2 (k_bcd_hscale)
   const size_t oCp = take(sizeof(double) * (size_t)nwc * r), oGp = take(sizeof(double) * (size_t)nwc * r * r);
   const int ndot = bcd_dot_ctas(m * r, h->num_sms);
   const size_t oD = take(sizeof(double) * ndot), oSq = take(sizeof(double) * sumsq_ctas());
@@ -1278,10 +1278,13 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   LAUNCH(h, launch_sum_partials(Gpart, nwc, (int64_t)r * r, G, st));
   if ((s = spec(Qc, bs + BS_LW))) return s;
   if ((s = spec(G, bs + BS_LH))) return s;
-  LAUNCH(h, launch_bcd_init(bs, delta, st));
   // ---- one iteration (l.5-27), a fixed launch sequence
   // small W (non-TC): one-CTA stages for the W side and for everything after the H pass
   const bool cta = !tc && bcd_cta_ok(m, r) && !getenv("NTT_BCD_NO_CTA");
+  // one-pass path with k_fused's staged H: the pass forms H_m from the two H buffers itself
+  // (BS_FOLD), so the per-iteration H commit (3 H-sized streams) disappears
+  const bool fold = cta && f1 && fused_fold_ok(m, n, r, ldx, X, H, Hp) && !getenv("NTT_BCD_NO_FOLD");
+  LAUNCH(h, launch_bcd_init(bs, delta, fold, st));
   auto iteration_cta = [&]() -> ntt_status {
     LAUNCH(h, launch_bcd_wside(Wm, W, Wp, (int)m, r, Pc, Qc, bs, c, G, sH, st));  // l.5-10
     int nPp = nP, nQp = qp.ncs;
@@ -1297,6 +1300,7 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
       pa.Hout = H;  // the two H buffers swap roles on acceptance (k_bcd_commit_h_role)
       pa.Hout2 = Hp;
       pa.bcdRole = bs + BS_ROLE;
+      pa.bcdFold = fold;
       PLAUNCH(h, 0, xbytes + 8.0 * r * (double)n,
               launch_fused(X, ldx, m, n, r, W, G, 1, 0.0f, Hm, Ppart, Qpart, kFusedUpdate | kFusedAcc,
                            fused_grid(m, n, r, h->num_sms), st, &pa));
@@ -1320,8 +1324,11 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
       }
     }
     LAUNCH(h, launch_bcd_post(Ppart, nPp, Qpart, nQp, (int)m, r, W, Wm, Wp, Pc, Qc, c, G, bs, dtrace, st));
-    if (f1) LAUNCH(h, launch_bcd_commit_h_role(H, Hp, Hm, r, n, sH, bs, st));  // l.18-27 (H side)
-    else LAUNCH(h, launch_bcd_commit_h(H, Hm, Hp, r, n, sH, bs, st));
+    if (f1) {  // l.18-27 (H side); with the fold the next pass forms H_m itself
+      if (!fold) LAUNCH(h, launch_bcd_commit_h_role(H, Hp, Hm, r, n, sH, bs, st));
+    } else {
+      LAUNCH(h, launch_bcd_commit_h(H, Hm, Hp, r, n, sH, bs, st));
+    }
     return NTT_OK;
   };
   auto iteration = [&]() -> ntt_status {

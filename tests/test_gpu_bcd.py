@@ -52,7 +52,10 @@ def branches(tr, obj0):
 
 @pytest.mark.parametrize("m,n,r,iters,lr", [
     (40, 300, 4, 15, 0), (257, 1000, 8, 15, 0), (100, 2000, 16, 12, 6), (513, 777, 32, 10, 0),
-    (3000, 64, 5, 15, 3), (1, 50, 1, 8, 0), (7, 7, 7, 10, 0)])
+    (3000, 64, 5, 15, 3), (1, 50, 1, 8, 0), (7, 7, 7, 10, 0),
+    # m <= 40 and n % 32 == 0: the one-pass kernel forms H_m = a H_prev - b H_prev2 itself
+    # (BS_FOLD); 15 iterations keep several accepted extrapolations in the window
+    (32, 4096, 8, 15, 0), (6, 2048, 5, 15, 0), (24, 1024, 4, 12, 3)])
 def test_bcd_parity(h, ora, m, n, r, iters, lr):
     X, W0, H0 = case(m, n, r, m * 7 + n + r, lr)
     Wg, Hg, trg = run_gpu(h, X, W0, H0, iters)
