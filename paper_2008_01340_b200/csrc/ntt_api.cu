@@ -1284,6 +1284,7 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   // one-pass path with k_fused's staged H: the pass forms H_m from the two H buffers itself
   // (BS_FOLD), so the per-iteration H commit (3 H-sized streams) disappears
   const bool fold = cta && f1 && fused_fold_ok(m, n, r, ldx, X, H, Hp) && !getenv("NTT_BCD_NO_FOLD");
+  const bool presum = !getenv("NTT_BCD_NO_PRESUM");
   LAUNCH(h, launch_bcd_init(bs, delta, fold, st));
   auto iteration_cta = [&]() -> ntt_status {
     LAUNCH(h, launch_bcd_wside(Wm, W, Wp, (int)m, r, Pc, Qc, bs, c, G, sH, st));  // l.5-10
@@ -1323,7 +1324,18 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
         nPp = xp.ncs;
       }
     }
-    LAUNCH(h, launch_bcd_post(Ppart, nPp, Qpart, nQp, (int)m, r, W, Wm, Wp, Pc, Qc, c, G, bs, dtrace, st));
+    // many partials (k_fused_c writes 2 per SM; m = 256): reduce them across the GPU first -- the
+    // one-CTA post kernel summing 296 x 2048 doubles itself took 225 us of a 600 us iteration
+    const double* Pin = Ppart;
+    const double* Qin = Qpart;
+    if (presum && (double)nPp * (double)(m * r) > 131072.0) {
+      LAUNCH(h, launch_sum_partials(Ppart, nPp, m * r, Pn, st));
+      LAUNCH(h, launch_sum_partials(Qpart, nQp, (int64_t)r * r, Qn, st));
+      Pin = Pn;
+      Qin = Qn;
+      nPp = nQp = 1;
+    }
+    LAUNCH(h, launch_bcd_post(Pin, nPp, Qin, nQp, (int)m, r, W, Wm, Wp, Pc, Qc, c, G, bs, dtrace, st));
     if (f1) {  // l.18-27 (H side); with the fold the next pass forms H_m itself
       if (!fold) LAUNCH(h, launch_bcd_commit_h_role(H, Hp, Hm, r, n, sH, bs, st));
     } else {
