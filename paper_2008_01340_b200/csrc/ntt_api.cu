@@ -1157,12 +1157,18 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   // one-pass fused kernels in BCD mode where they win (r <= 8): always for m <= 40 (k_fused);
   // for 40 < m <= 256 (k_fused_c, non-persistent) measured on config 3's shapes against the
   // tensor-core 2-pass path: 256 x 2^20 57 vs 88 ms / 100 it, 256 x 2^10 5.7 vs 7.5, but
-  // 256 x 2^15 19 vs 9.5 (per-launch CTA imbalance at ~3.5 tiles per CTA) -- so large or small n
+  // 256 x 2^15 19 vs 9.5 -- most of the 19 ms was k_bcd_post summing 296 partials in one CTA
   static const int f1_max = [] {
     const char* e = getenv("NTT_BCD_1PASS_M");
     return e ? atoi(e) : 256;
   }();
-  const bool f1_n = m <= 40 || n >= (int64_t(1) << 18) || n <= 4096;
+  // (with the GPU-wide partial pre-sum before k_bcd_post the one-pass path also wins at 2^15:
+  // 6.3 vs 8.9 ms / 100 it; NTT_BCD_1PASS_MIDN=0 restores the tensor-core path for 4096 < n < 2^18)
+  static const bool f1_midn = [] {
+    const char* e = getenv("NTT_BCD_1PASS_MIDN");
+    return !(e && e[0] == '0');
+  }();
+  const bool f1_n = m <= 40 || n >= (int64_t(1) << 18) || n <= 4096 || f1_midn;
   const bool f1_shape = m <= f1_max && f1_n && fused_supported(m, n, r, ldx, X, H) && !use_wc() &&
                         !getenv("NTT_BCD_NO_1PASS") && !getenv("NTT_BCD_NO_FUSED");
   bool tc = !f1_shape && tc_supported(m, n, r, ldx, X) && !getenv("NTT_NO_TC");
