@@ -55,7 +55,10 @@ def branches(tr, obj0):
     (3000, 64, 5, 15, 3), (1, 50, 1, 8, 0), (7, 7, 7, 10, 0),
     # m <= 40 and n % 32 == 0: the one-pass kernel forms H_m = a H_prev - b H_prev2 itself
     # (BS_FOLD); 15 iterations keep several accepted extrapolations in the window
-    (32, 4096, 8, 15, 0), (6, 2048, 5, 15, 0), (24, 1024, 4, 12, 3)])
+    (32, 4096, 8, 15, 0), (6, 2048, 5, 15, 0), (24, 1024, 4, 12, 3),
+    # 40 < m <= 256: one-pass k_fused_c; at n = 2^15 its 2-per-SM partials are pre-summed across
+    # the GPU before the one-CTA post kernel
+    (256, 32768, 8, 10, 0), (64, 8192, 8, 10, 4)])
 def test_bcd_parity(h, ora, m, n, r, iters, lr):
     X, W0, H0 = case(m, n, r, m * 7 + n + r, lr)
     Wg, Hg, trg = run_gpu(h, X, W0, H0, iters)
