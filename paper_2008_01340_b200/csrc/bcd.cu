@@ -845,13 +845,34 @@ __global__ void k_scale_copy(const float* __restrict__ src, float* __restrict__ 
   }
 }
 
+// ||v||^2 of a rows x cols block (row stride ld), per-CTA fp64 partials.  Work items are
+// (row, 4096-column chunk) pairs over the whole grid -- one CTA per row left all but `rows` SMs
+// idle (16 ms for config 3's 32 x 2^25 X) -- with 128-bit streaming loads when aligned.
+constexpr int SQ_CH = 4096;
 __global__ void k_sumsq(const float* __restrict__ v, int64_t rows, int64_t cols, int64_t ld, double* __restrict__ part) {
   double s = 0.0;
-  for (int64_t i = blockIdx.x; i < rows; i += gridDim.x)
-    for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) {
-      const double x = v[i * ld + j];
+  const int64_t nch = (cols + SQ_CH - 1) / SQ_CH;
+  const bool vec = ((reinterpret_cast<uintptr_t>(v) & 15) == 0) && ((ld & 3) == 0);
+  for (int64_t c = blockIdx.x; c < rows * nch; c += gridDim.x) {
+    const int64_t i = c / nch, j0 = (c - i * nch) * SQ_CH;
+    const int64_t len = (cols - j0 < SQ_CH) ? cols - j0 : SQ_CH;
+    const float* p = v + i * ld + j0;
+    int64_t done = 0;
+    if (vec) {
+      const float4* p4 = reinterpret_cast<const float4*>(p);
+      const int64_t n4 = len >> 2;
+#pragma unroll 4
+      for (int64_t q = threadIdx.x; q < n4; q += blockDim.x) {
+        const float4 x = __ldcs(p4 + q);
+        s += (double)x.x * x.x + (double)x.y * x.y + (double)x.z * x.z + (double)x.w * x.w;
+      }
+      done = n4 << 2;
+    }
+    for (int64_t j = done + threadIdx.x; j < len; j += blockDim.x) {
+      const double x = p[j];
       s += x * x;
     }
+  }
   s = warp_sum(s);
   __shared__ double red[32];
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
