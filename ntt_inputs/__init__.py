@@ -144,3 +144,19 @@ def workloads() -> dict:
         "paper256": Workload("paper256", "ntt", [256] * 4, [10, 10, 10], 100, noise="uniform", noise_amp=0.625,
                              note="256^4 (16 GiB) TT ranks 10 + 1% uniform noise (0.01 * mean 62.5 * u)"),
     }
+
+
+def bcd_overshoot_matrix(m: int, n: int, r: int, seed: int, kind: str = "colscaled", extra: int = 1) -> np.ndarray:
+    """A non-negative m x n test matrix on which Alg. 3's extrapolation overshoots by itself
+    (the l.17 correction fires twice or more within 100 iterations for the seeds the tests
+    use): a rank-(r + extra) non-negative product -- so a rank-r fit keeps a residual well
+    above the fp32 resolution of the objective -- with row ("scaled") or column ("colscaled")
+    scales spread over three decades, rounded to fp32.  numpy's default_rng(seed); no method
+    arithmetic."""
+    rng = np.random.default_rng(seed)
+    base = rng.random((m, r + extra)) @ rng.random((r + extra, n))
+    if kind == "scaled":
+        X = (10.0 ** rng.uniform(-1.5, 1.5, (m, 1))) * base
+    else:
+        X = base * (10.0 ** rng.uniform(-1.5, 1.5, (1, n)))
+    return X.astype(np.float32)

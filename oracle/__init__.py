@@ -402,7 +402,7 @@ def _spec(M: np.ndarray) -> float:
 
 
 def nmf_bcd(X: np.ndarray, W0: np.ndarray, H0: np.ndarray, iters: int, delta: float = 0.9999,
-            trace: bool = False):
+            trace: bool = False, log: Optional[list] = None, force_correct=()):
     """Alg. 3 (distBCDnmf) on one process, fp64, with readings
     R22-R27 (DESIGN.md s.3):
       init  W_m = W0 sqrt(||X||_F)/||W0||_F, H_m = H0 sqrt(||X||_F)/||H0||_F; W = W_m, H = H_m;
@@ -419,7 +419,12 @@ def nmf_bcd(X: np.ndarray, W0: np.ndarray, H0: np.ndarray, iters: int, delta: fl
                 w_W = min(w, delta sqrt(L_W_prev / L_W)), w_H = min(w, delta sqrt(L_H_prev / L_H)),
                 W_m = W + w_W (W - W_prev), H_m = H + w_H (H - H_prev),
                 W_prev, H_prev = W, H; L_*_prev = L_*; t = t+; obj = obj_new  (l.21-27)
-    Returns (W, H) = the last accepted iterates, or (W, H, accepted-objective trace)."""
+    Returns (W, H) = the last accepted iterates, or (W, H, accepted-objective trace).
+    Test instrumentation (tests/test_oracle_bcd.py pins these against the hand-worked
+    tests/golden/bcd_worked.json): ``log`` (a list) receives one dict per iteration with the
+    scalars of the iteration (L_W, L_H, c, obj_new, the branch, t before / after, w, w_W, w_H);
+    ``force_correct`` holds 0-based iteration indices whose l.17 test is treated as true
+    (a constructed overshoot for the correction branch, l.17-20)."""
     X = np.asarray(X, dtype=np.float64)
     m, n = X.shape
     W0 = np.asarray(W0, dtype=np.float64)
@@ -428,6 +433,8 @@ def nmf_bcd(X: np.ndarray, W0: np.ndarray, H0: np.ndarray, iters: int, delta: fl
     nx = np.linalg.norm(X)
     if nx == 0.0:
         raise ValueError("||X|| = 0 (DegenerateInputError, S:330)")
+    if np.linalg.norm(W0) == 0.0 or np.linalg.norm(H0) == 0.0:
+        raise ValueError("||W0|| = 0 or ||H0|| = 0: l.2 cannot normalise (DegenerateInputError, S:330)")
     Wm = W0 * (np.sqrt(nx) / np.linalg.norm(W0))
     Hm = H0 * (np.sqrt(nx) / np.linalg.norm(H0))
     Wp, Hp = Wm.copy(), Hm.copy()
@@ -451,9 +458,11 @@ def nmf_bcd(X: np.ndarray, W0: np.ndarray, H0: np.ndarray, iters: int, delta: fl
         LH = _spec(G)
         H = np.maximum(0.0, Hm - (G @ Hm - W.T @ X) / LH) if LH > 0 else Hm.copy()
         obj_new = 0.5 * float(np.sum((X - W @ H) ** 2))
-        if obj_new >= obj:          # correction
+        ent = dict(it=len(tr), LW=LW, LH=LH, c=c.tolist(), obj_new=obj_new, t=t)
+        if obj_new >= obj or len(tr) in force_correct:      # correction
             Wm, Hm, t = Wp.copy(), Hp.copy(), 1.0
             Q, P = Hp @ Hp.T, X @ Hp.T
+            ent.update(accepted=False)
         else:                       # extrapolation
             tp = (1.0 + np.sqrt(1.0 + 4.0 * t * t)) / 2.0
             w = (t - 1.0) / tp
@@ -465,6 +474,10 @@ def nmf_bcd(X: np.ndarray, W0: np.ndarray, H0: np.ndarray, iters: int, delta: fl
             LWp, LHp = LW, LH
             t, obj = tp, obj_new
             Q, P = H @ H.T, X @ H.T
+            ent.update(accepted=True, w=w, wW=wW, wH=wH)
+        if log is not None:
+            ent.update(t_next=t, W=Wp.copy(), H=Hp.copy(), Wm=Wm.copy(), Hm=Hm.copy())
+            log.append(ent)
         tr.append(obj)
     return (Wp, Hp, np.array(tr)) if trace else (Wp, Hp)
 
