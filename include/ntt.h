@@ -47,7 +47,7 @@ typedef enum {
     NTT_ERR_DIMENSION = 2,    /* d < 2, a dim < 1, size overflow        */
     NTT_ERR_RANK = 3,         /* rank outside 1..min(rows, cols), > 64  */
     NTT_ERR_DEGENERATE = 4,   /* ||A||_F = 0 in an error evaluation     */
-    NTT_ERR_NONNEG = 5,       /* reserved: negative input detected             */
+    NTT_ERR_NONNEG = 5,       /* negative / NaN input (NTT_VALIDATE_NONNEG)     */
     NTT_ERR_WORKSPACE = 6,    /* caller workspace too small                    */
     NTT_ERR_CUDA = 7,         /* CUDA runtime / launch failure                 */
     NTT_ERR_NCCL = 8,         /* NCCL failure (distributed handles)            */
@@ -67,6 +67,18 @@ ntt_status ntt_set_stream(ntt_handle h, void* cuda_stream);
 const char* ntt_status_string(ntt_status s);
 const char* ntt_last_error(ntt_handle h);
 int ntt_abi_version(void);
+/* Input validation (SURVEY s.8(b); SPEC's NonnegativityError).  With
+ * NTT_VALIDATE_NONNEG set, ntt_nmf_mu, ntt_nmf_bcd, ntt_decompose,
+ * ntt_decompose_eps and ntt_decompose_bcd first count the entries of X / A
+ * that are not >= 0 (negative values or NaN) in one extra read of the input and
+ * return NTT_ERR_NONNEG (nothing else launched) if there are any; the call
+ * synchronises the stream for the count.  Off by default (NMF's problem
+ * statement, Alg. 3 "Require X in R_+", makes it the caller's contract).
+ * ntt_tt_svd never checks (the TT-SVD baseline takes any sign).  Unknown flag
+ * bits give NTT_ERR_INVALID_ARG.                                             */
+#define NTT_VALIDATE_NONNEG 1
+ntt_status ntt_set_validation(ntt_handle h, int flags);
+
 /* Number of kernel launches this handle has issued since creation (for the
  * bench's gpu_launches count; graph-replayed kernels are counted per replay). */
 int64_t ntt_launch_count(ntt_handle h);
@@ -247,6 +259,31 @@ ntt_status ntt_profile_get_step(ntt_handle h, int cls, int step, int64_t* launch
  * the prologue), and for pass 1 of every CTA c < 1024 its start at [17408 + c]
  * and end at [16384 + c].  NULL otherwise.  Synchronises the handle's stream. */
 const unsigned long long* ntt_debug_persist_trace(ntt_handle h);
+
+/* Number of NCCL calls this handle has enqueued (collectives and group
+ * brackets; a captured graph's calls are counted once, at capture).  Proves in
+ * tests that a distributed branch ran.  -1 for a null handle.               */
+int64_t ntt_collective_count(ntt_handle h);
+
+/* Kernel-level diagnostics of the TT-mode partition (DESIGN.md s.7), so the
+ * layouts of p > 1 ranks can be checked on one GPU:
+ *  - ntt_debug_fill_uniform_cols: the local r x nloc H init of a rank that owns
+ *    last-mode slices [off, off + b) of nd: local column c is global column
+ *    (c / b) * nd + off + c % b, H[k][c] = u(seed, stream, k * nglob + that);
+ *  - ntt_debug_gather_last_core: core[k][i] (r x nd) from the rank-major staging
+ *    gath = [rank g: r x b_g block], b_g = floor((g+1) nd / p) - floor(g nd / p).
+ * Device pointers; enqueued on the handle's stream.                          */
+ntt_status ntt_debug_fill_uniform_cols(ntt_handle h, float* H, int32_t r, int64_t nloc, int64_t b, int64_t nd,
+                                       int64_t off, int64_t nglob, uint64_t seed, uint64_t stream);
+ntt_status ntt_debug_gather_last_core(ntt_handle h, const float* gath, int64_t r, int64_t nd, int32_t nranks,
+                                      float* core);
+
+/* Test hook for Alg. 3's correction branch (l.17-20): in every
+ * later ntt_nmf_bcd / ntt_decompose_bcd NMF on this handle, iteration i (0-based,
+ * i < 52) with bit i of `mask` set takes the correction branch whatever its
+ * objective (a constructed overshoot; the oracle's `force_correct`).  0 (the
+ * default) turns it off.  NTT_ERR_INVALID_ARG for a null handle.              */
+ntt_status ntt_debug_bcd_force_correct(ntt_handle h, uint64_t mask);
 
 /* ----------------------------------------------------- multi-GPU (NCCL) ----
  * One process per GPU.  Rank 0 calls ntt_get_unique_id and broadcasts the 128

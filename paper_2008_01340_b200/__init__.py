@@ -161,6 +161,28 @@ class Handle:
         self._check(lib().ntt_nmf_mu(self._h, _ptr(X), m, n, ldx, r, iters, eps, _ptr(W), _ptr(H), tr))
         return list(tr)[:iters] if trace else None
 
+    @property
+    def collective_count(self) -> int:
+        return int(lib().ntt_collective_count(self._h))
+
+    def ntt_debug_fill_uniform_cols(self, H, r: int, nloc: int, b: int, nd: int, off: int, nglob: int,
+                                    seed: int, stream: int):
+        self._check(lib().ntt_debug_fill_uniform_cols(self._h, _ptr(H), r, nloc, b, nd, off, nglob, seed, stream))
+
+    def ntt_debug_gather_last_core(self, gath, r: int, nd: int, nranks: int, core):
+        self._check(lib().ntt_debug_gather_last_core(self._h, _ptr(gath), r, nd, nranks, _ptr(core)))
+
+    def ntt_set_validation(self, nonneg: bool = True):
+        """NTT_VALIDATE_NONNEG: check X / A for negative or NaN entries before each call."""
+        self._check(lib().ntt_set_validation(self._h, 1 if nonneg else 0))
+
+    def ntt_debug_bcd_force_correct(self, iterations=()):
+        """Test hook: the BCD iterations listed (0-based, < 52) take the correction branch."""
+        mask = 0
+        for i in iterations:
+            mask |= 1 << int(i)
+        self._check(lib().ntt_debug_bcd_force_correct(self._h, mask))
+
     def ntt_nmf_bcd(self, X, m: int, n: int, ldx: int, r: int, iters: int, W, H, delta: float = 0.9999,
                     trace: bool = False):
         """Alg. 3 BCD NMF on device buffers (W, H in/out); returns the accepted-objective trace if asked."""

@@ -93,7 +93,8 @@ enum BcdState {
   BS_DELTA = 14,
   BS_ROLE = 15,   // one-pass path: which of (H, H_prev's buffer) holds the candidate (0 / 1)
   BS_FOLD = 16,   // one-pass path: H_m is read as a H_prev - b H_prev2 inside the pass (no H commit)
-  BS_COUNT = 17
+  BS_FORCE = 17,  // test hook: bit i set = the l.17 test of iteration i is treated as true
+  BS_COUNT = 18
 };
 int bcd_w_ctas(int64_t m);
 cudaError_t launch_bcd_w(const float* Wm, int64_t m, int r, const double* P, const double* Q, const double* LW,
@@ -128,7 +129,7 @@ int bcd_dot_ctas(int64_t len, int num_sms);
 cudaError_t launch_bcd_psum_dot(const double* part, int nparts, int64_t len, const float* W, double* P,
                                 double* dotpart, int num_sms, cudaStream_t st);
 cudaError_t launch_spec_norm(const double* M, int r, double* out, cudaStream_t st);
-cudaError_t launch_bcd_init(double* bs, double delta, bool fold, cudaStream_t st);
+cudaError_t launch_bcd_init(double* bs, double delta, bool fold, uint64_t force, cudaStream_t st);
 cudaError_t launch_bcd_decide(double* bs, double* trace, const double* dotpart, int ndot, const double* G,
                               const double* Q, int r, unsigned* mxslots, cudaStream_t st);
 cudaError_t launch_bcd_commit(const float* V, float* Vm, float* Vp, int64_t cnt, const double* bs, int widx,
@@ -138,7 +139,8 @@ cudaError_t launch_bcd_commit_pq(double* Pc, const double* Pn, int64_t m, int r,
 cudaError_t launch_scale_copy(const float* src, float* a, float* b, int64_t cnt, const double* num, const double* den,
                               cudaStream_t st);
 int sumsq_ctas();
-cudaError_t launch_sumsq(const float* v, int64_t rows, int64_t cols, int64_t ld, double* part, cudaStream_t st);
+cudaError_t launch_sumsq(const float* v, int64_t rows, int64_t cols, int64_t ld, double* part, cudaStream_t st,
+                         bool evict_first = false);
 
 // 1/2 ||X - W H||^2 partial sums (fp64), one per CTA; returns number of partials.
 int objective_ctas(int64_t n);
@@ -164,6 +166,9 @@ namespace ntt {
 // out[t] = sum_b part[b*len + t]   (fixed order b = 0..n-1)
 cudaError_t launch_sum_partials(const double* part, int nparts, int64_t len, double* out, cudaStream_t st);
 // H init for a last-mode column block (DESIGN.md s.7): H[k][c] = u(key, k*nglob + (c/b)*nd + off + c%b)
+// validation pass: number of entries that are not >= 0 (negatives, NaN) into *bad (device)
+cudaError_t launch_count_not_nonneg(const float* v, int64_t rows, int64_t cols, int64_t ld, unsigned long long* bad,
+                                    int num_sms, cudaStream_t st);
 cudaError_t launch_fill_uniform_cols(float* H, int r, int64_t nloc, int64_t b, int64_t nd, int64_t off, int64_t nglob,
                                      uint64_t seed, uint64_t stream, cudaStream_t st);
 // gathered rank-major blocks [g][r][b_g] -> core [r][nd]

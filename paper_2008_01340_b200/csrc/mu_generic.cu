@@ -447,3 +447,31 @@ cudaError_t launch_gather_last_core(const float* gath, int64_t r, int64_t nd, in
 }
 
 }  // namespace ntt
+
+namespace ntt {
+namespace {
+// validation (ntt_set_validation): count the entries of a rows x cols matrix (row stride ld)
+// that are not >= 0 -- negative values and NaNs (SPEC's NonnegativityError)
+__global__ void k_count_not_nonneg(const float* __restrict__ v, int64_t rows, int64_t cols, int64_t ld,
+                                   unsigned long long* __restrict__ bad) {
+  unsigned long long c = 0;
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / cols, j = e - i * cols;
+    c += !(__ldg(v + i * ld + j) >= 0.0f);
+  }
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(bad, c);
+}
+}  // namespace
+
+cudaError_t launch_count_not_nonneg(const float* v, int64_t rows, int64_t cols, int64_t ld, unsigned long long* bad,
+                                    int num_sms, cudaStream_t st) {
+  cudaMemsetAsync(bad, 0, sizeof(unsigned long long), st);
+  const int64_t total = rows * cols;
+  int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms * 8);
+  if (blocks < 1) blocks = 1;
+  k_count_not_nonneg<<<(unsigned)blocks, 256, 0, st>>>(v, rows, cols, ld, bad);
+  return cudaGetLastError();
+}
+}  // namespace ntt

@@ -74,6 +74,7 @@ struct ntt_handle_s {
   unsigned long long* ptrace = nullptr;  // persistent-kernel phase stamps (NTT_PERSIST_TRACE)
   std::string err;
   int64_t launches = 0;
+  int64_t collectives = 0;  // NCCL calls enqueued (ntt_collective_count)
   // internal scratch (grown, never shrunk)
   void* ws = nullptr;
   size_t ws_bytes = 0;
@@ -111,6 +112,11 @@ struct ntt_handle_s {
   };
   Acc acc[8][66];
   // CUDA graph of the last ntt_decompose (replayed when the arguments repeat)
+  // ntt_set_validation: NTT_VALIDATE_NONNEG checks X / A before the run (one extra read)
+  int validate = 0;
+  unsigned long long* vbad = nullptr;  // device counter of the check
+  // test hook (ntt_debug_bcd_force_correct): BCD iterations whose l.17 test is forced true
+  uint64_t bcd_force = 0;
   bool capturing = false;
   cudaStream_t gstream = nullptr;
   cudaEvent_t gev_in = nullptr, gev_out = nullptr;
@@ -139,6 +145,23 @@ ntt_status fail(ntt_handle h, ntt_status s, const char* fmt, ...) {
   return s;
 }
 
+// NTT_VALIDATE_NONNEG (ntt_set_validation): one counting pass over the rows x cols input
+// (row stride ld); NTT_ERR_NONNEG when any entry is negative or NaN.  Synchronises.
+ntt_status check_nonneg(ntt_handle h, const float* v, int64_t rows, int64_t cols, int64_t ld, const char* what) {
+  if (!(h->validate & 1)) return NTT_OK;
+  if (!h->vbad) {
+    cudaError_t e = cudaMalloc(&h->vbad, sizeof(unsigned long long));
+    if (e != cudaSuccess) return fail(h, NTT_ERR_CUDA, "validation buffer: %s", cudaGetErrorString(e));
+  }
+  cudaError_t e = launch_count_not_nonneg(v, rows, cols, ld, h->vbad, h->num_sms, h->stream);
+  unsigned long long bad = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, h->vbad, sizeof(bad), cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return fail(h, NTT_ERR_CUDA, "validation pass: %s", cudaGetErrorString(e));
+  if (bad) return fail(h, NTT_ERR_NONNEG, "%s has %llu negative or NaN entries", what, bad);
+  return NTT_OK;
+}
+
 #define CU(h, call)                                                                          \
   do {                                                                                       \
     cudaError_t e_ = (call);                                                                 \
@@ -162,6 +185,7 @@ ntt_status fail(ntt_handle h, ntt_status s, const char* fmt, ...) {
     ncclResult_t r_ = (call);                                                                   \
     if (r_ != ncclSuccess)                                                                      \
       return fail((h), NTT_ERR_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call, g_nccl.GetErrorString(r_)); \
+    (h)->collectives++;                                                                         \
   } while (0)
 
 bool is_device_ptr(const void* p) {
@@ -286,7 +310,9 @@ struct MuPlan {
   size_t off_P, off_Q, off_G, off_S, off_tc, off_pp, off_red, off_ctr, bytes;
 };
 
-MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, int nranks) {
+// dist: a handle from ntt_create_dist* (any number of ranks, 1 included) -- its MU runs
+// the distributed branches (all-reduce of the pass partials between passes)
+MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, bool dist) {
   MuPlan p;
   p.m = m;
   p.n = n;
@@ -329,8 +355,8 @@ MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, int nranks) {
     p.tp = plan_tc(m, n, r, num_sms);
     o = align_up(o + p.tp.bytes);
   }
-  p.persist = nranks == 1 && p.fused && !use_wc() && !getenv("NTT_NO_PERSIST");
-  p.tiny = nranks == 1 && tiny_supported(m, n, r) && !getenv("NTT_NO_TINY");
+  p.persist = !dist && p.fused && !use_wc() && !getenv("NTT_NO_PERSIST");
+  p.tiny = !dist && tiny_supported(m, n, r) && !getenv("NTT_NO_TINY");
   p.off_pp = o;
   if (p.persist) o = align_up(o + sizeof(double) * (size_t)p.fgrid * (size_t)(m * r + r * r));
   p.off_red = o;
@@ -338,7 +364,6 @@ MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, int nranks) {
   p.off_ctr = o;
   if (p.persist) o = align_up(o + 64);
   p.bytes = o;
-  (void)nranks;
   return p;
 }
 
@@ -358,7 +383,7 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
   double* Qpart = reinterpret_cast<double*>(scratch + p.off_Q);
   double* Gpart = reinterpret_cast<double*>(scratch + p.off_G);
   double* red = reinterpret_cast<double*>(scratch + p.off_S);
-  const bool dist = h->nranks > 1;
+  const bool dist = h->comm != nullptr;  // every ntt_create_dist* handle, 1 rank included
   cudaStream_t st = h->stream;
   int nobj = objective_ctas(n);
   if (iters <= 0) return NTT_OK;
@@ -786,6 +811,7 @@ ntt_status ntt_destroy(ntt_handle h) {
   fused_destroy(h->fused);
   if (h->ws) cudaFree(h->ws);
   if (h->ptrace) cudaFree(h->ptrace);
+  if (h->vbad) cudaFree(h->vbad);
   if (h->stage) cudaFree(h->stage);
   if (h->sweep) cudaFree(h->sweep);
   if (h->host_part) cudaFreeHost(h->host_part);
@@ -827,7 +853,7 @@ ntt_status ntt_nmf_mu(ntt_handle h, const float* X, int64_t m, int64_t n, int64_
   ntt_status s = check_mu_args(h, X, m, n, ldx, r, iters, eps, W, H);
   if (s) return s;
   CU(h, cudaSetDevice(h->device));
-  MuPlan p = plan_mu(m, n, r, h->num_sms, h->nranks);
+  MuPlan p = plan_mu(m, n, r, h->num_sms, h->comm != nullptr);
   const bool xd = is_device_ptr(X), wd = is_device_ptr(W), hd = is_device_ptr(H);
   // staging layout for host buffers: [X | W | H]
   size_t sx = xd ? 0 : align_up(sizeof(float) * (size_t)(m * ldx));
@@ -855,6 +881,7 @@ ntt_status ntt_nmf_mu(ntt_handle h, const float* X, int64_t m, int64_t n, int64_
     dH = reinterpret_cast<float*>(stg + sx + sw);
     CU(h, cudaMemcpyAsync(dH, H, sizeof(float) * (size_t)(r * n), cudaMemcpyHostToDevice, h->stream));
   }
+  if ((s = check_nonneg(h, dX, m, n, ldx, "X"))) return s;
   char* scratch = reinterpret_cast<char*>(h->ws);
   double* dtrace = objective_trace ? reinterpret_cast<double*>(scratch + p.bytes) : nullptr;
   if ((s = run_mu(h, p, dX, ldx, iters, eps, dW, dH, scratch, dtrace))) return s;
@@ -891,7 +918,7 @@ struct DecompPlan {
   ContractPlan cp;
 };
 
-void plan_decompose(const TTShape& s, int num_sms, int nranks, int rank, DecompPlan* P) {
+void plan_decompose(const TTShape& s, int num_sms, int nranks, int rank, bool dist, DecompPlan* P) {
   P->s = s;
   int64_t off = 0;
   P->nloc_last = ntt_dist_block(s.dims[s.d - 1], nranks, rank, &off);
@@ -908,7 +935,7 @@ void plan_decompose(const TTShape& s, int num_sms, int nranks, int rank, DecompP
     int64_t hsz = s.r[l] * rest;
     P->hbuf[(l - 1) & 1] = std::max(P->hbuf[(l - 1) & 1], hsz);
     P->wmax = std::max(P->wmax, P->m[l] * s.r[l]);
-    P->mu[l] = plan_mu(P->m[l], P->ncol[l], (int)s.r[l], num_sms, nranks);
+    P->mu[l] = plan_mu(P->m[l], P->ncol[l], (int)s.r[l], num_sms, dist);
     P->mu_bytes = std::max(P->mu_bytes, P->mu[l].bytes);
   }
   size_t o = 0;
@@ -952,7 +979,7 @@ ntt_status decompose_device(ntt_handle h, const DecompPlan& P, const TTShape& s,
     Hl = hb[(l - 1) & 1];
     h->cur_step = l;
     LAUNCH(h, launch_fill_uniform(Wd, m * r, seed, stream_w(l), 0, cs));
-    if (h->nranks == 1) {
+    if (!h->comm) {
       LAUNCH(h, launch_fill_uniform(Hl, (int64_t)r * n, seed, stream_h(l), 0, cs));
     } else {
       // global column index of local column c: (c / b) * n_d + off + c % b  (DESIGN.md s.7)
@@ -967,7 +994,7 @@ ntt_status decompose_device(ntt_handle h, const DecompPlan& P, const TTShape& s,
   h->cur_step = d;  // last-core gather and the error pass
   // last core G_d[k][i][0] = T_{d-1}[k][i]  (Alg. 2 l.11)
   const int64_t rl = s.r[d - 1], nd = s.dims[d - 1];
-  if (h->nranks == 1) {
+  if (!h->comm) {
     CU(h, cudaMemcpyAsync(dcores + s.off[d], Hl, sizeof(float) * (size_t)(rl * nd), cudaMemcpyDeviceToDevice, cs));
   } else {
     // all_gather of the ragged column blocks: one broadcast per rank into a
@@ -991,7 +1018,7 @@ ntt_status decompose_device(ntt_handle h, const DecompPlan& P, const TTShape& s,
     CU(h, cudaMemcpyAsync(lc, dcores, sizeof(float) * (size_t)s.off[d], cudaMemcpyDeviceToDevice, cs));
     CU(h, cudaMemcpyAsync(lc + s.off[d], Hl, sizeof(float) * (size_t)(rl * P.nloc_last), cudaMemcpyDeviceToDevice, cs));
     if ((st = contract_run(h, P.sl, P.cp, lc, nullptr, 0.0f, 0, dA, es))) return st;
-    if ((st = finish_error_device(h, P.cp, es, h->nranks > 1))) return st;
+    if ((st = finish_error_device(h, P.cp, es, h->comm != nullptr))) return st;
   }
   h->cur_step = 0;
   return NTT_OK;
@@ -1006,7 +1033,7 @@ size_t ntt_decompose_workspace_bytes(int32_t d, const int64_t* dims, const int32
   int dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaGetLastError();
-  plan_decompose(s, sms, 1, 0, P);
+  plan_decompose(s, sms, 1, 0, false, P);
   size_t b = P->bytes;
   delete P;
   return b;
@@ -1032,7 +1059,7 @@ ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t*
   DecompPlan* Pp = new DecompPlan();
   std::unique_ptr<DecompPlan> guard(Pp);
   DecompPlan& P = *Pp;
-  plan_decompose(s, h->num_sms, h->nranks, h->rank, &P);
+  plan_decompose(s, h->num_sms, h->nranks, h->rank, h->comm != nullptr, &P);
   char* ws;
   if (workspace) {
     if (workspace_bytes < P.bytes)
@@ -1050,6 +1077,7 @@ ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t*
     dA = reinterpret_cast<const float*>(h->stage);
     CU(h, cudaMemcpyAsync((void*)dA, A, sizeof(float) * (size_t)Nloc, cudaMemcpyHostToDevice, h->stream));
   }
+  if ((st = check_nonneg(h, dA, 1, Nloc, Nloc, "A"))) return st;
   const bool cores_dev = is_device_ptr(cores);
   float* dcores = cores_dev ? cores : reinterpret_cast<float*>(ws + P.off_cores);
   if (rel_err && (st = ensure_host_part(h, 2))) return st;
@@ -1163,13 +1191,8 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
     return e ? atoi(e) : 256;
   }();
   // (with the GPU-wide partial pre-sum before k_bcd_post the one-pass path also wins at 2^15:
-  // 6.3 vs 8.9 ms / 100 it; NTT_BCD_1PASS_MIDN=0 restores the tensor-core path for 4096 < n < 2^18)
-  static const bool f1_midn = [] {
-    const char* e = getenv("NTT_BCD_1PASS_MIDN");
-    return !(e && e[0] == '0');
-  }();
-  const bool f1_n = m <= 40 || n >= (int64_t(1) << 18) || n <= 4096 || f1_midn;
-  const bool f1_shape = m <= f1_max && f1_n && fused_supported(m, n, r, ldx, X, H) && !use_wc() &&
+  // 6.3 vs 8.9 ms / 100 it, so it is taken for every n)
+  const bool f1_shape = m <= f1_max && fused_supported(m, n, r, ldx, X, H) && !use_wc() &&
                         !getenv("NTT_BCD_NO_1PASS") && !getenv("NTT_BCD_NO_FUSED");
   bool tc = !f1_shape && tc_supported(m, n, r, ldx, X) && !getenv("NTT_NO_TC");
   TcPlan tp;
@@ -1202,8 +1225,11 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   const size_t oCp = take(sizeof(double) * (size_t)nwc * r), oGp = take(sizeof(double) * (size_t)nwc * r * r);
   const int ndot = bcd_dot_ctas(m * r, h->num_sms);
   const size_t oD = take(sizeof(double) * ndot), oSq = take(sizeof(double) * sumsq_ctas());
-  const size_t oBs = take(sizeof(double) * BS_COUNT), oTr = take(sizeof(double) * std::max(iters, 1));
+  const size_t oBs = take(sizeof(double) * BS_COUNT);
   const size_t oTc = tc ? take(tp.bytes) : 0;
+  // the trace goes last: it is the only region whose size depends on iters, so no offset the
+  // cached iteration graph bakes in (tensor-core scratch, tensor maps) moves with iters
+  const size_t oTr = take(sizeof(double) * std::max(iters, 1));
   ntt_status s = ensure_ws(h, o);
   if (s) return s;
   char* ws = reinterpret_cast<char*>(h->ws);
@@ -1260,18 +1286,21 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
     LAUNCH(h, launch_sum_partials(Qpart, fa ? fparts : qp.ncs, (int64_t)r * r, Q, st));
     return NTT_OK;
   };
+  if ((s = check_nonneg(h, X, m, n, ldx, "X"))) return s;
   // ---- init (Alg. 3 l.1-4, R22, R23)
   CU(h, cudaMemsetAsync(bs, 0, sizeof(double) * BS_COUNT, st));
-  LAUNCH(h, launch_sumsq(X, m, n, ldx, sq, st));
+  LAUNCH(h, launch_sumsq(X, m, n, ldx, sq, st, bef != 0));
   LAUNCH(h, launch_sum_partials(sq, sumsq_ctas(), 1, bs + BS_XX, st));
   LAUNCH(h, launch_sumsq(W, m, r, r, sq, st));
   LAUNCH(h, launch_sum_partials(sq, sumsq_ctas(), 1, bs + BS_W0, st));
   LAUNCH(h, launch_sumsq(H, r, n, n, sq, st));
   LAUNCH(h, launch_sum_partials(sq, sumsq_ctas(), 1, bs + BS_H0, st));
-  double xx = 0.0;
-  CU(h, cudaMemcpyAsync(&xx, bs + BS_XX, sizeof(double), cudaMemcpyDeviceToHost, st));
+  double nrm[3] = {0.0, 0.0, 0.0};  // ||X||^2, ||W0||^2, ||H0||^2 (BS_XX, BS_W0, BS_H0)
+  CU(h, cudaMemcpyAsync(nrm, bs + BS_XX, sizeof(nrm), cudaMemcpyDeviceToHost, st));
   CU(h, cudaStreamSynchronize(st));
-  if (!(xx > 0.0)) return fail(h, NTT_ERR_DEGENERATE, "||X|| = 0");
+  if (!(nrm[0] > 0.0)) return fail(h, NTT_ERR_DEGENERATE, "||X|| = 0");
+  // l.2 divides by ||W0|| and ||H0||: an all-zero initial factor has no normalisation
+  if (!(nrm[1] > 0.0) || !(nrm[2] > 0.0)) return fail(h, NTT_ERR_DEGENERATE, "||W0|| = 0 or ||H0|| = 0");
   LAUNCH(h, launch_scale_copy(W, Wm, Wp, m * r, bs + BS_XX, bs + BS_W0, st));
   LAUNCH(h, launch_scale_copy(H, Hm, Hp, (int64_t)r * n, bs + BS_XX, bs + BS_H0, st));
   LAUNCH(h, launch_bcd_hout(Hp, r, n, sH, nullptr, 1, nullptr, st));  // sH = 1
@@ -1291,7 +1320,7 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   // (BS_FOLD), so the per-iteration H commit (3 H-sized streams) disappears
   const bool fold = cta && f1 && fused_fold_ok(m, n, r, ldx, X, H, Hp) && !getenv("NTT_BCD_NO_FOLD");
   const bool presum = !getenv("NTT_BCD_NO_PRESUM");
-  LAUNCH(h, launch_bcd_init(bs, delta, fold, st));
+  LAUNCH(h, launch_bcd_init(bs, delta, fold, h->bcd_force, st));
   auto iteration_cta = [&]() -> ntt_status {
     LAUNCH(h, launch_bcd_wside(Wm, W, Wp, (int)m, r, Pc, Qc, bs, c, G, sH, st));  // l.5-10
     int nPp = nP, nQp = qp.ncs;
@@ -1406,8 +1435,8 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
     st = h->gstream;
     // the graph bakes in pointers, sizes and tensor maps: reuse it while they are unchanged
     char kb[256];
-    snprintf(kb, sizeof(kb), "%p %p %p %p %lld %lld %lld %d", (const void*)X, (void*)W, (void*)H, (void*)h->ws,
-             (long long)m, (long long)n, (long long)ldx, r);
+    snprintf(kb, sizeof(kb), "%p %p %p %p %lld %lld %lld %d %zu", (const void*)X, (void*)W, (void*)H, (void*)h->ws,
+             (long long)m, (long long)n, (long long)ldx, r, oTr);
     if (!h->bcd_exec || h->bcd_key != kb) {
       if (h->bcd_exec) {
         cudaGraphExecDestroy(h->bcd_exec);
@@ -1489,7 +1518,7 @@ ntt_status ntt_decompose_eps(ntt_handle h, const float* A, int32_t d, const int6
     // run_mu scratch for every (r_{l-1}, r_l) the rule may pick
     for (int64_t rp = 1; rp <= cap[l - 1]; ++rp)
       for (int64_t r = 1; r <= c && r <= rp * s0.dims[l - 1]; ++r)
-        mu_bytes = std::max(mu_bytes, plan_mu(rp * s0.dims[l - 1], ncol[l], (int)r, h->num_sms, 1).bytes);
+        mu_bytes = std::max(mu_bytes, plan_mu(rp * s0.dims[l - 1], ncol[l], (int)r, h->num_sms, false).bytes);
     // rank-rule scratch for every Gram size the step can see (min(m, n) <= 512 is checked per step)
     const int64_t nmax = std::min<int64_t>({mcap[l], ncol[l], 512});
     for (int64_t Nn = 1; Nn <= nmax; ++Nn)
@@ -1521,6 +1550,7 @@ ntt_status ntt_decompose_eps(ntt_handle h, const float* A, int32_t d, const int6
     dA = reinterpret_cast<const float*>(h->stage);
     CU(h, cudaMemcpyAsync((void*)dA, A, sizeof(float) * (size_t)s0.N, cudaMemcpyHostToDevice, cs));
   }
+  if ((st = check_nonneg(h, dA, 1, s0.N, s0.N, "A"))) return st;
   float* hb[2] = {reinterpret_cast<float*>(ws + off_h0), reinterpret_cast<float*>(ws + off_h1)};
   float* Wd = reinterpret_cast<float*>(ws + off_w);
   float* dcores = reinterpret_cast<float*>(ws + off_c);
@@ -1544,7 +1574,7 @@ ntt_status ntt_decompose_eps(ntt_handle h, const float* A, int32_t d, const int6
     Hl = hb[(l - 1) & 1];
     LAUNCH(h, launch_fill_uniform(Wd, m * r, seed, stream_w(l), 0, cs));
     LAUNCH(h, launch_fill_uniform(Hl, (int64_t)r * n, seed, stream_h(l), 0, cs));
-    MuPlan p = plan_mu(m, n, r, h->num_sms, 1);
+    MuPlan p = plan_mu(m, n, r, h->num_sms, false);
     if (p.bytes > mu_bytes) return fail(h, NTT_ERR_WORKSPACE, "internal: MU scratch plan exceeded");
     if ((st = run_mu(h, p, X, n, iters, eps, Wd, Hl, ws + off_mu, nullptr))) return st;
     CU(h, cudaMemcpyAsync(dcores + coff, Wd, sizeof(float) * (size_t)(m * r), cudaMemcpyDeviceToDevice, cs));
@@ -1601,6 +1631,7 @@ ntt_status ntt_decompose_bcd(ntt_handle h, const float* A, int32_t d, const int6
     dA = reinterpret_cast<const float*>(h->stage);
     CU(h, cudaMemcpyAsync((void*)dA, A, sizeof(float) * (size_t)s.N, cudaMemcpyHostToDevice, cs));
   }
+  if ((st = check_nonneg(h, dA, 1, s.N, s.N, "A"))) return st;
   float* buf = nullptr;
   const size_t nfl = 2 * hmax + wmax + (size_t)s.cores;
   if (h->sweep_bytes < sizeof(float) * nfl) {  // grown once, reused by later calls
@@ -1965,6 +1996,43 @@ int ntt_dist_rank(ntt_handle h) { return h ? h->rank : -1; }
 int ntt_dist_size(ntt_handle h) { return h ? h->nranks : -1; }
 
 }  // extern "C"
+
+extern "C" int64_t ntt_collective_count(ntt_handle h) { return h ? h->collectives : -1; }
+
+extern "C" ntt_status ntt_debug_fill_uniform_cols(ntt_handle h, float* H, int32_t r, int64_t nloc, int64_t b,
+                                                  int64_t nd, int64_t off, int64_t nglob, uint64_t seed,
+                                                  uint64_t stream) {
+  if (!h) return NTT_ERR_INVALID_ARG;
+  if (!H || r < 1 || nloc < 0 || b < 1 || nd < b || off < 0 || off + b > nd || nloc % b || nglob < nloc ||
+      !is_device_ptr(H))
+    return fail(h, NTT_ERR_INVALID_ARG, "bad fill_uniform_cols layout");
+  CU(h, cudaSetDevice(h->device));
+  LAUNCH(h, launch_fill_uniform_cols(H, r, nloc, b, nd, off, nglob, seed, stream, h->stream));
+  return NTT_OK;
+}
+
+extern "C" ntt_status ntt_debug_gather_last_core(ntt_handle h, const float* gath, int64_t r, int64_t nd,
+                                                 int32_t nranks, float* core) {
+  if (!h) return NTT_ERR_INVALID_ARG;
+  if (!gath || !core || r < 1 || nd < nranks || nranks < 1 || !is_device_ptr(gath) || !is_device_ptr(core))
+    return fail(h, NTT_ERR_INVALID_ARG, "bad gather_last_core arguments");
+  CU(h, cudaSetDevice(h->device));
+  LAUNCH(h, launch_gather_last_core(gath, r, nd, nranks, core, h->stream));
+  return NTT_OK;
+}
+
+extern "C" ntt_status ntt_set_validation(ntt_handle h, int flags) {
+  if (!h) return NTT_ERR_INVALID_ARG;
+  if (flags & ~NTT_VALIDATE_NONNEG) return fail(h, NTT_ERR_INVALID_ARG, "unknown validation flags 0x%x", flags);
+  h->validate = flags;
+  return NTT_OK;
+}
+
+extern "C" ntt_status ntt_debug_bcd_force_correct(ntt_handle h, uint64_t mask) {
+  if (!h) return NTT_ERR_INVALID_ARG;
+  h->bcd_force = mask & ((1ull << 52) - 1);
+  return NTT_OK;
+}
 
 extern "C" const unsigned long long* ntt_debug_persist_trace(ntt_handle h) {
   if (!h) return nullptr;

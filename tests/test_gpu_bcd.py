@@ -75,6 +75,74 @@ def test_bcd_parity(h, ora, m, n, r, iters, lr):
     assert Wg.min() >= 0 and Hg.min() >= 0
 
 
+FORCED = (2, 3, 6)   # iterations forced onto the correction branch (two in a row, then one more)
+
+
+@pytest.mark.parametrize("m,n,r,lr", [
+    (32, 4096, 8, 0),     # one pass, H_m folded inside k_fused (BS_FOLD)
+    (9, 40, 4, 0),        # one pass k_fused, H_m materialised (no fold: n % 32 != 0)
+    (256, 32768, 8, 0),   # one pass k_fused_c, GPU-wide partial pre-sum
+    (64, 8192, 8, 4),     # one pass k_fused_c
+    (300, 512, 16, 0),    # fp16x2 tensor-core passes, large-W kernels
+    (100, 2000, 16, 6),   # FFMA passes, one-CTA W side / post kernels
+    (3000, 64, 5, 3),     # FFMA passes, large-W kernels
+    (7, 7, 7, 0)])        # generic small case
+def test_bcd_forced_correction_parity(h, ora, m, n, r, lr):
+    """Alg. 3 l.17-20 (reading R26) on every BCD path: the hook forces the
+    correction branch at iterations 2, 3 and 6; GPU and oracle (same hook) must agree on the
+    branches, the accepted objectives and the factors.  After a correction the returned
+    factors are the last accepted ones, t restarts at 1 (w = 0 in the next accepted step)
+    and P, Q come from the rescaled H_prev (no pass over X)."""
+    iters = 10
+    X, W0, H0 = case(m, n, r, m * 3 + n + r, lr)
+    h.ntt_debug_bcd_force_correct(FORCED)
+    try:
+        Wg, Hg, trg = run_gpu(h, X, W0, H0, iters)
+    finally:
+        h.ntt_debug_bcd_force_correct(())
+    log = []
+    Wo, Ho, tro = ora.nmf_bcd(X.astype(np.float64), W0, H0, iters, trace=True, log=log,
+                              force_correct=set(FORCED))
+    obj0 = 0.5 * float(np.sum(X.astype(np.float64) ** 2))
+    acc_o = np.array([e["accepted"] for e in log])
+    assert (~acc_o).sum() >= len(FORCED)
+    assert np.array_equal(branches(trg, obj0), acc_o)
+    # a forced correction leaves the accepted objective where it was
+    for i in FORCED:
+        assert trg[i] == (trg[i - 1] if i else obj0)
+    assert np.abs(trg - tro).max() <= 1e-5 * tro.max() + 1e-5 * obj0
+    assert np.abs(Wg - Wo).max() <= 1e-4 * np.abs(Wo).max()
+    assert np.abs(Hg - Ho).max() <= 1e-4 * np.abs(Ho).max()
+
+
+# (m, n, r, seed, kind, iterations): inputs on which the extrapolation overshoots by itself,
+# run to two iterations past the second correction; every objective change up to there is
+# >= 1.6e-6 * 1/2 ||X||^2, far above the fp32 resolution of the GPU's Gram-identity
+# objective (~1e-7 of it; R25), so the branch decisions are well posed on both sides
+NATURAL = [(7, 64, 3, 11, "scaled", 52), (7, 64, 3, 10, "colscaled", 63)]
+
+
+@pytest.mark.parametrize("m,n,r,seed,kind,iters", NATURAL)
+def test_bcd_natural_correction_parity(h, ora, m, n, r, seed, kind, iters):
+    """Inputs on which the extrapolation overshoots by itself (ntt_inputs.bcd_overshoot_matrix:
+    row / column scales over three decades): the oracle takes >= 2 corrections (asserted), and
+    the GPU takes the same branches with factors within 1e-4."""
+    import ntt_inputs as ni
+    X = ni.bcd_overshoot_matrix(m, n, r, seed, kind)
+    W0 = ni.uniform(m * r, seed, ni.stream_w(1)).reshape(m, r).astype(np.float32)
+    H0 = ni.uniform(r * n, seed, ni.stream_h(1)).reshape(r, n).astype(np.float32)
+    Wg, Hg, trg = run_gpu(h, X, W0, H0, iters)
+    log = []
+    Wo, Ho, tro = ora.nmf_bcd(X.astype(np.float64), W0, H0, iters, trace=True, log=log)
+    obj0 = 0.5 * float(np.sum(X.astype(np.float64) ** 2))
+    corr = [e["it"] for e in log if not e["accepted"]]
+    assert len(corr) >= 2
+    assert np.array_equal(branches(trg, obj0), np.array([e["accepted"] for e in log]))
+    assert np.abs(trg - tro).max() <= 1e-5 * tro.max() + 1e-5 * obj0
+    assert np.abs(Wg - Wo).max() <= 1e-4 * np.abs(Wo).max()
+    assert np.abs(Hg - Ho).max() <= 1e-4 * np.abs(Ho).max()
+
+
 def test_bcd_zero_iterations_rescales(h, ora):
     X, W0, H0 = case(30, 70, 3, 1)
     Wg, Hg, _ = run_gpu(h, X, W0, H0, 0)
@@ -106,6 +174,10 @@ def test_bcd_errors(h):
     Z = torch.zeros(20 * 40, device="cuda")
     with pytest.raises(P.NttError):
         h.ntt_nmf_bcd(Z, 20, 40, 40, 4, 5, W, H)            # ||X|| = 0
+    with pytest.raises(P.NttError, match="W0"):
+        h.ntt_nmf_bcd(X, 20, 40, 40, 4, 5, torch.zeros(20 * 4, device="cuda"), H)   # ||W0|| = 0 (l.2)
+    with pytest.raises(P.NttError, match="H0"):
+        h.ntt_nmf_bcd(X, 20, 40, 40, 4, 5, W, torch.zeros(4 * 40, device="cuda"))   # ||H0|| = 0
 
 
 def test_bcd_fullsize_properties(h):

@@ -1,7 +1,16 @@
-"""The library's NCCL path (ntt_create_dist) on one GPU (a 1-rank communicator):
-exercises the per-pass all-reduce of the fp64 partials, the global-index H init
-and the last-core gather.  Results must match the single-GPU handle and the
-oracle (parity tolerances of test_gpu_parity)."""
+"""The library's NCCL path (ntt_create_dist / ntt_create_dist_grid) on one GPU.
+
+A handle made by ntt_create_dist* always takes the distributed branches, also with
+a 1-rank communicator: the per-pass reduction of the fp64 (X H^T, H H^T) partials
+followed by ncclAllReduce (dist_reduce), the global-column-index H init
+(k_fill_uniform_cols), the last-core gather by per-rank broadcasts into a staging
+area plus k_gather_last_core, the all-reduce of the Eq. 3 sums, and on the
+tensor-core path tc_reduce_PQ / tc_wupdate_ex / tc_reduce_S / tc_hupdate_ex over
+the grid-row and grid-column communicators.  ntt_collective_count proves the NCCL
+calls were issued.  Results must match the single-GPU handle and the oracle (parity
+tolerances of test_gpu_parity).  The p > 1 index maps of the init and of the gather
+are checked at kernel level on emulated layouts (p = 8, rank 3; ragged n_d = 7 over
+p = 3)."""
 import numpy as np
 import pytest
 
@@ -32,7 +41,10 @@ def test_dist_handle_decompose_matches(handles, ora, dims, ranks, iters):
     c1 = torch.empty(ora.cores_size(dims, ranks), device="cuda")
     cd = torch.empty_like(c1)
     e1 = h1.ntt_decompose(Ad, dims, ranks, iters, 0, 1e-16, c1, want_error=True)
+    n0 = hd.collective_count
     ed = hd.ntt_decompose(Ad, dims, ranks, iters, 0, 1e-16, cd, want_error=True)
+    # per MU pass one all-reduce; a graph replay of an identical call issues none anew
+    assert hd.collective_count - n0 >= (len(dims) - 1) * iters
     torch.cuda.synchronize()
     a, b = c1.cpu().numpy().astype(np.float64), cd.cpu().numpy().astype(np.float64)
     assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(a)
@@ -50,7 +62,9 @@ def test_dist_handle_nmf_mu(handles, ora, m, n, r):
     H0 = ni.uniform(r * n, 1, 0x203).reshape(r, n).astype(np.float32)
     Xd = torch.from_numpy(X).cuda()
     Wd, Hd = torch.from_numpy(W0.copy()).cuda(), torch.from_numpy(H0.copy()).cuda()
+    n0 = hd.collective_count
     hd.ntt_nmf_mu(Xd, m, n, n, r, 8, 1e-16, Wd, Hd)
+    assert hd.collective_count - n0 >= 8
     Wo, Ho = ora.nmf_mu(X, W0.astype(np.float64), H0.astype(np.float64), 8)
     W, H = Wd.cpu().numpy(), Hd.cpu().numpy()
     assert np.linalg.norm(W - Wo) <= 1e-4 * np.linalg.norm(Wo)
@@ -75,7 +89,10 @@ def test_grid_handle_tc_nmf_matches(handles, ora, m, n, r):
     for h in (h1, hg):
         Wd, Hd = torch.from_numpy(W0.copy()).cuda(), torch.from_numpy(H0.copy()).cuda()
         h.ntt_profile_enable(True)
+        n0 = h.collective_count
         h.ntt_nmf_mu(Xd, m, n, n, r, 6, 1e-16, Wd, Hd)
+        # grid handle: 3 all-reduces per iteration (row: X H^T | H H^T; column: W^T W, W^T X)
+        assert h.collective_count - n0 == (18 if h is hg else 0)
         assert h.ntt_profile_get(6)[0] == 6, "tensor-core path not taken"
         h.ntt_profile_enable(False)
         outs.append((Wd.cpu().numpy(), Hd.cpu().numpy()))
@@ -91,3 +108,43 @@ def test_grid_handle_rejects_bad_grid():
         pytest.skip("no CUDA device")
     with pytest.raises(P.NttError):
         P.Handle(0, unique_id=P.ntt_get_unique_id(), nranks=1, rank=0, grid=(2, 1))
+
+
+@pytest.mark.parametrize("dims,ranks,p,g", [([5, 4, 6, 16], [3, 4, 2], 8, 3), ([4, 3, 7], [2, 3], 3, 2),
+                                            ([4, 3, 7], [2, 3], 3, 0), ([6, 5, 9], [4, 2], 4, 1)])
+def test_fill_uniform_cols_layout(handles, dims, ranks, p, g):
+    """k_fill_uniform_cols on the local H of rank g of p (last mode block-partitioned,
+    DESIGN.md s.7): every entry equals the RNG spec drawn at the GLOBAL index of
+    ntt_inputs.rng_u24, at every TT step, so inits agree for any p."""
+    import paper_2008_01340_b200 as P
+    _, hd = handles
+    nd = dims[-1]
+    b, off = P.ntt_dist_block(nd, p, g)
+    rest = int(np.prod(dims))
+    for l in range(1, len(dims)):
+        rest //= dims[l - 1]
+        r = ranks[l - 1]
+        nglob = rest
+        nloc = rest // nd * b
+        H = torch.empty(r * nloc, device="cuda")
+        hd.ntt_debug_fill_uniform_cols(H, r, nloc, b, nd, off, nglob, 7, ni.stream_h(l))
+        c = np.arange(nloc)
+        cg = (c // b) * nd + off + c % b
+        idx = (np.arange(r)[:, None] * nglob + cg[None, :]).ravel()
+        ref = ni.rng_u24(7, ni.stream_h(l), idx).astype(np.float64) * 2.0 ** -24
+        assert np.array_equal(H.cpu().numpy().astype(np.float64), ref)
+
+
+@pytest.mark.parametrize("r,nd,p", [(3, 7, 3), (2, 16, 8), (5, 9, 4), (1, 5, 5)])
+def test_gather_last_core_ragged(handles, r, nd, p):
+    """k_gather_last_core: rank-major staging [rank g: r x b_g] -> core[k][i] (r x nd) for
+    ragged blocks b_g = floor((g+1) nd / p) - floor(g nd / p)."""
+    import paper_2008_01340_b200 as P
+    _, hd = handles
+    core = np.arange(r * nd, dtype=np.float32).reshape(r, nd) + 1
+    blocks = [P.ntt_dist_block(nd, p, g) for g in range(p)]
+    assert sum(b for b, _ in blocks) == nd
+    gath = np.concatenate([core[:, o:o + b].ravel() for b, o in blocks])
+    out = torch.full((r * nd,), -1.0, device="cuda")
+    hd.ntt_debug_gather_last_core(torch.from_numpy(gath).cuda(), r, nd, p, out)
+    assert np.array_equal(out.cpu().numpy().reshape(r, nd), core)

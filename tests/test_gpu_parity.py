@@ -316,3 +316,41 @@ def test_nmf_mu_small_path_parity(h, ora, m, n, r, monkeypatch):
     Wo, Ho = ora.nmf_mu(X, W0.astype(np.float64), H0.astype(np.float64), 10, eps=1e-16)
     assert_close_factor(host(Wd), Wo, what=f"small W {m}x{n} r{r}")
     assert_close_factor(host(Hd), Ho, what=f"small H {m}x{n} r{r}")
+
+
+def test_validation_nonneg(h):
+    """NTT_VALIDATE_NONNEG (SURVEY s.8(b)): with the flag on, a negative or NaN entry in
+    X / A is rejected with NTT_ERR_NONNEG (status 5) before anything runs; valid input runs as
+    without the flag (bit-identical); off by default."""
+    import paper_2008_01340_b200 as P
+    X, W0, H0 = _mu_inputs(8, 64, 2, 3)
+    ref_W, ref_H = dev(W0), dev(H0)
+    h.ntt_nmf_mu(dev(X), 8, 64, 64, 2, 3, 1e-16, ref_W, ref_H)
+    h.ntt_set_validation(True)
+    try:
+        W, H = dev(W0), dev(H0)
+        h.ntt_nmf_mu(dev(X), 8, 64, 64, 2, 3, 1e-16, W, H)
+        assert torch.equal(W, ref_W) and torch.equal(H, ref_H)
+        for bad in (-1e-3, float("nan")):
+            Xb = X.copy()
+            Xb[5, 17] = bad
+            with pytest.raises(P.NttError) as e:
+                h.ntt_nmf_mu(dev(Xb), 8, 64, 64, 2, 3, 1e-16, dev(W0), dev(H0))
+            assert e.value.status == 5
+            with pytest.raises(P.NttError) as e:
+                h.ntt_nmf_bcd(dev(Xb), 8, 64, 64, 2, 3, dev(W0), dev(H0))
+            assert e.value.status == 5
+        dims, ranks = [5, 4, 5, 6], [4, 3, 2]
+        A = _tt_case(dims, ranks)
+        A.ravel()[123] = -0.5
+        cores = torch.empty(P.cores_size(dims, ranks), device="cuda")
+        for call in (lambda: h.ntt_decompose(dev(A), dims, ranks, 3, 0, 1e-16, cores),
+                     lambda: h.ntt_decompose_bcd(dev(A), dims, ranks, 3, 0, cores)):
+            with pytest.raises(P.NttError) as e:
+                call()
+            assert e.value.status == 5
+    finally:
+        h.ntt_set_validation(False)
+    Xb = X.copy()
+    Xb[0, 0] = -1.0
+    h.ntt_nmf_mu(dev(Xb), 8, 64, 64, 2, 3, 1e-16, dev(W0), dev(H0))     # off: not checked
