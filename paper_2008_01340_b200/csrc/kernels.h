@@ -42,13 +42,7 @@ bool tiny_supported(int64_t m, int64_t n, int r);
 cudaError_t launch_tiny(const float* X, int64_t ldx, int64_t m, int64_t n, int r, int iters, float eps, float* W,
                         float* H, cudaStream_t st);
 
-// very short unfoldings (mu_small.cu): one lane per column pair, register-resident 1-pass
-// MU pass with the launch_fused modes (1 = H update, 2 = P/Q partials) and partial layout
-bool small_supported(int64_t m, int64_t n, int r, int64_t ldx, const void* X, const void* H);
-int small_grid(int64_t n, int num_sms);
-cudaError_t launch_small(const float* X, int64_t ldx, int64_t m, int64_t n, int r, const float* W, const double* Gpart,
-                         int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
-                         cudaStream_t st);
+
 
 // SVD rank rule of Alg. 2 l.5-6 (tt_rank.cu): Gram of X (min(m, n) <= 512) -> eigenvalues
 // (Householder + bisection, one CTA) -> r = smallest k with tail energy <= tt_eps.

@@ -19,13 +19,16 @@
 // read by broadcast.  fp32 FMA inside a tile, fp64 accumulation across tiles,
 // fixed-order CTA reduction into per-CTA fp64 partials (deterministic).
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 #include <utility>
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
 #include "mu_fused.h"
+#include "sm100.cuh"
 
 namespace ntt {
 
@@ -37,32 +40,8 @@ constexpr int BN = 128;             // tile columns
 constexpr int HN_FLOATS = 1168;     // per-warp transposed Hn tile (padded)
 constexpr int SMEM_BUDGET = 232448; // 227 KB opt-in
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+using namespace sm100;  // mbarrier / TMA wrappers (sm100.cuh)
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// try_wait in a C++ loop (not an asm-internal branch loop): the compiler must
-// see the divergent spin to place reconvergence before warp-synchronous code.
-__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try(bar, parity)) {
-  }
-}
 #ifdef NTT_WATCHDOG
 __device__ __forceinline__ void mbar_wait_dbg(uint64_t* bar, uint32_t parity, int tag, long long j) {
   long long t0 = clock64();
@@ -78,23 +57,18 @@ __device__ __forceinline__ void mbar_wait_dbg(uint64_t* bar, uint32_t parity, in
 #else
 #define MBAR_WAIT(bar, par, tag, j) mbar_wait(bar, par)
 #endif
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
-                                            uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-// one 3-D box {32 cols, rows, blocks} = `blocks` consecutive 32-column boxes in one transaction
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
-                                            uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
+#ifdef NTT_WATCHDOG
+#define MBAR_WAIT_BACKOFF(bar, par, tag, j) mbar_wait_dbg(bar, par, tag, j)
+#else
+// producer-side wait with a sleep between polls: a spinning producer warp takes issue
+// slots from the consumer warp sharing its scheduler (k_fused_c: 24 % of all executed
+// instructions were this poll, ncu source page)
+#define MBAR_WAIT_BACKOFF(bar, par, tag, j) \
+  do {                                     \
+    while (!mbar_try_sleep(bar, par)) {     \
+    }                                      \
+  } while (0)
+#endif
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
@@ -774,6 +748,54 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
 }
 
 
+
+// ---------------------------------------------------------------------------
+// fp16 hi/lo operand split for warp-level mma.sync (k_fused_c): v = 2^-e (hi + lo) with
+// hi = fp16(v 2^e), lo = fp16(v 2^e - hi) (~22 significant bits; the lo x lo product is
+// dropped), 2^e a power of two chosen per operand block so |v| 2^e < 2^14.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ void split2(float a, float b, float s, uint32_t& hi, uint32_t& lo) {
+  const float2 x = __fmul2_rn(make_float2(a, b), make_float2(s, s));
+  const __half2 h = __float22half2_rn(x);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __float22half2_rn(make_float2(x.x - hf.x, x.y - hf.y));
+  hi = h2_bits(h);
+  lo = h2_bits(l);
+}
+// power-of-two scale for a block whose max |v| is mx: (2^e, 2^-e) with mx 2^e in [2^13, 2^14)
+__device__ __forceinline__ float2 pow2_scale(float mx) {
+  const int ex = (int)((__float_as_uint(mx) >> 23) & 255u);
+  int e = ex == 0 ? 0 : 140 - ex;
+  e = e < -120 ? -120 : (e > 120 ? 120 : e);
+  return make_float2(__uint_as_float((uint32_t)(e + 127) << 23), __uint_as_float((uint32_t)(127 - e) << 23));
+}
+// max over the warp of non-negative floats: one redux.sync on the bit patterns (which order
+// like the values for v >= 0)
+__device__ __forceinline__ float warp_max(float v) {
+  return __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(v)));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t a, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t a, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a));
+}
+// D += A B (m16n8k16, fp16 inputs, fp32 accumulators)
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// byte offset of 16-byte chunk `ch` (0..3) of row `row` in a [rows][32] fp16 array (64-byte
+// rows, chunk XOR (row / 2) mod 4: conflict-free for ldmatrix's 8-row phases)
+__device__ __forceinline__ uint32_t h16_off(int row, int ch) { return (uint32_t)(row * 64 + ((ch ^ ((row >> 1) & 3)) << 4)); }
+
 // ===========================================================================
 // Variant C: CTA-cooperative tiles for 40 < m <= 256 (rank padded to 8).
 // Small CTAs (4 consumer warps + 1 TMA warp, <= 112 KB smem) so TWO CTAs share
@@ -826,6 +848,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   // BCD mode (PersistArgs::bcdL; see k_fused): row scales of H_m (smem), 1 / L_H, output buffer
   const bool bcd = pa.bcdL != nullptr;
   __shared__ float bsh[8];
+  __shared__ float hmx[NW];  // per-warp max |Hn| of the current tile (mma.sync phase B scale)
   if (tid < 8) bsh[tid] = (bcd && tid < r) ? (float)pa.bcdS[tid] : 1.f;
   const float binvL = (bcd && *pa.bcdL > 0.0) ? (float)(1.0 / *pa.bcdL) : 0.f;
   float* const Ho = (bcd && pa.Hout) ? ((pa.bcdRole && *pa.bcdRole != 0.0) ? pa.Hout2 : pa.Hout) : H;
@@ -839,19 +862,15 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       Gs[e] = (float)sum;
     }
   }
-#ifdef NTT_FC_PAIR_A
-  constexpr bool COLA = false;
-#else
-  // phase A with lanes = (2 columns, 4 ranks): X by LDS.64 (one 128-byte row per warp) and W
-  // by one half-warp-uniform LDS.128 per row; the (4 columns x 2 ranks) lane layout read X by
-  // 128-bit loads that 4 lanes share (4 wavefronts per row, tools/ldsbench.cu), and the
-  // (1 column x 8 ranks) layout spent 2 x 2 wavefronts per row on uniform LDS.128s of W
-  constexpr bool COLA = !WREG;
-#endif
-  constexpr bool WPAIR = !WREG && !COLA;  // W in row-pair layout (one 128-bit load per 2 rows in phase A)
   for (int e = tid; e < MP * 8; e += NTHR) {
     const int i = e >> 3, k = e & 7;
-    Wc[widx(i, k, WPAIR)] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
+    Wc[widx(i, k, false)] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
+  }
+  if (pa.x16) {
+    // X16 passes copy only the blocks of rows < m: the others must read as zeros in every stage
+    for (int e = tid; e < ns * (MP * 32); e += NTHR)
+      reinterpret_cast<uint32_t*>(stages + (size_t)(e / (MP * 32)) * SB)[e % (MP * 32)] = 0u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) {
@@ -864,6 +883,8 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 
   const int64_t ntiles = (n + BNC - 1) / BNC;
   const int64_t b = blockIdx.x;
+  const int nblk = (m + 31) / 32;                           // 32-row blocks of X present in a tile
+  const int64_t x16_stride = (int64_t)nblk * 4096 + 128;   // per-tile blob: blocks + 32 scales
   const int64_t J = (ntiles > b) ? (ntiles - b + gridDim.x - 1) / gridDim.x : 0;
 
   unsigned epoch = 0;
@@ -874,6 +895,9 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   const int md = persist ? (it == 0 ? kFusedAcc : (kFusedUpdate | (it < pa.iters ? kFusedAcc : 0))) : mode;
   const bool do_update = (md & kFusedUpdate) != 0;
   const bool do_acc = (md & kFusedAcc) != 0;
+  // X16 cache: the prologue pass (it == 0) writes it, every later pass streams it
+  const bool x16_write = pa.x16 != nullptr && persist && it == 0;
+  const bool x16_read = pa.x16 != nullptr && persist && it > 0;
   const int64_t pbase = (int64_t)it * J;
   pstamp(pa, it, 0);
   if (warp == NW) {
@@ -890,17 +914,27 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
           ring_s = 0;
           ring_ph ^= 1u;
         }
-        MBAR_WAIT(&empty[s], ph ^ 1u, 3, j);
-        mbar_expect_tx(&full[s], SB);
-        const int col0 = (int)((b + j * gridDim.x) * BNC);
+        MBAR_WAIT_BACKOFF(&empty[s], ph ^ 1u, 3, j);
+        const int64_t tile = b + j * gridDim.x;
+        const int col0 = (int)(tile * BNC);
         unsigned char* st = stages + (size_t)s * SB;
-        tma_load_2d(st, &tmX, col0, 0, &full[s], policy);
+        if (x16_read) {  // the tile's fp16 hi / lo blocks, one contiguous bulk copy
+          mbar_expect_tx(&full[s], (uint32_t)(nblk * 4096) + 1024u);
+          bulk_load_1d(st, pa.x16 + tile * x16_stride, (uint32_t)(nblk * 4096), &full[s], policy);
+        } else {
+          mbar_expect_tx(&full[s], SB);
+          tma_load_2d(st, &tmX, col0, 0, &full[s], policy);
+        }
         tma_load_2d(st + XB, &tmH, col0, 0, &full[s], policy);
       }
     }
   } else {
 
-  const int q = lane & 7, g = lane >> 3;   // phase A: columns 4q..4q+3, ranks 2g, 2g+1
+  // One pass's tile loop, instantiated per pass mode (UPD: phase A + H update, ACC: phase B,
+  // BCD: Alg. 3's prox-linear H step instead of the MU rule), so no per-tile branch on the mode.
+  auto pass_tiles = [&](auto upd_t, auto acc_t, auto bcd_t) {
+  constexpr bool UPD = decltype(upd_t)::value, ACC = decltype(acc_t)::value, BCD = decltype(bcd_t)::value;
+  const int q = lane & 7, g = lane >> 3;   // phase A (RW = 32): columns 4q..4q+3, ranks 2g, 2g+1
   const int rb = lane & 7, cs = lane >> 3; // phase B: rows rb + 8u of a 32-row chunk, columns 8cs..8cs+7
   double accd[NCH][8];
 #pragma unroll
@@ -912,12 +946,67 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   for (int qq = 0; qq < QR; ++qq) qd[qq] = 0.0;
   const bool h1 = (lane >> 4) & 1, h0 = (lane >> 3) & 1;
   constexpr int NBAR = NW * 32;
+#ifdef NTT_FC_FFMA
   // this warp's W rows (ranks 2g, 2g+1) in registers when it owns 32 rows
   float2 wreg[WREG ? 32 : 1];
-  if constexpr (WREG) {
+  if constexpr (WREG && UPD) {
 #pragma unroll
     for (int v = 0; v < 32; ++v) wreg[v] = *reinterpret_cast<const float2*>(Wc + widx(warp * RW + v, 2 * g, false));
   }
+#else
+  constexpr int NB = RW / 32;  // 32-row blocks per warp
+  constexpr int NN = 1;        // n-tiles of 8 ranks
+  const int fg = lane >> 2, ft = lane & 3;  // mma fragment coordinates (group, thread in group)
+  float xsi[NB];               // 2^-e of each block's X split (this tile)
+#pragma unroll
+  for (int bb = 0; bb < NB; ++bb) xsi[bb] = 1.f;
+  // phase A's B operand: W rows of this warp as fp16 hi / lo fragments, one scale per warp and pass:
+  // b0 = {W[r0 + 2ft][8nn + fg], W[r0 + 2ft + 1][..]}, b1 = rows + 8, + 9; r0 = warp RW + 32 bb + 16 ks
+  uint32_t wfh[NB][2][NN][2], wfl[NB][2][NN][2];
+  float wsi = 1.f;
+  if constexpr (UPD) {
+    float wm = 0.f;
+#pragma unroll
+    for (int bb = 0; bb < NB; ++bb)
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+        for (int nn = 0; nn < NN; ++nn)
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int r0 = warp * RW + 32 * bb + 16 * ks + 8 * h2 + 2 * ft, k = 8 * nn + fg;
+            wm = fmaxf(wm, fmaxf(fabsf(Wc[widx(r0, k, false)]), fabsf(Wc[widx(r0 + 1, k, false)])));
+          }
+    const float2 wsc = pow2_scale(warp_max(wm));
+    wsi = wsc.y;
+#pragma unroll
+    for (int bb = 0; bb < NB; ++bb)
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+        for (int nn = 0; nn < NN; ++nn)
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int r0 = warp * RW + 32 * bb + 16 * ks + 8 * h2 + 2 * ft, k = 8 * nn + fg;
+            split2(Wc[widx(r0, k, false)], Wc[widx(r0 + 1, k, false)], wsc.x, wfh[bb][ks][nn][h2], wfl[bb][ks][nn][h2]);
+          }
+  }
+  float pacc[NB][2][NN][4];
+  double paccd[NB][2][NN][4];
+#pragma unroll
+  for (int bb = 0; bb < NB; ++bb)
+#pragma unroll
+    for (int mh = 0; mh < 2; ++mh)
+#pragma unroll
+      for (int nn = 0; nn < NN; ++nn)
+#pragma unroll
+        for (int e4 = 0; e4 < 4; ++e4) {
+          pacc[bb][mh][nn][e4] = 0.f;
+          paccd[bb][mh][nn][e4] = 0.0;
+        }
+  int since_flush = 0;
+  constexpr int RS = 8;  // Sred row stride per warp (ranks)
+#endif
 
   for (int64_t j = 0; j < J; ++j) {
     const int s = ring_s;
@@ -930,30 +1019,44 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     const unsigned char* st = stages + (size_t)s * SB;
     const int64_t jt = (b + j * gridDim.x) * BNC;
 
-    if (do_update) {
+    if constexpr (!UPD) {
+      // prologue: Hn of the previous tile may still be read by phase B of other warps
+      asm volatile("bar.sync 1, %0;" ::"r"(NBAR) : "memory");
+    }
+#ifdef NTT_FC_FFMA
+    if constexpr (UPD) {
       // ---- phase A: partial S over this warp's rows
-      float2 sa = f2(0.f, 0.f), sb = f2(0.f, 0.f), sc = f2(0.f, 0.f), sd = f2(0.f, 0.f);
-      if constexpr (COLA) {
-        // lane = (cp = lane & 15: columns 2cp, 2cp+1; kh = lane >> 4: ranks 4kh..4kh+3);
-        // sa..sd = S[4kh + 0..3][2cp..2cp+1]
+      if constexpr (!WREG) {
+        // lane = (cp = lane & 15: columns 2cp, 2cp+1; kh = lane >> 4: ranks 4kh..4kh+3): X by one
+        // LDS.64 per row (the warp reads the 128-byte row), W by one half-warp-uniform LDS.128;
+        // even and odd rows in two accumulator sets (8 independent FFMA2 chains)
         const int cp = lane & 15, kh = lane >> 4;
         const unsigned char* xb = st + (size_t)(warp * RW) * 128 + (cp & 1) * 8;
         const float* wb = Wc + warp * RW * 8 + 4 * kh;
-#pragma unroll 8
-        for (int v = 0; v < RW; ++v) {
-          const float2 x = *reinterpret_cast<const float2*>(xb + v * 128 + (((cp >> 1) ^ (v & 7)) << 4));
-          const float4 w = *reinterpret_cast<const float4*>(wb + v * 8);
-          sa = __ffma2_rn(bc(w.x), x, sa);
-          sb = __ffma2_rn(bc(w.y), x, sb);
-          sc = __ffma2_rn(bc(w.z), x, sc);
-          sd = __ffma2_rn(bc(w.w), x, sd);
+        float2 sa = f2(0.f, 0.f), sb = f2(0.f, 0.f), sc = f2(0.f, 0.f), sd = f2(0.f, 0.f);
+        float2 ta = f2(0.f, 0.f), tb = f2(0.f, 0.f), tc = f2(0.f, 0.f), td = f2(0.f, 0.f);
+#pragma unroll 4
+        for (int v = 0; v < RW; v += 2) {
+          const float2 x0 = *reinterpret_cast<const float2*>(xb + v * 128 + (((cp >> 1) ^ (v & 7)) << 4));
+          const float2 x1 = *reinterpret_cast<const float2*>(xb + (v + 1) * 128 + (((cp >> 1) ^ ((v + 1) & 7)) << 4));
+          const float4 w0 = *reinterpret_cast<const float4*>(wb + v * 8);
+          const float4 w1 = *reinterpret_cast<const float4*>(wb + (v + 1) * 8);
+          sa = __ffma2_rn(bc(w0.x), x0, sa);
+          sb = __ffma2_rn(bc(w0.y), x0, sb);
+          sc = __ffma2_rn(bc(w0.z), x0, sc);
+          sd = __ffma2_rn(bc(w0.w), x0, sd);
+          ta = __ffma2_rn(bc(w1.x), x1, ta);
+          tb = __ffma2_rn(bc(w1.y), x1, tb);
+          tc = __ffma2_rn(bc(w1.z), x1, tc);
+          td = __ffma2_rn(bc(w1.w), x1, td);
         }
         float* sr = Sred + (warp * 8 + 4 * kh) * 32 + 2 * cp;
-        *reinterpret_cast<float2*>(sr) = sa;
-        *reinterpret_cast<float2*>(sr + 32) = sb;
-        *reinterpret_cast<float2*>(sr + 64) = sc;
-        *reinterpret_cast<float2*>(sr + 96) = sd;
-      } else if constexpr (WREG) {
+        *reinterpret_cast<float2*>(sr) = __fadd2_rn(sa, ta);
+        *reinterpret_cast<float2*>(sr + 32) = __fadd2_rn(sb, tb);
+        *reinterpret_cast<float2*>(sr + 64) = __fadd2_rn(sc, tc);
+        *reinterpret_cast<float2*>(sr + 96) = __fadd2_rn(sd, td);
+      } else {
+        float2 sa = f2(0.f, 0.f), sb = f2(0.f, 0.f), sc = f2(0.f, 0.f), sd = f2(0.f, 0.f);
 #pragma unroll
         for (int v = 0; v < RW; ++v) {
           const int i = warp * RW + v;
@@ -965,39 +1068,129 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
           sc = __ffma2_rn(bc(wv.y), x01, sc);
           sd = __ffma2_rn(bc(wv.y), x23, sd);
         }
-      } else {
-#pragma unroll 4
-        for (int v = 0; v < RW; v += 2) {
-          const int i = warp * RW + v;
-          const float4 xa = lds128(st + i * 128 + ((q ^ (i & 7)) << 4));
-          const float4 xb = lds128(st + (i + 1) * 128 + ((q ^ ((i + 1) & 7)) << 4));
-          // W[i][2g], W[i][2g+1], W[i+1][2g], W[i+1][2g+1]
-          const float4 w4 = *reinterpret_cast<const float4*>(Wc + widx(i, 2 * g, true));
-          sa = __ffma2_rn(bc(w4.x), f2(xa.x, xa.y), sa);
-          sb = __ffma2_rn(bc(w4.x), f2(xa.z, xa.w), sb);
-          sc = __ffma2_rn(bc(w4.y), f2(xa.x, xa.y), sc);
-          sd = __ffma2_rn(bc(w4.y), f2(xa.z, xa.w), sd);
-          sa = __ffma2_rn(bc(w4.z), f2(xb.x, xb.y), sa);
-          sb = __ffma2_rn(bc(w4.z), f2(xb.z, xb.w), sb);
-          sc = __ffma2_rn(bc(w4.w), f2(xb.x, xb.y), sc);
-          sd = __ffma2_rn(bc(w4.w), f2(xb.z, xb.w), sd);
-        }
-      }
-      if constexpr (!COLA) {
         float* sr = Sred + (warp * 8 + 2 * g) * 32 + 4 * q;
         *reinterpret_cast<float4*>(sr) = make_float4(sa.x, sa.y, sb.x, sb.y);
         *reinterpret_cast<float4*>(sr + 32) = make_float4(sc.x, sc.y, sd.x, sd.y);
       }
+      asm volatile("bar.sync 1, %0;" ::"r"(NBAR) : "memory");
     }
-    asm volatile("bar.sync 1, %0;" ::"r"(NBAR) : "memory");
+#else
+    if (x16_read) {
+      // the block scales of this tile (written by the prologue pass next to its blocks)
+      const float* sc = reinterpret_cast<const float*>(pa.x16 + (b + j * gridDim.x) * x16_stride + nblk * 4096);
+#pragma unroll
+      for (int bb = 0; bb < NB; ++bb) {
+        const int gb = warp * NB + bb;
+        xsi[bb] = gb < nblk ? __ldcg(sc + gb) : 0.f;
+      }
+    } else {
+      // ---- this warp's rows of the tile -> fp16 hi / lo parts, in place (each 32-row block of
+      // 4 KB fp32 becomes [hi: 32 x 32 fp16 | lo: 32 x 32 fp16]); per-block power-of-two scale;
+      // the prologue pass of a persistent launch also stores them to the X16 cache
+      unsigned char* gtile = x16_write ? pa.x16 + (b + j * gridDim.x) * x16_stride : nullptr;
+#pragma unroll
+      for (int bb = 0; bb < NB; ++bb) {
+        const int gb = warp * NB + bb;
+        unsigned char* blk = const_cast<unsigned char*>(st) + (size_t)(warp * RW + 32 * bb) * 128;
+        float v[32];
+#pragma unroll
+        for (int c16 = 0; c16 < 8; ++c16) {
+          const float4 f = lds128(blk + lane * 128 + ((c16 ^ (lane & 7)) << 4));
+          v[4 * c16] = f.x;
+          v[4 * c16 + 1] = f.y;
+          v[4 * c16 + 2] = f.z;
+          v[4 * c16 + 3] = f.w;
+        }
+        float m8[8];  // max |v| as a tree (depth 4) rather than a 31-long chain
+#pragma unroll
+        for (int q2 = 0; q2 < 8; ++q2)
+          m8[q2] = fmaxf(fmaxf(fabsf(v[4 * q2]), fabsf(v[4 * q2 + 1])), fmaxf(fabsf(v[4 * q2 + 2]), fabsf(v[4 * q2 + 3])));
+        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        const float2 sc = pow2_scale(warp_max(mx));
+        xsi[bb] = sc.y;
+        __syncwarp();
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+          uint32_t hh[4], ll[4];
+#pragma unroll
+          for (int p2 = 0; p2 < 4; ++p2) split2(v[8 * k4 + 2 * p2], v[8 * k4 + 2 * p2 + 1], sc.x, hh[p2], ll[p2]);
+          *reinterpret_cast<uint4*>(blk + h16_off(lane, k4)) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
+          *reinterpret_cast<uint4*>(blk + 2048 + h16_off(lane, k4)) = make_uint4(ll[0], ll[1], ll[2], ll[3]);
+          if (gtile && gb < nblk) {
+            __stcg(reinterpret_cast<uint4*>(gtile + gb * 4096 + h16_off(lane, k4)), make_uint4(hh[0], hh[1], hh[2], hh[3]));
+            __stcg(reinterpret_cast<uint4*>(gtile + gb * 4096 + 2048 + h16_off(lane, k4)),
+                   make_uint4(ll[0], ll[1], ll[2], ll[3]));
+          }
+        }
+        if (gtile && gb < nblk && lane == 0) __stcg(reinterpret_cast<float*>(gtile + nblk * 4096) + gb, sc.y);
+      }
+      __syncwarp();
+    }
+    if constexpr (UPD) {
+      // ---- phase A: S^T (32 cols x R) = X^T W over this warp's rows by mma.sync m16n8k16:
+      // A = X^T (ldmatrix.trans of the fp16 parts), B = W (fragments built per pass),
+      // hi.hi + hi.lo + lo.hi
+      float sacc[2][NN][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nn = 0; nn < NN; ++nn)
+#pragma unroll
+          for (int e4 = 0; e4 < 4; ++e4) sacc[mt][nn][e4] = 0.f;
+#pragma unroll
+      for (int bb = 0; bb < NB; ++bb) {
+        const uint32_t blk = smem_u32(st) + (uint32_t)(warp * RW + 32 * bb) * 128u;
+        float dacc[2][NN][4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nn = 0; nn < NN; ++nn)
+#pragma unroll
+            for (int e4 = 0; e4 < 4; ++e4) dacc[mt][nn][e4] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            const int mj = lane >> 3;
+            const uint32_t off = h16_off(16 * ks + (lane & 7) + 8 * (mj >> 1), 2 * mt + (mj & 1));
+            uint32_t ah[4], al[4];
+            ldsm_x4_t(blk + off, ah);
+            ldsm_x4_t(blk + 2048u + off, al);
+#pragma unroll
+            for (int nn = 0; nn < NN; ++nn) {
+              mma16816(dacc[mt][nn], ah, wfh[bb][ks][nn][0], wfh[bb][ks][nn][1]);
+              mma16816(dacc[mt][nn], ah, wfl[bb][ks][nn][0], wfl[bb][ks][nn][1]);
+              mma16816(dacc[mt][nn], al, wfh[bb][ks][nn][0], wfh[bb][ks][nn][1]);
+            }
+          }
+        const float f = xsi[bb] * wsi;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nn = 0; nn < NN; ++nn)
+#pragma unroll
+            for (int e4 = 0; e4 < 4; ++e4) sacc[mt][nn][e4] = fmaf(dacc[mt][nn][e4], f, sacc[mt][nn][e4]);
+      }
+      // fragment (col 16 mt + fg (+8 for e4 >= 2), rank 8 nn + 2 ft + (e4 & 1)) -> Sred[w][rank][col]
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nn = 0; nn < NN; ++nn)
+#pragma unroll
+          for (int e4 = 0; e4 < 4; ++e4)
+            Sred[(warp * RS + 8 * nn + 2 * ft + (e4 & 1)) * 32 + 16 * mt + fg + 8 * (e4 >> 1)] = sacc[mt][nn][e4];
+      asm volatile("bar.sync 1, %0;" ::"r"(NBAR) : "memory");
+    }
+#endif
     // ---- H update: thread handles (k, c) for k in {kt, kt+4}, c = ct
+    float hmax = 0.f;
 #pragma unroll
     for (int hh = 0; hh < HH; ++hh) {
       const int kt = (tid >> 5) + NW * hh, ct = tid & 31;
       const int64_t col = jt + ct;
       const float hkc = *reinterpret_cast<const float*>(st + XB + kt * 128 + (((ct >> 2) ^ kt) << 4) + (ct & 3) * 4);
       float hn;
-      if (do_update) {
+      if constexpr (UPD) {
         float S = 0.0f;
 #pragma unroll
         for (int w = 0; w < NW; ++w) S += Sred[(w * 8 + kt) * 32 + ct];
@@ -1005,7 +1198,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 #pragma unroll
         for (int l = 0; l < 8; ++l)
           hl[l] = *reinterpret_cast<const float*>(st + XB + l * 128 + (((ct >> 2) ^ l) << 4) + (ct & 3) * 4);
-        if (bcd) {
+        if constexpr (BCD) {
 #pragma unroll
           for (int l = 0; l < 8; ++l) hl[l] *= bsh[l];
         }
@@ -1015,7 +1208,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
           e0 = fmaf(Gs[kt * 8 + l], hl[l], e0);
           e1 = fmaf(Gs[kt * 8 + l + 1], hl[l + 1], e1);
         }
-        if (bcd)  // prox-linear step (Alg. 3 l.14) on H_m = diag(sH) H_m stored
+        if constexpr (BCD)  // prox-linear step (Alg. 3 l.14) on H_m = diag(sH) H_m stored
           hn = fmaxf(0.f, fmaf(-((e0 + e1) - S), binvL, hkc * bsh[kt]));
         else
           hn = mu_q(hkc, S, e0 + e1, eps);
@@ -1024,12 +1217,20 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       } else {
         hn = (kt < r && col < n) ? hkc : 0.0f;
       }
-      if (do_acc) Hn[hnc_idx(ct, kt)] = hn;
+      if constexpr (ACC) Hn[hnc_idx(ct, kt)] = hn;
+      hmax = fmaxf(hmax, fabsf(hn));
     }
-    asm volatile("bar.sync 1, %0;" ::"r"(NBAR) : "memory");
+#ifndef NTT_FC_FFMA
+    if constexpr (ACC) {
+      const float wm = warp_max(hmax);
+      if (lane == 0) hmx[warp] = wm;
+    }
+#endif
 
-    if (do_acc) {
+    if constexpr (ACC) {
+      asm volatile("bar.sync 1, %0;" ::"r"(NBAR) : "memory");
       // ---- phase B
+#ifdef NTT_FC_FFMA
       {
         float qa[QR];
 #pragma unroll
@@ -1101,16 +1302,96 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
           accd[h][v] += (double)(keep + __shfl_xor_sync(0xffffffffu, send, 8));
         }
       }
+#else
+      {  // Q rows QR w + qq over this lane's 8-column slice (FFMA; r x r)
+        float qa[QR];
+#pragma unroll
+        for (int qq = 0; qq < QR; ++qq) qa[qq] = 0.f;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const float* src = Hn + hnc_idx(8 * cs + t, 0);
+          const float hr = src[rb];
+#pragma unroll
+          for (int qq = 0; qq < QR; ++qq) qa[qq] = fmaf(src[QR * warp + qq], hr, qa[qq]);
+        }
+#pragma unroll
+        for (int qq = 0; qq < QR; ++qq) qd[qq] += (double)qa[qq];
+      }
+      // P (this warp's rows x R) += X Hn^T by mma.sync: A = X (ldmatrix of the fp16 parts),
+      // B = Hn^T split with the tile's power-of-two scale (max |Hn| from the H update)
+      float hm = hmx[0];
+#pragma unroll
+      for (int w = 1; w < NW; ++w) hm = fmaxf(hm, hmx[w]);
+      const float2 hsc = pow2_scale(hm);
+      uint32_t bh[2][NN][2], bl[2][NN][2];
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+        for (int nn = 0; nn < NN; ++nn) {
+          const int c0 = 16 * kk + 2 * ft, kr = 8 * nn + fg;
+          split2(Hn[hnc_idx(c0, kr)], Hn[hnc_idx(c0 + 1, kr)], hsc.x, bh[kk][nn][0], bl[kk][nn][0]);
+          split2(Hn[hnc_idx(c0 + 8, kr)], Hn[hnc_idx(c0 + 9, kr)], hsc.x, bh[kk][nn][1], bl[kk][nn][1]);
+        }
+#pragma unroll
+      for (int bb = 0; bb < NB; ++bb) {
+        const uint32_t blk = smem_u32(st) + (uint32_t)(warp * RW + 32 * bb) * 128u;
+        const float f = xsi[bb] * hsc.y;
+#pragma unroll
+        for (int mh = 0; mh < 2; ++mh) {
+          float d[NN][4];
+#pragma unroll
+          for (int nn = 0; nn < NN; ++nn)
+#pragma unroll
+            for (int e4 = 0; e4 < 4; ++e4) d[nn][e4] = 0.f;
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            const int mj = lane >> 3;
+            const uint32_t off = h16_off(16 * mh + (lane & 7) + 8 * (mj & 1), 2 * kk + (mj >> 1));
+            uint32_t ah[4], al[4];
+            ldsm_x4(blk + off, ah);
+            ldsm_x4(blk + 2048u + off, al);
+#pragma unroll
+            for (int nn = 0; nn < NN; ++nn) {
+              mma16816(d[nn], ah, bh[kk][nn][0], bh[kk][nn][1]);
+              mma16816(d[nn], ah, bl[kk][nn][0], bl[kk][nn][1]);
+              mma16816(d[nn], al, bh[kk][nn][0], bh[kk][nn][1]);
+            }
+          }
+#pragma unroll
+          for (int nn = 0; nn < NN; ++nn)
+#pragma unroll
+            for (int e4 = 0; e4 < 4; ++e4) pacc[bb][mh][nn][e4] = fmaf(d[nn][e4], f, pacc[bb][mh][nn][e4]);
+        }
+      }
+      if (++since_flush == 8) {  // two-level accumulation: fp32 over <= 8 tiles, then fp64
+        since_flush = 0;
+#pragma unroll
+        for (int bb = 0; bb < NB; ++bb)
+#pragma unroll
+          for (int mh = 0; mh < 2; ++mh)
+#pragma unroll
+            for (int nn = 0; nn < NN; ++nn)
+#pragma unroll
+              for (int e4 = 0; e4 < 4; ++e4) {
+                paccd[bb][mh][nn][e4] += (double)pacc[bb][mh][nn][e4];
+                pacc[bb][mh][nn][e4] = 0.f;
+              }
+      }
+#endif
+    } else if constexpr (UPD) {
+      // no phase B: the next tile's phase A must not overwrite Sred while it is still read
+      asm volatile("bar.sync 1, %0;" ::"r"(NBAR) : "memory");
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 
-  if (do_acc) {
-  // P: lane holds flat f = u*8 + k in [8 cs, 8 cs + 8) of sub-chunk h, rows warp*RW + 32h + rb + 8u
+  if constexpr (ACC) {
   const int mr = m * r, rr = r * r;
   double* Pb = persist ? pa.part + b * (mr + rr) : Ppart + b * mr;
   double* Qb = persist ? pa.part + b * (mr + rr) + mr : Qpart + b * rr;
+#ifdef NTT_FC_FFMA
+  // P: lane holds flat f = u*8 + k in [8 cs, 8 cs + 8) of sub-chunk h, rows warp*RW + 32h + rb + 8u
 #pragma unroll
   for (int h = 0; h < NCH; ++h)
 #pragma unroll
@@ -1120,6 +1401,20 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       const int row = warp * RW + 32 * h + rb + 8 * u;
       if (row < m && k < r) Pb[row * r + k] = accd[h][v];
     }
+#else
+  // P fragment: rows warp RW + 32 bb + 16 mh + fg (+ 8), ranks 8 nn + 2 ft (+ 1)
+#pragma unroll
+  for (int bb = 0; bb < NB; ++bb)
+#pragma unroll
+    for (int mh = 0; mh < 2; ++mh)
+#pragma unroll
+      for (int nn = 0; nn < NN; ++nn)
+#pragma unroll
+        for (int e4 = 0; e4 < 4; ++e4) {
+          const int row = warp * RW + 32 * bb + 16 * mh + fg + 8 * (e4 >> 1), k = 8 * nn + 2 * ft + (e4 & 1);
+          if (row < m && k < r) Pb[row * r + k] = paccd[bb][mh][nn][e4] + (double)pacc[bb][mh][nn][e4];
+        }
+#endif
   // Q rows QR w + qq, column rb: sum the 4 column slices
 #pragma unroll
   for (int qq = 0; qq < QR; ++qq) {
@@ -1128,9 +1423,15 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     if (cs == 0 && rb < r && QR * warp + qq < r) Qb[(QR * warp + qq) * r + rb] = qd[qq];
   }
   }
+  };  // pass_tiles
+  using T_ = std::true_type;
+  using F_ = std::false_type;
+  if (!do_update) pass_tiles(F_{}, T_{}, F_{});
+  else if (do_acc) bcd ? pass_tiles(T_{}, T_{}, T_{}) : pass_tiles(T_{}, T_{}, F_{});
+  else bcd ? pass_tiles(T_{}, F_{}, T_{}) : pass_tiles(T_{}, F_{}, F_{});
   }  // consumer warps
   if (!persist || !do_acc) break;
-  persist_step(pa, epoch, m, r, eps, Wc, Gs, reinterpret_cast<double*>(stages), it, WPAIR);
+  persist_step(pa, epoch, m, r, eps, Wc, Gs, reinterpret_cast<double*>(stages), it, false);
   }  // passes
 }
 
@@ -1138,17 +1439,9 @@ size_t fixed_bytes_c(int MP, int NW) {
   return (size_t)NW * 8 * 32 * 4 + 256 + HNC_FLOATS * 4 + (size_t)MP * 8 * 4 + 2 * 16 * 8 + 1024;
 }
 
-bool c_one_cta() {  // experiment: NTT_C_1CTA=1 runs the 4-warp variant at 1 CTA / SM with a deeper ring
-  static const bool on = [] {
-    const char* e = getenv("NTT_C_1CTA");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
 int stages_c(int MP, int NW) {
   const size_t SB = (size_t)MP * 128 + 1024;
-  const size_t budget = (NW == 4 && !c_one_cta()) ? (size_t)SMEM_C : (size_t)SMEM_BUDGET;  // 2 CTAs / SM or 1
+  const size_t budget = NW == 4 ? (size_t)SMEM_C : (size_t)SMEM_BUDGET;  // 2 CTAs / SM (4 warps) or 1 (8 warps)
   int ns = (int)((budget - fixed_bytes_c(MP, NW)) / SB);
   return ns > 12 ? 12 : ns;
 }
@@ -1183,336 +1476,7 @@ cudaError_t launch_c(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_
                            nG, eps, H, Ppart, Qpart, mode, ns, evict_first, pa);
 }
 
-// 8 consumer warps, 1 CTA / SM, W rows in registers for m > 128 (NTT_C_NW=4: the 2-CTA variant)
-int c_nw(int MP) {
-  static const int env = [] {
-    const char* e = getenv("NTT_C_NW");
-    return e ? atoi(e) : 4;  // the 8-warp variant measured slower (502 vs 362 us/iter, step 2)
-  }();
-  return (MP == 256 && env == 8) ? 8 : 4;
-}
 
-// ===========================================================================
-// Variant WC: warp-owned 32-column tiles for 40 < m <= 256 (rank padded to 8),
-// no CTA barriers in the loop.  6 consumer warps (<= 2 per SMSP, 255 regs) + 1
-// TMA warp; each warp owns `dpw` ring stages (stage = tile's warp * dpw +
-// round % dpw), so every warp waits only on rounds it consumed itself.
-//   phase A  lanes (q: columns 4q..4q+3, g: ranks 2g, 2g+1) stream all MP rows:
-//            X by 128-bit loads, W as row pairs (one 128-bit broadcast per 2 rows)
-//   H update lane forms E = G H and Hn for its 2 ranks x 4 columns; 128-bit
-//            coalesced stores; Hn into the warp's transposed smem tile
-//   phase B  32-row chunks, lanes (rb, cs: 8-column slice), reduce-scatter over
-//            the slices, per-lane fp32 accumulators for ALL rows (8 values per
-//            chunk) flushed every 32 tiles into the warp's private fp64 global
-//            partial (no atomics: deterministic); Q = Hn Hn^T likewise.
-// ===========================================================================
-constexpr int NWW = 6;
-constexpr int NTW = (NWW + 1) * 32;
-constexpr int WC_FLUSH = 32;
-
-template <int MP>
-__global__ void __launch_bounds__(NTW, 1)
-k_fused_wc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmH, int m, int64_t n, int r,
-           const float* __restrict__ W, const double* __restrict__ Gpart, int nG, float eps, float* __restrict__ H,
-           double* __restrict__ Ppart, double* __restrict__ Qpart, int mode, int dpw, int evict_first) {
-  extern __shared__ unsigned char smem_raw[];
-  // keep the shared address space visible to the compiler (LDS/STS, not generic LD/ST)
-  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  constexpr int NCH = MP / 32;
-  constexpr uint32_t XB = MP * 128u;
-  constexpr uint32_t SB = XB + 1024u;
-  const int ns = NWW * dpw;
-  unsigned char* stages = smem;
-  float* Wp = reinterpret_cast<float*>(smem + (size_t)ns * SB);  // [MP/2][4 g][4]: W row pairs
-  float* Gs = Wp + MP * 8;                                         // 8 x 8
-  float* HnAll = Gs + 64;                                          // NWW x HNC_FLOATS
-  uint64_t* full = reinterpret_cast<uint64_t*>(HnAll + NWW * HNC_FLOATS);
-  uint64_t* empty = full + ns;
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const bool do_update = (mode & kFusedUpdate) != 0;
-  const bool do_acc = (mode & kFusedAcc) != 0;
-  if (do_update) {
-    const int rr = r * r;
-    for (int e = tid; e < 64; e += NTW) {
-      int k = e >> 3, l = e & 7;
-      double sum = 0.0;
-      if (k < r && l < r)
-        for (int bq = 0; bq < nG; ++bq) sum += Gpart[(int64_t)bq * rr + k * r + l];
-      Gs[e] = (float)sum;
-    }
-  }
-  for (int e = tid; e < MP * 8; e += NTW) {
-    // Wp[(i/2)*16 + g*4 + (i&1)*2 + t] = W[i][2g + t]
-    const int ip = e >> 4, g = (e >> 2) & 3, w2 = e & 3;
-    const int i = 2 * ip + (w2 >> 1), k = 2 * g + (w2 & 1);
-    Wp[e] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
-  }
-  if (tid == 0) {
-    for (int s = 0; s < ns; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  const int64_t ntiles = (n + BNC - 1) / BNC;
-  const int64_t b = blockIdx.x;
-  const int64_t J = (ntiles > b) ? (ntiles - b + gridDim.x - 1) / gridDim.x : 0;
-
-  if (warp == NWW) {
-    if (lane == 0) {
-      uint64_t policy;
-      if (evict_first)
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-      else
-        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
-      for (int64_t j = 0; j < J; ++j) {
-        const int64_t rnd = j / NWW;
-        const int s = (int)(j % NWW) * dpw + (int)(rnd % dpw);
-        const uint32_t ph = (uint32_t)((rnd / dpw) & 1);
-        MBAR_WAIT(&empty[s], ph ^ 1u, 5, j);
-        mbar_expect_tx(&full[s], SB);
-        const int col0 = (int)((b + j * gridDim.x) * BNC);
-        unsigned char* st = stages + (size_t)s * SB;
-        tma_load_2d(st, &tmX, col0, 0, &full[s], policy);
-        tma_load_2d(st + XB, &tmH, col0, 0, &full[s], policy);
-      }
-    }
-    return;
-  }
-
-  float* Hw = HnAll + warp * HNC_FLOATS;
-  const int q = lane & 7, g = lane >> 3;    // phase A / H update
-  const int rb = lane & 7, cs = lane >> 3;  // phase B
-  const bool h1 = (lane >> 4) & 1, h0 = (lane >> 3) & 1;
-  float accf[NCH][8];
-  float qf[8];
-#pragma unroll
-  for (int h = 0; h < NCH; ++h)
-#pragma unroll
-    for (int v = 0; v < 8; ++v) accf[h][v] = 0.f;
-#pragma unroll
-  for (int v = 0; v < 8; ++v) qf[v] = 0.f;
-  const int mr = m * r, rr = r * r;
-  const int64_t slot = b * NWW + warp;  // this warp's private partial
-  int nflush = 0, since = 0;
-  // flush the fp32 accumulators into the warp's fp64 partial (first flush writes)
-  auto flush = [&]() {
-#pragma unroll
-    for (int h = 0; h < NCH; ++h)
-#pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        const int f = 8 * cs + v;  // flat u*8 + k within the chunk
-        const int u = f >> 3, k = f & 7;
-        const int row = 32 * h + rb + 8 * u;
-        if (row < m && k < r) {
-          double* dst = Ppart + slot * mr + row * r + k;
-          *dst = (nflush ? *dst : 0.0) + (double)accf[h][v];
-        }
-        accf[h][v] = 0.f;
-      }
-    // Q[rb][l]: sum the 4 column-slice lanes
-#pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      float t = qf[v];
-      t += __shfl_xor_sync(0xffffffffu, t, 16);
-      t += __shfl_xor_sync(0xffffffffu, t, 8);
-      if (cs == 0 && rb < r && v < r) {
-        double* dst = Qpart + slot * rr + rb * r + v;
-        *dst = (nflush ? *dst : 0.0) + (double)t;
-      }
-      qf[v] = 0.f;
-    }
-    ++nflush;
-    since = 0;
-  };
-
-  for (int64_t j = warp; j < J; j += NWW) {
-    const int64_t rnd = j / NWW;
-    const int s = warp * dpw + (int)(rnd % dpw);
-    const uint32_t ph = (uint32_t)((rnd / dpw) & 1);
-    MBAR_WAIT(&full[s], ph, 6, j);
-    const unsigned char* st = stages + (size_t)s * SB;
-    const int64_t jt = (b + j * gridDim.x) * BNC;
-    const int64_t c0 = jt + 4 * q;
-
-    // ---- phase A + H update (lane: ranks 2g, 2g+1 x columns 4q..4q+3)
-    // (rows 2g, 2g+1 of the H tile are loaded separately: indexing the hv
-    //  register array with the lane-dependent g would spill it to local memory)
-    float hk[2][4];
-#pragma unroll
-    for (int kk = 0; kk < 2; ++kk) {
-      const int k = 2 * g + kk;
-      const float4 t4 = lds128(st + XB + k * 128 + ((q ^ k) << 4));
-      hk[kk][0] = t4.x; hk[kk][1] = t4.y; hk[kk][2] = t4.z; hk[kk][3] = t4.w;
-    }
-    float hn[2][4];
-    if (do_update) {
-      float2 sa = f2(0.f, 0.f), sb = f2(0.f, 0.f), sc = f2(0.f, 0.f), sd = f2(0.f, 0.f);
-#pragma unroll 4
-      for (int ip = 0; ip < MP / 2; ++ip) {
-        const int i = 2 * ip;
-        const float4 x0 = lds128(st + i * 128 + ((q ^ (i & 7)) << 4));
-        const float4 x1 = lds128(st + (i + 1) * 128 + ((q ^ ((i + 1) & 7)) << 4));
-        const float4 wv = *reinterpret_cast<const float4*>(Wp + ip * 16 + g * 4);
-        sa = __ffma2_rn(bc(wv.x), f2(x0.x, x0.y), sa);
-        sb = __ffma2_rn(bc(wv.x), f2(x0.z, x0.w), sb);
-        sc = __ffma2_rn(bc(wv.y), f2(x0.x, x0.y), sc);
-        sd = __ffma2_rn(bc(wv.y), f2(x0.z, x0.w), sd);
-        sa = __ffma2_rn(bc(wv.z), f2(x1.x, x1.y), sa);
-        sb = __ffma2_rn(bc(wv.z), f2(x1.z, x1.w), sb);
-        sc = __ffma2_rn(bc(wv.w), f2(x1.x, x1.y), sc);
-        sd = __ffma2_rn(bc(wv.w), f2(x1.z, x1.w), sd);
-      }
-      const float S[2][4] = {{sa.x, sa.y, sb.x, sb.y}, {sc.x, sc.y, sd.x, sd.y}};
-      float hv[8][4];
-#pragma unroll
-      for (int l = 0; l < 8; ++l) {
-        const float4 t4 = lds128(st + XB + l * 128 + ((q ^ l) << 4));
-        hv[l][0] = t4.x; hv[l][1] = t4.y; hv[l][2] = t4.z; hv[l][3] = t4.w;
-      }
-#pragma unroll
-      for (int kk = 0; kk < 2; ++kk) {
-        const int k = 2 * g + kk;
-        float gk[8];
-        *reinterpret_cast<float4*>(gk) = *reinterpret_cast<const float4*>(Gs + k * 8);
-        *reinterpret_cast<float4*>(gk + 4) = *reinterpret_cast<const float4*>(Gs + k * 8 + 4);
-        float2 e01 = f2(0.f, 0.f), e23 = f2(0.f, 0.f);
-#pragma unroll
-        for (int l = 0; l < 8; ++l) {
-          e01 = __ffma2_rn(bc(gk[l]), f2(hv[l][0], hv[l][1]), e01);
-          e23 = __ffma2_rn(bc(gk[l]), f2(hv[l][2], hv[l][3]), e23);
-        }
-        const float e[4] = {e01.x, e01.y, e23.x, e23.y};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          float v = mu_q(hk[kk][t], S[kk][t], e[t], eps);
-          if (k >= r || c0 + t >= n) v = 0.f;
-          hn[kk][t] = v;
-        }
-        if (k < r) {
-          if (c0 + 3 < n) {
-            *reinterpret_cast<float4*>(H + (int64_t)k * n + c0) = make_float4(hn[kk][0], hn[kk][1], hn[kk][2], hn[kk][3]);
-          } else {
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-              if (c0 + t < n) H[(int64_t)k * n + c0 + t] = hn[kk][t];
-          }
-        }
-      }
-    } else {
-#pragma unroll
-      for (int kk = 0; kk < 2; ++kk)
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int k = 2 * g + kk;
-          hn[kk][t] = (k < r && c0 + t < n) ? hk[kk][t] : 0.f;
-        }
-    }
-
-    if (do_acc) {
-#pragma unroll
-      for (int t = 0; t < 4; ++t)
-        *reinterpret_cast<float2*>(Hw + hnc_idx(4 * q + t, 2 * g)) = f2(hn[0][t], hn[1][t]);
-      __syncwarp();
-      // ---- Q rows rb over this lane's 8 columns
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const float* src = Hw + hnc_idx(8 * cs + t, 0);
-        const float4 a = *reinterpret_cast<const float4*>(src);
-        const float4 bq = *reinterpret_cast<const float4*>(src + 4);
-        const float hr = src[rb];
-        qf[0] = fmaf(hr, a.x, qf[0]); qf[1] = fmaf(hr, a.y, qf[1]);
-        qf[2] = fmaf(hr, a.z, qf[2]); qf[3] = fmaf(hr, a.w, qf[3]);
-        qf[4] = fmaf(hr, bq.x, qf[4]); qf[5] = fmaf(hr, bq.y, qf[5]);
-        qf[6] = fmaf(hr, bq.z, qf[6]); qf[7] = fmaf(hr, bq.w, qf[7]);
-      }
-      // ---- phase B: P rows in 32-row chunks
-#pragma unroll
-      for (int h = 0; h < NCH; ++h) {
-        float2 acc[16];
-#pragma unroll
-        for (int v = 0; v < 16; ++v) acc[v] = f2(0.f, 0.f);
-#pragma unroll
-        for (int s4 = 0; s4 < 2; ++s4) {
-          float2 hq2[4][4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const float* src = Hw + hnc_idx(8 * cs + 4 * s4 + t, 0);
-            const float4 a = *reinterpret_cast<const float4*>(src);
-            const float4 bq = *reinterpret_cast<const float4*>(src + 4);
-            hq2[t][0] = f2(a.x, a.y);
-            hq2[t][1] = f2(a.z, a.w);
-            hq2[t][2] = f2(bq.x, bq.y);
-            hq2[t][3] = f2(bq.z, bq.w);
-          }
-          float xs[4][4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int i = 32 * h + rb + 8 * u;
-            const float4 x = lds128(st + i * 128 + (((2 * cs + s4) ^ rb) << 4));
-            xs[u][0] = x.x; xs[u][1] = x.y; xs[u][2] = x.z; xs[u][3] = x.w;
-          }
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-              for (int kp = 0; kp < 4; ++kp)
-                acc[u * 4 + kp] = __ffma2_rn(bc(xs[u][t]), hq2[t][kp], acc[u * 4 + kp]);
-        }
-        float a1[32];
-#pragma unroll
-        for (int v = 0; v < 16; ++v) {
-          a1[2 * v] = acc[v].x;
-          a1[2 * v + 1] = acc[v].y;
-        }
-        float a2[16];
-#pragma unroll
-        for (int v = 0; v < 16; ++v) {
-          const float send = h1 ? a1[v] : a1[v + 16];
-          const float keep = h1 ? a1[v + 16] : a1[v];
-          a2[v] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-        }
-#pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          const float send = h0 ? a2[v] : a2[v + 8];
-          const float keep = h0 ? a2[v + 8] : a2[v];
-          accf[h][v] += keep + __shfl_xor_sync(0xffffffffu, send, 8);
-        }
-      }
-      if (++since == WC_FLUSH) flush();
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-  if (do_acc) flush();  // final (also writes zeros for warps without tiles)
-}
-
-size_t fixed_bytes_wc(int MP) {
-  return (size_t)MP * 8 * 4 + 256 + (size_t)NWW * HNC_FLOATS * 4 + 2 * 24 * 8 + 1024;
-}
-
-int dpw_wc(int MP) {
-  const size_t SB = (size_t)MP * 128 + 1024;
-  int d = (int)((SMEM_BUDGET - fixed_bytes_wc(MP)) / (SB * NWW));
-  return d > 4 ? 4 : d;
-}
-
-template <int MP>
-cudaError_t launch_wc(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_t n, int r, const float* W,
-                      const double* Gpart, int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
-                      int evict_first, cudaStream_t st) {
-  const int dpw = dpw_wc(MP);
-  const size_t SB = (size_t)MP * 128 + 1024;
-  const size_t smem = (size_t)NWW * dpw * SB + fixed_bytes_wc(MP);
-  cudaError_t e = cudaFuncSetAttribute(k_fused_wc<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  k_fused_wc<MP><<<grid, NTW, smem, st>>>(mx, mh, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, dpw, evict_first);
-  return cudaGetLastError();
-}
 
 // ---------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -1708,19 +1672,9 @@ bool fused_supported(int64_t m, int64_t n, int r, int64_t ldx, const void* X, co
   return true;
 }
 
-// Variant WC (warp-owned m <= 256 tiles) is kept as an experiment (NTT_FUSED_WC=1);
-// the CTA-cooperative variant C measured faster on config 3 step 2 (DESIGN.md s.6).
-bool use_wc() {
-  static const bool on = [] {
-    const char* e = getenv("NTT_FUSED_WC");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
 int fused_partials(int64_t m, int64_t n, int r, int num_sms) {
   const int g = fused_grid(m, n, r, num_sms);
-  return (m > 40 && use_wc()) ? g * NWW : g;
+  return g;
 }
 
 int fused_grid(int64_t m, int64_t n, int r, int num_sms) {
@@ -1730,15 +1684,16 @@ int fused_grid(int64_t m, int64_t n, int r, int num_sms) {
     return (int)(ntiles < num_sms ? ntiles : num_sms);
   }
   int64_t ntiles = (n + BNC - 1) / BNC;
-  if (use_wc()) {  // variant WC: one CTA per SM, 6 warp-owned tiles in flight
-    int64_t need = (ntiles + NWW - 1) / NWW;
-    return (int)(need < num_sms ? (need < 1 ? 1 : need) : num_sms);
-  }
-  const int cps = (c_nw(m <= 128 ? 128 : 256) == 8 || c_one_cta()) ? 1 : 2;  // variant C: CTAs per SM
+  const int cps = 2;  // variant C: CTAs per SM (4 consumer warps each; one CTA of 8 warps measured slower)
   return (int)(ntiles < cps * num_sms ? ntiles : cps * num_sms);
 }
 
 size_t fused_scratch_bytes(int64_t, int64_t, int, int) { return 0; }
+
+size_t fused_x16_bytes(int64_t m, int64_t n) {
+  if (m <= 40) return 0;
+  return (size_t)((n + BNC - 1) / BNC) * (size_t)(((m + 31) / 32) * 4096 + 128);
+}
 void fused_destroy(FusedCtx&) {}
 
 struct FusedPlan {
@@ -1790,18 +1745,7 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
                          int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
                          cudaStream_t st, const PersistArgs* pap) {
   const PersistArgs pa = pap ? *pap : PersistArgs{0, nullptr, nullptr, nullptr, nullptr, nullptr};
-  if (pa.iters > 0 && m > 40 && use_wc()) return cudaErrorNotSupported;
   const int evict_first = ((double)m * (double)n * 4.0 > 48e6) ? 1 : 0;
-  if (m > 40 && use_wc()) {
-    const int MPc = m <= 128 ? 128 : 256;
-    CUtensorMap mx, mh;
-    cudaError_t e = make_map(&mx, X, (uint64_t)n, (uint64_t)m, (uint64_t)ldx, (uint32_t)MPc);
-    if (e != cudaSuccess) return e;
-    e = make_map(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u);
-    if (e != cudaSuccess) return e;
-    if (MPc == 128) return launch_wc<128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st);
-    return launch_wc<256>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, st);
-  }
   if (m > 40) {
     const int MPc = m <= 128 ? 128 : 256;
     CUtensorMap mx, mh;
@@ -1810,8 +1754,6 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
     e = make_map(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u);
     if (e != cudaSuccess) return e;
     if (MPc == 128) return launch_c<128, 4>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
-    if (c_nw(256) == 8)
-      return launch_c<256, 8>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
     return launch_c<256, 4>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
   }
   const int ux = ux_for(m);

@@ -15,7 +15,6 @@ bool fused_supported(int64_t m, int64_t n, int r, int64_t ldx, const void* X, co
 int fused_grid(int64_t m, int64_t n, int r, int num_sms);
 // number of (P, Q) partial slots one fused pass writes (>= grid)
 int fused_partials(int64_t m, int64_t n, int r, int num_sms);
-bool use_wc();
 size_t fused_scratch_bytes(int64_t m, int64_t n, int r, int grid);
 void fused_destroy(FusedCtx& c);
 
@@ -45,7 +44,13 @@ struct PersistArgs {
   // with bcdRole: H_m = diag(bcdS[0..r)) B[1 - role] - diag(bcdS[64..64+r)) B[role], B = (Hout,
   // Hout2), formed inside the pass (k_fused with staged H only; see fused_fold_ok)
   bool bcdFold = false;
+  // persistent k_fused_c (40 < m <= 256): X as fp16 hi / lo parts, written by the prologue pass and
+  // streamed by every later pass instead of converting the fp32 tile again (fused_x16_bytes;
+  // nullable: every pass converts)
+  unsigned char* x16 = nullptr;
 };
+// bytes of the PersistArgs::x16 cache for an m x n X (0 when m <= 40)
+size_t fused_x16_bytes(int64_t m, int64_t n);
 
 // One pass over X (m x n, row stride ldx) with the current W (m x r) and
 // G = sum_c Gpart[c] (nG partials).  mode = kFusedAcc alone is the prologue

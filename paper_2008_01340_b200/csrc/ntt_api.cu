@@ -301,13 +301,11 @@ struct MuPlan {
   int nwup;       // W-update CTAs
   int fgrid;      // fused kernel CTAs
   int fparts;     // fused kernel partial slots
-  bool small = false;  // m <= 8: register-resident pass (mu_small.cu)
-  int sgrid = 0;       // its CTAs (= partial slots)
   bool tc;        // tensor-core 2-pass path (mu_tc.cu) for tall / square X
   TcPlan tp;
   bool persist;   // fused path as one persistent cooperative launch per call
   bool tiny;      // whole MU loop in one CTA from shared memory (mu_tiny.cu)
-  size_t off_P, off_Q, off_G, off_S, off_tc, off_pp, off_red, off_ctr, bytes;
+  size_t off_P, off_Q, off_G, off_S, off_tc, off_pp, off_red, off_ctr, off_x16, bytes;
 };
 
 // dist: a handle from ntt_create_dist* (any number of ranks, 1 included) -- its MU runs
@@ -327,15 +325,6 @@ MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, bool dist) {
   p.nwup = wupdate_ctas(m, r);
   p.fgrid = fused_grid(m, n, r, num_sms);
   p.fparts = fused_partials(m, n, r, num_sms);
-  // m <= 8: the register-resident pass of mu_small.cu (opt-in, NTT_SMALL=1: on config 4
-  // step 1 it ties the persistent warp-tile kernel at 3.27 TB/s -- both are held by an
-  // uneven DRAM channel load, DESIGN.md s.6 -- and adds a W-update launch per iteration)
-  {
-    const char* se = getenv("NTT_SMALL");
-    p.small = small_supported(m, n, r, n, nullptr, nullptr) && se && se[0] == '1';
-  }
-  p.sgrid = small_grid(n, num_sms);
-  if (p.small) p.fparts = std::max(p.fparts, p.sgrid);
   int64_t nP = std::max<int64_t>({(int64_t)p.xp.ncs, p.acc ? p.hgrid : 0, (int64_t)p.fparts, 1});
   int64_t nQ = std::max<int64_t>({(int64_t)p.qp.ncs, p.acc ? p.hgrid : 0, (int64_t)p.fparts, 1});
   int64_t nG = std::max<int64_t>({(int64_t)p.nwup, (int64_t)wupdate2_ctas(m, r), 1});
@@ -355,7 +344,7 @@ MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, bool dist) {
     p.tp = plan_tc(m, n, r, num_sms);
     o = align_up(o + p.tp.bytes);
   }
-  p.persist = !dist && p.fused && !use_wc() && !getenv("NTT_NO_PERSIST");
+  p.persist = !dist && p.fused && !getenv("NTT_NO_PERSIST");
   p.tiny = !dist && tiny_supported(m, n, r) && !getenv("NTT_NO_TINY");
   p.off_pp = o;
   if (p.persist) o = align_up(o + sizeof(double) * (size_t)p.fgrid * (size_t)(m * r + r * r));
@@ -363,6 +352,8 @@ MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, bool dist) {
   if (p.persist) o = align_up(o + sizeof(double) * (size_t)(m * r + r * r));
   p.off_ctr = o;
   if (p.persist) o = align_up(o + 64);
+  p.off_x16 = o;  // fp16 hi / lo copy of X for the persistent k_fused_c (m > 40)
+  if (p.persist) o = align_up(o + fused_x16_bytes(m, n));
   p.bytes = o;
   return p;
 }
@@ -394,29 +385,6 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
             launch_tiny(X, ldx, m, n, r, iters, eps, W, H, st));
     return NTT_OK;
   }
-  if (p.small && small_supported(m, n, r, ldx, X, H)) {
-    // 1-pass with the register-resident small-m pass: prologue P0, Q0; then per iteration
-    // W update (reduces the partials) -> pass (H update + next P, Q)
-    const int fg = p.sgrid;
-    const int nG = wupdate2_ctas(m, r);
-    PLAUNCH(h, 1, 4.0 * (double)(m + r) * (double)n,
-            launch_small(X, ldx, m, n, r, W, nullptr, 0, eps, H, Ppart, Qpart, kFusedAcc, fg, st));
-    for (int it = 0; it < iters; ++it) {
-      if (dist) {
-        ntt_status s = dist_reduce(h, p, Ppart, fg, Qpart, fg, red);
-        if (s) return s;
-        PLAUNCH(h, 2, 8.0 * (double)(2 * m * r + r * r), launch_wupdate2(W, m, r, red, 1, red + m * r, 1, eps, Gpart, st));
-      } else {
-        PLAUNCH(h, 2, 8.0 * ((double)fg * (m * r + r * r) + m * r),
-                launch_wupdate2(W, m, r, Ppart, fg, Qpart, fg, eps, Gpart, st));
-      }
-      const int mode = kFusedUpdate | ((it + 1 < iters) ? kFusedAcc : 0);
-      PLAUNCH(h, 0, 4.0 * (double)(m + 2 * r) * (double)n,
-              launch_small(X, ldx, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, fg, st));
-      if (dev_trace) LAUNCH(h, launch_objective(X, ldx, m, n, W, H, r, dev_trace + (int64_t)it * nobj, st));
-    }
-    return NTT_OK;
-  }
   if (p.fused && p.persist && !dist && !dev_trace && fused_supported(m, n, r, ldx, X, H)) {
     // whole MU loop of this call in one cooperative launch (mu_fused.cu persist_step)
     PersistArgs pa;
@@ -426,6 +394,7 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
     pa.ctr = reinterpret_cast<unsigned*>(scratch + p.off_ctr);
     pa.Wout = W;
     pa.trace = h->ptrace;  // diagnostics (NTT_PERSIST_TRACE), else null
+    pa.x16 = fused_x16_bytes(m, n) ? reinterpret_cast<unsigned char*>(scratch + p.off_x16) : nullptr;
     CU(h, cudaMemsetAsync(pa.ctr, 0, 64, st));
     PLAUNCH(h, 0, (double)iters * 4.0 * (double)(m + 2 * r) * (double)n + 4.0 * (double)(m + r) * (double)n,
             launch_fused(X, ldx, m, n, r, W, nullptr, 0, eps, H, nullptr, nullptr, 0, p.fgrid, st, &pa));
@@ -1192,7 +1161,7 @@ ntt_status ntt_nmf_bcd(ntt_handle h, const float* X, int64_t m, int64_t n, int64
   }();
   // (with the GPU-wide partial pre-sum before k_bcd_post the one-pass path also wins at 2^15:
   // 6.3 vs 8.9 ms / 100 it, so it is taken for every n)
-  const bool f1_shape = m <= f1_max && fused_supported(m, n, r, ldx, X, H) && !use_wc() &&
+  const bool f1_shape = m <= f1_max && fused_supported(m, n, r, ldx, X, H) &&
                         !getenv("NTT_BCD_NO_1PASS") && !getenv("NTT_BCD_NO_FUSED");
   bool tc = !f1_shape && tc_supported(m, n, r, ldx, X) && !getenv("NTT_NO_TC");
   TcPlan tp;
