@@ -1554,6 +1554,399 @@ cudaError_t launch_t(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_
                            mh2 ? *mh2 : mh, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, ns, evict_first, pa);
 }
 
+// ===========================================================================
+// k_fused_m: the one-pass MU kernel for 16 < m <= 32 (rank <= 8; config 3 step 1, config 4
+// steps 2-9) with all three contractions on warp-level tensor cores (mma.sync m16n8k16,
+// fp16 hi / lo operand splits as in k_fused_c).  Structure as k_fused: one CTA per SM, a
+// TMA producer warp with dynamic stage assignment, 8 consumer warps that each own whole
+// 128-column tiles (no CTA barriers in the loop).  Per tile (lane fragment coordinates
+// g = lane / 4, t = lane % 4; "mt" = 16-column m-tile):
+//   E^T = H^T G      8 m-tiles x (A = H^T split in registers, B = G)      (MU denominator)
+//   S^T = X^T W      8 m-tiles x 2 k-steps (A = X^T by ldmatrix.trans)     (phase A)
+//   Hn  = H S / (E + eps) elementwise in the fragment layout, stored to H and over the
+//         stage's H boxes
+//   P  += X Hn^T     2 m-tiles x 8 k-steps (A = X by ldmatrix, B = Hn^T)    (phase B)
+//   Q  += Hn Hn^T    8 k-steps (A = B = the Hn fragments)
+// X is converted to fp16 hi / lo blocks in place (per 32 x 32 block scale); a persistent
+// launch stores them in the X16 cache in its prologue pass and streams them afterwards.
+// ===========================================================================
+constexpr int NWM = 8;                     // consumer warps
+constexpr int XBM = 4 * 32 * 128;          // X region: 4 boxes of 32 rows x 32 columns (fp32 / fp16 hi+lo)
+constexpr int HBM = 4 * 8 * 128;           // H region: 4 boxes of 8 ranks x 32 columns
+constexpr int SBM = XBM + HBM + 1024;      // + 16 B of block scales (1024-aligned stages)
+constexpr int X16M_STRIDE = XBM + 128;     // X16 blob per tile: 4 blocks + 4 scales
+
+// byte offset of element (k, c) (rank k < 8, column c < 128) of the H region (TMA SWIZZLE_128B)
+__device__ __forceinline__ int hbox_off(int k, int c) { return (c >> 5) * 1024 + k * 128 + ((((c & 31) >> 2) ^ k) << 4) + (c & 3) * 4; }
+
+__global__ void __launch_bounds__((NWM + 1) * 32, 1)
+k_fused_m(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmH, int m, int64_t n, int r,
+          const float* __restrict__ W, const double* __restrict__ Gpart, int nG, float eps, float* __restrict__ H,
+          double* __restrict__ Ppart, double* __restrict__ Qpart, int mode, int ns, int evict_first, PersistArgs pa) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  constexpr int NTHR = (NWM + 1) * 32;
+  unsigned char* stages = smem;
+  float* Ws = reinterpret_cast<float*>(smem + (size_t)ns * SBM);  // 32 x 8
+  float* Gs = Ws + 32 * 8;                                          // 8 x 8
+  uint64_t* full = reinterpret_cast<uint64_t*>(Gs + 64);
+  uint64_t* empty = full + ns;
+  uint32_t* issued = reinterpret_cast<uint32_t*>(empty + ns);
+  uint32_t* free_mask = issued + 1;
+  uint32_t* tag = issued + 2;  // [ns <= 24]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool persist = pa.iters > 0;
+
+  for (int e = tid; e < 32 * 8; e += NTHR) {
+    const int i = e >> 3, k = e & 7;
+    Ws[e] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
+  }
+  if (!persist && (mode & kFusedUpdate)) {
+    const int rr = r * r;
+    for (int e = tid; e < 64; e += NTHR) {
+      const int k = e >> 3, l = e & 7;
+      double s = 0.0;
+      if (k < r && l < r)
+        for (int q = 0; q < nG; ++q) s += Gpart[(int64_t)q * rr + k * r + l];
+      Gs[e] = (float)s;
+    }
+  }
+  if (tid == 0) {
+    for (int s = 0; s < ns; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    *issued = 0u;
+    *free_mask = (ns >= 32) ? 0xffffffffu : ((1u << ns) - 1u);
+    for (int q = 0; q < ns; ++q) tag[q] = 0xffffffffu;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t par_mask = 0u;
+
+  const int64_t ntiles = (n + 127) / 128;
+  const int64_t b = blockIdx.x;
+  const int64_t J = (ntiles > b) ? (ntiles - b + gridDim.x - 1) / gridDim.x : 0;
+  unsigned epoch = 0;
+  const int nit = persist ? pa.iters + 1 : 1;
+  for (int it = 0; it < nit; ++it) {
+  const int md = persist ? (it == 0 ? kFusedAcc : (kFusedUpdate | (it < pa.iters ? kFusedAcc : 0))) : mode;
+  const bool do_update = (md & kFusedUpdate) != 0;
+  const bool do_acc = (md & kFusedAcc) != 0;
+  const bool x16_write = pa.x16 != nullptr && persist && it == 0;
+  const bool x16_read = pa.x16 != nullptr && persist && it > 0;
+  const int64_t pbase = (int64_t)it * J;
+  pstamp(pa, it, 0);
+  if (warp == NWM) {
+    // ================= producer =================
+    if (lane == 0) {
+      const uint64_t policy = evict_first ? policy_evict_first() : policy_evict_normal();
+      for (int64_t j = 0; j < J; ++j) {
+        const int64_t pos = pbase + j;
+        uint32_t fm;
+        while ((fm = ld_acquire_u32(free_mask)) == 0u) __nanosleep(32);
+        const int s = __ffs(fm) - 1;
+        atomicAnd(free_mask, ~(1u << s));
+        const uint32_t ph = (par_mask >> s) & 1u;
+        par_mask ^= 1u << s;
+        tag[s] = ((uint32_t)pos << 1) | ph;
+        const int64_t tile = b + j * gridDim.x;
+        unsigned char* st = stages + (size_t)s * SBM;
+        if (x16_read) {
+          mbar_expect_tx(&full[s], XBM + HBM + 16);
+          const unsigned char* src = pa.x16 + tile * X16M_STRIDE;
+          bulk_load_1d(st, src, XBM, &full[s], policy);
+          bulk_load_1d(st + XBM + HBM, src + XBM, 16, &full[s], policy);
+        } else {
+          mbar_expect_tx(&full[s], XBM + HBM);
+          tma_load_3d(st, &tmX, 0, 0, (int)(tile * 4), &full[s], policy);
+        }
+        tma_load_3d(st + XBM, &tmH, 0, 0, (int)(tile * 4), &full[s], policy);
+        st_release_u32(issued, (uint32_t)(pos + 1));
+      }
+    }
+  } else {
+  // ================= consumer warps =================
+  auto pass_tiles = [&](auto upd_t, auto acc_t) {
+  constexpr bool UPD = decltype(upd_t)::value, ACC = decltype(acc_t)::value;
+  const int fg = lane >> 2, ft = lane & 3;
+  // per-pass B operands: W (phase A: b0 = W[16 ks + 2t, + 1][g], b1 = rows + 8) and G (E: b0 =
+  // G[2t, 2t + 1][g], b1 = 0), fp16 hi / lo with one power-of-two scale each
+  uint32_t wfh[2][2], wfl[2][2], gfh = 0u, gfl = 0u;
+  float wsi = 1.f, gsi = 1.f;
+  if constexpr (UPD) {
+    float wm = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int r0 = 16 * ks + 8 * h2 + 2 * ft;
+        wm = fmaxf(wm, fmaxf(fabsf(Ws[r0 * 8 + fg]), fabsf(Ws[(r0 + 1) * 8 + fg])));
+      }
+    const float2 wsc = pow2_scale(warp_max(wm));
+    wsi = wsc.y;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int r0 = 16 * ks + 8 * h2 + 2 * ft;
+        split2(Ws[r0 * 8 + fg], Ws[(r0 + 1) * 8 + fg], wsc.x, wfh[ks][h2], wfl[ks][h2]);
+      }
+    const float g0 = Gs[(2 * ft) * 8 + fg], g1 = Gs[(2 * ft + 1) * 8 + fg];
+    const float2 gsc = pow2_scale(warp_max(fmaxf(fabsf(g0), fabsf(g1))));
+    gsi = gsc.y;
+    split2(g0, g1, gsc.x, gfh, gfl);
+  }
+  double paccd[2][4], qaccd[2];
+#pragma unroll
+  for (int mh = 0; mh < 2; ++mh)
+#pragma unroll
+    for (int e4 = 0; e4 < 4; ++e4) paccd[mh][e4] = 0.0;
+  qaccd[0] = qaccd[1] = 0.0;
+
+  for (int64_t j = warp; j < J; j += NWM) {
+    const int64_t pos = pbase + j;
+    const int64_t jt = (b + j * gridDim.x) * 128;  // first column of the tile
+    if (lane == 0)
+      while (ld_acquire_u32(issued) <= (uint32_t)pos) __nanosleep(64);
+    __syncwarp();
+    const uint32_t tg = lane < ns ? *reinterpret_cast<volatile uint32_t*>(tag + lane) : 0xffffffffu;
+    const unsigned hit = __ballot_sync(0xffffffffu, (tg >> 1) == (uint32_t)pos && lane < ns);
+    const int s = __ffs(hit) - 1;
+    const uint32_t ph = __shfl_sync(0xffffffffu, tg, s) & 1u;
+    MBAR_WAIT(&full[s], ph, 2, j);
+    unsigned char* st = stages + (size_t)s * SBM;
+    unsigned char* hb = st + XBM;
+    const uint32_t xs = smem_u32(st);
+
+    // ---- X -> fp16 hi / lo blocks (in place), or the cached blocks' scales
+    float xsi[4];
+    if (x16_read) {
+      const float4 sc4 = *reinterpret_cast<const float4*>(st + XBM + HBM);
+      xsi[0] = sc4.x; xsi[1] = sc4.y; xsi[2] = sc4.z; xsi[3] = sc4.w;
+    } else {
+      unsigned char* gtile = x16_write ? pa.x16 + (b + j * gridDim.x) * X16M_STRIDE : nullptr;
+#pragma unroll
+      for (int bx = 0; bx < 4; ++bx) {
+        unsigned char* blk = st + bx * 4096;
+        float v[32];
+#pragma unroll
+        for (int c16 = 0; c16 < 8; ++c16) {
+          const float4 f = lds128(blk + lane * 128 + ((c16 ^ (lane & 7)) << 4));
+          v[4 * c16] = f.x;
+          v[4 * c16 + 1] = f.y;
+          v[4 * c16 + 2] = f.z;
+          v[4 * c16 + 3] = f.w;
+        }
+        float m8[8];
+#pragma unroll
+        for (int q2 = 0; q2 < 8; ++q2)
+          m8[q2] = fmaxf(fmaxf(fabsf(v[4 * q2]), fabsf(v[4 * q2 + 1])), fmaxf(fabsf(v[4 * q2 + 2]), fabsf(v[4 * q2 + 3])));
+        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        const float2 sc = pow2_scale(warp_max(mx));
+        xsi[bx] = sc.y;
+        __syncwarp();
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+          uint32_t hh[4], ll[4];
+#pragma unroll
+          for (int p2 = 0; p2 < 4; ++p2) split2(v[8 * k4 + 2 * p2], v[8 * k4 + 2 * p2 + 1], sc.x, hh[p2], ll[p2]);
+          *reinterpret_cast<uint4*>(blk + h16_off(lane, k4)) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
+          *reinterpret_cast<uint4*>(blk + 2048 + h16_off(lane, k4)) = make_uint4(ll[0], ll[1], ll[2], ll[3]);
+          if (gtile) {
+            __stcg(reinterpret_cast<uint4*>(gtile + bx * 4096 + h16_off(lane, k4)), make_uint4(hh[0], hh[1], hh[2], hh[3]));
+            __stcg(reinterpret_cast<uint4*>(gtile + bx * 4096 + 2048 + h16_off(lane, k4)),
+                   make_uint4(ll[0], ll[1], ll[2], ll[3]));
+          }
+        }
+        if (gtile && lane == 0) __stcg(reinterpret_cast<float*>(gtile + XBM) + bx, sc.y);
+      }
+      __syncwarp();
+    }
+
+    // ---- H of this lane's fragment entries: hv[mt][e] = H[2t + (e & 1)][16 mt + g + 8 (e >> 1)]
+    float hv[8][4];
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+      for (int e4 = 0; e4 < 4; ++e4)
+        hv[mt][e4] = *reinterpret_cast<const float*>(hb + hbox_off(2 * ft + (e4 & 1), 16 * mt + fg + 8 * (e4 >> 1)));
+    float hnm = 0.f;  // max |Hn| of the tile (B-operand scale of phase B / Q)
+    if constexpr (UPD) {
+      float hm = 0.f;
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt)
+        hm = fmaxf(hm, fmaxf(fmaxf(fabsf(hv[mt][0]), fabsf(hv[mt][1])), fmaxf(fabsf(hv[mt][2]), fabsf(hv[mt][3]))));
+      const float2 hsc = pow2_scale(warp_max(hm));
+      const float fE = hsc.y * gsi;
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        // E^T rows 16 mt .. + 15 (columns of the tile) = H^T G
+        uint32_t ah[4], al[4];
+        split2(hv[mt][0], hv[mt][1], hsc.x, ah[0], al[0]);
+        split2(hv[mt][2], hv[mt][3], hsc.x, ah[1], al[1]);
+        ah[2] = ah[3] = al[2] = al[3] = 0u;  // ranks 8 .. 15: padding
+        float de[4] = {0.f, 0.f, 0.f, 0.f};
+        mma16816(de, ah, gfh, 0u);
+        mma16816(de, ah, gfl, 0u);
+        mma16816(de, al, gfh, 0u);
+        // S^T rows 16 mt .. + 15 = X^T W over the 32 rows of X (2 k-steps)
+        const int bx = mt >> 1, mi = mt & 1;
+        float ds[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const int mj = lane >> 3;
+          const uint32_t off = bx * 4096 + h16_off(16 * ks + (lane & 7) + 8 * (mj >> 1), 2 * mi + (mj & 1));
+          uint32_t xh[4], xl[4];
+          ldsm_x4_t(xs + off, xh);
+          ldsm_x4_t(xs + off + 2048u, xl);
+          mma16816(ds, xh, wfh[ks][0], wfh[ks][1]);
+          mma16816(ds, xh, wfl[ks][0], wfl[ks][1]);
+          mma16816(ds, xl, wfh[ks][0], wfh[ks][1]);
+        }
+        const float fS = xsi[bx] * wsi;
+#pragma unroll
+        for (int e4 = 0; e4 < 4; ++e4) {
+          const int k = 2 * ft + (e4 & 1);
+          const int64_t col = jt + 16 * mt + fg + 8 * (e4 >> 1);
+          float v = mu_q(hv[mt][e4], ds[e4] * fS, de[e4] * fE, eps);
+          if (k >= r || col >= n) v = 0.f;  // padded ranks (0/0 when eps = 0), columns beyond n
+          else H[(int64_t)k * n + col] = v;
+          hv[mt][e4] = v;
+          hnm = fmaxf(hnm, fabsf(v));
+        }
+      }
+    } else {
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+        for (int e4 = 0; e4 < 4; ++e4) hnm = fmaxf(hnm, fabsf(hv[mt][e4]));
+    }
+
+    if constexpr (ACC) {
+      if constexpr (UPD) {
+        // Hn over the stage's H boxes (each entry rewritten by the lane that read it)
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+          for (int e4 = 0; e4 < 4; ++e4)
+            *reinterpret_cast<float*>(hb + hbox_off(2 * ft + (e4 & 1), 16 * mt + fg + 8 * (e4 >> 1))) = hv[mt][e4];
+        __syncwarp();
+      }
+      const float2 nsc = pow2_scale(warp_max(hnm));
+      // B = Hn^T fragments per 16-column k-step: b0 = Hn[g][16 kk + 2t, + 1], b1 = columns + 8
+      uint32_t bh[8][2], bl[8][2];
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const float2 p = *reinterpret_cast<const float2*>(hb + hbox_off(fg, 16 * kk + 8 * h2 + 2 * ft));
+          split2(p.x, p.y, nsc.x, bh[kk][h2], bl[kk][h2]);
+        }
+      // P (32 x 8) += X Hn^T: 2 m-tiles x 8 k-steps (per-block X scale -> one sum per block)
+#pragma unroll
+      for (int mh = 0; mh < 2; ++mh) {
+        float pt[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int bx = 0; bx < 4; ++bx) {
+          float d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int k2 = 0; k2 < 2; ++k2) {
+            const int kk = 2 * bx + k2, mj = lane >> 3;
+            const uint32_t off = bx * 4096 + h16_off(16 * mh + (lane & 7) + 8 * (mj & 1), 2 * k2 + (mj >> 1));
+            uint32_t xh[4], xl[4];
+            ldsm_x4(xs + off, xh);
+            ldsm_x4(xs + off + 2048u, xl);
+            mma16816(d, xh, bh[kk][0], bh[kk][1]);
+            mma16816(d, xh, bl[kk][0], bl[kk][1]);
+            mma16816(d, xl, bh[kk][0], bh[kk][1]);
+          }
+#pragma unroll
+          for (int e4 = 0; e4 < 4; ++e4) pt[e4] = fmaf(d[e4], xsi[bx], pt[e4]);
+        }
+#pragma unroll
+        for (int e4 = 0; e4 < 4; ++e4) paccd[mh][e4] += (double)(pt[e4] * nsc.y);
+      }
+      // Q (8 x 8) += Hn Hn^T: A = {b0, 0, b1, 0} (ranks 8 .. 15 padding), B = {b0, b1}
+      {
+        float dq[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t ah[4] = {bh[kk][0], 0u, bh[kk][1], 0u};
+          const uint32_t al[4] = {bl[kk][0], 0u, bl[kk][1], 0u};
+          mma16816(dq, ah, bh[kk][0], bh[kk][1]);
+          mma16816(dq, ah, bl[kk][0], bl[kk][1]);
+          mma16816(dq, al, bh[kk][0], bh[kk][1]);
+        }
+        qaccd[0] += (double)(dq[0] * (nsc.y * nsc.y));
+        qaccd[1] += (double)(dq[1] * (nsc.y * nsc.y));
+      }
+      // Hn was written over the stage with generic stores: order them before the producer's
+      // next TMA (async-proxy) write into this stage
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    } else if (!x16_read) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the in-place X conversion
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("red.release.cta.shared::cta.or.b32 [%0], %1;" ::"r"(smem_u32(free_mask)), "r"(1u << s) : "memory");
+  }
+
+  if constexpr (ACC) {
+    // ---- fixed-order CTA reduction of the warps' fp64 partials: red[w][0 .. 256) = P (32 x 8),
+    // red[w][256 .. 320) = Q (8 x 8)
+    asm volatile("bar.sync 1, %0;" ::"r"(NWM * 32) : "memory");
+    double* red = reinterpret_cast<double*>(stages);
+#pragma unroll
+    for (int mh = 0; mh < 2; ++mh)
+#pragma unroll
+      for (int e4 = 0; e4 < 4; ++e4)
+        red[warp * 320 + (16 * mh + fg + 8 * (e4 >> 1)) * 8 + 2 * ft + (e4 & 1)] = paccd[mh][e4];
+    red[warp * 320 + 256 + fg * 8 + 2 * ft] = qaccd[0];
+    red[warp * 320 + 256 + fg * 8 + 2 * ft + 1] = qaccd[1];
+    asm volatile("bar.sync 1, %0;" ::"r"(NWM * 32) : "memory");
+    const int mr = m * r, rr = r * r;
+    double* Pb = persist ? pa.part + b * (mr + rr) : Ppart + b * mr;
+    double* Qb = persist ? pa.part + b * (mr + rr) + mr : Qpart + b * rr;
+    for (int e = tid; e < 320; e += NWM * 32) {
+      const bool isQ = e >= 256;
+      const int row = isQ ? (e - 256) >> 3 : e >> 3, k = e & 7;
+      if (k >= r || (isQ ? row >= r : row >= m)) continue;
+      double sum = 0.0;
+      for (int w = 0; w < NWM; ++w) sum += red[w * 320 + e];
+      if (isQ) Qb[row * r + k] = sum;
+      else Pb[row * r + k] = sum;
+    }
+  }
+  };  // pass_tiles
+  using T_ = std::true_type;
+  using F_ = std::false_type;
+  if (!do_update) pass_tiles(F_{}, T_{});
+  else if (do_acc) pass_tiles(T_{}, T_{});
+  else pass_tiles(T_{}, F_{});
+  }  // consumer warps
+  if (!persist || !do_acc) break;
+  persist_step(pa, epoch, m, r, eps, Ws, Gs, reinterpret_cast<double*>(stages), it);
+  }  // passes
+}
+
+size_t fixed_bytes_m() { return 32 * 8 * 4 + 256 + 2 * 24 * 8 + 160 + 1024; }
+
+int stages_m() {
+  int ns = (int)((SMEM_BUDGET - fixed_bytes_m()) / SBM);
+  return ns > 24 ? 24 : ns;
+}
+
+cudaError_t launch_m(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_t n, int r, const float* W,
+                     const double* Gpart, int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
+                     int evict_first, const PersistArgs& pa, cudaStream_t st) {
+  const int ns = stages_m();
+  const size_t smem = (size_t)ns * SBM + fixed_bytes_m();
+  cudaError_t e = cudaFuncSetAttribute(k_fused_m, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_maybe_coop(k_fused_m, grid, (NWM + 1) * 32, smem, st, pa.iters > 0, mx, mh, m, n, r, W, Gpart, nG,
+                           eps, H, Ppart, Qpart, mode, ns, evict_first, pa);
+}
+
 // ------------------------------------------------------------ W update v2 --
 // CTA c owns rows [c*RB, c*RB+RB) with RB*r <= 64 entries; 1024 threads = 64
 // entries x 16 chunks of partials; each thread sums its chunk with 4
@@ -1690,7 +2083,11 @@ int fused_grid(int64_t m, int64_t n, int r, int num_sms) {
 
 size_t fused_scratch_bytes(int64_t, int64_t, int, int) { return 0; }
 
+// the tensor-core one-pass kernel for 16 < m <= 32 (k_fused_m) takes the shape (MU only)
+bool fused_m_ok(int64_t m, int64_t n, int r) { return m > 16 && m <= 32 && r <= 8 && (n % 32) == 0; }
+
 size_t fused_x16_bytes(int64_t m, int64_t n) {
+  if (m > 16 && m <= 32 && (n % 32) == 0) return (size_t)((n + 127) / 128) * (size_t)X16M_STRIDE;
   if (m <= 40) return 0;
   return (size_t)((n + BNC - 1) / BNC) * (size_t)(((m + 31) / 32) * 4096 + 128);
 }
@@ -1755,6 +2152,13 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
     if (e != cudaSuccess) return e;
     if (MPc == 128) return launch_c<128, 4>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
     return launch_c<256, 4>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
+  }
+  if (!pa.bcdL && fused_m_ok(m, n, r)) {  // MU on tensor cores (k_fused_m)
+    CUtensorMap mx, mh;
+    cudaError_t e = make_map3(&mx, X, (uint64_t)n, (uint64_t)m, (uint64_t)ldx, 32u, 4u);
+    if (e != cudaSuccess) return e;
+    if ((e = make_map3(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u, 4u)) != cudaSuccess) return e;
+    return launch_m(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
   }
   const int ux = ux_for(m);
   CUtensorMap mx, mh, mb0, mb1;
