@@ -118,6 +118,16 @@ __device__ __forceinline__ void pstamp(const PersistArgs& pa, int it, int ph) {
   }
 }
 
+// fine-grained diagnostics inside persist_step: [12288 + 4 it + k], k < 4, CTA 0 only
+__device__ __forceinline__ void pstamp2(const PersistArgs& pa, int it, int k) {
+  if (pa.trace && threadIdx.x == 0 && blockIdx.x == 0 && it < 1024) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    pa.trace[12288 + it * 4 + k] = t;
+    pa.trace[8192 + it * 4 + k] = (unsigned long long)clock64();
+  }
+}
+
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -192,62 +202,79 @@ __device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int 
   }
   pstamp(pa, it, 3);
   const double* srcv = gridDim.x > 1 ? pa.red : pa.part;
-  for (int e0 = 0; e0 < L; e0 += 8 * T) {
-    double v[8];
+  // (P, Q) into shared memory (coalesced; all loads of a thread issued before any is used), W as
+  // fp64 once: the fp64 pipe's conversions, not its FMAs, bounded this step (8 F2F per entry)
+  double* P = scr;                                                    // m x r
+  double* Q = scr + m * r;                                            // r x r
+  double* Wd = scr + L + 16;                                          // m x 8: W (fp64 copy)
+  double* Wnd = Wd + m * 8;                                           // m x 8: new W, rounded to fp32
+  double* Gp = Wnd + m * 8;                                           // [GC][64] Gram chunk partials
+  for (int e0 = 0; e0 < L; e0 += 16 * T) {
+    double v[16];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < 16; ++q) {
       const int e = e0 + q * T + tid;
       v[q] = e < L ? __ldcg(srcv + e) : 0.0;
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < 16; ++q) {
       const int e = e0 + q * T + tid;
       if (e < L) scr[e] = v[q];
     }
   }
+  for (int e = tid; e < m * 8; e += T) Wd[e] = (double)Ws[widx(e >> 3, e & 7, pairs)];
   __syncthreads();
-  double* P = scr;           // m x r
-  double* Q = scr + m * r;   // r x r
-  float* Wn = reinterpret_cast<float*>(scr + L + 16);
-  double* Gp = scr + L + 16 + (m * 8 + 1) / 2 + 8;  // [C][64] Gram chunk partials
-  for (int e = tid; e < m * 8; e += T) {
-    const int i = e >> 3, k = e & 7;
-    float v = 0.0f;
-    if (k < r) {
-      double d = 0.0;
-      for (int l = 0; l < r; ++l) d += (double)Ws[widx(i, l, pairs)] * Q[l * r + k];
-      v = (float)mu_quot((double)Ws[widx(i, k, pairs)], P[i * r + k], d, (double)eps);
+  pstamp2(pa, it, 0);
+  // W <- W o P / (W Q + eps) (fp64, reading R4), two entries (i, k) per step (independent chains)
+  for (int e0 = tid; e0 < m * 8; e0 += 2 * T) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int e = e0 + u * T;
+      if (e < m * 8) {
+        const int i = e >> 3, k = e & 7;
+        double v = 0.0;
+        if (k < r) {
+          double d = 0.0;
+          for (int l = 0; l < r; ++l) d += Wd[i * 8 + l] * Q[l * r + k];
+          v = (double)(float)mu_quot(Wd[e], P[i * r + k], d, (double)eps);
+        }
+        Wnd[e] = v;
+      }
     }
-    Wn[e] = v;
   }
   __syncthreads();
-  for (int e = tid; e < m * 8; e += T) Ws[widx(e >> 3, e & 7, pairs)] = Wn[e];
-  // G = Wn^T Wn: 64 entries x C row chunks (fixed order), then combine
+  pstamp2(pa, it, 1);
+  for (int e = tid; e < m * 8; e += T) Ws[widx(e >> 3, e & 7, pairs)] = (float)Wnd[e];
+  // G = Wn^T Wn: 64 entries x GC row chunks (fixed order), 4 interleaved accumulators per chunk
   const int GC = T / 64 < 1 ? 1 : (T / 64 > 4 ? 4 : T / 64);
   for (int t = tid; t < 64 * GC; t += T) {
     const int e = t & 63, c = t >> 6;
     const int k = e >> 3, l = e & 7;
     const int i0 = m * c / GC, i1 = m * (c + 1) / GC;
-    double s0 = 0.0, s1 = 0.0;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     if (k < r && l < r) {
       int i = i0;
-      for (; i + 1 < i1; i += 2) {
-        s0 += (double)Wn[i * 8 + k] * (double)Wn[i * 8 + l];
-        s1 += (double)Wn[(i + 1) * 8 + k] * (double)Wn[(i + 1) * 8 + l];
+      for (; i + 3 < i1; i += 4) {
+        s0 += Wnd[i * 8 + k] * Wnd[i * 8 + l];
+        s1 += Wnd[(i + 1) * 8 + k] * Wnd[(i + 1) * 8 + l];
+        s2 += Wnd[(i + 2) * 8 + k] * Wnd[(i + 2) * 8 + l];
+        s3 += Wnd[(i + 3) * 8 + k] * Wnd[(i + 3) * 8 + l];
       }
-      if (i < i1) s0 += (double)Wn[i * 8 + k] * (double)Wn[i * 8 + l];
+      for (; i < i1; ++i) s0 += Wnd[i * 8 + k] * Wnd[i * 8 + l];
     }
-    Gp[c * 64 + e] = s0 + s1;
+    Gp[c * 64 + e] = (s0 + s1) + (s2 + s3);
   }
   __syncthreads();
+  pstamp2(pa, it, 2);
   for (int e = tid; e < 64; e += T) {
     double sg = 0.0;
     for (int c = 0; c < GC; ++c) sg += Gp[c * 64 + e];
     Gs[e] = (float)sg;
   }
   if (blockIdx.x == 0)
-    for (int e = tid; e < m * r; e += T) pa.Wout[e] = Wn[(e / r) * 8 + (e % r)];
+    for (int e = tid; e < m * r; e += T) pa.Wout[e] = (float)Wnd[(e / r) * 8 + (e % r)];
   __syncthreads();
+  pstamp2(pa, it, 3);
 }
 
 template <int R, int UX, int NWT, bool HDIRECT, int BNT, bool FOLD>

@@ -33,6 +33,15 @@ for (m, n, r, it) in shapes:
     b1 = np.median(ps[:, 2] - ps[:, 1]) / 1e3
     b2 = np.median(ps[:, 3] - ps[:, 2]) / 1e3
     wu = np.median(nxt - ps[:, 3]) / 1e3
+    f = np.array([tr[12288 + i] for i in range(4 * (it + 1))], dtype=np.float64).reshape(it + 1, 4)[1:-1]
+    q = np.median(f[:, 0] - ps[:, 3]) / 1e3
+    wupd = np.median(f[:, 1] - f[:, 0]) / 1e3
+    gram = np.median(f[:, 2] - f[:, 1]) / 1e3
+    tail = np.median(f[:, 3] - f[:, 2]) / 1e3
+    nx = np.median(nxt - f[:, 3]) / 1e3
+    cy = np.array([tr[8192 + i] for i in range(4 * (it + 1))], dtype=np.float64).reshape(it + 1, 4)[1:-1]
+    print("   clock64 cycles: W update", np.median(cy[:, 1] - cy[:, 0]), "Gram", np.median(cy[:, 2] - cy[:, 1]))
     print(f"{m}x{n} r{r}: {tot:.2f} us/iter | pass {passt:.2f} barrier1 {b1:.2f} slice+barrier2 {b2:.2f} "
-          f"Wupdate->next {wu:.2f} us", flush=True)
+          f"Wupdate->next {wu:.2f} us [Q load {q:.2f}, W update {wupd:.2f}, Gram {gram:.2f}, Wout {tail:.2f}, "
+          f"-> next pass {nx:.2f}]", flush=True)
     del X, W, H
