@@ -152,7 +152,8 @@ __device__ __forceinline__ void grid_sync(unsigned* ctr, unsigned& epoch) {
 }
 
 // Reduce the per-CTA partials and apply the W update in every CTA (see above).
-// Ws: [i * 8 + k] (rows >= m stay zero), Gs: [k * 8 + l]; scr: >= (L + 16) doubles + m*8 floats
+// Ws: [i * 8 + k] (rows >= m stay zero), Gs: [k * 8 + l]; scr (the stage area, free between passes):
+// >= L + 16 + 16 m + 256 doubles
 // + 256 doubles of smem.  Global reads are issued in independent batches (L2 latency is ~1 us).
 // W layout in smem: row-major [i * 8 + k], or (pairs) [i/2][k/2][i%2][k%2] so that a
 // lane reading ranks (2g, 2g+1) of rows (i, i+1) issues one 128-bit load (k_fused_c)
@@ -893,12 +894,6 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     const int i = e >> 3, k = e & 7;
     Wc[widx(i, k, false)] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
   }
-  if (pa.x16) {
-    // X16 passes copy only the blocks of rows < m: the others must read as zeros in every stage
-    for (int e = tid; e < ns * (MP * 32); e += NTHR)
-      reinterpret_cast<uint32_t*>(stages + (size_t)(e / (MP * 32)) * SB)[e % (MP * 32)] = 0u;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) {
       mbar_init(&full[s], 1);
@@ -1166,6 +1161,8 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
           for (int e4 = 0; e4 < 4; ++e4) sacc[mt][nn][e4] = 0.f;
 #pragma unroll
       for (int bb = 0; bb < NB; ++bb) {
+        // blocks of rows >= m are not loaded by the X16 passes (stale shared memory): skip them
+        if (warp * NB + bb >= nblk) continue;
         const uint32_t blk = smem_u32(st) + (uint32_t)(warp * RW + 32 * bb) * 128u;
         float dacc[2][NN][4];
 #pragma unroll
@@ -1361,6 +1358,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         }
 #pragma unroll
       for (int bb = 0; bb < NB; ++bb) {
+        if (warp * NB + bb >= nblk) continue;  // rows >= m (see phase A)
         const uint32_t blk = smem_u32(st) + (uint32_t)(warp * RW + 32 * bb) * 128u;
         const float f = xsi[bb] * hsc.y;
 #pragma unroll

@@ -94,6 +94,15 @@ MU_CASES = [
     (100, 1000, 5, 10),
     (200, 4100, 3, 10),
     (41, 260, 8, 10),
+    # tensor-core one-pass kernels: k_fused_m (16 < m <= 32, n % 32 == 0; ragged 128-column tiles,
+    # n < 128) and k_fused_c's X16 cache with row blocks beyond m (persistent, 30 passes)
+    (17, 4096, 8, 10),
+    (32, 4128, 3, 10),
+    (20, 96, 6, 10),
+    (30, 7776, 5, 12),
+    (72, 8192, 8, 30),
+    (200, 16384, 8, 30),
+    (136, 2080, 6, 30),
 ]
 
 
