@@ -3,6 +3,25 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Device-side bounds / invariant checks of the hand-written kernels (compute-sanitizer is not
+// available on the GPU pool): a -DNTT_CHECKED build traps with a message on the first violation
+// (tests run against it: profiles/checked_r2.md).  Compiled out otherwise.
+#ifdef NTT_CHECKED
+#include <cstdio>
+#define NTT_DCHECK(c)                                                                                  \
+  do {                                                                                                 \
+    if (!(c)) {                                                                                        \
+      printf("NTT_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, blockIdx.x, \
+             threadIdx.x);                                                                             \
+      __trap();                                                                                        \
+    }                                                                                                  \
+  } while (0)
+#else
+#define NTT_DCHECK(c) \
+  do {                \
+  } while (0)
+#endif
+
 namespace ntt {
 
 constexpr int kMaxRank = 64;

@@ -941,6 +941,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         const int col0 = (int)(tile * BNC);
         unsigned char* st = stages + (size_t)s * SB;
         if (x16_read) {  // the tile's fp16 hi / lo blocks, one contiguous bulk copy
+          NTT_DCHECK(tile < ntiles);
           mbar_expect_tx(&full[s], (uint32_t)(nblk * 4096) + 1024u);
           bulk_load_1d(st, pa.x16 + tile * x16_stride, (uint32_t)(nblk * 4096), &full[s], policy);
         } else {
@@ -1037,6 +1038,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       ring_s = 0;
       ring_ph ^= 1u;
     }
+    NTT_DCHECK(s >= 0 && s < ns);
     MBAR_WAIT(&full[s], ph, 4, j);
     const unsigned char* st = stages + (size_t)s * SB;
     const int64_t jt = (b + j * gridDim.x) * BNC;
@@ -1237,7 +1239,10 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         else
           hn = mu_q(hkc, S, e0 + e1, eps);
         if (kt >= r || col >= n) hn = 0.0f;
-        if (kt < r && col < n) Ho[(int64_t)kt * n + col] = hn;
+        if (kt < r && col < n) {
+          NTT_DCHECK((int64_t)kt * n + col < (int64_t)r * n);
+          Ho[(int64_t)kt * n + col] = hn;
+        }
       } else {
         hn = (kt < r && col < n) ? hkc : 0.0f;
       }
@@ -1460,6 +1465,13 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   }  // passes
 }
 
+// shared-memory scratch persist_step takes from the stage area between passes (doubles)
+size_t persist_scratch_bytes(int64_t m, int r, int threads) {
+  const int64_t L = m * r + (int64_t)r * r;
+  const int GC = threads / 64 < 1 ? 1 : (threads / 64 > 4 ? 4 : threads / 64);
+  return sizeof(double) * (size_t)(L + 16 + 16 * m + 64 * GC + 8);
+}
+
 size_t fixed_bytes_c(int MP, int NW) {
   return (size_t)NW * 8 * 32 * 4 + 256 + HNC_FLOATS * 4 + (size_t)MP * 8 * 4 + 2 * 16 * 8 + 1024;
 }
@@ -1495,6 +1507,7 @@ cudaError_t launch_c(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_
   const int ns = stages_c(MP, NW);
   const size_t SB = (size_t)MP * 128 + 1024;
   const size_t smem = (size_t)ns * SB + fixed_bytes_c(MP, NW);
+  if (pa.iters > 0 && persist_scratch_bytes(m, r, (NW + 1) * 32) > (size_t)ns * SB) return cudaErrorInvalidConfiguration;
   cudaError_t e = cudaFuncSetAttribute(k_fused_c<MP, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_maybe_coop(k_fused_c<MP, NW>, grid, (NW + 1) * 32, smem, st, pa.iters > 0, mx, mh, m, n, r, W, Gpart,
@@ -1573,6 +1586,7 @@ cudaError_t launch_t(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_
   int ns = FOLD ? (int)((SMEM_BUDGET - fixed_bytes(UX, NWT, HD)) / SB) : stages_for(UX, NWT, HD, BNT);
   if (ns > 24) ns = 24;
   const size_t smem = (size_t)ns * SB + fixed_bytes(UX, NWT, HD);
+  if (pa.iters > 0 && persist_scratch_bytes(m, r, (NWT + 1) * 32) > (size_t)ns * SB) return cudaErrorInvalidConfiguration;
   cudaError_t e = cudaFuncSetAttribute(k_fused<R, UX, NWT, HD, BNT, FOLD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_maybe_coop(k_fused<R, UX, NWT, HD, BNT, FOLD>, grid, (NWT + 1) * 32, smem, st, pa.iters > 0, mx, mh,
@@ -1678,6 +1692,7 @@ k_fused_m(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         const int64_t tile = b + j * gridDim.x;
         unsigned char* st = stages + (size_t)s * SBM;
         if (x16_read) {
+          NTT_DCHECK(tile < ntiles);
           mbar_expect_tx(&full[s], XBM + HBM + 16);
           const unsigned char* src = pa.x16 + tile * X16M_STRIDE;
           bulk_load_1d(st, src, XBM, &full[s], policy);
@@ -1739,6 +1754,7 @@ k_fused_m(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     const unsigned hit = __ballot_sync(0xffffffffu, (tg >> 1) == (uint32_t)pos && lane < ns);
     const int s = __ffs(hit) - 1;
     const uint32_t ph = __shfl_sync(0xffffffffu, tg, s) & 1u;
+    NTT_DCHECK(s >= 0 && s < ns);
     MBAR_WAIT(&full[s], ph, 2, j);
     unsigned char* st = stages + (size_t)s * SBM;
     unsigned char* hb = st + XBM;
@@ -1836,7 +1852,10 @@ k_fused_m(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
           const int64_t col = jt + 16 * mt + fg + 8 * (e4 >> 1);
           float v = mu_q(hv[mt][e4], ds[e4] * fS, de[e4] * fE, eps);
           if (k >= r || col >= n) v = 0.f;  // padded ranks (0/0 when eps = 0), columns beyond n
-          else H[(int64_t)k * n + col] = v;
+          else {
+            NTT_DCHECK((int64_t)k * n + col < (int64_t)r * n);
+            H[(int64_t)k * n + col] = v;
+          }
           hv[mt][e4] = v;
           hnm = fmaxf(hnm, fabsf(v));
         }
@@ -1966,6 +1985,7 @@ cudaError_t launch_m(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_
                      int evict_first, const PersistArgs& pa, cudaStream_t st) {
   const int ns = stages_m();
   const size_t smem = (size_t)ns * SBM + fixed_bytes_m();
+  if (pa.iters > 0 && persist_scratch_bytes(m, r, (NWM + 1) * 32) > (size_t)ns * SBM) return cudaErrorInvalidConfiguration;
   cudaError_t e = cudaFuncSetAttribute(k_fused_m, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_maybe_coop(k_fused_m, grid, (NWM + 1) * 32, smem, st, pa.iters > 0, mx, mh, m, n, r, W, Gpart, nG,
