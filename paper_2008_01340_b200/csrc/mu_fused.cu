@@ -161,8 +161,8 @@ __device__ __forceinline__ int widx(int i, int k, bool pairs) {
   return pairs ? ((i >> 1) << 4) + ((k >> 1) << 2) + ((i & 1) << 1) + (k & 1) : (i << 3) + k;
 }
 
-__device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int r, float eps, float* Ws, float* Gs,
-                             double* scr, int it, bool pairs = false) {
+__device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int r, int rk, float eps, float* Ws,
+                             float* Gs, double* scr, int it) {
   const int L = m * r + r * r;
   const int T = blockDim.x, tid = threadIdx.x;
   pstamp(pa, it, 1);
@@ -203,77 +203,65 @@ __device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int 
   }
   pstamp(pa, it, 3);
   const double* srcv = gridDim.x > 1 ? pa.red : pa.part;
-  // (P, Q) into shared memory (coalesced; all loads of a thread issued before any is used), W as
-  // fp64 once: the fp64 pipe's conversions, not its FMAs, bounded this step (8 F2F per entry)
-  double* P = scr;                                                    // m x r
-  double* Q = scr + m * r;                                            // r x r
-  double* Wd = scr + L + 16;                                          // m x 8: W (fp64 copy)
-  double* Wnd = Wd + m * 8;                                           // m x 8: new W, rounded to fp32
-  double* Gp = Wnd + m * 8;                                           // [GC][64] Gram chunk partials
-  for (int e0 = 0; e0 < L; e0 += 16 * T) {
-    double v[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int e = e0 + q * T + tid;
-      v[q] = e < L ? __ldcg(srcv + e) : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int e = e0 + q * T + tid;
-      if (e < L) scr[e] = v[q];
-    }
-  }
-  for (int e = tid; e < m * 8; e += T) Wd[e] = (double)Ws[widx(e >> 3, e & 7, pairs)];
+  // scratch: Q (r x r), W as fp64 (m x rk), the new W (m x rk floats), Gram chunk partials; P is
+  // read straight from the reduced vector (L2) by the thread that updates the entry
+  double* Q = scr;                                                    // r x r (<= 256)
+  double* Wd = scr + 256;                                             // m x rk
+  float* Wn = reinterpret_cast<float*>(Wd + m * rk);                  // m x rk
+  double* Gp = Wd + m * rk + (m * rk + 1) / 2 + 2;                    // [GC][rk rk]
+  for (int e = tid; e < r * r; e += T) Q[e] = __ldcg(srcv + m * r + e);
+  for (int e = tid; e < m * rk; e += T) Wd[e] = (double)Ws[e];
   __syncthreads();
   pstamp2(pa, it, 0);
-  // W <- W o P / (W Q + eps) (fp64, reading R4), two entries (i, k) per step (independent chains)
-  for (int e0 = tid; e0 < m * 8; e0 += 2 * T) {
+  // W <- W o P / (W Q + eps) (fp64, reading R4); Ws / Wn layout [i rk + k], ranks >= r stay 0
+  for (int e0 = tid; e0 < m * rk; e0 += 2 * T) {
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int e = e0 + u * T;
-      if (e < m * 8) {
-        const int i = e >> 3, k = e & 7;
-        double v = 0.0;
+      if (e < m * rk) {
+        const int i = e / rk, k = e - (e / rk) * rk;
+        float v = 0.0f;
         if (k < r) {
           double d = 0.0;
-          for (int l = 0; l < r; ++l) d += Wd[i * 8 + l] * Q[l * r + k];
-          v = (double)(float)mu_quot(Wd[e], P[i * r + k], d, (double)eps);
+          for (int l = 0; l < r; ++l) d += Wd[i * rk + l] * Q[l * r + k];
+          v = (float)mu_quot(Wd[e], __ldcg(srcv + i * r + k), d, (double)eps);
         }
-        Wnd[e] = v;
+        Wn[e] = v;
       }
     }
   }
   __syncthreads();
   pstamp2(pa, it, 1);
-  for (int e = tid; e < m * 8; e += T) Ws[widx(e >> 3, e & 7, pairs)] = (float)Wnd[e];
-  // G = Wn^T Wn: 64 entries x GC row chunks (fixed order), 4 interleaved accumulators per chunk
-  const int GC = T / 64 < 1 ? 1 : (T / 64 > 4 ? 4 : T / 64);
-  for (int t = tid; t < 64 * GC; t += T) {
-    const int e = t & 63, c = t >> 6;
-    const int k = e >> 3, l = e & 7;
+  for (int e = tid; e < m * rk; e += T) Ws[e] = Wn[e];
+  // G = Wn^T Wn: rk^2 entries x GC row chunks (fixed order), 4 interleaved accumulators per chunk
+  const int RR = rk * rk;
+  const int GC = T / RR < 1 ? 1 : (T / RR > 4 ? 4 : T / RR);
+  for (int t = tid; t < RR * GC; t += T) {
+    const int e = t % RR, c = t / RR;
+    const int k = e / rk, l = e - (e / rk) * rk;
     const int i0 = m * c / GC, i1 = m * (c + 1) / GC;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     if (k < r && l < r) {
       int i = i0;
       for (; i + 3 < i1; i += 4) {
-        s0 += Wnd[i * 8 + k] * Wnd[i * 8 + l];
-        s1 += Wnd[(i + 1) * 8 + k] * Wnd[(i + 1) * 8 + l];
-        s2 += Wnd[(i + 2) * 8 + k] * Wnd[(i + 2) * 8 + l];
-        s3 += Wnd[(i + 3) * 8 + k] * Wnd[(i + 3) * 8 + l];
+        s0 += (double)Wn[i * rk + k] * (double)Wn[i * rk + l];
+        s1 += (double)Wn[(i + 1) * rk + k] * (double)Wn[(i + 1) * rk + l];
+        s2 += (double)Wn[(i + 2) * rk + k] * (double)Wn[(i + 2) * rk + l];
+        s3 += (double)Wn[(i + 3) * rk + k] * (double)Wn[(i + 3) * rk + l];
       }
-      for (; i < i1; ++i) s0 += Wnd[i * 8 + k] * Wnd[i * 8 + l];
+      for (; i < i1; ++i) s0 += (double)Wn[i * rk + k] * (double)Wn[i * rk + l];
     }
-    Gp[c * 64 + e] = (s0 + s1) + (s2 + s3);
+    Gp[c * RR + e] = (s0 + s1) + (s2 + s3);
   }
   __syncthreads();
   pstamp2(pa, it, 2);
-  for (int e = tid; e < 64; e += T) {
+  for (int e = tid; e < RR; e += T) {
     double sg = 0.0;
-    for (int c = 0; c < GC; ++c) sg += Gp[c * 64 + e];
+    for (int c = 0; c < GC; ++c) sg += Gp[c * RR + e];
     Gs[e] = (float)sg;
   }
   if (blockIdx.x == 0)
-    for (int e = tid; e < m * r; e += T) pa.Wout[e] = (float)Wnd[(e / r) * 8 + (e % r)];
+    for (int e = tid; e < m * r; e += T) pa.Wout[e] = Wn[(e / r) * rk + (e % r)];
   __syncthreads();
   pstamp2(pa, it, 3);
 }
@@ -771,7 +759,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   }
   }  // consumer warps
   if (!persist || !do_acc) break;
-  persist_step(pa, epoch, m, r, eps, Ws, Gs, reinterpret_cast<double*>(stages), it);
+  persist_step(pa, epoch, m, r, 8, eps, Ws, Gs, reinterpret_cast<double*>(stages), it);
   }  // passes
 }
 
@@ -825,74 +813,80 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
 __device__ __forceinline__ uint32_t h16_off(int row, int ch) { return (uint32_t)(row * 64 + ((ch ^ ((row >> 1) & 3)) << 4)); }
 
 // ===========================================================================
-// Variant C: CTA-cooperative tiles for 40 < m <= 256 (rank padded to 8).
-// Small CTAs (4 consumer warps + 1 TMA warp, <= 112 KB smem) so TWO CTAs share
-// an SM and one CTA's serial sections (S reduction, H update, barriers) overlap
-// the other's FMA phases.  Tile = 32 columns x MP rows (one SWIZZLE_128B box)
-// + the 8 x 32 H box.  Phase A splits the m-long dot products across the 4
-// warps (warp w owns rows [RW w, RW w + RW)), reduces the partial S tiles
-// through smem in fixed order; 128 threads form E = G H and Hn (2 entries
-// each).  Phase B: warp w owns the same rows of P = X Hn^T in sub-chunks of 32
-// (lanes = row block x 8-column slice, reduce-scatter over the slices, fp64
-// accumulation), and rows 2w, 2w+1 of Q = Hn Hn^T.  Rows are disjoint across
-// warps, so per-CTA partials need no cross-warp reduction.
+// k_fused_c: the one-pass MU / BCD kernel for 40 < m <= 256, rank padded to RK = 8 or 16,
+// on warp-level tensor cores (mma.sync m16n8k16, fp16 hi / lo splits; helpers above).
+// Small CTAs (4 consumer warps + 1 TMA warp, <= 113 KB smem) so TWO CTAs share an SM and
+// one CTA's serial sections (S reduction, H update, barriers) overlap the other's.  Tile =
+// 32 columns x MP rows of X (one box) + the RK x 32 box of H.  Warp w owns rows
+// [RW w, RW w + RW) in 32-row blocks:
+//   X      -> fp16 hi / lo blocks in place (per-block scale); a persistent launch stores them
+//             in the X16 cache in its prologue pass and streams them afterwards
+//   phase A S^T (32 x RK) partial = X^T W over the warp's rows; fixed-order sum over the
+//           warps in smem
+//   H update 128 threads form E = G H and Hn (RK / 4 entries each; MU rule or BCD step)
+//   phase B P (the warp's rows x RK) += X Hn^T; warp 0 adds Q += Hn Hn^T
+// Rows are disjoint across warps, so per-CTA partials need no cross-warp reduction.
 // ===========================================================================
 constexpr int BNC = 32;
-constexpr int NWC = 4;                  // consumer warps per CTA
-constexpr int NTC = (NWC + 1) * 32;
-constexpr int HNC_FLOATS = 32 * 8 + 16; // transposed Hn tile [c][k] + 4 floats per 8-column group
 constexpr int SMEM_C = 113 * 1024;      // two CTAs per SM
 
-__device__ __forceinline__ int hnc_idx(int c, int k) { return c * 8 + k + 4 * (c >> 3); }
+// transposed Hn tile [c][k], RK floats per column + 4 floats of padding per 8 columns
+template <int RK>
+__device__ __forceinline__ int hnc_idx(int c, int k) { return c * RK + k + 4 * (c >> 3); }
+constexpr int hnc_floats(int rk) { return 32 * rk + 16; }
+// byte offset of element (k, c) of the RK x 32 H box (TMA SWIZZLE_128B: 1 KB atoms of 8 rows)
+__device__ __forceinline__ int hc_off(int k, int c) { return k * 128 + ((((c >> 2) ^ k) & 7) << 4) + (c & 3) * 4; }
 
-template <int MP, int NW>
+template <int MP, int NW, int RK>
+// NW = 4: two CTAs per SM (10 warps over 4 sub-partitions: <= 3 x 32 x 170 registers in one 16 K
+// bank -> 168 registers); NW = 8 (the RK = 16 class at MP = 256): one CTA per SM, <= 224 registers
 __global__ void __launch_bounds__((NW + 1) * 32, NW == 4 ? 2 : 1)
 k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmH, int m, int64_t n, int r,
           const float* __restrict__ W, const double* __restrict__ Gpart, int nG, float eps, float* __restrict__ H,
           double* __restrict__ Ppart, double* __restrict__ Qpart, int mode, int ns, int evict_first,
           PersistArgs pa) {
   extern __shared__ unsigned char smem_raw[];
-  // keep the shared address space visible to the compiler (LDS/STS, not generic LD/ST)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int RW = MP / NW;           // rows per warp (32 or 64)
-  constexpr int NCH = RW / 32;          // phase-B sub-chunks of 32 rows
+  constexpr int NB = RW / 32;           // 32-row blocks per warp
+  constexpr int NN = RK / 8;            // n-tiles of 8 ranks
   static_assert(RW >= 32 && RW % 32 == 0, "k_fused_c: at least 32 rows per consumer warp");
-  constexpr int HH = 256 / (NW * 32);   // H-update (k, c) pairs per thread
-  constexpr int QR = 8 / NW;            // Q rows per warp
-  constexpr bool WREG = (RW == 32);     // W rows of this warp kept in registers
+  static_assert(NW == 4 || NW == 8, "k_fused_c: 4 or 8 consumer warps");
+  constexpr int HH = RK / NW;           // H-update (k, c) pairs per thread
   constexpr int NTHR = (NW + 1) * 32;
+  constexpr int NBAR = NW * 32;
   constexpr uint32_t XB = MP * 128u;
-  constexpr uint32_t SB = XB + 1024u;
+  constexpr uint32_t SB = XB + RK * 128u;
   unsigned char* stages = smem;
-  float* Sred = reinterpret_cast<float*>(smem + (size_t)ns * SB);  // [NW][8 k][32 c]
-  float* Gs = Sred + NW * 8 * 32;                                    // 8 x 8
-  float* Hn = Gs + 64;                                               // HNC_FLOATS
-  float* Wc = Hn + HNC_FLOATS;                                       // MP x 8 (rank padded)
-  uint64_t* full = reinterpret_cast<uint64_t*>(Wc + MP * 8);
+  float* Sred = reinterpret_cast<float*>(smem + (size_t)ns * SB);  // [NW][RK k][32 c]
+  float* Gs = Sred + NW * RK * 32;                                   // RK x RK
+  float* Hn = Gs + RK * RK;                                          // hnc_floats(RK)
+  float* Wc = Hn + hnc_floats(RK);                                   // MP x RK (rank padded)
+  uint64_t* full = reinterpret_cast<uint64_t*>(Wc + MP * RK);
   uint64_t* empty = full + ns;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool persist = pa.iters > 0;
   // BCD mode (PersistArgs::bcdL; see k_fused): row scales of H_m (smem), 1 / L_H, output buffer
   const bool bcd = pa.bcdL != nullptr;
-  __shared__ float bsh[8];
-  __shared__ float hmx[NW];  // per-warp max |Hn| of the current tile (mma.sync phase B scale)
-  if (tid < 8) bsh[tid] = (bcd && tid < r) ? (float)pa.bcdS[tid] : 1.f;
+  __shared__ float bsh[RK];
+  __shared__ float hmx[NW];  // per-warp max |Hn| of the current tile (phase B scale)
+  if (tid < RK) bsh[tid] = (bcd && tid < r) ? (float)pa.bcdS[tid] : 1.f;
   const float binvL = (bcd && *pa.bcdL > 0.0) ? (float)(1.0 / *pa.bcdL) : 0.f;
   float* const Ho = (bcd && pa.Hout) ? ((pa.bcdRole && *pa.bcdRole != 0.0) ? pa.Hout2 : pa.Hout) : H;
   if (!persist && (mode & kFusedUpdate)) {
     const int rr = r * r;
-    for (int e = tid; e < 64; e += NTHR) {
-      int k = e >> 3, l = e & 7;
+    for (int e = tid; e < RK * RK; e += NTHR) {
+      const int k = e / RK, l = e % RK;
       double sum = 0.0;
       if (k < r && l < r)
         for (int bq = 0; bq < nG; ++bq) sum += Gpart[(int64_t)bq * rr + k * r + l];
       Gs[e] = (float)sum;
     }
   }
-  for (int e = tid; e < MP * 8; e += NTHR) {
-    const int i = e >> 3, k = e & 7;
-    Wc[widx(i, k, false)] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
+  for (int e = tid; e < MP * RK; e += NTHR) {
+    const int i = e / RK, k = e % RK;
+    Wc[e] = (i < m && k < r) ? W[(int64_t)i * r + k] : 0.0f;
   }
   if (tid == 0) {
     for (int s = 0; s < ns; ++s) {
@@ -910,8 +904,8 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   const int64_t J = (ntiles > b) ? (ntiles - b + gridDim.x - 1) / gridDim.x : 0;
 
   unsigned epoch = 0;
-  int ring_s = 0;          // ring stage / parity of the next tile (continues across passes;
-  uint32_t ring_ph = 0;    // incremental: a 64-bit pos % ns was a division call per tile)
+  int ring_s = 0;          // ring stage / parity of the next tile (continues across passes)
+  uint32_t ring_ph = 0;
   const int nit = persist ? pa.iters + 1 : 1;
   for (int it = 0; it < nit; ++it) {
   const int md = persist ? (it == 0 ? kFusedAcc : (kFusedUpdate | (it < pa.iters ? kFusedAcc : 0))) : mode;
@@ -920,15 +914,10 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   // X16 cache: the prologue pass (it == 0) writes it, every later pass streams it
   const bool x16_write = pa.x16 != nullptr && persist && it == 0;
   const bool x16_read = pa.x16 != nullptr && persist && it > 0;
-  const int64_t pbase = (int64_t)it * J;
   pstamp(pa, it, 0);
   if (warp == NW) {
     if (lane == 0) {
-      uint64_t policy;
-      if (evict_first)
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-      else
-        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
+      const uint64_t policy = evict_first ? policy_evict_first() : policy_evict_normal();
       for (int64_t j = 0; j < J; ++j) {
         const int s = ring_s;
         const uint32_t ph = ring_ph;
@@ -942,7 +931,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         unsigned char* st = stages + (size_t)s * SB;
         if (x16_read) {  // the tile's fp16 hi / lo blocks, one contiguous bulk copy
           NTT_DCHECK(tile < ntiles);
-          mbar_expect_tx(&full[s], (uint32_t)(nblk * 4096) + 1024u);
+          mbar_expect_tx(&full[s], (uint32_t)(nblk * 4096) + RK * 128u);
           bulk_load_1d(st, pa.x16 + tile * x16_stride, (uint32_t)(nblk * 4096), &full[s], policy);
         } else {
           mbar_expect_tx(&full[s], SB);
@@ -957,28 +946,6 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   // BCD: Alg. 3's prox-linear H step instead of the MU rule), so no per-tile branch on the mode.
   auto pass_tiles = [&](auto upd_t, auto acc_t, auto bcd_t) {
   constexpr bool UPD = decltype(upd_t)::value, ACC = decltype(acc_t)::value, BCD = decltype(bcd_t)::value;
-  const int q = lane & 7, g = lane >> 3;   // phase A (RW = 32): columns 4q..4q+3, ranks 2g, 2g+1
-  const int rb = lane & 7, cs = lane >> 3; // phase B: rows rb + 8u of a 32-row chunk, columns 8cs..8cs+7
-  double accd[NCH][8];
-#pragma unroll
-  for (int h = 0; h < NCH; ++h)
-#pragma unroll
-    for (int v = 0; v < 8; ++v) accd[h][v] = 0.0;
-  double qd[QR];
-#pragma unroll
-  for (int qq = 0; qq < QR; ++qq) qd[qq] = 0.0;
-  const bool h1 = (lane >> 4) & 1, h0 = (lane >> 3) & 1;
-  constexpr int NBAR = NW * 32;
-#ifdef NTT_FC_FFMA
-  // this warp's W rows (ranks 2g, 2g+1) in registers when it owns 32 rows
-  float2 wreg[WREG ? 32 : 1];
-  if constexpr (WREG && UPD) {
-#pragma unroll
-    for (int v = 0; v < 32; ++v) wreg[v] = *reinterpret_cast<const float2*>(Wc + widx(warp * RW + v, 2 * g, false));
-  }
-#else
-  constexpr int NB = RW / 32;  // 32-row blocks per warp
-  constexpr int NN = 1;        // n-tiles of 8 ranks
   const int fg = lane >> 2, ft = lane & 3;  // mma fragment coordinates (group, thread in group)
   float xsi[NB];               // 2^-e of each block's X split (this tile)
 #pragma unroll
@@ -998,7 +965,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 #pragma unroll
           for (int h2 = 0; h2 < 2; ++h2) {
             const int r0 = warp * RW + 32 * bb + 16 * ks + 8 * h2 + 2 * ft, k = 8 * nn + fg;
-            wm = fmaxf(wm, fmaxf(fabsf(Wc[widx(r0, k, false)]), fabsf(Wc[widx(r0 + 1, k, false)])));
+            wm = fmaxf(wm, fmaxf(fabsf(Wc[r0 * RK + k]), fabsf(Wc[(r0 + 1) * RK + k])));
           }
     const float2 wsc = pow2_scale(warp_max(wm));
     wsi = wsc.y;
@@ -1011,11 +978,16 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 #pragma unroll
           for (int h2 = 0; h2 < 2; ++h2) {
             const int r0 = warp * RW + 32 * bb + 16 * ks + 8 * h2 + 2 * ft, k = 8 * nn + fg;
-            split2(Wc[widx(r0, k, false)], Wc[widx(r0 + 1, k, false)], wsc.x, wfh[bb][ks][nn][h2], wfl[bb][ks][nn][h2]);
+            split2(Wc[r0 * RK + k], Wc[(r0 + 1) * RK + k], wsc.x, wfh[bb][ks][nn][h2], wfl[bb][ks][nn][h2]);
           }
   }
-  float pacc[NB][2][NN][4];
+  // two-level P accumulation (fp32 over <= 8 tiles, then fp64); RK = 16 adds each tile's fp32 sum to
+  // fp64 directly (the fp32 set would not fit in 200 registers next to the fp64 one)
+  constexpr bool P32 = RK == 8;
+  float pacc[P32 ? NB : 1][2][NN][4];
   double paccd[NB][2][NN][4];
+  constexpr int QR = RK / NW;  // Q rows per warp
+  double qd[QR];
 #pragma unroll
   for (int bb = 0; bb < NB; ++bb)
 #pragma unroll
@@ -1024,12 +996,12 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       for (int nn = 0; nn < NN; ++nn)
 #pragma unroll
         for (int e4 = 0; e4 < 4; ++e4) {
-          pacc[bb][mh][nn][e4] = 0.f;
+          if constexpr (P32) pacc[bb][mh][nn][e4] = 0.f;
           paccd[bb][mh][nn][e4] = 0.0;
         }
+#pragma unroll
+  for (int qq = 0; qq < QR; ++qq) qd[qq] = 0.0;
   int since_flush = 0;
-  constexpr int RS = 8;  // Sred row stride per warp (ranks)
-#endif
 
   for (int64_t j = 0; j < J; ++j) {
     const int s = ring_s;
@@ -1040,65 +1012,14 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     }
     NTT_DCHECK(s >= 0 && s < ns);
     MBAR_WAIT(&full[s], ph, 4, j);
-    const unsigned char* st = stages + (size_t)s * SB;
+    unsigned char* st = stages + (size_t)s * SB;
+    const unsigned char* hbox = st + XB;
     const int64_t jt = (b + j * gridDim.x) * BNC;
 
     if constexpr (!UPD) {
       // prologue: Hn of the previous tile may still be read by phase B of other warps
       asm volatile("bar.sync 1, %0;" ::"r"(NBAR) : "memory");
     }
-#ifdef NTT_FC_FFMA
-    if constexpr (UPD) {
-      // ---- phase A: partial S over this warp's rows
-      if constexpr (!WREG) {
-        // lane = (cp = lane & 15: columns 2cp, 2cp+1; kh = lane >> 4: ranks 4kh..4kh+3): X by one
-        // LDS.64 per row (the warp reads the 128-byte row), W by one half-warp-uniform LDS.128;
-        // even and odd rows in two accumulator sets (8 independent FFMA2 chains)
-        const int cp = lane & 15, kh = lane >> 4;
-        const unsigned char* xb = st + (size_t)(warp * RW) * 128 + (cp & 1) * 8;
-        const float* wb = Wc + warp * RW * 8 + 4 * kh;
-        float2 sa = f2(0.f, 0.f), sb = f2(0.f, 0.f), sc = f2(0.f, 0.f), sd = f2(0.f, 0.f);
-        float2 ta = f2(0.f, 0.f), tb = f2(0.f, 0.f), tc = f2(0.f, 0.f), td = f2(0.f, 0.f);
-#pragma unroll 4
-        for (int v = 0; v < RW; v += 2) {
-          const float2 x0 = *reinterpret_cast<const float2*>(xb + v * 128 + (((cp >> 1) ^ (v & 7)) << 4));
-          const float2 x1 = *reinterpret_cast<const float2*>(xb + (v + 1) * 128 + (((cp >> 1) ^ ((v + 1) & 7)) << 4));
-          const float4 w0 = *reinterpret_cast<const float4*>(wb + v * 8);
-          const float4 w1 = *reinterpret_cast<const float4*>(wb + (v + 1) * 8);
-          sa = __ffma2_rn(bc(w0.x), x0, sa);
-          sb = __ffma2_rn(bc(w0.y), x0, sb);
-          sc = __ffma2_rn(bc(w0.z), x0, sc);
-          sd = __ffma2_rn(bc(w0.w), x0, sd);
-          ta = __ffma2_rn(bc(w1.x), x1, ta);
-          tb = __ffma2_rn(bc(w1.y), x1, tb);
-          tc = __ffma2_rn(bc(w1.z), x1, tc);
-          td = __ffma2_rn(bc(w1.w), x1, td);
-        }
-        float* sr = Sred + (warp * 8 + 4 * kh) * 32 + 2 * cp;
-        *reinterpret_cast<float2*>(sr) = __fadd2_rn(sa, ta);
-        *reinterpret_cast<float2*>(sr + 32) = __fadd2_rn(sb, tb);
-        *reinterpret_cast<float2*>(sr + 64) = __fadd2_rn(sc, tc);
-        *reinterpret_cast<float2*>(sr + 96) = __fadd2_rn(sd, td);
-      } else {
-        float2 sa = f2(0.f, 0.f), sb = f2(0.f, 0.f), sc = f2(0.f, 0.f), sd = f2(0.f, 0.f);
-#pragma unroll
-        for (int v = 0; v < RW; ++v) {
-          const int i = warp * RW + v;
-          const float4 x = lds128(st + i * 128 + ((q ^ (i & 7)) << 4));
-          const float2 x01 = f2(x.x, x.y), x23 = f2(x.z, x.w);
-          const float2 wv = wreg[v & 31];
-          sa = __ffma2_rn(bc(wv.x), x01, sa);
-          sb = __ffma2_rn(bc(wv.x), x23, sb);
-          sc = __ffma2_rn(bc(wv.y), x01, sc);
-          sd = __ffma2_rn(bc(wv.y), x23, sd);
-        }
-        float* sr = Sred + (warp * 8 + 2 * g) * 32 + 4 * q;
-        *reinterpret_cast<float4*>(sr) = make_float4(sa.x, sa.y, sb.x, sb.y);
-        *reinterpret_cast<float4*>(sr + 32) = make_float4(sc.x, sc.y, sd.x, sd.y);
-      }
-      asm volatile("bar.sync 1, %0;" ::"r"(NBAR) : "memory");
-    }
-#else
     if (x16_read) {
       // the block scales of this tile (written by the prologue pass next to its blocks)
       const float* sc = reinterpret_cast<const float*>(pa.x16 + (b + j * gridDim.x) * x16_stride + nblk * 4096);
@@ -1115,7 +1036,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 #pragma unroll
       for (int bb = 0; bb < NB; ++bb) {
         const int gb = warp * NB + bb;
-        unsigned char* blk = const_cast<unsigned char*>(st) + (size_t)(warp * RW + 32 * bb) * 128;
+        unsigned char* blk = st + (size_t)(warp * RW + 32 * bb) * 128;
         float v[32];
 #pragma unroll
         for (int c16 = 0; c16 < 8; ++c16) {
@@ -1151,9 +1072,8 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       __syncwarp();
     }
     if constexpr (UPD) {
-      // ---- phase A: S^T (32 cols x R) = X^T W over this warp's rows by mma.sync m16n8k16:
-      // A = X^T (ldmatrix.trans of the fp16 parts), B = W (fragments built per pass),
-      // hi.hi + hi.lo + lo.hi
+      // ---- phase A: S^T (32 cols x RK) = X^T W over this warp's rows: A = X^T (ldmatrix.trans
+      // of the fp16 parts), B = W fragments, hi.hi + hi.lo + lo.hi
       float sacc[2][NN][4];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
@@ -1204,150 +1124,54 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         for (int nn = 0; nn < NN; ++nn)
 #pragma unroll
           for (int e4 = 0; e4 < 4; ++e4)
-            Sred[(warp * RS + 8 * nn + 2 * ft + (e4 & 1)) * 32 + 16 * mt + fg + 8 * (e4 >> 1)] = sacc[mt][nn][e4];
+            Sred[(warp * RK + 8 * nn + 2 * ft + (e4 & 1)) * 32 + 16 * mt + fg + 8 * (e4 >> 1)] = sacc[mt][nn][e4];
       asm volatile("bar.sync 1, %0;" ::"r"(NBAR) : "memory");
     }
-#endif
-    // ---- H update: thread handles (k, c) for k in {kt, kt+4}, c = ct
+    // ---- H update: thread handles (k, c) for k = kt + NW hh, c = ct
     float hmax = 0.f;
-#pragma unroll
-    for (int hh = 0; hh < HH; ++hh) {
-      const int kt = (tid >> 5) + NW * hh, ct = tid & 31;
+    {
+      const int ct = tid & 31;
       const int64_t col = jt + ct;
-      const float hkc = *reinterpret_cast<const float*>(st + XB + kt * 128 + (((ct >> 2) ^ kt) << 4) + (ct & 3) * 4);
-      float hn;
-      if constexpr (UPD) {
-        float S = 0.0f;
+      float hl[RK];
 #pragma unroll
-        for (int w = 0; w < NW; ++w) S += Sred[(w * 8 + kt) * 32 + ct];
-        float hl[8];
+      for (int l = 0; l < RK; ++l) hl[l] = *reinterpret_cast<const float*>(hbox + hc_off(l, ct));
 #pragma unroll
-        for (int l = 0; l < 8; ++l)
-          hl[l] = *reinterpret_cast<const float*>(st + XB + l * 128 + (((ct >> 2) ^ l) << 4) + (ct & 3) * 4);
-        if constexpr (BCD) {
+      for (int hh = 0; hh < HH; ++hh) {
+        const int kt = (tid >> 5) + NW * hh;
+        const float hkc = hl[kt];
+        float hn;
+        if constexpr (UPD) {
+          float S = 0.0f;
 #pragma unroll
-          for (int l = 0; l < 8; ++l) hl[l] *= bsh[l];
+          for (int w = 0; w < NW; ++w) S += Sred[(w * RK + kt) * 32 + ct];
+          float e0 = 0.0f, e1 = 0.0f;
+#pragma unroll
+          for (int l = 0; l < RK; l += 2) {
+            e0 = fmaf(Gs[kt * RK + l], BCD ? hl[l] * bsh[l] : hl[l], e0);
+            e1 = fmaf(Gs[kt * RK + l + 1], BCD ? hl[l + 1] * bsh[l + 1] : hl[l + 1], e1);
+          }
+          if constexpr (BCD)  // prox-linear step (Alg. 3 l.14) on H_m = diag(sH) H_m stored
+            hn = fmaxf(0.f, fmaf(-((e0 + e1) - S), binvL, hkc * bsh[kt]));
+          else
+            hn = mu_q(hkc, S, e0 + e1, eps);
+          if (kt >= r || col >= n) hn = 0.0f;
+          if (kt < r && col < n) {
+            NTT_DCHECK((int64_t)kt * n + col < (int64_t)r * n);
+            Ho[(int64_t)kt * n + col] = hn;
+          }
+        } else {
+          hn = (kt < r && col < n) ? hkc : 0.0f;
         }
-        float e0 = 0.0f, e1 = 0.0f;
-#pragma unroll
-        for (int l = 0; l < 8; l += 2) {
-          e0 = fmaf(Gs[kt * 8 + l], hl[l], e0);
-          e1 = fmaf(Gs[kt * 8 + l + 1], hl[l + 1], e1);
-        }
-        if constexpr (BCD)  // prox-linear step (Alg. 3 l.14) on H_m = diag(sH) H_m stored
-          hn = fmaxf(0.f, fmaf(-((e0 + e1) - S), binvL, hkc * bsh[kt]));
-        else
-          hn = mu_q(hkc, S, e0 + e1, eps);
-        if (kt >= r || col >= n) hn = 0.0f;
-        if (kt < r && col < n) {
-          NTT_DCHECK((int64_t)kt * n + col < (int64_t)r * n);
-          Ho[(int64_t)kt * n + col] = hn;
-        }
-      } else {
-        hn = (kt < r && col < n) ? hkc : 0.0f;
+        if constexpr (ACC) Hn[hnc_idx<RK>(ct, kt)] = hn;
+        hmax = fmaxf(hmax, fabsf(hn));
       }
-      if constexpr (ACC) Hn[hnc_idx(ct, kt)] = hn;
-      hmax = fmaxf(hmax, fabsf(hn));
     }
-#ifndef NTT_FC_FFMA
     if constexpr (ACC) {
       const float wm = warp_max(hmax);
       if (lane == 0) hmx[warp] = wm;
-    }
-#endif
-
-    if constexpr (ACC) {
       asm volatile("bar.sync 1, %0;" ::"r"(NBAR) : "memory");
-      // ---- phase B
-#ifdef NTT_FC_FFMA
-      {
-        float qa[QR];
-#pragma unroll
-        for (int qq = 0; qq < QR; ++qq) qa[qq] = 0.f;
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const float* src = Hn + hnc_idx(8 * cs + t, 0);
-          const float hr = src[rb];
-#pragma unroll
-          for (int qq = 0; qq < QR; ++qq) qa[qq] = fmaf(src[QR * warp + qq], hr, qa[qq]);
-        }
-#pragma unroll
-        for (int qq = 0; qq < QR; ++qq) qd[qq] += (double)qa[qq];
-      }
-#pragma unroll
-      for (int h = 0; h < NCH; ++h) {
-        float2 acc[16];
-#pragma unroll
-        for (int v = 0; v < 16; ++v) acc[v] = f2(0.f, 0.f);
-#pragma unroll
-        for (int s4 = 0; s4 < 2; ++s4) {
-          float2 hq2[4][4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const float* src = Hn + hnc_idx(8 * cs + 4 * s4 + t, 0);
-            const float4 a = *reinterpret_cast<const float4*>(src);
-            const float4 bq = *reinterpret_cast<const float4*>(src + 4);
-            hq2[t][0] = f2(a.x, a.y);
-            hq2[t][1] = f2(a.z, a.w);
-            hq2[t][2] = f2(bq.x, bq.y);
-            hq2[t][3] = f2(bq.z, bq.w);
-          }
-          float xs[4][4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int i = warp * RW + 32 * h + rb + 8 * u;
-            const float4 x = lds128(st + i * 128 + (((2 * cs + s4) ^ rb) << 4));
-            xs[u][0] = x.x;
-            xs[u][1] = x.y;
-            xs[u][2] = x.z;
-            xs[u][3] = x.w;
-          }
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-              for (int kp = 0; kp < 4; ++kp)
-                acc[u * 4 + kp] = __ffma2_rn(bc(xs[u][t]), hq2[t][kp], acc[u * 4 + kp]);
-        }
-        // reduce-scatter over the 4 column-slice lanes: keep flat f in [8 cs, 8 cs + 8)
-        float a1[32];
-#pragma unroll
-        for (int v = 0; v < 16; ++v) {
-          a1[2 * v] = acc[v].x;
-          a1[2 * v + 1] = acc[v].y;
-        }
-        float a2[16];
-#pragma unroll
-        for (int v = 0; v < 16; ++v) {
-          const float send = h1 ? a1[v] : a1[v + 16];
-          const float keep = h1 ? a1[v + 16] : a1[v];
-          a2[v] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-        }
-#pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          const float send = h0 ? a2[v] : a2[v + 8];
-          const float keep = h0 ? a2[v + 8] : a2[v];
-          accd[h][v] += (double)(keep + __shfl_xor_sync(0xffffffffu, send, 8));
-        }
-      }
-#else
-      {  // Q rows QR w + qq over this lane's 8-column slice (FFMA; r x r)
-        float qa[QR];
-#pragma unroll
-        for (int qq = 0; qq < QR; ++qq) qa[qq] = 0.f;
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          const float* src = Hn + hnc_idx(8 * cs + t, 0);
-          const float hr = src[rb];
-#pragma unroll
-          for (int qq = 0; qq < QR; ++qq) qa[qq] = fmaf(src[QR * warp + qq], hr, qa[qq]);
-        }
-#pragma unroll
-        for (int qq = 0; qq < QR; ++qq) qd[qq] += (double)qa[qq];
-      }
-      // P (this warp's rows x R) += X Hn^T by mma.sync: A = X (ldmatrix of the fp16 parts),
-      // B = Hn^T split with the tile's power-of-two scale (max |Hn| from the H update)
+      // B = Hn^T fragments, split with the tile's power-of-two scale: b0 = Hn[8 nn + g][16 kk + 2t, + 1],
+      // b1 = columns + 8, + 9
       float hm = hmx[0];
 #pragma unroll
       for (int w = 1; w < NW; ++w) hm = fmaxf(hm, hmx[w]);
@@ -1358,9 +1182,10 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 #pragma unroll
         for (int nn = 0; nn < NN; ++nn) {
           const int c0 = 16 * kk + 2 * ft, kr = 8 * nn + fg;
-          split2(Hn[hnc_idx(c0, kr)], Hn[hnc_idx(c0 + 1, kr)], hsc.x, bh[kk][nn][0], bl[kk][nn][0]);
-          split2(Hn[hnc_idx(c0 + 8, kr)], Hn[hnc_idx(c0 + 9, kr)], hsc.x, bh[kk][nn][1], bl[kk][nn][1]);
+          split2(Hn[hnc_idx<RK>(c0, kr)], Hn[hnc_idx<RK>(c0 + 1, kr)], hsc.x, bh[kk][nn][0], bl[kk][nn][0]);
+          split2(Hn[hnc_idx<RK>(c0 + 8, kr)], Hn[hnc_idx<RK>(c0 + 9, kr)], hsc.x, bh[kk][nn][1], bl[kk][nn][1]);
         }
+      // P (this warp's rows x RK) += X Hn^T: A = X (ldmatrix of the fp16 parts)
 #pragma unroll
       for (int bb = 0; bb < NB; ++bb) {
         if (warp * NB + bb >= nblk) continue;  // rows >= m (see phase A)
@@ -1390,10 +1215,29 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 #pragma unroll
           for (int nn = 0; nn < NN; ++nn)
 #pragma unroll
-            for (int e4 = 0; e4 < 4; ++e4) pacc[bb][mh][nn][e4] = fmaf(d[nn][e4], f, pacc[bb][mh][nn][e4]);
+            for (int e4 = 0; e4 < 4; ++e4) {
+              if constexpr (P32) pacc[bb][mh][nn][e4] = fmaf(d[nn][e4], f, pacc[bb][mh][nn][e4]);
+              else paccd[bb][mh][nn][e4] += (double)(d[nn][e4] * f);
+            }
         }
       }
-      if (++since_flush == 8) {  // two-level accumulation: fp32 over <= 8 tiles, then fp64
+      {  // Q rows QR w + qq (QR = RK / NW), column qc = lane % RK, over this lane's slice of the
+         // tile's columns (32 / RK slices of RK columns); the slices are summed at the end of the pass
+        float qa[QR];
+#pragma unroll
+        for (int qq = 0; qq < QR; ++qq) qa[qq] = 0.f;
+        const int qc = lane % RK, qs = lane / RK;
+#pragma unroll
+        for (int t = 0; t < RK; ++t) {
+          const int c = qs * RK + t;
+          const float hr = Hn[hnc_idx<RK>(c, qc)];
+#pragma unroll
+          for (int qq = 0; qq < QR; ++qq) qa[qq] = fmaf(Hn[hnc_idx<RK>(c, QR * warp + qq)], hr, qa[qq]);
+        }
+#pragma unroll
+        for (int qq = 0; qq < QR; ++qq) qd[qq] += (double)qa[qq];
+      }
+      if (P32 && ++since_flush == 8) {  // two-level accumulation: fp32 over <= 8 tiles, then fp64
         since_flush = 0;
 #pragma unroll
         for (int bb = 0; bb < NB; ++bb)
@@ -1403,55 +1247,47 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
             for (int nn = 0; nn < NN; ++nn)
 #pragma unroll
               for (int e4 = 0; e4 < 4; ++e4) {
-                paccd[bb][mh][nn][e4] += (double)pacc[bb][mh][nn][e4];
-                pacc[bb][mh][nn][e4] = 0.f;
+                if constexpr (P32) {
+                  paccd[bb][mh][nn][e4] += (double)pacc[bb][mh][nn][e4];
+                  pacc[bb][mh][nn][e4] = 0.f;
+                }
               }
       }
-#endif
     } else if constexpr (UPD) {
       // no phase B: the next tile's phase A must not overwrite Sred while it is still read
       asm volatile("bar.sync 1, %0;" ::"r"(NBAR) : "memory");
     }
+    // the in-place X conversion wrote the stage with generic stores: order them before the
+    // producer's next TMA (async-proxy) write into it
+    if (!x16_read) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 
   if constexpr (ACC) {
-  const int mr = m * r, rr = r * r;
-  double* Pb = persist ? pa.part + b * (mr + rr) : Ppart + b * mr;
-  double* Qb = persist ? pa.part + b * (mr + rr) + mr : Qpart + b * rr;
-#ifdef NTT_FC_FFMA
-  // P: lane holds flat f = u*8 + k in [8 cs, 8 cs + 8) of sub-chunk h, rows warp*RW + 32h + rb + 8u
+    const int mr = m * r, rr = r * r;
+    double* Pb = persist ? pa.part + b * (mr + rr) : Ppart + b * mr;
+    double* Qb = persist ? pa.part + b * (mr + rr) + mr : Qpart + b * rr;
+    // P fragment: rows warp RW + 32 bb + 16 mh + fg (+ 8), ranks 8 nn + 2 ft (+ 1)
 #pragma unroll
-  for (int h = 0; h < NCH; ++h)
+    for (int bb = 0; bb < NB; ++bb)
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      const int f = 8 * cs + v;
-      const int u = f >> 3, k = f & 7;
-      const int row = warp * RW + 32 * h + rb + 8 * u;
-      if (row < m && k < r) Pb[row * r + k] = accd[h][v];
+      for (int mh = 0; mh < 2; ++mh)
+#pragma unroll
+        for (int nn = 0; nn < NN; ++nn)
+#pragma unroll
+          for (int e4 = 0; e4 < 4; ++e4) {
+            const int row = warp * RW + 32 * bb + 16 * mh + fg + 8 * (e4 >> 1), k = 8 * nn + 2 * ft + (e4 & 1);
+            if (row < m && k < r) Pb[row * r + k] = paccd[bb][mh][nn][e4] + (P32 ? (double)pacc[P32 ? bb : 0][mh][nn][e4] : 0.0);
+          }
+    // Q rows QR w + qq, column lane % RK: sum the 32 / RK column slices
+#pragma unroll
+    for (int qq = 0; qq < QR; ++qq) {
+      qd[qq] += __shfl_xor_sync(0xffffffffu, qd[qq], 16);
+      if (RK == 8) qd[qq] += __shfl_xor_sync(0xffffffffu, qd[qq], 8);
+      const int row = QR * warp + qq, k = lane % RK;
+      if (lane < RK && row < r && k < r) Qb[row * r + k] = qd[qq];
     }
-#else
-  // P fragment: rows warp RW + 32 bb + 16 mh + fg (+ 8), ranks 8 nn + 2 ft (+ 1)
-#pragma unroll
-  for (int bb = 0; bb < NB; ++bb)
-#pragma unroll
-    for (int mh = 0; mh < 2; ++mh)
-#pragma unroll
-      for (int nn = 0; nn < NN; ++nn)
-#pragma unroll
-        for (int e4 = 0; e4 < 4; ++e4) {
-          const int row = warp * RW + 32 * bb + 16 * mh + fg + 8 * (e4 >> 1), k = 8 * nn + 2 * ft + (e4 & 1);
-          if (row < m && k < r) Pb[row * r + k] = paccd[bb][mh][nn][e4] + (double)pacc[bb][mh][nn][e4];
-        }
-#endif
-  // Q rows QR w + qq, column rb: sum the 4 column slices
-#pragma unroll
-  for (int qq = 0; qq < QR; ++qq) {
-    qd[qq] += __shfl_xor_sync(0xffffffffu, qd[qq], 16);
-    qd[qq] += __shfl_xor_sync(0xffffffffu, qd[qq], 8);
-    if (cs == 0 && rb < r && QR * warp + qq < r) Qb[(QR * warp + qq) * r + rb] = qd[qq];
-  }
   }
   };  // pass_tiles
   using T_ = std::true_type;
@@ -1461,25 +1297,24 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   else bcd ? pass_tiles(T_{}, F_{}, T_{}) : pass_tiles(T_{}, F_{}, F_{});
   }  // consumer warps
   if (!persist || !do_acc) break;
-  persist_step(pa, epoch, m, r, eps, Wc, Gs, reinterpret_cast<double*>(stages), it, false);
+  persist_step(pa, epoch, m, r, RK, eps, Wc, Gs, reinterpret_cast<double*>(stages), it);
   }  // passes
 }
 
 // shared-memory scratch persist_step takes from the stage area between passes (doubles)
-size_t persist_scratch_bytes(int64_t m, int r, int threads) {
-  const int64_t L = m * r + (int64_t)r * r;
-  const int GC = threads / 64 < 1 ? 1 : (threads / 64 > 4 ? 4 : threads / 64);
-  return sizeof(double) * (size_t)(L + 16 + 16 * m + 64 * GC + 8);
+size_t persist_scratch_bytes(int64_t m, int rk, int threads) {
+  const int RR = rk * rk;
+  const int GC = threads / RR < 1 ? 1 : (threads / RR > 4 ? 4 : threads / RR);
+  return sizeof(double) * (size_t)(256 + m * rk + (m * rk + 1) / 2 + 2 + (int64_t)GC * RR);
 }
 
-size_t fixed_bytes_c(int MP, int NW) {
-  return (size_t)NW * 8 * 32 * 4 + 256 + HNC_FLOATS * 4 + (size_t)MP * 8 * 4 + 2 * 16 * 8 + 1024;
+size_t fixed_bytes_c(int MP, int NW, int RK) {
+  return (size_t)NW * RK * 32 * 4 + RK * RK * 4 + hnc_floats(RK) * 4 + (size_t)MP * RK * 4 + 2 * 16 * 8 + 1024;
 }
 
-int stages_c(int MP, int NW) {
-  const size_t SB = (size_t)MP * 128 + 1024;
-  const size_t budget = NW == 4 ? (size_t)SMEM_C : (size_t)SMEM_BUDGET;  // 2 CTAs / SM (4 warps) or 1 (8 warps)
-  int ns = (int)((budget - fixed_bytes_c(MP, NW)) / SB);
+int stages_c(int MP, int NW, int RK) {
+  const size_t SB = (size_t)MP * 128 + RK * 128;
+  int ns = (int)(((NW == 4 ? SMEM_C : SMEM_BUDGET) - fixed_bytes_c(MP, NW, RK)) / SB);
   return ns > 12 ? 12 : ns;
 }
 
@@ -1500,21 +1335,20 @@ cudaError_t launch_maybe_coop(void (*kern)(KArgs...), int grid, int threads, siz
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
-template <int MP, int NW>
+template <int MP, int NW, int RK>
 cudaError_t launch_c(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_t n, int r, const float* W,
                      const double* Gpart, int nG, float eps, float* H, double* Ppart, double* Qpart, int mode, int grid,
                      int evict_first, const PersistArgs& pa, cudaStream_t st) {
-  const int ns = stages_c(MP, NW);
-  const size_t SB = (size_t)MP * 128 + 1024;
-  const size_t smem = (size_t)ns * SB + fixed_bytes_c(MP, NW);
-  if (pa.iters > 0 && persist_scratch_bytes(m, r, (NW + 1) * 32) > (size_t)ns * SB) return cudaErrorInvalidConfiguration;
-  cudaError_t e = cudaFuncSetAttribute(k_fused_c<MP, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int ns = stages_c(MP, NW, RK);
+  const size_t SB = (size_t)MP * 128 + RK * 128;
+  const size_t smem = (size_t)ns * SB + fixed_bytes_c(MP, NW, RK);
+  if (ns < 2) return cudaErrorInvalidConfiguration;
+  if (pa.iters > 0 && persist_scratch_bytes(m, RK, (NW + 1) * 32) > (size_t)ns * SB) return cudaErrorInvalidConfiguration;
+  cudaError_t e = cudaFuncSetAttribute(k_fused_c<MP, NW, RK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_maybe_coop(k_fused_c<MP, NW>, grid, (NW + 1) * 32, smem, st, pa.iters > 0, mx, mh, m, n, r, W, Gpart,
-                           nG, eps, H, Ppart, Qpart, mode, ns, evict_first, pa);
+  return launch_maybe_coop(k_fused_c<MP, NW, RK>, grid, (NW + 1) * 32, smem, st, pa.iters > 0, mx, mh, m, n, r, W,
+                           Gpart, nG, eps, H, Ppart, Qpart, mode, ns, evict_first, pa);
 }
-
-
 
 // ---------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -1969,7 +1803,7 @@ k_fused_m(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   else pass_tiles(T_{}, F_{});
   }  // consumer warps
   if (!persist || !do_acc) break;
-  persist_step(pa, epoch, m, r, eps, Ws, Gs, reinterpret_cast<double*>(stages), it);
+  persist_step(pa, epoch, m, r, 8, eps, Ws, Gs, reinterpret_cast<double*>(stages), it);
   }  // passes
 }
 
@@ -1985,7 +1819,7 @@ cudaError_t launch_m(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_
                      int evict_first, const PersistArgs& pa, cudaStream_t st) {
   const int ns = stages_m();
   const size_t smem = (size_t)ns * SBM + fixed_bytes_m();
-  if (pa.iters > 0 && persist_scratch_bytes(m, r, (NWM + 1) * 32) > (size_t)ns * SBM) return cudaErrorInvalidConfiguration;
+  if (pa.iters > 0 && persist_scratch_bytes(m, 8, (NWM + 1) * 32) > (size_t)ns * SBM) return cudaErrorInvalidConfiguration;
   cudaError_t e = cudaFuncSetAttribute(k_fused_m, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_maybe_coop(k_fused_m, grid, (NWM + 1) * 32, smem, st, pa.iters > 0, mx, mh, m, n, r, W, Gpart, nG,
@@ -2103,7 +1937,8 @@ int rb2_for(int r) {
 }  // namespace
 
 bool fused_supported(int64_t m, int64_t n, int r, int64_t ldx, const void* X, const void* H) {
-  if (m < 1 || m > 256 || r < 1 || r > 8 || n < 4) return false;
+  // ranks up to 8 (k_fused, m <= 40) or 16 (k_fused_c's RK = 16 class, 40 < m <= 256)
+  if (m < 1 || m > 256 || r < 1 || r > (m > 40 ? 16 : 8) || n < 4) return false;
   if ((n & 3) || (ldx & 3)) return false;
   if ((reinterpret_cast<uintptr_t>(X) & 15) || (reinterpret_cast<uintptr_t>(H) & 15)) return false;
   if (n > (int64_t)INT32_MAX - 256) return false;
@@ -2122,7 +1957,8 @@ int fused_grid(int64_t m, int64_t n, int r, int num_sms) {
     return (int)(ntiles < num_sms ? ntiles : num_sms);
   }
   int64_t ntiles = (n + BNC - 1) / BNC;
-  const int cps = 2;  // variant C: CTAs per SM (4 consumer warps each; one CTA of 8 warps measured slower)
+  // k_fused_c: two CTAs of 4 consumer warps per SM; one CTA of 8 for the RK = 16 class at MP = 256
+  const int cps = (m > 128 && r > 8) ? 1 : 2;
   return (int)(ntiles < cps * num_sms ? ntiles : cps * num_sms);
 }
 
@@ -2193,10 +2029,19 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
     CUtensorMap mx, mh;
     cudaError_t e = make_map(&mx, X, (uint64_t)n, (uint64_t)m, (uint64_t)ldx, (uint32_t)MPc);
     if (e != cudaSuccess) return e;
-    e = make_map(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, 8u);
+    const int RKc = r <= 8 ? 8 : 16;
+    e = make_map(&mh, H, (uint64_t)n, (uint64_t)r, (uint64_t)n, (uint32_t)RKc);
     if (e != cudaSuccess) return e;
-    if (MPc == 128) return launch_c<128, 4>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
-    return launch_c<256, 4>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
+#define LC(MP_, RK_) \
+  return launch_c<MP_, 4, RK_>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st)
+    if (MPc == 128) {
+      if (RKc == 8) LC(128, 8);
+      LC(128, 16);
+    }
+    if (RKc == 8) LC(256, 8);
+#undef LC
+    return launch_c<256, 8, 16>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, evict_first, pa, st);
+#undef LC
   }
   if (!pa.bcdL && fused_m_ok(m, n, r)) {  // MU on tensor cores (k_fused_m)
     CUtensorMap mx, mh;

@@ -103,6 +103,11 @@ MU_CASES = [
     (72, 8192, 8, 30),
     (200, 16384, 8, 30),
     (136, 2080, 6, 30),
+    # k_fused_c's rank-16 class (9 <= r <= 16; the paper's 256^4 ranks 10): persistent + X16
+    (256, 16384, 10, 30),
+    (256, 4100, 12, 10),
+    (100, 8192, 16, 20),
+    (64, 1000, 9, 10),
 ]
 
 
