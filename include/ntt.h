@@ -242,6 +242,16 @@ double ntt_compression_ratio(int32_t d, const int64_t* dims, const int32_t* rank
  * stream (error / generate), 4 = other, 5 = generic 2-pass H pass, 6 = tensor-core
  * X H^T pass, 7 = tensor-core W^T X pass (mu_tc.cu, tall / square X).
  * Enabling resets the counters.                                              */
+/* Read-only HBM streaming ceiling ("report HBM % against ... a
+ * harness-measured read-only streaming ceiling"; SURVEY s.8(d)).  Reads `bytes`
+ * (> 0, multiple of 16) of the DEVICE buffer `buf` (16-byte aligned, contents
+ * irrelevant, not modified; the caller owns it) once untimed and then `reps` (>= 1)
+ * times with 128-bit evict-first loads from a grid of 8 x SM-count CTAs, timed with
+ * CUDA events on the handle's stream, and stores bytes * reps / time in GB/s into
+ * *gbps.  Synchronises the stream.  NTT_ERR_INVALID_ARG for bad sizes, alignment
+ * or a non-device buffer.  A measurement utility, not part of the method.      */
+ntt_status ntt_stream_ceiling(ntt_handle h, const void* buf, int64_t bytes, int32_t reps, double* gbps);
+
 #define NTT_PROF_CLASSES 8
 ntt_status ntt_profile_enable(ntt_handle h, int enable);
 ntt_status ntt_profile_get(ntt_handle h, int cls, int64_t* launches, double* total_ms,

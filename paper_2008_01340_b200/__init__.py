@@ -161,6 +161,12 @@ class Handle:
         self._check(lib().ntt_nmf_mu(self._h, _ptr(X), m, n, ldx, r, iters, eps, _ptr(W), _ptr(H), tr))
         return list(tr)[:iters] if trace else None
 
+    def ntt_stream_ceiling(self, buf, nbytes: int, reps: int = 10) -> float:
+        """Read-only HBM stream rate over a device buffer in GB/s (BASELINE.md s.3 ceiling)."""
+        g = ctypes.c_double(0.0)
+        self._check(lib().ntt_stream_ceiling(self._h, _ptr(buf), nbytes, reps, ctypes.byref(g)))
+        return float(g.value)
+
     @property
     def collective_count(self) -> int:
         return int(lib().ntt_collective_count(self._h))

@@ -54,6 +54,7 @@ SIGNATURES = {
     "ntt_debug_bcd_force_correct": (c_int, [c_p, ctypes.c_uint64]),
     "ntt_set_validation": (c_int, [c_p, c_int]),
     "ntt_collective_count": (c_i64, [c_p]),
+    "ntt_stream_ceiling": (c_int, [c_p, c_p, c_i64, c_i32, ctypes.POINTER(c_f64)]),
     "ntt_debug_fill_uniform_cols": (c_int, [c_p, c_p, c_i32, c_i64, c_i64, c_i64, c_i64, c_i64, c_u64, c_u64]),
     "ntt_debug_gather_last_core": (c_int, [c_p, c_p, c_i64, c_i64, c_i32, c_p]),
 }

@@ -168,5 +168,6 @@ cudaError_t launch_fill_uniform_cols(float* H, int r, int64_t nloc, int64_t b, i
 // gathered rank-major blocks [g][r][b_g] -> core [r][nd]
 // fixed-order sum of npart (a, b) pairs -> out[0..1]
 cudaError_t launch_sum_pairs(const double* part, int npart, double* out, cudaStream_t st);
+cudaError_t launch_read_stream(const void* buf, int64_t bytes, float* sink, int num_sms, cudaStream_t st);
 cudaError_t launch_gather_last_core(const float* gath, int64_t r, int64_t nd, int nranks, float* core, cudaStream_t st);
 }  // namespace ntt

@@ -152,17 +152,16 @@ __device__ __forceinline__ void grid_sync(unsigned* ctr, unsigned& epoch) {
 }
 
 // Reduce the per-CTA partials and apply the W update in every CTA (see above).
-// Ws: [i * 8 + k] (rows >= m stay zero), Gs: [k * 8 + l]; scr (the stage area, free between passes):
-// >= L + 16 + 16 m + 256 doubles
-// + 256 doubles of smem.  Global reads are issued in independent batches (L2 latency is ~1 us).
-// W layout in smem: row-major [i * 8 + k], or (pairs) [i/2][k/2][i%2][k%2] so that a
-// lane reading ranks (2g, 2g+1) of rows (i, i+1) issues one 128-bit load (k_fused_c)
-__device__ __forceinline__ int widx(int i, int k, bool pairs) {
-  return pairs ? ((i >> 1) << 4) + ((k >> 1) << 2) + ((i & 1) << 1) + (k & 1) : (i << 3) + k;
+// Scratch layout (doubles): P (m r) | Qp (RK x RK, Q zero-padded) | Wd (m RK, W as fp64) |
+// Wnd (m RK, new W rounded to fp32, held as fp64) | Gp ([<= T / RK chunks][RK][RK] Gram partials).
+// RK = 8 or 16 (the kernel's padded rank); Ws / Wnd layout [i RK + k], ranks >= r stay 0.
+__host__ __device__ constexpr int64_t persist_scratch_doubles(int64_t m, int r, int rk, int threads) {
+  return m * r + 1 + (int64_t)rk * rk + 2 * m * rk + (int64_t)(threads / rk) * rk * rk;
 }
 
-__device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int r, int rk, float eps, float* Ws,
-                             float* Gs, double* scr, int it) {
+template <int RK>
+__device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int r, float eps, float* Ws, float* Gs,
+                             double* scr, int it) {
   const int L = m * r + r * r;
   const int T = blockDim.x, tid = threadIdx.x;
   pstamp(pa, it, 1);
@@ -174,21 +173,23 @@ __device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int 
     const int e0 = blockIdx.x * SL;
     const int ne = min(L, e0 + SL) - e0;
     if (ne > 0) {
+      // slice [e0, e0 + ne) summed over the G partials: (entry, chunk of partials) per thread, all
+      // loads of a chunk (<= 16) issued before any is used (one L2 round trip)
       int C = T / ne;
       C = C < 1 ? 1 : (C > 32 ? 32 : C);
       for (int t = tid; t < ne * C; t += T) {
         const int e = t % ne, c = t / ne;
         const int g0 = (int)((int64_t)G * c / C), g1 = (int)((int64_t)G * (c + 1) / C);
         const double* src = pa.part + e0 + e;
-        double a[8];
+        double acc = 0.0;
+        for (int gb = g0; gb < g1; gb += 16) {
+          double a[16];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) a[q] = 0.0;
-        for (int g = g0; g < g1; g += 8) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (g + q < g1) a[q] += __ldcg(src + (int64_t)(g + q) * L);
+          for (int q = 0; q < 16; ++q) a[q] = (gb + q < g1) ? __ldcg(src + (int64_t)(gb + q) * L) : 0.0;
+          acc += (((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]))) +
+                 (((a[8] + a[9]) + (a[10] + a[11])) + ((a[12] + a[13]) + (a[14] + a[15])));
         }
-        scr[c * ne + e] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+        scr[c * ne + e] = acc;
       }
       __syncthreads();
       for (int e = tid; e < ne; e += T) {
@@ -203,65 +204,92 @@ __device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int 
   }
   pstamp(pa, it, 3);
   const double* srcv = gridDim.x > 1 ? pa.red : pa.part;
-  // scratch: Q (r x r), W as fp64 (m x rk), the new W (m x rk floats), Gram chunk partials; P is
-  // read straight from the reduced vector (L2) by the thread that updates the entry
-  double* Q = scr;                                                    // r x r (<= 256)
-  double* Wd = scr + 256;                                             // m x rk
-  float* Wn = reinterpret_cast<float*>(Wd + m * rk);                  // m x rk
-  double* Gp = Wd + m * rk + (m * rk + 1) / 2 + 2;                    // [GC][rk rk]
-  for (int e = tid; e < r * r; e += T) Q[e] = __ldcg(srcv + m * r + e);
-  for (int e = tid; e < m * rk; e += T) Wd[e] = (double)Ws[e];
-  __syncthreads();
-  pstamp2(pa, it, 0);
-  // W <- W o P / (W Q + eps) (fp64, reading R4); Ws / Wn layout [i rk + k], ranks >= r stay 0
-  for (int e0 = tid; e0 < m * rk; e0 += 2 * T) {
+  double* P = scr;                 // m x r
+  double* Qp = scr + ((m * r + 1) & ~1);  // RK x RK (16-byte aligned for the double2 loads)
+  double* Wd = Qp + RK * RK;       // m x RK
+  double* Wnd = Wd + m * RK;       // m x RK
+  double* Gp = Wnd + m * RK;       // [GC][RK][RK]
+  // (P, Q) into shared memory: coalesced, all 8 loads of a thread issued before any is used
+  for (int e0 = 0; e0 < L; e0 += 8 * T) {
+    double v[8];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int e = e0 + u * T;
-      if (e < m * rk) {
-        const int i = e / rk, k = e - (e / rk) * rk;
-        float v = 0.0f;
-        if (k < r) {
-          double d = 0.0;
-          for (int l = 0; l < r; ++l) d += Wd[i * rk + l] * Q[l * r + k];
-          v = (float)mu_quot(Wd[e], __ldcg(srcv + i * r + k), d, (double)eps);
-        }
-        Wn[e] = v;
+    for (int q = 0; q < 8; ++q) {
+      const int e = e0 + q * T + tid;
+      v[q] = e < L ? __ldcg(srcv + e) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = e0 + q * T + tid;
+      if (e < m * r) P[e] = v[q];
+      else if (e < L) {
+        const int f = e - m * r;
+        Qp[(f / r) * RK + f % r] = v[q];
       }
     }
+  }
+  for (int e = tid; e < RK * RK; e += T)
+    if ((e / RK) >= r || (e % RK) >= r) Qp[e] = 0.0;
+  for (int e = tid; e < m * RK; e += T) Wd[e] = (double)Ws[e];
+  __syncthreads();
+  pstamp2(pa, it, 0);
+  // W <- W o P / (W Q + eps) (fp64, reading R4): a thread owns whole rows i (RK independent
+  // chains d_k = sum_l W[i][l] Q[l][k], Q rows broadcast from shared memory)
+  for (int i = tid; i < m; i += T) {
+    double w[RK], d[RK];
+#pragma unroll
+    for (int l = 0; l < RK; l += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(Wd + i * RK + l);
+      w[l] = v.x;
+      w[l + 1] = v.y;
+    }
+#pragma unroll
+    for (int k = 0; k < RK; ++k) d[k] = 0.0;
+#pragma unroll
+    for (int l = 0; l < RK; ++l) {
+#pragma unroll
+      for (int k = 0; k < RK; k += 2) {
+        const double2 q = *reinterpret_cast<const double2*>(Qp + l * RK + k);
+        d[k] = fma(w[l], q.x, d[k]);
+        d[k + 1] = fma(w[l], q.y, d[k + 1]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < RK; ++k)
+      Wnd[i * RK + k] = k < r ? (double)(float)mu_quot(w[k], P[i * r + k], d[k], (double)eps) : 0.0;
   }
   __syncthreads();
   pstamp2(pa, it, 1);
-  for (int e = tid; e < m * rk; e += T) Ws[e] = Wn[e];
-  // G = Wn^T Wn: rk^2 entries x GC row chunks (fixed order), 4 interleaved accumulators per chunk
-  const int RR = rk * rk;
-  const int GC = T / RR < 1 ? 1 : (T / RR > 4 ? 4 : T / RR);
-  for (int t = tid; t < RR * GC; t += T) {
-    const int e = t % RR, c = t / RR;
-    const int k = e / rk, l = e - (e / rk) * rk;
-    const int i0 = m * c / GC, i1 = m * (c + 1) / GC;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    if (k < r && l < r) {
-      int i = i0;
-      for (; i + 3 < i1; i += 4) {
-        s0 += (double)Wn[i * rk + k] * (double)Wn[i * rk + l];
-        s1 += (double)Wn[(i + 1) * rk + k] * (double)Wn[(i + 1) * rk + l];
-        s2 += (double)Wn[(i + 2) * rk + k] * (double)Wn[(i + 2) * rk + l];
-        s3 += (double)Wn[(i + 3) * rk + k] * (double)Wn[(i + 3) * rk + l];
+  for (int e = tid; e < m * RK; e += T) Ws[e] = (float)Wnd[e];
+  // G = Wn^T Wn: thread (k, chunk c) accumulates row k of G over the chunk's rows (RK
+  // independent chains); chunks summed in fixed order below
+  const int GC = T / RK;
+  for (int t = tid; t < RK * GC; t += T) {
+    const int k = t % RK, c = t / RK;
+    const int i0 = (int)((int64_t)m * c / GC), i1 = (int)((int64_t)m * (c + 1) / GC);
+    double g[RK];
+#pragma unroll
+    for (int l = 0; l < RK; ++l) g[l] = 0.0;
+    for (int i = i0; i < i1; ++i) {
+      const double wk = Wnd[i * RK + k];
+#pragma unroll
+      for (int l = 0; l < RK; l += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(Wnd + i * RK + l);
+        g[l] = fma(wk, v.x, g[l]);
+        g[l + 1] = fma(wk, v.y, g[l + 1]);
       }
-      for (; i < i1; ++i) s0 += (double)Wn[i * rk + k] * (double)Wn[i * rk + l];
     }
-    Gp[c * RR + e] = (s0 + s1) + (s2 + s3);
+#pragma unroll
+    for (int l = 0; l < RK; ++l) Gp[(c * RK + k) * RK + l] = g[l];
   }
   __syncthreads();
   pstamp2(pa, it, 2);
-  for (int e = tid; e < RR; e += T) {
+  for (int e = tid; e < RK * RK; e += T) {
     double sg = 0.0;
-    for (int c = 0; c < GC; ++c) sg += Gp[c * RR + e];
-    Gs[e] = (float)sg;
+    for (int c = 0; c < GC; ++c) sg += Gp[c * RK * RK + e];
+    Gs[e] = ((e / RK) < r && (e % RK) < r) ? (float)sg : 0.0f;
   }
-  if (blockIdx.x == 0)
-    for (int e = tid; e < m * r; e += T) pa.Wout[e] = Wn[(e / r) * rk + (e % r)];
+  if (blockIdx.x == 0 && it == pa.iters - 1)  // the final W (later passes only update H)
+    for (int e = tid; e < m * r; e += T) pa.Wout[e] = (float)Wnd[(e / r) * RK + (e % r)];
   __syncthreads();
   pstamp2(pa, it, 3);
 }
@@ -759,7 +787,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   }
   }  // consumer warps
   if (!persist || !do_acc) break;
-  persist_step(pa, epoch, m, r, 8, eps, Ws, Gs, reinterpret_cast<double*>(stages), it);
+  persist_step<8>(pa, epoch, m, r, eps, Ws, Gs, reinterpret_cast<double*>(stages), it);
   }  // passes
 }
 
@@ -1297,15 +1325,16 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   else bcd ? pass_tiles(T_{}, F_{}, T_{}) : pass_tiles(T_{}, F_{}, F_{});
   }  // consumer warps
   if (!persist || !do_acc) break;
-  persist_step(pa, epoch, m, r, RK, eps, Wc, Gs, reinterpret_cast<double*>(stages), it);
+  persist_step<RK>(pa, epoch, m, r, eps, Wc, Gs, reinterpret_cast<double*>(stages), it);
   }  // passes
 }
 
-// shared-memory scratch persist_step takes from the stage area between passes (doubles)
-size_t persist_scratch_bytes(int64_t m, int rk, int threads) {
-  const int RR = rk * rk;
-  const int GC = threads / RR < 1 ? 1 : (threads / RR > 4 ? 4 : threads / RR);
-  return sizeof(double) * (size_t)(256 + m * rk + (m * rk + 1) / 2 + 2 + (int64_t)GC * RR);
+// shared-memory scratch persist_step takes from the stage area between passes
+size_t persist_scratch_bytes(int64_t m, int r, int rk, int threads) {
+  // the slice reduction's [C][ne] partials (<= threads doubles) also live in the scratch
+  int64_t d = persist_scratch_doubles(m, r, rk, threads);
+  if (d < threads) d = threads;
+  return sizeof(double) * (size_t)d;
 }
 
 size_t fixed_bytes_c(int MP, int NW, int RK) {
@@ -1343,7 +1372,7 @@ cudaError_t launch_c(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_
   const size_t SB = (size_t)MP * 128 + RK * 128;
   const size_t smem = (size_t)ns * SB + fixed_bytes_c(MP, NW, RK);
   if (ns < 2) return cudaErrorInvalidConfiguration;
-  if (pa.iters > 0 && persist_scratch_bytes(m, RK, (NW + 1) * 32) > (size_t)ns * SB) return cudaErrorInvalidConfiguration;
+  if (pa.iters > 0 && persist_scratch_bytes(m, r, RK, (NW + 1) * 32) > (size_t)ns * SB) return cudaErrorInvalidConfiguration;
   cudaError_t e = cudaFuncSetAttribute(k_fused_c<MP, NW, RK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_maybe_coop(k_fused_c<MP, NW, RK>, grid, (NW + 1) * 32, smem, st, pa.iters > 0, mx, mh, m, n, r, W,
@@ -1420,7 +1449,7 @@ cudaError_t launch_t(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_
   int ns = FOLD ? (int)((SMEM_BUDGET - fixed_bytes(UX, NWT, HD)) / SB) : stages_for(UX, NWT, HD, BNT);
   if (ns > 24) ns = 24;
   const size_t smem = (size_t)ns * SB + fixed_bytes(UX, NWT, HD);
-  if (pa.iters > 0 && persist_scratch_bytes(m, r, (NWT + 1) * 32) > (size_t)ns * SB) return cudaErrorInvalidConfiguration;
+  if (pa.iters > 0 && persist_scratch_bytes(m, r, 8, (NWT + 1) * 32) > (size_t)ns * SB) return cudaErrorInvalidConfiguration;
   cudaError_t e = cudaFuncSetAttribute(k_fused<R, UX, NWT, HD, BNT, FOLD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_maybe_coop(k_fused<R, UX, NWT, HD, BNT, FOLD>, grid, (NWT + 1) * 32, smem, st, pa.iters > 0, mx, mh,
@@ -1803,7 +1832,7 @@ k_fused_m(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   else pass_tiles(T_{}, F_{});
   }  // consumer warps
   if (!persist || !do_acc) break;
-  persist_step(pa, epoch, m, r, 8, eps, Ws, Gs, reinterpret_cast<double*>(stages), it);
+  persist_step<8>(pa, epoch, m, r, eps, Ws, Gs, reinterpret_cast<double*>(stages), it);
   }  // passes
 }
 
@@ -1819,7 +1848,7 @@ cudaError_t launch_m(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_
                      int evict_first, const PersistArgs& pa, cudaStream_t st) {
   const int ns = stages_m();
   const size_t smem = (size_t)ns * SBM + fixed_bytes_m();
-  if (pa.iters > 0 && persist_scratch_bytes(m, 8, (NWM + 1) * 32) > (size_t)ns * SBM) return cudaErrorInvalidConfiguration;
+  if (pa.iters > 0 && persist_scratch_bytes(m, r, 8, (NWM + 1) * 32) > (size_t)ns * SBM) return cudaErrorInvalidConfiguration;
   cudaError_t e = cudaFuncSetAttribute(k_fused_m, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_maybe_coop(k_fused_m, grid, (NWM + 1) * 32, smem, st, pa.iters > 0, mx, mh, m, n, r, W, Gpart, nG,

@@ -20,20 +20,27 @@ namespace {
 constexpr int TINY_THREADS = 512;
 constexpr int TINY_BLK = 64;  // fp32 partial block: 32 lanes x 64 columns
 
+// shared-memory row stride of X and H: odd, so that threads reading one column of
+// consecutive rows hit distinct banks
+__host__ __device__ inline int tiny_ld(int n) { return (n & 1) ? n : n + 1; }
+
 template <int R>
 struct TinyLayout {
   // offsets in bytes, all 16-aligned
   static size_t bytes(int m, int n, int nch) {
+    const size_t ld = (size_t)tiny_ld(n);
     size_t o = 0;
     auto al = [](size_t v) { return (v + 15) & ~size_t(15); };
-    o = al(o + sizeof(float) * (size_t)m * n);        // X
-    o = al(o + sizeof(float) * (size_t)R * n);        // H (rows >= r zero)
+    o = al(o + sizeof(float) * (size_t)m * ld);       // X
+    o = al(o + sizeof(float) * (size_t)R * ld);       // H (rows >= r zero)
     o = al(o + sizeof(float) * (size_t)m * R);        // W
     o = al(o + sizeof(float) * (size_t)m * R);        // W new
     o = al(o + sizeof(double) * (size_t)m * R);       // P
     o = al(o + sizeof(double) * (size_t)R * R);       // Q
     o = al(o + sizeof(float) * (size_t)R * R);        // G (fp32 for E = G H)
     o = al(o + sizeof(double) * (size_t)nch * (m * R + R * R));  // chunk partials (n <= 256)
+    o = al(o + sizeof(float) * (size_t)R * ld);       // H new (row-chunked H update)
+    o = al(o + sizeof(double) * (size_t)TINY_THREADS);  // S / G row-chunk partials
     return o;
   }
 };
@@ -44,11 +51,12 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
        float* __restrict__ H, int nch) {
   extern __shared__ __align__(16) unsigned char sm[];
   auto al = [](size_t v) { return (v + 15) & ~size_t(15); };
+  const int ld = tiny_ld(n);
   size_t o = 0;
   float* Xs = reinterpret_cast<float*>(sm + o);
-  o = al(o + sizeof(float) * (size_t)m * n);
+  o = al(o + sizeof(float) * (size_t)m * ld);
   float* Hs = reinterpret_cast<float*>(sm + o);
-  o = al(o + sizeof(float) * (size_t)R * n);
+  o = al(o + sizeof(float) * (size_t)R * ld);
   float* Ws = reinterpret_cast<float*>(sm + o);
   o = al(o + sizeof(float) * (size_t)m * R);
   float* Wn = reinterpret_cast<float*>(sm + o);
@@ -60,15 +68,19 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
   float* Gf = reinterpret_cast<float*>(sm + o);
   o = al(o + sizeof(float) * (size_t)R * R);
   double* part = reinterpret_cast<double*>(sm + o);
+  o = al(o + sizeof(double) * (size_t)nch * (m * R + R * R));
+  float* Hn = reinterpret_cast<float*>(sm + o);
+  o = al(o + sizeof(float) * (size_t)R * ld);
+  double* cp = reinterpret_cast<double*>(sm + o);  // TINY_THREADS doubles
 
   const int tid = threadIdx.x, T = blockDim.x;
   for (int64_t e = tid; e < (int64_t)m * n; e += T) {
     const int i = (int)(e / n), j = (int)(e % n);
-    Xs[e] = X[(int64_t)i * ldx + j];
+    Xs[i * ld + j] = X[(int64_t)i * ldx + j];
   }
   for (int e = tid; e < R * n; e += T) {
     const int k = e / n, j = e % n;
-    Hs[e] = k < r ? H[(int64_t)k * n + j] : 0.0f;
+    Hs[k * ld + j] = k < r ? H[(int64_t)k * n + j] : 0.0f;
   }
   for (int e = tid; e < m * R; e += T) {
     const int i = e / R, k = e % R;
@@ -78,14 +90,28 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
 
   const int EP = m * R, EQ = R * R, E = EP + EQ;
   const int nblk = (n + TINY_BLK - 1) / TINY_BLK;
+  const int ES = R * n;
+  // row chunks of the tall-X H update (S = W^T X entry-parallel; see below)
+  int cs = T / ES;
+  cs = cs < 1 ? 1 : cs;
+  if (cs > m / 16) cs = m / 16 < 1 ? 1 : m / 16;
+  const bool tall = m > 64 || 2 * ES <= T;
   for (int it = 0; it < iters; ++it) {
     if (n <= 256) {
     // ---- short rows: P = X H^T and Q = H H^T entry-parallel, entry e x chunk c of
-    //      64-column blocks, fp32 inside a block, fp64 across
+    //      64-column blocks, fp32 inside a block, fp64 across.  P entries run row-fastest
+    //      (e = k m + i: one X row per thread at a common column, H broadcast)
     for (int t = tid; t < E * nch; t += T) {
       const int e = t % E, c = t / E;
-      const float* a = e < EP ? Xs + (e / R) * n : Hs + ((e - EP) / R) * n;
-      const float* bv = e < EP ? Hs + (e % R) * n : Hs + ((e - EP) % R) * n;
+      const float* a;
+      const float* bv;
+      if (e < EP) {
+        a = Xs + (e % m) * ld;
+        bv = Hs + (e / m) * ld;
+      } else {
+        a = Hs + ((e - EP) / R) * ld;
+        bv = Hs + ((e - EP) % R) * ld;
+      }
       const int b0 = nblk * c / nch, b1 = nblk * (c + 1) / nch;
       double acc = 0.0;
       for (int bk = b0; bk < b1; ++bk) {
@@ -105,7 +131,7 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
     for (int e = tid; e < E; e += T) {
       double sv = 0.0;
       for (int c = 0; c < nch; ++c) sv += part[c * E + e];
-      if (e < EP) P[e] = sv;
+      if (e < EP) P[(e % m) * R + e / m] = sv;
       else Q[e - EP] = sv;
     }
     __syncthreads();
@@ -116,7 +142,7 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
     {
       const int warp = tid >> 5, lane = tid & 31, nw = T >> 5;
       for (int task = warp; task < m + R; task += nw) {
-        const float* a = task < m ? Xs + (int64_t)task * n : Hs + (int64_t)(task - m) * n;
+        const float* a = task < m ? Xs + (int64_t)task * ld : Hs + (int64_t)(task - m) * ld;
         double acc[R];
 #pragma unroll
         for (int k = 0; k < R; ++k) acc[k] = 0.0;
@@ -128,7 +154,7 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
           for (int j = j0 + lane; j < j1; j += 32) {
             const float x = a[j];
 #pragma unroll
-            for (int k = 0; k < R; ++k) s[k] = fmaf(x, Hs[k * n + j], s[k]);
+            for (int k = 0; k < R; ++k) s[k] = fmaf(x, Hs[k * ld + j], s[k]);
           }
 #pragma unroll
           for (int k = 0; k < R; ++k) acc[k] += (double)s[k];
@@ -164,25 +190,88 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
     }
     __syncthreads();
     for (int e = tid; e < EP; e += T) Ws[e] = Wn[e];
-    // ---- G = W^T W (fp64, fixed order over rows)
-    for (int e = tid; e < EQ; e += T) {
-      const int k = e / R, l = e % R;
-      double s = 0.0;
-      if (k < r && l < r)
-        for (int i = 0; i < m; ++i) s += (double)Wn[i * R + k] * (double)Wn[i * R + l];
-      Gf[e] = (float)s;
+    // ---- G = W^T W (fp64): gc row chunks (fixed order), summed in chunk order
+    {
+      int gc = T / EQ;
+      gc = gc < 1 ? 1 : (gc > 8 ? 8 : gc);
+      if (gc > m) gc = m;
+      for (int t = tid; t < EQ * gc; t += T) {
+        const int e = t % EQ, c = t / EQ;
+        const int k = e / R, l = e % R;
+        const int i0 = m * c / gc, i1 = m * (c + 1) / gc;
+        double s0 = 0.0, s1 = 0.0;
+        if (k < r && l < r) {
+          int i = i0;
+          for (; i + 1 < i1; i += 2) {
+            s0 += (double)Wn[i * R + k] * (double)Wn[i * R + l];
+            s1 += (double)Wn[(i + 1) * R + k] * (double)Wn[(i + 1) * R + l];
+          }
+          if (i < i1) s0 += (double)Wn[i * R + k] * (double)Wn[i * R + l];
+        }
+        cp[c * EQ + e] = s0 + s1;
+      }
+      __syncthreads();
+      for (int e = tid; e < EQ; e += T) {
+        double s = 0.0;
+        for (int c = 0; c < gc; ++c) s += cp[c * EQ + e];
+        Gf[e] = (float)s;
+      }
     }
     __syncthreads();
+    if (tall) {
+      // ---- H update for tall X (few columns per thread): S = W^T X entry-parallel over
+      //      (k, j) x cs row chunks (fp32 inside a chunk, fp64 across), then E = G H and the
+      //      quotient; consecutive threads take consecutive columns (conflict-free X reads)
+      for (int t = tid; t < ES * cs; t += T) {
+        const int e = t % ES, c = t / ES;
+        const int k = e / n, j = e % n;
+        const int i0 = m * c / cs, i1 = m * (c + 1) / cs;
+        float s0 = 0.0f, s1 = 0.0f;
+        int i = i0;
+        for (; i + 1 < i1; i += 2) {
+          s0 = fmaf(Ws[i * R + k], Xs[i * ld + j], s0);
+          s1 = fmaf(Ws[(i + 1) * R + k], Xs[(i + 1) * ld + j], s1);
+        }
+        if (i < i1) s0 = fmaf(Ws[i * R + k], Xs[i * ld + j], s0);
+        if (cs == 1) {
+          float ek = 0.0f;
+#pragma unroll
+          for (int l = 0; l < R; ++l) ek = fmaf(Gf[k * R + l], Hs[l * ld + j], ek);
+          Hn[k * ld + j] = (k < r) ? mu_quot(Hs[k * ld + j], s0 + s1, ek, eps) : 0.0f;
+        } else {
+          cp[c * ES + e] = (double)(s0 + s1);
+        }
+      }
+      __syncthreads();
+      if (cs > 1) {
+        for (int e = tid; e < ES; e += T) {
+          const int k = e / n, j = e % n;
+          double s = 0.0;
+          for (int c = 0; c < cs; ++c) s += cp[c * ES + e];
+          float ek = 0.0f;
+#pragma unroll
+          for (int l = 0; l < R; ++l) ek = fmaf(Gf[k * R + l], Hs[l * ld + j], ek);
+          Hn[k * ld + j] = (k < r) ? mu_quot(Hs[k * ld + j], (float)s, ek, eps) : 0.0f;
+        }
+        __syncthreads();
+      }
+      for (int e = tid; e < ES; e += T) {
+        const int k = e / n, j = e % n;
+        Hs[k * ld + j] = Hn[k * ld + j];
+      }
+      __syncthreads();
+      continue;
+    }
     // ---- H update, one thread per column: S = W^T X[:, j], E = G H[:, j]
     for (int j = tid; j < n; j += T) {
       float s[R], h[R];
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         s[k] = 0.0f;
-        h[k] = Hs[k * n + j];
+        h[k] = Hs[k * ld + j];
       }
       for (int i = 0; i < m; ++i) {
-        const float x = Xs[i * n + j];
+        const float x = Xs[i * ld + j];
 #pragma unroll
         for (int k = 0; k < R; ++k) s[k] = fmaf(Ws[i * R + k], x, s[k]);
       }
@@ -191,12 +280,12 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
         float ek = 0.0f;
 #pragma unroll
         for (int l = 0; l < R; ++l) ek = fmaf(Gf[k * R + l], h[l], ek);
-        Hs[k * n + j] = (k < r) ? mu_quot(h[k], s[k], ek, eps) : 0.0f;
+        Hs[k * ld + j] = (k < r) ? mu_quot(h[k], s[k], ek, eps) : 0.0f;
       }
     }
     __syncthreads();
   }
-  for (int e = tid; e < r * n; e += T) H[e] = Hs[e];
+  for (int e = tid; e < r * n; e += T) H[e] = Hs[(e / n) * ld + e % n];
   for (int e = tid; e < m * r; e += T) W[e] = Ws[(e / r) * R + (e % r)];
 }
 

@@ -1968,6 +1968,31 @@ int ntt_dist_size(ntt_handle h) { return h ? h->nranks : -1; }
 
 extern "C" int64_t ntt_collective_count(ntt_handle h) { return h ? h->collectives : -1; }
 
+extern "C" ntt_status ntt_stream_ceiling(ntt_handle h, const void* buf, int64_t bytes, int32_t reps, double* gbps) {
+  if (!h || !buf || !gbps || bytes < 16 || (bytes & 15) || reps < 1 || (reinterpret_cast<uintptr_t>(buf) & 15))
+    return NTT_ERR_INVALID_ARG;
+  cudaPointerAttributes pa;
+  if (cudaPointerGetAttributes(&pa, buf) != cudaSuccess || pa.type != cudaMemoryTypeDevice)
+    return fail(h, NTT_ERR_INVALID_ARG, "ntt_stream_ceiling: buf must be device memory");
+  float* sink = nullptr;
+  CU(h, cudaMallocAsync(reinterpret_cast<void**>(&sink), 16, h->stream));
+  cudaEvent_t e0, e1;
+  CU(h, cudaEventCreate(&e0));
+  CU(h, cudaEventCreate(&e1));
+  LAUNCH(h, launch_read_stream(buf, bytes, sink, h->num_sms, h->stream));  // warm-up
+  CU(h, cudaEventRecord(e0, h->stream));
+  for (int i = 0; i < reps; ++i) LAUNCH(h, launch_read_stream(buf, bytes, sink, h->num_sms, h->stream));
+  CU(h, cudaEventRecord(e1, h->stream));
+  CU(h, cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CU(h, cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  CU(h, cudaFreeAsync(sink, h->stream));
+  *gbps = (double)bytes * reps / (ms * 1e-3) / 1e9;
+  return NTT_OK;
+}
+
 extern "C" ntt_status ntt_debug_fill_uniform_cols(ntt_handle h, float* H, int32_t r, int64_t nloc, int64_t b,
                                                   int64_t nd, int64_t off, int64_t nglob, uint64_t seed,
                                                   uint64_t stream) {

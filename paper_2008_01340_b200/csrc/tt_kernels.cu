@@ -55,14 +55,16 @@ cudaError_t launch_contract_right(const float* G, int rp, int64_t nl, int rl, co
   return cudaGetLastError();
 }
 
-// Streaming kernel.  Work item = (block of 32 rows a, block of 1024 columns b);
+// Streaming kernel.  Work item = (block of 64 rows a, block of 1024 columns b);
 // thread owns 4 consecutive columns, keeps R[:, b..b+3] in registers for the
-// whole row block (R is read from L2 once per 32 rows), L rows of the block are
+// whole row block (R is read from L2 once per 64 rows), L rows of the block are
 // staged in smem (broadcast).  A~ (and noise) are formed in fp32; ||ref - A~||^2
-// and ||ref||^2 per thread in fp32 over the 32 rows, then fp64 across items.
+// and ||ref||^2 per thread in fp32 over the 64 rows, then fp64 across items.
+// The error-only form (no output) issues the 128-bit loads of 8 rows before it
+// uses any (8 x 16 B in flight per thread: the stream is latency-bound otherwise).
 // Persistent grid (<= 8 CTAs/SM) -> one fp64 (num, den) partial per CTA.
 constexpr int TS_THREADS = 256;
-constexpr int TS_RA = 32;
+constexpr int TS_RA = 64;
 constexpr int TS_CB = 4 * TS_THREADS;
 
 template <int RK>
@@ -103,6 +105,34 @@ k_tt_stream(const float* __restrict__ L, const float* __restrict__ R, int64_t NL
       }
     }
     float fnum = 0.0f, fden = 0.0f;
+    if (RK <= 16 && !out && ref && full4 && rows == TS_RA) {
+#pragma unroll 1
+      for (int a8 = 0; a8 < TS_RA; a8 += 8) {
+        float4 xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xv[u] = __ldcs(reinterpret_cast<const float4*>(ref + (a0 + a8 + u) * NR + b0));
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          float v[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int q = 0; q < RK; ++q) {
+            const float lq = Ls[a8 + u][q];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) v[t] = fmaf(lq, rq[q][t], v[t]);
+          }
+          const float x[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float e = x[t] - v[t];
+            fnum = fmaf(e, e, fnum);
+            fden = fmaf(x[t], x[t], fden);
+          }
+        }
+      }
+      num += (double)fnum;
+      den += (double)fden;
+      continue;
+    }
     for (int aa = 0; aa < rows; ++aa) {
       float v[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -184,6 +214,32 @@ cudaError_t launch_tt_stream(const float* L, const float* R, int64_t NL, int64_t
   else if (rk <= 32) TS(32);
   else TS(64);
 #undef TS
+  return cudaGetLastError();
+}
+
+// Read-only HBM stream (the harness-measured ceiling of BASELINE.md s.3, reported next to the
+// roofline): 128-bit evict-first loads, 8 independent loads per thread in flight, grid-stride.
+// The sum is stored only if it equals a value no finite input produces, so the loads stay live.
+__global__ void __launch_bounds__(256) k_read_stream(const float4* __restrict__ p, int64_t n4, float* __restrict__ sink) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  float acc = 0.0f;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 7 * stride < n4; i += 8 * stride) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcs(p + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += (v[u].x + v[u].y) + (v[u].z + v[u].w);
+  }
+  for (; i < n4; i += stride) {
+    const float4 v = __ldcs(p + i);
+    acc += (v.x + v.y) + (v.z + v.w);
+  }
+  if (acc == -1.0e38f) sink[0] = acc;
+}
+
+cudaError_t launch_read_stream(const void* buf, int64_t bytes, float* sink, int num_sms, cudaStream_t st) {
+  k_read_stream<<<num_sms * 8, 256, 0, st>>>(reinterpret_cast<const float4*>(buf), bytes / 16, sink);
   return cudaGetLastError();
 }
 
