@@ -285,168 +285,221 @@ k_skinny_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 }
 
 // ---------------------------------------------------------------- updates ---
-constexpr int UPD_ROWS = 128;
+// Both update kernels work on blocks of UPD_B rows (W) / columns (H) with 4 threads per row /
+// column, each owning ranks k = kq + 4u: the per-thread serial work (the latency that bounds
+// these small kernels: ~3 k warp instructions at 9.5 cycles each with one thread per row, ncu on
+// config 2) is a quarter, and config 2's 4096 rows / columns give 128 CTAs instead of 32.
+constexpr int UPD_THREADS = 128;
+constexpr int UPD_B = 32;
 
-// W update for TC_ROWS rows per CTA: P = sum_s Ppart[s] (fixed order), Q (r x r,
-// reduced), W <- W o P / (W Q + eps) in fp64 (as k_wupdate), WcatT rows k < r:
-// hi = Wn, rows R + k: lo(Wn); Gpart[cta] = Wn^T Wn over the CTA's rows.
+// W update for UPD_B rows per CTA: P = sum_s Ppart[s] (fixed order), Q (r x r, reduced),
+// W <- W o P / (W Q + eps) in fp64 (as k_wupdate), WcatT rows k < r: hi = Wn, rows R + k:
+// lo(Wn); Gpart[cta] = Wn^T Wn over the CTA's rows.
 template <int R>
-__global__ void __launch_bounds__(UPD_ROWS)
+__global__ void __launch_bounds__(UPD_THREADS)
 k_tc_wupdate(float* __restrict__ W, int64_t m, int r, const double* __restrict__ Ppart, int nP,
              const double* __restrict__ Qred, float eps, float* __restrict__ WcatT, int64_t ldw,
              double* __restrict__ Gpart, unsigned* __restrict__ maxw) {
+  constexpr int U = R / 4;
   __shared__ double Qs[R * R];
-  __shared__ float Wn[UPD_ROWS][R + 1];
-  // the CTA's rows own a contiguous run of rows * r doubles in every split partial: summed
-  // coalesced (thread t: elements t + 128 q, in split order) straight into shared memory (no
-  // register staging: fewer registers, more CTAs per SM for this latency-bound kernel)
-  extern __shared__ double Ps[];  // UPD_ROWS * r
+  __shared__ double Ps[UPD_B * R];
+  __shared__ float Wo[UPD_B][R + 1];
+  __shared__ float Wn[UPD_B][R + 1];
+  const int tid = threadIdx.x;
   const int rr = r * r;
-  for (int t = threadIdx.x; t < R * R; t += blockDim.x) {
+  const int64_t i0 = (int64_t)blockIdx.x * UPD_B;
+  const int rows = (int)min((int64_t)UPD_B, m - i0);
+  for (int t = tid; t < R * R; t += UPD_THREADS) {
     const int k = t / R, l = t % R;
     Qs[t] = (k < r && l < r) ? Qred[k * r + l] : 0.0;
   }
-  const int64_t i0 = (int64_t)blockIdx.x * UPD_ROWS;
-  const int64_t i = i0 + threadIdx.x;
+  for (int e = tid; e < UPD_B * R; e += UPD_THREADS) {
+    const int row = e / R, k = e % R;
+    Wo[row][k] = (row < rows && k < r) ? W[(i0 + row) * r + k] : 0.0f;
+  }
   {
-    const int len = (int)(min((int64_t)UPD_ROWS, m - i0) * r);
+    // the block's rows are a contiguous run of rows * r doubles in every split partial:
+    // element e = tid + 128 q, fp64 sums in registers, each split's loads issued together
+    const int len = rows * r;
     const int64_t mr = m * r;
-    for (int e = threadIdx.x; e < len; e += UPD_ROWS) Ps[e] = 0.0;
+    double acc[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) acc[q] = 0.0;
     for (int b = 0; b < nP; ++b) {
       const double* src = Ppart + (int64_t)b * mr + i0 * r;
-      for (int e = threadIdx.x; e < len; e += UPD_ROWS) Ps[e] += src[e];
+      double v[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int e = tid + q * UPD_THREADS;
+        v[q] = e < len ? __ldcg(src + e) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) acc[q] += v[q];
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int e = tid + q * UPD_THREADS;
+      if (e < len) Ps[(e / r) * R + e % r] = acc[q];
     }
   }
   __syncthreads();
-  if (i < m) {
-    double w[R];
+  float wmax = 0.0f;
+  {
+    const int row = tid >> 2, kq = tid & 3;
+    double d[U];
 #pragma unroll
-    for (int k = 0; k < R; ++k) w[k] = (k < r) ? (double)W[i * r + k] : 0.0;
+    for (int u = 0; u < U; ++u) d[u] = 0.0;
 #pragma unroll
-    for (int k = 0; k < R; ++k) {
+    for (int l = 0; l < R; ++l) {
+      const double wl = (double)Wo[row][l];
+#pragma unroll
+      for (int u = 0; u < U; ++u) d[u] = fma(wl, Qs[l * R + kq + 4 * u], d[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = kq + 4 * u;
       float wn = 0.0f;
-      if (k < r) {
-        const double p = Ps[threadIdx.x * r + k];
-        double d = 0.0;
-#pragma unroll
-        for (int l = 0; l < R; ++l) d += w[l] * Qs[l * R + k];
-        wn = (float)mu_quot(w[k], p, d, (double)eps);
-      }
-      Wn[threadIdx.x][k] = wn;
+      if (row < rows && k < r) wn = (float)mu_quot((double)Wo[row][k], Ps[row * R + k], d[u], (double)eps);
+      Wn[row][k] = wn;
+      wmax = fmaxf(wmax, wn);
     }
-    for (int k = 0; k < r; ++k) W[i * r + k] = Wn[threadIdx.x][k];
-    if (maxw) {  // max |W| for the fp16x2 scale (fp16 variant); order-independent
-      float mx = 0.0f;
-      for (int k = 0; k < r; ++k) mx = fmaxf(mx, Wn[threadIdx.x][k]);
-      atomicMax(maxw, __float_as_uint(mx));
-    }
-    if (WcatT) {
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        const float v = Wn[threadIdx.x][k];
-        WcatT[(int64_t)k * ldw + i] = v;
-        WcatT[(int64_t)(R + k) * ldw + i] = tf32_lo(v);
-      }
-    }
-  } else {
-    for (int k = 0; k < R; ++k) Wn[threadIdx.x][k] = 0.0f;
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < rr; t += blockDim.x) {
+  for (int e = tid; e < rows * r; e += UPD_THREADS) W[i0 * r + e] = Wn[e / r][e % r];
+  if (maxw) {  // max |W| for the fp16x2 scale (fp16 variant); order-independent
+    for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+    if ((tid & 31) == 0) atomicMax(maxw, __float_as_uint(wmax));
+  }
+  if (WcatT)
+    for (int e = tid; e < R * UPD_B; e += UPD_THREADS) {
+      const int k = e / UPD_B, row = e % UPD_B;
+      if (row < rows) {
+        const float v = Wn[row][k];
+        WcatT[(int64_t)k * ldw + i0 + row] = v;
+        WcatT[(int64_t)(R + k) * ldw + i0 + row] = tf32_lo(v);
+      }
+    }
+  for (int t = tid; t < rr; t += UPD_THREADS) {
     const int k = t / r, l = t % r;
-    double s = 0.0;
-    for (int qq = 0; qq < UPD_ROWS; ++qq) s += (double)Wn[qq][k] * (double)Wn[qq][l];
-    Gpart[(int64_t)blockIdx.x * rr + t] = s;
+    double s0 = 0.0, s1 = 0.0;
+    for (int q = 0; q < UPD_B; q += 2) {
+      s0 = fma((double)Wn[q][k], (double)Wn[q][l], s0);
+      s1 = fma((double)Wn[q + 1][k], (double)Wn[q + 1][l], s1);
+    }
+    Gpart[(int64_t)blockIdx.x * rr + t] = s0 + s1;
   }
 }
 
-// H update (or prep: update = false keeps H) for UPD_ROWS columns per CTA:
+// H update (or prep: update = false keeps H) for blocks of UPD_B columns (grid-stride):
 // S = sum_s Spart[s][j] (fixed order), E = G H (fp32, G reduced in fp64),
 // H <- H o S / (E + eps); Hcat rows k < r: hi = Hn, rows R + k: lo(Hn);
-// Qpart[cta] = Hn Hn^T over the CTA's columns.
+// Qpart[cta] = Hn Hn^T over the CTA's columns (fp64, in block order: deterministic).
 template <int R>
-__global__ void __launch_bounds__(UPD_ROWS)
+__global__ void __launch_bounds__(UPD_THREADS)
 k_tc_hupdate(float* __restrict__ H, int64_t n, int r, const double* __restrict__ Spart, int nS,
              const double* __restrict__ Gred, float eps, bool update, float* __restrict__ Hcat, int64_t ldh,
              double* __restrict__ Qpart, unsigned* __restrict__ maxh) {
+  constexpr int U = R / 4;
+  constexpr int NQ = (R * R + UPD_THREADS - 1) / UPD_THREADS;
   float hmax = 0.0f;
   __shared__ float Gs[R * R];
-  __shared__ float Hn[R][UPD_ROWS + 1];
-  // S of the block's 128 columns (a contiguous run of cols * r doubles per split), summed
-  // coalesced straight into shared memory in split order (no register staging)
-  extern __shared__ double Ss[];  // UPD_ROWS * r
+  __shared__ float Ho[R][UPD_B + 1];
+  __shared__ float Hn[R][UPD_B + 1];
+  __shared__ double Ss[UPD_B * R];
+  const int tid = threadIdx.x;
   const int rr = r * r;
   if (update)
-    for (int t = threadIdx.x; t < R * R; t += blockDim.x) {
+    for (int t = tid; t < R * R; t += UPD_THREADS) {
       const int k = t / R, l = t % R;
       Gs[t] = (k < r && l < r) ? (float)Gred[k * r + l] : 0.0f;
     }
-  // grid-stride over 128-column blocks; Q partial of this CTA accumulated in fp64 in
-  // block order (fixed, so deterministic), one entry per thread (rr <= 1024)
-  double qacc[(R * R + UPD_ROWS - 1) / UPD_ROWS];
+  double qacc[NQ];
 #pragma unroll
-  for (int u = 0; u < (R * R + UPD_ROWS - 1) / UPD_ROWS; ++u) qacc[u] = 0.0;
-  const int64_t nblk = (n + UPD_ROWS - 1) / UPD_ROWS;
+  for (int u = 0; u < NQ; ++u) qacc[u] = 0.0;
+  const int64_t nblk = (n + UPD_B - 1) / UPD_B;
   for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int64_t j0 = blk * UPD_B;
+    const int cols = (int)min((int64_t)UPD_B, n - j0);
     __syncthreads();
-    const int64_t j = blk * UPD_ROWS + threadIdx.x;
-    if (update) {
-      const int len = (int)(min((int64_t)UPD_ROWS, n - blk * UPD_ROWS) * r);
-      const int64_t nr = n * r;
-      for (int e = threadIdx.x; e < len; e += UPD_ROWS) Ss[e] = 0.0;
-      for (int b = 0; b < nS; ++b) {
-        const double* src = Spart + (int64_t)b * nr + blk * UPD_ROWS * r;
-        for (int e = threadIdx.x; e < len; e += UPD_ROWS) Ss[e] += src[e];
-      }
-      __syncthreads();
+    for (int e = tid; e < R * UPD_B; e += UPD_THREADS) {
+      const int k = e / UPD_B, c = e % UPD_B;
+      Ho[k][c] = (k < r && c < cols) ? H[(int64_t)k * n + j0 + c] : 0.0f;
     }
-    if (j < n) {
-      float h[R];
+    if (update) {
+      const int len = cols * r;
+      const int64_t nr = n * r;
+      double acc[U];
 #pragma unroll
-      for (int k = 0; k < R; ++k) h[k] = (k < r) ? H[(int64_t)k * n + j] : 0.0f;
+      for (int q = 0; q < U; ++q) acc[q] = 0.0;
+      for (int b = 0; b < nS; ++b) {
+        const double* src = Spart + (int64_t)b * nr + j0 * r;
+        double v[U];
 #pragma unroll
-      for (int k = 0; k < R; ++k) {
-        float hn = h[k];
-        if (update && k < r) {
-          const double sd = Ss[threadIdx.x * r + k];
+        for (int q = 0; q < U; ++q) {
+          const int e = tid + q * UPD_THREADS;
+          v[q] = e < len ? __ldcg(src + e) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q) acc[q] += v[q];
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int e = tid + q * UPD_THREADS;
+        if (e < len) Ss[(e / r) * R + e % r] = acc[q];
+      }
+    }
+    __syncthreads();
+    {
+      const int c = tid >> 2, kq = tid & 3;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = kq + 4 * u;
+        float hn = Ho[k][c];
+        if (update && k < r && c < cols) {
           float e = 0.0f;
 #pragma unroll
-          for (int l = 0; l < R; ++l) e = fmaf(Gs[k * R + l], h[l], e);
-          hn = mu_quot(h[k], (float)sd, e, eps);
+          for (int l = 0; l < R; ++l) e = fmaf(Gs[k * R + l], Ho[l][c], e);
+          hn = mu_quot(hn, (float)Ss[c * R + k], e, eps);
         }
-        if (k >= r) hn = 0.0f;
+        if (k >= r || c >= cols) hn = 0.0f;
         hmax = fmaxf(hmax, hn);
-        Hn[k][threadIdx.x] = hn;
-        if (update && k < r) H[(int64_t)k * n + j] = hn;
-        if (Hcat) {
-          Hcat[(int64_t)k * ldh + j] = hn;
-          Hcat[(int64_t)(R + k) * ldh + j] = tf32_lo(hn);
-        }
+        Hn[k][c] = hn;
       }
-    } else {
-#pragma unroll
-      for (int k = 0; k < R; ++k) Hn[k][threadIdx.x] = 0.0f;
     }
     __syncthreads();
+    for (int e = tid; e < R * UPD_B; e += UPD_THREADS) {
+      const int k = e / UPD_B, c = e % UPD_B;
+      if (c < cols) {
+        const float v = Hn[k][c];
+        if (update && k < r) H[(int64_t)k * n + j0 + c] = v;
+        if (Hcat) {
+          Hcat[(int64_t)k * ldh + j0 + c] = v;
+          Hcat[(int64_t)(R + k) * ldh + j0 + c] = tf32_lo(v);
+        }
+      }
+    }
 #pragma unroll
-    for (int u = 0; u < (R * R + UPD_ROWS - 1) / UPD_ROWS; ++u) {
-      const int t = threadIdx.x + u * UPD_ROWS;
+    for (int u = 0; u < NQ; ++u) {
+      const int t = tid + u * UPD_THREADS;
       if (t < rr) {
         const int k = t / r, l = t % r;
-        double sq = 0.0;
-        for (int c = 0; c < UPD_ROWS; ++c) sq += (double)Hn[k][c] * (double)Hn[l][c];
-        qacc[u] += sq;
+        double s0 = 0.0, s1 = 0.0;
+        for (int c = 0; c < UPD_B; c += 2) {
+          s0 = fma((double)Hn[k][c], (double)Hn[l][c], s0);
+          s1 = fma((double)Hn[k][c + 1], (double)Hn[l][c + 1], s1);
+        }
+        qacc[u] += s0 + s1;
       }
     }
   }
 #pragma unroll
-  for (int u = 0; u < (R * R + UPD_ROWS - 1) / UPD_ROWS; ++u) {
-    const int t = threadIdx.x + u * UPD_ROWS;
+  for (int u = 0; u < NQ; ++u) {
+    const int t = tid + u * UPD_THREADS;
     if (t < rr) Qpart[(int64_t)blockIdx.x * rr + t] = qacc[u];
   }
   if (maxh) {  // max |H| for the fp16x2 scale (fp16 variant)
     for (int o = 16; o > 0; o >>= 1) hmax = fmaxf(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(maxh, __float_as_uint(hmax));
+    if ((tid & 31) == 0) atomicMax(maxh, __float_as_uint(hmax));
   }
 }
 
@@ -554,8 +607,8 @@ TcPlan plan_tc(int64_t m, int64_t n, int r, int num_sms) {
   p.ldw = (m + 3) & ~int64_t(3);
   pick_split((m + TC_BM - 1) / TC_BM, (n + TC_BK - 1) / TC_BK, num_sms, &p.splitW, &p.kchW);
   pick_split((n + TC_BM - 1) / TC_BM, (m + TC_BK - 1) / TC_BK, num_sms, &p.splitH, &p.kchH);
-  p.nG = (int)((m + UPD_ROWS - 1) / UPD_ROWS);
-  p.nQ = (int)std::min<int64_t>((n + UPD_ROWS - 1) / UPD_ROWS, 4 * num_sms);  // H-update CTAs (grid-stride)
+  p.nG = (int)((m + UPD_B - 1) / UPD_B);
+  p.nQ = (int)std::min<int64_t>((n + UPD_B - 1) / UPD_B, 4 * num_sms);  // H-update CTAs (grid-stride)
   size_t o = 0;
   auto take = [&](size_t b) {
     size_t at = o;
@@ -608,10 +661,10 @@ cudaError_t tc_prepare(const TcPlan& p, const float* X, int64_t ldx, float* H, c
   double* Qpart = reinterpret_cast<double*>(ws + p.off_Q);
   const unsigned g = (unsigned)p.nQ;
   if (p.R == 16)
-    k_tc_hupdate<16><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, nullptr, 0, nullptr, 0.f, false, Hcat, p.ldh, Qpart,
+    k_tc_hupdate<16><<<g, UPD_THREADS, 0, st>>>(H, p.n, p.r, nullptr, 0, nullptr, 0.f, false, Hcat, p.ldh, Qpart,
                                              nullptr);
   else
-    k_tc_hupdate<32><<<g, UPD_ROWS, 0, st>>>(H, p.n, p.r, nullptr, 0, nullptr, 0.f, false, Hcat, p.ldh, Qpart,
+    k_tc_hupdate<32><<<g, UPD_THREADS, 0, st>>>(H, p.n, p.r, nullptr, 0, nullptr, 0.f, false, Hcat, p.ldh, Qpart,
                                              nullptr);
   return cudaGetLastError();
 }
@@ -646,16 +699,10 @@ cudaError_t tc_wupdate_ex(const TcPlan& p, float* W, float eps, char* ws, const 
   unsigned* mxw = tc_maxw(p, ws, 3 + (it & 1));
   double* G = reinterpret_cast<double*>(ws + p.off_G);
   const unsigned g = (unsigned)p.nG;
-  const size_t dsm = sizeof(double) * UPD_ROWS * p.r;  // <= 32 KB (+ ~25 KB static: opt in above 48 KB)
-  {
-    cudaError_t ea = p.R == 16 ? cudaFuncSetAttribute(k_tc_wupdate<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm)
-                               : cudaFuncSetAttribute(k_tc_wupdate<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
-    if (ea) return ea;
-  }
   if (p.R == 16)
-    k_tc_wupdate<16><<<g, UPD_ROWS, dsm, st>>>(W, p.m, p.r, P, nP, Qr, eps, Wcat, p.ldw, G, mxw);
+    k_tc_wupdate<16><<<g, UPD_THREADS, 0, st>>>(W, p.m, p.r, P, nP, Qr, eps, Wcat, p.ldw, G, mxw);
   else
-    k_tc_wupdate<32><<<g, UPD_ROWS, dsm, st>>>(W, p.m, p.r, P, nP, Qr, eps, Wcat, p.ldw, G, mxw);
+    k_tc_wupdate<32><<<g, UPD_THREADS, 0, st>>>(W, p.m, p.r, P, nP, Qr, eps, Wcat, p.ldw, G, mxw);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
   return launch_sum_partials(G, p.nG, (int64_t)p.r * p.r, reinterpret_cast<double*>(ws + p.off_Gred), st);
@@ -680,18 +727,10 @@ cudaError_t tc_hupdate_ex(const TcPlan& p, float* H, float eps, char* ws, const 
   float* Hcat = p.f16 ? nullptr : reinterpret_cast<float*>(ws + p.off_hcat);
   double* Q = reinterpret_cast<double*>(ws + p.off_Q);
   const unsigned g = (unsigned)p.nQ;
-  {
-    const int dsm = (int)(sizeof(double) * UPD_ROWS * p.r);
-    cudaError_t ea = p.R == 16 ? cudaFuncSetAttribute(k_tc_hupdate<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm)
-                               : cudaFuncSetAttribute(k_tc_hupdate<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);
-    if (ea) return ea;
-  }
   if (p.R == 16)
-    k_tc_hupdate<16><<<g, UPD_ROWS, sizeof(double) * UPD_ROWS * p.r, st>>>(H, p.n, p.r, S, nS, Gr, eps, true, Hcat,
-                                                                            p.ldh, Q, mxh);
+    k_tc_hupdate<16><<<g, UPD_THREADS, 0, st>>>(H, p.n, p.r, S, nS, Gr, eps, true, Hcat, p.ldh, Q, mxh);
   else
-    k_tc_hupdate<32><<<g, UPD_ROWS, sizeof(double) * UPD_ROWS * p.r, st>>>(H, p.n, p.r, S, nS, Gr, eps, true, Hcat,
-                                                                            p.ldh, Q, mxh);
+    k_tc_hupdate<32><<<g, UPD_THREADS, 0, st>>>(H, p.n, p.r, S, nS, Gr, eps, true, Hcat, p.ldh, Q, mxh);
   return cudaGetLastError();
 }
 

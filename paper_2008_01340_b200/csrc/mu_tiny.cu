@@ -24,6 +24,9 @@ constexpr int TINY_BLK = 64;  // fp32 partial block: 32 lanes x 64 columns
 // consecutive rows hit distinct banks
 __host__ __device__ inline int tiny_ld(int n) { return (n & 1) ? n : n + 1; }
 
+// the row-chunked H update (S = W^T X entry-parallel) for few columns; one thread per column otherwise
+__host__ __device__ inline bool tiny_tall(int m, int n, int R) { return m > 64 || 2 * R * n <= TINY_THREADS; }
+
 template <int R>
 struct TinyLayout {
   // offsets in bytes, all 16-aligned
@@ -39,7 +42,7 @@ struct TinyLayout {
     o = al(o + sizeof(double) * (size_t)R * R);       // Q
     o = al(o + sizeof(float) * (size_t)R * R);        // G (fp32 for E = G H)
     o = al(o + sizeof(double) * (size_t)nch * (m * R + R * R));  // chunk partials (n <= 256)
-    o = al(o + sizeof(float) * (size_t)R * ld);       // H new (row-chunked H update)
+    if (tiny_tall(m, n, R)) o = al(o + sizeof(float) * (size_t)R * ld);  // H new (row-chunked H update)
     o = al(o + sizeof(double) * (size_t)TINY_THREADS);  // S / G row-chunk partials
     return o;
   }
@@ -69,8 +72,9 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
   o = al(o + sizeof(float) * (size_t)R * R);
   double* part = reinterpret_cast<double*>(sm + o);
   o = al(o + sizeof(double) * (size_t)nch * (m * R + R * R));
+  const bool tall = tiny_tall(m, n, R);
   float* Hn = reinterpret_cast<float*>(sm + o);
-  o = al(o + sizeof(float) * (size_t)R * ld);
+  if (tall) o = al(o + sizeof(float) * (size_t)R * ld);
   double* cp = reinterpret_cast<double*>(sm + o);  // TINY_THREADS doubles
 
   const int tid = threadIdx.x, T = blockDim.x;
@@ -95,7 +99,6 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
   int cs = T / ES;
   cs = cs < 1 ? 1 : cs;
   if (cs > m / 16) cs = m / 16 < 1 ? 1 : m / 16;
-  const bool tall = m > 64 || 2 * ES <= T;
   for (int it = 0; it < iters; ++it) {
     if (n <= 256) {
     // ---- short rows: P = X H^T and Q = H H^T entry-parallel, entry e x chunk c of
@@ -316,7 +319,7 @@ cudaError_t launch_tiny_t(const float* X, int64_t ldx, int m, int n, int r, int 
 bool tiny_supported(int64_t m, int64_t n, int r) {
   if (r < 1 || r > 16 || m < 1 || n < 1 || m > 64) return false;
   const int R = r <= 4 ? 4 : (r <= 8 ? 8 : 16);
-  if (m * n > 48 * 1024) return false;
+  if (m * n > 12 * 1024) return false;  // measured: the persistent fused kernel wins above (64 x 700, 30 x 1296)
   size_t b = R == 4 ? TinyLayout<4>::bytes((int)m, (int)n, tiny_nch((int)m, r, (int)n))
                     : (R == 8 ? TinyLayout<8>::bytes((int)m, (int)n, tiny_nch((int)m, r, (int)n))
                               : TinyLayout<16>::bytes((int)m, (int)n, tiny_nch((int)m, r, (int)n)));
