@@ -153,7 +153,7 @@ ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t*
  * singular values are the eigenvalues of the fp64 Gram matrix of X_l (computed on
  * the device: split-K Gram, Householder tridiagonalisation and bisection), so the
  * rule is exact for tt_eps >= ~1e-7 (reading R21); each step needs
- * min(m, n) <= 512 (else NTT_ERR_UNSUPPORTED).  The call synchronises once per step
+ * min(m, n) <= 4096 (else NTT_ERR_UNSUPPORTED).  The call synchronises once per step
  * (the next step's shapes depend on the chosen rank).
  *   cores : packed output (device or host) with room for cores_capacity floats;
  *           the layout is ntt_decompose's for the chosen ranks (NTT_ERR_WORKSPACE if
@@ -164,8 +164,11 @@ ntt_status ntt_decompose_eps(ntt_handle h, const float* A, int32_t d, const int6
                              const int32_t* max_ranks, int32_t iters, uint64_t seed, float eps, float* cores,
                              int64_t cores_capacity, int32_t* ranks_out, double* rel_err);
 /* The rank rule alone on a device matrix X (m x n, row stride ldx,
- * min(m, n) <= 512): *rank = r for tt_eps; eig (nullable host, min(m, n)
- * doubles) receives the squared singular values in ascending order.            */
+ * min(m, n) <= 4096, else NTT_ERR_UNSUPPORTED): *rank = r for tt_eps; eig
+ * (nullable host, min(m, n) doubles) receives the squared singular values in
+ * ascending order.  Up to 512 the eigensolver runs in one CTA; above, the
+ * Householder reduction runs on the whole grid (one cooperative launch, fp64
+ * matrix of min(m, n)^2 doubles in the handle's workspace).                    */
 ntt_status ntt_rank_rule(ntt_handle h, const float* X, int64_t m, int64_t n, int64_t ldx, double tt_eps,
                          int32_t* rank, double* eig);
 

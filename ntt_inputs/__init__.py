@@ -101,6 +101,24 @@ def make_cores(dims, ranks, seed: int = 0, streams: Optional[List[int]] = None) 
     return np.concatenate(parts)
 
 
+def make_cores_decay(dims, ranks, rho: float, seed: int = 0) -> np.ndarray:
+    """Packed non-negative TT cores with a graded spectrum (the eps-sweep input of SURVEY s.8(f)
+    f2): the entries of make_cores scaled by rho^(a + b), a / b the left / right bond index of the
+    entry, so that bond direction k carries ~rho^k of the energy and the unfoldings' singular
+    values decay geometrically instead of the U[0,1) train's one dominant direction plus a flat
+    rest.  rho in (0, 1]; rho = 1 gives make_cores."""
+    c = make_cores(dims, ranks, seed)
+    fr = full_ranks(ranks)
+    out = np.empty_like(c)
+    o = 0
+    for l in range(len(dims)):
+        a, n, b = fr[l], dims[l], fr[l + 1]
+        s = np.power(float(rho), np.add.outer(np.arange(a), np.arange(b)))
+        out[o:o + a * n * b] = (c[o:o + a * n * b].reshape(a, n, b) * s[:, None, :]).ravel()
+        o += a * n * b
+    return out
+
+
 def make_factor_cores(m: int, n: int, r: int, seed: int = 0) -> Tuple[List[int], List[int], np.ndarray]:
     """X = W0 H0 written as a d=2 train (W0: 1 x m x r, H0: r x n x 1) with W0, H0 drawn
     from streams 0x400 / 0x401 (configs 2 and 5)."""

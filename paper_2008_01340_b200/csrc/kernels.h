@@ -44,9 +44,11 @@ cudaError_t launch_tiny(const float* X, int64_t ldx, int64_t m, int64_t n, int r
 
 
 
-// SVD rank rule of Alg. 2 l.5-6 (tt_rank.cu): Gram of X (min(m, n) <= 512) -> eigenvalues
-// (Householder + bisection, one CTA) -> r = smallest k with tail energy <= tt_eps.
+// SVD rank rule of Alg. 2 l.5-6 (tt_rank.cu): Gram of X (N = min(m, n) <= kRankMaxN) ->
+// eigenvalues (Householder + bisection: one CTA for N <= 512, a cooperative grid-wide reduction
+// and a warp-per-eigenvalue multisection above) -> r = smallest k with tail energy <= tt_eps.
 // Writes d_rank[0] (and the N eigenvalues ascending to d_eig when non-null).
+constexpr int kRankMaxN = 4096;
 size_t rank_rule_bytes(int64_t N, int64_t T, int num_sms);
 cudaError_t launch_rank_rule(const float* X, int64_t m, int64_t n, int64_t ldx, double tt_eps, char* ws,
                              int num_sms, int* d_rank, double* d_eig, cudaStream_t st);

@@ -1488,8 +1488,8 @@ ntt_status ntt_decompose_eps(ntt_handle h, const float* A, int32_t d, const int6
     for (int64_t rp = 1; rp <= cap[l - 1]; ++rp)
       for (int64_t r = 1; r <= c && r <= rp * s0.dims[l - 1]; ++r)
         mu_bytes = std::max(mu_bytes, plan_mu(rp * s0.dims[l - 1], ncol[l], (int)r, h->num_sms, false).bytes);
-    // rank-rule scratch for every Gram size the step can see (min(m, n) <= 512 is checked per step)
-    const int64_t nmax = std::min<int64_t>({mcap[l], ncol[l], 512});
+    // rank-rule scratch for every Gram size the step can see (min(m, n) <= kRankMaxN is checked per step)
+    const int64_t nmax = std::min<int64_t>({mcap[l], ncol[l], kRankMaxN});
     for (int64_t Nn = 1; Nn <= nmax; ++Nn)
       rk_bytes = std::max(rk_bytes, rank_rule_bytes(Nn, std::max(mcap[l], ncol[l]), h->num_sms));
   }
@@ -1531,8 +1531,8 @@ ntt_status ntt_decompose_eps(ntt_handle h, const float* A, int32_t d, const int6
   for (int l = 1; l < d; ++l) {
     const int64_t m = rprev * s0.dims[l - 1], n = ncol[l];
     h->cur_step = l;
-    if (std::min(m, n) > 512)
-      return fail(h, NTT_ERR_UNSUPPORTED, "rank rule needs min(m, n) <= 512 (step %d: %lld x %lld)", l,
+    if (std::min(m, n) > kRankMaxN)
+      return fail(h, NTT_ERR_UNSUPPORTED, "rank rule needs min(m, n) <= %d (step %d: %lld x %lld)", kRankMaxN, l,
                   (long long)m, (long long)n);
     LAUNCH(h, launch_rank_rule(X, m, n, n, tt_eps, ws + off_rk, h->num_sms, d_rank, nullptr, cs));
     int rk = 1;
@@ -1796,7 +1796,7 @@ ntt_status ntt_rank_rule(ntt_handle h, const float* X, int64_t m, int64_t n, int
   if (!h || !X || !rank) return NTT_ERR_INVALID_ARG;
   if (m < 1 || n < 1 || ldx < n) return fail(h, NTT_ERR_INVALID_ARG, "bad shape");
   if (!(tt_eps >= 0.0)) return fail(h, NTT_ERR_INVALID_ARG, "tt_eps must be >= 0");
-  if (std::min(m, n) > 512) return fail(h, NTT_ERR_UNSUPPORTED, "rank rule needs min(m, n) <= 512");
+  if (std::min(m, n) > kRankMaxN) return fail(h, NTT_ERR_UNSUPPORTED, "rank rule needs min(m, n) <= %d", kRankMaxN);
   if (!is_device_ptr(X)) return fail(h, NTT_ERR_INVALID_ARG, "X must be device memory");
   CU(h, cudaSetDevice(h->device));
   const int64_t N = std::min(m, n);

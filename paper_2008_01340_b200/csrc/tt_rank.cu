@@ -10,6 +10,7 @@
 //                  L2), Sturm-count bisection for every eigenvalue, then the tail rule
 // Gram-based eigenvalues carry an absolute error ~1e-16 * trace(C), so the rule is
 // exact for eps >= ~1e-7 (reading R21).  Deterministic (fixed reduction orders).
+#include <algorithm>
 #include <cstdint>
 
 #include "common.cuh"
@@ -19,6 +20,7 @@ namespace ntt {
 
 namespace {
 
+constexpr int kRankOneCta = 512;  // the one-CTA eigensolver up to this size, the grid path above
 constexpr int GT = 32;   // Gram output tile (GT x GT)
 constexpr int GK = 32;   // columns of the long dimension per smem block
 
@@ -275,6 +277,189 @@ k_eig_rank(double* __restrict__ C, int N, double* __restrict__ vg, double* __res
     for (int i = tid; i < N; i += T) eig[i] = lam[i];
 }
 
+// ------------------------------------------- N > 512: the same algorithm on the whole grid
+// (SURVEY s.8(f) f2 at the paper's 256^4 scale, whose step 2 has min(m, n) = 2560).  The matrix
+// (fp64, up to 4096^2 = 128 MB) stays in global memory / L2; every step of the Householder
+// reduction is split across all CTAs of one cooperative launch:
+//   every CTA   x = row k of the trailing matrix (= column k by symmetry, contiguous), ||x||, v
+//               (redundantly: no barrier needed for v)
+//   warp-rows   p_i = sum_j A'[i][j] v_j for the rows this warp owns (row i -> global warp i % W)
+//   -- grid barrier --
+//   every CTA   K = v^T p, w = p - K v (redundantly)
+//   warp-rows   A'[i][j] -= 2 (v_i w_j + w_i v_j)
+//   -- grid barrier --
+// with the arithmetic of k_eig_rank (same reflector, same update formula; the row sums are
+// lane-strided warp sums instead of one warp per row of a 1024-thread CTA, so the tridiagonal
+// agrees to rounding).  Eigenvalues: k_bisect_grid, a warp per eigenvalue, 32-point
+// multisection with the Sturm count of k_eig_rank.
+constexpr int TG_T = 256;
+
+__device__ __forceinline__ void tg_barrier(unsigned* ctr, unsigned& epoch) {
+  __syncthreads();
+  epoch += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while (v < epoch);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(TG_T)
+k_tridiag_grid(double* __restrict__ C, int N, double* __restrict__ pg, double* __restrict__ dg,
+               double* __restrict__ eg, unsigned* __restrict__ ctr) {
+  extern __shared__ double tsm[];
+  double* v = tsm;      // N
+  double* w = v + N;    // N
+  __shared__ double red[33];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int W = gridDim.x * (TG_T / 32);
+  const int gw = blockIdx.x * (TG_T / 32) + warp;
+  unsigned epoch = 0;
+  for (int k = 0; k + 2 < N; ++k) {
+    const int L = N - k - 1;
+    const double* xrow = C + (int64_t)k * N + (k + 1);
+    double xs = 0.0;
+    for (int j = tid; j < L; j += TG_T) {
+      const double xj = __ldcg(xrow + j);
+      v[j] = xj;
+      xs += xj * xj;
+    }
+    const double nx2 = block_sum(xs, red);
+    const double x0 = v[0];
+    const double nx = sqrt(nx2);
+    const double alpha = (x0 > 0.0) ? -nx : nx;
+    const double nv2 = nx2 - 2.0 * alpha * x0 + alpha * alpha;
+    if (blockIdx.x == 0 && tid == 0) {
+      dg[k] = __ldcg(C + (int64_t)k * N + k);
+      eg[k] = (nx2 > 0.0) ? alpha : 0.0;
+    }
+    if (nv2 <= 0.0 || nx2 == 0.0) {  // already reduced (every CTA takes this branch)
+      if (blockIdx.x == 0 && tid == 0) eg[k] = x0;
+      __syncthreads();
+      continue;
+    }
+    const double inv = 1.0 / sqrt(nv2);
+    __syncthreads();
+    for (int j = tid; j < L; j += TG_T) v[j] = (j == 0 ? v[0] - alpha : v[j]) * inv;
+    __syncthreads();
+    for (int i = gw; i < L; i += W) {
+      const double* row = C + (int64_t)(k + 1 + i) * N + (k + 1);
+      double a0 = 0.0, a1 = 0.0;
+      int j = lane;
+      for (; j + 32 < L; j += 64) {
+        a0 = fma(__ldcg(row + j), v[j], a0);
+        a1 = fma(__ldcg(row + j + 32), v[j + 32], a1);
+      }
+      if (j < L) a0 = fma(__ldcg(row + j), v[j], a0);
+      const double sum = warp_sum(a0 + a1);
+      if (lane == 0) pg[i] = sum;
+    }
+    tg_barrier(ctr, epoch);
+    double kp = 0.0;
+    for (int j = tid; j < L; j += TG_T) {
+      const double pj = __ldcg(pg + j);
+      w[j] = pj;
+      kp += v[j] * pj;
+    }
+    const double K = block_sum(kp, red);
+    for (int j = tid; j < L; j += TG_T) w[j] = w[j] - K * v[j];
+    __syncthreads();
+    for (int i = gw; i < L; i += W) {
+      double* row = C + (int64_t)(k + 1 + i) * N + (k + 1);
+      const double vi = v[i], wi = w[i];
+      for (int j = lane; j < L; j += 32) row[j] = __ldcg(row + j) - 2.0 * (vi * w[j] + wi * v[j]);
+    }
+    tg_barrier(ctr, epoch);
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    if (N >= 2) {
+      dg[N - 2] = __ldcg(C + (int64_t)(N - 2) * N + (N - 2));
+      eg[N - 2] = __ldcg(C + (int64_t)(N - 1) * N + (N - 2));
+    }
+    dg[N - 1] = __ldcg(C + (int64_t)(N - 1) * N + (N - 1));
+  }
+}
+
+// number of eigenvalues of the tridiagonal (d, e) strictly below x (k_eig_rank's sturm_count
+// with e^2 formed on the fly)
+__device__ int sturm_count_e(const double* __restrict__ d, const double* __restrict__ e, int N, double x) {
+  int c = 0;
+  double q = d[0] - x;
+  if (q < 0.0) ++c;
+  for (int i = 1; i < N; ++i) {
+    if (q == 0.0) q = 1e-300;
+    q = (d[i] - x) - (e[i - 1] * e[i - 1]) / q;
+    if (q < 0.0) ++c;
+  }
+  return c;
+}
+
+// lam[i] (ascending) for every i: a warp per eigenvalue, each round evaluates the Sturm count at
+// 32 interior points of [lo, hi] (one per lane) and keeps the 1/33 sub-interval that holds
+// eigenvalue i; stops at the bisection tolerance of k_eig_rank.
+__global__ void __launch_bounds__(256) k_bisect_grid(const double* __restrict__ d, const double* __restrict__ e, int N,
+                                                    double* __restrict__ lam) {
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  double gl = 1e300, gu = -1e300;
+  for (int i = lane; i < N; i += 32) {
+    const double rad = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < N ? fabs(e[i]) : 0.0);
+    gl = fmin(gl, d[i] - rad);
+    gu = fmax(gu, d[i] + rad);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
+    gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
+  }
+  const double span = fmax(gu - gl, 1e-300);
+  for (int idx = gwarp; idx < N; idx += nwarps) {
+    double lo = gl - 1e-12 * span, hi = gu + 1e-12 * span;
+    for (int it = 0; it < 64 && hi - lo > 1e-15 * fmax(fabs(lo), fabs(hi)) + 1e-300; ++it) {
+      const double wdt = hi - lo;
+      const double x = lo + wdt * (double)(lane + 1) / 33.0;
+      const unsigned above = __ballot_sync(0xffffffffu, sturm_count_e(d, e, N, x) > idx);
+      const int l = above ? __ffs(above) - 1 : 32;
+      const double nlo = lo + wdt * (double)l / 33.0;
+      const double nhi = (l == 32) ? hi : lo + wdt * (double)(l + 1) / 33.0;
+      lo = nlo;
+      hi = nhi;
+    }
+    if (lane == 0) lam[idx] = fmax(0.5 * (lo + hi), 0.0);  // PSD: clamp round-off negatives
+  }
+}
+
+// the tail rule of k_eig_rank on ascending eigenvalues (one thread)
+__global__ void k_rank_from_eig(const double* __restrict__ lam, int N, double tt_eps, int* __restrict__ rank_out,
+                                double* __restrict__ eig) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double tot = 0.0;
+    for (int i = 0; i < N; ++i) tot += lam[i];
+    int r = N;
+    if (tot <= 0.0) {
+      r = 1;
+    } else {
+      double asc = 0.0;
+      int best = 0;
+      for (int j = 1; j < N; ++j) {
+        asc += lam[j - 1];
+        if (sqrt(asc / tot) <= tt_eps) best = j;
+        else break;
+      }
+      r = N - best;
+    }
+    rank_out[0] = r;
+  }
+  if (eig)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) eig[i] = lam[i];
+}
+
 }  // namespace
 
 size_t rank_rule_bytes(int64_t N, int64_t T, int num_sms) {
@@ -317,10 +502,36 @@ cudaError_t launch_rank_rule(const float* X, int64_t m, int64_t n, int64_t ldx, 
   if (e) return e;
   double* vg = C + (size_t)N * N;
   double* pg = vg + N;
-  const size_t sm = sizeof(double) * (6 * (size_t)N + 40);
-  e = cudaFuncSetAttribute(k_eig_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (N <= kRankOneCta) {
+    const size_t sm = sizeof(double) * (6 * (size_t)N + 40);
+    e = cudaFuncSetAttribute(k_eig_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e) return e;
+    k_eig_rank<<<1, ET, sm, st>>>(C, N, vg, pg, tt_eps, d_eig, d_rank);
+    return cudaGetLastError();
+  }
+  // grid path: p (N, at vg) | d (N) | e (N) | lam (N) | barrier counter, after C (4 N + 64 doubles)
+  double* dg = vg + N;
+  double* eg = dg + N;
+  double* lam = eg + N;
+  unsigned* ctr = reinterpret_cast<unsigned*>(lam + N);
+  e = cudaMemsetAsync(ctr, 0, 64, st);
   if (e) return e;
-  k_eig_rank<<<1, ET, sm, st>>>(C, N, vg, pg, tt_eps, d_eig, d_rank);
+  const size_t sm = sizeof(double) * 2 * (size_t)N;
+  e = cudaFuncSetAttribute(k_tridiag_grid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tridiag_grid, TG_T, sm);
+  if (e) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const int grid = num_sms * std::min(per_sm, 2);
+  int Ni = N;
+  void* args[] = {&C, &Ni, &vg, &dg, &eg, &ctr};
+  e = cudaLaunchCooperativeKernel((const void*)k_tridiag_grid, dim3(grid), dim3(TG_T), args, sm, st);
+  if (e) return e;
+  k_bisect_grid<<<(unsigned)std::min<int64_t>((N + 7) / 8, 4 * num_sms), 256, 0, st>>>(dg, eg, N, lam);
+  e = cudaGetLastError();
+  if (e) return e;
+  k_rank_from_eig<<<1, 256, 0, st>>>(lam, N, tt_eps, d_rank, d_eig);
   return cudaGetLastError();
 }
 

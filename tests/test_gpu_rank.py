@@ -94,3 +94,57 @@ def test_decompose_eps_max_ranks_and_capacity(h):
     assert ranks[0] <= 2 and ranks[1] <= 3 and ranks[2] <= 2
     with pytest.raises(P.NttError):
         h.ntt_decompose_eps(A, dims, 1e-6, 3, 0, 1e-16, cores, 3)
+
+
+# ---- min(m, n) > 512: the grid-wide Householder reduction + warp multisection (tt_rank.cu) ----
+@pytest.mark.parametrize("m,n", [(600, 2000), (2000, 700), (1500, 1600), (2560, 2600)])
+def test_rank_rule_grid_known_spectrum(h, ora, m, n):
+    N = min(m, n)
+    s = np.concatenate([[10, 5, 1, 0.1, 0.01], 1e-4 * np.ones(N - 5)])
+    X = spectrum_matrix(s, m, n, seed=m + n)
+    Xd = torch.from_numpy(X.ravel()).cuda()
+    for eps in (2.0, 0.3, 0.05, 0.005, 3e-4):
+        r_ora = ora.svd_tail_rank(X, eps)
+        r_gpu, eig = h.ntt_rank_rule(Xd, m, n, n, eps, want_eig=True)
+        assert r_gpu == r_ora, (m, n, eps, r_gpu, r_ora)
+    sv = np.linalg.svd(X.astype(np.float64), compute_uv=False)
+    ref = np.sort(sv ** 2)
+    assert np.abs(np.array(eig) - ref).max() <= 1e-12 * ref.sum()
+
+
+def test_rank_rule_grid_graded_spectrum(h, ora):
+    """A geometric spectrum (no flat tail): every eps picks a different rank, and the
+    eigenvalues match LAPACK's squared singular values to 1e-12 of the trace."""
+    m, n = 900, 1200
+    s = 0.7 ** np.arange(m)
+    X = spectrum_matrix(s, m, n, seed=5)
+    Xd = torch.from_numpy(X.ravel()).cuda()
+    for eps in (0.5, 0.2, 0.1, 0.03, 0.01, 3e-3):
+        assert h.ntt_rank_rule(Xd, m, n, n, eps)[0] == ora.svd_tail_rank(X, eps)
+
+
+def test_decompose_eps_grid_step(h, ora):
+    """ntt_decompose_eps with a first unfolding of 600 x 1000 (grid path) on a non-negative
+    exact rank-4 tensor: ranks identical to the oracle's, cores within 1e-4."""
+    import paper_2008_01340_b200 as P
+    dims = [600, 10, 100]
+    rng = np.random.default_rng(11)
+    A = (rng.random((600, 4)) @ rng.random((4, 1000))).astype(np.float32).reshape(dims)
+    Ad = torch.from_numpy(A.ravel()).cuda()
+    cap = P.cores_size(dims, [64] * 2)
+    for tt_eps in (0.3, 1e-4):
+        cores = torch.zeros(cap, device="cuda")
+        ranks, err = h.ntt_decompose_eps(Ad, dims, tt_eps, 10, 3, 1e-16, cores, cap, want_error=True)
+        r_ora, c_ora = ora.ntt_decompose_eps(A, tt_eps, iters=10, seed=3)
+        assert ranks == r_ora, (tt_eps, ranks, r_ora)
+        got = cores.cpu().numpy()[: c_ora.size].astype(np.float64)
+        assert np.linalg.norm(got - c_ora) / np.linalg.norm(c_ora) <= 1e-4
+        e_ora = ora.tt_rel_error(A, r_ora, c_ora)
+        assert abs(err - e_ora) <= 1e-3 * e_ora + 1e-6
+
+
+def test_rank_rule_limit(h):
+    import paper_2008_01340_b200 as P
+    X = torch.zeros(4097 * 4100, device="cuda")
+    with pytest.raises(P.NttError):
+        h.ntt_rank_rule(X, 4097, 4100, 4100, 0.1)
