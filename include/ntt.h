@@ -278,6 +278,28 @@ const unsigned long long* ntt_debug_persist_trace(ntt_handle h);
  * tests that a distributed branch ran.  -1 for a null handle.               */
 int64_t ntt_collective_count(ntt_handle h);
 
+/* Cross-GPU reduction of the MU passes on an ntt_create_dist* handle (SURVEY
+ * s.8(e); the all_reduce of Alg. 4 P:256-266 on the TT partition, DESIGN.md s.7).
+ *   mode 1 (default): the persistent one-pass kernels keep running for the whole
+ *     MU loop of a step; after each pass CTA 0 stores this GPU's reduced fp64
+ *     (X H^T, H H^T) vector (m r + r^2 <= 4352 doubles) into every rank's
+ *     exchange buffer over NVLink (buffers allocated by ntt_create_dist*,
+ *     exported / mapped with CUDA IPC, so all ranks must be one node's GPUs),
+ *     raises a release flag there, waits for all ranks' flags, and every CTA
+ *     sums the ranks' vectors in rank order -- no host round trip, no NCCL call
+ *     per pass.  Shapes outside the persistent kernels use mode 0's path.
+ *   mode 0: one ncclAllReduce per pass between per-pass kernel launches.
+ * Both give the same sums up to the rank-order vs NCCL reduction order.
+ * NTT_ERR_INVALID_ARG for other modes / non-distributed handles,
+ * NTT_ERR_UNSUPPORTED for mode 1 if the buffers could not be mapped.
+ * Synchronises the handle's stream.                                         */
+ntt_status ntt_set_dist_exchange(ntt_handle h, int mode);
+
+/* Number of in-kernel exchanges (passes) completed on this handle's exchange
+ * buffer: a device-side counter the persistent kernels advance, read after a
+ * stream synchronisation.  -1 if the handle has no exchange buffer.          */
+int64_t ntt_peer_exchange_count(ntt_handle h);
+
 /* Kernel-level diagnostics of the TT-mode partition (DESIGN.md s.7), so the
  * layouts of p > 1 ranks can be checked on one GPU:
  *  - ntt_debug_fill_uniform_cols: the local r x nloc H init of a rank that owns

@@ -167,6 +167,14 @@ class Handle:
         self._check(lib().ntt_stream_ceiling(self._h, _ptr(buf), nbytes, reps, ctypes.byref(g)))
         return float(g.value)
 
+    def ntt_set_dist_exchange(self, mode: int):
+        """1: in-kernel NVLink exchange of the pass partials (default); 0: per-pass ncclAllReduce."""
+        self._check(lib().ntt_set_dist_exchange(self._h, int(mode)))
+
+    @property
+    def peer_exchange_count(self) -> int:
+        return int(lib().ntt_peer_exchange_count(self._h))
+
     @property
     def collective_count(self) -> int:
         return int(lib().ntt_collective_count(self._h))

@@ -55,6 +55,8 @@ SIGNATURES = {
     "ntt_set_validation": (c_int, [c_p, c_int]),
     "ntt_collective_count": (c_i64, [c_p]),
     "ntt_stream_ceiling": (c_int, [c_p, c_p, c_i64, c_i32, ctypes.POINTER(c_f64)]),
+    "ntt_set_dist_exchange": (c_int, [c_p, c_int]),
+    "ntt_peer_exchange_count": (c_i64, [c_p]),
     "ntt_debug_fill_uniform_cols": (c_int, [c_p, c_p, c_i32, c_i64, c_i64, c_i64, c_i64, c_i64, c_u64, c_u64]),
     "ntt_debug_gather_last_core": (c_int, [c_p, c_p, c_i64, c_i64, c_i32, c_p]),
 }

@@ -151,6 +151,72 @@ __device__ __forceinline__ void grid_sync(unsigned* ctr, unsigned& epoch) {
   __syncthreads();
 }
 
+// ---- cross-GPU exchange (PersistArgs::xpeers; SURVEY s.8(e)): system-scope flags
+__device__ __forceinline__ unsigned long long* xflags(double* base, int nranks) {
+  return reinterpret_cast<unsigned long long*>(base + 2 * (size_t)nranks * kXLmax);
+}
+__device__ __forceinline__ unsigned long long xseq_load(const PersistArgs& pa) {
+  if (pa.nranks <= 0) return 0ull;
+  const unsigned long long* sp = xflags(pa.xpeers[pa.rank], pa.nranks) + 2 * pa.nranks;
+  return *reinterpret_cast<const volatile unsigned long long*>(sp);
+}
+// end of a persistent launch: advance the buffer's pass counter (CTA 0, after the last barrier)
+__device__ __forceinline__ void xseq_store(const PersistArgs& pa, unsigned long long xs0) {
+  if (pa.nranks > 0 && blockIdx.x == 0 && threadIdx.x == 0)
+    *(xflags(pa.xpeers[pa.rank], pa.nranks) + 2 * pa.nranks) = xs0 + (unsigned long long)pa.iters;
+}
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// CTA 0: stage this GPU's reduced vector src (L doubles, L2) in shared memory (one round trip:
+// all 8 loads of a thread issued together), store it into slot [par][rank] of every rank's
+// buffer, then one thread per rank: fence + release flag [par][rank] on that rank.
+__device__ void xpush(const PersistArgs& pa, const double* src, int L, unsigned long long seq, double* stg) {
+  const int p = pa.nranks, T = blockDim.x, tid = threadIdx.x;
+  const int par = (int)(seq & 1ull);
+  for (int e0 = 0; e0 < L; e0 += 8 * T) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = e0 + q * T + tid;
+      v[q] = e < L ? __ldcg(src + e) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = e0 + q * T + tid;
+      if (e < L) stg[e] = v[q];
+    }
+  }
+  __syncthreads();
+  for (int q = 0; q < p; ++q) {
+    double* dst = pa.xpeers[q] + ((size_t)par * p + pa.rank) * kXLmax;
+    for (int e = tid; e < L; e += T) dst[e] = stg[e];
+  }
+  __syncthreads();
+  if (tid < p) {
+    __threadfence_system();
+    st_release_sys_u64(xflags(pa.xpeers[tid], p) + par * p + pa.rank, seq);
+  }
+}
+
+// every CTA: wait until all ranks' flags [par][*] of the own buffer carry seq (acquire, system
+// scope), so the slot reads that follow see the peers' stores
+__device__ void xwait(const PersistArgs& pa, unsigned long long seq) {
+  const int p = pa.nranks, tid = threadIdx.x;
+  if (tid < p) {
+    const unsigned long long* f = xflags(pa.xpeers[pa.rank], p) + (int)(seq & 1ull) * p + tid;
+    while (ld_acquire_sys_u64(f) < seq) {
+    }
+  }
+  __syncthreads();
+}
+
 // Reduce the per-CTA partials and apply the W update in every CTA (see above).
 // Scratch layout (doubles): P (m r) | Qp (RK x RK, Q zero-padded) | Wd (m RK, W as fp64) |
 // Wnd (m RK, new W rounded to fp32, held as fp64) | Gp ([<= T / RK chunks][RK][RK] Gram partials).
@@ -161,7 +227,7 @@ __host__ __device__ constexpr int64_t persist_scratch_doubles(int64_t m, int r, 
 
 template <int RK>
 __device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int r, float eps, float* Ws, float* Gs,
-                             double* scr, int it) {
+                             double* scr, int it, unsigned long long xs0) {
   const int L = m * r + r * r;
   const int T = blockDim.x, tid = threadIdx.x;
   pstamp(pa, it, 1);
@@ -202,20 +268,40 @@ __device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int 
   } else {
     __syncthreads();  // single CTA: its own partial is the sum
   }
-  pstamp(pa, it, 3);
   const double* srcv = gridDim.x > 1 ? pa.red : pa.part;
+  const unsigned long long seq = xs0 + (unsigned long long)it + 1ull;
+  if (pa.nranks > 0) {  // every rank's vector into every rank's slots (see PersistArgs::xpeers)
+    if (blockIdx.x == 0) xpush(pa, srcv, L, seq, scr);
+    xwait(pa, seq);
+  }
+  pstamp(pa, it, 3);
   double* P = scr;                 // m x r
   double* Qp = scr + ((m * r + 1) & ~1);  // RK x RK (16-byte aligned for the double2 loads)
   double* Wd = Qp + RK * RK;       // m x RK
   double* Wnd = Wd + m * RK;       // m x RK
   double* Gp = Wnd + m * RK;       // [GC][RK][RK]
   // (P, Q) into shared memory: coalesced, all 8 loads of a thread issued before any is used
+  const double* xslots = pa.nranks > 0 ? pa.xpeers[pa.rank] + (size_t)(seq & 1ull) * pa.nranks * kXLmax : nullptr;
   for (int e0 = 0; e0 < L; e0 += 8 * T) {
     double v[8];
+    if (pa.nranks > 0) {  // sum of the ranks' vectors in rank order (identical on every rank)
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int e = e0 + q * T + tid;
-      v[q] = e < L ? __ldcg(srcv + e) : 0.0;
+      for (int q = 0; q < 8; ++q) v[q] = 0.0;
+#pragma unroll 4
+      for (int sr = 0; sr < pa.nranks; ++sr) {
+        const double* sl = xslots + (size_t)sr * kXLmax;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int e = e0 + q * T + tid;
+          if (e < L) v[q] += __ldcg(sl + e);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int e = e0 + q * T + tid;
+        v[q] = e < L ? __ldcg(srcv + e) : 0.0;
+      }
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -379,6 +465,7 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
 
   unsigned epoch = 0;
   const int nit = persist ? pa.iters + 1 : 1;
+  const unsigned long long xs0 = persist ? xseq_load(pa) : 0ull;
   for (int it = 0; it < nit; ++it) {
   // persistent: pass 0 = acc-only prologue, passes 1..iters update (+ acc except the last)
   const int md = persist ? (it == 0 ? kFusedAcc : (kFusedUpdate | (it < pa.iters ? kFusedAcc : 0))) : mode;
@@ -787,8 +874,9 @@ k_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtenso
   }
   }  // consumer warps
   if (!persist || !do_acc) break;
-  persist_step<8>(pa, epoch, m, r, eps, Ws, Gs, reinterpret_cast<double*>(stages), it);
+  persist_step<8>(pa, epoch, m, r, eps, Ws, Gs, reinterpret_cast<double*>(stages), it, xs0);
   }  // passes
+  if (persist) xseq_store(pa, xs0);
 }
 
 
@@ -935,6 +1023,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   int ring_s = 0;          // ring stage / parity of the next tile (continues across passes)
   uint32_t ring_ph = 0;
   const int nit = persist ? pa.iters + 1 : 1;
+  const unsigned long long xs0 = persist ? xseq_load(pa) : 0ull;
   for (int it = 0; it < nit; ++it) {
   const int md = persist ? (it == 0 ? kFusedAcc : (kFusedUpdate | (it < pa.iters ? kFusedAcc : 0))) : mode;
   const bool do_update = (md & kFusedUpdate) != 0;
@@ -1325,8 +1414,9 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   else bcd ? pass_tiles(T_{}, F_{}, T_{}) : pass_tiles(T_{}, F_{}, F_{});
   }  // consumer warps
   if (!persist || !do_acc) break;
-  persist_step<RK>(pa, epoch, m, r, eps, Wc, Gs, reinterpret_cast<double*>(stages), it);
+  persist_step<RK>(pa, epoch, m, r, eps, Wc, Gs, reinterpret_cast<double*>(stages), it, xs0);
   }  // passes
+  if (persist) xseq_store(pa, xs0);
 }
 
 // shared-memory scratch persist_step takes from the stage area between passes
@@ -1531,6 +1621,7 @@ k_fused_m(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   const int64_t J = (ntiles > b) ? (ntiles - b + gridDim.x - 1) / gridDim.x : 0;
   unsigned epoch = 0;
   const int nit = persist ? pa.iters + 1 : 1;
+  const unsigned long long xs0 = persist ? xseq_load(pa) : 0ull;
   for (int it = 0; it < nit; ++it) {
   const int md = persist ? (it == 0 ? kFusedAcc : (kFusedUpdate | (it < pa.iters ? kFusedAcc : 0))) : mode;
   const bool do_update = (md & kFusedUpdate) != 0;
@@ -1832,8 +1923,9 @@ k_fused_m(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   else pass_tiles(T_{}, F_{});
   }  // consumer warps
   if (!persist || !do_acc) break;
-  persist_step<8>(pa, epoch, m, r, eps, Ws, Gs, reinterpret_cast<double*>(stages), it);
+  persist_step<8>(pa, epoch, m, r, eps, Ws, Gs, reinterpret_cast<double*>(stages), it, xs0);
   }  // passes
+  if (persist) xseq_store(pa, xs0);
 }
 
 size_t fixed_bytes_m() { return 32 * 8 * 4 + 256 + 2 * 24 * 8 + 160 + 1024; }

@@ -48,7 +48,22 @@ struct PersistArgs {
   // streamed by every later pass instead of converting the fp32 tile again (fused_x16_bytes;
   // nullable: every pass converts)
   unsigned char* x16 = nullptr;
+  // cross-GPU exchange (persistent launch on an ntt_create_dist handle, SURVEY s.8(e)): after the
+  // per-GPU reduction of every pass, CTA 0 stores the (P, Q) vector into slot [seq & 1][rank] of
+  // every rank's exchange buffer (NVLink peer stores; IPC-mapped, own buffer included), raises
+  // flag [seq & 1][rank] there with a release store, waits for the nranks flags of its own
+  // buffer, and every CTA then sums the nranks slots in rank order (the same sum on every rank).
+  // seq: a per-buffer pass counter kept on the device (read at launch, advanced by `iters`).
+  // nranks = 0: single-GPU reduction only.
+  double* const* xpeers = nullptr;  // [nranks] exchange buffer bases (device array)
+  int nranks = 0;
+  int rank = 0;
 };
+// exchange buffer layout (doubles): slots [2][nranks][kXLmax], flags (u64) [2][nranks], seq (u64)
+constexpr int kXLmax = 256 * 16 + 16 * 16;  // largest m r + r r of the persistent kernels
+__host__ __device__ inline size_t xbuf_bytes(int nranks) {
+  return sizeof(double) * 2 * (size_t)nranks * kXLmax + sizeof(unsigned long long) * (2 * (size_t)nranks + 8);
+}
 // bytes of the PersistArgs::x16 cache for an m x n X (0 when m <= 40)
 size_t fused_x16_bytes(int64_t m, int64_t n);
 

@@ -93,6 +93,13 @@ struct ntt_handle_s {
   int pr = 1, pc = 1, ga = 0, gb = 0;
   ncclComm_t comm_row = nullptr, comm_col = nullptr;
   ncclComm_t comm = nullptr;
+  // in-kernel cross-GPU exchange of the persistent MU kernels (PersistArgs::xpeers): own buffer
+  // (IPC-exported), the peers' buffers opened through IPC, the device array of all bases
+  void* xbuf = nullptr;
+  std::vector<void*> xopened;
+  double** xpeers = nullptr;
+  bool xready = false;  // buffers mapped on every rank
+  int xmode = 1;        // ntt_set_dist_exchange: 1 = in-kernel exchange, 0 = per-pass ncclAllReduce
   FusedCtx fused;
   // profiling (ntt_profile_enable)
   bool prof = false;
@@ -310,7 +317,7 @@ struct MuPlan {
 
 // dist: a handle from ntt_create_dist* (any number of ranks, 1 included) -- its MU runs
 // the distributed branches (all-reduce of the pass partials between passes)
-MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, bool dist) {
+MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, bool dist, bool xpersist = false) {
   MuPlan p;
   p.m = m;
   p.n = n;
@@ -344,7 +351,7 @@ MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, bool dist) {
     p.tp = plan_tc(m, n, r, num_sms);
     o = align_up(o + p.tp.bytes);
   }
-  p.persist = !dist && p.fused && !getenv("NTT_NO_PERSIST");
+  p.persist = (!dist || xpersist) && p.fused && !getenv("NTT_NO_PERSIST");
   p.tiny = !dist && tiny_supported(m, n, r) && !getenv("NTT_NO_TINY");
   p.off_pp = o;
   if (p.persist) o = align_up(o + sizeof(double) * (size_t)p.fgrid * (size_t)(m * r + r * r));
@@ -385,9 +392,16 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
             launch_tiny(X, ldx, m, n, r, iters, eps, W, H, st));
     return NTT_OK;
   }
-  if (p.fused && p.persist && !dist && !dev_trace && fused_supported(m, n, r, ldx, X, H)) {
-    // whole MU loop of this call in one cooperative launch (mu_fused.cu persist_step)
+  if (p.fused && p.persist && (!dist || (h->xready && h->xmode == 1)) && !dev_trace &&
+      fused_supported(m, n, r, ldx, X, H)) {
+    // whole MU loop of this call in one cooperative launch (mu_fused.cu persist_step); on a
+    // distributed handle the ranks' partials are exchanged inside the kernel (PersistArgs::xpeers)
     PersistArgs pa;
+    if (dist) {
+      pa.xpeers = h->xpeers;
+      pa.nranks = h->nranks;
+      pa.rank = h->rank;
+    }
     pa.iters = iters;
     pa.part = reinterpret_cast<double*>(scratch + p.off_pp);
     pa.red = reinterpret_cast<double*>(scratch + p.off_red);
@@ -784,6 +798,9 @@ ntt_status ntt_destroy(ntt_handle h) {
   if (h->stage) cudaFree(h->stage);
   if (h->sweep) cudaFree(h->sweep);
   if (h->host_part) cudaFreeHost(h->host_part);
+  for (void* pp : h->xopened) cudaIpcCloseMemHandle(pp);
+  if (h->xpeers) cudaFree(h->xpeers);
+  if (h->xbuf) cudaFree(h->xbuf);
   if (h->comm_row && g_nccl.loaded) g_nccl.CommDestroy(h->comm_row);
   if (h->comm_col && g_nccl.loaded) g_nccl.CommDestroy(h->comm_col);
   if (h->comm && g_nccl.loaded) g_nccl.CommDestroy(h->comm);
@@ -822,7 +839,7 @@ ntt_status ntt_nmf_mu(ntt_handle h, const float* X, int64_t m, int64_t n, int64_
   ntt_status s = check_mu_args(h, X, m, n, ldx, r, iters, eps, W, H);
   if (s) return s;
   CU(h, cudaSetDevice(h->device));
-  MuPlan p = plan_mu(m, n, r, h->num_sms, h->comm != nullptr);
+  MuPlan p = plan_mu(m, n, r, h->num_sms, h->comm != nullptr, h->xready && h->xmode == 1);
   const bool xd = is_device_ptr(X), wd = is_device_ptr(W), hd = is_device_ptr(H);
   // staging layout for host buffers: [X | W | H]
   size_t sx = xd ? 0 : align_up(sizeof(float) * (size_t)(m * ldx));
@@ -887,7 +904,7 @@ struct DecompPlan {
   ContractPlan cp;
 };
 
-void plan_decompose(const TTShape& s, int num_sms, int nranks, int rank, bool dist, DecompPlan* P) {
+void plan_decompose(const TTShape& s, int num_sms, int nranks, int rank, bool dist, DecompPlan* P, bool xpersist = false) {
   P->s = s;
   int64_t off = 0;
   P->nloc_last = ntt_dist_block(s.dims[s.d - 1], nranks, rank, &off);
@@ -904,7 +921,7 @@ void plan_decompose(const TTShape& s, int num_sms, int nranks, int rank, bool di
     int64_t hsz = s.r[l] * rest;
     P->hbuf[(l - 1) & 1] = std::max(P->hbuf[(l - 1) & 1], hsz);
     P->wmax = std::max(P->wmax, P->m[l] * s.r[l]);
-    P->mu[l] = plan_mu(P->m[l], P->ncol[l], (int)s.r[l], num_sms, dist);
+    P->mu[l] = plan_mu(P->m[l], P->ncol[l], (int)s.r[l], num_sms, dist, xpersist);
     P->mu_bytes = std::max(P->mu_bytes, P->mu[l].bytes);
   }
   size_t o = 0;
@@ -1028,7 +1045,7 @@ ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t*
   DecompPlan* Pp = new DecompPlan();
   std::unique_ptr<DecompPlan> guard(Pp);
   DecompPlan& P = *Pp;
-  plan_decompose(s, h->num_sms, h->nranks, h->rank, h->comm != nullptr, &P);
+  plan_decompose(s, h->num_sms, h->nranks, h->rank, h->comm != nullptr, &P, h->xready && h->xmode == 1);
   char* ws;
   if (workspace) {
     if (workspace_bytes < P.bytes)
@@ -1915,6 +1932,71 @@ ntt_status ntt_get_unique_id(void* id128) {
   return NTT_OK;
 }
 
+// Exchange buffers of the persistent kernels' in-kernel cross-GPU reduction (PersistArgs::xpeers):
+// every rank allocates xbuf_bytes(nranks), exports it with cudaIpcGetMemHandle, the handles are
+// all-gathered by nranks ncclBroadcasts of 64 bytes, and every rank opens the others' buffers
+// (NVLink peer access within one node).  The ranks then agree (ncclAllReduce of a 0/1 flag, min)
+// so that either all of them run the in-kernel exchange or all keep the per-pass ncclAllReduce
+// path (xready = false) -- a mixed outcome would deadlock the first pass.
+static ntt_status setup_exchange(ntt_handle h) {
+  const int p = h->nranks;
+  const size_t bytes = xbuf_bytes(p);
+  CU(h, cudaMalloc(&h->xbuf, bytes));
+  CU(h, cudaMemset(h->xbuf, 0, bytes));
+  std::vector<void*> bases(p, nullptr);
+  bases[h->rank] = h->xbuf;
+  bool ok = true;
+  if (p > 1) {
+    cudaIpcMemHandle_t mine;
+    memset(&mine, 0, sizeof mine);
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    if (cudaIpcGetMemHandle(&mine, h->xbuf) != cudaSuccess) {
+      ok = false;
+      cudaGetLastError();
+    }
+    char* dh = nullptr;
+    CU(h, cudaMalloc(&dh, 64 * (size_t)p));
+    CU(h, cudaMemcpy(dh + 64 * (size_t)h->rank, &mine, 64, cudaMemcpyHostToDevice));
+    for (int q = 0; q < p; ++q)
+      NC(h, g_nccl.Broadcast(dh + 64 * (size_t)q, dh + 64 * (size_t)q, 64, ncclInt8, q, h->comm, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    std::vector<cudaIpcMemHandle_t> all(p);
+    CU(h, cudaMemcpy(all.data(), dh, 64 * (size_t)p, cudaMemcpyDeviceToHost));
+    cudaFree(dh);
+    for (int q = 0; q < p && ok; ++q) {
+      if (q == h->rank) continue;
+      if (cudaIpcOpenMemHandle(&bases[q], all[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        ok = false;
+        cudaGetLastError();
+        break;
+      }
+      h->xopened.push_back(bases[q]);
+    }
+    int* dflag = nullptr;
+    CU(h, cudaMalloc(&dflag, sizeof(int)));
+    const int mine_ok = ok ? 1 : 0;
+    CU(h, cudaMemcpy(dflag, &mine_ok, sizeof(int), cudaMemcpyHostToDevice));
+    NC(h, g_nccl.AllReduce(dflag, dflag, 1, ncclInt32, ncclMin, h->comm, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    int all_ok = 0;
+    CU(h, cudaMemcpy(&all_ok, dflag, sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(dflag);
+    ok = all_ok == 1;
+  }
+  if (!ok) {  // every rank: per-pass ncclAllReduce path
+    for (void* pp : h->xopened) cudaIpcCloseMemHandle(pp);
+    h->xopened.clear();
+    cudaFree(h->xbuf);
+    h->xbuf = nullptr;
+    h->xmode = 0;
+    return NTT_OK;
+  }
+  CU(h, cudaMalloc(reinterpret_cast<void**>(&h->xpeers), sizeof(double*) * (size_t)p));
+  CU(h, cudaMemcpy(h->xpeers, bases.data(), sizeof(double*) * (size_t)p, cudaMemcpyHostToDevice));
+  h->xready = true;
+  return NTT_OK;
+}
+
 ntt_status ntt_create_dist(ntt_handle* out, int device, void* cuda_stream, const void* id128, int nranks, int rank) {
   return ntt_create_dist_grid(out, device, cuda_stream, id128, nranks, rank, 1, nranks);
 }
@@ -1949,6 +2031,11 @@ ntt_status ntt_create_dist_grid(ntt_handle* out, int device, void* cuda_stream, 
     *out = nullptr;
     return NTT_ERR_NCCL;
   }
+  if ((s = setup_exchange(h))) {
+    ntt_destroy(h);
+    *out = nullptr;
+    return s;
+  }
   return NTT_OK;
 }
 
@@ -1967,6 +2054,29 @@ int ntt_dist_size(ntt_handle h) { return h ? h->nranks : -1; }
 }  // extern "C"
 
 extern "C" int64_t ntt_collective_count(ntt_handle h) { return h ? h->collectives : -1; }
+
+extern "C" ntt_status ntt_set_dist_exchange(ntt_handle h, int mode) {
+  if (!h || (mode != 0 && mode != 1)) return NTT_ERR_INVALID_ARG;
+  if (!h->comm) return fail(h, NTT_ERR_INVALID_ARG, "ntt_set_dist_exchange needs an ntt_create_dist* handle");
+  if (mode == 1 && !h->xready) return fail(h, NTT_ERR_UNSUPPORTED, "exchange buffers are not mapped");
+  CU(h, cudaStreamSynchronize(h->stream));
+  if (h->gstream) CU(h, cudaStreamSynchronize(h->gstream));
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);  // the decompose graph bakes in the path
+  h->gexec = nullptr;
+  h->gkey.clear();
+  h->xmode = mode;
+  return NTT_OK;
+}
+
+extern "C" int64_t ntt_peer_exchange_count(ntt_handle h) {
+  if (!h || !h->xready) return -1;
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) return -1;
+  if (h->gstream && cudaStreamSynchronize(h->gstream) != cudaSuccess) return -1;
+  unsigned long long v = 0;
+  const char* seqp = reinterpret_cast<const char*>(h->xbuf) + xbuf_bytes(h->nranks) - sizeof(unsigned long long) * 8;
+  if (cudaMemcpy(&v, seqp, sizeof v, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return (int64_t)v;
+}
 
 extern "C" ntt_status ntt_stream_ceiling(ntt_handle h, const void* buf, int64_t bytes, int32_t reps, double* gbps) {
   if (!h || !buf || !gbps || bytes < 16 || (bytes & 15) || reps < 1 || (reinterpret_cast<uintptr_t>(buf) & 15))

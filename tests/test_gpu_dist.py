@@ -1,8 +1,12 @@
-"""The library's NCCL path (ntt_create_dist / ntt_create_dist_grid) on one GPU.
+"""The library's distributed path (ntt_create_dist / ntt_create_dist_grid) on one GPU.
 
 A handle made by ntt_create_dist* always takes the distributed branches, also with
-a 1-rank communicator: the per-pass reduction of the fp64 (X H^T, H H^T) partials
-followed by ncclAllReduce (dist_reduce), the global-column-index H init
+a 1-rank communicator.  The per-pass cross-GPU reduction of the fp64 (X H^T, H H^T)
+partials runs either inside the persistent kernels (ntt_set_dist_exchange mode 1,
+the default: NVLink peer stores into the ranks' IPC-mapped exchange buffers, release /
+acquire flags, rank-order sum; ntt_peer_exchange_count proves the device did it) or
+as a per-pass ncclAllReduce between kernel launches (mode 0, dist_reduce); then the
+global-column-index H init
 (k_fill_uniform_cols), the last-core gather by per-rank broadcasts into a staging
 area plus k_gather_last_core, the all-reduce of the Eq. 3 sums, and on the
 tensor-core path tc_reduce_PQ / tc_wupdate_ex / tc_reduce_S / tc_hupdate_ex over
@@ -34,41 +38,65 @@ def handles():
 @pytest.mark.parametrize("dims,ranks,iters", [([5, 4, 5, 6], [4, 3, 2], 10), ([16, 16, 16, 16], [8, 8, 8], 10),
                                               ([6] * 6, [5] * 5, 10), ([64, 32, 64], [8, 8], 5),
                                               ([20, 30, 40, 30], [10, 12, 9], 5)])
-def test_dist_handle_decompose_matches(handles, ora, dims, ranks, iters):
+@pytest.mark.parametrize("mode", [0, 1])
+def test_dist_handle_decompose_matches(handles, ora, dims, ranks, iters, mode):
     h1, hd = handles
+    hd.ntt_set_dist_exchange(mode)
     A = ora.tt_full_f32(dims, ranks, ni.make_cores(dims, ranks, 0), noise_amp=0.3, seed=0)
     Ad = torch.from_numpy(A).cuda()
     c1 = torch.empty(ora.cores_size(dims, ranks), device="cuda")
     cd = torch.empty_like(c1)
     e1 = h1.ntt_decompose(Ad, dims, ranks, iters, 0, 1e-16, c1, want_error=True)
-    n0 = hd.collective_count
+    n0, x0 = hd.collective_count, hd.peer_exchange_count
     ed = hd.ntt_decompose(Ad, dims, ranks, iters, 0, 1e-16, cd, want_error=True)
-    # per MU pass one all-reduce; a graph replay of an identical call issues none anew
-    assert hd.collective_count - n0 >= (len(dims) - 1) * iters
+    if mode == 0:
+        # per MU pass one all-reduce; a graph replay of an identical call issues none anew
+        assert hd.collective_count - n0 >= (len(dims) - 1) * iters
+    else:
+        # steps on a persistent one-pass kernel exchange inside it (one per pass), the others
+        # (n % 4 != 0, tall / square unfoldings) all-reduce per pass
+        nx = hd.peer_exchange_count - x0
+        assert nx % iters == 0
+        if dims == [16, 16, 16, 16]:  # m = 16 and 128 at r = 8: all three steps persistent
+            assert nx == 3 * iters
+        assert nx + (hd.collective_count - n0) >= (len(dims) - 1) * iters
     torch.cuda.synchronize()
     a, b = c1.cpu().numpy().astype(np.float64), cd.cpu().numpy().astype(np.float64)
     assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(a)
     ref = ora.ntt_decompose(A, ranks, iters, seed=0)
     assert np.linalg.norm(b - ref) <= 1e-4 * np.linalg.norm(ref)
     assert abs(ed - e1) <= 1e-5 * e1
+    hd.ntt_set_dist_exchange(1)
 
 
-@pytest.mark.parametrize("m,n,r", [(32, 4096, 8), (256, 2048, 8), (100, 700, 16)])
-def test_dist_handle_nmf_mu(handles, ora, m, n, r):
+@pytest.mark.parametrize("m,n,r", [(32, 4096, 8), (256, 2048, 8), (100, 700, 16), (8, 4096, 4), (40, 1024, 8),
+                                   (256, 4096, 12), (64, 2048, 8)])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_dist_handle_nmf_mu(handles, ora, m, n, r, mode):
     h1, hd = handles
+    hd.ntt_set_dist_exchange(mode)
     rng = np.random.default_rng(1)
     X = rng.random((m, n)).astype(np.float32)
     W0 = ni.uniform(m * r, 1, 0x202).reshape(m, r).astype(np.float32)
     H0 = ni.uniform(r * n, 1, 0x203).reshape(r, n).astype(np.float32)
     Xd = torch.from_numpy(X).cuda()
     Wd, Hd = torch.from_numpy(W0.copy()).cuda(), torch.from_numpy(H0.copy()).cuda()
-    n0 = hd.collective_count
+    n0, x0 = hd.collective_count, hd.peer_exchange_count
     hd.ntt_nmf_mu(Xd, m, n, n, r, 8, 1e-16, Wd, Hd)
-    assert hd.collective_count - n0 >= 8
+    if mode == 0:  # every shape here runs a persistent one-pass kernel on mode 1
+        assert hd.collective_count - n0 >= 8
+    else:
+        assert hd.collective_count == n0 and hd.peer_exchange_count - x0 == 8
+        # 1 rank: the rank-order sum of one vector is that vector, so the in-kernel exchange is
+        # bit-identical to the single-GPU persistent kernel
+        W1, H1 = torch.from_numpy(W0.copy()).cuda(), torch.from_numpy(H0.copy()).cuda()
+        h1.ntt_nmf_mu(Xd, m, n, n, r, 8, 1e-16, W1, H1)
+        assert torch.equal(W1, Wd) and torch.equal(H1, Hd)
     Wo, Ho = ora.nmf_mu(X, W0.astype(np.float64), H0.astype(np.float64), 8)
     W, H = Wd.cpu().numpy(), Hd.cpu().numpy()
     assert np.linalg.norm(W - Wo) <= 1e-4 * np.linalg.norm(Wo)
     assert np.linalg.norm(H - Ho) <= 1e-4 * np.linalg.norm(Ho)
+    hd.ntt_set_dist_exchange(1)
 
 
 @pytest.mark.parametrize("m,n,r", [(512, 1024, 16), (1000, 776, 32)])
