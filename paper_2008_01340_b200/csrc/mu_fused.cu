@@ -2101,35 +2101,19 @@ struct FusedPlan {
   int bn;    // tile width (columns)
 };
 
-// the k_fused variant launch_fused picks for m <= 40 (environment knobs: DESIGN.md s.6)
+// the k_fused variant launch_fused picks for m <= 40
 FusedPlan fused_plan(int64_t m, int64_t n, int r) {
-  static const bool x3d_on = [] {
-    const char* e = getenv("NTT_X3D");
-    const char* b = getenv("NTT_W_BN");  // the 3-D box spans 4 blocks: 128-column tiles only
-    return !(e && e[0] == '0') && !(b && b[0] == '6');
-  }();
-  static const int x3d_max_ux = [] {
-    const char* e = getenv("NTT_X3D_UX");
-    return e ? atoi(e) : 5;
-  }();
-  // experiment knobs: NTT_W_BN=64 (64-column tiles for UX >= 4), NTT_W_HDIRECT=0/1 (default: direct H loads
-  // when m <= 16 or r < 8, i.e. when H is a large share of the traffic)
-  static const int w_bn = [] {
-    const char* e = getenv("NTT_W_BN");
-    return (e && e[0] == '6') ? 64 : 128;
-  }();
-  static const int w_hd = [] {
-    const char* e = getenv("NTT_W_HDIRECT");
-    return e ? (e[0] == '1' ? 1 : 0) : -1;
-  }();
   const int ux = ux_for(m);
   FusedPlan p;
-  p.x3d = ux <= x3d_max_ux && (n % 32) == 0 && x3d_on;
+  // X (and staged H) through 3-D maps {32 cols, 8 rows, n / 32 blocks}: one 4 KB box per
+  // 128-column tile instead of four 1 KB boxes (TMA wants multi-KB transactions, tools/tmabench.cu)
+  p.x3d = (n % 32) == 0;
   // with the 3-D maps staging H through TMA (one 4 KB box per tile) beats the lanes' direct
   // loads, which cannot keep enough bytes in flight (tools/membench.cu): config 4 step 1
-  // 59.4 -> 53.7 ms, steps 2-5 -2 to -5 %
-  p.hd = (w_hd >= 0) ? (w_hd == 1) : (p.x3d ? false : (ux <= 2 || r < 8));
-  p.bn = (ux >= 4 && w_bn == 64) ? 64 : 128;
+  // 59.4 -> 53.7 ms, steps 2-5 -2 to -5 %; without them direct H loads win where H is a large
+  // share of the traffic (m <= 16 or r < 8)
+  p.hd = p.x3d ? false : (ux <= 2 || r < 8);
+  p.bn = 128;
   return p;
 }
 
@@ -2184,7 +2168,6 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
   }
   if (e != cudaSuccess) return e;
   const int rc = rcls_for(r);
-  const int w_bn = fp.bn;
   const bool hd = fp.hd;
   // H boxes (staged path): 3-D as well when X uses the 3-D map (block stride 128 B of row pitch n)
   auto hmap = [&](CUtensorMap* mp, const float* base) {
@@ -2194,7 +2177,7 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
   e = hmap(&mh, H);
   if (e != cudaSuccess) return e;
   if (pa.bcdFold) {  // BCD H_m fold: both H buffers (fused_fold_ok() said this variant runs)
-    if (hd || w_bn != 128 || !pa.Hout || !pa.Hout2 || !pa.bcdRole) return cudaErrorNotSupported;
+    if (hd || !pa.Hout || !pa.Hout2 || !pa.bcdRole) return cudaErrorNotSupported;
     if ((e = hmap(&mb0, pa.Hout)) != cudaSuccess) return e;
     if ((e = hmap(&mb1, pa.Hout2)) != cudaSuccess) return e;
 #define LFF(RR, UU) \
@@ -2223,12 +2206,9 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
     LFF(8, 5);
 #undef LFF
   }
-#define LF(RR, UU)                                                                                                              \
-  return (UU >= 4 && w_bn == 64)                                                                                                  \
-             ? (hd ? launch_t<RR, UU, 8, true, 64>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, ef, pa, st)  \
-                   : launch_t<RR, UU, 8, false, 64>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, ef, pa, st)) \
-             : (hd ? launch_t<RR, UU, 8, true, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, ef, pa, st) \
-                   : launch_t<RR, UU, 8, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, ef, pa, st))
+#define LF(RR, UU)                                                                                                   \
+  return hd ? launch_t<RR, UU, 8, true, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, ef, pa, st) \
+            : launch_t<RR, UU, 8, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, ef, pa, st)
   if (rc == 2) {
     if (ux == 1) LF(2, 1);
     if (ux == 2) LF(2, 2);
@@ -2249,16 +2229,6 @@ cudaError_t launch_fused(const float* X, int64_t ldx, int64_t m, int64_t n, int 
   }
   if (ux == 1) LF(8, 1);
   if (ux == 2) LF(8, 2);
-  static const int w_nwt = [] {
-    const char* e = getenv("NTT_W_NWT");
-    return e ? atoi(e) : 8;
-  }();
-  if (ux == 4 && !hd && w_bn == 128 && w_nwt == 6)
-    return launch_t<8, 4, 6, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, ef, pa, st);
-  if (ux == 4 && !hd && w_bn == 128 && w_nwt == 9)
-    return launch_t<8, 4, 9, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, ef, pa, st);
-  if (ux == 4 && !hd && w_bn == 128 && w_nwt == 7)
-    return launch_t<8, 4, 7, false, 128>(mx, mh, (int)m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, grid, ef, pa, st);
   if (ux == 4) LF(8, 4);
   LF(8, 5);
 #undef LF

@@ -321,9 +321,9 @@ def test_generate_matches_oracle_generator(h, ora):
 
 @pytest.mark.parametrize("m,n,r", [(2, 4100, 2), (4, 60000, 4), (6, 70004, 5), (8, 1 << 16, 3), (1, 1024, 1),
                                    (6, 800, 6), (7, 4000, 4)])
-def test_nmf_mu_small_path_parity(h, ora, m, n, r, monkeypatch):
-    """The register-resident m <= 8 pass (mu_small.cu, NTT_SMALL=1) against the oracle."""
-    monkeypatch.setenv("NTT_SMALL", "1")
+def test_nmf_mu_small_path_parity(h, ora, m, n, r):
+    """Very short unfoldings (m <= 8: config 4 step 1's shape class; k_fused with the 3-D X boxes,
+    or direct H loads when n % 32 != 0) against the oracle."""
     X, W0, H0 = _mu_inputs(m, n, r, m * 11 + n)
     Xd, Wd, Hd = dev(X), dev(W0), dev(H0)
     h.ntt_nmf_mu(Xd, m, n, n, r, 10, 1e-16, Wd, Hd)
