@@ -1100,7 +1100,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   }
   // two-level P accumulation (fp32 over <= 8 tiles, then fp64); RK = 16 adds each tile's fp32 sum to
   // fp64 directly (the fp32 set would not fit in 200 registers next to the fp64 one)
-  constexpr bool P32 = RK == 8;
+  constexpr bool P32 = false;  // RK = 8 too: the fp32 level cost 16 registers and 72 B of spills in the tile loop
   float pacc[P32 ? NB : 1][2][NN][4];
   double paccd[NB][2][NN][4];
   constexpr int QR = RK / NW;  // Q rows per warp
@@ -1255,7 +1255,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 #pragma unroll
       for (int hh = 0; hh < HH; ++hh) {
         const int kt = (tid >> 5) + NW * hh;
-        const float hkc = hl[kt];
+        const float hkc = *reinterpret_cast<const float*>(hbox + hc_off(kt, ct));  // not hl[kt]: a run-time index would put hl in local memory
         float hn;
         if constexpr (UPD) {
           float S = 0.0f;
