@@ -27,6 +27,13 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# what the paths compute in (R13): storage fp32 everywhere
+ARITH_NTT = ("X.W and X.Hn^T products on warp-level tensor cores (mma.sync m16n8k16) as fp16 hi + lo splits of "
+             "power-of-two-scaled operands (hi.hi + hi.lo + lo.hi, ~22 significant bits), fp32 accumulation within a "
+             "tile, fp64 across tiles / CTAs / GPUs; m <= 16 unfoldings: fp32 FFMA; H update fp32; W update and "
+             "Grams fp64 (k_fused_m / k_fused_c / k_fused)")
+ARITH_TC = ("tcgen05 kind::f16 with fp16 hi + lo splits (~22 significant bits), fp32 TMEM accumulation flushed to "
+            "fp64; W update fp64, H update fp32")
 METRIC = "NMF-MU iterations/sec (nTT sweep, all d-1 steps; ntt wall time and HBM GB/s in roofline)"
 UNIT = "MU-iter/s"
 
@@ -208,24 +215,30 @@ def other_workloads(h, P, ni, torch, steps=2):
     import numpy as np
     out = {}
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    for name in ("config1", "config4"):
+    for name in ("config1", "config4", "paper256"):
         w = ni.workloads()[name]
         cores0 = torch.from_numpy(ni.make_cores(w.dims, w.ranks, w.seed).astype(np.float32)).cuda()
         A = torch.empty(w.numel, device="cuda")
         h.ntt_generate(w.dims, w.ranks, cores0, w.noise_amp, w.seed, ni.STREAM_NOISE, A)
         cores = torch.empty(P.cores_size(w.dims, w.ranks), device="cuda")
         err = h.ntt_decompose(A, w.dims, w.ranks, w.iters, w.seed, 1e-16, cores, want_error=True)
+        nrep = 1 if name == "paper256" else steps
         e0, e1 = ev(), ev()
         e0.record()
-        for _ in range(steps):
+        for _ in range(nrep):
             h.ntt_decompose(A, w.dims, w.ranks, w.iters, w.seed, 1e-16, cores)
         e1.record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / steps
+        ms = e0.elapsed_time(e1) / nrep
         its = (len(w.dims) - 1) * w.iters
         out[name] = {"ntt_wall_ms": ms, "mu_iter_per_s": its / (ms / 1e3), "rel_error": err,
-                     "dims": w.dims, "ranks": w.ranks, "iters_per_step": w.iters}
+                     "dims": w.dims, "ranks": w.ranks, "iters_per_step": w.iters,
+                     "arithmetic": ARITH_NTT}
+        if name == "paper256":
+            out[name]["note"] = ("the paper's strong-scaling tensor (P:311-312, P:338: 256^4, TT ranks 1,10,10,10,1) "
+                                 "at 1 GPU; step 1 runs k_fused_c's rank-16 class")
         del A, cores
+        torch.cuda.empty_cache()
     for name, rows, iters in (("config2", None, 20), ("config5", 32768, 10)):
         w = ni.workloads()[name]
         m, n = w.dims
@@ -250,7 +263,7 @@ def other_workloads(h, P, ni, torch, steps=2):
         alg = 4.0 * n * (2 * m + 3 * r)  # 2-pass algorithmic bytes per iteration
         out[name] = {"mu_iter_per_s": 1e3 / ms, "ms_per_iter": ms, "m": m, "n": n, "r": r, "timed_iters": iters,
                      "effective_GBps": alg / (ms / 1e3) / 1e9,
-                     "path": "tcgen05 kind::f16 fp16x2 2-pass (mu_tc16.cu)",
+                     "path": "tcgen05 kind::f16 fp16x2 2-pass (mu_tc16.cu)", "arithmetic": ARITH_TC,
                      "note": "config 5 on the 1-GPU row slice (SURVEY s.8(d)); inputs X = W0 H0 + noise on device"}
         # BCD NMF (Alg. 3, SURVEY s.8(f) f1) on the same X: two passes over X per iteration
         h.ntt_fill_uniform(W, m * r, w.seed, ni.stream_w(1))
@@ -498,7 +511,7 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": its / (ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if ws > 1 else "strong",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f32", "arithmetic": ARITH_NTT, "data": "synthetic",
         "config": {"workload": args.workload, "dims": dims, "ranks": ranks, "iters_per_step": iters,
                    "mu_iters_per_step": its, "noise": f"{w.noise} amp {w.noise_amp}",
                    "l2": "input (4.29 GB) larger than L2; no flush", "parallelism": f"last-mode x{ws}",

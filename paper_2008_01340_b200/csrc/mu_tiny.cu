@@ -24,9 +24,6 @@ constexpr int TINY_BLK = 64;  // fp32 partial block: 32 lanes x 64 columns
 // consecutive rows hit distinct banks
 __host__ __device__ inline int tiny_ld(int n) { return (n & 1) ? n : n + 1; }
 
-// the row-chunked H update (S = W^T X entry-parallel) for few columns; one thread per column otherwise
-__host__ __device__ inline bool tiny_tall(int m, int n, int R) { return m > 64 || 2 * R * n <= TINY_THREADS; }
-
 template <int R>
 struct TinyLayout {
   // offsets in bytes, all 16-aligned
@@ -42,8 +39,6 @@ struct TinyLayout {
     o = al(o + sizeof(double) * (size_t)R * R);       // Q
     o = al(o + sizeof(float) * (size_t)R * R);        // G (fp32 for E = G H)
     o = al(o + sizeof(double) * (size_t)nch * (m * R + R * R));  // chunk partials (n <= 256)
-    if (tiny_tall(m, n, R)) o = al(o + sizeof(float) * (size_t)R * ld);  // H new (row-chunked H update)
-    o = al(o + sizeof(double) * (size_t)TINY_THREADS);  // S / G row-chunk partials
     return o;
   }
 };
@@ -72,10 +67,6 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
   o = al(o + sizeof(float) * (size_t)R * R);
   double* part = reinterpret_cast<double*>(sm + o);
   o = al(o + sizeof(double) * (size_t)nch * (m * R + R * R));
-  const bool tall = tiny_tall(m, n, R);
-  float* Hn = reinterpret_cast<float*>(sm + o);
-  if (tall) o = al(o + sizeof(float) * (size_t)R * ld);
-  double* cp = reinterpret_cast<double*>(sm + o);  // TINY_THREADS doubles
 
   const int tid = threadIdx.x, T = blockDim.x;
   for (int64_t e = tid; e < (int64_t)m * n; e += T) {
@@ -94,11 +85,6 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
 
   const int EP = m * R, EQ = R * R, E = EP + EQ;
   const int nblk = (n + TINY_BLK - 1) / TINY_BLK;
-  const int ES = R * n;
-  // row chunks of the tall-X H update (S = W^T X entry-parallel; see below)
-  int cs = T / ES;
-  cs = cs < 1 ? 1 : cs;
-  if (cs > m / 16) cs = m / 16 < 1 ? 1 : m / 16;
   for (int it = 0; it < iters; ++it) {
     if (n <= 256) {
     // ---- short rows: P = X H^T and Q = H H^T entry-parallel, entry e x chunk c of
@@ -193,78 +179,15 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
     }
     __syncthreads();
     for (int e = tid; e < EP; e += T) Ws[e] = Wn[e];
-    // ---- G = W^T W (fp64): gc row chunks (fixed order), summed in chunk order
-    {
-      int gc = T / EQ;
-      gc = gc < 1 ? 1 : (gc > 8 ? 8 : gc);
-      if (gc > m) gc = m;
-      for (int t = tid; t < EQ * gc; t += T) {
-        const int e = t % EQ, c = t / EQ;
-        const int k = e / R, l = e % R;
-        const int i0 = m * c / gc, i1 = m * (c + 1) / gc;
-        double s0 = 0.0, s1 = 0.0;
-        if (k < r && l < r) {
-          int i = i0;
-          for (; i + 1 < i1; i += 2) {
-            s0 += (double)Wn[i * R + k] * (double)Wn[i * R + l];
-            s1 += (double)Wn[(i + 1) * R + k] * (double)Wn[(i + 1) * R + l];
-          }
-          if (i < i1) s0 += (double)Wn[i * R + k] * (double)Wn[i * R + l];
-        }
-        cp[c * EQ + e] = s0 + s1;
-      }
-      __syncthreads();
-      for (int e = tid; e < EQ; e += T) {
-        double s = 0.0;
-        for (int c = 0; c < gc; ++c) s += cp[c * EQ + e];
-        Gf[e] = (float)s;
-      }
+    // ---- G = W^T W (fp64, fixed order over rows)
+    for (int e = tid; e < EQ; e += T) {
+      const int k = e / R, l = e % R;
+      double sg = 0.0;
+      if (k < r && l < r)
+        for (int i = 0; i < m; ++i) sg += (double)Wn[i * R + k] * (double)Wn[i * R + l];
+      Gf[e] = (float)sg;
     }
     __syncthreads();
-    if (tall) {
-      // ---- H update for tall X (few columns per thread): S = W^T X entry-parallel over
-      //      (k, j) x cs row chunks (fp32 inside a chunk, fp64 across), then E = G H and the
-      //      quotient; consecutive threads take consecutive columns (conflict-free X reads)
-      for (int t = tid; t < ES * cs; t += T) {
-        const int e = t % ES, c = t / ES;
-        const int k = e / n, j = e % n;
-        const int i0 = m * c / cs, i1 = m * (c + 1) / cs;
-        float s0 = 0.0f, s1 = 0.0f;
-        int i = i0;
-        for (; i + 1 < i1; i += 2) {
-          s0 = fmaf(Ws[i * R + k], Xs[i * ld + j], s0);
-          s1 = fmaf(Ws[(i + 1) * R + k], Xs[(i + 1) * ld + j], s1);
-        }
-        if (i < i1) s0 = fmaf(Ws[i * R + k], Xs[i * ld + j], s0);
-        if (cs == 1) {
-          float ek = 0.0f;
-#pragma unroll
-          for (int l = 0; l < R; ++l) ek = fmaf(Gf[k * R + l], Hs[l * ld + j], ek);
-          Hn[k * ld + j] = (k < r) ? mu_quot(Hs[k * ld + j], s0 + s1, ek, eps) : 0.0f;
-        } else {
-          cp[c * ES + e] = (double)(s0 + s1);
-        }
-      }
-      __syncthreads();
-      if (cs > 1) {
-        for (int e = tid; e < ES; e += T) {
-          const int k = e / n, j = e % n;
-          double s = 0.0;
-          for (int c = 0; c < cs; ++c) s += cp[c * ES + e];
-          float ek = 0.0f;
-#pragma unroll
-          for (int l = 0; l < R; ++l) ek = fmaf(Gf[k * R + l], Hs[l * ld + j], ek);
-          Hn[k * ld + j] = (k < r) ? mu_quot(Hs[k * ld + j], (float)s, ek, eps) : 0.0f;
-        }
-        __syncthreads();
-      }
-      for (int e = tid; e < ES; e += T) {
-        const int k = e / n, j = e % n;
-        Hs[k * ld + j] = Hn[k * ld + j];
-      }
-      __syncthreads();
-      continue;
-    }
     // ---- H update, one thread per column: S = W^T X[:, j], E = G H[:, j]
     for (int j = tid; j < n; j += T) {
       float s[R], h[R];
