@@ -1119,6 +1119,18 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 #pragma unroll
   for (int qq = 0; qq < QR; ++qq) qd[qq] = 0.0;
   int since_flush = 0;
+  // X16 passes: the block scales of a tile (written by the prologue pass next to its blocks, read
+  // from L2) are loaded one tile ahead -- on the critical path they cost an L2 round trip per tile
+  float xsn[NB];
+  auto load_scales = [&](int64_t jj) {
+    const float* sc = reinterpret_cast<const float*>(pa.x16 + (b + jj * gridDim.x) * x16_stride + nblk * 4096);
+#pragma unroll
+    for (int bb = 0; bb < NB; ++bb) {
+      const int gb = warp * NB + bb;
+      xsn[bb] = gb < nblk ? __ldcg(sc + gb) : 0.f;
+    }
+  };
+  if (x16_read && J > 0) load_scales(0);
 
   for (int64_t j = 0; j < J; ++j) {
     const int s = ring_s;
@@ -1138,13 +1150,9 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       asm volatile("bar.sync 1, %0;" ::"r"(NBAR) : "memory");
     }
     if (x16_read) {
-      // the block scales of this tile (written by the prologue pass next to its blocks)
-      const float* sc = reinterpret_cast<const float*>(pa.x16 + (b + j * gridDim.x) * x16_stride + nblk * 4096);
 #pragma unroll
-      for (int bb = 0; bb < NB; ++bb) {
-        const int gb = warp * NB + bb;
-        xsi[bb] = gb < nblk ? __ldcg(sc + gb) : 0.f;
-      }
+      for (int bb = 0; bb < NB; ++bb) xsi[bb] = xsn[bb];
+      if (j + 1 < J) load_scales(j + 1);
     } else {
       // ---- this warp's rows of the tile -> fp16 hi / lo parts, in place (each 32-row block of
       // 4 KB fp32 becomes [hi: 32 x 32 fp16 | lo: 32 x 32 fp16]); per-block power-of-two scale;
