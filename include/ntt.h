@@ -187,7 +187,8 @@ ntt_status ntt_decompose_bcd(ntt_handle h, const float* A, int32_t d, const int6
  * truncated SVD of X_l: core l = U_r (left singular vectors, signs fixed so the
  * largest-magnitude entry of every column is positive), X_{l+1} = reshape(S_r V_r^T).
  * Singular vectors come from the fp64 Gram of the smaller side (Householder +
- * bisection + inverse iteration + Rayleigh-Ritz in one CTA), so min(m, n) <= 512
+ * bisection + inverse iteration + Rayleigh-Ritz; one CTA up to min(m, n) = 512, the
+ * Householder reduction and bisection on the whole grid above), so min(m, n) <= 4096
  * per step (else NTT_ERR_UNSUPPORTED) and ranks <= 64 (max_ranks caps further).
  * Cores may be negative.  Arguments, layouts and errors as ntt_decompose_eps.   */
 ntt_status ntt_tt_svd(ntt_handle h, const float* A, int32_t d, const int64_t* dims, double tt_eps,

@@ -49,6 +49,11 @@ cudaError_t launch_tiny(const float* X, int64_t ldx, int64_t m, int64_t n, int r
 // and a warp-per-eigenvalue multisection above) -> r = smallest k with tail energy <= tt_eps.
 // Writes d_rank[0] (and the N eigenvalues ascending to d_eig when non-null).
 constexpr int kRankMaxN = 4096;
+// the grid-wide part for N > 512 (tt_rank.cu): cooperative Householder reduction of C (destroyed;
+// reflector k stored in row k of Vh when non-null) to the tridiagonal (d, e), then every
+// eigenvalue ascending into lam by warp multisection.  p: N doubles scratch, ctr: 64 bytes.
+cudaError_t launch_tridiag_eig(double* C, int N, double* p, double* d, double* e, double* lam, unsigned* ctr,
+                               double* Vh, int num_sms, cudaStream_t st);
 size_t rank_rule_bytes(int64_t N, int64_t T, int num_sms);
 cudaError_t launch_rank_rule(const float* X, int64_t m, int64_t n, int64_t ldx, double tt_eps, char* ws,
                              int num_sms, int* d_rank, double* d_eig, cudaStream_t st);
@@ -59,10 +64,11 @@ cudaError_t launch_gram(const float* X, int64_t m, int64_t n, int64_t ldx, char*
                         cudaStream_t st);
 
 // TT-SVD baseline (tt_svd.cu, SURVEY s.8(f) f4): eigenvectors of the top r eigenvalues of a
-// symmetric PSD C (N <= 512, r <= 64 chosen by the tail rule and capped at rcap)
+// symmetric PSD C (N <= kRankMaxN: one CTA up to 512, the grid reduction + k_svd_vec +
+// k_backtransform above; r <= 64 chosen by the tail rule and capped at rcap)
 size_t svd_eig_bytes(int64_t N);
 cudaError_t launch_svd_eig(double* C, int N, char* ws, double tt_eps, int rcap, double* eig_asc, double* lam,
-                           int* d_rank, double* U, cudaStream_t st);
+                           int* d_rank, double* U, int num_sms, cudaStream_t st);
 cudaError_t launch_sign_cols(const double* M, int64_t rows, int r, const double* scale, float* out, double* sgn,
                              cudaStream_t st);
 cudaError_t launch_rows_from_spart(const double* Spart, int nS, int64_t n, int r, float* Xn, cudaStream_t st);

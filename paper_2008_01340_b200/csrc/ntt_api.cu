@@ -1692,7 +1692,7 @@ ntt_status ntt_tt_svd(ntt_handle h, const float* A, int32_t d, const int64_t* di
     // per-step scratch for every m the previous rank allows
     for (int64_t rp = 1; rp <= cap[l - 1]; ++rp) {
       const int64_t m = rp * s0.dims[l - 1], n = ncol[l], N = std::min(m, n);
-      if (N > 512) continue;  // rejected at run time
+      if (N > kRankMaxN) continue;  // rejected at run time
       size_t b = align_up(rank_rule_bytes(N, std::max(m, n), h->num_sms)) + align_up(svd_eig_bytes(N)) +
                  align_up(sizeof(double) * (size_t)N * 64) + align_up(sizeof(double) * (size_t)(N + 64 * 4 + 8));
       if (m <= n) {
@@ -1733,8 +1733,8 @@ ntt_status ntt_tt_svd(ntt_handle h, const float* A, int32_t d, const int64_t* di
   for (int l = 1; l < d; ++l) {
     const int64_t m = rprev * s0.dims[l - 1], n = ncol[l], N = std::min(m, n);
     h->cur_step = l;
-    if (N > 512)
-      return fail(h, NTT_ERR_UNSUPPORTED, "TT-SVD needs min(m, n) <= 512 (step %d: %lld x %lld)", l, (long long)m,
+    if (N > kRankMaxN)
+      return fail(h, NTT_ERR_UNSUPPORTED, "TT-SVD needs min(m, n) <= %d (step %d: %lld x %lld)", kRankMaxN, l, (long long)m,
                   (long long)n);
     const int rcap = (int)std::min<int64_t>(cap[l], N);
     // step scratch
@@ -1757,7 +1757,7 @@ ntt_status ntt_tt_svd(ntt_handle h, const float* A, int32_t d, const int64_t* di
     int* d_rank = reinterpret_cast<int*>(sgn + 64);
     double* C = nullptr;
     LAUNCH(h, launch_gram(X, m, n, n, gws, h->num_sms, &C, cs));
-    LAUNCH(h, launch_svd_eig(C, (int)N, ews, tt_eps, rcap, eig, lam, d_rank, Uv, cs));
+    LAUNCH(h, launch_svd_eig(C, (int)N, ews, tt_eps, rcap, eig, lam, d_rank, Uv, h->num_sms, cs));
     int rk = 1;
     CU(h, cudaMemcpyAsync(&rk, d_rank, sizeof(int), cudaMemcpyDeviceToHost, cs));
     CU(h, cudaStreamSynchronize(cs));

@@ -311,7 +311,7 @@ __device__ __forceinline__ void tg_barrier(unsigned* ctr, unsigned& epoch) {
 
 __global__ void __launch_bounds__(TG_T)
 k_tridiag_grid(double* __restrict__ C, int N, double* __restrict__ pg, double* __restrict__ dg,
-               double* __restrict__ eg, unsigned* __restrict__ ctr) {
+               double* __restrict__ eg, unsigned* __restrict__ ctr, double* __restrict__ Vh) {
   extern __shared__ double tsm[];
   double* v = tsm;      // N
   double* w = v + N;    // N
@@ -340,6 +340,8 @@ k_tridiag_grid(double* __restrict__ C, int N, double* __restrict__ pg, double* _
     }
     if (nv2 <= 0.0 || nx2 == 0.0) {  // already reduced (every CTA takes this branch)
       if (blockIdx.x == 0 && tid == 0) eg[k] = x0;
+      if (Vh && blockIdx.x == 0)  // identity reflector (TT-SVD back-transformation)
+        for (int j = tid; j < L; j += TG_T) Vh[(int64_t)k * N + j] = 0.0;
       __syncthreads();
       continue;
     }
@@ -347,6 +349,8 @@ k_tridiag_grid(double* __restrict__ C, int N, double* __restrict__ pg, double* _
     __syncthreads();
     for (int j = tid; j < L; j += TG_T) v[j] = (j == 0 ? v[0] - alpha : v[j]) * inv;
     __syncthreads();
+    if (Vh && blockIdx.x == 0)  // the reflector, kept for the TT-SVD back-transformation (row k)
+      for (int j = tid; j < L; j += TG_T) Vh[(int64_t)k * N + j] = v[j];
     for (int i = gw; i < L; i += W) {
       const double* row = C + (int64_t)(k + 1 + i) * N + (k + 1);
       double a0 = 0.0, a1 = 0.0;
@@ -514,24 +518,29 @@ cudaError_t launch_rank_rule(const float* X, int64_t m, int64_t n, int64_t ldx, 
   double* eg = dg + N;
   double* lam = eg + N;
   unsigned* ctr = reinterpret_cast<unsigned*>(lam + N);
-  e = cudaMemsetAsync(ctr, 0, 64, st);
+  e = launch_tridiag_eig(C, N, vg, dg, eg, lam, ctr, nullptr, num_sms, st);
   if (e) return e;
+  k_rank_from_eig<<<1, 256, 0, st>>>(lam, N, tt_eps, d_rank, d_eig);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tridiag_eig(double* C, int N, double* p, double* d, double* e, double* lam, unsigned* ctr,
+                               double* Vh, int num_sms, cudaStream_t st) {
+  cudaError_t err = cudaMemsetAsync(ctr, 0, 64, st);
+  if (err) return err;
   const size_t sm = sizeof(double) * 2 * (size_t)N;
-  e = cudaFuncSetAttribute(k_tridiag_grid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e) return e;
+  err = cudaFuncSetAttribute(k_tridiag_grid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (err) return err;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tridiag_grid, TG_T, sm);
-  if (e) return e;
+  err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tridiag_grid, TG_T, sm);
+  if (err) return err;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const int grid = num_sms * std::min(per_sm, 2);
   int Ni = N;
-  void* args[] = {&C, &Ni, &vg, &dg, &eg, &ctr};
-  e = cudaLaunchCooperativeKernel((const void*)k_tridiag_grid, dim3(grid), dim3(TG_T), args, sm, st);
-  if (e) return e;
-  k_bisect_grid<<<(unsigned)std::min<int64_t>((N + 7) / 8, 4 * num_sms), 256, 0, st>>>(dg, eg, N, lam);
-  e = cudaGetLastError();
-  if (e) return e;
-  k_rank_from_eig<<<1, 256, 0, st>>>(lam, N, tt_eps, d_rank, d_eig);
+  void* args[] = {&C, &Ni, &p, &d, &e, &ctr, &Vh};
+  err = cudaLaunchCooperativeKernel((const void*)k_tridiag_grid, dim3(grid), dim3(TG_T), args, sm, st);
+  if (err) return err;
+  k_bisect_grid<<<(unsigned)std::min<int64_t>((N + 7) / 8, 4 * num_sms), 256, 0, st>>>(d, e, N, lam);
   return cudaGetLastError();
 }
 

@@ -60,119 +60,16 @@ __device__ __forceinline__ double start_value(int i, int k) {
   return (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;  // [-1, 1)
 }
 
-// C: N x N symmetric (destroyed).  Vh: N x N (reflectors).  vg, pg: N.  work: 6 N RMAX.
-// Y, Z: N RMAX each (vector-major).  Outputs: eig_asc[N] (all eigenvalues, bisection),
-// lam[r] (Ritz values, descending), rank_out[0] = r, U[N x r] row-major (eigenvectors).
-__global__ void __launch_bounds__(ST)
-k_svd_eig(double* __restrict__ C, int N, double* __restrict__ Vh, double* __restrict__ vg, double* __restrict__ pg,
-          double* __restrict__ work, double* __restrict__ Y, double* __restrict__ Z, double tt_eps, int rcap,
-          double* __restrict__ eig_asc, double* __restrict__ lam_out, int* __restrict__ rank_out,
-          double* __restrict__ U) {
-  extern __shared__ double sm[];
-  double* d = sm;                      // N
-  double* e = d + N;                   // N
-  double* e2 = e + N;                  // N
-  double* lam = e2 + N;                // N
-  vg = lam + N;                        // N: the Householder vector, in shared memory
-  pg = vg + N;                         // N (the global vg / pg arguments are not used)
-  double* red = pg + N;                // 40
-  double* B = red + 40;                // RMAX x (RMAX + 1)
-  double* Q = B + RMAX * (RMAX + 1);   // RMAX x (RMAX + 1)
-  double* dots = Q + RMAX * (RMAX + 1);  // RMAX
-  double* pc = dots + RMAX;            // RMAX / 2
-  double* ps = pc + RMAX / 2;          // RMAX / 2
-  int* ipq = reinterpret_cast<int*>(ps + RMAX / 2);  // RMAX (pairs) + RMAX (order) + 4
-  int* order = ipq + RMAX;
-  int* misc = order + RMAX;
+// Steps 3-9 of the TT-SVD eigensolver on the tridiagonal T = (d, e) with its ascending eigenvalues
+// lam[N] (all in shared memory): the tail rule and cap -> r; inverse iteration for the top r
+// eigenvalues; CGS2; Rayleigh-Ritz (parallel Jacobi on Y^T T Y); Ritz order; Z = Y Q sorted
+// (vector-major r x N, global).  Returns r (every thread).  Shared by k_svd_eig (N <= 512, one CTA
+// for everything) and k_svd_vec (N > 512, after the grid-wide reduction).
+__device__ int svd_vectors(const double* d, const double* e, const double* e2, const double* lam, int N, double tnorm,
+                           double tt_eps, int rcap, double* __restrict__ work, double* __restrict__ Y,
+                           double* __restrict__ Z, double* B, double* Q, double* dots, double* pc, double* ps, int* ipq,
+                           int* order, int* misc, double* red) {
   const int tid = threadIdx.x, T = blockDim.x, wid = tid >> 5, ln = tid & 31, NW = T >> 5;
-  // ---- 1. Householder tridiagonalisation, H_k = I - 2 v v^T on indices k+1..N-1
-  for (int k = 0; k + 2 < N; ++k) {
-    const int L = N - k - 1;
-    double* A = C + (int64_t)(k + 1) * N + (k + 1);
-    double xs = 0.0;
-    for (int i = tid; i < L; i += T) {
-      const double xi = C[(int64_t)(k + 1 + i) * N + k];
-      vg[i] = xi;
-      xs += xi * xi;
-    }
-    const double nx2 = blk_sum(xs, red);
-    const double x0 = vg[0];
-    const double nx = sqrt(nx2);
-    const double alpha = (x0 > 0.0) ? -nx : nx;
-    const double nv2 = nx2 - 2.0 * alpha * x0 + alpha * alpha;
-    if (tid == 0) {
-      d[k] = C[(int64_t)k * N + k];
-      e[k] = (nx2 > 0.0) ? alpha : 0.0;
-    }
-    if (nv2 <= 0.0 || nx2 == 0.0) {  // already reduced: identity reflector
-      __syncthreads();
-      if (tid == 0) e[k] = vg[0];
-      for (int i = tid; i < L; i += T) Vh[(int64_t)k * N + i] = 0.0;
-      __syncthreads();
-      continue;
-    }
-    const double inv = 1.0 / sqrt(nv2);
-    __syncthreads();
-    for (int i = tid; i < L; i += T) {
-      const double v = (i == 0 ? vg[0] - alpha : vg[i]) * inv;
-      vg[i] = v;
-      Vh[(int64_t)k * N + i] = v;
-    }
-    __syncthreads();
-    for (int i = wid; i < L; i += NW) {
-      double s = 0.0;
-      for (int j = ln; j < L; j += 32) s += A[(int64_t)i * N + j] * vg[j];
-      s = warp_sum(s);
-      if (ln == 0) pg[i] = s;
-    }
-    __syncthreads();
-    double kp = 0.0;
-    for (int i = tid; i < L; i += T) kp += vg[i] * pg[i];
-    const double K = blk_sum(kp, red);
-    for (int i = tid; i < L; i += T) pg[i] = pg[i] - K * vg[i];
-    __syncthreads();
-    for (int q = tid; q < L * L; q += T) {
-      const int i = q / L, j = q - i * L;
-      A[(int64_t)i * N + j] -= 2.0 * (vg[i] * pg[j] + pg[i] * vg[j]);
-    }
-    __syncthreads();
-  }
-  if (tid == 0) {
-    if (N >= 2) {
-      d[N - 2] = C[(int64_t)(N - 2) * N + (N - 2)];
-      e[N - 2] = C[(int64_t)(N - 1) * N + (N - 2)];
-    }
-    d[N - 1] = C[(int64_t)(N - 1) * N + (N - 1)];
-    e[N - 1] = 0.0;
-  }
-  __syncthreads();
-  for (int i = tid; i < N; i += T) e2[i] = (i < N - 1) ? e[i] * e[i] : 0.0;
-  // ---- 2. all eigenvalues by Sturm bisection (ascending)
-  if (tid == 0) {
-    double gl = 1e300, gu = -1e300;
-    for (int i = 0; i < N; ++i) {
-      const double rad = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < N ? fabs(e[i]) : 0.0);
-      gl = fmin(gl, d[i] - rad);
-      gu = fmax(gu, d[i] + rad);
-    }
-    red[0] = gl;
-    red[1] = gu;
-  }
-  __syncthreads();
-  const double gl = red[0], gu = red[1];
-  const double span = fmax(gu - gl, 1e-300);
-  const double tnorm = fmax(fabs(gl), fabs(gu));
-  for (int i = tid; i < N; i += T) {
-    double lo = gl - 1e-12 * span, hi = gu + 1e-12 * span;
-    for (int it = 0; it < 200 && hi - lo > 1e-15 * fmax(fabs(lo), fabs(hi)) + 1e-300; ++it) {
-      const double mid = 0.5 * (lo + hi);
-      if (sturm(d, e2, N, mid) <= i) lo = mid;
-      else hi = mid;
-    }
-    lam[i] = fmax(0.5 * (lo + hi), 0.0);
-  }
-  __syncthreads();
-  for (int i = tid; i < N; i += T) eig_asc[i] = lam[i];
   // ---- 3. the tail rule (R21) and the cap
   if (tid == 0) {
     double tot = 0.0;
@@ -398,6 +295,124 @@ k_svd_eig(double* __restrict__ C, int N, double* __restrict__ Vh, double* __rest
     Z[(int64_t)k * N + i] = v;
   }
   __syncthreads();
+  return r;
+}
+
+// C: N x N symmetric (destroyed).  Vh: N x N (reflectors).  vg, pg: N.  work: 6 N RMAX.
+// Y, Z: N RMAX each (vector-major).  Outputs: eig_asc[N] (all eigenvalues, bisection),
+// lam[r] (Ritz values, descending), rank_out[0] = r, U[N x r] row-major (eigenvectors).
+__global__ void __launch_bounds__(ST)
+k_svd_eig(double* __restrict__ C, int N, double* __restrict__ Vh, double* __restrict__ vg, double* __restrict__ pg,
+          double* __restrict__ work, double* __restrict__ Y, double* __restrict__ Z, double tt_eps, int rcap,
+          double* __restrict__ eig_asc, double* __restrict__ lam_out, int* __restrict__ rank_out,
+          double* __restrict__ U) {
+  extern __shared__ double sm[];
+  double* d = sm;                      // N
+  double* e = d + N;                   // N
+  double* e2 = e + N;                  // N
+  double* lam = e2 + N;                // N
+  vg = lam + N;                        // N: the Householder vector, in shared memory
+  pg = vg + N;                         // N (the global vg / pg arguments are not used)
+  double* red = pg + N;                // 40
+  double* B = red + 40;                // RMAX x (RMAX + 1)
+  double* Q = B + RMAX * (RMAX + 1);   // RMAX x (RMAX + 1)
+  double* dots = Q + RMAX * (RMAX + 1);  // RMAX
+  double* pc = dots + RMAX;            // RMAX / 2
+  double* ps = pc + RMAX / 2;          // RMAX / 2
+  int* ipq = reinterpret_cast<int*>(ps + RMAX / 2);  // RMAX (pairs) + RMAX (order) + 4
+  int* order = ipq + RMAX;
+  int* misc = order + RMAX;
+  const int tid = threadIdx.x, T = blockDim.x, wid = tid >> 5, ln = tid & 31, NW = T >> 5;
+  // ---- 1. Householder tridiagonalisation, H_k = I - 2 v v^T on indices k+1..N-1
+  for (int k = 0; k + 2 < N; ++k) {
+    const int L = N - k - 1;
+    double* A = C + (int64_t)(k + 1) * N + (k + 1);
+    double xs = 0.0;
+    for (int i = tid; i < L; i += T) {
+      const double xi = C[(int64_t)(k + 1 + i) * N + k];
+      vg[i] = xi;
+      xs += xi * xi;
+    }
+    const double nx2 = blk_sum(xs, red);
+    const double x0 = vg[0];
+    const double nx = sqrt(nx2);
+    const double alpha = (x0 > 0.0) ? -nx : nx;
+    const double nv2 = nx2 - 2.0 * alpha * x0 + alpha * alpha;
+    if (tid == 0) {
+      d[k] = C[(int64_t)k * N + k];
+      e[k] = (nx2 > 0.0) ? alpha : 0.0;
+    }
+    if (nv2 <= 0.0 || nx2 == 0.0) {  // already reduced: identity reflector
+      __syncthreads();
+      if (tid == 0) e[k] = vg[0];
+      for (int i = tid; i < L; i += T) Vh[(int64_t)k * N + i] = 0.0;
+      __syncthreads();
+      continue;
+    }
+    const double inv = 1.0 / sqrt(nv2);
+    __syncthreads();
+    for (int i = tid; i < L; i += T) {
+      const double v = (i == 0 ? vg[0] - alpha : vg[i]) * inv;
+      vg[i] = v;
+      Vh[(int64_t)k * N + i] = v;
+    }
+    __syncthreads();
+    for (int i = wid; i < L; i += NW) {
+      double s = 0.0;
+      for (int j = ln; j < L; j += 32) s += A[(int64_t)i * N + j] * vg[j];
+      s = warp_sum(s);
+      if (ln == 0) pg[i] = s;
+    }
+    __syncthreads();
+    double kp = 0.0;
+    for (int i = tid; i < L; i += T) kp += vg[i] * pg[i];
+    const double K = blk_sum(kp, red);
+    for (int i = tid; i < L; i += T) pg[i] = pg[i] - K * vg[i];
+    __syncthreads();
+    for (int q = tid; q < L * L; q += T) {
+      const int i = q / L, j = q - i * L;
+      A[(int64_t)i * N + j] -= 2.0 * (vg[i] * pg[j] + pg[i] * vg[j]);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (N >= 2) {
+      d[N - 2] = C[(int64_t)(N - 2) * N + (N - 2)];
+      e[N - 2] = C[(int64_t)(N - 1) * N + (N - 2)];
+    }
+    d[N - 1] = C[(int64_t)(N - 1) * N + (N - 1)];
+    e[N - 1] = 0.0;
+  }
+  __syncthreads();
+  for (int i = tid; i < N; i += T) e2[i] = (i < N - 1) ? e[i] * e[i] : 0.0;
+  // ---- 2. all eigenvalues by Sturm bisection (ascending)
+  if (tid == 0) {
+    double gl = 1e300, gu = -1e300;
+    for (int i = 0; i < N; ++i) {
+      const double rad = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < N ? fabs(e[i]) : 0.0);
+      gl = fmin(gl, d[i] - rad);
+      gu = fmax(gu, d[i] + rad);
+    }
+    red[0] = gl;
+    red[1] = gu;
+  }
+  __syncthreads();
+  const double gl = red[0], gu = red[1];
+  const double span = fmax(gu - gl, 1e-300);
+  const double tnorm = fmax(fabs(gl), fabs(gu));
+  for (int i = tid; i < N; i += T) {
+    double lo = gl - 1e-12 * span, hi = gu + 1e-12 * span;
+    for (int it = 0; it < 200 && hi - lo > 1e-15 * fmax(fabs(lo), fabs(hi)) + 1e-300; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      if (sturm(d, e2, N, mid) <= i) lo = mid;
+      else hi = mid;
+    }
+    lam[i] = fmax(0.5 * (lo + hi), 0.0);
+  }
+  __syncthreads();
+  for (int i = tid; i < N; i += T) eig_asc[i] = lam[i];
+  const int r = svd_vectors(d, e, e2, lam, N, tnorm, tt_eps, rcap, work, Y, Z, B, Q, dots, pc, ps, ipq, order, misc,
+                          red);
   for (int k = wid; k < r; k += NW) {
     double* z = Z + (int64_t)k * N;
     for (int kk = N - 3; kk >= 0; --kk) {
@@ -417,6 +432,75 @@ k_svd_eig(double* __restrict__ C, int N, double* __restrict__ Vh, double* __rest
   }
   if (tid < r) lam_out[tid] = fmax(B[order[tid] * (RMAX + 1) + order[tid]], 0.0);
   if (tid == 0) rank_out[0] = r;
+}
+
+// N > 512 (after launch_tridiag_eig): steps 3-9 in one CTA from the tridiagonal (d, e) and the
+// ascending eigenvalues lam in global memory (copied to shared memory: 4 N + 2 RMAX (RMAX + 1)
+// doubles <= 200 KB at N = 4096); eig_asc <- lam, lam_out (Ritz values, descending), rank_out.
+__global__ void __launch_bounds__(ST)
+k_svd_vec(const double* __restrict__ dg, const double* __restrict__ eg, const double* __restrict__ lamg, int N,
+          double* __restrict__ work, double* __restrict__ Y, double* __restrict__ Z, double tt_eps, int rcap,
+          double* __restrict__ eig_asc, double* __restrict__ lam_out, int* __restrict__ rank_out) {
+  extern __shared__ double sm[];
+  double* d = sm;                      // N
+  double* e = d + N;                   // N
+  double* e2 = e + N;                  // N
+  double* lam = e2 + N;                // N
+  double* red = lam + N;               // 40
+  double* B = red + 40;                // RMAX x (RMAX + 1)
+  double* Q = B + RMAX * (RMAX + 1);   // RMAX x (RMAX + 1)
+  double* dots = Q + RMAX * (RMAX + 1);  // RMAX
+  double* pc = dots + RMAX;            // RMAX / 2
+  double* ps = pc + RMAX / 2;          // RMAX / 2
+  int* ipq = reinterpret_cast<int*>(ps + RMAX / 2);
+  int* order = ipq + RMAX;
+  int* misc = order + RMAX;
+  const int tid = threadIdx.x, T = blockDim.x;
+  for (int i = tid; i < N; i += T) {
+    d[i] = dg[i];
+    e[i] = (i < N - 1) ? eg[i] : 0.0;
+    lam[i] = lamg[i];
+    eig_asc[i] = lamg[i];
+  }
+  __syncthreads();
+  for (int i = tid; i < N; i += T) e2[i] = (i < N - 1) ? e[i] * e[i] : 0.0;
+  if (tid == 0) {
+    double gl = 1e300, gu = -1e300;
+    for (int i = 0; i < N; ++i) {
+      const double rad = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < N ? fabs(e[i]) : 0.0);
+      gl = fmin(gl, d[i] - rad);
+      gu = fmax(gu, d[i] + rad);
+    }
+    red[0] = fmax(fabs(gl), fabs(gu));
+  }
+  __syncthreads();
+  const double tnorm = red[0];
+  __syncthreads();
+  const int r = svd_vectors(d, e, e2, lam, N, tnorm, tt_eps, rcap, work, Y, Z, B, Q, dots, pc, ps, ipq, order, misc,
+                            red);
+  if (tid < r) lam_out[tid] = fmax(B[order[tid] * (RMAX + 1) + order[tid]], 0.0);
+  if (tid == 0) rank_out[0] = r;
+}
+
+// u = H_0 ... H_{N-3} z for every vector (one warp per vector; the 8 warps of a CTA read the same
+// reflector rows, so L1 serves 7 of 8), U[N x r] row-major.  r from the device (rank_out).
+__global__ void __launch_bounds__(256) k_backtransform(const double* __restrict__ Vh, int N,
+                                                       const int* __restrict__ rank_in, double* __restrict__ Z,
+                                                       double* __restrict__ U) {
+  const int r = rank_in[0];
+  const int k = blockIdx.x * 8 + (threadIdx.x >> 5), ln = threadIdx.x & 31;
+  if (k >= r) return;
+  double* z = Z + (int64_t)k * N;
+  for (int kk = N - 3; kk >= 0; --kk) {
+    const int L = N - kk - 1;
+    const double* v = Vh + (int64_t)kk * N;
+    double s = 0.0;
+    for (int i = ln; i < L; i += 32) s += v[i] * z[kk + 1 + i];
+    s = warp_sum(s);
+    for (int i = ln; i < L; i += 32) z[kk + 1 + i] -= 2.0 * s * v[i];
+    __syncwarp();
+  }
+  for (int i = ln; i < N; i += 32) U[(int64_t)i * r + k] = z[i];
 }
 
 // one CTA per column k of an fp64 rows x r matrix M: the sign that makes the largest-|.|
@@ -518,14 +602,31 @@ size_t svd_eig_bytes(int64_t N) {
 }
 
 cudaError_t launch_svd_eig(double* C, int N, char* ws, double tt_eps, int rcap, double* eig_asc, double* lam,
-                           int* d_rank, double* U, cudaStream_t st) {
-  if (N > 512 || rcap > RMAX) return cudaErrorInvalidValue;
+                           int* d_rank, double* U, int num_sms, cudaStream_t st) {
+  if (N > kRankMaxN || rcap > RMAX) return cudaErrorInvalidValue;
   double* Vh = reinterpret_cast<double*>(ws);
   double* vg = Vh + (size_t)N * N;
   double* pg = vg + N;
   double* work = pg + N;
   double* Y = work + 6 * (size_t)N * RMAX;
   double* Z = Y + (size_t)N * RMAX;
+  if (N > 512) {
+    // the grid-wide reduction (reflectors into Vh) and multisection, then steps 3-9 in one CTA
+    // and the back-transformation with a warp per vector.  d = vg, e and lam after Z.
+    double* eg = Z + (size_t)N * RMAX;
+    double* lamg = eg + N;
+    unsigned* ctr = reinterpret_cast<unsigned*>(lamg + N);
+    cudaError_t e = launch_tridiag_eig(C, N, pg, vg, eg, lamg, ctr, Vh, num_sms, st);
+    if (e) return e;
+    const size_t smv = sizeof(double) * (4 * (size_t)N + 40 + 2 * RMAX * (RMAX + 1) + RMAX + RMAX) +
+                       sizeof(int) * (2 * RMAX + 8);
+    e = cudaFuncSetAttribute(k_svd_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smv);
+    if (e) return e;
+    k_svd_vec<<<1, ST, smv, st>>>(vg, eg, lamg, N, work, Y, Z, tt_eps, rcap, eig_asc, lam, d_rank);
+    if ((e = cudaGetLastError())) return e;
+    k_backtransform<<<RMAX / 8, 256, 0, st>>>(Vh, N, d_rank, Z, U);
+    return cudaGetLastError();
+  }
   const size_t sm = sizeof(double) * (6 * (size_t)N + 40 + 2 * RMAX * (RMAX + 1) + RMAX + RMAX) + sizeof(int) * (2 * RMAX + 8);
   cudaError_t e = cudaFuncSetAttribute(k_svd_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e) return e;

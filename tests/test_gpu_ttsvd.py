@@ -96,11 +96,12 @@ def test_ttsvd_larger_and_error_decomposition(h, ora):
 
 
 def test_ttsvd_unsupported(h):
+    """min(m, n) above the eigensolver's 4096 limit is rejected."""
     import paper_2008_01340_b200 as P
-    A = torch.rand(600 * 700, device="cuda")
+    A = torch.zeros(4100 * 4100, device="cuda")
     cores = torch.empty(10 ** 6, device="cuda")
     with pytest.raises(P.NttError):
-        h.ntt_tt_svd(A, [600, 700], 0.1, cores, 10 ** 6)
+        h.ntt_tt_svd(A, [4100, 4100], 0.1, cores, 10 ** 6)
 
 
 def test_ttsvd_host_buffers(h, ora):
@@ -124,3 +125,17 @@ def test_ttsvd_large_ranks(h, ora):
     ranks, cores, err = run(h, A, 1e-3)
     compare(ora, A, 1e-3, ranks, cores, err)
     assert ranks == [40, 30]
+
+
+@pytest.mark.parametrize("dims,tr,noise,eps", [
+    ((600, 10, 100), (5, 4), 0.001, 0.01),     # step 1: 600 x 1000 (grid-wide eigensolver)
+    ((40, 30, 1200), (20, 12), 0.001, 0.01),   # step 2: 600 x 1200 (m = r1 n2 = 600 > 512)
+    ((1100, 2, 1000), (6, 3), 0.0005, 0.01)])  # step 1: 1100 x 2000
+def test_ttsvd_parity_grid_eigensolver(h, ora, dims, tr, noise, eps):
+    """min(m, n) > 512 at a step: the grid-wide Householder reduction (reflectors kept), the warp
+    multisection, k_svd_vec (inverse iteration, CGS2, Rayleigh-Ritz) and k_backtransform --
+    ranks identical to LAPACK's, cores, reconstruction and Eq. 3 as the one-CTA path."""
+    A = rand_tt(dims, tr, sum(dims), noise)
+    ranks, cores, err = run(h, A, eps)
+    compare(ora, A, eps, ranks, cores, err)
+    assert list(ranks) == list(tr)
