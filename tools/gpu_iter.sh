@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_ttsvd.py tests/test_gpu_rank.py -x -q > gpurun_out/gputests_x.log 2>&1; echo "pytest rc $?"; tail -25 gpurun_out/gputests_x.log
+timeout 1200 python tools/eps256.py > gpurun_out/eps256.md 2> gpurun_out/eps256.err; echo "rc $?"; cat gpurun_out/eps256.md; tail -3 gpurun_out/eps256.err
