@@ -58,7 +58,10 @@ def branches(tr, obj0):
     (32, 4096, 8, 15, 0), (6, 2048, 5, 15, 0), (24, 1024, 4, 12, 3),
     # 40 < m <= 256: one-pass k_fused_c; at n = 2^15 its 2-per-SM partials are pre-summed across
     # the GPU before the one-CTA post kernel
-    (256, 32768, 8, 10, 0), (64, 8192, 8, 10, 4)])
+    (256, 32768, 8, 10, 0), (64, 8192, 8, 10, 4),
+    # 9 <= r <= 16 at 40 < m <= 256: k_fused_c's rank-16 class in BCD mode (one CTA of 8 consumer
+    # warps for m > 128)
+    (200, 4096, 10, 10, 0), (256, 2048, 16, 8, 0), (72, 1000, 12, 10, 5)])
 def test_bcd_parity(h, ora, m, n, r, iters, lr):
     X, W0, H0 = case(m, n, r, m * 7 + n + r, lr)
     Wg, Hg, trg = run_gpu(h, X, W0, H0, iters)
@@ -84,7 +87,8 @@ FORCED = (2, 3, 6)   # iterations forced onto the correction branch (two in a ro
     (256, 32768, 8, 0),   # one pass k_fused_c, GPU-wide partial pre-sum
     (64, 8192, 8, 4),     # one pass k_fused_c
     (300, 512, 16, 0),    # fp16x2 tensor-core passes, large-W kernels
-    (100, 2000, 16, 6),   # FFMA passes, one-CTA W side / post kernels
+    (100, 2000, 16, 6),   # one pass k_fused_c, rank-16 class; one-CTA W side / post kernels
+    (200, 4096, 12, 0),   # one pass k_fused_c, rank-16 class with 8 consumer warps
     (3000, 64, 5, 3),     # FFMA passes, large-W kernels
     (7, 7, 7, 0)])        # generic small case
 def test_bcd_forced_correction_parity(h, ora, m, n, r, lr):

@@ -1,1 +1,1 @@
-timeout 1200 python tools/eps256.py > gpurun_out/eps256.md 2> gpurun_out/eps256.err; echo "rc $?"; cat gpurun_out/eps256.md; tail -3 gpurun_out/eps256.err
+timeout 900 python -m pytest tests/test_gpu_bcd.py -x -q > gpurun_out/gputests_z.log 2>&1; echo "pytest rc $?"; tail -15 gpurun_out/gputests_z.log
