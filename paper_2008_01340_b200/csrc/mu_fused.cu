@@ -1103,8 +1103,16 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   constexpr bool P32 = false;  // RK = 8 too: the fp32 level cost 16 registers and 72 B of spills in the tile loop
   float pacc[P32 ? NB : 1][2][NN][4];
   double paccd[NB][2][NN][4];
-  constexpr int QR = RK / NW;  // Q rows per warp
-  double qd[QR];
+  // Q = Hn Hn^T.  RK = 16: on mma.sync by warp 0 (the A fragments of Hn are phase B's B
+  // fragments; 7 % faster at 256 x 2^24, r 10, than 48 shared loads per thread and tile), fp64
+  // accumulation per tile, rows fg (+ 8), ranks 8 nn + 2 ft (+ 1).  RK = 8: FFMA over column
+  // slices (the mma form's registers cost 76 B of spills and 4 % in <256,4,8>)
+  constexpr bool QMMA = RK == 16;
+  constexpr int QR = RK / NW;  // Q rows per warp (FFMA form)
+  double qdd[QMMA ? NN : 1][4];
+  double qd[QMMA ? 1 : QR];
+#pragma unroll
+  for (int qq = 0; qq < (QMMA ? 1 : QR); ++qq) qd[qq] = 0.0;
 #pragma unroll
   for (int bb = 0; bb < NB; ++bb)
 #pragma unroll
@@ -1117,7 +1125,9 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
           paccd[bb][mh][nn][e4] = 0.0;
         }
 #pragma unroll
-  for (int qq = 0; qq < QR; ++qq) qd[qq] = 0.0;
+  for (int nn = 0; nn < (QMMA ? NN : 1); ++nn)
+#pragma unroll
+    for (int e4 = 0; e4 < 4; ++e4) qdd[nn][e4] = 0.0;
   int since_flush = 0;
   // X16 passes: the block scales of a tile (written by the prologue pass next to its blocks, read
   // from L2) are loaded one tile ahead -- on the critical path they cost an L2 round trip per tile
@@ -1346,8 +1356,8 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
             }
         }
       }
-      {  // Q rows QR w + qq (QR = RK / NW), column qc = lane % RK, over this lane's slice of the
-         // tile's columns (32 / RK slices of RK columns); the slices are summed at the end of the pass
+      if constexpr (!QMMA) {  // Q rows QR w + qq, column qc = lane % RK, over this lane's slice of
+                              // the tile's columns (32 / RK slices); slices summed at the end of the pass
         float qa[QR];
 #pragma unroll
         for (int qq = 0; qq < QR; ++qq) qa[qq] = 0.f;
@@ -1361,6 +1371,24 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         }
 #pragma unroll
         for (int qq = 0; qq < QR; ++qq) qd[qq] += (double)qa[qq];
+      } else if (warp == 0) {  // Q += Hn Hn^T: A = Hn (ranks x columns) = the B fragments read as A
+        const float q2 = hsc.y * hsc.y;
+#pragma unroll
+        for (int nq = 0; nq < NN; ++nq) {
+          float d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            const uint32_t ah[4] = {bh[kk][0][0], NN > 1 ? bh[kk][NN - 1][0] : 0u, bh[kk][0][1],
+                                    NN > 1 ? bh[kk][NN - 1][1] : 0u};
+            const uint32_t al[4] = {bl[kk][0][0], NN > 1 ? bl[kk][NN - 1][0] : 0u, bl[kk][0][1],
+                                    NN > 1 ? bl[kk][NN - 1][1] : 0u};
+            mma16816(d, ah, bh[kk][nq][0], bh[kk][nq][1]);
+            mma16816(d, ah, bl[kk][nq][0], bl[kk][nq][1]);
+            mma16816(d, al, bh[kk][nq][0], bh[kk][nq][1]);
+          }
+#pragma unroll
+          for (int e4 = 0; e4 < 4; ++e4) qdd[QMMA ? nq : 0][e4] += (double)(d[e4] * q2);
+        }
       }
       if (P32 && ++since_flush == 8) {  // two-level accumulation: fp32 over <= 8 tiles, then fp64
         since_flush = 0;
@@ -1405,13 +1433,23 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
             const int row = warp * RW + 32 * bb + 16 * mh + fg + 8 * (e4 >> 1), k = 8 * nn + 2 * ft + (e4 & 1);
             if (row < m && k < r) Pb[row * r + k] = paccd[bb][mh][nn][e4] + (P32 ? (double)pacc[P32 ? bb : 0][mh][nn][e4] : 0.0);
           }
-    // Q rows QR w + qq, column lane % RK: sum the 32 / RK column slices
+    if constexpr (QMMA) {  // Q fragment (warp 0): rank rows fg (+ 8), rank columns 8 nn + 2 ft (+ 1)
+      if (warp == 0)
 #pragma unroll
-    for (int qq = 0; qq < QR; ++qq) {
-      qd[qq] += __shfl_xor_sync(0xffffffffu, qd[qq], 16);
-      if (RK == 8) qd[qq] += __shfl_xor_sync(0xffffffffu, qd[qq], 8);
-      const int row = QR * warp + qq, k = lane % RK;
-      if (lane < RK && row < r && k < r) Qb[row * r + k] = qd[qq];
+        for (int nn = 0; nn < NN; ++nn)
+#pragma unroll
+          for (int e4 = 0; e4 < 4; ++e4) {
+            const int row = fg + 8 * (e4 >> 1), k = 8 * nn + 2 * ft + (e4 & 1);
+            if (row < r && k < r) Qb[row * r + k] = qdd[QMMA ? nn : 0][e4];
+          }
+    } else {  // Q rows QR w + qq, column lane % RK: sum the 32 / RK column slices
+#pragma unroll
+      for (int qq = 0; qq < QR; ++qq) {
+        qd[qq] += __shfl_xor_sync(0xffffffffu, qd[qq], 16);
+        if (RK == 8) qd[qq] += __shfl_xor_sync(0xffffffffu, qd[qq], 8);
+        const int row = QR * warp + qq, k = lane % RK;
+        if (lane < RK && row < r && k < r) Qb[row * r + k] = qd[qq];
+      }
     }
   }
   };  // pass_tiles
