@@ -1280,10 +1280,15 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 #pragma unroll
           for (int w = 0; w < NW; ++w) S += Sred[(w * RK + kt) * 32 + ct];
           float e0 = 0.0f, e1 = 0.0f;
+          const float4* g4 = reinterpret_cast<const float4*>(Gs + kt * RK);  // row kt, 128-bit loads
 #pragma unroll
-          for (int l = 0; l < RK; l += 2) {
-            e0 = fmaf(Gs[kt * RK + l], BCD ? hl[l] * bsh[l] : hl[l], e0);
-            e1 = fmaf(Gs[kt * RK + l + 1], BCD ? hl[l + 1] * bsh[l + 1] : hl[l + 1], e1);
+          for (int l4 = 0; l4 < RK / 4; ++l4) {
+            const float4 g = g4[l4];
+            const int l = 4 * l4;
+            e0 = fmaf(g.x, BCD ? hl[l] * bsh[l] : hl[l], e0);
+            e1 = fmaf(g.y, BCD ? hl[l + 1] * bsh[l + 1] : hl[l + 1], e1);
+            e0 = fmaf(g.z, BCD ? hl[l + 2] * bsh[l + 2] : hl[l + 2], e0);
+            e1 = fmaf(g.w, BCD ? hl[l + 3] * bsh[l + 3] : hl[l + 3], e1);
           }
           if constexpr (BCD)  // prox-linear step (Alg. 3 l.14) on H_m = diag(sH) H_m stored
             hn = fmaxf(0.f, fmaf(-((e0 + e1) - S), binvL, hkc * bsh[kt]));
