@@ -870,6 +870,19 @@ ntt_status ntt_nmf_mu(ntt_handle h, const float* X, int64_t m, int64_t n, int64_
   if ((s = check_nonneg(h, dX, m, n, ldx, "X"))) return s;
   char* scratch = reinterpret_cast<char*>(h->ws);
   double* dtrace = objective_trace ? reinterpret_cast<double*>(scratch + p.bytes) : nullptr;
+  if (h->comm && h->nranks > 1 && h->xready && h->xmode == 1) {
+    // every rank in the persistent kernel or none (the in-kernel exchange; see ntt_decompose):
+    // the ranks' local shapes / alignments may differ
+    int flag = (p.persist && !dtrace && fused_supported(m, n, r, ldx, dX, dH)) ? 1 : 0;
+    int* dfl = nullptr;
+    CU(h, cudaMallocAsync(reinterpret_cast<void**>(&dfl), sizeof(int), h->stream));
+    CU(h, cudaMemcpyAsync(dfl, &flag, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+    NC(h, g_nccl.AllReduce(dfl, dfl, 1, ncclInt32, ncclMin, h->comm, h->stream));
+    CU(h, cudaMemcpyAsync(&flag, dfl, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CU(h, cudaFreeAsync(dfl, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    p.persist = flag != 0;
+  }
   if ((s = run_mu(h, p, dX, ldx, iters, eps, dW, dH, scratch, dtrace))) return s;
   if (!wd) CU(h, cudaMemcpyAsync(W, dW, sizeof(float) * (size_t)(m * r), cudaMemcpyDeviceToHost, h->stream));
   if (!hd) CU(h, cudaMemcpyAsync(H, dH, sizeof(float) * (size_t)(r * n), cudaMemcpyDeviceToHost, h->stream));
@@ -1046,6 +1059,22 @@ ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t*
   std::unique_ptr<DecompPlan> guard(Pp);
   DecompPlan& P = *Pp;
   plan_decompose(s, h->num_sms, h->nranks, h->rank, h->comm != nullptr, &P, h->xready && h->xmode == 1);
+  if (h->comm && h->nranks > 1 && h->xready && h->xmode == 1) {
+    // the in-kernel exchange needs every rank in the persistent kernel of a step: ragged last-mode
+    // blocks can make a step persistent-eligible on some ranks only (n % 4), so the ranks agree
+    // per step (min over the ranks' flags); the per-pass NCCL paths issue one identical
+    // all-reduce per pass on any kernel path
+    int flags[64] = {0};
+    for (int l = 1; l < d; ++l) flags[l] = P.mu[l].persist ? 1 : 0;
+    int* dfl = nullptr;
+    CU(h, cudaMallocAsync(reinterpret_cast<void**>(&dfl), sizeof flags, h->stream));
+    CU(h, cudaMemcpyAsync(dfl, flags, sizeof flags, cudaMemcpyHostToDevice, h->stream));
+    NC(h, g_nccl.AllReduce(dfl, dfl, 64, ncclInt32, ncclMin, h->comm, h->stream));
+    CU(h, cudaMemcpyAsync(flags, dfl, sizeof flags, cudaMemcpyDeviceToHost, h->stream));
+    CU(h, cudaFreeAsync(dfl, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    for (int l = 1; l < d; ++l) P.mu[l].persist = flags[l] != 0;
+  }
   char* ws;
   if (workspace) {
     if (workspace_bytes < P.bytes)
