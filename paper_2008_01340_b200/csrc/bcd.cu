@@ -972,8 +972,7 @@ cudaError_t launch_bcd_post(const double* Ppart, int nP, const double* Qpart, in
                             double* trace, cudaStream_t st) {
   const size_t sm = sizeof(double) * (size_t)m * r;
   if (sm > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(r <= 8 ? k_bcd_post<8> : k_bcd_post<16>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = smem_optin((const void*)(r <= 8 ? k_bcd_post<8> : k_bcd_post<16>), sm);
     if (e) return e;
   }
   if (r <= 8) k_bcd_post<8><<<1, WS_T, sm, st>>>(Ppart, nP, Qpart, nQ, m, r, W, Wm, Wp, Pc, Qc, c, G, bs, trace);

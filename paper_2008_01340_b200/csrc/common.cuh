@@ -72,4 +72,26 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   return __ffma2_rn(a, b, c);
 }
 
+
+// Dynamic shared-memory opt-in of a kernel: raised to the device's per-block maximum, never
+// lowered.  Setting it to each call's own size would lower it for later, smaller shapes -- and a
+// kernel node captured earlier into a CUDA graph with a larger size then fails when a profiler
+// (ncu, per-node graph profiling) re-launches that node against the function's current
+// attribute.  The launch's own dynamic size still decides occupancy.
+inline cudaError_t smem_optin(const void* kern, size_t bytes) {
+  static const int mx = [] {
+    int d = 0, v = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, d);
+    return v;
+  }();
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+  if (e != cudaSuccess) return e;
+  const int dyn = mx - (int)fa.sharedSizeBytes;  // the opt-in maximum covers static + dynamic
+  if (bytes > (size_t)(dyn > 0 ? dyn : 0)) return cudaErrorInvalidValue;
+  if (fa.maxDynamicSharedSizeBytes >= dyn) return cudaSuccess;
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+}
+
 }  // namespace ntt

@@ -1514,7 +1514,7 @@ cudaError_t launch_c(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_
   const size_t smem = (size_t)ns * SB + fixed_bytes_c(MP, NW, RK);
   if (ns < 2) return cudaErrorInvalidConfiguration;
   if (pa.iters > 0 && persist_scratch_bytes(m, r, RK, (NW + 1) * 32) > (size_t)ns * SB) return cudaErrorInvalidConfiguration;
-  cudaError_t e = cudaFuncSetAttribute(k_fused_c<MP, NW, RK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_optin((const void*)(k_fused_c<MP, NW, RK>), smem);
   if (e != cudaSuccess) return e;
   return launch_maybe_coop(k_fused_c<MP, NW, RK>, grid, (NW + 1) * 32, smem, st, pa.iters > 0, mx, mh, m, n, r, W,
                            Gpart, nG, eps, H, Ppart, Qpart, mode, ns, evict_first, pa);
@@ -1591,7 +1591,7 @@ cudaError_t launch_t(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_
   if (ns > 24) ns = 24;
   const size_t smem = (size_t)ns * SB + fixed_bytes(UX, NWT, HD);
   if (pa.iters > 0 && persist_scratch_bytes(m, r, 8, (NWT + 1) * 32) > (size_t)ns * SB) return cudaErrorInvalidConfiguration;
-  cudaError_t e = cudaFuncSetAttribute(k_fused<R, UX, NWT, HD, BNT, FOLD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_optin((const void*)(k_fused<R, UX, NWT, HD, BNT, FOLD>), smem);
   if (e != cudaSuccess) return e;
   return launch_maybe_coop(k_fused<R, UX, NWT, HD, BNT, FOLD>, grid, (NWT + 1) * 32, smem, st, pa.iters > 0, mx, mh,
                            mh2 ? *mh2 : mh, m, n, r, W, Gpart, nG, eps, H, Ppart, Qpart, mode, ns, evict_first, pa);
@@ -1992,7 +1992,7 @@ cudaError_t launch_m(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_
   const int ns = stages_m();
   const size_t smem = (size_t)ns * SBM + fixed_bytes_m();
   if (pa.iters > 0 && persist_scratch_bytes(m, r, 8, (NWM + 1) * 32) > (size_t)ns * SBM) return cudaErrorInvalidConfiguration;
-  cudaError_t e = cudaFuncSetAttribute(k_fused_m, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_optin((const void*)(k_fused_m), smem);
   if (e != cudaSuccess) return e;
   return launch_maybe_coop(k_fused_m, grid, (NWM + 1) * 32, smem, st, pa.iters > 0, mx, mh, m, n, r, W, Gpart, nG,
                            eps, H, Ppart, Qpart, mode, ns, evict_first, pa);

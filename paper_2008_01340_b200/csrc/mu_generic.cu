@@ -313,7 +313,7 @@ static cudaError_t hpass_t(const float* X, int64_t ldx, int64_t m, int64_t n, co
   if (Ppart) {
     size_t sm = base + sizeof(float) * R * HP_BN + sizeof(double) * (size_t)(m * r + r * r);
     sm = (sm + 15) & ~(size_t)15;
-    cudaError_t e = cudaFuncSetAttribute(k_hpass<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = smem_optin((const void*)(k_hpass<R, true>), sm);
     if (e != cudaSuccess) return e;
     k_hpass<R, true><<<grid, HP_BN, sm, st>>>(X, ldx, m, n, W, r, Gpart, nG, eps, H, Ppart, Qpart);
   } else {

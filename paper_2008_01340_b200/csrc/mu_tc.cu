@@ -578,7 +578,7 @@ cudaError_t launch_skinny(const CUtensorMap& ma, const CUtensorMap& mb, int64_t 
                           int64_t kchunk, int grid, int r, double* part, int evict_first, cudaStream_t st) {
   const int ns = tc_stages<R>();
   const size_t sm = tc_smem<R>(ns);
-  cudaError_t e = cudaFuncSetAttribute(k_skinny_tc<R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = smem_optin((const void*)(k_skinny_tc<R, MODE>), sm);
   if (e != cudaSuccess) return e;
   k_skinny_tc<R, MODE><<<grid, TC_THREADS, sm, st>>>(ma, mb, Mtot, ktiles, nsplit, kchunk, ns, 32, r, part,
                                                      evict_first);

@@ -383,7 +383,7 @@ cudaError_t launch16(const CUtensorMap& ma, const CUtensorMap& mb, int64_t Mtot,
                      cudaStream_t st, int flush) {
   const int ns = t16_stages<R>();
   const size_t sm = (size_t)ns * T16Cfg<R>::SB + 2048;
-  cudaError_t e = cudaFuncSetAttribute(k_skinny_tc16<R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = smem_optin((const void*)(k_skinny_tc16<R, MODE>), sm);
   if (e != cudaSuccess) return e;
   k_skinny_tc16<R, MODE><<<grid, T16_THREADS, sm, st>>>(ma, mb, Mtot, ktiles, nsplit, kchunk, ns, flush, r, part,
                                                         scales, sidx, ef);

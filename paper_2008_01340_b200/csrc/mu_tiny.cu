@@ -229,7 +229,7 @@ cudaError_t launch_tiny_t(const float* X, int64_t ldx, int m, int n, int r, int 
                           cudaStream_t st) {
   const int nch = tiny_nch(m, r, n);
   const size_t sm = TinyLayout<R>::bytes(m, n, nch);
-  cudaError_t e = cudaFuncSetAttribute(k_tiny<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = smem_optin((const void*)(k_tiny<R>), sm);
   if (e != cudaSuccess) return e;
   k_tiny<R><<<1, TINY_THREADS, sm, st>>>(X, ldx, m, n, r, iters, eps, W, H, nch);
   return cudaGetLastError();

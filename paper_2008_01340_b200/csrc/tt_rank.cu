@@ -508,7 +508,7 @@ cudaError_t launch_rank_rule(const float* X, int64_t m, int64_t n, int64_t ldx, 
   double* pg = vg + N;
   if (N <= kRankOneCta) {
     const size_t sm = sizeof(double) * (6 * (size_t)N + 40);
-    e = cudaFuncSetAttribute(k_eig_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    e = smem_optin((const void*)(k_eig_rank), sm);
     if (e) return e;
     k_eig_rank<<<1, ET, sm, st>>>(C, N, vg, pg, tt_eps, d_eig, d_rank);
     return cudaGetLastError();
@@ -529,7 +529,7 @@ cudaError_t launch_tridiag_eig(double* C, int N, double* p, double* d, double* e
   cudaError_t err = cudaMemsetAsync(ctr, 0, 64, st);
   if (err) return err;
   const size_t sm = sizeof(double) * 2 * (size_t)N;
-  err = cudaFuncSetAttribute(k_tridiag_grid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  err = smem_optin((const void*)(k_tridiag_grid), sm);
   if (err) return err;
   int per_sm = 0;
   err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tridiag_grid, TG_T, sm);

@@ -620,7 +620,7 @@ cudaError_t launch_svd_eig(double* C, int N, char* ws, double tt_eps, int rcap, 
     if (e) return e;
     const size_t smv = sizeof(double) * (4 * (size_t)N + 40 + 2 * RMAX * (RMAX + 1) + RMAX + RMAX) +
                        sizeof(int) * (2 * RMAX + 8);
-    e = cudaFuncSetAttribute(k_svd_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smv);
+    e = smem_optin((const void*)(k_svd_vec), smv);
     if (e) return e;
     k_svd_vec<<<1, ST, smv, st>>>(vg, eg, lamg, N, work, Y, Z, tt_eps, rcap, eig_asc, lam, d_rank);
     if ((e = cudaGetLastError())) return e;
@@ -628,7 +628,7 @@ cudaError_t launch_svd_eig(double* C, int N, char* ws, double tt_eps, int rcap, 
     return cudaGetLastError();
   }
   const size_t sm = sizeof(double) * (6 * (size_t)N + 40 + 2 * RMAX * (RMAX + 1) + RMAX + RMAX) + sizeof(int) * (2 * RMAX + 8);
-  cudaError_t e = cudaFuncSetAttribute(k_svd_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = smem_optin((const void*)(k_svd_eig), sm);
   if (e) return e;
   k_svd_eig<<<1, ST, sm, st>>>(C, N, Vh, vg, pg, work, Y, Z, tt_eps, rcap, eig_asc, lam, d_rank, U);
   return cudaGetLastError();

@@ -41,6 +41,15 @@ for (m, n, r, it) in shapes:
     nx = np.median(nxt - f[:, 3]) / 1e3
     cy = np.array([tr[8192 + i] for i in range(4 * (it + 1))], dtype=np.float64).reshape(it + 1, 4)[1:-1]
     print("   clock64 cycles: W update", np.median(cy[:, 1] - cy[:, 0]), "Gram", np.median(cy[:, 2] - cy[:, 1]))
+    g = min((n + 127) // 128, 148 if m <= 40 else (148 if (m > 128 and r > 8) else 296))
+    st1 = np.array([tr[17408 + i] for i in range(min(g, 1024))], dtype=np.float64)
+    en1 = np.array([tr[16384 + i] for i in range(min(g, 1024))], dtype=np.float64)
+    ok = (st1 > 0) & (en1 > 0)
+    if ok.sum() > 1:
+        d = (en1[ok] - st1[ok]) / 1e3
+        e = (en1[ok] - en1[ok].min()) / 1e3
+        print(f"   pass-1 per-CTA ({ok.sum()} CTAs) duration us: min {d.min():.1f} p50 {np.median(d):.1f} "
+              f"max {d.max():.1f}; end spread p50 {np.median(e):.1f} p90 {np.percentile(e, 90):.1f} max {e.max():.1f}")
     print(f"{m}x{n} r{r}: {tot:.2f} us/iter | pass {passt:.2f} barrier1 {b1:.2f} slice+barrier2 {b2:.2f} "
           f"Wupdate->next {wu:.2f} us [Q load {q:.2f}, W update {wupd:.2f}, Gram {gram:.2f}, Wout {tail:.2f}, "
           f"-> next pass {nx:.2f}]", flush=True)
