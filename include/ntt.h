@@ -274,6 +274,14 @@ ntt_status ntt_profile_get_step(ntt_handle h, int cls, int step, int64_t* launch
  * and end at [16384 + c].  NULL otherwise.  Synchronises the handle's stream. */
 const unsigned long long* ntt_debug_persist_trace(ntt_handle h);
 
+/* Which kernel path ntt_nmf_mu takes for an m x n X at rank r on this handle
+ * (16-byte aligned X and H, ldx = n; DESIGN.md s.6 "plan_mu"): 1 tiny (one CTA,
+ * mu_tiny.cu), 2 cluster (one thread-block cluster, X in distributed shared
+ * memory, mu_cluster.cu), 3 persistent one-pass (mu_fused.cu), 4 per-pass
+ * one-pass, 5 tensor-core two-pass (mu_tc16.cu), 6 generic two-pass.  Lets
+ * tests prove which path a parity case ran.  -1 for a null handle or r < 1. */
+int32_t ntt_debug_mu_path(ntt_handle h, int64_t m, int64_t n, int32_t r);
+
 /* Number of NCCL calls this handle has enqueued (collectives and group
  * brackets; a captured graph's calls are counted once, at capture).  Proves in
  * tests that a distributed branch ran.  -1 for a null handle.               */

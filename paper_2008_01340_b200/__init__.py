@@ -161,6 +161,10 @@ class Handle:
         self._check(lib().ntt_nmf_mu(self._h, _ptr(X), m, n, ldx, r, iters, eps, _ptr(W), _ptr(H), tr))
         return list(tr)[:iters] if trace else None
 
+    def mu_path(self, m: int, n: int, r: int) -> int:
+        """ntt_debug_mu_path: 1 tiny, 2 cluster, 3 persistent 1-pass, 4 per-pass 1-pass, 5 tc, 6 generic."""
+        return int(lib().ntt_debug_mu_path(self._h, m, n, r))
+
     def ntt_stream_ceiling(self, buf, nbytes: int, reps: int = 10) -> float:
         """Read-only HBM stream rate over a device buffer in GB/s (BASELINE.md s.3 ceiling)."""
         g = ctypes.c_double(0.0)

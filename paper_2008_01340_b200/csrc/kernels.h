@@ -42,6 +42,14 @@ bool tiny_supported(int64_t m, int64_t n, int r);
 cudaError_t launch_tiny(const float* X, int64_t ldx, int64_t m, int64_t n, int r, int iters, float eps, float* W,
                         float* H, cudaStream_t st);
 
+// cluster mode (mu_cluster.cu): the whole MU loop of a mid-size X (m <= 256, r <= 16, at most
+// ~16 K entries of X per CTA) in one thread-block cluster of <= 16 CTAs, X resident in the
+// cluster's distributed shared memory; cluster_size_for = 0 when the shape does not fit
+int cluster_size_for(int64_t m, int64_t n, int r);
+bool cluster_supported(int64_t m, int64_t n, int r);
+cudaError_t launch_cluster_mu(const float* X, int64_t ldx, int64_t m, int64_t n, int r, int iters, float eps, float* W,
+                              float* H, cudaStream_t st, unsigned long long* trace = nullptr);
+
 
 
 // SVD rank rule of Alg. 2 l.5-6 (tt_rank.cu): Gram of X (N = min(m, n) <= kRankMaxN) ->

@@ -312,6 +312,7 @@ struct MuPlan {
   TcPlan tp;
   bool persist;   // fused path as one persistent cooperative launch per call
   bool tiny;      // whole MU loop in one CTA from shared memory (mu_tiny.cu)
+  bool clu;       // whole MU loop in one thread-block cluster, X in distributed smem (mu_cluster.cu)
   size_t off_P, off_Q, off_G, off_S, off_tc, off_pp, off_red, off_ctr, off_x16, bytes;
 };
 
@@ -353,6 +354,7 @@ MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, bool dist, bool xpersis
   }
   p.persist = (!dist || xpersist) && p.fused && !getenv("NTT_NO_PERSIST");
   p.tiny = !dist && tiny_supported(m, n, r) && !getenv("NTT_NO_TINY");
+  p.clu = !dist && !p.tiny && !getenv("NTT_NO_CLUSTER") && cluster_supported(m, n, r);
   p.off_pp = o;
   if (p.persist) o = align_up(o + sizeof(double) * (size_t)p.fgrid * (size_t)(m * r + r * r));
   p.off_red = o;
@@ -390,6 +392,12 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
     // tiny mode: every iteration in one CTA from shared memory (mu_tiny.cu)
     PLAUNCH(h, 0, (double)iters * 4.0 * (double)(m + 2 * r) * (double)n,
             launch_tiny(X, ldx, m, n, r, iters, eps, W, H, st));
+    return NTT_OK;
+  }
+  if (p.clu && !dist && !dev_trace) {
+    // cluster mode: every iteration in one thread-block cluster, X in distributed shared memory
+    PLAUNCH(h, 0, (double)iters * 4.0 * (double)(m + 2 * r) * (double)n,
+            launch_cluster_mu(X, ldx, m, n, r, iters, eps, W, H, st, h->ptrace));
     return NTT_OK;
   }
   if (p.fused && p.persist && (!dist || (h->xready && h->xmode == 1)) && !dev_trace &&
@@ -2165,6 +2173,18 @@ extern "C" ntt_status ntt_debug_bcd_force_correct(ntt_handle h, uint64_t mask) {
   if (!h) return NTT_ERR_INVALID_ARG;
   h->bcd_force = mask & ((1ull << 52) - 1);
   return NTT_OK;
+}
+
+extern "C" int32_t ntt_debug_mu_path(ntt_handle h, int64_t m, int64_t n, int32_t r) {
+  if (!h || r < 1 || m < 1 || n < 1) return -1;
+  const bool dist = h->comm != nullptr;
+  const MuPlan p = plan_mu(m, n, r, h->num_sms, dist, h->xready && h->xmode == 1);
+  if (p.tiny && !dist) return 1;
+  if (p.clu && !dist) return 2;
+  if (p.fused && p.persist && (!dist || (h->xready && h->xmode == 1))) return 3;
+  if (p.fused) return 4;
+  if (p.tc) return 5;
+  return 6;
 }
 
 extern "C" const unsigned long long* ntt_debug_persist_trace(ntt_handle h) {

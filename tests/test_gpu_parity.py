@@ -132,7 +132,11 @@ def _mu_inputs(m, n, r, seed):
 
 
 @pytest.mark.parametrize("m,n,r,iters", MU_CASES)
-def test_nmf_mu_parity(h, ora, m, n, r, iters):
+def test_nmf_mu_parity(h, ora, m, n, r, iters, monkeypatch):
+    # the grid-wide / tiny / two-pass kernels: cluster mode (tested below) would take the
+    # mid-size shapes here, so it is switched off for this list
+    monkeypatch.setenv("NTT_NO_CLUSTER", "1")
+    assert h.mu_path(m, n, r) != 2
     X, W0, H0 = _mu_inputs(m, n, r, m * 7 + n)
     Xd, Wd, Hd = dev(X), dev(W0), dev(H0)
     h.ntt_nmf_mu(Xd, m, n, n, r, iters, 1e-16, Wd, Hd)
@@ -140,6 +144,54 @@ def test_nmf_mu_parity(h, ora, m, n, r, iters):
     assert_close_factor(host(Wd), Wo, what=f"W {m}x{n} r{r}")
     assert_close_factor(host(Hd), Ho, what=f"H {m}x{n} r{r}")
     assert np.all(host(Wd) >= 0) and np.all(host(Hd) >= 0)
+
+
+# cluster mode (mu_cluster.cu): X in the distributed shared memory of one thread-block cluster.
+# Config 3 steps 4-5 and config 4 steps 5-6 shapes, ragged column / row ownership across the
+# CTAs (incl. CTAs that own no W row), both rank classes (RK = 8, 16), 1..16-CTA clusters.
+CLU_CASES = [
+    (256, 1024, 8, 10),
+    (256, 40, 8, 10),
+    (30, 1296, 5, 12),
+    (256, 1000, 8, 10),
+    (100, 1000, 5, 10),
+    (200, 333, 16, 10),
+    (41, 600, 8, 10),
+    (128, 700, 16, 10),
+    (64, 300, 9, 30),
+    (30, 2000, 5, 10),
+    (64, 1024, 16, 10),
+    (8, 2000, 3, 10),
+]
+
+
+@pytest.mark.parametrize("m,n,r,iters", CLU_CASES)
+def test_nmf_mu_cluster_parity(h, ora, m, n, r, iters):
+    assert h.mu_path(m, n, r) == 2, "shape should take cluster mode"
+    X, W0, H0 = _mu_inputs(m, n, r, m * 5 + n)
+    Xd, Wd, Hd = dev(X), dev(W0), dev(H0)
+    h.ntt_nmf_mu(Xd, m, n, n, r, iters, 1e-16, Wd, Hd)
+    Wo, Ho = ora.nmf_mu(X, W0.astype(np.float64), H0.astype(np.float64), iters, eps=1e-16)
+    W1, H1 = host(Wd), host(Hd)
+    assert_close_factor(W1, Wo, what=f"W {m}x{n} r{r}")
+    assert_close_factor(H1, Ho, what=f"H {m}x{n} r{r}")
+    assert np.all(W1 >= 0) and np.all(H1 >= 0)
+    # fixed-order sums: a second run is bit-identical
+    Wd2, Hd2 = dev(W0), dev(H0)
+    h.ntt_nmf_mu(Xd, m, n, n, r, iters, 1e-16, Wd2, Hd2)
+    assert np.array_equal(host(Wd2), W1) and np.array_equal(host(Hd2), H1)
+
+
+def test_nmf_mu_cluster_leading_dimension(h, ora):
+    m, n, r, ldx = 256, 1000, 8, 1030
+    X, W0, H0 = _mu_inputs(m, ldx, r, 6)
+    H0 = np.ascontiguousarray(H0[:, :n])
+    assert h.mu_path(m, n, r) == 2
+    Xd, Wd, Hd = dev(X), dev(W0), dev(H0)
+    h.ntt_nmf_mu(Xd, m, n, ldx, r, 8, 1e-16, Wd, Hd)
+    Wo, Ho = ora.nmf_mu(np.ascontiguousarray(X[:, :n]), W0.astype(np.float64), H0.astype(np.float64), 8)
+    assert_close_factor(host(Wd), Wo, what="W ldx")
+    assert_close_factor(host(Hd), Ho, what="H ldx")
 
 
 def test_nmf_mu_leading_dimension(h, ora):
