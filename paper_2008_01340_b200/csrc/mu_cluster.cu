@@ -513,13 +513,13 @@ bool cluster_fits(int rk, int cs, size_t smem) {
 // <= kCluCols columns of X per CTA, raised until the shared-memory plan fits; 0 = not eligible
 // (also for one CTA: 256 x 32 measured slower than the persistent kernel's 1-CTA grid).
 int cluster_size_for(int64_t m, int64_t n, int r) {
-  constexpr int64_t kCluEntries = 8 * 1024, kCluCols = 192;
+  constexpr int64_t kCluEntries = 1024, kCluCols = 192;
   if (m < 1 || m > 255 + 1 || n < 1 || r < 1 || r > 16 || n > (int64_t)CLU_MAXCS * 4096) return 0;
   int cs = 1;
   while (cs < CLU_MAXCS && (m * ((n + cs - 1) / cs) > kCluEntries || (n + cs - 1) / cs > kCluCols)) cs *= 2;
   if ((n + cs - 1) / cs > kCluCols) return 0;  // measured: wide column blocks (30 x 7776) lose to the grid kernel
   if (const char* f = getenv("NTT_CLU_CS")) cs = std::max(cs, atoi(f));  // experiments: a larger cluster
-  if (cs < 2) return 0;  // measured: one CTA (256 x 32) is slower than the persistent kernel's 1-CTA grid
+  if (cs < 2) return 0;  // one CTA: the tiny / persistent kernels
   for (; cs <= CLU_MAXCS; cs *= 2) {
     const CluPlan g = make_plan(m, n, r, cs);
     if (g.bytes + 1024 <= (size_t)max_smem()) return cs;

@@ -115,6 +115,13 @@ __device__ __forceinline__ void pstamp(const PersistArgs& pa, int it, int ph) {
     // per-CTA end of pass 1 (load-balance diagnostics): [16384 + cta], start of pass 1: [17408 + cta]
     if (it == 1 && ph == 1 && blockIdx.x < 1024) pa.trace[16384 + blockIdx.x] = t;
     if (it == 1 && ph == 0 && blockIdx.x < 1024) pa.trace[17408 + blockIdx.x] = t;
+    // passes 2..4: per-CTA ends at [18432 + 1024 (it - 2) + cta]; the CTA's SM at [21504 + cta]
+    if (it >= 2 && it <= 4 && ph == 1 && blockIdx.x < 1024) pa.trace[18432 + 1024 * (it - 2) + blockIdx.x] = t;
+    if (it == 1 && ph == 0 && blockIdx.x < 1024) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      pa.trace[21504 + blockIdx.x] = smid;
+    }
   }
 }
 

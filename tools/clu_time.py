@@ -8,7 +8,7 @@ import torch
 sys.path.insert(0, ".")
 import paper_2008_01340_b200 as P  # noqa: E402
 
-shapes = [(256, 1024, 8), (256, 40, 8), (256, 128, 8), (256, 256, 8), (30, 7776, 5), (30, 1296, 5), (30, 216, 5), (30, 36, 5),
+shapes = [(256, 1024, 8), (256, 32, 8), (256, 40, 8), (256, 128, 8), (256, 256, 8), (100, 60, 5), (128, 32, 8), (30, 7776, 5), (30, 1296, 5), (30, 216, 5), (30, 36, 5),
           (256, 1024, 10), (256, 2048, 8), (64, 4096, 8), (128, 1024, 16), (20, 30, 4), (12, 5, 3)]
 h = P.Handle(0)
 for (m, n, r) in shapes:

@@ -10,8 +10,9 @@ sys.path.insert(0, ".")
 import paper_2008_01340_b200 as P  # noqa: E402
 from paper_2008_01340_b200._lib import lib  # noqa: E402
 
-shapes = [(32, 32**5, 8, 20), (256, 32**4, 8, 20), (256, 32**3, 8, 50), (256, 32**2, 8, 50), (256, 32, 8, 50),
-          (6, 6**9, 5, 20), (30, 6**4, 5, 50)]
+shapes = [(int(a), int(b), int(c), int(d)) for a, b, c, d in (x.split(',') for x in sys.argv[1:])] or \
+    [(32, 32**5, 8, 20), (256, 32**4, 8, 20), (256, 32**3, 8, 50), (256, 32**2, 8, 50), (256, 32, 8, 50),
+     (6, 6**9, 5, 20), (30, 6**4, 5, 50)]
 h = P.Handle(0)
 for (m, n, r, it) in shapes:
     X = torch.rand(m * n, device="cuda")
