@@ -56,6 +56,25 @@ __device__ __forceinline__ double mu_quot(double w, double num, double den, doub
   return __ddiv_rn(__dmul_rn(w, num), __dadd_rn(den, eps));
 }
 
+// The fp64 MU quotient of the in-kernel W updates, rounded to fp32 by the caller: (w num) /
+// (den + eps) through a hardware reciprocal estimate, two Newton steps and one residual
+// correction (no call into the IEEE division routine, whose serial slow-path checks dominated the
+// persistent kernels' W update).  Within one fp64 ulp of the IEEE quotient, so the fp32 result is
+// the IEEE one except when the fp64 quotient lies within an ulp of an fp32 rounding boundary
+// (reading R4).  Zero, subnormal, huge or non-finite divisors take the IEEE division.
+__device__ __forceinline__ double mu_quot_fast(double w, double num, double den, double eps) {
+  const double a = __dmul_rn(w, num), b = __dadd_rn(den, eps);
+  if (!(b > 1e-290 && b < 1e290)) return __ddiv_rn(a, b);
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+  double e = fma(-b, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-b, r, 1.0);
+  r = fma(r, e, r);
+  const double q = a * r;
+  return fma(r, fma(-b, q, a), q);
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

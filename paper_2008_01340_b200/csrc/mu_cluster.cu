@@ -274,7 +274,7 @@ k_clu(const float* __restrict__ X, int64_t ldx, float* __restrict__ W, float* __
         double d = 0.0;
 #pragma unroll
         for (int l = 0; l < RK; ++l) d = fma((double)wr[l], Ql[l * RK + k], d);
-        v = (float)mu_quot((double)wr[k], Pl[e], d, (double)eps);
+        v = (float)mu_quot_fast((double)wr[k], Pl[e], d, (double)eps);
       }
       Wp[e] = v;
     }

@@ -287,31 +287,33 @@ __device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int 
   double* Wd = Qp + RK * RK;       // m x RK
   double* Wnd = Wd + m * RK;       // m x RK
   double* Gp = Wnd + m * RK;       // [GC][RK][RK]
-  // (P, Q) into shared memory: coalesced, all 8 loads of a thread issued before any is used
+  // (P, Q) into shared memory: coalesced, all 16 loads of a thread issued before any is used
+  // (one L2 round trip for L <= 16 T: m = 256, r = 8 at 160 threads)
   const double* xslots = pa.nranks > 0 ? pa.xpeers[pa.rank] + (size_t)(seq & 1ull) * pa.nranks * kXLmax : nullptr;
-  for (int e0 = 0; e0 < L; e0 += 8 * T) {
-    double v[8];
+  constexpr int NV = 16;
+  for (int e0 = 0; e0 < L; e0 += NV * T) {
+    double v[NV];
     if (pa.nranks > 0) {  // sum of the ranks' vectors in rank order (identical on every rank)
 #pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = 0.0;
+      for (int q = 0; q < NV; ++q) v[q] = 0.0;
 #pragma unroll 4
       for (int sr = 0; sr < pa.nranks; ++sr) {
         const double* sl = xslots + (size_t)sr * kXLmax;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < NV; ++q) {
           const int e = e0 + q * T + tid;
           if (e < L) v[q] += __ldcg(sl + e);
         }
       }
     } else {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < NV; ++q) {
         const int e = e0 + q * T + tid;
         v[q] = e < L ? __ldcg(srcv + e) : 0.0;
       }
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < NV; ++q) {
       const int e = e0 + q * T + tid;
       if (e < m * r) P[e] = v[q];
       else if (e < L) {
@@ -325,30 +327,30 @@ __device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int 
   for (int e = tid; e < m * RK; e += T) Wd[e] = (double)Ws[e];
   __syncthreads();
   pstamp2(pa, it, 0);
-  // W <- W o P / (W Q + eps) (fp64, reading R4): a thread owns whole rows i (RK independent
-  // chains d_k = sum_l W[i][l] Q[l][k], Q rows broadcast from shared memory)
-  for (int i = tid; i < m; i += T) {
-    double w[RK], d[RK];
+  // W <- W o P / (W Q + eps) (fp64, reading R4): thread (rank kq = tid % RK, row group) keeps
+  // column kq of Q in registers and walks rows tid / RK, + T / RK, ...: one quotient per row and
+  // thread (independent across the unrolled rows; a thread owning whole rows serialised RK
+  // quotients), the d = sum_l W[i][l] Q[l][kq] chain in the same order as before
+  {
+    const int kq = tid % RK, di = T / RK;
+    double qc[RK];
 #pragma unroll
-    for (int l = 0; l < RK; l += 2) {
-      const double2 v = *reinterpret_cast<const double2*>(Wd + i * RK + l);
-      w[l] = v.x;
-      w[l + 1] = v.y;
-    }
+    for (int l = 0; l < RK; ++l) qc[l] = Qp[l * RK + kq];
+#pragma unroll 2
+    for (int i = tid / RK; i < m; i += di) {
+      double w[RK];
 #pragma unroll
-    for (int k = 0; k < RK; ++k) d[k] = 0.0;
-#pragma unroll
-    for (int l = 0; l < RK; ++l) {
-#pragma unroll
-      for (int k = 0; k < RK; k += 2) {
-        const double2 q = *reinterpret_cast<const double2*>(Qp + l * RK + k);
-        d[k] = fma(w[l], q.x, d[k]);
-        d[k + 1] = fma(w[l], q.y, d[k + 1]);
+      for (int l = 0; l < RK; l += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(Wd + i * RK + l);
+        w[l] = v.x;
+        w[l + 1] = v.y;
       }
-    }
+      double d = 0.0;
 #pragma unroll
-    for (int k = 0; k < RK; ++k)
-      Wnd[i * RK + k] = k < r ? (double)(float)mu_quot(w[k], P[i * r + k], d[k], (double)eps) : 0.0;
+      for (int l = 0; l < RK; ++l) d = fma(w[l], qc[l], d);
+      const double wk = Wd[i * RK + kq];  // not w[kq]: a run-time index puts w in local memory
+      Wnd[i * RK + kq] = kq < r ? (double)(float)mu_quot_fast(wk, P[i * r + kq], d, (double)eps) : 0.0;
+    }
   }
   __syncthreads();
   pstamp2(pa, it, 1);
