@@ -354,16 +354,18 @@ __device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int 
   }
   __syncthreads();
   pstamp2(pa, it, 1);
+#pragma unroll 4
   for (int e = tid; e < m * RK; e += T) Ws[e] = (float)Wnd[e];
   // G = Wn^T Wn: thread (k, chunk c) accumulates row k of G over the chunk's rows (RK
   // independent chains); chunks summed in fixed order below
   const int GC = T / RK;
   for (int t = tid; t < RK * GC; t += T) {
     const int k = t % RK, c = t / RK;
-    const int i0 = (int)((int64_t)m * c / GC), i1 = (int)((int64_t)m * (c + 1) / GC);
+    const int i0 = m * c / GC, i1 = m * (c + 1) / GC;  // m <= 256: 32-bit
     double g[RK];
 #pragma unroll
     for (int l = 0; l < RK; ++l) g[l] = 0.0;
+#pragma unroll 4
     for (int i = i0; i < i1; ++i) {
       const double wk = Wnd[i * RK + k];
 #pragma unroll
@@ -380,6 +382,7 @@ __device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int 
   pstamp2(pa, it, 2);
   for (int e = tid; e < RK * RK; e += T) {
     double sg = 0.0;
+#pragma unroll 4
     for (int c = 0; c < GC; ++c) sg += Gp[c * RK * RK + e];
     Gs[e] = ((e / RK) < r && (e % RK) < r) ? (float)sg : 0.0f;
   }
