@@ -223,6 +223,7 @@ k_clu(const float* __restrict__ X, int64_t ldx, float* __restrict__ W, float* __
       for (int u = 0; u < NR; ++u) {
         const int a = ap + u * mh;
         if (a < m) {
+          NTT_DCHECK(ch < nc2 && a < m);
           double* dst = nc2 == 1 ? PQ + a * RK : CH + ((size_t)ch * m + a) * RK;
 #pragma unroll
           for (int k = 0; k < RK; k += 2)
@@ -255,6 +256,7 @@ k_clu(const float* __restrict__ X, int64_t ldx, float* __restrict__ W, float* __
     //      thread's remote loads in flight together), W update of the owned rows
     for (int e = tid; e < E1; e += T) {
       const int off = e < nrow * RK ? r0 * RK + e : m * RK + (e - nrow * RK);
+      NTT_DCHECK(off < m * RK + RK * RK && e < g.rows_max * RK + RK * RK);
       double v[CLU_MAXCS];
 #pragma unroll
       for (int q = 0; q < CLU_MAXCS; ++q) v[q] = q < CS ? cl.map_shared_rank(PQ, q)[off] : 0.0;
@@ -310,6 +312,7 @@ k_clu(const float* __restrict__ X, int64_t ldx, float* __restrict__ W, float* __
           v[u] = 0.0f;
           if (e < m * RK) {
             const int i = e / RK, o = own[i];
+            NTT_DCHECK(o < CS && i - clu_row0(o, m, lcs) < g.rows_max);
             v[u] = cl.map_shared_rank(Wp, o)[(i - clu_row0(o, m, lcs)) * RK + (e % RK)];
           }
         }
@@ -346,6 +349,7 @@ k_clu(const float* __restrict__ X, int64_t ldx, float* __restrict__ W, float* __
         const int ja = t % half, q = t / half;
         const bool two = ja + half < ncl;
         const int jb = two ? ja + half : ja;
+        NTT_DCHECK(q < g.nq && jb < ncl && ncl <= g.ncmax);
         const int i0 = m * q / nq, i1 = m * (q + 1) / nq;
         float2 sa[R2], sb[R2];
 #pragma unroll
