@@ -19,6 +19,9 @@ if [ $rc -eq 0 ]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_fused_c -c 1 -f \
     -o gpurun_out/fused_c_$tag python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-other \
     > gpurun_out/ncu_full_c_$tag.log 2>&1; echo "ncu full c rc $?"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_clu -c 1 -f \
+    -o gpurun_out/clu_$tag python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-other \
+    > gpurun_out/ncu_full_clu_$tag.log 2>&1; echo "ncu full clu rc $?"
 fi
 if [ -n "$2" ]; then
   timeout 1200 python bench.py --oracle-full --steps 2 --warmup 3 > gpurun_out/bench_oraclefull_$tag.json 2> gpurun_out/bench_oraclefull_$tag.err; echo "oracle-full bench rc $?"
