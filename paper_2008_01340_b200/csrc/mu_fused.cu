@@ -242,17 +242,18 @@ __device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int 
     grid_sync(pa.ctr, epoch);
     pstamp(pa, it, 2);
     const int G = gridDim.x;
+    const int NP = G + 8 * pa.tail_groups;  // partial slots: one per CTA, then the dynamic tail's
     const int SL = (L + G - 1) / G;
     const int e0 = blockIdx.x * SL;
     const int ne = min(L, e0 + SL) - e0;
     if (ne > 0) {
-      // slice [e0, e0 + ne) summed over the G partials: (entry, chunk of partials) per thread, all
+      // slice [e0, e0 + ne) summed over the NP partials: (entry, chunk of partials) per thread, all
       // loads of a chunk (<= 16) issued before any is used (one L2 round trip)
       int C = T / ne;
-      C = C < 1 ? 1 : (C > 32 ? 32 : C);
+      C = C < 1 ? 1 : (C > 96 ? 96 : C);
       for (int t = tid; t < ne * C; t += T) {
         const int e = t % ne, c = t / ne;
-        const int g0 = (int)((int64_t)G * c / C), g1 = (int)((int64_t)G * (c + 1) / C);
+        const int g0 = (int)((int64_t)NP * c / C), g1 = (int)((int64_t)NP * (c + 1) / C);
         const double* src = pa.part + e0 + e;
         double acc = 0.0;
         for (int gb = g0; gb < g1; gb += 16) {
@@ -265,10 +266,14 @@ __device__ void persist_step(const PersistArgs& pa, unsigned& epoch, int m, int 
         scr[c * ne + e] = acc;
       }
       __syncthreads();
-      for (int e = tid; e < ne; e += T) {
+      // the C chunk sums of an entry: a warp per entry, lane l adds chunks l, l + 32, ... in order,
+      // then a fixed xor butterfly (a sequential loop over C <= 96 chunks was ~1.5 us)
+      const int wid = tid >> 5, ln = tid & 31;
+      for (int e = wid; e < ne; e += (T >> 5)) {
         double sv = 0.0;
-        for (int c = 0; c < C; ++c) sv += scr[c * ne + e];
-        __stcg(pa.red + e0 + e, sv);
+        for (int c = ln; c < C; c += 32) sv += scr[c * ne + e];
+        sv = warp_sum(sv);
+        if (ln == 0) __stcg(pa.red + e0 + e, sv);
       }
     }
     grid_sync(pa.ctr, epoch);
@@ -1626,6 +1631,7 @@ cudaError_t launch_t(const CUtensorMap& mx, const CUtensorMap& mh, int m, int64_
 // launch stores them in the X16 cache in its prologue pass and streams them afterwards.
 // ===========================================================================
 constexpr int NWM = 8;                     // consumer warps
+constexpr int kTailGroup = 16;             // dynamic-tail claim unit (tiles; a multiple of NWM)
 constexpr int XBM = 4 * 32 * 128;          // X region: 4 boxes of 32 rows x 32 columns (fp32 / fp16 hi+lo)
 constexpr int HBM = 4 * 8 * 128;           // H region: 4 boxes of 8 ranks x 32 columns
 constexpr int SBM = XBM + HBM + 1024;      // + 16 B of block scales (1024-aligned stages)
@@ -1649,6 +1655,8 @@ k_fused_m(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   uint32_t* issued = reinterpret_cast<uint32_t*>(empty + ns);
   uint32_t* free_mask = issued + 1;
   uint32_t* tag = issued + 2;  // [ns <= 24]
+  uint32_t* ptot = tag + 24;   // [2] dynamic tail: absolute end position of the pass, by parity
+  int32_t* tileid = reinterpret_cast<int32_t*>(tag + 26);  // [ns <= 24] tile held by the stage
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool persist = pa.iters > 0;
 
@@ -1674,6 +1682,7 @@ k_fused_m(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     *issued = 0u;
     *free_mask = (ns >= 32) ? 0xffffffffu : ((1u << ns) - 1u);
     for (int q = 0; q < ns; ++q) tag[q] = 0xffffffffu;
+    ptot[0] = ptot[1] = 0xffffffffu;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -1681,7 +1690,13 @@ k_fused_m(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
 
   const int64_t ntiles = (n + 127) / 128;
   const int64_t b = blockIdx.x;
-  const int64_t J = (ntiles > b) ? (ntiles - b + gridDim.x - 1) / gridDim.x : 0;
+  const int G = gridDim.x;
+  // static tiles [0, S) round robin; the dynamic tail [S, ntiles) = TG groups of kTailGroup (persistent)
+  const int TG = persist ? pa.tail_groups : 0;
+  const int64_t S = ntiles - kTailGroup * (int64_t)TG;
+  const int64_t J = (S > b) ? (S - b + G - 1) / G : 0;  // static tiles of this CTA
+  const int64_t Jmax = J + kTailGroup * (int64_t)TG;      // positions per pass (unique across passes)
+  unsigned long long* pool = reinterpret_cast<unsigned long long*>(pa.ctr + 8);
   unsigned epoch = 0;
   const int nit = persist ? pa.iters + 1 : 1;
   const unsigned long long xs0 = persist ? xseq_load(pa) : 0ull;
@@ -1691,14 +1706,14 @@ k_fused_m(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   const bool do_acc = (md & kFusedAcc) != 0;
   const bool x16_write = pa.x16 != nullptr && persist && it == 0;
   const bool x16_read = pa.x16 != nullptr && persist && it > 0;
-  const int64_t pbase = (int64_t)it * J;
+  const int64_t pbase = (int64_t)it * Jmax;
   pstamp(pa, it, 0);
   if (warp == NWM) {
     // ================= producer =================
     if (lane == 0) {
       const uint64_t policy = evict_first ? policy_evict_first() : policy_evict_normal();
-      for (int64_t j = 0; j < J; ++j) {
-        const int64_t pos = pbase + j;
+      if (TG > 0) ptot[(it + 1) & 1] = 0xffffffffu;  // the next pass's total; nobody reads it now
+      auto issue = [&](const int64_t tile, const int64_t pos) {
         uint32_t fm;
         while ((fm = ld_acquire_u32(free_mask)) == 0u) __nanosleep(32);
         const int s = __ffs(fm) - 1;
@@ -1706,7 +1721,7 @@ k_fused_m(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         const uint32_t ph = (par_mask >> s) & 1u;
         par_mask ^= 1u << s;
         tag[s] = ((uint32_t)pos << 1) | ph;
-        const int64_t tile = b + j * gridDim.x;
+        tileid[s] = (int32_t)tile;
         unsigned char* st = stages + (size_t)s * SBM;
         if (x16_read) {
           NTT_DCHECK(tile < ntiles);
@@ -1720,6 +1735,19 @@ k_fused_m(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         }
         tma_load_3d(st + XBM, &tmH, 0, 0, (int)(tile * 4), &full[s], policy);
         st_release_u32(issued, (uint32_t)(pos + 1));
+      };
+      for (int64_t j = 0; j < J; ++j) issue(b + j * G, pbase + j);
+      if (TG > 0) {
+        // claims of this pass are [it (TG + G), (it + 1) (TG + G)): TG succeed, each CTA fails once
+        const unsigned long long base = (unsigned long long)it * (unsigned long long)(TG + G);
+        int64_t k = 0;
+        for (;;) {
+          const long long g = (long long)(atomicAdd(pool, 1ull) - base);
+          if (g >= TG) break;
+          for (int u = 0; u < kTailGroup; ++u) issue(S + kTailGroup * g + u, pbase + J + kTailGroup * k + u);
+          ++k;
+        }
+        st_release_u32(&ptot[it & 1], (uint32_t)(pbase + J + kTailGroup * k));
       }
     }
   } else {
@@ -1761,17 +1789,48 @@ k_fused_m(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     for (int e4 = 0; e4 < 4; ++e4) paccd[mh][e4] = 0.0;
   qaccd[0] = qaccd[1] = 0.0;
 
-  for (int64_t j = warp; j < J; j += NWM) {
+  bool parked = false;  // static accumulators parked in pa.park while this warp serves the tail
+  for (int64_t j = warp;; j += NWM) {
+    if (TG == 0 && j >= J) break;
     const int64_t pos = pbase + j;
-    const int64_t jt = (b + j * gridDim.x) * 128;  // first column of the tile
-    if (lane == 0)
-      while (ld_acquire_u32(issued) <= (uint32_t)pos) __nanosleep(64);
-    __syncwarp();
+    int go = 1;
+    if (lane == 0) {
+      // static positions are always issued; a tail position is issued unless the pass's total
+      // (known once the producer's claims fail) ends before it
+      while (ld_acquire_u32(issued) <= (uint32_t)pos) {
+        if (j >= J && ld_acquire_u32(&ptot[it & 1]) <= (uint32_t)pos) {
+          go = 0;
+          break;
+        }
+        __nanosleep(64);
+      }
+    }
+    if (!__shfl_sync(0xffffffffu, go, 0)) break;
     const uint32_t tg = lane < ns ? *reinterpret_cast<volatile uint32_t*>(tag + lane) : 0xffffffffu;
     const unsigned hit = __ballot_sync(0xffffffffu, (tg >> 1) == (uint32_t)pos && lane < ns);
     const int s = __ffs(hit) - 1;
     const uint32_t ph = __shfl_sync(0xffffffffu, tg, s) & 1u;
     NTT_DCHECK(s >= 0 && s < ns);
+    const int64_t tile = TG ? (int64_t)*reinterpret_cast<volatile int32_t*>(tileid + s) : b + j * G;
+    const bool tail = j >= J;
+    NTT_DCHECK(tile < ntiles && (tail == (tile >= S)));
+    const int64_t jt = tile * 128;  // first column of the tile
+    if constexpr (ACC) {
+      if (tail && !parked) {  // first tail tile of this warp: park the static sums
+        double* pk = pa.park + ((size_t)b * NWM + warp) * 320 + lane * 10;
+#pragma unroll
+        for (int mh = 0; mh < 2; ++mh)
+#pragma unroll
+          for (int e4 = 0; e4 < 4; ++e4) {
+            pk[mh * 4 + e4] = paccd[mh][e4];
+            paccd[mh][e4] = 0.0;
+          }
+        pk[8] = qaccd[0];
+        pk[9] = qaccd[1];
+        qaccd[0] = qaccd[1] = 0.0;
+        parked = true;
+      }
+    }
     MBAR_WAIT(&full[s], ph, 2, j);
     unsigned char* st = stages + (size_t)s * SBM;
     unsigned char* hb = st + XBM;
@@ -1783,7 +1842,7 @@ k_fused_m(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
       const float4 sc4 = *reinterpret_cast<const float4*>(st + XBM + HBM);
       xsi[0] = sc4.x; xsi[1] = sc4.y; xsi[2] = sc4.z; xsi[3] = sc4.w;
     } else {
-      unsigned char* gtile = x16_write ? pa.x16 + (b + j * gridDim.x) * X16M_STRIDE : nullptr;
+      unsigned char* gtile = x16_write ? pa.x16 + tile * X16M_STRIDE : nullptr;
 #pragma unroll
       for (int bx = 0; bx < 4; ++bx) {
         unsigned char* blk = st + bx * 4096;
@@ -1950,9 +2009,39 @@ k_fused_m(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
     }
     __syncwarp();
     if (lane == 0) asm volatile("red.release.cta.shared::cta.or.b32 [%0], %1;" ::"r"(smem_u32(free_mask)), "r"(1u << s) : "memory");
+    if constexpr (ACC) {
+      const int64_t ut = tile - S;  // tail: group ut / kTailGroup, member ut % kTailGroup
+      if (tail && (ut % kTailGroup) >= kTailGroup - NWM) {
+        // this warp's last tile of the group (members u, u + 8, ...): their sums -> slot G + 8 g + u % 8
+        const int mr = m * r;
+        double* dst = pa.part + ((int64_t)G + NWM * (ut / kTailGroup) + (ut % NWM)) * (mr + r * r);
+#pragma unroll
+        for (int mh = 0; mh < 2; ++mh)
+#pragma unroll
+          for (int e4 = 0; e4 < 4; ++e4) {
+            const int row = 16 * mh + fg + 8 * (e4 >> 1), k = 2 * ft + (e4 & 1);
+            if (row < m && k < r) dst[row * r + k] = paccd[mh][e4];
+            paccd[mh][e4] = 0.0;
+          }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (fg < r && 2 * ft + q < r) dst[mr + fg * r + 2 * ft + q] = qaccd[q];
+          qaccd[q] = 0.0;
+        }
+      }
+    }
   }
 
   if constexpr (ACC) {
+    if (parked) {  // the static sums back (the tail's were flushed to their slots)
+      const double* pk = pa.park + ((size_t)b * NWM + warp) * 320 + lane * 10;
+#pragma unroll
+      for (int mh = 0; mh < 2; ++mh)
+#pragma unroll
+        for (int e4 = 0; e4 < 4; ++e4) paccd[mh][e4] = pk[mh * 4 + e4];
+      qaccd[0] = pk[8];
+      qaccd[1] = pk[9];
+    }
     // ---- fixed-order CTA reduction of the warps' fp64 partials: red[w][0 .. 256) = P (32 x 8),
     // red[w][256 .. 320) = Q (8 x 8)
     asm volatile("bar.sync 1, %0;" ::"r"(NWM * 32) : "memory");
@@ -1991,7 +2080,7 @@ k_fused_m(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   if (persist) xseq_store(pa, xs0);
 }
 
-size_t fixed_bytes_m() { return 32 * 8 * 4 + 256 + 2 * 24 * 8 + 160 + 1024; }
+size_t fixed_bytes_m() { return 32 * 8 * 4 + 256 + 2 * 24 * 8 + 256 + 1024; }
 
 int stages_m() {
   int ns = (int)((SMEM_BUDGET - fixed_bytes_m()) / SBM);
@@ -2150,6 +2239,19 @@ size_t fused_scratch_bytes(int64_t, int64_t, int, int) { return 0; }
 
 // the tensor-core one-pass kernel for 16 < m <= 32 (k_fused_m) takes the shape (MU only)
 bool fused_m_ok(int64_t m, int64_t n, int r) { return m > 16 && m <= 32 && r <= 8 && (n % 32) == 0; }
+
+// Dynamic tail of the persistent k_fused_m (PersistArgs::tail_groups): ~kTailPerCta tiles per CTA
+// at the end of every pass, in groups of kTailGroup, when each CTA has > 2 kTailPerCta tiles.  Measured:
+// CTA pass times spread 4-7 % (systematic by SM group), i.e. 35-40 us of barrier wait per pass on
+// config 3 step 1.  NTT_NO_TAIL=1: static schedule.
+int fused_tail_groups(int64_t m, int64_t n, int r, int grid) {
+  constexpr int64_t kTailPerCta = 40;
+  const bool off = getenv("NTT_NO_TAIL") != nullptr;
+  if (off || !fused_m_ok(m, n, r) || grid < 1) return 0;
+  const int64_t ntiles = (n + 127) / 128, jfull = ntiles / grid;
+  if (jfull <= 2 * kTailPerCta) return 0;
+  return (int)((ntiles - (jfull - kTailPerCta) * grid) / kTailGroup);
+}
 
 size_t fused_x16_bytes(int64_t m, int64_t n) {
   if (m > 16 && m <= 32 && (n % 32) == 0) return (size_t)((n + 127) / 128) * (size_t)X16M_STRIDE;

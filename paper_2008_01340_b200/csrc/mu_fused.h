@@ -48,6 +48,13 @@ struct PersistArgs {
   // streamed by every later pass instead of converting the fp32 tile again (fused_x16_bytes;
   // nullable: every pass converts)
   unsigned char* x16 = nullptr;
+  // dynamic tail (persistent k_fused_m; the per-SM pass-time spread is systematic, DESIGN s.6): the
+  // last tail_groups groups of 16 tiles of every pass are claimed at run time through a counter in
+  // ctr[8..9] (one failing claim per CTA per pass); the warp that serves members u, u + 8, ... of group
+  // g adds them into partial slot gridDim.x + 8 g + u of part (fixed grouping -> deterministic sums)
+  // and parks its static accumulators in park[cta][warp][320] meanwhile.  0 = static schedule.
+  int tail_groups = 0;
+  double* park = nullptr;
   // cross-GPU exchange (persistent launch on an ntt_create_dist handle, SURVEY s.8(e)): after the
   // per-GPU reduction of every pass, CTA 0 stores the (P, Q) vector into slot [seq & 1][rank] of
   // every rank's exchange buffer (NVLink peer stores; IPC-mapped, own buffer included), raises
@@ -66,6 +73,10 @@ __host__ __device__ inline size_t xbuf_bytes(int nranks) {
 }
 // bytes of the PersistArgs::x16 cache for an m x n X (0 when m <= 40)
 size_t fused_x16_bytes(int64_t m, int64_t n);
+// groups of 16 tiles served dynamically at the end of every pass of the persistent k_fused_m
+// (0 = static schedule); the launcher needs pa.part with grid + 8 groups slots and pa.park with
+// grid * 8 * 320 doubles
+int fused_tail_groups(int64_t m, int64_t n, int r, int grid);
 
 // One pass over X (m x n, row stride ldx) with the current W (m x r) and
 // G = sum_c Gpart[c] (nG partials).  mode = kFusedAcc alone is the prologue

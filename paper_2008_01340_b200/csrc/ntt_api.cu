@@ -313,7 +313,8 @@ struct MuPlan {
   bool persist;   // fused path as one persistent cooperative launch per call
   bool tiny;      // whole MU loop in one CTA from shared memory (mu_tiny.cu)
   bool clu;       // whole MU loop in one thread-block cluster, X in distributed smem (mu_cluster.cu)
-  size_t off_P, off_Q, off_G, off_S, off_tc, off_pp, off_red, off_ctr, off_x16, bytes;
+  int tail;       // k_fused_m dynamic-tail groups (fused_tail_groups)
+  size_t off_P, off_Q, off_G, off_S, off_tc, off_pp, off_park, off_red, off_ctr, off_x16, bytes;
 };
 
 // dist: a handle from ntt_create_dist* (any number of ranks, 1 included) -- its MU runs
@@ -359,7 +360,10 @@ MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, bool dist, bool xpersis
   p.tiny = !dist && tiny_supported(m, n, r) && !getenv("NTT_NO_TINY") && !(clu_ok && m * n >= 4096);
   p.clu = clu_ok && !p.tiny;
   p.off_pp = o;
-  if (p.persist) o = align_up(o + sizeof(double) * (size_t)p.fgrid * (size_t)(m * r + r * r));
+  p.tail = p.persist ? fused_tail_groups(m, n, r, p.fgrid) : 0;
+  if (p.persist) o = align_up(o + sizeof(double) * (size_t)(p.fgrid + 8 * p.tail) * (size_t)(m * r + r * r));
+  p.off_park = o;
+  if (p.tail) o = align_up(o + sizeof(double) * (size_t)p.fgrid * 8 * 320);
   p.off_red = o;
   if (p.persist) o = align_up(o + sizeof(double) * (size_t)(m * r + r * r));
   p.off_ctr = o;
@@ -420,6 +424,10 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
     pa.Wout = W;
     pa.trace = h->ptrace;  // diagnostics (NTT_PERSIST_TRACE), else null
     pa.x16 = fused_x16_bytes(m, n) ? reinterpret_cast<unsigned char*>(scratch + p.off_x16) : nullptr;
+    if (p.tail) {  // the k_fused_m shapes only (fused_tail_groups)
+      pa.tail_groups = p.tail;
+      pa.park = reinterpret_cast<double*>(scratch + p.off_park);
+    }
     CU(h, cudaMemsetAsync(pa.ctr, 0, 64, st));
     PLAUNCH(h, 0, (double)iters * 4.0 * (double)(m + 2 * r) * (double)n + 4.0 * (double)(m + r) * (double)n,
             launch_fused(X, ldx, m, n, r, W, nullptr, 0, eps, H, nullptr, nullptr, 0, p.fgrid, st, &pa));

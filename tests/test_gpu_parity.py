@@ -420,3 +420,29 @@ def test_validation_nonneg(h):
     Xb = X.copy()
     Xb[0, 0] = -1.0
     h.ntt_nmf_mu(dev(Xb), 8, 64, 64, 2, 3, 1e-16, dev(W0), dev(H0))     # off: not checked
+
+
+def test_nmf_mu_dynamic_tail(h, ora, monkeypatch):
+    """k_fused_m's dynamic tail (the last ~64 tiles per CTA of every pass claimed at run time in
+    groups of 16, each group's sums in a fixed slot): active from ~2.4 M columns on.  Bit-identical
+    across runs (the claim order varies, the grouping does not), within rounding of the static
+    schedule, and against the oracle at 1e-4."""
+    m, n, r, iters = 32, 1 << 22, 8, 3
+    assert h.mu_path(m, n, r) == 3
+    X, W0, H0 = _mu_inputs(m, n, r, 4)
+    Xd = dev(X)
+    outs = []
+    for tail in (True, True, False):
+        if tail:
+            monkeypatch.delenv("NTT_NO_TAIL", raising=False)
+        else:
+            monkeypatch.setenv("NTT_NO_TAIL", "1")
+        Wd, Hd = dev(W0), dev(H0)
+        h.ntt_nmf_mu(Xd, m, n, n, r, iters, 1e-16, Wd, Hd)
+        outs.append((host(Wd), host(Hd)))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    for a, b in zip(outs[0], outs[2]):
+        assert np.linalg.norm(a.astype(np.float64) - b) <= 1e-6 * np.linalg.norm(b)
+    Wo, Ho = ora.nmf_mu(X, W0.astype(np.float64), H0.astype(np.float64), iters, eps=1e-16)
+    assert_close_factor(outs[0][0], Wo, what="W tail")
+    assert_close_factor(outs[0][1], Ho, what="H tail")
