@@ -70,7 +70,8 @@ def test_dist_handle_decompose_matches(handles, ora, dims, ranks, iters, mode):
 
 
 @pytest.mark.parametrize("m,n,r", [(32, 4096, 8), (256, 2048, 8), (100, 700, 16), (8, 4096, 4), (40, 1024, 8),
-                                   (256, 4096, 12), (64, 2048, 8)])
+                                   (256, 4096, 12), (64, 2048, 8),
+                                   (32, 1 << 22, 8)])  # k_fused_m with its dynamic tail + the exchange
 @pytest.mark.parametrize("mode", [0, 1])
 def test_dist_handle_nmf_mu(handles, ora, m, n, r, mode, monkeypatch):
     h1, hd = handles

@@ -446,3 +446,16 @@ def test_nmf_mu_dynamic_tail(h, ora, monkeypatch):
     Wo, Ho = ora.nmf_mu(X, W0.astype(np.float64), H0.astype(np.float64), iters, eps=1e-16)
     assert_close_factor(outs[0][0], Wo, what="W tail")
     assert_close_factor(outs[0][1], Ho, what="H tail")
+
+
+def test_plan_paths_of_the_workloads(h):
+    """Which kernel path plan_mu gives the TT steps of configs 3 and 4 and the paper's 256^4
+    (ntt_debug_mu_path: 1 tiny, 2 cluster, 3 persistent one-pass); DESIGN.md s.6."""
+    expect = {
+        (32, 32 ** 5, 8): 3, (256, 32 ** 4, 8): 3, (256, 32 ** 3, 8): 3, (256, 32 ** 2, 8): 2, (256, 32, 8): 2,
+        (6, 6 ** 9, 5): 3, (30, 6 ** 8, 5): 3, (30, 6 ** 7, 5): 3, (30, 6 ** 6, 5): 3, (30, 6 ** 5, 5): 3,
+        (30, 6 ** 4, 5): 2, (30, 6 ** 3, 5): 2, (30, 36, 5): 1, (30, 6, 5): 1,
+        (256, 256 ** 3, 10): 3,
+    }
+    got = {k: h.mu_path(*k) for k in expect}
+    assert got == expect
