@@ -40,7 +40,7 @@ cudaError_t launch_hpass(const float* X, int64_t ldx, int64_t m, int64_t n, cons
 // r <= 16) in one CTA from shared memory
 bool tiny_supported(int64_t m, int64_t n, int r);
 cudaError_t launch_tiny(const float* X, int64_t ldx, int64_t m, int64_t n, int r, int iters, float eps, float* W,
-                        float* H, cudaStream_t st);
+                        float* H, cudaStream_t st, unsigned long long* trace = nullptr);
 
 // cluster mode (mu_cluster.cu): the whole MU loop of a mid-size X (m <= 256, r <= 16, at most
 // ~16 K entries of X per CTA) in one thread-block cluster of <= 16 CTAs, X resident in the

@@ -46,7 +46,10 @@ struct TinyLayout {
 template <int R>
 __global__ void __launch_bounds__(TINY_THREADS, 1)
 k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters, float eps, float* __restrict__ W,
-       float* __restrict__ H, int nch) {
+       float* __restrict__ H, int nch, unsigned long long* trace) {
+  auto stamp = [&](int it, int k) {  // diagnostics (NTT_PERSIST_TRACE): clock64 of thread 0
+    if (trace && threadIdx.x == 0 && it < 512) trace[12288 + it * 8 + k] = (unsigned long long)clock64();
+  };
   extern __shared__ __align__(16) unsigned char sm[];
   auto al = [](size_t v) { return (v + 15) & ~size_t(15); };
   const int ld = tiny_ld(n);
@@ -86,6 +89,7 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
   const int EP = m * R, EQ = R * R, E = EP + EQ;
   const int nblk = (n + TINY_BLK - 1) / TINY_BLK;
   for (int it = 0; it < iters; ++it) {
+    stamp(it, 0);
     if (n <= 256) {
     // ---- short rows: P = X H^T and Q = H H^T entry-parallel, entry e x chunk c of
     //      64-column blocks, fp32 inside a block, fp64 across.  P entries run row-fastest
@@ -117,6 +121,7 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
       part[c * E + e] = acc;
     }
     __syncthreads();
+    stamp(it, 1);
     for (int e = tid; e < E; e += T) {
       double sv = 0.0;
       for (int c = 0; c < nch; ++c) sv += part[c * E + e];
@@ -124,6 +129,7 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
       else Q[e - EP] = sv;
     }
     __syncthreads();
+    stamp(it, 2);
     } else {
     // ---- long rows: P = X H^T and Q = H H^T: one warp per row task (X row i, then H row k);
     //      lanes stride the columns (conflict-free), fp32 per lane over <= 64
@@ -178,6 +184,7 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
       Wn[e] = v;
     }
     __syncthreads();
+    stamp(it, 3);
     for (int e = tid; e < EP; e += T) Ws[e] = Wn[e];
     // ---- G = W^T W (fp64, fixed order over rows)
     for (int e = tid; e < EQ; e += T) {
@@ -188,6 +195,7 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
       Gf[e] = (float)sg;
     }
     __syncthreads();
+    stamp(it, 4);
     // ---- H update, one thread per column: S = W^T X[:, j], E = G H[:, j]
     for (int j = tid; j < n; j += T) {
       float s[R], h[R];
@@ -210,6 +218,7 @@ k_tiny(const float* __restrict__ X, int64_t ldx, int m, int n, int r, int iters,
       }
     }
     __syncthreads();
+    stamp(it, 5);
   }
   for (int e = tid; e < r * n; e += T) H[e] = Hs[(e / n) * ld + e % n];
   for (int e = tid; e < m * r; e += T) W[e] = Ws[(e / r) * R + (e % r)];
@@ -226,12 +235,12 @@ int tiny_nch(int m, int r, int n) {
 
 template <int R>
 cudaError_t launch_tiny_t(const float* X, int64_t ldx, int m, int n, int r, int iters, float eps, float* W, float* H,
-                          cudaStream_t st) {
+                          cudaStream_t st, unsigned long long* trace) {
   const int nch = tiny_nch(m, r, n);
   const size_t sm = TinyLayout<R>::bytes(m, n, nch);
   cudaError_t e = smem_optin((const void*)(k_tiny<R>), sm);
   if (e != cudaSuccess) return e;
-  k_tiny<R><<<1, TINY_THREADS, sm, st>>>(X, ldx, m, n, r, iters, eps, W, H, nch);
+  k_tiny<R><<<1, TINY_THREADS, sm, st>>>(X, ldx, m, n, r, iters, eps, W, H, nch, trace);
   return cudaGetLastError();
 }
 
@@ -250,10 +259,10 @@ bool tiny_supported(int64_t m, int64_t n, int r) {
 }
 
 cudaError_t launch_tiny(const float* X, int64_t ldx, int64_t m, int64_t n, int r, int iters, float eps, float* W,
-                        float* H, cudaStream_t st) {
-  if (r <= 4) return launch_tiny_t<4>(X, ldx, (int)m, (int)n, r, iters, eps, W, H, st);
-  if (r <= 8) return launch_tiny_t<8>(X, ldx, (int)m, (int)n, r, iters, eps, W, H, st);
-  return launch_tiny_t<16>(X, ldx, (int)m, (int)n, r, iters, eps, W, H, st);
+                        float* H, cudaStream_t st, unsigned long long* trace) {
+  if (r <= 4) return launch_tiny_t<4>(X, ldx, (int)m, (int)n, r, iters, eps, W, H, st, trace);
+  if (r <= 8) return launch_tiny_t<8>(X, ldx, (int)m, (int)n, r, iters, eps, W, H, st, trace);
+  return launch_tiny_t<16>(X, ldx, (int)m, (int)n, r, iters, eps, W, H, st, trace);
 }
 
 }  // namespace ntt

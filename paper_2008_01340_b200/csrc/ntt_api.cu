@@ -398,7 +398,7 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
   if (p.tiny && !dist && !dev_trace) {
     // tiny mode: every iteration in one CTA from shared memory (mu_tiny.cu)
     PLAUNCH(h, 0, (double)iters * 4.0 * (double)(m + 2 * r) * (double)n,
-            launch_tiny(X, ldx, m, n, r, iters, eps, W, H, st));
+            launch_tiny(X, ldx, m, n, r, iters, eps, W, H, st, h->ptrace));
     return NTT_OK;
   }
   if (p.clu && !dist && !dev_trace) {
