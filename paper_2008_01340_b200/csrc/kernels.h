@@ -31,6 +31,12 @@ cudaError_t launch_wupdate(float* W, int64_t m, int r, const double* Ppart, int 
 // If Ppart != nullptr, also accumulates per-CTA partials of P' = X Hn^T, Q' = Hn Hn^T
 // (the 1-pass fusion; requires m*r <= kMaxAccMR) into Ppart[cta], Qpart[cta].
 constexpr int64_t kMaxAccMR = 4096;
+// split-K H pass (no P, Q accumulation) for few column tiles and many rows: hpass_splits() splits
+// (0 = not used), Spart = splits x n x Rpad fp64 (Rpad = r rounded up to 2/4/8/16/32/64)
+int hpass_splits(int64_t m, int64_t n, int num_sms);
+cudaError_t launch_hpass_sk(const float* X, int64_t ldx, int64_t m, int64_t n, const float* W, int r,
+                            const double* Gpart, int nG, float eps, float* H, int ks, double* Spart, double* Gred,
+                            cudaStream_t st);
 int hpass_ctas(int64_t m, int64_t n, int r, bool acc, int num_sms);
 cudaError_t launch_hpass(const float* X, int64_t ldx, int64_t m, int64_t n, const float* W, int r,
                          const double* Gpart, int nG, float eps, float* H, int grid, double* Ppart,

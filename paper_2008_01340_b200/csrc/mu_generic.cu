@@ -322,6 +322,119 @@ static cudaError_t hpass_t(const float* X, int64_t ldx, int64_t m, int64_t n, co
   return cudaGetLastError();
 }
 
+// Split-K H pass for few column tiles and many rows (e.g. the 500 GB tensor's step 3, 15360 x 64,
+// r 40: one 128-column tile left one CTA walking all rows).  k_hpass_sk: CTA (tile, split) sums
+// S = W^T X over its rows (fp32 per HP_MCH-row chunk, fp64 across, as k_hpass) into
+// Spart[split][j][R]; k_hpass_fin: CTA of 256 threads = HF_C columns x R ranks sums the splits in
+// order (fp64), then thread (column, rank) applies the MU H update.
+template <int R>
+__global__ void __launch_bounds__(HP_BN)
+k_hpass_sk(const float* __restrict__ X, int64_t ldx, int64_t m, int64_t n, const float* __restrict__ W, int r, int ks,
+           double* __restrict__ Spart) {
+  __shared__ float Ws[HP_MCH * R];
+  const int64_t tile = blockIdx.x, k = blockIdx.y;
+  const int64_t i0 = m * k / ks, i1 = m * (k + 1) / ks;
+  const int64_t j = tile * HP_BN + threadIdx.x;
+  const bool valid = j < n;
+  double Sd[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) Sd[q] = 0.0;
+  for (int64_t c0 = i0; c0 < i1; c0 += HP_MCH) {
+    const int rows = (int)min((int64_t)HP_MCH, i1 - c0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < HP_MCH * R; e += blockDim.x) {
+      const int ii = e / R, kk = e % R;
+      Ws[e] = (ii < rows && kk < r) ? W[(c0 + ii) * r + kk] : 0.0f;
+    }
+    __syncthreads();
+    float S[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) S[q] = 0.0f;
+    if (valid)
+      for (int ii = 0; ii < rows; ++ii) {
+        const float x = X[(c0 + ii) * ldx + j];
+#pragma unroll
+        for (int q = 0; q < R; ++q) S[q] = fmaf(Ws[ii * R + q], x, S[q]);
+      }
+#pragma unroll
+    for (int q = 0; q < R; ++q) Sd[q] += (double)S[q];
+  }
+  if (valid) {
+    double* dst = Spart + ((int64_t)k * n + j) * R;
+#pragma unroll
+    for (int q = 0; q < R; ++q) dst[q] = Sd[q];
+  }
+}
+
+constexpr int HF_T = 256;
+template <int R>
+__global__ void __launch_bounds__(HF_T)
+k_hpass_fin(int64_t n, int r, int ks, const double* __restrict__ Spart, const double* __restrict__ Gred,
+            float eps, float* __restrict__ H) {
+  constexpr int C = HF_T / R;  // columns per CTA
+  __shared__ float Gs[R * R];
+  __shared__ float Hc[C][R];
+  for (int t = threadIdx.x; t < R * R; t += HF_T) {  // G already summed over its partials (r x r)
+    const int a = t / R, b = t % R;
+    Gs[t] = (a < r && b < r) ? (float)Gred[a * r + b] : 0.0f;
+  }
+  const int c = threadIdx.x / R, kk = threadIdx.x % R;
+  const int64_t j = (int64_t)blockIdx.x * C + c;
+  const bool valid = j < n && kk < r;
+  Hc[c][kk] = valid ? H[(int64_t)kk * n + j] : 0.0f;
+  double sd = 0.0;
+  if (valid) {
+    const double* src = Spart + j * R + kk;
+    const int64_t stride = n * R;
+    int q = 0;
+    for (; q + 8 <= ks; q += 8) {  // 8 loads in flight, summed in split order
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (int64_t)(q + u) * stride);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sd += v[u];
+    }
+    for (; q < ks; ++q) sd += __ldcg(src + (int64_t)q * stride);
+  }
+  __syncthreads();
+  if (valid) {
+    float e = 0.0f;
+#pragma unroll
+    for (int l = 0; l < R; ++l) e = fmaf(Gs[kk * R + l], Hc[c][l], e);
+    H[(int64_t)kk * n + j] = mu_quot(Hc[c][kk], (float)sd, e, eps);
+  }
+}
+
+// split count of the split-K H pass (0 = the per-tile kernel): few column tiles, many rows
+int hpass_splits(int64_t m, int64_t n, int num_sms) {
+  const int64_t ntiles = (n + HP_BN - 1) / HP_BN;
+  if (ntiles * 4 > num_sms || m < 1024) return 0;
+  int64_t ks = std::min<int64_t>(m / 64, (2 * num_sms + ntiles - 1) / ntiles);
+  return ks >= 2 ? (int)ks : 0;
+}
+
+cudaError_t launch_hpass_sk(const float* X, int64_t ldx, int64_t m, int64_t n, const float* W, int r,
+                            const double* Gpart, int nG, float eps, float* H, int ks, double* Spart, double* Gred,
+                            cudaStream_t st) {
+  const int64_t ntiles = (n + HP_BN - 1) / HP_BN;
+  cudaError_t e0 = launch_sum_partials(Gpart, nG, (int64_t)r * r, Gred, st);  // fixed order
+  if (e0 != cudaSuccess) return e0;
+#define HSK(RR)                                                                                         \
+  do {                                                                                                  \
+    k_hpass_sk<RR><<<dim3((unsigned)ntiles, (unsigned)ks), HP_BN, 0, st>>>(X, ldx, m, n, W, r, ks, Spart); \
+    k_hpass_fin<RR><<<(unsigned)((n + HF_T / RR - 1) / (HF_T / RR)), HF_T, 0, st>>>(n, r, ks, Spart, Gred, eps, \
+                                                                                     H);                \
+  } while (0)
+  if (r <= 2) HSK(2);
+  else if (r <= 4) HSK(4);
+  else if (r <= 8) HSK(8);
+  else if (r <= 16) HSK(16);
+  else if (r <= 32) HSK(32);
+  else HSK(64);
+#undef HSK
+  return cudaGetLastError();
+}
+
 cudaError_t launch_hpass(const float* X, int64_t ldx, int64_t m, int64_t n, const float* W, int r,
                          const double* Gpart, int nG, float eps, float* H, int grid, double* Ppart, double* Qpart,
                          cudaStream_t st) {

@@ -314,6 +314,8 @@ struct MuPlan {
   bool tiny;      // whole MU loop in one CTA from shared memory (mu_tiny.cu)
   bool clu;       // whole MU loop in one thread-block cluster, X in distributed smem (mu_cluster.cu)
   int tail;       // k_fused_m dynamic-tail groups (fused_tail_groups)
+  int hks;        // generic path: split-K H pass splits (0 = per-tile k_hpass)
+  size_t off_hs;  // its S partials
   size_t off_P, off_Q, off_G, off_S, off_tc, off_pp, off_park, off_red, off_ctr, off_x16, bytes;
 };
 
@@ -346,6 +348,12 @@ MuPlan plan_mu(int64_t m, int64_t n, int r, int num_sms, bool dist, bool xpersis
   o = align_up(o + sizeof(double) * (size_t)(nG * r * r));
   p.off_S = o;  // reduced (m r + r r) vector for the distributed all-reduce
   o = align_up(o + sizeof(double) * (size_t)(m * r + r * r));
+  p.hks = p.acc ? 0 : hpass_splits(m, n, num_sms);
+  p.off_hs = o;
+  if (p.hks) {
+    const int rpad = r <= 2 ? 2 : r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : r <= 32 ? 32 : 64;
+    o = align_up(o + sizeof(double) * (size_t)p.hks * (size_t)n * (size_t)rpad);
+  }
   // shape-level eligibility of the tensor-core path (alignment re-checked at run time)
   p.tc = !p.fused && tc_supported(m, n, r, n, nullptr) && !getenv("NTT_NO_TC");
   p.off_tc = o;
@@ -527,8 +535,13 @@ ntt_status run_mu(ntt_handle h, const MuPlan& p, const float* X, int64_t ldx, in
               launch_wupdate(W, m, r, Ppart, nP, Qpart, nQ, eps, Gpart, st));
     }
     const bool acc_now = p.acc && (it + 1 < iters);
-    PLAUNCH(h, 5, 4.0 * (double)(m + 2 * r) * (double)n,
-            launch_hpass(X, ldx, m, n, W, r, Gpart, p.nwup, eps, H, p.hgrid, acc_now ? Ppart : nullptr,
+    if (p.hks && !acc_now)  // few column tiles, many rows: split-K over the rows
+      PLAUNCH(h, 5, 4.0 * (double)(m + 2 * r) * (double)n,
+              launch_hpass_sk(X, ldx, m, n, W, r, Gpart, p.nwup, eps, H, p.hks,
+                              reinterpret_cast<double*>(scratch + p.off_hs), red, st));
+    else
+      PLAUNCH(h, 5, 4.0 * (double)(m + 2 * r) * (double)n,
+              launch_hpass(X, ldx, m, n, W, r, Gpart, p.nwup, eps, H, p.hgrid, acc_now ? Ppart : nullptr,
                            acc_now ? Qpart : nullptr, st));
     if (acc_now) {
       nP = p.hgrid;

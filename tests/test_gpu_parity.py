@@ -76,6 +76,10 @@ MU_CASES = [
     (300, 257, 32, 6),
     (1, 50, 1, 10),
     (40, 1, 1, 10),
+    # generic two-pass with the split-K H pass (few column tiles, many rows; the 500 GB tensor's
+    # step 3 shape at r 40, and r 20 with n < 256 so the tensor-core path does not take it)
+    (15360, 64, 40, 6),
+    (3000, 200, 20, 10),
     # fused 1-pass TMA kernel (m <= 40, r <= 8, n % 4 == 0): every (R, UX) class, ragged last tile
     (32, 5004, 8, 10),
     (32, 1 << 16, 8, 10),
