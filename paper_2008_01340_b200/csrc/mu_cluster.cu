@@ -86,8 +86,11 @@ k_clu(const float* __restrict__ X, int64_t ldx, float* __restrict__ W, float* __
   float* HT2 = reinterpret_cast<float*>(sm + g.oH2);   // the other buffer of the H update
   float* Ws = reinterpret_cast<float*>(sm + g.oW);     // [m][RK] replicated W
   float* Sp = reinterpret_cast<float*>(sm + g.oS);     // [nq][ncmax][RK] S = W^T X row-chunk partials
-  double* PQ = reinterpret_cast<double*>(sm + g.oPQ);  // published: P_c [m][RK] | Q_c [RK][RK]
-  double* CH = reinterpret_cast<double*>(sm + g.oCH);  // [nc2][m][RK] column-chunk partials of P_c
+  // P rows padded to LDP = RK + 2 doubles: the per-row 16-byte stores of consecutive rows by
+  // consecutive lanes hit distinct bank groups (a 64-byte stride made every store 4x conflicted)
+  constexpr int LDP = RK + 2;
+  double* PQ = reinterpret_cast<double*>(sm + g.oPQ);  // published: P_c [m][LDP] | Q_c [RK][RK]
+  double* CH = reinterpret_cast<double*>(sm + g.oCH);  // [nc2][m][LDP] column-chunk partials of P_c
   double* Qw = reinterpret_cast<double*>(sm + g.oQw);  // [NW][RK][RK] per-warp partials of Q_c
   double* Pl = reinterpret_cast<double*>(sm + g.oPl);  // owned rows of P [rows][RK] | Q [RK][RK]
   float* Wp = reinterpret_cast<float*>(sm + g.oWp);    // published: new W of the owned rows
@@ -165,7 +168,7 @@ k_clu(const float* __restrict__ X, int64_t ldx, float* __restrict__ W, float* __
     for (int e = tid; e < RK * RK; e += T) {
       double s = 0.0;
       for (int w = 0; w < CLU_NW; ++w) s += Qw[w * RK * RK + e];
-      PQ[m * RK + e] = s;
+      PQ[m * LDP + e] = s;
     }
   };
 
@@ -224,7 +227,7 @@ k_clu(const float* __restrict__ X, int64_t ldx, float* __restrict__ W, float* __
         const int a = ap + u * mh;
         if (a < m) {
           NTT_DCHECK(ch < nc2 && a < m);
-          double* dst = nc2 == 1 ? PQ + a * RK : CH + ((size_t)ch * m + a) * RK;
+          double* dst = nc2 == 1 ? PQ + a * LDP : CH + ((size_t)ch * m + a) * LDP;
 #pragma unroll
           for (int k = 0; k < RK; k += 2)
             *reinterpret_cast<double2*>(dst + k) = make_double2(acc[u][k], acc[u][k + 1]);
@@ -235,8 +238,9 @@ k_clu(const float* __restrict__ X, int64_t ldx, float* __restrict__ W, float* __
       __syncthreads();
       for (int e = tid; e < m * RK; e += T) {
         double s = 0.0;
-        for (int ch = 0; ch < nc2; ++ch) s += CH[(size_t)ch * m * RK + e];
-        PQ[e] = s;
+        const int pe = (e / RK) * LDP + e % RK;
+        for (int ch = 0; ch < nc2; ++ch) s += CH[(size_t)ch * m * LDP + pe];
+        PQ[pe] = s;
       }
     }
   };
@@ -255,8 +259,8 @@ k_clu(const float* __restrict__ X, int64_t ldx, float* __restrict__ W, float* __
     // ---- phase 1: owned rows of P and all of Q over the CS partials (fixed order, all of a
     //      thread's remote loads in flight together), W update of the owned rows
     for (int e = tid; e < E1; e += T) {
-      const int off = e < nrow * RK ? r0 * RK + e : m * RK + (e - nrow * RK);
-      NTT_DCHECK(off < m * RK + RK * RK && e < g.rows_max * RK + RK * RK);
+      const int off = e < nrow * RK ? (r0 + e / RK) * LDP + e % RK : m * LDP + (e - nrow * RK);
+      NTT_DCHECK(off < m * LDP + RK * RK && e < g.rows_max * RK + RK * RK);
       double v[CLU_MAXCS];
 #pragma unroll
       for (int q = 0; q < CLU_MAXCS; ++q) v[q] = q < CS ? cl.map_shared_rank(PQ, q)[off] : 0.0;
@@ -448,9 +452,9 @@ CluPlan make_plan(int64_t m, int64_t n, int r, int cs) {
   g.oS = o;
   o = al16(o + sizeof(float) * (size_t)g.nq * g.ncmax * RK);
   g.oPQ = o;
-  o = al16(o + sizeof(double) * (size_t)(m * RK + RK * RK));
+  o = al16(o + sizeof(double) * (size_t)(m * (RK + 2) + RK * RK));
   g.oCH = o;
-  if (g.nc2 > 1) o = al16(o + sizeof(double) * (size_t)g.nc2 * m * RK);
+  if (g.nc2 > 1) o = al16(o + sizeof(double) * (size_t)g.nc2 * m * (RK + 2));
   g.oQw = o;
   o = al16(o + sizeof(double) * (size_t)CLU_NW * RK * RK);
   g.oPl = o;
