@@ -471,8 +471,35 @@ def run_ours(args):
             t = torch.tensor([ems], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
-        e2e = {"value": its / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(Nloc * 4) * ws,
-               "d2h_bytes_per_step": int(cores.numel() * 4 + 8) * ws, "ms_per_step": ems}
+        # the same steps as a stream of inputs: step k+1's H2D (ntt_prefetch_input, pinned host
+        # memory -> the next of two device slots, on the library's copy stream) overlaps step k's
+        # decomposition; every step still copies its 4.29 GB and reads its cores + error back.
+        # Wall clock around all K steps, synchronised on both sides (first copy not overlapped).
+        h.ntt_prefetch_input(Ah, Nloc)
+        h.ntt_decompose(Ah, dims, ranks, iters, w.seed, 1e-16, ch, want_error=True)  # warm slots + graphs
+        h.ntt_prefetch_input(Ah, Nloc)
+        h.ntt_decompose(Ah, dims, ranks, iters, w.seed, 1e-16, ch, want_error=True)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        tp0 = time.perf_counter()
+        h.ntt_prefetch_input(Ah, Nloc)
+        for k in range(args.steps):
+            if k + 1 < args.steps:
+                h.ntt_prefetch_input(Ah, Nloc)
+            h.ntt_decompose(Ah, dims, ranks, iters, w.seed, 1e-16, ch, want_error=True)
+        torch.cuda.synchronize()
+        pms = (time.perf_counter() - tp0) * 1e3 / args.steps
+        if dist:
+            t = torch.tensor([pms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            pms = float(t.item())
+        e2e = {"value": its / (pms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(Nloc * 4) * ws,
+               "d2h_bytes_per_step": int(cores.numel() * 4 + 8) * ws, "ms_per_step": pms,
+               "pipelined": ("step k+1's host-to-device copy (ntt_prefetch_input, pinned memory, the library's "
+                             "copy stream, two device input slots) overlaps step k's decomposition; wall clock "
+                             "over all steps, the first copy not overlapped"),
+               "serial_ms_per_step": ems, "serial_value": its / (ems / 1e3)}
         del Ah
 
     # ---- roofline: dominant kernel = the fused 1-pass X-stream kernel on TT step 1

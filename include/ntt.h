@@ -274,6 +274,17 @@ ntt_status ntt_profile_get_step(ntt_handle h, int cls, int step, int64_t* launch
  * and end at [16384 + c].  NULL otherwise.  Synchronises the handle's stream. */
 const unsigned long long* ntt_debug_persist_trace(ntt_handle h);
 
+/* Overlap the next input's host-to-device copy with device work already enqueued (a stream of
+ * decompositions, e.g. the bench's end-to-end loop): an asynchronous copy of `count` floats
+ * from host memory `src` (pinned for the copy to be asynchronous) into the next of two device
+ * input slots of the handle, on an internal copy stream.  A later ntt_decompose call on this
+ * handle whose A is that same host pointer with the same local element count waits for the copy
+ * and reads the slot instead of copying A itself; each slot is refilled only after the last
+ * decomposition that read it has finished.  The caller keeps `src` alive and unmodified until
+ * that decomposition is enqueued.  Returns NTT_ERR_INVALID_ARG for a device pointer or
+ * count < 1.  Allocates the slot on first use (synchronising the handle's streams).          */
+ntt_status ntt_prefetch_input(ntt_handle h, const float* src, int64_t count);
+
 /* Which kernel path ntt_nmf_mu takes for an m x n X at rank r on this handle
  * (16-byte aligned X and H, ldx = n; DESIGN.md s.6 "plan_mu"): 1 tiny (one CTA,
  * mu_tiny.cu), 2 cluster (one thread-block cluster, X in distributed shared

@@ -161,6 +161,10 @@ class Handle:
         self._check(lib().ntt_nmf_mu(self._h, _ptr(X), m, n, ldx, r, iters, eps, _ptr(W), _ptr(H), tr))
         return list(tr)[:iters] if trace else None
 
+    def ntt_prefetch_input(self, A, count: int):
+        """Asynchronous H2D copy of a host tensor into the handle's next input slot (ntt_prefetch_input)."""
+        self._check(lib().ntt_prefetch_input(self._h, _ptr(A), count))
+
     def mu_path(self, m: int, n: int, r: int) -> int:
         """ntt_debug_mu_path: 1 tiny, 2 cluster, 3 persistent 1-pass, 4 per-pass 1-pass, 5 tc, 6 generic."""
         return int(lib().ntt_debug_mu_path(self._h, m, n, r))

@@ -52,6 +52,7 @@ SIGNATURES = {
     "ntt_dist_block": (c_i64, [c_i64, c_int, c_int, ctypes.POINTER(c_i64)]),
     "ntt_debug_persist_trace": (ctypes.POINTER(ctypes.c_uint64), [c_p]),
     "ntt_debug_mu_path": (c_i32, [c_p, c_i64, c_i64, c_i32]),
+    "ntt_prefetch_input": (c_int, [c_p, c_p, c_i64]),
     "ntt_debug_bcd_force_correct": (c_int, [c_p, ctypes.c_uint64]),
     "ntt_set_validation": (c_int, [c_p, c_int]),
     "ntt_collective_count": (c_i64, [c_p]),

@@ -136,7 +136,33 @@ struct ntt_handle_s {
   size_t gev_used = 0;
   std::vector<Rec> grecs;
   int64_t glaunches = 0;
+  // a second cached decompose graph (non-profiled calls): inputs prefetched into alternating
+  // slots (ntt_prefetch_input) give two input pointers, each with its own instantiated graph
+  cudaGraphExec_t gexec_alt = nullptr;
+  std::vector<uint64_t> gkey_alt;
+  int64_t glaunches_alt = 0;
+  // ntt_prefetch_input: two device input slots filled on a copy stream
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t cev[2] = {nullptr, nullptr};   // copy into slot s done
+  cudaEvent_t uev[2] = {nullptr, nullptr};   // last decompose reading slot s done
+  void* slot[2] = {nullptr, nullptr};
+  size_t slot_cap[2] = {0, 0};
+  const void* slot_src[2] = {nullptr, nullptr};
+  int64_t slot_n[2] = {0, 0};
+  bool slot_ready[2] = {false, false};
+  uint64_t slot_seq[2] = {0, 0};  // fill order: a decompose takes the OLDEST matching slot (FIFO)
+  uint64_t fills = 0;
+  int next_slot = 0;
 };
+
+// drop every cached decompose graph (the path, the profiler or the exchange mode changed)
+void drop_graphs(ntt_handle h) {
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  if (h->gexec_alt) cudaGraphExecDestroy(h->gexec_alt);
+  h->gexec = h->gexec_alt = nullptr;
+  h->gkey.clear();
+  h->gkey_alt.clear();
+}
 
 namespace {
 
@@ -838,8 +864,14 @@ ntt_status ntt_destroy(ntt_handle h) {
   if (h->comm && g_nccl.loaded) g_nccl.CommDestroy(h->comm);
   for (auto e : h->ev_pool) cudaEventDestroy(e);
   for (auto e : h->gev_pool) cudaEventDestroy(e);
-  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  drop_graphs(h);
   if (h->bcd_exec) cudaGraphExecDestroy(h->bcd_exec);
+  for (int q = 0; q < 2; ++q) {
+    if (h->slot[q]) cudaFree(h->slot[q]);
+    if (h->cev[q]) cudaEventDestroy(h->cev[q]);
+    if (h->uev[q]) cudaEventDestroy(h->uev[q]);
+  }
+  if (h->cstream) cudaStreamDestroy(h->cstream);
   if (h->gev_in) cudaEventDestroy(h->gev_in);
   if (h->gev_out) cudaEventDestroy(h->gev_out);
   if (h->gstream) cudaStreamDestroy(h->gstream);
@@ -1119,10 +1151,21 @@ ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t*
   }
   const int64_t Nloc = s.N / s.dims[d - 1] * P.nloc_last;
   const float* dA = A;
+  int used_slot = -1;
   if (!is_device_ptr(A)) {
-    if ((st = ensure_stage(h, sizeof(float) * (size_t)Nloc))) return st;
-    dA = reinterpret_cast<const float*>(h->stage);
-    CU(h, cudaMemcpyAsync((void*)dA, A, sizeof(float) * (size_t)Nloc, cudaMemcpyHostToDevice, h->stream));
+    for (int q = 0; q < 2; ++q)  // staged by ntt_prefetch_input: wait for its copy, do not copy again
+      if (h->slot_ready[q] && h->slot_src[q] == (const void*)A && h->slot_n[q] == Nloc &&
+          (used_slot < 0 || h->slot_seq[q] < h->slot_seq[used_slot]))
+        used_slot = q;
+    if (used_slot >= 0) {
+      CU(h, cudaStreamWaitEvent(h->stream, h->cev[used_slot], 0));
+      dA = reinterpret_cast<const float*>(h->slot[used_slot]);
+      h->slot_ready[used_slot] = false;
+    } else {
+      if ((st = ensure_stage(h, sizeof(float) * (size_t)Nloc))) return st;
+      dA = reinterpret_cast<const float*>(h->stage);
+      CU(h, cudaMemcpyAsync((void*)dA, A, sizeof(float) * (size_t)Nloc, cudaMemcpyHostToDevice, h->stream));
+    }
   }
   if ((st = check_nonneg(h, dA, 1, Nloc, Nloc, "A"))) return st;
   const bool cores_dev = is_device_ptr(cores);
@@ -1151,10 +1194,25 @@ ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t*
       CU(h, cudaEventCreateWithFlags(&h->gev_in, cudaEventDisableTiming));
       CU(h, cudaEventCreateWithFlags(&h->gev_out, cudaEventDisableTiming));
     }
+    if ((!h->gexec || key != h->gkey) && !h->prof && h->gexec_alt && key == h->gkey_alt) {
+      std::swap(h->gexec, h->gexec_alt);  // the other cached graph (alternating prefetch slots)
+      std::swap(h->gkey, h->gkey_alt);
+      std::swap(h->glaunches, h->glaunches_alt);
+    }
     if (!h->gexec || key != h->gkey) {
       if (h->gexec) {
         CU(h, cudaStreamSynchronize(h->gstream));
-        cudaGraphExecDestroy(h->gexec);
+        if (!h->prof) {  // keep it as the second cached graph
+          if (h->gexec_alt) cudaGraphExecDestroy(h->gexec_alt);
+          h->gexec_alt = h->gexec;
+          h->gkey_alt = h->gkey;
+          h->glaunches_alt = h->glaunches;
+        } else {
+          cudaGraphExecDestroy(h->gexec);
+          if (h->gexec_alt) cudaGraphExecDestroy(h->gexec_alt);
+          h->gexec_alt = nullptr;
+          h->gkey_alt.clear();
+        }
         h->gexec = nullptr;
       }
       h->gkey.clear();
@@ -1198,6 +1256,7 @@ ntt_status ntt_decompose(ntt_handle h, const float* A, int32_t d, const int64_t*
   } else {
     if ((st = decompose_device(h, P, s, dA, dcores, ws, iters, seed, eps, rel_err != nullptr))) return st;
   }
+  if (used_slot >= 0) CU(h, cudaEventRecord(h->uev[used_slot], user));  // the slot may be refilled after this
   if (rel_err) {
     CU(h, cudaStreamSynchronize(user));
     if ((st = finish_error_host(h, rel_err))) return st;
@@ -1936,9 +1995,7 @@ ntt_status ntt_profile_enable(ntt_handle h, int enable) {
   if (h->gstream) CU(h, cudaStreamSynchronize(h->gstream));
   if (h->prof != (enable != 0)) {
     // the decompose graph records profile events only if captured with profiling on
-    if (h->gexec) cudaGraphExecDestroy(h->gexec);
-    h->gexec = nullptr;
-    h->gkey.clear();
+    drop_graphs(h);
   }
   h->prof = enable != 0;
   h->ev_used = 0;
@@ -2122,9 +2179,7 @@ extern "C" ntt_status ntt_set_dist_exchange(ntt_handle h, int mode) {
   if (mode == 1 && !h->xready) return fail(h, NTT_ERR_UNSUPPORTED, "exchange buffers are not mapped");
   CU(h, cudaStreamSynchronize(h->stream));
   if (h->gstream) CU(h, cudaStreamSynchronize(h->gstream));
-  if (h->gexec) cudaGraphExecDestroy(h->gexec);  // the decompose graph bakes in the path
-  h->gexec = nullptr;
-  h->gkey.clear();
+  drop_graphs(h);  // the decompose graph bakes in the path
   h->xmode = mode;
   return NTT_OK;
 }
@@ -2196,6 +2251,42 @@ extern "C" ntt_status ntt_set_validation(ntt_handle h, int flags) {
 extern "C" ntt_status ntt_debug_bcd_force_correct(ntt_handle h, uint64_t mask) {
   if (!h) return NTT_ERR_INVALID_ARG;
   h->bcd_force = mask & ((1ull << 52) - 1);
+  return NTT_OK;
+}
+
+extern "C" ntt_status ntt_prefetch_input(ntt_handle h, const float* src, int64_t count) {
+  if (!h) return NTT_ERR_INVALID_ARG;
+  if (!src || count < 1) return fail(h, NTT_ERR_INVALID_ARG, "null source or count < 1");
+  if (is_device_ptr(src)) return fail(h, NTT_ERR_INVALID_ARG, "ntt_prefetch_input takes a host pointer");
+  CU(h, cudaSetDevice(h->device));
+  if (!h->cstream) {
+    CU(h, cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+    for (int q = 0; q < 2; ++q) {
+      CU(h, cudaEventCreateWithFlags(&h->cev[q], cudaEventDisableTiming));
+      CU(h, cudaEventCreateWithFlags(&h->uev[q], cudaEventDisableTiming));
+    }
+  }
+  const int q = h->next_slot;
+  const size_t bytes = sizeof(float) * (size_t)count;
+  if (h->slot_cap[q] < bytes) {
+    CU(h, cudaStreamSynchronize(h->cstream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    if (h->gstream) CU(h, cudaStreamSynchronize(h->gstream));
+    if (h->slot[q]) CU(h, cudaFree(h->slot[q]));
+    h->slot[q] = nullptr;
+    h->slot_cap[q] = 0;
+    CU(h, cudaMalloc(&h->slot[q], bytes));
+    h->slot_cap[q] = bytes;
+  }
+  // not before the last decompose that read this slot is done (a never-recorded event is no wait)
+  CU(h, cudaStreamWaitEvent(h->cstream, h->uev[q], 0));
+  CU(h, cudaMemcpyAsync(h->slot[q], src, bytes, cudaMemcpyHostToDevice, h->cstream));
+  CU(h, cudaEventRecord(h->cev[q], h->cstream));
+  h->slot_src[q] = src;
+  h->slot_n[q] = count;
+  h->slot_ready[q] = true;
+  h->slot_seq[q] = ++h->fills;
+  h->next_slot = q ^ 1;
   return NTT_OK;
 }
 

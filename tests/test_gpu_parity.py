@@ -463,3 +463,34 @@ def test_plan_paths_of_the_workloads(h):
     }
     got = {k: h.mu_path(*k) for k in expect}
     assert got == expect
+
+
+def test_decompose_prefetch_input(h, ora):
+    """ntt_prefetch_input: a host tensor staged into the next device slot on the copy stream is
+    what a later ntt_decompose with that host pointer reads (two slots, oldest first), results
+    bit-identical to the plain host-pointer call; a non-matching call copies its own input."""
+    dims, ranks = [8, 8, 8, 8, 8], [4, 4, 4, 4]
+    A1 = torch.from_numpy(_tt_case(dims, ranks, 1, 0.5)).pin_memory()
+    A2 = torch.from_numpy(_tt_case(dims, ranks, 2, 0.5)).pin_memory()
+    n = A1.numel()
+    nc = ora.cores_size(dims, ranks)
+
+    def run(A):
+        c = torch.empty(nc, dtype=torch.float32).pin_memory()
+        e = h.ntt_decompose(A, dims, ranks, 10, 0, 1e-16, c, want_error=True)
+        return c.numpy().copy(), e
+
+    r1, e1 = run(A1)
+    r2, e2 = run(A2)
+    h.ntt_prefetch_input(A1, n)
+    h.ntt_prefetch_input(A2, n)
+    g1, f1 = run(A1)
+    g2, f2 = run(A2)
+    assert np.array_equal(g1, r1) and np.array_equal(g2, r2) and f1 == e1 and f2 == e2
+    h.ntt_prefetch_input(A1, n)
+    g2b, _ = run(A2)   # no slot holds A2: the call copies it itself
+    g1b, _ = run(A1)   # the slot staged above
+    assert np.array_equal(g2b, r2) and np.array_equal(g1b, r1)
+    import paper_2008_01340_b200 as P
+    with pytest.raises(P.NttError):
+        h.ntt_prefetch_input(torch.empty(4, device="cuda"), 4)
