@@ -179,3 +179,30 @@ def test_gather_last_core_ragged(handles, r, nd, p):
     out = torch.full((r * nd,), -1.0, device="cuda")
     hd.ntt_debug_gather_last_core(torch.from_numpy(gath).cuda(), r, nd, p, out)
     assert np.array_equal(out.cpu().numpy().reshape(r, nd), core)
+
+
+def test_dist_handle_generic_split_k(handles, ora):
+    """The generic two-pass path with the split-K H pass on a 1-rank NCCL handle (per-pass
+    all-reduce of the (X H^T, H H^T) vector, then the W update and the split H pass; the split
+    pass reuses the reduced vector's buffer for G): oracle parity and agreement with the
+    single-GPU handle."""
+    h1, hd = handles
+    m, n, r, it = 3000, 200, 20, 8
+    rng = np.random.default_rng(3)
+    X = rng.random((m, n)).astype(np.float32)
+    W0 = ni.uniform(m * r, 3, 0x202).reshape(m, r).astype(np.float32)
+    H0 = ni.uniform(r * n, 3, 0x203).reshape(r, n).astype(np.float32)
+    Xd = torch.from_numpy(X).cuda()
+    outs = []
+    for h in (h1, hd):
+        Wd, Hd = torch.from_numpy(W0.copy()).cuda(), torch.from_numpy(H0.copy()).cuda()
+        n0 = h.collective_count
+        h.ntt_nmf_mu(Xd, m, n, n, r, it, 1e-16, Wd, Hd)
+        if h is hd:
+            assert h.collective_count - n0 >= it
+        outs.append((Wd.cpu().numpy(), Hd.cpu().numpy()))
+    Wo, Ho = ora.nmf_mu(X, W0.astype(np.float64), H0.astype(np.float64), it)
+    for W, H in outs:
+        assert np.linalg.norm(W - Wo) <= 1e-4 * np.linalg.norm(Wo)
+        assert np.linalg.norm(H - Ho) <= 1e-4 * np.linalg.norm(Ho)
+    assert np.linalg.norm(outs[0][1] - outs[1][1]) <= 1e-5 * np.linalg.norm(outs[0][1])
