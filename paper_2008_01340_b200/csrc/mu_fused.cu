@@ -991,8 +991,11 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
   constexpr uint32_t XB = MP * 128u;
   constexpr uint32_t SB = XB + RK * 128u;
   unsigned char* stages = smem;
-  float* Sred = reinterpret_cast<float*>(smem + (size_t)ns * SB);  // [NW][RK k][32 c]
-  float* Gs = Sred + NW * RK * 32;                                   // RK x RK
+  // [NW][RK k][SRS] (32 columns + 4 floats of padding: the phase-A fragment stores (column g,
+  // rank 2t) of a warp hit 32 distinct banks; a 32-float row made them 4-way conflicted)
+  constexpr int SRS = 36;
+  float* Sred = reinterpret_cast<float*>(smem + (size_t)ns * SB);
+  float* Gs = Sred + NW * RK * SRS;                                  // RK x RK
   float* Hn = Gs + RK * RK;                                          // hnc_floats(RK)
   float* Wc = Hn + hnc_floats(RK);                                   // MP x RK (rank padded)
   uint64_t* full = reinterpret_cast<uint64_t*>(Wc + MP * RK);
@@ -1276,7 +1279,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         for (int nn = 0; nn < NN; ++nn)
 #pragma unroll
           for (int e4 = 0; e4 < 4; ++e4)
-            Sred[(warp * RK + 8 * nn + 2 * ft + (e4 & 1)) * 32 + 16 * mt + fg + 8 * (e4 >> 1)] = sacc[mt][nn][e4];
+            Sred[(warp * RK + 8 * nn + 2 * ft + (e4 & 1)) * SRS + 16 * mt + fg + 8 * (e4 >> 1)] = sacc[mt][nn][e4];
       asm volatile("bar.sync 1, %0;" ::"r"(NBAR) : "memory");
     }
     // ---- H update: thread handles (k, c) for k = kt + NW hh, c = ct
@@ -1295,7 +1298,7 @@ k_fused_c(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUten
         if constexpr (UPD) {
           float S = 0.0f;
 #pragma unroll
-          for (int w = 0; w < NW; ++w) S += Sred[(w * RK + kt) * 32 + ct];
+          for (int w = 0; w < NW; ++w) S += Sred[(w * RK + kt) * SRS + ct];
           float e0 = 0.0f, e1 = 0.0f;
           const float4* g4 = reinterpret_cast<const float4*>(Gs + kt * RK);  // row kt, 128-bit loads
 #pragma unroll
@@ -1496,7 +1499,7 @@ size_t persist_scratch_bytes(int64_t m, int r, int rk, int threads) {
 }
 
 size_t fixed_bytes_c(int MP, int NW, int RK) {
-  return (size_t)NW * RK * 32 * 4 + RK * RK * 4 + hnc_floats(RK) * 4 + (size_t)MP * RK * 4 + 2 * 16 * 8 + 1024;
+  return (size_t)NW * RK * 36 * 4 + RK * RK * 4 + hnc_floats(RK) * 4 + (size_t)MP * RK * 4 + 2 * 16 * 8 + 1024;
 }
 
 int stages_c(int MP, int NW, int RK) {
