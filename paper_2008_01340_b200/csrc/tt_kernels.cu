@@ -196,6 +196,143 @@ k_tt_stream(const float* __restrict__ L, const float* __restrict__ R, int64_t NL
   }
 }
 
+// Error-only stream (Eq. 3) for full tiles: the same work items, per-element
+// arithmetic and per-item fp32 -> fp64 accumulation order as k_tt_stream's error path, but the
+// reference rows reach shared memory through per-thread asynchronous copies (cp.async.cg, 16 B)
+// in a TE_S-stage ring of 8-row batches, so the bytes in flight are set by the ring (TE_S - 1
+// batches x 32 KB per CTA, MINB CTAs per SM) instead of by registers (k_tt_stream: 96 registers, 2 CTAs x 256
+// threads x 128 B = 64 KB per SM; ~4.7 TB/s on config 3).  Every thread copies and later reads
+// only its own 16-byte slots, so the ring needs no barrier; batches continue across work items.
+// The next item's L rows (double-buffered smem) and R columns (registers) are fetched half an
+// item ahead, so an item boundary costs one CTA barrier while the copies stay in flight.  CTAs
+// with no item of their own still zero their partial; CTA b also zeroes slots b + G, b + 2G, ...
+// < npart (npart = the plan's partial count), so the fixed-order k_sum_pairs sees that layout.
+
+// (no L2::cache_hint operand: with it ptxas 12.9 emitted, for RK <= 4, LDGSTS with an odd uniform
+// register pair as the cache-policy descriptor that was never written -- an illegal instruction on
+// the GPU)
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int RK, int TE_S, int MINB>
+__global__ void __launch_bounds__(TS_THREADS, MINB)
+k_tt_err(const float* __restrict__ L, const float* __restrict__ R, int64_t NL, int64_t NR, int rk,
+         const float* __restrict__ ref, double* __restrict__ err_part, int npart) {
+  extern __shared__ float4 ring[];                 // [TE_S][8 rows][TS_THREADS]
+  __shared__ float Ls[2][TS_RA][RK];
+  __shared__ double red[2][TS_THREADS / 32];
+  const int tid = threadIdx.x;
+  const int64_t ncb = NR / TS_CB, items = ncb * (NL / TS_RA);
+  const int64_t G = gridDim.x, b = blockIdx.x;
+  const int64_t nI = items > b ? (items - b + G - 1) / G : 0;
+  const int64_t nb = nI * (TS_RA / 8);             // 8-row batches of this CTA
+  const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(ring) + 16u * tid;
+  auto issue = [&](int64_t g) {
+    if (g < nb) {
+      const int64_t item = b + (g >> 3) * G;
+      const int64_t a = (item / ncb) * TS_RA + (g & 7) * 8, col = (item % ncb) * TS_CB + 4 * tid;
+      const uint32_t dst = ring0 + (uint32_t)(g % TE_S) * (8u * TS_THREADS * 16u);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) cp_async16(dst + u * (TS_THREADS * 16u), ref + (a + u) * NR + col);
+    }
+    cp_async_commit();  // empty groups keep the group count uniform
+  };
+#pragma unroll
+  for (int g = 0; g < TE_S - 1; ++g) issue(g);
+  double num = 0.0, den = 0.0;
+  float fnum = 0.0f, fden = 0.0f;
+  float rq[RK][4], rqn[RK][4];
+  // item j's L rows (into Ls[j & 1]) and R columns (into rqn), issued mid-way through item j - 1
+  auto fetch_lr = [&](int64_t j) {
+    const int64_t item = b + j * G;
+    const int64_t a0 = (item / ncb) * TS_RA, b0 = (item % ncb) * TS_CB + 4 * tid;
+    for (int e = tid; e < TS_RA * RK; e += TS_THREADS) {
+      const int aa = e / RK, q = e % RK;
+      Ls[j & 1][aa][q] = q < rk ? L[(a0 + aa) * rk + q] : 0.0f;
+    }
+#pragma unroll
+    for (int q = 0; q < RK; ++q) {
+      const float4 v = q < rk ? *reinterpret_cast<const float4*>(R + (int64_t)q * NR + b0) : make_float4(0.f, 0.f, 0.f, 0.f);
+      rqn[q][0] = v.x; rqn[q][1] = v.y; rqn[q][2] = v.z; rqn[q][3] = v.w;
+    }
+  };
+  if (nb > 0) fetch_lr(0);
+  int stg = 0;  // ring stage of batch g
+  for (int64_t g = 0; g < nb; ++g) {
+    if ((g & 7) == 0) {  // item boundary: Ls[(g >> 3) & 1] complete, Ls of the item before no longer read
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < RK; ++q)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) rq[q][t] = rqn[q][t];
+    } else if ((g & 7) == 4 && g + 4 < nb) {
+      fetch_lr((g >> 3) + 1);
+    }
+    issue(g + TE_S - 1);          // into the stage this thread consumed at g - 1
+    cp_async_wait<TE_S - 1>();    // batch g has landed (this thread's own copies)
+    const float4* st = ring + (size_t)stg * 8 * TS_THREADS + tid;
+    if (++stg == TE_S) stg = 0;
+    const int a8 = (int)(g & 7) * 8;
+    const float(*Lc)[RK] = Ls[(g >> 3) & 1];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const float4 xv = st[u * TS_THREADS];
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int q = 0; q < RK; ++q) {
+        const float lq = Lc[a8 + u][q];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) v[t] = fmaf(lq, rq[q][t], v[t]);
+      }
+      const float x[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float e = x[t] - v[t];
+        fnum = fmaf(e, e, fnum);
+        fden = fmaf(x[t], x[t], fden);
+      }
+    }
+    if ((g & 7) == 7) {  // end of the item: fp32 item sums into fp64, as k_tt_stream
+      num += (double)fnum;
+      den += (double)fden;
+      fnum = fden = 0.0f;
+    }
+  }
+  cp_async_wait<0>();
+  num = warp_sum(num);
+  den = warp_sum(den);
+  if ((tid & 31) == 0) {
+    red[0][tid >> 5] = num;
+    red[1][tid >> 5] = den;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double sn = 0.0, sd = 0.0;
+    for (int w = 0; w < TS_THREADS / 32; ++w) {
+      sn += red[0][w];
+      sd += red[1][w];
+    }
+    err_part[2 * b] = sn;
+    err_part[2 * b + 1] = sd;
+    for (int64_t s = b + G; s < npart; s += G) err_part[2 * s] = err_part[2 * s + 1] = 0.0;
+  }
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n < 1) n = 1;
+  }
+  return n;
+}
+
 int stream_ctas(int64_t NL, int64_t NR, int num_sms) {
   int64_t items = ((NR + TS_CB - 1) / TS_CB) * ((NL + TS_RA - 1) / TS_RA);
   int64_t cap = (int64_t)num_sms * 8;
@@ -205,6 +342,31 @@ int stream_ctas(int64_t NL, int64_t NR, int num_sms) {
 cudaError_t launch_tt_stream(const float* L, const float* R, int64_t NL, int64_t NR, int rk, float* out,
                              float noise_amp, uint64_t noise_key, const float* ref, double* err_part, int grid,
                              cudaStream_t st) {
+  // error-only streams over full tiles take the cp.async ring (k_tt_err); grid = the plan's partials
+  const bool err_fast = !out && ref && err_part && rk <= 16 && NR % TS_CB == 0 && NL % TS_RA == 0 && NL > 0 &&
+                        ((reinterpret_cast<uintptr_t>(R) | reinterpret_cast<uintptr_t>(ref)) & 15) == 0;
+  if (err_fast) {
+    const int64_t items = (NR / TS_CB) * (NL / TS_RA);
+    // two CTAs of a 3-stage ring per SM (16 warps, 128 KB in flight): config 3's error pass 0.707 ms
+    // = 6.1 TB/s, against 0.867 ms for one CTA of a 6-stage ring and 0.842 ms for 4 stages; RK = 16
+    // (186 registers with the prefetched R columns) keeps one CTA per SM
+#define TE1(K, S, MB)                                                                                         \
+  do {                                                                                                       \
+    const size_t smem = (size_t)S * 8 * TS_THREADS * sizeof(float4);                                         \
+    static cudaError_t attr = cudaFuncSetAttribute(k_tt_err<K, S, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                                   (int)smem);                                               \
+    if (attr != cudaSuccess) return attr;                                                                    \
+    const int gg = (int)std::min<int64_t>(std::min<int64_t>(items, (int64_t)MB * sm_count()), grid);       \
+    k_tt_err<K, S, MB><<<gg, TS_THREADS, smem, st>>>(L, R, NL, NR, rk, ref, err_part, grid);                \
+  } while (0)
+    if (rk <= 1) TE1(1, 3, 2);
+    else if (rk <= 2) TE1(2, 3, 2);
+    else if (rk <= 4) TE1(4, 3, 2);
+    else if (rk <= 8) TE1(8, 3, 2);
+    else TE1(16, 6, 1);
+#undef TE1
+    return cudaGetLastError();
+  }
 #define TS(K) k_tt_stream<K><<<grid, TS_THREADS, 0, st>>>(L, R, NL, NR, rk, out, noise_amp, noise_key, ref, err_part)
   if (rk <= 1) TS(1);
   else if (rk <= 2) TS(2);

@@ -358,6 +358,23 @@ def test_reconstruct_parity(h, ora, dims, ranks):
     assert abs(e - eo) <= 1e-5 * eo
 
 
+@pytest.mark.parametrize("dims,ranks", [([32, 32, 32, 32], [3, 8, 5]),      # 16 items, 16 CTAs
+                                        ([64, 64, 64, 64], [4, 16, 2]),     # 256 items on 148 CTAs
+                                        ([16, 64, 64, 64], [2, 1, 7]),
+                                        ([64, 64, 64, 64], [2, 12, 3])])
+def test_error_stream_full_tiles(h, ora, dims, ranks):
+    """Eq. 3 on split shapes with N_L % 64 == 0 and N_R % 1024 == 0: the error-only
+    cp.async ring kernel (k_tt_err), incl. CTAs with several items and the zeroed spare partial
+    slots (fewer CTAs than the plan's partials), against the oracle's fp64 error."""
+    cores = ni.make_cores(dims, ranks, seed=7).astype(np.float32)
+    A = ora.tt_full_f32(dims, ranks, ni.make_cores(dims, ranks, seed=8), noise_amp=0.2, seed=8)
+    e = h.ntt_reconstruct(dims, ranks, dev(cores), ref=dev(A), want_error=True)
+    eo = ora.tt_rel_error(A, ranks, cores.astype(np.float64))
+    assert abs(e - eo) <= 1e-5 * eo
+    e2 = h.ntt_reconstruct(dims, ranks, dev(cores), ref=dev(A), want_error=True)
+    assert e2 == e  # fixed-order partial sums: bit-reproducible
+
+
 def test_reconstruct_degenerate(h):
     import paper_2008_01340_b200 as P
     dims, ranks = [3, 4], [2]

@@ -22,3 +22,11 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 10
 print(f"error pass {ms:.3f} ms = {4 * 32 ** 6 / ms / 1e9:.2f} TB/s")
+h.ntt_profile_enable(True)
+for _ in range(10):
+    h.ntt_reconstruct(dims, ranks, cores, ref=A, want_error=True)
+torch.cuda.synchronize()
+for l in range(0, 8):
+    k, kms, by = h.ntt_profile_get(3, l)
+    if k:
+        print(f"stream kernel (class 3, level {l}): {kms / k:.3f} ms per launch = {by / (kms / 1e3) / 1e12:.2f} TB/s")
