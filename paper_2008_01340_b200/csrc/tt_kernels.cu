@@ -196,8 +196,9 @@ k_tt_stream(const float* __restrict__ L, const float* __restrict__ R, int64_t NL
   }
 }
 
-// Error-only stream (Eq. 3) for full tiles: the same work items, per-element
-// arithmetic and per-item fp32 -> fp64 accumulation order as k_tt_stream's error path, but the
+// Error-only stream (Eq. 3) for full tiles: the same work items and per-element
+// arithmetic as k_tt_stream's error path (on packed fp32 pairs, FFMA2: the kernel is otherwise
+// issue-bound), per-item fp32 -> fp64 accumulation, but the
 // reference rows reach shared memory through per-thread asynchronous copies (cp.async.cg, 16 B)
 // in a TE_S-stage ring of 8-row batches, so the bytes in flight are set by the ring (TE_S - 1
 // batches x 32 KB per CTA, MINB CTAs per SM) instead of by registers (k_tt_stream: 96 registers, 2 CTAs x 256
@@ -231,21 +232,31 @@ k_tt_err(const float* __restrict__ L, const float* __restrict__ R, int64_t NL, i
   const int64_t nI = items > b ? (items - b + G - 1) / G : 0;
   const int64_t nb = nI * (TS_RA / 8);             // 8-row batches of this CTA
   const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(ring) + 16u * tid;
+  // issue side: batches are issued in order g = 0, 1, ...; the item's row-0 pointer is formed once
+  // per item (one 64-bit division per 8 batches, not per batch)
+  const float* isrc = ref;
+  int istg = 0;
   auto issue = [&](int64_t g) {
     if (g < nb) {
-      const int64_t item = b + (g >> 3) * G;
-      const int64_t a = (item / ncb) * TS_RA + (g & 7) * 8, col = (item % ncb) * TS_CB + 4 * tid;
-      const uint32_t dst = ring0 + (uint32_t)(g % TE_S) * (8u * TS_THREADS * 16u);
+      if ((g & 7) == 0) {
+        const int64_t item = b + (g >> 3) * G;
+        isrc = ref + (item / ncb) * TS_RA * NR + (item % ncb) * TS_CB + 4 * tid;
+      } else {
+        isrc += 8 * NR;
+      }
+      const uint32_t dst = ring0 + (uint32_t)istg * (8u * TS_THREADS * 16u);
+      if (++istg == TE_S) istg = 0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) cp_async16(dst + u * (TS_THREADS * 16u), ref + (a + u) * NR + col);
+      for (int u = 0; u < 8; ++u) cp_async16(dst + u * (TS_THREADS * 16u), isrc + u * NR);
     }
     cp_async_commit();  // empty groups keep the group count uniform
   };
 #pragma unroll
   for (int g = 0; g < TE_S - 1; ++g) issue(g);
   double num = 0.0, den = 0.0;
-  float fnum = 0.0f, fden = 0.0f;
-  float rq[RK][4], rqn[RK][4];
+  // packed fp32 pairs (FFMA2): columns (0, 1) and (2, 3) of the thread's four
+  float2 fnum = make_float2(0.f, 0.f), fden = make_float2(0.f, 0.f);
+  float2 rq[RK][2], rqn[RK][2];
   // item j's L rows (into Ls[j & 1]) and R columns (into rqn), issued mid-way through item j - 1
   auto fetch_lr = [&](int64_t j) {
     const int64_t item = b + j * G;
@@ -257,18 +268,21 @@ k_tt_err(const float* __restrict__ L, const float* __restrict__ R, int64_t NL, i
 #pragma unroll
     for (int q = 0; q < RK; ++q) {
       const float4 v = q < rk ? *reinterpret_cast<const float4*>(R + (int64_t)q * NR + b0) : make_float4(0.f, 0.f, 0.f, 0.f);
-      rqn[q][0] = v.x; rqn[q][1] = v.y; rqn[q][2] = v.z; rqn[q][3] = v.w;
+      rqn[q][0] = make_float2(v.x, v.y);
+      rqn[q][1] = make_float2(v.z, v.w);
     }
   };
   if (nb > 0) fetch_lr(0);
+  const float2 mone = make_float2(-1.f, -1.f);
   int stg = 0;  // ring stage of batch g
   for (int64_t g = 0; g < nb; ++g) {
     if ((g & 7) == 0) {  // item boundary: Ls[(g >> 3) & 1] complete, Ls of the item before no longer read
       __syncthreads();
 #pragma unroll
-      for (int q = 0; q < RK; ++q)
-#pragma unroll
-        for (int t = 0; t < 4; ++t) rq[q][t] = rqn[q][t];
+      for (int q = 0; q < RK; ++q) {
+        rq[q][0] = rqn[q][0];
+        rq[q][1] = rqn[q][1];
+      }
     } else if ((g & 7) == 4 && g + 4 < nb) {
       fetch_lr((g >> 3) + 1);
     }
@@ -281,25 +295,25 @@ k_tt_err(const float* __restrict__ L, const float* __restrict__ R, int64_t NL, i
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const float4 xv = st[u * TS_THREADS];
-      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      float2 v0 = make_float2(0.f, 0.f), v1 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int q = 0; q < RK; ++q) {
         const float lq = Lc[a8 + u][q];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) v[t] = fmaf(lq, rq[q][t], v[t]);
+        const float2 l2 = make_float2(lq, lq);
+        v0 = __ffma2_rn(l2, rq[q][0], v0);
+        v1 = __ffma2_rn(l2, rq[q][1], v1);
       }
-      const float x[4] = {xv.x, xv.y, xv.z, xv.w};
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const float e = x[t] - v[t];
-        fnum = fmaf(e, e, fnum);
-        fden = fmaf(x[t], x[t], fden);
-      }
+      const float2 x0 = make_float2(xv.x, xv.y), x1 = make_float2(xv.z, xv.w);
+      const float2 e0 = __ffma2_rn(v0, mone, x0), e1 = __ffma2_rn(v1, mone, x1);  // x - v, one rounding
+      fnum = __ffma2_rn(e0, e0, fnum);
+      fnum = __ffma2_rn(e1, e1, fnum);
+      fden = __ffma2_rn(x0, x0, fden);
+      fden = __ffma2_rn(x1, x1, fden);
     }
-    if ((g & 7) == 7) {  // end of the item: fp32 item sums into fp64, as k_tt_stream
-      num += (double)fnum;
-      den += (double)fden;
-      fnum = fden = 0.0f;
+    if ((g & 7) == 7) {  // end of the item: fp32 item sums into fp64
+      num += (double)fnum.x + (double)fnum.y;
+      den += (double)fden.x + (double)fden.y;
+      fnum = fden = make_float2(0.f, 0.f);
     }
   }
   cp_async_wait<0>();
