@@ -17,9 +17,22 @@
 namespace ntt {
 
 // ---------------------------------------------------------------- RNG fill --
+// 128-bit stores when p is 16-byte aligned (the first count & ~3 elements; the <= 3 left over
+// by thread 0); element i is rng_uniform(key, off + i) either way
 __global__ void k_fill_uniform(float* __restrict__ p, int64_t count, uint64_t key, int64_t off) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+    const int64_t n4 = count >> 2;
+    for (int64_t q = i; q < n4; q += stride) {
+      const uint64_t e = (uint64_t)(off + 4 * q);
+      reinterpret_cast<float4*>(p)[q] =
+          make_float4(rng_uniform(key, e), rng_uniform(key, e + 1), rng_uniform(key, e + 2), rng_uniform(key, e + 3));
+    }
+    if (i == 0)
+      for (int64_t t = 4 * n4; t < count; ++t) p[t] = rng_uniform(key, (uint64_t)(off + t));
+    return;
+  }
   for (; i < count; i += stride) p[i] = rng_uniform(key, (uint64_t)(off + i));
 }
 

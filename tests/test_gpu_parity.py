@@ -56,6 +56,16 @@ def test_fill_uniform_bit_exact(h, ora, seed, stream, off):
     assert [got[i] for i in idx] == [ora.fill_uniform(1, seed, stream, off + i)[0] for i in idx]
 
 
+@pytest.mark.parametrize("shift,n", [(1, 100_003), (2, 7), (0, 3), (0, 1 << 20)])
+def test_fill_uniform_alignment(h, shift, n):
+    """128-bit store path (16-byte aligned, ragged count) and the scalar path (misaligned start)."""
+    t = torch.zeros(n + 8, dtype=torch.float32, device="cuda")
+    h.ntt_fill_uniform(t[shift:], n, 11, 0x207, 5)
+    got = host(t).astype(np.float64)
+    assert np.array_equal(got[shift:shift + n], ni.uniform(n, 11, 0x207, 5))
+    assert not got[:shift].any() and not got[shift + n:].any()
+
+
 def test_fill_uniform_host_pointer(h):
     a = np.empty(1000, np.float32)
     h.ntt_fill_uniform(a, 1000, 3, 0x205, 0)
