@@ -219,7 +219,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int RK, int TE_S, int MINB>
+template <int RK, int TE_S, int MINB, bool PF>
 __global__ void __launch_bounds__(TS_THREADS, MINB)
 k_tt_err(const float* __restrict__ L, const float* __restrict__ R, int64_t NL, int64_t NR, int rk,
          const float* __restrict__ ref, double* __restrict__ err_part, int npart) {
@@ -256,21 +256,27 @@ k_tt_err(const float* __restrict__ L, const float* __restrict__ R, int64_t NL, i
   double num = 0.0, den = 0.0;
   // packed fp32 pairs (FFMA2): columns (0, 1) and (2, 3) of the thread's four
   float2 fnum = make_float2(0.f, 0.f), fden = make_float2(0.f, 0.f);
-  float2 rq[RK][2], rqn[RK][2];
-  // item j's L rows (into Ls[j & 1]) and R columns (into rqn), issued mid-way through item j - 1
+  float2 rq[RK][2], rqn[PF ? RK : 1][2];
+  // item j's L rows (into Ls[j & 1]) and, PF, R columns (into rqn), issued mid-way through item j - 1;
+  // !PF (RK > 8: the second register set would cost the second CTA per SM) loads rq at the boundary
+  auto load_r = [&](int64_t j, float2 (&dst)[RK][2]) {
+    const int64_t item = b + j * G;
+    const int64_t b0 = (item % ncb) * TS_CB + 4 * tid;
+#pragma unroll
+    for (int q = 0; q < RK; ++q) {
+      const float4 v = q < rk ? *reinterpret_cast<const float4*>(R + (int64_t)q * NR + b0) : make_float4(0.f, 0.f, 0.f, 0.f);
+      dst[q][0] = make_float2(v.x, v.y);
+      dst[q][1] = make_float2(v.z, v.w);
+    }
+  };
   auto fetch_lr = [&](int64_t j) {
     const int64_t item = b + j * G;
-    const int64_t a0 = (item / ncb) * TS_RA, b0 = (item % ncb) * TS_CB + 4 * tid;
+    const int64_t a0 = (item / ncb) * TS_RA;
     for (int e = tid; e < TS_RA * RK; e += TS_THREADS) {
       const int aa = e / RK, q = e % RK;
       Ls[j & 1][aa][q] = q < rk ? L[(a0 + aa) * rk + q] : 0.0f;
     }
-#pragma unroll
-    for (int q = 0; q < RK; ++q) {
-      const float4 v = q < rk ? *reinterpret_cast<const float4*>(R + (int64_t)q * NR + b0) : make_float4(0.f, 0.f, 0.f, 0.f);
-      rqn[q][0] = make_float2(v.x, v.y);
-      rqn[q][1] = make_float2(v.z, v.w);
-    }
+    if constexpr (PF) load_r(j, rqn);
   };
   if (nb > 0) fetch_lr(0);
   const float2 mone = make_float2(-1.f, -1.f);
@@ -278,10 +284,14 @@ k_tt_err(const float* __restrict__ L, const float* __restrict__ R, int64_t NL, i
   for (int64_t g = 0; g < nb; ++g) {
     if ((g & 7) == 0) {  // item boundary: Ls[(g >> 3) & 1] complete, Ls of the item before no longer read
       __syncthreads();
+      if constexpr (PF) {
 #pragma unroll
-      for (int q = 0; q < RK; ++q) {
-        rq[q][0] = rqn[q][0];
-        rq[q][1] = rqn[q][1];
+        for (int q = 0; q < RK; ++q) {
+          rq[q][0] = rqn[q][0];
+          rq[q][1] = rqn[q][1];
+        }
+      } else {
+        load_r(g >> 3, rq);
       }
     } else if ((g & 7) == 4 && g + 4 < nb) {
       fetch_lr((g >> 3) + 1);
@@ -362,22 +372,24 @@ cudaError_t launch_tt_stream(const float* L, const float* R, int64_t NL, int64_t
   if (err_fast) {
     const int64_t items = (NR / TS_CB) * (NL / TS_RA);
     // two CTAs of a 3-stage ring per SM (16 warps, 128 KB in flight): config 3's error pass 0.707 ms
-    // = 6.1 TB/s, against 0.867 ms for one CTA of a 6-stage ring and 0.842 ms for 4 stages; RK = 16
-    // (186 registers with the prefetched R columns) keeps one CTA per SM
-#define TE1(K, S, MB)                                                                                         \
+    // = 6.1 TB/s, against 0.867 ms for one CTA of a 6-stage ring and 0.842 ms for 4 stages.  RK = 12
+    // / 16 load their R columns at the item boundary instead (the prefetched set took 186 registers,
+    // i.e. one CTA per SM: 256^4 at r 10 ran at 4.0 TB/s on <16, 6, 1>); rk 9..12 takes RK = 12
+#define TE1(K, S, MB, PF)                                                                                     \
   do {                                                                                                       \
     const size_t smem = (size_t)S * 8 * TS_THREADS * sizeof(float4);                                         \
-    static cudaError_t attr = cudaFuncSetAttribute(k_tt_err<K, S, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                                   (int)smem);                                               \
+    static cudaError_t attr = cudaFuncSetAttribute(k_tt_err<K, S, MB, PF>,                                   \
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
     if (attr != cudaSuccess) return attr;                                                                    \
     const int gg = (int)std::min<int64_t>(std::min<int64_t>(items, (int64_t)MB * sm_count()), grid);       \
-    k_tt_err<K, S, MB><<<gg, TS_THREADS, smem, st>>>(L, R, NL, NR, rk, ref, err_part, grid);                \
+    k_tt_err<K, S, MB, PF><<<gg, TS_THREADS, smem, st>>>(L, R, NL, NR, rk, ref, err_part, grid);            \
   } while (0)
-    if (rk <= 1) TE1(1, 3, 2);
-    else if (rk <= 2) TE1(2, 3, 2);
-    else if (rk <= 4) TE1(4, 3, 2);
-    else if (rk <= 8) TE1(8, 3, 2);
-    else TE1(16, 6, 1);
+    if (rk <= 1) TE1(1, 3, 2, true);
+    else if (rk <= 2) TE1(2, 3, 2, true);
+    else if (rk <= 4) TE1(4, 3, 2, true);
+    else if (rk <= 8) TE1(8, 3, 2, true);
+    else if (rk <= 12) TE1(12, 3, 2, false);
+    else TE1(16, 3, 2, false);
 #undef TE1
     return cudaGetLastError();
   }
